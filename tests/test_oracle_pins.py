@@ -1,0 +1,334 @@
+"""Pins of the CPU oracle against what the paper and the mathematics fix.
+
+Nothing here compares the oracle with itself: every expected value comes from
+a golden fixture (cited), from brute force written here independently (full
+recomputation of TD after a swap, exhaustive search over medoid sets), from
+the paper's Appendix-A decomposition, or from an invariant the paper states.
+"""
+import itertools
+import json
+import os
+
+import numpy as np
+import pytest
+
+import oracle
+
+GOLD = os.path.join(os.path.dirname(__file__), "golden")
+
+
+def _gold(name):
+    with open(os.path.join(GOLD, name)) as f:
+        return json.load(f)
+
+
+def line_matrix(points):
+    x = np.asarray(points, dtype=np.int64)
+    return np.abs(x[:, None] - x[None, :]).astype(np.uint32)
+
+
+# ---------- brute force, written independently of oracle/ ----------
+
+def bf_td(D, M):
+    """TD by definition: every object to its closest medoid (Eq. eqn:td)."""
+    n = D.shape[0]
+    tot = 0
+    for o in range(n):
+        tot += min(int(D[o, m]) if D.dtype == np.uint32 else float(D[o, m]) for m in M)
+    return tot
+
+
+def bf_delta(D, M, i, c):
+    M2 = list(M)
+    M2[i] = c
+    return bf_td(D, M2) - bf_td(D, M)
+
+
+def rand_int_matrix(rng, n, hi=50, symmetric=True):
+    A = rng.integers(0, hi, size=(n, n)).astype(np.uint32)
+    if symmetric:
+        A = np.triu(A, 1)
+        A = A + A.T
+    np.fill_diagonal(A, 0)
+    return A
+
+
+# ---------- golden worked examples ----------
+
+def test_spec_line_example_cache_and_removal_loss():
+    g = _gold("spec_line_0_5_6_10.json")
+    D = line_matrix(g["points"])
+    c = oracle.assign(D, g["medoids"])
+    assert c.nearest.tolist() == g["nearest"]
+    assert c.dn.tolist() == g["dn"]
+    assert c.ds.tolist() == g["ds"]
+    assert oracle.td(D, g["medoids"]) == g["td"]
+    assert oracle.removal_loss(c, 2).tolist() == g["removal_loss"]
+
+
+def test_spec_line_example_change_function():
+    g = _gold("spec_line_0_5_6_10.json")
+    D = line_matrix(g["points"])
+    c = oracle.assign(D, g["medoids"])
+    s = g["swap_slot0_with_point1"]
+    per = [oracle.change(int(D[o, 1]), int(c.nearest[o]), int(c.dn[o]), int(c.ds[o]), 0) for o in range(4)]
+    assert per == s["per_object_change"]
+    assert sum(per) == s["delta_td"] == bf_delta(D, g["medoids"], 0, 1)
+    assert bf_td(D, [1, 3]) == s["td_after"]
+
+
+def test_spec_line_example_fastpam1_vectors_and_trace():
+    g = _gold("spec_line_0_5_6_10.json")
+    D = line_matrix(g["points"])
+    c = oracle.assign(D, g["medoids"])
+    R = oracle.removal_loss(c, 2)
+    for cand in (1, 2):
+        gg = g[f"fastpam1_candidate_{cand}"]
+        vec, plus = oracle.fastpam1_candidate(D, cand, c, R)
+        assert vec.tolist() == gg["vec"] and plus == gg["plus"]
+        assert [int(v + plus) for v in vec] == gg["delta_td"]
+        assert gg["delta_td"] == [bf_delta(D, g["medoids"], i, cand) for i in range(2)]
+    for variant in (oracle.PAM, oracle.FASTPAM1, oracle.FASTPAM2):
+        r = oracle.swap_run(D, g["medoids"], variant)
+        assert [list(t) for t in r.trace] == g["trace"]
+        assert r.medoids.tolist() == g["final_medoids"] and r.td == g["final_td"]
+    # the final state is the exhaustive optimum over all C(4,2) medoid sets
+    assert g["final_td"] == min(bf_td(D, list(s)) for s in itertools.combinations(range(4), 2))
+
+
+def test_fig1_trace_reproduces_printed_losses():
+    g = _gold("fig1_alternating.json")
+    D = line_matrix(g["points"])
+    assert bf_td(D, g["medoids"]) == g["losses"][0]
+    for variant in (oracle.PAM, oracle.FASTPAM1):
+        r = oracle.swap_run(D, g["medoids"], variant)
+        assert [list(t) for t in r.trace] == g["trace"]
+        M = list(g["medoids"])
+        losses = [bf_td(D, M)]
+        for (i, cnd, dtd) in r.trace:
+            M[i] = cnd
+            losses.append(bf_td(D, M))
+        assert losses == g["losses"]
+        assert r.medoids.tolist() == g["final_medoids"]
+        assert r.td == min(bf_td(D, list(s)) for s in itertools.combinations(range(6), 2))
+
+
+def test_build_golden():
+    g = _gold("spec_build_0_1_2_10.json")
+    D = line_matrix(g["points"])
+    assert [int(D[:, c].sum()) for c in range(4)] == g["first_medoid_sums"]
+    M, td, gains = oracle.build_init(D, g["k"])
+    assert M.tolist() == g["medoids"] and td == g["td"] and gains.tolist() == g["gains"]
+    assert bf_td(D, g["medoids"]) == g["td"]
+
+
+# ---------- Appendix A: decomposition == four-case change ----------
+
+def test_appendix_a_identity():
+    rng = np.random.default_rng(7)
+    for _ in range(1000):
+        dn = int(rng.integers(0, 20))
+        ds = dn + int(rng.integers(0, 20))
+        doc = int(rng.integers(0, 45))
+        k = int(rng.integers(2, 6))
+        near = int(rng.integers(0, k))
+        i = int(rng.integers(0, k))
+        minus = (ds - dn) if near == i else 0
+        plus = (doc - dn) if doc < dn else 0
+        if near == i and doc < dn:
+            corr = dn - ds
+        elif near == i and doc < ds:
+            corr = doc - ds
+        else:
+            corr = 0
+        assert oracle.change(doc, near, dn, ds, i) == minus + plus + corr
+
+
+# ---------- brute force on random instances ----------
+
+@pytest.mark.parametrize("symmetric", [True, False])
+def test_change_sum_and_fastpam1_table_equal_bruteforce(symmetric):
+    rng = np.random.default_rng(11 + symmetric)
+    for trial in range(60):
+        n = int(rng.integers(5, 18))
+        k = int(rng.integers(2, min(6, n - 1) + 1))
+        D = rand_int_matrix(rng, n, hi=30, symmetric=symmetric)
+        M = rng.choice(n, size=k, replace=False).astype(np.int32)
+        c = oracle.assign(D, M)
+        R = oracle.removal_loss(c, k)
+        T = oracle.fastpam1_table(D, M, c, R)
+        for i in range(k):
+            for x in range(n):
+                if x in M:
+                    continue
+                bf = bf_delta(D, M, i, x)
+                # Eq. eqn:td2 with Alg.2's object set (x_o not in M \ m_i)
+                s = sum(oracle.change(int(D[o, x]), int(c.nearest[o]), int(c.dn[o]), int(c.ds[o]), i)
+                        for o in range(n) if o == M[i] or o not in M)
+                assert s == bf
+                assert T[i, x] == bf
+
+
+def test_assign_against_sorting():
+    rng = np.random.default_rng(3)
+    for _ in range(100):
+        n = int(rng.integers(3, 30))
+        k = int(rng.integers(2, n))
+        D = rand_int_matrix(rng, n, hi=8)    # many ties
+        M = rng.choice(n, size=k, replace=False)
+        c = oracle.assign(D, M)
+        for o in range(n):
+            order = sorted(range(k), key=lambda j: (int(D[o, M[j]]), j))
+            assert c.nearest[o] == order[0] and c.second[o] == order[1]
+            assert c.dn[o] == D[o, M[order[0]]] and c.ds[o] == D[o, M[order[1]]]
+        R = oracle.removal_loss(c, k)
+        assert (R >= 0).all()
+        assert R.sum() == (c.ds - c.dn).sum()
+        for i in range(k):
+            # removal loss = TD increase when medoid i is simply deleted
+            Mi = [m for j, m in enumerate(M) if j != i]
+            assert R[i] == bf_td(D, Mi) - bf_td(D, M)
+
+
+def test_pam_equals_fastpam1_traces_and_local_optimum():
+    rng = np.random.default_rng(2008)
+    for trial in range(200):
+        n = int(rng.integers(10, 41))
+        k = int(rng.integers(2, 9))
+        D = rand_int_matrix(rng, n, hi=int(rng.choice([5, 20, 1000])), symmetric=bool(trial % 4))
+        M0 = rng.choice(n, size=k, replace=False)
+        a = oracle.swap_run(D, M0, oracle.PAM)
+        b = oracle.swap_run(D, M0, oracle.FASTPAM1)
+        assert a.trace == b.trace and a.td == b.td and a.medoids.tolist() == b.medoids.tolist()
+        assert a.converged and a.n_iter == a.n_swaps + 1
+        assert b.td == bf_td(D, b.medoids)                          # TD bookkeeping
+        M = list(M0)
+        prev = bf_td(D, M)
+        for (i, c, dtd) in b.trace:                                  # each applied dTD is exact
+            assert dtd == bf_delta(D, M, i, c) and dtd < 0
+            M[i] = c
+            cur = bf_td(D, M)
+            assert cur < prev
+            prev = cur
+        if trial % 5 == 0:                                           # local optimality (exhaustive)
+            Mf = b.medoids.tolist()
+            for i in range(k):
+                for x in range(n):
+                    if x not in Mf:
+                        assert bf_delta(D, Mf, i, x) >= 0
+            assert b.assignment.tolist() == oracle.assign(D, Mf).nearest.tolist()
+
+
+def test_best_swap_key_is_delta_slot_candidate():
+    """Reading R1: on exact ties the smaller slot, then the smaller candidate wins."""
+    rng = np.random.default_rng(5)
+    seen_tie = 0
+    for _ in range(300):
+        n = int(rng.integers(6, 16))
+        k = int(rng.integers(2, 5))
+        D = rand_int_matrix(rng, n, hi=4)
+        M = rng.choice(n, size=k, replace=False)
+        c = oracle.assign(D, M)
+        R = oracle.removal_loss(c, k)
+        cands = [(bf_delta(D, M, i, x), i, x) for i in range(k) for x in range(n) if x not in M]
+        best = min(cands)
+        if sum(1 for t in cands if t[0] == best[0]) > 1:
+            seen_tie += 1
+        got_p = oracle.pam_best(D, M, c)
+        got_f = oracle.fastpam1_best(D, M, c, R)
+        if best[0] < 0:
+            assert (got_p[0], got_p[1], got_p[2]) == best
+            assert (got_f[0], got_f[1], got_f[2]) == best
+        else:
+            assert got_p[1] == -1 and got_f[1] == -1
+    assert seen_tie > 20
+
+
+def test_degenerate_inputs():
+    # all-zero matrix: every dTD is 0, nothing is accepted (strict <)
+    D = np.zeros((7, 7), np.uint32)
+    r = oracle.swap_run(D, [0, 1, 2], oracle.FASTPAM1)
+    assert r.n_swaps == 0 and r.n_iter == 1 and r.td == 0
+    # exact duplicate points: the duplicate of a medoid is a valid candidate with dTD 0
+    D = line_matrix([0, 0, 5, 5, 9])
+    r = oracle.swap_run(D, [0, 2], oracle.FASTPAM1)
+    assert r.td == bf_td(D, r.medoids)
+    # k = n - 1
+    D = line_matrix([0, 1, 3, 7, 15])
+    r = oracle.swap_run(D, [0, 1, 2, 3], oracle.PAM)
+    r2 = oracle.swap_run(D, [0, 1, 2, 3], oracle.FASTPAM1)
+    assert r.trace == r2.trace and r.td == min(bf_td(D, list(s)) for s in itertools.combinations(range(5), 4))
+    with pytest.raises(ValueError):
+        oracle.swap_run(D, [0], oracle.FASTPAM1)
+
+
+# ---------- BUILD (Alg.1) ----------
+
+def test_build_is_greedy_exact_td_reduction():
+    """Reading R3: each BUILD step adds argmin_c TD(M + {c}) (exact TD change, smallest c)."""
+    rng = np.random.default_rng(17)
+    for trial in range(60):
+        n = int(rng.integers(4, 25))
+        k = int(rng.integers(1, min(7, n - 1) + 1))
+        D = rand_int_matrix(rng, n, hi=int(rng.choice([4, 100])), symmetric=bool(trial % 3))
+        M, td, gains = oracle.build_init(D, k)
+        # first medoid: smallest column sum, smallest index on ties
+        sums = [int(D[:, c].sum()) for c in range(n)]
+        assert M[0] == int(np.argmin(sums)) and gains[0] == min(sums)
+        cur = [int(M[0])]
+        for i in range(1, k):
+            opts = [(bf_td(D, cur + [c]) - bf_td(D, cur), c) for c in range(n) if c not in cur]
+            g, cbest = min(opts)
+            assert (gains[i], M[i]) == (g, cbest)
+            cur.append(cbest)
+        assert td == bf_td(D, cur)
+        assert len(set(M.tolist())) == k
+
+
+# ---------- float path ----------
+
+def test_float_path_bruteforce_and_traces():
+    rng = np.random.default_rng(99)
+    for trial in range(40):
+        n = int(rng.integers(8, 30))
+        k = int(rng.integers(2, 6))
+        X = rng.normal(size=(n, 3))
+        D = np.sqrt(((X[:, None, :] - X[None, :, :]) ** 2).sum(-1)).astype(np.float32)
+        M0 = rng.choice(n, size=k, replace=False)
+        c = oracle.assign(D, M0)
+        R = oracle.removal_loss(c, k)
+        T = oracle.fastpam1_table(D, M0, c, R)
+        for i in range(k):
+            for x in range(n):
+                if x not in M0:
+                    assert T[i, x] == pytest.approx(bf_delta(D, M0, i, x), rel=1e-9, abs=1e-9)
+        a = oracle.swap_run(D, M0, oracle.PAM)
+        b = oracle.swap_run(D, M0, oracle.FASTPAM1)
+        assert [t[:2] for t in a.trace] == [t[:2] for t in b.trace]
+        assert b.td == pytest.approx(bf_td(D, b.medoids), rel=1e-12)
+
+
+# ---------- FastPAM2 (reading R6; parity unpinned by the paper) ----------
+
+def test_fastpam2_reading_properties():
+    rng = np.random.default_rng(45)
+    for trial in range(80):
+        n = int(rng.integers(10, 40))
+        k = int(rng.integers(2, 8))
+        D = rand_int_matrix(rng, n, hi=int(rng.choice([6, 200])))
+        M0 = rng.choice(n, size=k, replace=False)
+        r2 = oracle.swap_run(D, M0, oracle.FASTPAM2)
+        r1 = oracle.swap_run(D, M0, oracle.FASTPAM1)
+        if r1.trace:
+            assert r2.trace[0] == r1.trace[0]             # first swap = FastPAM1's choice
+        M = list(M0)
+        for (i, c, dtd) in r2.trace:                       # every applied dTD is exact and < 0
+            assert c not in M and dtd == bf_delta(D, M, i, c) and dtd < 0
+            M[i] = c
+        assert M == r2.medoids.tolist()
+        assert r2.td == bf_td(D, M)
+        for i in range(k):                                 # final state is a local optimum
+            for x in range(n):
+                if x not in M:
+                    assert bf_delta(D, M, i, x) >= 0
+        assert r2.converged and r2.n_iter >= 1
