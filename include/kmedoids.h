@@ -1,0 +1,192 @@
+/*
+ * kmedoids.h -- C ABI of the B200-native FastPAM SWAP library (libkmedoids.so).
+ *
+ * The problem: given a dissimilarity matrix D
+ * and k, find k medoids M, the assignment of every object to its nearest
+ * medoid, and the total deviation TD = sum_o min_j d(x_o, m_j) (Eq. eqn:td,
+ * P:112-118).  The library implements PAM BUILD (Alg.1), the
+ * FastPAM1 SWAP iteration (Alg.3, Eq. eqn:better-change3
+ * P:797-837) and the FastPAM2 multi-swap iteration (P:861-862, P:945-947,
+ * DESIGN.md reading R6) on one B200 or on a column-sharded set of B200s.
+ *
+ * Conventions that hold for every entry point:
+ *  - d(x_o, x_c) = D[o][c]: row = object o, column = medoid/candidate c
+ *    (reading R0).  D needs no symmetry and no triangle inequality
+ *     but must be >= 0 with d(x,x) = 0 on the diagonal.
+ *  - D is BORROWED: device memory owned by the caller, alive and unmodified
+ *    for the handle's lifetime.  The library never frees it.  Row stride
+ *    `ld` (elements) must be a multiple of 4 and D 16-byte aligned (128-bit
+ *    loads).  Element (o, c) of the local slab is D[o*ld + (c - col_begin)].
+ *  - Sharding: rank r of R holds the column slab [col_begin, col_end) of all
+ *    n rows (candidates are columns).  A single GPU has col_begin = 0,
+ *    col_end = n.  Sharded runs are driven through the phase entry points
+ *    below; every rank calls every function with the same arguments.
+ *  - Medoids live in k slots; a swap replaces slot i in place.
+ *    assignment[o] is the slot of o's nearest medoid; ties go to the smaller
+ *    slot (reading R2).  The best swap is the lexicographic minimum of
+ *    (dTD, slot, candidate) (reading R1).
+ *  - TD / dTD values are int64 for KM_U32 inputs (exact) and double for
+ *    KM_F32 inputs (fp64 sums of f32 values); `td_out` points to an int64_t
+ *    or a double accordingly.  A swap is accepted iff dTD < 0 (U32) or
+ *    dTD < -1e-12*|TD| (F32, reading R5).
+ *  - Errors: every function returns a km_status; nothing is thrown.
+ *    kmedoids_last_error() returns a thread-local description of the last
+ *    failure.  KM_ECUDA leaves the handle unusable (destroy it).
+ *  - All work is enqueued on the handle's CUDA stream; functions that return
+ *    host values synchronise that stream before returning.
+ */
+#ifndef KMEDOIDS_H
+#define KMEDOIDS_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+    KM_OK = 0,
+    KM_CONVERGED = 1,      /* not an error: the best dTD does not improve (Alg.2) */
+    KM_NOT_CONVERGED = 2,  /* max_iter passes ran without convergence */
+    KM_EINVAL = 10,        /* bad argument (sizes, duplicate/out-of-range medoids, alignment, state) */
+    KM_ENOMEM = 11,        /* device or host allocation failed */
+    KM_ECUDA = 12,         /* a CUDA call failed; the handle must be destroyed */
+    KM_ECOMM = 13          /* the sharded exchange was used inconsistently */
+} km_status;
+
+typedef enum { KM_U32 = 0, KM_F32 = 1 } km_dtype;
+typedef enum { KM_FASTPAM1 = 0, KM_FASTPAM2 = 1 } km_variant;
+
+typedef struct km_handle km_handle;  /* opaque; owns only its scratch buffers */
+
+/* Create a handle over the borrowed device slab D (see conventions).
+ *   n: number of objects (rows), 3 <= n < 2^31;  k: medoids, 2 <= k < n
+ *   (BUILD also allows k = 1 through kmedoids_init_build);
+ *   cuda_stream: a cudaStream_t (NULL = legacy default stream).
+ * Allocates O(k*n + n*P) bytes of device scratch (P = internal row parts).
+ * Errors: KM_EINVAL for bad sizes/alignment, KM_ENOMEM, KM_ECUDA. */
+km_status kmedoids_create(km_handle** out, const void* D, km_dtype dtype, int64_t n, int64_t ld,
+                          int64_t col_begin, int64_t col_end, int32_t k, void* cuda_stream);
+
+/* Release the handle's scratch (never D).  Safe on NULL. */
+km_status kmedoids_destroy(km_handle* h);
+
+/* Thread-local message describing the last non-OK status ("" if none). */
+const char* kmedoids_last_error(void);
+
+/* Set the k initial medoids (host array, distinct point indices in [0, n),
+ * slot order) and compute the nearest/second cache (Alg.3) and TD.
+ * Single GPU only; a sharded handle uses kmedoids_shard_set_medoids.
+ * Errors: KM_EINVAL for duplicates / out of range. */
+km_status kmedoids_set_medoids(km_handle* h, const int32_t* medoids);
+
+/* PAM BUILD (Alg.1; readings R3/R4) on the device; leaves the
+ * handle ready for SWAP.  medoids_out (host, k entries) and td_out
+ * (int64_t* or double*) may be NULL.  Single GPU only (sharded BUILD is
+ * driven through kmedoids_build_step*). */
+km_status kmedoids_init_build(km_handle* h, int32_t* medoids_out, void* td_out);
+
+/* One SWAP iteration (FastPAM1: Alg.3; FastPAM2: reading R6) from
+ * the current state.  *swaps_done_out (may be NULL) receives the number of
+ * swaps applied (0 or 1 for FastPAM1, 0..k for FastPAM2); *td_out the TD
+ * after the iteration.  Returns KM_CONVERGED when no swap improves.
+ * Single GPU only. */
+km_status kmedoids_swap_iter(km_handle* h, km_variant variant, int32_t* swaps_done_out, void* td_out);
+
+/* BUILD (if use_build) or the medoids already set, then SWAP iterations until
+ * convergence or max_iter passes (max_iter <= 0 means 2000).  Outputs are
+ * host arrays (any may be NULL): medoids_out[k], assignment_out[n] (slot of
+ * the nearest medoid), td_out, n_iter_out (passes including the final
+ * non-improving one), n_swaps_out.
+ * Returns KM_OK (converged) or KM_NOT_CONVERGED.  Single GPU only. */
+km_status kmedoids_run(km_handle* h, int32_t use_build, km_variant variant, int32_t max_iter,
+                       int32_t* medoids_out, int32_t* assignment_out, void* td_out,
+                       int32_t* n_iter_out, int32_t* n_swaps_out);
+
+/* Whole job from HOST memory: copies D_host (n x n, row stride ld elements,
+ * preferably pinned) to a device buffer the call allocates and frees, then
+ * behaves as kmedoids_run (use_build, variant, max_iter as there).
+ * initial_medoids (host, k) is used when use_build == 0.  Outputs are host
+ * arrays as in kmedoids_run.  Everything (H2D, BUILD, SWAP, D2H) runs on
+ * cuda_stream. */
+km_status kmedoids_run_host(const void* D_host, km_dtype dtype, int64_t n, int64_t ld, int32_t k,
+                            int32_t use_build, const int32_t* initial_medoids, km_variant variant,
+                            int32_t max_iter, void* cuda_stream, int32_t* medoids_out,
+                            int32_t* assignment_out, void* td_out, int32_t* n_iter_out,
+                            int32_t* n_swaps_out);
+
+/* Copy the current state to host arrays (any may be NULL): medoids[k],
+ * assignment[n], td, counters.  Synchronises the stream. */
+km_status kmedoids_get_state(km_handle* h, int32_t* medoids_out, int32_t* assignment_out, void* td_out,
+                             int32_t* n_iter_out, int32_t* n_swaps_out);
+
+/* Copy the nearest/second cache to host: nearest[n], second[n] (slots),
+ * dn[n], ds[n] (in D's element type).  Any may be NULL. */
+km_status kmedoids_get_cache(km_handle* h, int32_t* nearest_out, int32_t* second_out, void* dn_out,
+                             void* ds_out);
+
+/* Diagnostics for parity tests: after kmedoids_eval_candidates, copies the
+ * per-candidate result of the last FastPAM1 evaluation for the local columns
+ * [col_begin, col_end): dtd[c] = min_i dTD(m_i, x_c) (int64/double), slot[c]
+ * = its lexicographic argmin slot; medoid columns get slot -1. */
+km_status kmedoids_eval_candidates(km_handle* h, void* dtd_out, int32_t* slot_out);
+
+/* Profiling: enable (1) / disable (0) CUDA-event timing of the SWAP-delta
+ * stream kernel on the handle's stream; kmedoids_stream_time returns the
+ * accumulated milliseconds and launch count since the last reset. */
+km_status kmedoids_set_profiling(km_handle* h, int32_t enable);
+km_status kmedoids_stream_time(km_handle* h, double* ms_out, int64_t* launches_out, int32_t reset);
+
+/* Number of CUDA kernel launches this handle has issued (all kernels). */
+km_status kmedoids_launch_count(km_handle* h, int64_t* count_out);
+
+/* ---------------- sharded (column-slab) phase API ----------------------
+ * A sharded SWAP iteration on R ranks is, on every rank:
+ *   1. kmedoids_shard_eval(h)          local candidates -> 16-byte record
+ *   2. all-gather the records          (caller, e.g. NCCL over NVLink)
+ *   3. kmedoids_shard_select(h, ...)   lexicographic reduce of the R records
+ *   4. if *found: the owner rank (*owner) packs column c* with
+ *      kmedoids_shard_pack_column, the caller broadcasts the n-element
+ *      column buffer from *owner, and every rank calls
+ *      kmedoids_shard_apply(h) (update M, TD and the nearest/second cache).
+ * Buffers are device memory owned by the handle; the caller moves bytes
+ * between them.  BUILD follows the same pattern with the build_* calls. */
+typedef struct {
+    void* record_send;     /* this rank's record (record_bytes) */
+    void* record_recv;     /* R records, rank order (R*record_bytes), filled by the caller */
+    size_t record_bytes;
+    void* column;          /* n elements of D's type: column c* (owner packs, others receive) */
+    size_t column_bytes;
+} km_exchange;
+
+km_status kmedoids_shard_exchange(km_handle* h, int32_t nranks, km_exchange* out);
+/* Set the medoids on a sharded handle; columns[j*n + o] = d(x_o, m_j) must
+ * be provided by the caller (device, k*n elements), gathered from owners. */
+km_status kmedoids_shard_set_medoids(km_handle* h, const int32_t* medoids, const void* columns_dev);
+km_status kmedoids_shard_eval(km_handle* h);
+/* Reads the R gathered records; writes (host) *found (1 if an improving
+ * swap exists), *slot, *cand (global index), *owner (rank owning cand given
+ * the column ranges passed to kmedoids_shard_exchange... computed from
+ * rank_col_begin[R+1], the column boundaries of all ranks), *dtd (int64_t*
+ * or double*).  Returns KM_CONVERGED when nothing improves. */
+km_status kmedoids_shard_select(km_handle* h, const int64_t* rank_col_begin, int32_t* found, int32_t* slot,
+                                int32_t* cand, int32_t* owner, void* dtd);
+km_status kmedoids_shard_pack_column(km_handle* h, int32_t cand);
+km_status kmedoids_shard_apply(km_handle* h);
+
+/* Sharded BUILD: step 0 evaluates the distance sums (first medoid), steps
+ * 1..k-1 the BUILD gains of the local candidates into record_send; after the
+ * gather, kmedoids_build_select picks the global (value, c) minimum, the
+ * owner packs the column, the caller broadcasts it and kmedoids_build_apply
+ * adds the medoid. */
+km_status kmedoids_build_eval(km_handle* h, int32_t step);
+km_status kmedoids_build_select(km_handle* h, const int64_t* rank_col_begin, int32_t* cand,
+                                int32_t* owner, void* gain);
+km_status kmedoids_build_apply(km_handle* h, int32_t step);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* KMEDOIDS_H */

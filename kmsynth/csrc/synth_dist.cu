@@ -1,0 +1,72 @@
+// synth_dist.cu -- materialise a synthetic dissimilarity matrix on the GPU.
+//
+// INPUT GENERATOR (kmsynth), not part of the method: it turns the seeded
+// point sets of kmsynth/__init__.py into the dense matrix D that both the
+// CUDA path and the oracle consume.  It holds none of the FastPAM arithmetic.
+//
+// metric 0 (L1 on integer coordinates):  D[o][c] = sum_t |x_ot - x_ct|  (exact, uint32)
+// metric 1 (Euclidean, fp64 coordinates): D[o][c] = f32(sqrt(sum_t (x_ot - x_ct)^2))
+//   with every fp64 operation individually rounded in t order (no FMA), so the
+//   result is bit-identical to kmsynth.dist_numpy.
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace {
+constexpr int TILE = 32;
+constexpr int KT = 16;   // coordinates staged per step
+
+template <int METRIC, typename X>
+__global__ void k_dist(const X* __restrict__ pts, int n, int d, int64_t c0, int64_t c1, int64_t ld, void* out) {
+    __shared__ X so[TILE][KT + 1];
+    __shared__ X sc[TILE][KT + 1];
+    const int tx = threadIdx.x, ty = threadIdx.y;          // 32 x 8
+    const int64_t obase = (int64_t)blockIdx.y * TILE, cbase = c0 + (int64_t)blockIdx.x * TILE;
+    long long iacc[4] = {0, 0, 0, 0};
+    double facc[4] = {0, 0, 0, 0};
+    for (int t0 = 0; t0 < d; t0 += KT) {
+        for (int r = ty; r < TILE; r += 8) {
+            for (int t = tx; t < KT; t += 32) {
+                int64_t o = obase + r, c = cbase + r;
+                so[r][t] = (o < n && t0 + t < d) ? pts[o * d + t0 + t] : (X)0;
+                sc[r][t] = (c < c1 && t0 + t < d) ? pts[c * d + t0 + t] : (X)0;
+            }
+        }
+        __syncthreads();
+        const int tend = min(KT, d - t0);
+        for (int t = 0; t < tend; ++t) {
+            const X xc = sc[tx][t];
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                const X xo = so[ty + 8 * q][t];
+                if (METRIC == 0) {
+                    long long df = (long long)xo - (long long)xc;
+                    iacc[q] += df < 0 ? -df : df;
+                } else {
+                    double df = __dsub_rn((double)xo, (double)xc);
+                    facc[q] = __dadd_rn(facc[q], __dmul_rn(df, df));
+                }
+            }
+        }
+        __syncthreads();
+    }
+    const int64_t c = cbase + tx;
+    if (c >= c1) return;
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+        const int64_t o = obase + ty + 8 * q;
+        if (o >= n) continue;
+        if (METRIC == 0) ((uint32_t*)out)[o * ld + (c - c0)] = (uint32_t)iacc[q];
+        else ((float*)out)[o * ld + (c - c0)] = __double2float_rn(__dsqrt_rn(facc[q]));
+    }
+}
+}  // namespace
+
+extern "C" int kmsynth_dist(const void* pts_dev, int metric, int n, int d, int64_t c0, int64_t c1, int64_t ld,
+                            void* out_dev, void* stream) {
+    dim3 blk(32, 8);
+    dim3 grd((unsigned)((c1 - c0 + TILE - 1) / TILE), (unsigned)((n + TILE - 1) / TILE));
+    cudaStream_t st = (cudaStream_t)stream;
+    if (metric == 0) k_dist<0, int32_t><<<grd, blk, 0, st>>>((const int32_t*)pts_dev, n, d, c0, c1, ld, out_dev);
+    else k_dist<1, double><<<grd, blk, 0, st>>>((const double*)pts_dev, n, d, c0, c1, ld, out_dev);
+    return (int)cudaGetLastError();
+}

@@ -1,0 +1,642 @@
+// km_kernels.cuh -- sm_100a kernels of the FastPAM SWAP / BUILD hot path.
+//
+// Kernel map:
+//   a1/a5  k_gather_medoid_cols, k_gather_decided_col, k_assign_full, k_assign_incremental
+//   a2     k_slot_hist, k_scan_counts, k_slot_scatter, k_removal_loss, k_part_meta
+//   a3     k_swap_stream   (the HBM stream; Alg.3, Eq. eqn:better-change3)
+//   a4     k_swap_combine  (per-candidate argmin over slots) + k_select
+//   a7     k_build_stream / k_build_combine / k_build_select / k_build_apply (Alg.1)
+//   a8     k_td_from_dn
+#pragma once
+#include "km_common.cuh"
+
+namespace km {
+
+constexpr unsigned FULL = 0xffffffffu;
+constexpr int SORT_CHUNK = 1024;   // objects per block of the stable counting sort
+
+// ---------------------------------------------------------------------------
+// small helpers
+// ---------------------------------------------------------------------------
+template <typename T> struct Vec4;
+template <> struct Vec4<float> { using type = float4; };
+template <> struct Vec4<uint32_t> { using type = uint4; };
+
+// 128-bit streaming load: read-only path, no L1 allocation (D is read once
+// per iteration; keep L1 for the sorted row info).
+template <typename T>
+__device__ __forceinline__ typename Vec4<T>::type ld_stream4(const T* p) {
+    uint4 r;
+    asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
+                 : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w) : "l"(p));
+    typename Vec4<T>::type v;
+    memcpy(&v, &r, sizeof(r));
+    return v;
+}
+
+template <typename A>
+__device__ __forceinline__ Rec<A> shfl_rec(const Rec<A>& r, int src_xor) {
+    Rec<A> o;
+    o.v = __shfl_xor_sync(FULL, r.v, src_xor);
+    o.slot = __shfl_xor_sync(FULL, r.slot, src_xor);
+    o.c = __shfl_xor_sync(FULL, r.c, src_xor);
+    return o;
+}
+
+template <typename A>
+__device__ __forceinline__ Rec<A> warp_min_rec(Rec<A> r) {
+#pragma unroll
+    for (int s = 16; s >= 1; s >>= 1) {
+        Rec<A> o = shfl_rec(r, s);
+        if (rec_less(o, r)) r = o;
+    }
+    return r;
+}
+
+// Block-wide lexicographic min; result valid in thread 0.
+template <typename A>
+__device__ Rec<A> block_min_rec(Rec<A> r) {
+    __shared__ Rec<A> sm[32];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    r = warp_min_rec(r);
+    if (lane == 0) sm[warp] = r;
+    __syncthreads();
+    const int nw = (blockDim.x + 31) >> 5;
+    if (warp == 0) {
+        r = lane < nw ? sm[lane] : rec_none<A>();
+        r = warp_min_rec(r);
+    }
+    __syncthreads();
+    return r;
+}
+
+// Grid-wide lexicographic min with the last-block-done pattern: every block
+// writes its partial; the last block to finish reduces them in block order
+// (deterministic) and writes *out.  *counter must be 0 on entry; it is reset.
+template <typename A>
+__device__ void grid_min_rec(Rec<A> r, Rec<A>* partials, unsigned* counter, Rec<A>* out) {
+    __shared__ bool am_last;
+    r = block_min_rec(r);
+    if (threadIdx.x == 0) {
+        partials[blockIdx.x] = r;
+        __threadfence();
+        unsigned prev = atomicAdd(counter, 1u);
+        am_last = (prev == gridDim.x - 1);
+    }
+    __syncthreads();
+    if (!am_last) return;
+    __threadfence();
+    Rec<A> m = rec_none<A>();
+    for (int b = threadIdx.x; b < (int)gridDim.x; b += blockDim.x) {
+        Rec<A> q;
+        q.v = __ldcg(&partials[b].v);
+        q.slot = __ldcg(&partials[b].slot);
+        q.c = __ldcg(&partials[b].c);
+        if (rec_less(q, m)) m = q;
+    }
+    m = block_min_rec(m);
+    if (threadIdx.x == 0) {
+        *out = m;
+        *counter = 0;
+    }
+}
+
+// ---------------------------------------------------------------------------
+// a1/a5: medoid columns and the nearest/second cache
+// ---------------------------------------------------------------------------
+
+// MC[j][o] = d(x_o, m_j) for every slot j whose medoid lies in the local
+// column range (single GPU: all of them).  grid = (ceil(n/256), k).
+template <typename T>
+__global__ void k_gather_medoid_cols(const T* __restrict__ D, int64_t ld, int n, int64_t col_begin,
+                                     int64_t col_end, const int* __restrict__ M, T* __restrict__ MC) {
+    const int j = blockIdx.y;
+    const int o = blockIdx.x * blockDim.x + threadIdx.x;
+    const int64_t c = M[j];
+    if (o >= n || c < col_begin || c >= col_end) return;
+    MC[(int64_t)j * n + o] = D[(int64_t)o * ld + (c - col_begin)];
+}
+
+// Column of the decided swap/BUILD candidate: MC[slot][o] = d(x_o, x_c*),
+// written only when the decision applies and c* is local.  For a sharded
+// handle `colbuf` (n elements) also receives the column (pack for broadcast).
+template <typename T, typename A>
+__global__ void k_gather_decided_col(const T* __restrict__ D, int64_t ld, int n, int64_t col_begin,
+                                     int64_t col_end, const Decision<A>* __restrict__ dec,
+                                     T* __restrict__ MC, T* __restrict__ colbuf) {
+    if (!dec->apply) return;
+    const int64_t c = dec->c;
+    if (c < col_begin || c >= col_end) return;
+    const int o = blockIdx.x * blockDim.x + threadIdx.x;
+    if (o >= n) return;
+    T v = D[(int64_t)o * ld + (c - col_begin)];
+    if (MC) MC[(int64_t)dec->slot * n + o] = v;
+    if (colbuf) colbuf[o] = v;
+}
+
+// Sharded: copy the broadcast column into MC[slot].
+template <typename T, typename A>
+__global__ void k_column_to_mc(const T* __restrict__ colbuf, int n, const Decision<A>* __restrict__ dec,
+                               T* __restrict__ MC) {
+    if (!dec->apply) return;
+    const int o = blockIdx.x * blockDim.x + threadIdx.x;
+    if (o < n) MC[(int64_t)dec->slot * n + o] = colbuf[o];
+}
+
+// nearest = lexicographic argmin over slots of (d(x_o, m_j), j); second = the
+// same over j != nearest (reading R2).  One thread per object; MC reads are
+// coalesced across threads.  Needs k >= 2.
+template <typename T>
+__global__ void k_assign_full(const T* __restrict__ MC, int n, int k, int* __restrict__ near,
+                              int* __restrict__ sec, T* __restrict__ dn, T* __restrict__ ds) {
+    const int o = blockIdx.x * blockDim.x + threadIdx.x;
+    if (o >= n) return;
+    T a = MC[o], b = MC[(int64_t)n + o];
+    T d1, d2;
+    int j1, j2;
+    if (b < a) { d1 = b; j1 = 1; d2 = a; j2 = 0; } else { d1 = a; j1 = 0; d2 = b; j2 = 1; }
+    for (int j = 2; j < k; ++j) {
+        T d = MC[(int64_t)j * n + o];
+        if (d < d1) { d2 = d1; j2 = j1; d1 = d; j1 = j; }
+        else if (d < d2) { d2 = d; j2 = j; }
+    }
+    near[o] = j1; sec[o] = j2; dn[o] = d1; ds[o] = d2;
+}
+
+// Incremental update after slot i = dec->slot received a new medoid whose
+// column is MC[i]: objects whose nearest or second was slot i rescan all k
+// slots; every other object only compares the new medoid against its current
+// (nearest, second) pair.  Equal to k_assign_full on the new medoid set.
+template <typename T, typename A>
+__global__ void k_assign_incremental(const T* __restrict__ MC, int n, int k,
+                                     const Decision<A>* __restrict__ dec, int* __restrict__ near,
+                                     int* __restrict__ sec, T* __restrict__ dn, T* __restrict__ ds) {
+    if (!dec->apply) return;
+    const int o = blockIdx.x * blockDim.x + threadIdx.x;
+    if (o >= n) return;
+    const int i = dec->slot;
+    int j1 = near[o], j2 = sec[o];
+    if (j1 == i || j2 == i) {
+        T a = MC[o], b = MC[(int64_t)n + o];
+        T d1, d2;
+        if (b < a) { d1 = b; j1 = 1; d2 = a; j2 = 0; } else { d1 = a; j1 = 0; d2 = b; j2 = 1; }
+        for (int j = 2; j < k; ++j) {
+            T d = MC[(int64_t)j * n + o];
+            if (d < d1) { d2 = d1; j2 = j1; d1 = d; j1 = j; }
+            else if (d < d2) { d2 = d; j2 = j; }
+        }
+        near[o] = j1; sec[o] = j2; dn[o] = d1; ds[o] = d2;
+        return;
+    }
+    const T x = MC[(int64_t)i * n + o];
+    const T d1 = dn[o], d2 = ds[o];
+    if (x < d1 || (x == d1 && i < j1)) {
+        near[o] = i; dn[o] = x; sec[o] = j1; ds[o] = d1;
+    } else if (x < d2 || (x == d2 && i < j2)) {
+        sec[o] = i; ds[o] = x;
+    }
+}
+
+// TD = sum_o d_n(o) (Eq. eqn:td), fixed reduction order.
+template <typename T, typename A>
+__global__ void k_td_from_dn(const T* __restrict__ dn, int n, A* __restrict__ partials,
+                             unsigned* __restrict__ counter, A* __restrict__ td) {
+    __shared__ A sm[32];
+    __shared__ bool am_last;
+    A s = 0;
+    for (int o = blockIdx.x * blockDim.x + threadIdx.x; o < n; o += gridDim.x * blockDim.x) s += (A)dn[o];
+#pragma unroll
+    for (int x = 16; x >= 1; x >>= 1) s += __shfl_xor_sync(FULL, s, x);
+    if ((threadIdx.x & 31) == 0) sm[threadIdx.x >> 5] = s;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        A t = 0;
+        for (int w = 0; w < (int)(blockDim.x >> 5); ++w) t += sm[w];
+        partials[blockIdx.x] = t;
+        __threadfence();
+        am_last = atomicAdd(counter, 1u) == gridDim.x - 1;
+    }
+    __syncthreads();
+    if (am_last && threadIdx.x == 0) {
+        __threadfence();
+        A t = 0;
+        for (int b = 0; b < (int)gridDim.x; ++b) t += __ldcg(&partials[b]);
+        *td = t;
+        *counter = 0;
+    }
+}
+
+// ---------------------------------------------------------------------------
+// a2: stable counting sort of the objects by nearest slot, removal loss
+// ---------------------------------------------------------------------------
+
+// counts[s*B + b] = #objects of chunk b with nearest slot s.
+__global__ void k_slot_hist(const int* __restrict__ near, int n, int k, int* __restrict__ counts) {
+    extern __shared__ int h[];
+    const int B = gridDim.x, b = blockIdx.x;
+    for (int s = threadIdx.x; s < k; s += blockDim.x) h[s] = 0;
+    __syncthreads();
+    const int e0 = b * SORT_CHUNK, e1 = min(n, e0 + SORT_CHUNK);
+    for (int e = e0 + threadIdx.x; e < e1; e += blockDim.x) atomicAdd(&h[near[e]], 1);
+    __syncthreads();
+    for (int s = threadIdx.x; s < k; s += blockDim.x) counts[(int64_t)s * B + b] = h[s];
+}
+
+// Exclusive scan of counts (slot-major) -> offsets; seg_start[s] = first
+// sorted position of slot s, seg_start[k] = n.  Single block of 1024.
+__global__ void k_scan_counts(const int* __restrict__ counts, int total, int B, int k,
+                              int* __restrict__ offsets, int* __restrict__ seg_start) {
+    __shared__ int sums[1024];
+    const int t = threadIdx.x, nt = blockDim.x;
+    const int per = (total + nt - 1) / nt;
+    const int a = t * per, z = min(total, a + per);
+    int s = 0;
+    for (int i = a; i < z; ++i) s += counts[i];
+    sums[t] = s;
+    __syncthreads();
+    for (int off = 1; off < nt; off <<= 1) {     // Hillis-Steele inclusive scan
+        int v = (t >= off) ? sums[t - off] : 0;
+        __syncthreads();
+        sums[t] += v;
+        __syncthreads();
+    }
+    int run = sums[t] - s;
+    for (int i = a; i < z; ++i) {
+        offsets[i] = run;
+        run += counts[i];
+    }
+    __syncthreads();
+    for (int sl = t; sl < k; sl += nt) seg_start[sl] = offsets[(int64_t)sl * B];
+    if (t == 0) seg_start[k] = sums[nt - 1];
+}
+
+// Stable scatter: one warp per chunk walks its objects in index order and
+// places each at offsets[slot][chunk] + (rank among earlier same-slot
+// objects).  The sorted order is therefore (slot, o) ascending -- fixed for a
+// given cache, so every sum over it is deterministic.
+template <typename T>
+__global__ void k_slot_scatter(const int* __restrict__ near, const T* __restrict__ dn,
+                               const T* __restrict__ ds, int n, int k, const int* __restrict__ offsets,
+                               RowInfo<T>* __restrict__ ri) {
+    extern __shared__ int cnt[];
+    const int B = gridDim.x, b = blockIdx.x, lane = threadIdx.x;
+    for (int s = lane; s < k; s += 32) cnt[s] = offsets[(int64_t)s * B + b];
+    __syncwarp();
+    const int e0 = b * SORT_CHUNK, e1 = min(n, e0 + SORT_CHUNK);
+    const unsigned lt = (1u << lane) - 1u;
+    for (int base = e0; base < e1; base += 32) {
+        const int e = base + lane;
+        const bool valid = e < e1;
+        const int s = valid ? near[e] : -1 - lane;
+        const unsigned peers = __match_any_sync(FULL, s);
+        const int rank = __popc(peers & lt);
+        const int leader = __ffs(peers) - 1;
+        int bp = 0;
+        if (valid && lane == leader) bp = cnt[s];
+        bp = __shfl_sync(FULL, bp, leader);
+        __syncwarp();
+        if (valid && lane == leader) cnt[s] = bp + __popc(peers);
+        __syncwarp();
+        if (valid) {
+            RowInfo<T> r;
+            r.o = e; r.slot = s; r.dn = dn[e]; r.ds = ds[e];
+            ri[bp + rank] = r;
+        }
+    }
+}
+
+// Removal loss dTD^{-m_i} = sum_{nearest(o)=i} d_s(o) - d_n(o),
+// one warp per slot over its sorted segment (fixed order).  Slots with an
+// empty segment have R_i = 0 and acc_i = 0: their smallest index is kept in
+// *empty_slot (dTD(m_i, x_c) = dTD^{+x_c} for them).
+template <typename T, typename A>
+__global__ void k_removal_loss(const RowInfo<T>* __restrict__ ri, const int* __restrict__ seg_start, int k,
+                               A* __restrict__ R, int* __restrict__ empty_slot) {
+    const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+    if (warp >= k) return;
+    const int a = seg_start[warp], z = seg_start[warp + 1];
+    A s = 0;
+    for (int p = a + lane; p < z; p += 32) s += (A)ri[p].ds - (A)ri[p].dn;
+#pragma unroll
+    for (int x = 16; x >= 1; x >>= 1) s += __shfl_xor_sync(FULL, s, x);
+    if (lane == 0) {
+        R[warp] = s;
+        if (a == z) atomicMin(empty_slot, warp);
+    }
+}
+
+// Row parts of the stream: part q covers sorted positions [q*n/P, (q+1)*n/P);
+// head/tail slot = slot of its first/last row.
+template <typename T>
+__global__ void k_part_meta(const RowInfo<T>* __restrict__ ri, int n, int P, int* __restrict__ head_slot,
+                            int* __restrict__ tail_slot) {
+    const int q = blockIdx.x * blockDim.x + threadIdx.x;
+    if (q >= P) return;
+    const int64_t p0 = (int64_t)q * n / P, p1 = (int64_t)(q + 1) * n / P;
+    head_slot[q] = ri[p0].slot;
+    tail_slot[q] = ri[p1 - 1].slot;
+}
+
+// ---------------------------------------------------------------------------
+// a3: the SWAP-delta stream (Alg.3, Eq. eqn:better-change3)
+// ---------------------------------------------------------------------------
+//
+// A CTA of WARPS warps owns WARPS*128 consecutive candidate columns; lane l of
+// warp w owns the 4 columns cb..cb+3.  blockIdx.y selects a part of the
+// slot-sorted row order.  For every row o (in sorted order) the warp loads
+// D[o][cb..cb+3] (one 128-bit load per lane, 512 contiguous bytes per warp)
+// and applies, per candidate column c:
+//     d < d_n(o):          plus_c += d - d_n(o);  acc_c[nearest(o)] += d_n - d_s
+//     d_n(o) <= d < d_s(o): acc_c[nearest(o)] += d - d_s(o)
+// Because rows arrive grouped by nearest(o), acc_c[i] is the running segment
+// sum `seg` held in registers; at the end of each slot's segment the value
+// dTD_i - dTD^{+x_c} = R_i + seg is final and enters a running
+// lexicographic min (interior segments), or is emitted as the part's head /
+// tail partial sum (segments cut by part boundaries; completed by
+// k_swap_combine).  No k-vector is ever materialised.
+template <typename T, typename A, int WARPS, int U>
+__global__ void __launch_bounds__(WARPS * 32)
+k_swap_stream(const T* __restrict__ D, int64_t ld, int w, int n, int P,
+              const RowInfo<T>* __restrict__ ri, const A* __restrict__ R,
+              A* __restrict__ out_plus, A* __restrict__ out_head, A* __restrict__ out_tail,
+              A* __restrict__ out_imin, int* __restrict__ out_islot) {
+    using V = typename Vec4<T>::type;
+    const int q = blockIdx.y;
+    const int64_t p0 = (int64_t)q * n / P, p1 = (int64_t)(q + 1) * n / P;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int cb = (blockIdx.x * WARPS + warp) * 128 + lane * 4;
+    const bool active = cb < w;
+    const T* Dc = D + (active ? cb : 0);
+
+    A plus[4], seg[4], head[4], imin[4];
+    int islot[4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) { plus[j] = 0; seg[j] = 0; head[j] = 0; imin[j] = amax<A>(); islot[j] = -1; }
+    int cur = ri[p0].slot;
+    bool first = true;
+
+    for (int64_t p = p0; p < p1; p += U) {
+        const int nb = (int)min((int64_t)U, p1 - p);
+        RowInfo<T> r[U];
+        V v[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u)
+            if (u < nb) r[u] = ri[p + u];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            if (u < nb && active) {
+                v[u] = ld_stream4(Dc + (int64_t)r[u].o * ld);
+            } else {
+                T big = dmax<T>();
+                memcpy(&v[u].x, &big, sizeof(T)); memcpy(&v[u].y, &big, sizeof(T));
+                memcpy(&v[u].z, &big, sizeof(T)); memcpy(&v[u].w, &big, sizeof(T));
+            }
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            if (u >= nb) break;
+            if (r[u].slot != cur) {                       // end of slot cur's segment (warp-uniform)
+                if (first) {
+#pragma unroll
+                    for (int j = 0; j < 4; ++j) head[j] = seg[j];
+                    first = false;
+                } else {
+                    const A rv = R[cur];
+#pragma unroll
+                    for (int j = 0; j < 4; ++j) {
+                        const A val = rv + seg[j];
+                        if (val < imin[j]) { imin[j] = val; islot[j] = cur; }
+                    }
+                }
+#pragma unroll
+                for (int j = 0; j < 4; ++j) seg[j] = 0;
+                cur = r[u].slot;
+            }
+            const T dn = r[u].dn, ds = r[u].ds;
+            T x[4];
+            memcpy(&x[0], &v[u].x, sizeof(T)); memcpy(&x[1], &v[u].y, sizeof(T));
+            memcpy(&x[2], &v[u].z, sizeof(T)); memcpy(&x[3], &v[u].w, sizeof(T));
+            const bool hit = (x[0] < ds) | (x[1] < ds) | (x[2] < ds) | (x[3] < ds);
+            if (__any_sync(FULL, hit)) {
+                const A dnA = (A)dn, dsA = (A)ds, dnds = dnA - dsA;
+#pragma unroll
+                for (int j = 0; j < 4; ++j) {
+                    if (x[j] < ds) {
+                        const A xa = (A)x[j];
+                        if (x[j] < dn) { plus[j] += xa - dnA; seg[j] += dnds; }
+                        else { seg[j] += xa - dsA; }
+                    }
+                }
+            }
+        }
+    }
+    if (first) {
+#pragma unroll
+        for (int j = 0; j < 4; ++j) { head[j] = seg[j]; seg[j] = 0; }
+    }
+    if (!active) return;
+    const int64_t base = (int64_t)q * w;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+        const int c = cb + j;
+        if (c < w) {
+            out_plus[base + c] = plus[j];
+            out_head[base + c] = head[j];
+            out_tail[base + c] = seg[j];
+            out_imin[base + c] = imin[j];
+            out_islot[base + c] = islot[j];
+        }
+    }
+}
+
+// a4: complete the segments cut by part boundaries, take the lexicographic
+// min over slots of (R_i + acc_i, i) (Alg.3, smaller slot on ties), add
+// dTD^{+x_c}, mask medoids, and reduce (dTD, i, c) over the grid.
+template <typename A>
+__global__ void k_swap_combine(int w, int64_t col_begin, int P, const A* __restrict__ in_plus,
+                               const A* __restrict__ in_head, const A* __restrict__ in_tail,
+                               const A* __restrict__ in_imin, const int* __restrict__ in_islot,
+                               const int* __restrict__ head_slot, const int* __restrict__ tail_slot,
+                               const A* __restrict__ R, const int* __restrict__ empty_slot,
+                               const int* __restrict__ point_slot, A* __restrict__ cand_v,
+                               int* __restrict__ cand_slot, Rec<A>* partials, unsigned* counter,
+                               Rec<A>* out) {
+    const int cl = blockIdx.x * blockDim.x + threadIdx.x;
+    Rec<A> best = rec_none<A>();
+    if (cl < w) {
+        A bv = amax<A>();
+        int bs = INT_MAX;
+        const int es = *empty_slot;
+        if (es != INT_MAX) { bv = 0; bs = es; }
+        auto fin = [&](int s, A sum) {
+            const A val = R[s] + sum;
+            if (val < bv || (val == bv && s < bs)) { bv = val; bs = s; }
+        };
+        A plus = 0, carry = 0;
+        int cs = -1;
+        for (int q = 0; q < P; ++q) {
+            const int64_t idx = (int64_t)q * w + cl;
+            plus += in_plus[idx];
+            const int h = head_slot[q], t = tail_slot[q];
+            const A hv = in_head[idx];
+            if (h == cs) {
+                carry += hv;
+            } else {
+                if (cs >= 0) fin(cs, carry);
+                cs = h;
+                carry = hv;
+            }
+            const int is = in_islot[idx];
+            if (is >= 0) {
+                const A iv = in_imin[idx];
+                if (iv < bv || (iv == bv && is < bs)) { bv = iv; bs = is; }
+            }
+            if (t != h) {
+                fin(cs, carry);
+                cs = t;
+                carry = in_tail[idx];
+            }
+        }
+        fin(cs, carry);
+        const A dtd = bv + plus;
+        const int64_t c = col_begin + cl;
+        const bool medoid = point_slot[c] >= 0;
+        cand_v[cl] = dtd;
+        cand_slot[cl] = medoid ? -1 : bs;
+        if (!medoid) { best.v = dtd; best.slot = bs; best.c = (int)c; }
+    }
+    grid_min_rec(best, partials, counter, out);
+}
+
+// Acceptance (reading R5) and bookkeeping of the chosen swap (Alg.3):
+// lexicographic min over the gathered per-rank records, then M[i*] <- c*,
+// TD <- TD + dTD*.  Runs as one thread; identical on every rank.
+template <typename A>
+__global__ void k_select(const Rec<A>* __restrict__ recs, int nrec, A* __restrict__ td, int* __restrict__ M,
+                         int* __restrict__ point_slot, Decision<A>* __restrict__ dec) {
+    Rec<A> b = rec_none<A>();
+    for (int r = 0; r < nrec; ++r)
+        if (rec_less(recs[r], b)) b = recs[r];
+    bool improving;
+    if (b.slot == INT_MAX) improving = false;
+    else if (std::is_same<A, double>::value) improving = (double)b.v < -1e-12 * fabs((double)*td);
+    else improving = b.v < 0;
+    dec->iters += 1;
+    dec->apply = improving ? 1 : 0;
+    dec->dtd = b.v;
+    dec->slot = b.slot;
+    dec->c = b.c;
+    if (improving) {
+        const int old = M[b.slot];
+        dec->old_m = old;
+        M[b.slot] = b.c;
+        point_slot[old] = -1;
+        point_slot[b.c] = b.slot;
+        *td += b.v;
+        dec->swaps += 1;
+    }
+}
+
+// ---------------------------------------------------------------------------
+// a7: BUILD (Alg.1)
+// ---------------------------------------------------------------------------
+// Same column-tile layout as k_swap_stream, rows in natural order.
+// MODE 0 (first medoid):  acc_c = sum_o d(x_o, x_c)
+// MODE 1 (later medoids): acc_c = sum_o min(d(x_o, x_c) - d_n(o), 0)
+// (medoid rows have d_n = 0 and contribute 0 since D >= 0; the x_o = x_c row
+// contributes -d_n(c): reading R3).
+template <typename T, typename A, int WARPS, int U, int MODE>
+__global__ void __launch_bounds__(WARPS * 32)
+k_build_stream(const T* __restrict__ D, int64_t ld, int w, int n, int P, const T* __restrict__ dn,
+               A* __restrict__ out) {
+    using V = typename Vec4<T>::type;
+    const int q = blockIdx.y;
+    const int64_t p0 = (int64_t)q * n / P, p1 = (int64_t)(q + 1) * n / P;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int cb = (blockIdx.x * WARPS + warp) * 128 + lane * 4;
+    if (cb >= w) return;                      // no warp-collective ops below
+    const T* Dc = D + cb;
+    A acc[4] = {0, 0, 0, 0};
+    for (int64_t p = p0; p < p1; p += U) {
+        const int nb = (int)min((int64_t)U, p1 - p);
+        V v[U];
+        T dv[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u)
+            if (u < nb) {
+                v[u] = ld_stream4(Dc + (p + u) * ld);
+                if (MODE == 1) dv[u] = dn[p + u];
+            }
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            if (u >= nb) break;
+            T x[4];
+            memcpy(&x[0], &v[u].x, sizeof(T)); memcpy(&x[1], &v[u].y, sizeof(T));
+            memcpy(&x[2], &v[u].z, sizeof(T)); memcpy(&x[3], &v[u].w, sizeof(T));
+            if (MODE == 0) {
+#pragma unroll
+                for (int j = 0; j < 4; ++j) acc[j] += (A)x[j];
+            } else {
+                const T d0 = dv[u];
+                const A dA = (A)d0;
+#pragma unroll
+                for (int j = 0; j < 4; ++j)
+                    if (x[j] < d0) acc[j] += (A)x[j] - dA;
+            }
+        }
+    }
+    const int64_t base = (int64_t)q * w;
+#pragma unroll
+    for (int j = 0; j < 4; ++j)
+        if (cb + j < w) out[base + cb + j] = acc[j];
+}
+
+// Per candidate: sum the parts in order; MODE 0 removes the x_o = x_c term
+// (Alg.1 P:288 "x_o != x_c"); non-medoids enter a (value, c) min (slot = 0).
+template <typename T, typename A, int MODE>
+__global__ void k_build_combine(const T* __restrict__ D, int64_t ld, int w, int64_t col_begin, int P,
+                                const A* __restrict__ in, const int* __restrict__ point_slot,
+                                Rec<A>* partials, unsigned* counter, Rec<A>* out) {
+    const int cl = blockIdx.x * blockDim.x + threadIdx.x;
+    Rec<A> best = rec_none<A>();
+    if (cl < w) {
+        const int64_t c = col_begin + cl;
+        A s = 0;
+        for (int q = 0; q < P; ++q) s += in[(int64_t)q * w + cl];
+        if (MODE == 0) s -= (A)D[c * ld + cl];
+        if (point_slot[c] < 0) { best.v = s; best.slot = 0; best.c = (int)c; }
+    }
+    grid_min_rec(best, partials, counter, out);
+}
+
+// BUILD step bookkeeping: slot `step` <- c*, TD <- value (step
+// 0) or TD + dTD* (later steps).
+template <typename A>
+__global__ void k_build_select(const Rec<A>* __restrict__ recs, int nrec, int step, A* __restrict__ td,
+                               int* __restrict__ M, int* __restrict__ point_slot, Decision<A>* __restrict__ dec) {
+    Rec<A> b = rec_none<A>();
+    for (int r = 0; r < nrec; ++r)
+        if (rec_less(recs[r], b)) b = recs[r];
+    dec->apply = 1;
+    dec->dtd = b.v;
+    dec->slot = step;
+    dec->c = b.c;
+    dec->old_m = -1;
+    M[step] = b.c;
+    point_slot[b.c] = step;
+    if (step == 0) *td = b.v; else *td += b.v;
+}
+
+// d_nearest update (P:295-298 for step 0, P:313-316 later): medoids get 0.
+template <typename T, typename A>
+__global__ void k_build_dn(const T* __restrict__ MC, int n, const Decision<A>* __restrict__ dec,
+                           const int* __restrict__ point_slot, T* __restrict__ dn) {
+    const int o = blockIdx.x * blockDim.x + threadIdx.x;
+    if (o >= n) return;
+    const int step = dec->slot;
+    const T x = MC[(int64_t)step * n + o];
+    if (point_slot[o] >= 0) dn[o] = 0;
+    else if (step == 0 || x < dn[o]) dn[o] = x;
+}
+
+}  // namespace km

@@ -1,0 +1,716 @@
+// kmedoids.cu -- host driver and C ABI (include/kmedoids.h) of the B200
+// FastPAM SWAP library.  Every step of the hot path runs in the kernels of
+// km_kernels.cuh; this file only validates arguments, owns scratch buffers,
+// enqueues kernels on the handle's stream and copies the per-iteration
+// decision (one 32-byte record) back to the host for the convergence test.
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <memory>
+#include <string>
+#include <type_traits>
+#include <vector>
+
+#include "../../include/kmedoids.h"
+#include "km_kernels.cuh"
+
+namespace {
+
+thread_local std::string g_err;
+
+km_status fail(km_status s, const char* fmt, ...) {
+    char buf[512];
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(buf, sizeof(buf), fmt, ap);
+    va_end(ap);
+    g_err = buf;
+    return s;
+}
+
+#define KM_CK(call)                                                                               \
+    do {                                                                                          \
+        cudaError_t e_ = (call);                                                                  \
+        if (e_ != cudaSuccess) return fail(KM_ECUDA, "%s failed: %s", #call, cudaGetErrorString(e_)); \
+    } while (0)
+
+#define KM_CKL()                                                                                  \
+    do {                                                                                          \
+        ++launches;                                                                               \
+        cudaError_t e_ = cudaGetLastError();                                                      \
+        if (e_ != cudaSuccess) return fail(KM_ECUDA, "kernel launch failed (kmedoids.cu:%d): %s", __LINE__, cudaGetErrorString(e_)); \
+    } while (0)
+
+#define KM_TRY(expr)                  \
+    do {                              \
+        km_status s_ = (expr);        \
+        if (s_ != KM_OK) return s_;   \
+    } while (0)
+
+constexpr int NUM_SMS = 148;
+constexpr int STREAM_WARPS = 4;               // 4 warps x 128 columns = 512 columns per CTA
+constexpr int STREAM_COLS = STREAM_WARPS * 128;
+constexpr int STREAM_U = 8;                   // rows in flight per warp
+constexpr int RESIDENT_CTAS = 4;              // ~16 warps per SM
+constexpr int TARGET_WAVES = 3;
+constexpr int MAX_K = 8192;
+
+int64_t cdiv(int64_t a, int64_t b) { return (a + b - 1) / b; }
+
+// Number of row parts so the (column tiles x parts) grid fills the GPU.
+int choose_parts(int64_t n, int64_t w) {
+    const int64_t ncb = cdiv(w, STREAM_COLS);
+    int64_t P = cdiv((int64_t)NUM_SMS * RESIDENT_CTAS * TARGET_WAVES, ncb);
+    P = std::min<int64_t>(P, std::max<int64_t>(1, n / 64));
+    P = std::max<int64_t>(P, 1);
+    return (int)P;
+}
+
+
+}  // namespace
+
+struct ImplBase {
+    virtual ~ImplBase() {}
+    virtual km_status set_medoids(const int32_t* M) = 0;
+    virtual km_status init_build(int32_t* M_out, void* td_out) = 0;
+    virtual km_status swap_iter(km_variant v, int32_t* swaps, void* td_out) = 0;
+    virtual km_status get_state(int32_t* M, int32_t* asg, void* td, int32_t* it, int32_t* sw) = 0;
+    virtual km_status get_cache(int32_t* nr, int32_t* sc, void* dn, void* ds) = 0;
+    virtual km_status eval_candidates(void* v, int32_t* s) = 0;
+    virtual km_status shard_exchange(int32_t nranks, km_exchange* out) = 0;
+    virtual km_status shard_set_medoids(const int32_t* M, const void* cols) = 0;
+    virtual km_status shard_eval() = 0;
+    virtual km_status shard_select(const int64_t* rcb, int32_t* found, int32_t* slot, int32_t* cand,
+                                   int32_t* owner, void* dtd) = 0;
+    virtual km_status shard_pack_column(int32_t cand) = 0;
+    virtual km_status shard_apply() = 0;
+    virtual km_status build_eval(int32_t step) = 0;
+    virtual km_status build_select(const int64_t* rcb, int32_t* cand, int32_t* owner, void* gain) = 0;
+    virtual km_status build_apply(int32_t step) = 0;
+    bool profiling = false;
+    double prof_ms = 0.0;
+    int64_t prof_launches = 0;
+    int64_t launches = 0;
+    int k = 0;
+    int64_t n = 0;
+    bool sharded = false;
+};
+
+struct km_handle {
+    std::unique_ptr<ImplBase> impl;
+};
+
+namespace {
+
+template <typename T>
+struct Impl : ImplBase {
+    using A = typename km::Acc<T>::type;
+    using RI = km::RowInfo<T>;
+    using Rec = km::Rec<A>;
+    using Dec = km::Decision<A>;
+
+    const T* D = nullptr;
+    int64_t ld = 0, c0 = 0, c1 = 0;
+    int w = 0;
+    cudaStream_t st = nullptr;
+    int P = 1, Pb = 1, B = 1, ncomb = 1, ntd = 1;
+    int nranks = 1;
+    bool ready = false;     // medoids + cache valid
+
+    std::vector<void*> bufs;        // every device allocation, freed in the destructor
+    int *M = nullptr, *point_slot = nullptr, *near = nullptr, *sec = nullptr;
+    T *MC = nullptr, *dn = nullptr, *ds = nullptr, *colbuf = nullptr;
+    RI* ri = nullptr;
+    int *counts = nullptr, *offsets = nullptr, *seg_start = nullptr, *empty_slot = nullptr;
+    int *head_slot = nullptr, *tail_slot = nullptr;
+    A *R = nullptr, *o_plus = nullptr, *o_head = nullptr, *o_tail = nullptr, *o_imin = nullptr;
+    int* o_islot = nullptr;
+    A* b_out = nullptr;
+    A* cand_v = nullptr;
+    int* cand_slot = nullptr;
+    Rec *partials = nullptr, *rec_local = nullptr, *rec_recv = nullptr;
+    unsigned* counters = nullptr;   // [0] combine, [1] td
+    A *td = nullptr, *td_partials = nullptr;
+    Dec* dec = nullptr;
+    Dec* h_dec = nullptr;           // pinned mirror
+    cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+
+    ~Impl() override {
+        for (void* p : bufs) cudaFree(p);
+        if (h_dec) cudaFreeHost(h_dec);
+        if (ev0) cudaEventDestroy(ev0);
+        if (ev1) cudaEventDestroy(ev1);
+    }
+
+    template <typename X>
+    km_status alloc(X** out, size_t count) {
+        void* p = nullptr;
+        size_t bytes = std::max<size_t>(count, 1) * sizeof(X);
+        cudaError_t e = cudaMalloc(&p, bytes);
+        if (e != cudaSuccess) {
+            cudaGetLastError();
+            return fail(KM_ENOMEM, "cudaMalloc(%zu bytes) failed: %s", bytes, cudaGetErrorString(e));
+        }
+        bufs.push_back(p);
+        *out = (X*)p;
+        return KM_OK;
+    }
+
+    km_status init(const void* Dp, int64_t n_, int64_t ld_, int64_t c0_, int64_t c1_, int k_, cudaStream_t s) {
+        D = (const T*)Dp; n = n_; ld = ld_; c0 = c0_; c1 = c1_; k = k_; st = s;
+        w = (int)(c1 - c0);
+        sharded = !(c0 == 0 && c1 == n);
+        P = choose_parts(n, w);
+        Pb = P;
+        B = (int)cdiv(n, km::SORT_CHUNK);
+        ncomb = (int)cdiv(w, 256);
+        ntd = (int)std::min<int64_t>(cdiv(n, 256), 1024);
+        KM_TRY(alloc(&M, k));
+        KM_TRY(alloc(&point_slot, n));
+        KM_TRY(alloc(&near, n));
+        KM_TRY(alloc(&sec, n));
+        KM_TRY(alloc(&MC, (size_t)k * n));
+        KM_TRY(alloc(&dn, n));
+        KM_TRY(alloc(&ds, n));
+        KM_TRY(alloc(&colbuf, n));
+        KM_TRY(alloc(&ri, n));
+        KM_TRY(alloc(&counts, (size_t)k * B));
+        KM_TRY(alloc(&offsets, (size_t)k * B));
+        KM_TRY(alloc(&seg_start, k + 1));
+        KM_TRY(alloc(&empty_slot, 1));
+        KM_TRY(alloc(&head_slot, P));
+        KM_TRY(alloc(&tail_slot, P));
+        KM_TRY(alloc(&R, k));
+        const size_t pw = (size_t)P * w;
+        KM_TRY(alloc(&o_plus, pw));
+        KM_TRY(alloc(&o_head, pw));
+        KM_TRY(alloc(&o_tail, pw));
+        KM_TRY(alloc(&o_imin, pw));
+        KM_TRY(alloc(&o_islot, pw));
+        b_out = o_plus;   // BUILD partial sums reuse the plus buffer (Pb == P)
+        KM_TRY(alloc(&cand_v, w));
+        KM_TRY(alloc(&cand_slot, w));
+        KM_TRY(alloc(&partials, std::max(ncomb, 1)));
+        KM_TRY(alloc(&rec_local, 1));
+        KM_TRY(alloc(&counters, 2));
+        KM_TRY(alloc(&td, 1));
+        KM_TRY(alloc(&td_partials, ntd));
+        KM_TRY(alloc(&dec, 1));
+        KM_CK(cudaMemsetAsync(counters, 0, 2 * sizeof(unsigned), st));
+        KM_CK(cudaMemsetAsync(dec, 0, sizeof(Dec), st));
+        KM_CK(cudaMemsetAsync(point_slot, 0xff, n * sizeof(int), st));
+        KM_CK(cudaMallocHost((void**)&h_dec, sizeof(Dec)));
+        memset(h_dec, 0, sizeof(Dec));
+        KM_CK(cudaEventCreate(&ev0));
+        KM_CK(cudaEventCreate(&ev1));
+        KM_CK(cudaStreamSynchronize(st));
+        return KM_OK;
+    }
+
+    // ---- pieces of the hot path -------------------------------------------
+    km_status sync_dec() {
+        KM_CK(cudaMemcpyAsync(h_dec, dec, sizeof(Dec), cudaMemcpyDeviceToHost, st));
+        KM_CK(cudaStreamSynchronize(st));
+        if (profiling && pending_prof) {
+            float ms = 0.f;
+            KM_CK(cudaEventElapsedTime(&ms, ev0, ev1));
+            prof_ms += ms;
+            prof_launches += 1;
+            pending_prof = false;
+        }
+        return KM_OK;
+    }
+    bool pending_prof = false;
+
+    km_status assign_full_and_td() {
+        const int nb = (int)cdiv(n, 256);
+        km::k_assign_full<T><<<nb, 256, 0, st>>>(MC, (int)n, k, near, sec, dn, ds);
+        KM_CKL();
+        km::k_td_from_dn<T, A><<<ntd, 256, 0, st>>>(dn, (int)n, td_partials, counters + 1, td);
+        KM_CKL();
+        return KM_OK;
+    }
+
+    km_status set_point_slots(const int32_t* Mh) {
+        std::vector<int32_t> ps((size_t)n, -1);
+        for (int j = 0; j < k; ++j) {
+            if (Mh[j] < 0 || Mh[j] >= n) return fail(KM_EINVAL, "medoid %d out of range [0,%lld)", Mh[j], (long long)n);
+            if (ps[Mh[j]] >= 0) return fail(KM_EINVAL, "duplicate medoid %d", Mh[j]);
+            ps[Mh[j]] = j;
+        }
+        KM_CK(cudaMemcpyAsync(M, Mh, k * sizeof(int32_t), cudaMemcpyHostToDevice, st));
+        KM_CK(cudaMemcpyAsync(point_slot, ps.data(), n * sizeof(int32_t), cudaMemcpyHostToDevice, st));
+        KM_CK(cudaStreamSynchronize(st));   // ps goes out of scope
+        return KM_OK;
+    }
+
+    km_status reset_counters() {
+        KM_CK(cudaMemsetAsync(dec, 0, sizeof(Dec), st));
+        return KM_OK;
+    }
+
+    km_status set_medoids(const int32_t* Mh) override {
+        if (sharded) return fail(KM_EINVAL, "set_medoids on a sharded handle; use kmedoids_shard_set_medoids");
+        if (k < 2) return fail(KM_EINVAL, "SWAP needs k >= 2");
+        KM_TRY(set_point_slots(Mh));
+        dim3 g((unsigned)cdiv(n, 256), k);
+        km::k_gather_medoid_cols<T><<<g, 256, 0, st>>>(D, ld, (int)n, c0, c1, M, MC);
+        KM_CKL();
+        KM_TRY(assign_full_and_td());
+        KM_TRY(reset_counters());
+        KM_CK(cudaStreamSynchronize(st));
+        ready = true;
+        return KM_OK;
+    }
+
+    // a2: sort rows by nearest slot, removal loss, part metadata.
+    km_status prep() {
+        km::k_slot_hist<<<B, 256, k * sizeof(int), st>>>(near, (int)n, k, counts);
+        KM_CKL();
+        km::k_scan_counts<<<1, 1024, 0, st>>>(counts, k * B, B, k, offsets, seg_start);
+        KM_CKL();
+        const int big = INT_MAX;
+        KM_CK(cudaMemcpyAsync(empty_slot, &big, sizeof(int), cudaMemcpyHostToDevice, st));
+        km::k_slot_scatter<T><<<B, 32, k * sizeof(int), st>>>(near, dn, ds, (int)n, k, offsets, ri);
+        KM_CKL();
+        km::k_removal_loss<T, A><<<(unsigned)cdiv((int64_t)k * 32, 256), 256, 0, st>>>(ri, seg_start, k, R, empty_slot);
+        KM_CKL();
+        km::k_part_meta<T><<<(unsigned)cdiv(P, 128), 128, 0, st>>>(ri, (int)n, P, head_slot, tail_slot);
+        KM_CKL();
+        return KM_OK;
+    }
+
+    // a3 + a4 (local): stream the slab, combine into the local best record.
+    km_status eval_local() {
+        KM_TRY(prep());
+        dim3 g((unsigned)cdiv(w, STREAM_COLS), P);
+        if (profiling) KM_CK(cudaEventRecord(ev0, st));
+        km::k_swap_stream<T, A, STREAM_WARPS, STREAM_U><<<g, STREAM_WARPS * 32, 0, st>>>(
+            D, ld, w, (int)n, P, ri, R, o_plus, o_head, o_tail, o_imin, o_islot);
+        KM_CKL();
+        if (profiling) { KM_CK(cudaEventRecord(ev1, st)); pending_prof = true; }
+        km::k_swap_combine<A><<<ncomb, 256, 0, st>>>(w, c0, P, o_plus, o_head, o_tail, o_imin, o_islot, head_slot,
+                                                      tail_slot, R, empty_slot, point_slot, cand_v, cand_slot,
+                                                      partials, counters, rec_local);
+        KM_CKL();
+        return KM_OK;
+    }
+
+    km_status apply_local() {
+        const int nb = (int)cdiv(n, 256);
+        km::k_gather_decided_col<T, A><<<nb, 256, 0, st>>>(D, ld, (int)n, c0, c1, dec, MC, nullptr);
+        KM_CKL();
+        km::k_assign_incremental<T, A><<<nb, 256, 0, st>>>(MC, (int)n, k, dec, near, sec, dn, ds);
+        KM_CKL();
+        return KM_OK;
+    }
+
+    void copy_td(void* td_out) {
+        if (!td_out) return;
+        A v;
+        cudaMemcpy(&v, td, sizeof(A), cudaMemcpyDeviceToHost);
+        memcpy(td_out, &v, sizeof(A));
+    }
+
+    km_status swap_iter(km_variant v, int32_t* swaps, void* td_out) override {
+        if (sharded) return fail(KM_EINVAL, "swap_iter on a sharded handle; use the kmedoids_shard_* phases");
+        if (!ready) return fail(KM_EINVAL, "no medoids: call kmedoids_set_medoids or kmedoids_init_build first");
+        if (v != KM_FASTPAM1 && v != KM_FASTPAM2) return fail(KM_EINVAL, "unknown variant %d", (int)v);
+        if (v == KM_FASTPAM2) return swap_iter_fp2(swaps, td_out);
+        KM_TRY(eval_local());
+        km::k_select<A><<<1, 1, 0, st>>>(rec_local, 1, td, M, point_slot, dec);
+        KM_CKL();
+        KM_TRY(apply_local());
+        KM_TRY(sync_dec());
+        if (swaps) *swaps = h_dec->apply;
+        copy_td(td_out);
+        return h_dec->apply ? KM_OK : KM_CONVERGED;
+    }
+
+    km_status swap_iter_fp2(int32_t*, void*) {
+        return fail(KM_EINVAL, "FastPAM2 is not implemented yet");
+    }
+
+    // ---- BUILD ---------------------------------------------------------------
+    km_status build_eval(int32_t step) override {
+        if (step < 0 || step >= k) return fail(KM_EINVAL, "build step %d out of range", step);
+        dim3 g((unsigned)cdiv(w, STREAM_COLS), Pb);
+        if (step == 0) {
+            km::k_build_stream<T, A, STREAM_WARPS, STREAM_U, 0><<<g, STREAM_WARPS * 32, 0, st>>>(D, ld, w, (int)n, Pb, dn, b_out);
+            KM_CKL();
+            km::k_build_combine<T, A, 0><<<ncomb, 256, 0, st>>>(D, ld, w, c0, Pb, b_out, point_slot, partials, counters, rec_local);
+            KM_CKL();
+        } else {
+            km::k_build_stream<T, A, STREAM_WARPS, STREAM_U, 1><<<g, STREAM_WARPS * 32, 0, st>>>(D, ld, w, (int)n, Pb, dn, b_out);
+            KM_CKL();
+            km::k_build_combine<T, A, 1><<<ncomb, 256, 0, st>>>(D, ld, w, c0, Pb, b_out, point_slot, partials, counters, rec_local);
+            KM_CKL();
+        }
+        return KM_OK;
+    }
+
+    km_status build_finish() {
+        if (k >= 2) {
+            KM_TRY(assign_full_and_td());
+            ready = true;
+        }
+        KM_TRY(reset_counters());
+        return KM_OK;
+    }
+
+    km_status init_build(int32_t* M_out, void* td_out) override {
+        if (sharded) return fail(KM_EINVAL, "init_build on a sharded handle; use kmedoids_build_* phases");
+        KM_CK(cudaMemsetAsync(point_slot, 0xff, n * sizeof(int), st));
+        ready = false;
+        const int nb = (int)cdiv(n, 256);
+        for (int step = 0; step < k; ++step) {
+            KM_TRY(build_eval(step));
+            km::k_build_select<A><<<1, 1, 0, st>>>(rec_local, 1, step, td, M, point_slot, dec);
+            KM_CKL();
+            km::k_gather_decided_col<T, A><<<nb, 256, 0, st>>>(D, ld, (int)n, c0, c1, dec, MC, nullptr);
+            KM_CKL();
+            km::k_build_dn<T, A><<<nb, 256, 0, st>>>(MC, (int)n, dec, point_slot, dn);
+            KM_CKL();
+        }
+        KM_TRY(build_finish());
+        KM_CK(cudaStreamSynchronize(st));
+        if (M_out) KM_CK(cudaMemcpy(M_out, M, k * sizeof(int32_t), cudaMemcpyDeviceToHost));
+        copy_td(td_out);
+        return KM_OK;
+    }
+
+    // ---- state ---------------------------------------------------------------
+    km_status get_state(int32_t* Mo, int32_t* asg, void* td_out, int32_t* it, int32_t* sw) override {
+        KM_CK(cudaStreamSynchronize(st));
+        if (Mo) KM_CK(cudaMemcpy(Mo, M, k * sizeof(int32_t), cudaMemcpyDeviceToHost));
+        if (asg) KM_CK(cudaMemcpy(asg, near, n * sizeof(int32_t), cudaMemcpyDeviceToHost));
+        copy_td(td_out);
+        KM_CK(cudaMemcpy(h_dec, dec, sizeof(Dec), cudaMemcpyDeviceToHost));
+        if (it) *it = h_dec->iters;
+        if (sw) *sw = h_dec->swaps;
+        return KM_OK;
+    }
+
+    km_status get_cache(int32_t* nr, int32_t* sc, void* dno, void* dso) override {
+        KM_CK(cudaStreamSynchronize(st));
+        if (nr) KM_CK(cudaMemcpy(nr, near, n * sizeof(int32_t), cudaMemcpyDeviceToHost));
+        if (sc) KM_CK(cudaMemcpy(sc, sec, n * sizeof(int32_t), cudaMemcpyDeviceToHost));
+        if (dno) KM_CK(cudaMemcpy(dno, dn, n * sizeof(T), cudaMemcpyDeviceToHost));
+        if (dso) KM_CK(cudaMemcpy(dso, ds, n * sizeof(T), cudaMemcpyDeviceToHost));
+        return KM_OK;
+    }
+
+    km_status eval_candidates(void* vo, int32_t* so) override {
+        if (!ready) return fail(KM_EINVAL, "no medoids set");
+        KM_TRY(eval_local());
+        KM_CK(cudaStreamSynchronize(st));
+        if (vo) KM_CK(cudaMemcpy(vo, cand_v, (size_t)w * sizeof(A), cudaMemcpyDeviceToHost));
+        if (so) KM_CK(cudaMemcpy(so, cand_slot, (size_t)w * sizeof(int32_t), cudaMemcpyDeviceToHost));
+        pending_prof = false;
+        return KM_OK;
+    }
+
+    // ---- sharded phases --------------------------------------------------------
+    km_status shard_exchange(int32_t nr, km_exchange* out) override {
+        if (nr < 1) return fail(KM_EINVAL, "nranks must be >= 1");
+        if (!rec_recv || nr != nranks) {
+            nranks = nr;
+            KM_TRY(alloc(&rec_recv, nr));
+        }
+        out->record_send = rec_local;
+        out->record_recv = rec_recv;
+        out->record_bytes = sizeof(Rec);
+        out->column = colbuf;
+        out->column_bytes = (size_t)n * sizeof(T);
+        return KM_OK;
+    }
+
+    km_status shard_set_medoids(const int32_t* Mh, const void* cols) override {
+        if (k < 2) return fail(KM_EINVAL, "SWAP needs k >= 2");
+        KM_TRY(set_point_slots(Mh));
+        KM_CK(cudaMemcpyAsync(MC, cols, (size_t)k * n * sizeof(T), cudaMemcpyDeviceToDevice, st));
+        KM_TRY(assign_full_and_td());
+        KM_TRY(reset_counters());
+        KM_CK(cudaStreamSynchronize(st));
+        ready = true;
+        return KM_OK;
+    }
+
+    km_status shard_eval() override {
+        if (!ready) return fail(KM_EINVAL, "no medoids set");
+        return eval_local();
+    }
+
+    static int owner_of(const int64_t* rcb, int nr, int64_t c) {
+        for (int r = 0; r < nr; ++r)
+            if (c >= rcb[r] && c < rcb[r + 1]) return r;
+        return -1;
+    }
+
+    km_status shard_select(const int64_t* rcb, int32_t* found, int32_t* slot, int32_t* cand, int32_t* owner,
+                           void* dtd) override {
+        if (!rec_recv) return fail(KM_ECOMM, "call kmedoids_shard_exchange first");
+        km::k_select<A><<<1, 1, 0, st>>>(rec_recv, nranks, td, M, point_slot, dec);
+        KM_CKL();
+        KM_TRY(sync_dec());
+        if (found) *found = h_dec->apply;
+        if (slot) *slot = h_dec->slot;
+        if (cand) *cand = h_dec->c;
+        if (owner) *owner = h_dec->apply ? owner_of(rcb, nranks, h_dec->c) : -1;
+        if (dtd) memcpy(dtd, &h_dec->dtd, sizeof(A));
+        return h_dec->apply ? KM_OK : KM_CONVERGED;
+    }
+
+    km_status shard_pack_column(int32_t cand) override {
+        if (cand < c0 || cand >= c1) return fail(KM_ECOMM, "candidate %d is not in this rank's columns", cand);
+        const int nb = (int)cdiv(n, 256);
+        km::k_gather_decided_col<T, A><<<nb, 256, 0, st>>>(D, ld, (int)n, c0, c1, dec, nullptr, colbuf);
+        KM_CKL();
+        KM_CK(cudaStreamSynchronize(st));
+        return KM_OK;
+    }
+
+    km_status shard_apply() override {
+        const int nb = (int)cdiv(n, 256);
+        km::k_column_to_mc<T, A><<<nb, 256, 0, st>>>(colbuf, (int)n, dec, MC);
+        KM_CKL();
+        km::k_assign_incremental<T, A><<<nb, 256, 0, st>>>(MC, (int)n, k, dec, near, sec, dn, ds);
+        KM_CKL();
+        KM_CK(cudaStreamSynchronize(st));
+        return KM_OK;
+    }
+
+    int build_step = 0;
+    km_status build_select(const int64_t* rcb, int32_t* cand, int32_t* owner, void* gain) override {
+        if (!rec_recv) return fail(KM_ECOMM, "call kmedoids_shard_exchange first");
+        if (build_step == 0) {
+            KM_CK(cudaMemsetAsync(point_slot, 0xff, n * sizeof(int), st));
+            ready = false;
+        }
+        km::k_build_select<A><<<1, 1, 0, st>>>(rec_recv, nranks, build_step, td, M, point_slot, dec);
+        KM_CKL();
+        KM_TRY(sync_dec());
+        if (cand) *cand = h_dec->c;
+        if (owner) *owner = owner_of(rcb, nranks, h_dec->c);
+        if (gain) memcpy(gain, &h_dec->dtd, sizeof(A));
+        return KM_OK;
+    }
+
+    km_status build_apply(int32_t step) override {
+        const int nb = (int)cdiv(n, 256);
+        km::k_column_to_mc<T, A><<<nb, 256, 0, st>>>(colbuf, (int)n, dec, MC);
+        KM_CKL();
+        km::k_build_dn<T, A><<<nb, 256, 0, st>>>(MC, (int)n, dec, point_slot, dn);
+        KM_CKL();
+        build_step = step + 1;
+        if (step == k - 1) {
+            KM_TRY(build_finish());
+            build_step = 0;
+        }
+        KM_CK(cudaStreamSynchronize(st));
+        return KM_OK;
+    }
+};
+
+}  // namespace
+
+// ============================================================================
+// C ABI
+// ============================================================================
+extern "C" {
+
+const char* kmedoids_last_error(void) { return g_err.c_str(); }
+
+km_status kmedoids_create(km_handle** out, const void* D, km_dtype dtype, int64_t n, int64_t ld, int64_t col_begin,
+                          int64_t col_end, int32_t k, void* cuda_stream) {
+    g_err.clear();
+    if (!out) return fail(KM_EINVAL, "out is NULL");
+    *out = nullptr;
+    if (!D) return fail(KM_EINVAL, "D is NULL");
+    if (dtype != KM_U32 && dtype != KM_F32) return fail(KM_EINVAL, "unknown dtype %d", (int)dtype);
+    if (n < 3 || n >= (int64_t)INT32_MAX) return fail(KM_EINVAL, "n=%lld out of range [3, 2^31)", (long long)n);
+    if (k < 1 || k >= n) return fail(KM_EINVAL, "k=%d must satisfy 1 <= k < n", k);
+    if (k > MAX_K) return fail(KM_EINVAL, "k=%d exceeds the supported maximum %d", k, MAX_K);
+    if (col_begin < 0 || col_end > n || col_begin >= col_end)
+        return fail(KM_EINVAL, "column range [%lld,%lld) invalid for n=%lld", (long long)col_begin,
+                    (long long)col_end, (long long)n);
+    if (ld < col_end - col_begin || ld % 4 != 0)
+        return fail(KM_EINVAL, "ld=%lld must be >= the slab width and a multiple of 4", (long long)ld);
+    if (((uintptr_t)D) % 16 != 0) return fail(KM_EINVAL, "D must be 16-byte aligned");
+    std::unique_ptr<km_handle> h(new km_handle());
+    km_status s;
+    if (dtype == KM_U32) {
+        auto* im = new Impl<uint32_t>();
+        h->impl.reset(im);
+        s = im->init(D, n, ld, col_begin, col_end, k, (cudaStream_t)cuda_stream);
+    } else {
+        auto* im = new Impl<float>();
+        h->impl.reset(im);
+        s = im->init(D, n, ld, col_begin, col_end, k, (cudaStream_t)cuda_stream);
+    }
+    if (s != KM_OK) return s;
+    *out = h.release();
+    return KM_OK;
+}
+
+km_status kmedoids_destroy(km_handle* h) {
+    delete h;
+    return KM_OK;
+}
+
+#define KM_H()                                                  \
+    do {                                                        \
+        g_err.clear();                                          \
+        if (!h || !h->impl) return fail(KM_EINVAL, "null handle"); \
+    } while (0)
+
+km_status kmedoids_set_medoids(km_handle* h, const int32_t* medoids) {
+    KM_H();
+    if (!medoids) return fail(KM_EINVAL, "medoids is NULL");
+    return h->impl->set_medoids(medoids);
+}
+
+km_status kmedoids_init_build(km_handle* h, int32_t* medoids_out, void* td_out) {
+    KM_H();
+    return h->impl->init_build(medoids_out, td_out);
+}
+
+km_status kmedoids_swap_iter(km_handle* h, km_variant variant, int32_t* swaps_done_out, void* td_out) {
+    KM_H();
+    return h->impl->swap_iter(variant, swaps_done_out, td_out);
+}
+
+km_status kmedoids_run(km_handle* h, int32_t use_build, km_variant variant, int32_t max_iter, int32_t* medoids_out,
+                       int32_t* assignment_out, void* td_out, int32_t* n_iter_out, int32_t* n_swaps_out) {
+    KM_H();
+    if (h->impl->sharded) return fail(KM_EINVAL, "kmedoids_run on a sharded handle; drive the shard phases");
+    if (max_iter <= 0) max_iter = 2000;
+    if (use_build) KM_TRY(h->impl->init_build(nullptr, nullptr));
+    km_status st = KM_NOT_CONVERGED;
+    for (int it = 0; it < max_iter; ++it) {
+        km_status s = h->impl->swap_iter(variant, nullptr, nullptr);
+        if (s == KM_CONVERGED) { st = KM_OK; break; }
+        if (s != KM_OK) return s;
+    }
+    KM_TRY(h->impl->get_state(medoids_out, assignment_out, td_out, n_iter_out, n_swaps_out));
+    return st;
+}
+
+km_status kmedoids_run_host(const void* D_host, km_dtype dtype, int64_t n, int64_t ld, int32_t k, int32_t use_build,
+                            const int32_t* initial_medoids, km_variant variant, int32_t max_iter, void* cuda_stream,
+                            int32_t* medoids_out, int32_t* assignment_out, void* td_out, int32_t* n_iter_out,
+                            int32_t* n_swaps_out) {
+    g_err.clear();
+    if (!D_host) return fail(KM_EINVAL, "D_host is NULL");
+    if (!use_build && !initial_medoids) return fail(KM_EINVAL, "initial_medoids required without BUILD");
+    if (n < 3 || ld < n) return fail(KM_EINVAL, "bad n/ld");
+    const size_t bytes = (size_t)n * (size_t)ld * 4;
+    void* Dd = nullptr;
+    cudaError_t e = cudaMalloc(&Dd, bytes);
+    if (e != cudaSuccess) return fail(KM_ENOMEM, "cudaMalloc(%zu) for D failed: %s", bytes, cudaGetErrorString(e));
+    cudaStream_t st = (cudaStream_t)cuda_stream;
+    km_status s = KM_OK;
+    km_handle* h = nullptr;
+    e = cudaMemcpyAsync(Dd, D_host, bytes, cudaMemcpyHostToDevice, st);
+    if (e != cudaSuccess) s = fail(KM_ECUDA, "H2D copy of D failed: %s", cudaGetErrorString(e));
+    if (s == KM_OK) s = kmedoids_create(&h, Dd, dtype, n, ld, 0, n, k, cuda_stream);
+    if (s == KM_OK && !use_build) s = kmedoids_set_medoids(h, initial_medoids);
+    if (s == KM_OK) {
+        km_status r = kmedoids_run(h, use_build, variant, max_iter, medoids_out, assignment_out, td_out, n_iter_out,
+                                   n_swaps_out);
+        s = r;
+    }
+    kmedoids_destroy(h);
+    cudaStreamSynchronize(st);
+    cudaFree(Dd);
+    return s;
+}
+
+km_status kmedoids_get_state(km_handle* h, int32_t* medoids_out, int32_t* assignment_out, void* td_out,
+                             int32_t* n_iter_out, int32_t* n_swaps_out) {
+    KM_H();
+    return h->impl->get_state(medoids_out, assignment_out, td_out, n_iter_out, n_swaps_out);
+}
+
+km_status kmedoids_get_cache(km_handle* h, int32_t* nearest_out, int32_t* second_out, void* dn_out, void* ds_out) {
+    KM_H();
+    return h->impl->get_cache(nearest_out, second_out, dn_out, ds_out);
+}
+
+km_status kmedoids_eval_candidates(km_handle* h, void* dtd_out, int32_t* slot_out) {
+    KM_H();
+    return h->impl->eval_candidates(dtd_out, slot_out);
+}
+
+km_status kmedoids_set_profiling(km_handle* h, int32_t enable) {
+    KM_H();
+    h->impl->profiling = enable != 0;
+    return KM_OK;
+}
+
+km_status kmedoids_stream_time(km_handle* h, double* ms_out, int64_t* launches_out, int32_t reset) {
+    KM_H();
+    if (ms_out) *ms_out = h->impl->prof_ms;
+    if (launches_out) *launches_out = h->impl->prof_launches;
+    if (reset) { h->impl->prof_ms = 0.0; h->impl->prof_launches = 0; }
+    return KM_OK;
+}
+
+km_status kmedoids_launch_count(km_handle* h, int64_t* count_out) {
+    KM_H();
+    if (count_out) *count_out = h->impl->launches;
+    return KM_OK;
+}
+
+km_status kmedoids_shard_exchange(km_handle* h, int32_t nranks, km_exchange* out) {
+    KM_H();
+    if (!out) return fail(KM_EINVAL, "out is NULL");
+    return h->impl->shard_exchange(nranks, out);
+}
+
+km_status kmedoids_shard_set_medoids(km_handle* h, const int32_t* medoids, const void* columns_dev) {
+    KM_H();
+    if (!medoids || !columns_dev) return fail(KM_EINVAL, "NULL argument");
+    return h->impl->shard_set_medoids(medoids, columns_dev);
+}
+
+km_status kmedoids_shard_eval(km_handle* h) {
+    KM_H();
+    return h->impl->shard_eval();
+}
+
+km_status kmedoids_shard_select(km_handle* h, const int64_t* rank_col_begin, int32_t* found, int32_t* slot,
+                                int32_t* cand, int32_t* owner, void* dtd) {
+    KM_H();
+    if (!rank_col_begin) return fail(KM_EINVAL, "rank_col_begin is NULL");
+    return h->impl->shard_select(rank_col_begin, found, slot, cand, owner, dtd);
+}
+
+km_status kmedoids_shard_pack_column(km_handle* h, int32_t cand) {
+    KM_H();
+    return h->impl->shard_pack_column(cand);
+}
+
+km_status kmedoids_shard_apply(km_handle* h) {
+    KM_H();
+    return h->impl->shard_apply();
+}
+
+km_status kmedoids_build_eval(km_handle* h, int32_t step) {
+    KM_H();
+    return h->impl->build_eval(step);
+}
+
+km_status kmedoids_build_select(km_handle* h, const int64_t* rank_col_begin, int32_t* cand, int32_t* owner,
+                                void* gain) {
+    KM_H();
+    if (!rank_col_begin) return fail(KM_EINVAL, "rank_col_begin is NULL");
+    return h->impl->build_select(rank_col_begin, cand, owner, gain);
+}
+
+km_status kmedoids_build_apply(km_handle* h, int32_t step) {
+    KM_H();
+    return h->impl->build_apply(step);
+}
+
+}  // extern "C"

@@ -1,0 +1,327 @@
+"""Thin Python binding of libkmedoids.so (include/kmedoids.h).
+
+Argument marshalling only: every step of BUILD / SWAP runs in the library's
+sm_100a kernels.  There is no CPU fallback -- importing this module on a
+machine without the built library raises, and every call checks the status
+code the C ABI returns.
+
+Function names follow the C ABI (``kmedoids_create``, ``kmedoids_init_build``,
+``kmedoids_swap_iter``, ``kmedoids_run``, ...).  ``KMedoids`` wraps a handle
+for convenience.  Device buffers are torch CUDA tensors (PyTorch supplies
+device memory and streams only).
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+from dataclasses import dataclass
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libkmedoids.so")
+
+KM_OK, KM_CONVERGED, KM_NOT_CONVERGED = 0, 1, 2
+KM_EINVAL, KM_ENOMEM, KM_ECUDA, KM_ECOMM = 10, 11, 12, 13
+KM_U32, KM_F32 = 0, 1
+KM_FASTPAM1, KM_FASTPAM2 = 0, 1
+VARIANTS = {"fastpam1": KM_FASTPAM1, "fastpam2": KM_FASTPAM2}
+
+
+class KMError(RuntimeError):
+    def __init__(self, status: int, msg: str):
+        super().__init__(f"kmedoids status {status}: {msg}")
+        self.status = status
+
+
+class _Exchange(ctypes.Structure):
+    _fields_ = [("record_send", ctypes.c_void_p), ("record_recv", ctypes.c_void_p),
+                ("record_bytes", ctypes.c_size_t), ("column", ctypes.c_void_p),
+                ("column_bytes", ctypes.c_size_t)]
+
+
+_lib = None
+
+
+def load_library() -> ctypes.CDLL:
+    """Load libkmedoids.so; raises if it has not been built (no fallback)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(LIB_PATH):
+        raise ImportError(f"{LIB_PATH} is missing: run __graft_entry__.build() (nvcc, sm_100a)")
+    lib = ctypes.CDLL(LIB_PATH)
+    vp, i32, i64 = ctypes.c_void_p, ctypes.c_int32, ctypes.c_int64
+    sig = {
+        "kmedoids_create": [ctypes.POINTER(vp), vp, ctypes.c_int, i64, i64, i64, i64, i32, vp],
+        "kmedoids_destroy": [vp],
+        "kmedoids_set_medoids": [vp, vp],
+        "kmedoids_init_build": [vp, vp, vp],
+        "kmedoids_swap_iter": [vp, ctypes.c_int, vp, vp],
+        "kmedoids_run": [vp, i32, ctypes.c_int, i32, vp, vp, vp, vp, vp],
+        "kmedoids_run_host": [vp, ctypes.c_int, i64, i64, i32, i32, vp, ctypes.c_int, i32, vp, vp, vp, vp, vp, vp],
+        "kmedoids_get_state": [vp, vp, vp, vp, vp, vp],
+        "kmedoids_get_cache": [vp, vp, vp, vp, vp],
+        "kmedoids_eval_candidates": [vp, vp, vp],
+        "kmedoids_set_profiling": [vp, i32],
+        "kmedoids_stream_time": [vp, vp, vp, i32],
+        "kmedoids_launch_count": [vp, vp],
+        "kmedoids_shard_exchange": [vp, i32, ctypes.POINTER(_Exchange)],
+        "kmedoids_shard_set_medoids": [vp, vp, vp],
+        "kmedoids_shard_eval": [vp],
+        "kmedoids_shard_select": [vp, vp, vp, vp, vp, vp, vp],
+        "kmedoids_shard_pack_column": [vp, i32],
+        "kmedoids_shard_apply": [vp],
+        "kmedoids_build_eval": [vp, i32],
+        "kmedoids_build_select": [vp, vp, vp, vp, vp],
+        "kmedoids_build_apply": [vp, i32],
+    }
+    for name, args in sig.items():
+        f = getattr(lib, name)
+        f.argtypes = args
+        f.restype = ctypes.c_int
+    lib.kmedoids_last_error.restype = ctypes.c_char_p
+    lib.kmedoids_last_error.argtypes = []
+    _lib = lib
+    return lib
+
+
+def _check(status: int, ok=(KM_OK,)) -> int:
+    if status not in ok:
+        raise KMError(status, load_library().kmedoids_last_error().decode())
+    return status
+
+
+def _p(a: np.ndarray):
+    return ctypes.c_void_p(a.ctypes.data)
+
+
+def _dtype_code(t) -> int:
+    import torch
+    if t.dtype in (torch.int32, getattr(torch, "uint32", torch.int32)):
+        return KM_U32
+    if t.dtype == torch.float32:
+        return KM_F32
+    raise TypeError(f"D must be int32/uint32 (u32 bits) or float32, got {t.dtype}")
+
+
+@dataclass
+class Result:
+    medoids: np.ndarray
+    assignment: np.ndarray
+    td: int | float
+    n_iter: int
+    n_swaps: int
+    converged: bool
+
+
+class KMedoids:
+    """A handle over a borrowed device slab D (see include/kmedoids.h)."""
+
+    def __init__(self, D, n: int, k: int, col_begin: int = 0, col_end: int | None = None, stream=None):
+        import torch
+        lib = load_library()
+        if not D.is_cuda:
+            raise ValueError("D must be a CUDA tensor (use kmedoids_run_host for host data)")
+        if D.dim() != 2 or D.stride(1) != 1:
+            raise ValueError("D must be a 2-D row-major tensor")
+        self.D = D                       # keep the borrowed slab alive
+        self.n, self.k = int(n), int(k)
+        self.col_begin = int(col_begin)
+        self.col_end = int(n if col_end is None else col_end)
+        self.dtype = _dtype_code(D)
+        self.acc = np.int64 if self.dtype == KM_U32 else np.float64
+        self.stream = stream if stream is not None else torch.cuda.current_stream(D.device)
+        h = ctypes.c_void_p()
+        _check(lib.kmedoids_create(ctypes.byref(h), ctypes.c_void_p(D.data_ptr()), self.dtype, self.n,
+                                   int(D.stride(0)), self.col_begin, self.col_end, self.k,
+                                   ctypes.c_void_p(self.stream.cuda_stream)))
+        self.h = h
+
+    def close(self):
+        if getattr(self, "h", None):
+            load_library().kmedoids_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *a):
+        self.close()
+
+    # ---- single-GPU API -------------------------------------------------------
+    def set_medoids(self, medoids):
+        M = np.ascontiguousarray(np.asarray(medoids, dtype=np.int32))
+        if M.shape != (self.k,):
+            raise ValueError(f"expected {self.k} medoids")
+        _check(load_library().kmedoids_set_medoids(self.h, _p(M)))
+
+    def init_build(self):
+        M = np.zeros(self.k, np.int32)
+        td = np.zeros(1, self.acc)
+        _check(load_library().kmedoids_init_build(self.h, _p(M), _p(td)))
+        return M, td[0].item()
+
+    def swap_iter(self, variant="fastpam1"):
+        sw = np.zeros(1, np.int32)
+        td = np.zeros(1, self.acc)
+        s = _check(load_library().kmedoids_swap_iter(self.h, VARIANTS[variant], _p(sw), _p(td)),
+                   ok=(KM_OK, KM_CONVERGED))
+        return s == KM_CONVERGED, int(sw[0]), td[0].item()
+
+    def run(self, use_build=True, variant="fastpam1", max_iter=2000) -> Result:
+        M = np.zeros(self.k, np.int32)
+        asg = np.zeros(self.n, np.int32)
+        td = np.zeros(1, self.acc)
+        it = np.zeros(1, np.int32)
+        sw = np.zeros(1, np.int32)
+        s = _check(load_library().kmedoids_run(self.h, int(use_build), VARIANTS[variant], int(max_iter), _p(M),
+                                               _p(asg), _p(td), _p(it), _p(sw)), ok=(KM_OK, KM_NOT_CONVERGED))
+        return Result(M, asg, td[0].item(), int(it[0]), int(sw[0]), s == KM_OK)
+
+    def get_state(self) -> Result:
+        M = np.zeros(self.k, np.int32)
+        asg = np.zeros(self.n, np.int32)
+        td = np.zeros(1, self.acc)
+        it = np.zeros(1, np.int32)
+        sw = np.zeros(1, np.int32)
+        _check(load_library().kmedoids_get_state(self.h, _p(M), _p(asg), _p(td), _p(it), _p(sw)))
+        return Result(M, asg, td[0].item(), int(it[0]), int(sw[0]), True)
+
+    def get_cache(self):
+        dt = np.uint32 if self.dtype == KM_U32 else np.float32
+        near = np.zeros(self.n, np.int32); sec = np.zeros(self.n, np.int32)
+        dn = np.zeros(self.n, dt); ds = np.zeros(self.n, dt)
+        _check(load_library().kmedoids_get_cache(self.h, _p(near), _p(sec), _p(dn), _p(ds)))
+        return near, sec, dn, ds
+
+    def eval_candidates(self):
+        w = self.col_end - self.col_begin
+        v = np.zeros(w, self.acc); s = np.zeros(w, np.int32)
+        _check(load_library().kmedoids_eval_candidates(self.h, _p(v), _p(s)))
+        return v, s
+
+    def set_profiling(self, on=True):
+        _check(load_library().kmedoids_set_profiling(self.h, int(on)))
+
+    def stream_time(self, reset=False):
+        ms = ctypes.c_double(); cnt = ctypes.c_int64()
+        _check(load_library().kmedoids_stream_time(self.h, ctypes.byref(ms), ctypes.byref(cnt), int(reset)))
+        return ms.value, cnt.value
+
+    def launch_count(self) -> int:
+        c = ctypes.c_int64()
+        _check(load_library().kmedoids_launch_count(self.h, ctypes.byref(c)))
+        return c.value
+
+    # ---- sharded phase API ------------------------------------------------------
+    def shard_exchange(self, nranks: int) -> _Exchange:
+        x = _Exchange()
+        _check(load_library().kmedoids_shard_exchange(self.h, int(nranks), ctypes.byref(x)))
+        return x
+
+    def shard_set_medoids(self, medoids, columns):
+        M = np.ascontiguousarray(np.asarray(medoids, dtype=np.int32))
+        _check(load_library().kmedoids_shard_set_medoids(self.h, _p(M), ctypes.c_void_p(columns.data_ptr())))
+
+    def shard_eval(self):
+        _check(load_library().kmedoids_shard_eval(self.h))
+
+    def shard_select(self, rank_col_begin):
+        rcb = np.ascontiguousarray(np.asarray(rank_col_begin, dtype=np.int64))
+        f = np.zeros(1, np.int32); sl = np.zeros(1, np.int32); c = np.zeros(1, np.int32)
+        ow = np.zeros(1, np.int32); d = np.zeros(1, self.acc)
+        _check(load_library().kmedoids_shard_select(self.h, _p(rcb), _p(f), _p(sl), _p(c), _p(ow), _p(d)),
+               ok=(KM_OK, KM_CONVERGED))
+        return bool(f[0]), int(sl[0]), int(c[0]), int(ow[0]), d[0].item()
+
+    def shard_pack_column(self, cand: int):
+        _check(load_library().kmedoids_shard_pack_column(self.h, int(cand)))
+
+    def shard_apply(self):
+        _check(load_library().kmedoids_shard_apply(self.h))
+
+    def build_eval(self, step: int):
+        _check(load_library().kmedoids_build_eval(self.h, int(step)))
+
+    def build_select(self, rank_col_begin):
+        rcb = np.ascontiguousarray(np.asarray(rank_col_begin, dtype=np.int64))
+        c = np.zeros(1, np.int32); ow = np.zeros(1, np.int32); g = np.zeros(1, self.acc)
+        _check(load_library().kmedoids_build_select(self.h, _p(rcb), _p(c), _p(ow), _p(g)))
+        return int(c[0]), int(ow[0]), g[0].item()
+
+    def build_apply(self, step: int):
+        _check(load_library().kmedoids_build_apply(self.h, int(step)))
+
+
+# ---- C-ABI-named module functions ----------------------------------------------
+def kmedoids_create(D, n, k, col_begin=0, col_end=None, stream=None) -> KMedoids:
+    return KMedoids(D, n, k, col_begin, col_end, stream)
+
+
+def kmedoids_destroy(h: KMedoids):
+    h.close()
+
+
+def kmedoids_set_medoids(h: KMedoids, medoids):
+    h.set_medoids(medoids)
+
+
+def kmedoids_init_build(h: KMedoids):
+    return h.init_build()
+
+
+def kmedoids_swap_iter(h: KMedoids, variant="fastpam1"):
+    return h.swap_iter(variant)
+
+
+def kmedoids_run(h: KMedoids, use_build=True, variant="fastpam1", max_iter=2000) -> Result:
+    return h.run(use_build, variant, max_iter)
+
+
+def kmedoids_run_host(D_host: np.ndarray, k: int, use_build=True, medoids=None, variant="fastpam1",
+                      max_iter=2000, stream=None) -> Result:
+    """Whole job from host memory (H2D of D, BUILD/SWAP, D2H of the result).
+
+    D_host: (n, ld) uint32 or float32 numpy array (pin it for full PCIe speed,
+    e.g. with ``pinned_empty``)."""
+    import torch
+    lib = load_library()
+    if D_host.dtype == np.uint32 or D_host.dtype == np.int32:
+        dt, acc = KM_U32, np.int64
+    elif D_host.dtype == np.float32:
+        dt, acc = KM_F32, np.float64
+    else:
+        raise TypeError(D_host.dtype)
+    if not D_host.flags.c_contiguous:
+        raise ValueError("D_host must be C-contiguous (n, ld)")
+    n, ld = D_host.shape
+    M = np.zeros(k, np.int32)
+    asg = np.zeros(n, np.int32)
+    td = np.zeros(1, acc)
+    it = np.zeros(1, np.int32)
+    sw = np.zeros(1, np.int32)
+    init = np.ascontiguousarray(np.asarray(medoids, np.int32)) if medoids is not None else None
+    st = stream if stream is not None else torch.cuda.current_stream()
+    s = _check(lib.kmedoids_run_host(_p(D_host), dt, n, ld, int(k), int(use_build),
+                                     _p(init) if init is not None else None, VARIANTS[variant], int(max_iter),
+                                     ctypes.c_void_p(st.cuda_stream), _p(M), _p(asg), _p(td), _p(it), _p(sw)),
+               ok=(KM_OK, KM_NOT_CONVERGED))
+    return Result(M, asg, td[0].item(), int(it[0]), int(sw[0]), s == KM_OK)
+
+
+def pinned_empty(shape, dtype):
+    """Page-locked host numpy array (via torch's pinned allocator)."""
+    import torch
+    tdt = {np.dtype(np.uint32): torch.int32, np.dtype(np.int32): torch.int32,
+           np.dtype(np.float32): torch.float32}[np.dtype(dtype)]
+    t = torch.empty(shape, dtype=tdt, pin_memory=True)
+    a = t.numpy()
+    a = a.view(np.uint32) if np.dtype(dtype) == np.uint32 else a
+    return a, t

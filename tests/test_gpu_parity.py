@@ -1,0 +1,283 @@
+"""Parity of the CUDA path (through the C ABI) with the CPU oracle.
+
+Bar (BASELINE.json north_star): uint32 dissimilarities bit-exact (medoids,
+assignment, swap sequence, int64 TD); float32 TD within relative 1e-5 and
+identical medoids wherever the best and second-best dTD differ by more than
+that tolerance (lockstep protocol, reading R8).
+"""
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+import kmsynth  # noqa: E402
+import oracle  # noqa: E402
+
+FTOL = 1e-5
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _cuda():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    torch.cuda.set_device(0)
+
+
+def KM(*a, **kw):
+    from paper_2008_05171_b200 import KMedoids
+    return KMedoids(*a, **kw)
+
+
+def to_dev(D: np.ndarray, ld=None):
+    """(n, n) numpy -> padded (n, ld) CUDA tensor (uint32 carried as int32 bits)."""
+    n = D.shape[0]
+    ld = ld or kmsynth.round_ld(n)
+    buf = np.zeros((n, ld), D.dtype)
+    buf[:, :n] = D
+    t = torch.from_numpy(buf.view(np.int32) if D.dtype == np.uint32 else buf).cuda()
+    return t
+
+
+def rand_int(rng, n, hi, symmetric=True):
+    A = rng.integers(0, hi, size=(n, n)).astype(np.uint32)
+    if symmetric:
+        A = np.triu(A, 1)
+        A = A + A.T
+    np.fill_diagonal(A, 0)
+    return A
+
+
+def gpu_trace(km, k, variant="fastpam1", max_iter=2000):
+    """Step the GPU one SWAP iteration at a time; return the swap trace."""
+    trace = []
+    prev = km.get_state().medoids.copy()
+    for _ in range(max_iter):
+        conv, swaps, td = km.swap_iter(variant)
+        cur = km.get_state().medoids
+        changed = [i for i in range(k) if cur[i] != prev[i]]
+        trace.append((changed, [int(cur[i]) for i in changed], td))
+        prev = cur.copy()
+        if conv:
+            break
+    return trace
+
+
+# ---------------- input generator: GPU == numpy, bit for bit ----------------
+
+@pytest.mark.parametrize("cid,n,c0,c1", [(1, 500, 0, 500), (2, 700, 0, 700), (3, 333, 0, 333),
+                                         (5, 257, 0, 257), (4, 301, 100, 251), (5, 129, 64, 129)])
+def test_synth_cuda_matches_numpy(cid, n, c0, c1):
+    cfg = kmsynth.CONFIGS[cid]
+    X = kmsynth.make_points(cfg, n=n)
+    a = kmsynth.as_numpy_D(kmsynth.dist_cuda(X, cfg.metric, c0, c1))
+    b = kmsynth.dist_numpy(X, cfg.metric, c0, c1)
+    assert a.shape == b.shape and a.tobytes() == b.tobytes()
+    if c0 == 0 and c1 == n:
+        S = a[:, :n]
+        assert (S == S.T).all() and (np.diag(S) == 0).all()
+
+
+# ---------------- integer path: bit-exact ----------------
+
+def test_c1_build_fastpam1_bit_exact():
+    cfg = kmsynth.CONFIGS[1]
+    X = kmsynth.make_points(cfg)
+    Dt = kmsynth.dist_cuda(X, cfg.metric)
+    D = kmsynth.as_numpy_D(Dt)[:, :cfg.n]
+    Mb, tdb, _ = oracle.build_init(D, cfg.k)
+    ref = oracle.swap_run(D, Mb, oracle.FASTPAM1)
+    km = KM(Dt, cfg.n, cfg.k)
+    Mg, tdg = km.init_build()
+    assert Mg.tolist() == Mb.tolist() and tdg == tdb
+    near, sec, dn, ds = km.get_cache()
+    c = oracle.assign(D, Mb)
+    assert near.tolist() == c.nearest.tolist() and sec.tolist() == c.second.tolist()
+    assert dn.tolist() == c.dn.tolist() and ds.tolist() == c.ds.tolist()
+    tr = gpu_trace(km, cfg.k)
+    got = [(ch[0], cs[0]) for ch, cs, _ in tr if ch]
+    assert got == [(i, c) for i, c, _ in ref.trace]
+    st = km.get_state()
+    assert st.medoids.tolist() == ref.medoids.tolist()
+    assert st.assignment.tolist() == ref.assignment.tolist()
+    assert st.td == ref.td and st.n_iter == ref.n_iter and st.n_swaps == ref.n_swaps
+
+
+@pytest.mark.parametrize("seed", range(12))
+def test_random_int_instances_trace_exact(seed):
+    rng = np.random.default_rng(1000 + seed)
+    n = int(rng.choice([7, 37, 130, 257, 600, 1031]))
+    k = int(rng.integers(2, min(12, n - 1) + 1))
+    hi = int(rng.choice([3, 50, 100000]))          # hi=3: massive ties
+    D = rand_int(rng, n, hi, symmetric=bool(seed % 3))
+    M0 = rng.choice(n, size=k, replace=False).astype(np.int32)
+    ref = oracle.swap_run(D, M0, oracle.FASTPAM1)
+    km = KM(to_dev(D), n, k)
+    km.set_medoids(M0)
+    tr = gpu_trace(km, k)
+    got = [(ch[0], cs[0]) for ch, cs, _ in tr if ch]
+    assert got == [(i, c) for i, c, _ in ref.trace]
+    st = km.get_state()
+    assert st.medoids.tolist() == ref.medoids.tolist()
+    assert st.assignment.tolist() == ref.assignment.tolist()
+    assert st.td == ref.td and st.n_iter == ref.n_iter and st.n_swaps == ref.n_swaps
+    # cache after convergence equals a from-scratch assignment
+    near, sec, dn, ds = km.get_cache()
+    c = oracle.assign(D, ref.medoids)
+    assert near.tolist() == c.nearest.tolist() and sec.tolist() == c.second.tolist()
+    assert dn.tolist() == c.dn.tolist() and ds.tolist() == c.ds.tolist()
+
+
+@pytest.mark.parametrize("seed", range(6))
+def test_per_candidate_values_exact(seed):
+    rng = np.random.default_rng(77 + seed)
+    n = int(rng.choice([64, 513, 2000]))
+    k = int(rng.integers(2, 40))
+    D = rand_int(rng, n, int(rng.choice([10, 1000])))
+    M0 = rng.choice(n, size=k, replace=False)
+    km = KM(to_dev(D), n, k)
+    km.set_medoids(M0)
+    v, s = km.eval_candidates()
+    c = oracle.assign(D, M0)
+    R = oracle.removal_loss(c, k)
+    for x in range(n):
+        if x in M0:
+            assert s[x] == -1
+            continue
+        vec, plus = oracle.fastpam1_candidate(D, x, c, R)
+        i = int(np.argmin(vec))                       # smallest slot on ties
+        assert (int(v[x]), int(s[x])) == (int(vec[i] + plus), i)
+
+
+def test_build_int_bit_exact_random():
+    rng = np.random.default_rng(5)
+    for trial in range(6):
+        n = int(rng.choice([9, 100, 777]))
+        k = int(rng.integers(1, min(9, n - 1) + 1))
+        D = rand_int(rng, n, int(rng.choice([4, 1000])), symmetric=bool(trial % 2))
+        Mb, tdb, _ = oracle.build_init(D, k)
+        km = KM(to_dev(D), n, k)
+        Mg, tdg = km.init_build()
+        assert Mg.tolist() == Mb.tolist()
+        if k >= 2:
+            assert tdg == oracle.td(D, Mb)
+        else:
+            assert tdg == tdb
+
+
+def test_edge_cases():
+    # all-zero matrix: nothing improves
+    D = np.zeros((9, 9), np.uint32)
+    km = KM(to_dev(D), 9, 3)
+    km.set_medoids([0, 1, 2])
+    r = km.run(use_build=False)
+    assert r.n_swaps == 0 and r.n_iter == 1 and r.td == 0 and r.converged
+    # duplicated points and k = n - 1
+    x = np.array([0, 0, 5, 5, 9, 9, 14])
+    D = np.abs(x[:, None] - x[None, :]).astype(np.uint32)
+    for k in (2, 6):
+        M0 = list(range(k))
+        ref = oracle.swap_run(D, M0, oracle.FASTPAM1)
+        km = KM(to_dev(D), 7, k)
+        km.set_medoids(M0)
+        r = km.run(use_build=False)
+        assert r.medoids.tolist() == ref.medoids.tolist() and r.td == ref.td
+        assert r.assignment.tolist() == ref.assignment.tolist()
+    # padded rows (ld > n) and an asymmetric matrix
+    rng = np.random.default_rng(3)
+    D = rand_int(rng, 45, 60, symmetric=False)
+    ref = oracle.swap_run(D, [1, 2, 3], oracle.FASTPAM1)
+    km = KM(to_dev(D, ld=64), 45, 3)
+    km.set_medoids([1, 2, 3])
+    r = km.run(use_build=False)
+    assert r.medoids.tolist() == ref.medoids.tolist() and r.td == ref.td
+
+
+def test_invalid_arguments():
+    from paper_2008_05171_b200 import KMError
+    D = to_dev(np.zeros((8, 8), np.uint32))
+    with pytest.raises(KMError):
+        KM(D, 8, 8)                       # k >= n
+    km = KM(D, 8, 3)
+    with pytest.raises(KMError):
+        km.set_medoids([0, 0, 1])         # duplicate
+    with pytest.raises(KMError):
+        km.set_medoids([0, 1, 8])         # out of range
+    with pytest.raises(KMError):
+        km.swap_iter()                    # no medoids yet
+
+
+# ---------------- float path: tolerance + lockstep ----------------
+
+def lockstep_fastpam1(D, Dt, n, k, M0, max_iter=10_000, table=True):
+    """Lockstep protocol (reading R8): at every iteration the GPU's chosen swap
+    must be within FTOL*TD of the oracle's best; the oracle then follows it."""
+    km = KM(Dt, n, k)
+    km.set_medoids(M0)
+    M = np.array(M0, np.int32)
+    iters = 0
+    while iters < max_iter:
+        iters += 1
+        c = oracle.assign(D, M)
+        R = oracle.removal_loss(c, k)
+        td_ref = oracle.td(D, M)
+        bd, bi, bc = oracle.fastpam1_best(D, M, c, R)
+        conv, swaps, td_gpu = km.swap_iter()
+        assert td_gpu == pytest.approx(td_ref + (0 if conv else 0), rel=FTOL) or not conv
+        st = km.get_state()
+        if conv:
+            assert bi < 0 or bd >= -FTOL * abs(td_ref), "GPU converged but the oracle improves"
+            assert st.td == pytest.approx(td_ref, rel=FTOL)
+            return st, iters
+        changed = [i for i in range(k) if st.medoids[i] != M[i]]
+        assert len(changed) == 1
+        gi, gc = changed[0], int(st.medoids[changed[0]])
+        vec, plus = oracle.fastpam1_candidate(D, gc, c, R)
+        assert vec[gi] + plus <= bd + FTOL * abs(td_ref)
+        if (gi, gc) != (bi, bc) and table:
+            # only allowed on a near tie
+            assert abs((vec[gi] + plus) - bd) <= FTOL * abs(td_ref)
+        M[gi] = gc
+        assert td_gpu == pytest.approx(oracle.td(D, M), rel=FTOL)
+    raise AssertionError("no convergence")
+
+
+def test_c2_float_build_and_lockstep():
+    cfg = kmsynth.CONFIGS[2]
+    n = 2000                                  # C2 recipe, oracle-sized prefix
+    X = kmsynth.make_points(cfg, n=n)
+    Dt = kmsynth.dist_cuda(X, cfg.metric)
+    D = kmsynth.as_numpy_D(Dt)[:, :n]
+    Mb, tdb, gains = oracle.build_init(D, cfg.k)
+    km = KM(Dt, n, cfg.k)
+    Mg, tdg = km.init_build()
+    assert tdg == pytest.approx(tdb, rel=FTOL)
+    assert Mg.tolist() == Mb.tolist()        # no near ties in BUILD on this input
+    st, iters = lockstep_fastpam1(D, Dt, n, cfg.k, Mg)
+    ref = oracle.swap_run(D, Mg, oracle.FASTPAM1)
+    assert st.td == pytest.approx(ref.td, rel=FTOL)
+    assert st.medoids.tolist() == ref.medoids.tolist()
+    assert st.assignment.tolist() == ref.assignment.tolist()
+
+
+def test_float_per_candidate_values():
+    rng = np.random.default_rng(8)
+    n, k = 1500, 17
+    X = rng.normal(size=(n, 5))
+    D = kmsynth.dist_numpy(X, kmsynth.L2_F32)[:, :n]
+    M0 = rng.choice(n, size=k, replace=False)
+    km = KM(to_dev(D), n, k)
+    km.set_medoids(M0)
+    v, s = km.eval_candidates()
+    c = oracle.assign(D, M0)
+    R = oracle.removal_loss(c, k)
+    td = oracle.td(D, M0)
+    for x in range(0, n, 7):
+        if x in M0:
+            continue
+        vec, plus = oracle.fastpam1_candidate(D, x, c, R)
+        full = vec + plus
+        assert v[x] == pytest.approx(full.min(), rel=1e-9, abs=1e-9 * td)
+        srt = np.sort(full)
+        if srt[1] - srt[0] > 1e-9 * td:
+            assert s[x] == int(np.argmin(full))
