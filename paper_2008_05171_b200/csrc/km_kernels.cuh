@@ -277,7 +277,7 @@ __global__ void k_scan_counts(const int* __restrict__ counts, int total, int B, 
 template <typename T>
 __global__ void k_slot_scatter(const int* __restrict__ near, const T* __restrict__ dn,
                                const T* __restrict__ ds, int n, int k, const int* __restrict__ offsets,
-                               RowInfo<T>* __restrict__ ri) {
+                               RowInfo<T>* __restrict__ ri, int natural_order) {
     extern __shared__ int cnt[];
     const int B = gridDim.x, b = blockIdx.x, lane = threadIdx.x;
     for (int s = lane; s < k; s += 32) cnt[s] = offsets[(int64_t)s * B + b];
@@ -300,7 +300,7 @@ __global__ void k_slot_scatter(const int* __restrict__ near, const T* __restrict
         if (valid) {
             RowInfo<T> r;
             r.o = e; r.slot = s; r.dn = dn[e]; r.ds = ds[e];
-            ri[bp + rank] = r;
+            ri[natural_order ? e : bp + rank] = r;
         }
     }
 }
@@ -445,6 +445,242 @@ k_swap_stream(const T* __restrict__ D, int64_t ld, int w, int n, int P,
             out_tail[base + c] = seg[j];
             out_imin[base + c] = imin[j];
             out_islot[base + c] = islot[j];
+        }
+    }
+}
+
+// ---------------------------------------------------------------------------
+// a3, TMA-staged variant: a producer warp streams each row chunk of the
+// CTA's column tile with one cp.async.bulk (TMA bulk copy, SASS UBLKCP) into
+// an S-stage shared-memory ring guarded by mbarriers; NC consumer warps read
+// rows from shared memory and apply the same per-element update as
+// k_swap_stream.  Loads never occupy consumer registers, so the bytes in
+// flight per SM (S x RB x NC x 512 B per CTA) are set by the ring depth, not
+// by occupancy.
+// ---------------------------------------------------------------------------
+// Per-lane accumulator state of the SWAP-delta stream for the 4 candidate
+// columns a lane owns (Eq. eqn:better-change3 / Alg.3):
+//   plus[j]  dTD^{+x_c} so far
+//   seg[j]   acc_c[cur]: the current slot's running removal correction
+//   head[j]  the part's first (possibly cut) segment
+//   imin/islot  lexicographic min of R_i + acc_c[i] over closed interior segments
+template <typename A>
+struct StreamAcc {
+    A plus[4], seg[4], head[4], imin[4];
+    int islot[4];
+    int cur;
+    bool first;
+    __device__ __forceinline__ void init(int slot0) {
+#pragma unroll
+        for (int j = 0; j < 4; ++j) { plus[j] = 0; seg[j] = 0; head[j] = 0; imin[j] = amax<A>(); islot[j] = -1; }
+        cur = slot0;
+        first = true;
+    }
+    // One row o with cached (d_n, d_s); x[j] = d(x_o, x_c) for the lane's 4
+    // candidates.  Cases (i)/(ii) of Alg.3; the per-element work is
+    // entered only when some lane of the warp has d < d_s for that element.
+    template <typename T>
+    __device__ __forceinline__ void row(const T (&x)[4], T dn, T ds) {
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            if (__any_sync(FULL, x[j] < ds)) {
+                const A xa = (A)x[j];
+                const A dnA = (A)dn, dsA = (A)ds;
+                const bool c1 = x[j] < dn, c2 = x[j] < ds;
+                const A tp = c1 ? xa - dnA : (A)0;
+                const A ts = c1 ? dnA - dsA : (c2 ? xa - dsA : (A)0);
+                plus[j] += tp;
+                seg[j] += ts;
+            }
+        }
+    }
+    // The segment of slot `cur` ended; `next` starts.
+    template <typename RA>
+    __device__ __forceinline__ void close_segment(int next, const RA* __restrict__ R) {
+        if (first) {
+#pragma unroll
+            for (int j = 0; j < 4; ++j) head[j] = seg[j];
+            first = false;
+        } else {
+            const A rv = R[cur];
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+                const A val = rv + seg[j];
+                if (val < imin[j]) { imin[j] = val; islot[j] = cur; }
+            }
+        }
+#pragma unroll
+        for (int j = 0; j < 4; ++j) seg[j] = 0;
+        cur = next;
+    }
+    // End of the part: the open segment becomes the tail (or the head if the
+    // part held a single segment; its tail is then 0).
+    __device__ __forceinline__ void finish() {
+        if (first) {
+#pragma unroll
+            for (int j = 0; j < 4; ++j) { head[j] = seg[j]; seg[j] = 0; }
+        }
+    }
+};
+
+namespace ptx {
+__device__ __forceinline__ uint32_t sa(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(sa(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void fence_mbar_init() { asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory"); }
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(sa(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(sa(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+    asm volatile(
+        "{\n\t.reg .pred P;\n"
+        "KM_WAIT_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 P, [%0], %1;\n\t"
+        "@!P bra KM_WAIT_%=;\n}" ::"r"(sa(bar)),
+        "r"(parity)
+        : "memory");
+}
+__device__ __forceinline__ uint64_t policy_evict_first() {
+    uint64_t p;
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+    return p;
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar, uint64_t pol) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;" ::"r"(
+            sa(dst)),
+        "l"(src), "r"(bytes), "r"(sa(bar)), "l"(pol)
+        : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(sa(dst)),
+                 "l"(src), "r"(bytes), "r"(sa(bar))
+                 : "memory");
+}
+}  // namespace ptx
+
+template <typename T, int NC, int RB, int S>
+struct TmaCfg {
+    static constexpr int COLS = NC * 128;                  // columns per CTA
+    static constexpr int ROWB = COLS * (int)sizeof(T);     // bytes of one row chunk
+    static constexpr int DATAB = S * RB * ROWB;
+    static constexpr int RIB = S * RB * 16;
+    static constexpr int SMEM = DATAB + RIB + 2 * S * 8;
+    static constexpr int THREADS = (NC + 1) * 32;
+};
+
+template <typename T, typename A, int NC, int RB, int S>
+__global__ void __launch_bounds__((NC + 1) * 32, 2)
+k_swap_stream_tma(const T* __restrict__ D, int64_t ld, int w, int wpad, int n, int P,
+                  const RowInfo<T>* __restrict__ ri, const A* __restrict__ R,
+                  A* __restrict__ out_plus, A* __restrict__ out_head, A* __restrict__ out_tail,
+                  A* __restrict__ out_imin, int* __restrict__ out_islot) {
+    using C = TmaCfg<T, NC, RB, S>;
+    using V = typename Vec4<T>::type;
+    extern __shared__ __align__(128) unsigned char smem[];
+    T* sdata = reinterpret_cast<T*>(smem);
+    RowInfo<T>* sri = reinterpret_cast<RowInfo<T>*>(smem + C::DATAB);
+    uint64_t* full = reinterpret_cast<uint64_t*>(smem + C::DATAB + C::RIB);
+    uint64_t* empty = full + S;
+
+    const int q = blockIdx.y;
+    const int64_t p0 = (int64_t)q * n / P, p1 = (int64_t)(q + 1) * n / P;
+    const int nstages = (int)((p1 - p0 + RB - 1) / RB);
+    const int ctacol = blockIdx.x * C::COLS;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < S; ++s) {
+            ptx::mbar_init(&full[s], 1);
+            ptx::mbar_init(&empty[s], NC);
+        }
+        ptx::fence_mbar_init();
+    }
+    __syncthreads();
+
+    if (warp == NC) {
+        // ---------------- producer warp ----------------
+        const uint32_t cbytes = (uint32_t)min(C::COLS, wpad - ctacol) * (uint32_t)sizeof(T);
+        const uint64_t pol = ptx::policy_evict_first();
+        int o_next = (lane < RB && p0 + lane < p1) ? ri[p0 + lane].o : 0;
+        for (int st = 0; st < nstages; ++st) {
+            const int s = st % S;
+            if (st >= S) ptx::mbar_wait(&empty[s], ((st / S) & 1) ^ 1);
+            const int64_t pr = p0 + (int64_t)st * RB;
+            const int nb = (int)min((int64_t)RB, p1 - pr);
+            const int o = o_next;
+            const int64_t pn = pr + RB + lane;
+            if (lane < RB && pn < p1) o_next = ri[pn].o;     // prefetch the next stage's rows
+            if (lane == 0) ptx::mbar_expect_tx(&full[s], (uint32_t)nb * (cbytes + 16u));
+            __syncwarp();
+            if (lane < nb)
+                ptx::bulk_g2s(sdata + (size_t)(s * RB + lane) * C::COLS, D + (int64_t)o * ld + ctacol, cbytes,
+                              &full[s], pol);
+            if (lane == 0) ptx::bulk_g2s(sri + s * RB, ri + pr, (uint32_t)nb * 16u, &full[s]);
+        }
+        return;
+    }
+
+    // ---------------- consumer warps ----------------
+    const int cb = ctacol + warp * 128 + lane * 4;
+    const bool active = cb < w;
+    StreamAcc<A> acc;
+    acc.init(ri[p0].slot);
+    const T big = dmax<T>();
+
+    for (int st = 0; st < nstages; ++st) {
+        const int s = st % S;
+        ptx::mbar_wait(&full[s], (st / S) & 1);
+        const int64_t pr = p0 + (int64_t)st * RB;
+        const int nb = (int)min((int64_t)RB, p1 - pr);
+        RowInfo<T> r[RB];
+        T x[RB][4];
+#pragma unroll
+        for (int u = 0; u < RB; ++u) {
+            r[u] = sri[s * RB + u];    // rows >= nb hold stale data and are never used
+            V v = *reinterpret_cast<const V*>(sdata + (size_t)(s * RB + u) * C::COLS + warp * 128 + lane * 4);
+            memcpy(&x[u][0], &v.x, sizeof(T)); memcpy(&x[u][1], &v.y, sizeof(T));
+            memcpy(&x[u][2], &v.z, sizeof(T)); memcpy(&x[u][3], &v.w, sizeof(T));
+        }
+        __syncwarp();
+        if (lane == 0) ptx::mbar_arrive(&empty[s]);
+        if (!active) {
+#pragma unroll
+            for (int u = 0; u < RB; ++u)
+#pragma unroll
+                for (int j = 0; j < 4; ++j) x[u][j] = big;
+        }
+        if (nb == RB && r[RB - 1].slot == acc.cur) {
+            // fast path: a full stage inside the current slot's segment (rows are
+            // sorted by slot, so the last row's slot decides).
+#pragma unroll
+            for (int u = 0; u < RB; ++u) acc.row(x[u], r[u].dn, r[u].ds);
+        } else {
+#pragma unroll
+            for (int u = 0; u < RB; ++u) {
+                if (u < nb) {
+                    if (r[u].slot != acc.cur) acc.close_segment(r[u].slot, R);
+                    acc.row(x[u], r[u].dn, r[u].ds);
+                }
+            }
+        }
+    }
+    acc.finish();
+    if (!active) return;
+    const int64_t base = (int64_t)q * w;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+        const int c = cb + j;
+        if (c < w) {
+            out_plus[base + c] = acc.plus[j];
+            out_head[base + c] = acc.head[j];
+            out_tail[base + c] = acc.seg[j];
+            out_imin[base + c] = acc.imin[j];
+            out_islot[base + c] = acc.islot[j];
         }
     }
 }

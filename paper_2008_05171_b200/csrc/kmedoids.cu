@@ -4,6 +4,7 @@
 // enqueues kernels on the handle's stream and copies the per-iteration
 // decision (one 32-byte record) back to the host for the convergence test.
 #include <cstdarg>
+#include <cstdlib>
 #include <cstdio>
 #include <cstring>
 #include <memory>
@@ -54,13 +55,19 @@ constexpr int STREAM_U = 8;                   // rows in flight per warp
 constexpr int RESIDENT_CTAS = 4;              // ~16 warps per SM
 constexpr int TARGET_WAVES = 3;
 constexpr int MAX_K = 8192;
+// TMA-staged stream kernel: 7 consumer warps (896 columns) + 1 producer warp
+// (8 warps: 2 CTAs = 4 warps per SM sub-partition), 4 rows per stage, 7 stages
+// (~100 KB shared memory, 2 CTAs per SM).
+constexpr int TMA_NC = 7, TMA_RB = 4, TMA_S = 7;
+constexpr int TMA_COLS = TMA_NC * 128;
+constexpr int TMA_RESIDENT = 2;
 
 int64_t cdiv(int64_t a, int64_t b) { return (a + b - 1) / b; }
 
 // Number of row parts so the (column tiles x parts) grid fills the GPU.
-int choose_parts(int64_t n, int64_t w) {
-    const int64_t ncb = cdiv(w, STREAM_COLS);
-    int64_t P = cdiv((int64_t)NUM_SMS * RESIDENT_CTAS * TARGET_WAVES, ncb);
+int choose_parts(int64_t n, int64_t w, int cols_per_cta, int resident) {
+    const int64_t ncb = cdiv(w, cols_per_cta);
+    int64_t P = cdiv((int64_t)NUM_SMS * resident * TARGET_WAVES, ncb);
     P = std::min<int64_t>(P, std::max<int64_t>(1, n / 64));
     P = std::max<int64_t>(P, 1);
     return (int)P;
@@ -115,6 +122,9 @@ struct Impl : ImplBase {
     cudaStream_t st = nullptr;
     int P = 1, Pb = 1, B = 1, ncomb = 1, ntd = 1;
     int nranks = 1;
+    int wpad = 0;
+    bool use_tma = true;
+    int debug_natural = 0;
     bool ready = false;     // medoids + cache valid
 
     std::vector<void*> bufs;        // every device allocation, freed in the destructor
@@ -160,8 +170,13 @@ struct Impl : ImplBase {
         D = (const T*)Dp; n = n_; ld = ld_; c0 = c0_; c1 = c1_; k = k_; st = s;
         w = (int)(c1 - c0);
         sharded = !(c0 == 0 && c1 == n);
-        P = choose_parts(n, w);
-        Pb = P;
+        const char* ev = getenv("KM_STREAM");
+        use_tma = !(ev && strcmp(ev, "ldg") == 0);
+        const char* dbg = getenv("KM_DEBUG_NATURAL_ORDER");   // perf experiment only: wrong results
+        debug_natural = (dbg && dbg[0] == '1') ? 1 : 0;
+        P = use_tma ? choose_parts(n, w, TMA_COLS, TMA_RESIDENT) : choose_parts(n, w, STREAM_COLS, RESIDENT_CTAS);
+        Pb = choose_parts(n, w, STREAM_COLS, RESIDENT_CTAS);
+        wpad = (int)((w + 3) / 4 * 4);
         B = (int)cdiv(n, km::SORT_CHUNK);
         ncomb = (int)cdiv(w, 256);
         ntd = (int)std::min<int64_t>(cdiv(n, 256), 1024);
@@ -181,13 +196,13 @@ struct Impl : ImplBase {
         KM_TRY(alloc(&head_slot, P));
         KM_TRY(alloc(&tail_slot, P));
         KM_TRY(alloc(&R, k));
-        const size_t pw = (size_t)P * w;
+        const size_t pw = (size_t)std::max(P, Pb) * w;
         KM_TRY(alloc(&o_plus, pw));
         KM_TRY(alloc(&o_head, pw));
         KM_TRY(alloc(&o_tail, pw));
         KM_TRY(alloc(&o_imin, pw));
         KM_TRY(alloc(&o_islot, pw));
-        b_out = o_plus;   // BUILD partial sums reuse the plus buffer (Pb == P)
+        b_out = o_plus;   // BUILD partial sums reuse the plus buffer (sized for max(P, Pb))
         KM_TRY(alloc(&cand_v, w));
         KM_TRY(alloc(&cand_slot, w));
         KM_TRY(alloc(&partials, std::max(ncomb, 1)));
@@ -221,6 +236,7 @@ struct Impl : ImplBase {
         return KM_OK;
     }
     bool pending_prof = false;
+    bool tma_attr_set = false;
 
     km_status assign_full_and_td() {
         const int nb = (int)cdiv(n, 256);
@@ -271,7 +287,7 @@ struct Impl : ImplBase {
         KM_CKL();
         const int big = INT_MAX;
         KM_CK(cudaMemcpyAsync(empty_slot, &big, sizeof(int), cudaMemcpyHostToDevice, st));
-        km::k_slot_scatter<T><<<B, 32, k * sizeof(int), st>>>(near, dn, ds, (int)n, k, offsets, ri);
+        km::k_slot_scatter<T><<<B, 32, k * sizeof(int), st>>>(near, dn, ds, (int)n, k, offsets, ri, debug_natural);
         KM_CKL();
         km::k_removal_loss<T, A><<<(unsigned)cdiv((int64_t)k * 32, 256), 256, 0, st>>>(ri, seg_start, k, R, empty_slot);
         KM_CKL();
@@ -283,10 +299,22 @@ struct Impl : ImplBase {
     // a3 + a4 (local): stream the slab, combine into the local best record.
     km_status eval_local() {
         KM_TRY(prep());
-        dim3 g((unsigned)cdiv(w, STREAM_COLS), P);
         if (profiling) KM_CK(cudaEventRecord(ev0, st));
-        km::k_swap_stream<T, A, STREAM_WARPS, STREAM_U><<<g, STREAM_WARPS * 32, 0, st>>>(
-            D, ld, w, (int)n, P, ri, R, o_plus, o_head, o_tail, o_imin, o_islot);
+        if (use_tma) {
+            using C = km::TmaCfg<T, TMA_NC, TMA_RB, TMA_S>;
+            auto kern = km::k_swap_stream_tma<T, A, TMA_NC, TMA_RB, TMA_S>;
+            if (!tma_attr_set) {
+                KM_CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM));
+                tma_attr_set = true;
+            }
+            dim3 g((unsigned)cdiv(w, C::COLS), P);
+            kern<<<g, C::THREADS, C::SMEM, st>>>(D, ld, w, wpad, (int)n, P, ri, R, o_plus, o_head, o_tail, o_imin,
+                                                  o_islot);
+        } else {
+            dim3 g((unsigned)cdiv(w, STREAM_COLS), P);
+            km::k_swap_stream<T, A, STREAM_WARPS, STREAM_U><<<g, STREAM_WARPS * 32, 0, st>>>(
+                D, ld, w, (int)n, P, ri, R, o_plus, o_head, o_tail, o_imin, o_islot);
+        }
         KM_CKL();
         if (profiling) { KM_CK(cudaEventRecord(ev1, st)); pending_prof = true; }
         km::k_swap_combine<A><<<ncomb, 256, 0, st>>>(w, c0, P, o_plus, o_head, o_tail, o_imin, o_islot, head_slot,
