@@ -479,18 +479,62 @@ struct StreamAcc {
     // One row o with cached (d_n, d_s); x[j] = d(x_o, x_c) for the lane's 4
     // candidates.  Cases (i)/(ii) of Alg.3; the per-element work is
     // entered only when some lane of the warp has d < d_s for that element.
+    // One row o with cached (d_n, d_s); x[j] = d(x_o, x_c) for the lane's 4
+    // candidates.  Cases (i)/(ii) of Alg.3 P:883-889.
     template <typename T>
     __device__ __forceinline__ void row(const T (&x)[4], T dn, T ds) {
+        const T mn = min(min(x[0], x[1]), min(x[2], x[3]));
+        if (!__any_sync(FULL, mn < ds)) return;
+        const A dnA = (A)dn, dsA = (A)ds, dnds = dnA - dsA;
+#pragma unroll
+        for (int j = 0; j < 4; ++j) elem(j, x[j], dn, ds, dnA, dsA, dnds);
+    }
+    template <typename T>
+    __device__ __forceinline__ void elem(int j, T x, T dn, T ds, A dnA, A dsA, A dnds) {
+        const A xa = (A)x;
+        const bool c1 = x < dn, c2 = x < ds;
+        if (c1) { plus[j] += xa - dnA; seg[j] += dnds; }
+        if (c2 && !c1) seg[j] += xa - dsA;
+    }
+    // RB rows that all belong to the current slot's segment.  One warp-wide OR
+    // of the lanes' 4-bit masks "element j has d < d_s in some row of the
+    // stage" decides which of the 4 element columns need the update at all
+    // (~1% of the stream's pairs hit).  For a column that does, the RB row
+    // terms are computed independently (select form, no data-dependent
+    // branches) and summed as a tree, so the fixed-latency fp64 chain per
+    // stage is log2(RB)+1 deep instead of 2*RB.
+    template <typename T, int RB>
+    __device__ __forceinline__ void stage(const T (&x)[RB][4], const RowInfo<T> (&r)[RB]) {
+        unsigned m = 0;
 #pragma unroll
         for (int j = 0; j < 4; ++j) {
-            if (__any_sync(FULL, x[j] < ds)) {
-                const A xa = (A)x[j];
-                const A dnA = (A)dn, dsA = (A)ds;
-                const bool c1 = x[j] < dn, c2 = x[j] < ds;
-                const A tp = c1 ? xa - dnA : (A)0;
-                const A ts = c1 ? dnA - dsA : (c2 ? xa - dsA : (A)0);
-                plus[j] += tp;
-                seg[j] += ts;
+            bool h = false;
+#pragma unroll
+            for (int u = 0; u < RB; ++u) h |= x[u][j] < r[u].ds;
+            m |= (unsigned)h << j;
+        }
+        const unsigned wm = __reduce_or_sync(FULL, m);
+        if (wm == 0) return;
+        A dnA[RB], dsA[RB], dnds[RB];
+#pragma unroll
+        for (int u = 0; u < RB; ++u) { dnA[u] = (A)r[u].dn; dsA[u] = (A)r[u].ds; dnds[u] = dnA[u] - dsA[u]; }
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            if (wm & (1u << j)) {
+                A tp[RB], ts[RB];
+#pragma unroll
+                for (int u = 0; u < RB; ++u) {
+                    const bool c1 = x[u][j] < r[u].dn, c2 = x[u][j] < r[u].ds;
+                    const A t = (A)x[u][j] - (c1 ? dnA[u] : dsA[u]);
+                    tp[u] = c1 ? t : (A)0;
+                    ts[u] = c1 ? dnds[u] : (c2 ? t : (A)0);
+                }
+#pragma unroll
+                for (int h = 1; h < RB; h <<= 1)
+#pragma unroll
+                    for (int u = 0; u + h < RB; u += 2 * h) { tp[u] += tp[u + h]; ts[u] += ts[u + h]; }
+                plus[j] += tp[0];
+                seg[j] += ts[0];
             }
         }
     }
@@ -529,6 +573,7 @@ __device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
     asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(sa(bar)), "r"(count) : "memory");
 }
 __device__ __forceinline__ void fence_mbar_init() { asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory"); }
+__device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
 __device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
     asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(sa(bar)), "r"(bytes) : "memory");
 }
@@ -578,7 +623,7 @@ __global__ void __launch_bounds__((NC + 1) * 32, 2)
 k_swap_stream_tma(const T* __restrict__ D, int64_t ld, int w, int wpad, int n, int P,
                   const RowInfo<T>* __restrict__ ri, const A* __restrict__ R,
                   A* __restrict__ out_plus, A* __restrict__ out_head, A* __restrict__ out_tail,
-                  A* __restrict__ out_imin, int* __restrict__ out_islot) {
+                  A* __restrict__ out_imin, int* __restrict__ out_islot, int debug_nocompute) {
     using C = TmaCfg<T, NC, RB, S>;
     using V = typename Vec4<T>::type;
     extern __shared__ __align__(128) unsigned char smem[];
@@ -654,11 +699,11 @@ k_swap_stream_tma(const T* __restrict__ D, int64_t ld, int w, int wpad, int n, i
 #pragma unroll
                 for (int j = 0; j < 4; ++j) x[u][j] = big;
         }
+        if (debug_nocompute) continue;
         if (nb == RB && r[RB - 1].slot == acc.cur) {
             // fast path: a full stage inside the current slot's segment (rows are
             // sorted by slot, so the last row's slot decides).
-#pragma unroll
-            for (int u = 0; u < RB; ++u) acc.row(x[u], r[u].dn, r[u].ds);
+            acc.template stage<T, RB>(x, r);
         } else {
 #pragma unroll
             for (int u = 0; u < RB; ++u) {
@@ -681,6 +726,371 @@ k_swap_stream_tma(const T* __restrict__ D, int64_t ld, int w, int wpad, int n, i
             out_tail[base + c] = acc.seg[j];
             out_imin[base + c] = acc.imin[j];
             out_islot[base + c] = acc.islot[j];
+        }
+    }
+}
+
+// ---------------------------------------------------------------------------
+// a3, warp-autonomous TMA variant (default).  Every warp owns 128 candidate
+// columns and its own S-stage shared-memory ring: it refills a stage with
+// cp.async.bulk copies (one 512-byte row chunk per row, plus the 16-byte
+// RowInfo records) as soon as it has moved that stage into registers.  No
+// barrier couples the warps of a CTA, so a warp whose candidates are hit
+// often (case (i)/(ii) updates) never stalls the refills of the others.
+// ---------------------------------------------------------------------------
+template <typename T, int NW, int RB, int S>
+struct WTmaCfg {
+    static constexpr int ROWB = 128 * (int)sizeof(T);                  // one warp's row chunk
+    static constexpr int WARPB = S * RB * (ROWB + 16) + S * 8;          // data + RowInfo + full barriers
+    static constexpr int SMEM = NW * WARPB;
+    static constexpr int THREADS = NW * 32;
+};
+
+template <typename T, typename A, int NW, int RB, int S>
+__global__ void __launch_bounds__(NW * 32)
+k_swap_stream_wtma(const T* __restrict__ D, int64_t ld, int w, int wpad, int n, int P,
+                   const RowInfo<T>* __restrict__ ri, const A* __restrict__ R,
+                   A* __restrict__ out_plus, A* __restrict__ out_head, A* __restrict__ out_tail,
+                   A* __restrict__ out_imin, int* __restrict__ out_islot, int debug_nocompute) {
+    using C = WTmaCfg<T, NW, RB, S>;
+    using V = typename Vec4<T>::type;
+    extern __shared__ __align__(128) unsigned char smem[];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    unsigned char* wbase = smem + warp * C::WARPB;
+    T* sdata = reinterpret_cast<T*>(wbase);                                   // [S][RB][128]
+    RowInfo<T>* sri = reinterpret_cast<RowInfo<T>*>(wbase + S * RB * C::ROWB); // [S][RB]
+    uint64_t* full = reinterpret_cast<uint64_t*>(wbase + S * RB * (C::ROWB + 16));
+
+    const int q = blockIdx.y;
+    const int64_t p0 = (int64_t)q * n / P, p1 = (int64_t)(q + 1) * n / P;
+    const int nstages = (int)((p1 - p0 + RB - 1) / RB);
+    const int cw = (blockIdx.x * NW + warp) * 128;          // first column of this warp
+    if (cw >= w) return;                                     // no warp-collective op spans warps
+    const uint32_t cbytes = (uint32_t)min(128, wpad - cw) * (uint32_t)sizeof(T);
+    const T* Dw = D + cw;
+
+    if (lane == 0) {
+        for (int s = 0; s < S; ++s) ptx::mbar_init(&full[s], 1);
+        ptx::fence_mbar_init();
+    }
+    __syncwarp();
+    const uint64_t pol = ptx::policy_evict_first();
+
+    // refill of stage st (buffer st % S); `o` = row index held by lane u < RB
+    auto issue = [&](int st, int o) {
+        const int64_t pr = p0 + (int64_t)st * RB;
+        if (pr >= p1) return;
+        const int nb = (int)min((int64_t)RB, p1 - pr);
+        const int s = st % S;
+        if (lane == 0) ptx::mbar_expect_tx(&full[s], (uint32_t)nb * (cbytes + 16u));
+        __syncwarp();
+        if (lane < nb) ptx::bulk_g2s(sdata + (size_t)(s * RB + lane) * 128, Dw + (int64_t)o * ld, cbytes, &full[s], pol);
+        if (lane == 0) ptx::bulk_g2s(sri + s * RB, ri + pr, (uint32_t)nb * 16u, &full[s]);
+    };
+    auto row_of = [&](int st) -> int {
+        const int64_t p = p0 + (int64_t)st * RB + lane;
+        return (lane < RB && p < p1) ? ri[p].o : 0;
+    };
+    for (int st = 0; st < S; ++st) issue(st, row_of(st));
+    int o_pref = row_of(S);                                  // rows of the next refill
+
+    const int cb = cw + lane * 4;
+    const bool active = cb < w;
+    StreamAcc<A> acc;
+    acc.init(ri[p0].slot);
+    const T big = dmax<T>();
+
+    for (int st = 0; st < nstages; ++st) {
+        const int s = st % S;
+        ptx::mbar_wait(&full[s], (st / S) & 1);
+        const int64_t pr = p0 + (int64_t)st * RB;
+        const int nb = (int)min((int64_t)RB, p1 - pr);
+        RowInfo<T> r[RB];
+        T x[RB][4];
+#pragma unroll
+        for (int u = 0; u < RB; ++u) {
+            r[u] = sri[s * RB + u];
+            V v = *reinterpret_cast<const V*>(sdata + (size_t)(s * RB + u) * 128 + lane * 4);
+            memcpy(&x[u][0], &v.x, sizeof(T)); memcpy(&x[u][1], &v.y, sizeof(T));
+            memcpy(&x[u][2], &v.z, sizeof(T)); memcpy(&x[u][3], &v.w, sizeof(T));
+        }
+        if (!active) {
+#pragma unroll
+            for (int u = 0; u < RB; ++u)
+#pragma unroll
+                for (int j = 0; j < 4; ++j) x[u][j] = big;
+        }
+        const bool fast = (nb == RB) && (r[RB - 1].slot == acc.cur);
+        // the stage's shared memory has been read into registers (r[] is used
+        // just above); order those generic-proxy reads before the async-proxy
+        // refill of the same buffer.
+        __syncwarp();
+        ptx::fence_proxy_async();
+        const int o_now = o_pref;
+        o_pref = row_of(st + S + 1);
+        issue(st + S, o_now);
+        if (debug_nocompute) continue;
+        if (fast) {
+            acc.template stage<T, RB>(x, r);
+        } else {
+#pragma unroll
+            for (int u = 0; u < RB; ++u) {
+                if (u < nb) {
+                    if (r[u].slot != acc.cur) acc.close_segment(r[u].slot, R);
+                    acc.row(x[u], r[u].dn, r[u].ds);
+                }
+            }
+        }
+    }
+    acc.finish();
+    if (!active) return;
+    const int64_t base = (int64_t)q * w;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+        const int c = cb + j;
+        if (c < w) {
+            out_plus[base + c] = acc.plus[j];
+            out_head[base + c] = acc.head[j];
+            out_tail[base + c] = acc.seg[j];
+            out_imin[base + c] = acc.imin[j];
+            out_islot[base + c] = acc.islot[j];
+        }
+    }
+}
+
+// ---------------------------------------------------------------------------
+// a3, TMA ring + compacted hit processing (default stream kernel).
+//
+// Same producer / S-stage ring as k_swap_stream_tma.  Only ~1% of the
+// (row, candidate) pairs satisfy d < d_s, so the consumers
+// split every stage in two phases:
+//   A  every consumer lane compares its 4 columns x RB rows against d_s and
+//      appends one entry (column, row mask) per column that has a hit to a
+//      CTA-wide list in shared memory (warp-aggregated atomic);
+//   B  after a named barrier, the list is spread over all consumer threads;
+//      each entry updates its column's dTD^{+x_c} and acc_c[slot] partial
+//      sums (fp64 / int64, shared memory) for the marked rows in row order.
+// The per-column accumulation order is fixed (rows ascending, one writer per
+// column and stage), so results are deterministic, and the fp64 work is
+// spread evenly over the warps instead of following where the hits are.
+// Stages that contain a slot change (the end of a segment) or a part's last
+// partial stage take a simple per-lane path.
+// ---------------------------------------------------------------------------
+template <typename T, typename A, int NC, int RB, int S>
+struct CmpCfg {
+    static constexpr int COLS = NC * 128;
+    static constexpr int ROWB = COLS * (int)sizeof(T);
+    static constexpr int DATAB = S * RB * ROWB;
+    static constexpr int RIB = S * RB * 16;
+    static constexpr int BARB = 2 * S * 8;
+    static constexpr int ACCB = 2 * COLS * (int)sizeof(A);      // plus, seg per column
+    static constexpr int HITB = COLS * 4 + S * 4;                 // entries + per-stage counters
+    static constexpr int SMEM = DATAB + RIB + BARB + ACCB + HITB;
+    static constexpr int THREADS = (NC + 1) * 32;
+};
+
+__device__ __forceinline__ void named_bar_sync(int id, int nthreads) {
+    asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
+}
+
+template <typename T, typename A, int NC, int RB, int S>
+__global__ void __launch_bounds__((NC + 1) * 32, 2)
+k_swap_stream_cmp(const T* __restrict__ D, int64_t ld, int w, int wpad, int n, int P,
+                  const RowInfo<T>* __restrict__ ri, const A* __restrict__ R,
+                  A* __restrict__ out_plus, A* __restrict__ out_head, A* __restrict__ out_tail,
+                  A* __restrict__ out_imin, int* __restrict__ out_islot) {
+    using C = CmpCfg<T, A, NC, RB, S>;
+    using V = typename Vec4<T>::type;
+    extern __shared__ __align__(128) unsigned char smem[];
+    T* sdata = reinterpret_cast<T*>(smem);
+    RowInfo<T>* sri = reinterpret_cast<RowInfo<T>*>(smem + C::DATAB);
+    uint64_t* full = reinterpret_cast<uint64_t*>(smem + C::DATAB + C::RIB);
+    uint64_t* empty = full + S;
+    A* accp = reinterpret_cast<A*>(smem + C::DATAB + C::RIB + C::BARB);
+    A* accs = accp + C::COLS;
+    int* hits = reinterpret_cast<int*>(smem + C::DATAB + C::RIB + C::BARB + C::ACCB);
+    int* hitcnt = hits + C::COLS;
+
+    const int q = blockIdx.y;
+    const int64_t p0 = (int64_t)q * n / P, p1 = (int64_t)(q + 1) * n / P;
+    const int nstages = (int)((p1 - p0 + RB - 1) / RB);
+    const int ctacol = blockIdx.x * C::COLS;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    constexpr int NCT = NC * 32;   // consumer threads
+
+    if (threadIdx.x == 0) {
+        for (int st = 0; st < S; ++st) {
+            ptx::mbar_init(&full[st], 1);
+            ptx::mbar_init(&empty[st], 1);
+        }
+        ptx::fence_mbar_init();
+    }
+    for (int i = threadIdx.x; i < C::COLS; i += blockDim.x) { accp[i] = 0; accs[i] = 0; }
+    for (int i = threadIdx.x; i < S; i += blockDim.x) hitcnt[i] = 0;
+    __syncthreads();
+
+    if (warp == NC) {
+        // ---------------- producer warp (as in k_swap_stream_tma) ----------------
+        const uint32_t cbytes = (uint32_t)min(C::COLS, wpad - ctacol) * (uint32_t)sizeof(T);
+        const uint64_t pol = ptx::policy_evict_first();
+        int o_next = (lane < RB && p0 + lane < p1) ? ri[p0 + lane].o : 0;
+        for (int st = 0; st < nstages; ++st) {
+            const int s = st % S;
+            if (st >= S) ptx::mbar_wait(&empty[s], ((st / S) & 1) ^ 1);
+            const int64_t pr = p0 + (int64_t)st * RB;
+            const int nb = (int)min((int64_t)RB, p1 - pr);
+            const int o = o_next;
+            const int64_t pn = pr + RB + lane;
+            if (lane < RB && pn < p1) o_next = ri[pn].o;
+            if (lane == 0) ptx::mbar_expect_tx(&full[s], (uint32_t)nb * (cbytes + 16u));
+            __syncwarp();
+            if (lane < nb)
+                ptx::bulk_g2s(sdata + (size_t)(s * RB + lane) * C::COLS, D + (int64_t)o * ld + ctacol, cbytes,
+                              &full[s], pol);
+            if (lane == 0) ptx::bulk_g2s(sri + s * RB, ri + pr, (uint32_t)nb * 16u, &full[s]);
+        }
+        return;
+    }
+
+    // ---------------- consumer warps ----------------
+    const int cl0 = warp * 128 + lane * 4;          // this lane's first column within the tile
+    const int cb = ctacol + cl0;
+    const bool active = cb < w;
+    const T big = dmax<T>();
+    A head[4], imin[4];
+    int islot[4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) { head[j] = 0; imin[j] = amax<A>(); islot[j] = -1; }
+    int cur = ri[p0].slot;
+    bool first = true;
+    const unsigned lt = (1u << lane) - 1u;
+
+    auto close_segment = [&](int next) {      // the lane's own 4 columns
+        if (first) {
+#pragma unroll
+            for (int j = 0; j < 4; ++j) head[j] = accs[cl0 + j];
+            first = false;
+        } else {
+            const A rv = R[cur];
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+                const A val = rv + accs[cl0 + j];
+                if (val < imin[j]) { imin[j] = val; islot[j] = cur; }
+            }
+        }
+#pragma unroll
+        for (int j = 0; j < 4; ++j) accs[cl0 + j] = 0;
+        cur = next;
+    };
+
+    for (int st = 0; st < nstages; ++st) {
+        const int s = st % S;
+        ptx::mbar_wait(&full[s], (st / S) & 1);
+        const int64_t pr = p0 + (int64_t)st * RB;
+        const int nb = (int)min((int64_t)RB, p1 - pr);
+        const T* srow = sdata + (size_t)(s * RB) * C::COLS;
+        const RowInfo<T>* srii = sri + s * RB;
+        const bool fast = (nb == RB) && (srii[RB - 1].slot == cur);   // identical in every consumer warp
+        if (fast) {
+            // ---- phase A: per-column row masks, compacted into the hit list ----
+            unsigned colmask[4] = {0, 0, 0, 0};
+#pragma unroll
+            for (int u = 0; u < RB; ++u) {
+                const T ds = srii[u].ds;
+                const V v = *reinterpret_cast<const V*>(srow + (size_t)u * C::COLS + cl0);
+                T x[4];
+                memcpy(&x[0], &v.x, sizeof(T)); memcpy(&x[1], &v.y, sizeof(T));
+                memcpy(&x[2], &v.z, sizeof(T)); memcpy(&x[3], &v.w, sizeof(T));
+#pragma unroll
+                for (int j = 0; j < 4; ++j) colmask[j] |= (unsigned)(active && x[j] < ds) << u;
+            }
+            const int hc = (colmask[0] != 0) + (colmask[1] != 0) + (colmask[2] != 0) + (colmask[3] != 0);
+            const unsigned anyb = __ballot_sync(FULL, hc != 0);
+            if (anyb) {
+                int incl = hc;
+#pragma unroll
+                for (int d = 1; d < 32; d <<= 1) {
+                    const int y = __shfl_up_sync(FULL, incl, d);
+                    if (lane >= d) incl += y;
+                }
+                int base = 0;
+                if (lane == 31) base = atomicAdd(&hitcnt[s], incl);
+                base = __shfl_sync(FULL, base, 31);
+                int pos = base + incl - hc;
+#pragma unroll
+                for (int j = 0; j < 4; ++j)
+                    if (colmask[j]) hits[pos++] = (cl0 + j) | (int)(colmask[j] << 16);
+            }
+            (void)lt;
+            named_bar_sync(1, NCT);
+            // ---- phase B: one thread per hit column, rows in order ----
+            const int H = hitcnt[s];
+            for (int e = warp + NC * lane; e < H; e += NCT) {     // spread entries over the warps
+                const int ent = hits[e];
+                const int c = ent & 0xffff;
+                const unsigned rm = (unsigned)ent >> 16;
+                A pp = 0, sg = 0;
+#pragma unroll
+                for (int u = 0; u < RB; ++u) {
+                    if (rm & (1u << u)) {
+                        const T xv = srow[(size_t)u * C::COLS + c];
+                        const T dn = srii[u].dn, ds = srii[u].ds;
+                        const A xa = (A)xv;
+                        if (xv < dn) { pp += xa - (A)dn; sg += (A)dn - (A)ds; }
+                        else { sg += xa - (A)ds; }
+                    }
+                }
+                accp[c] += pp;
+                accs[c] += sg;
+            }
+            named_bar_sync(1, NCT);
+            if (warp == 0 && lane == 0) {
+                hitcnt[s] = 0;
+                ptx::mbar_arrive(&empty[s]);
+            }
+        } else {
+            // ---- slow path: per lane, its own 4 columns, row by row ----
+            for (int u = 0; u < nb; ++u) {
+                const RowInfo<T> r = srii[u];
+                if (r.slot != cur) close_segment(r.slot);
+                const V v = *reinterpret_cast<const V*>(srow + (size_t)u * C::COLS + cl0);
+                T x[4];
+                memcpy(&x[0], &v.x, sizeof(T)); memcpy(&x[1], &v.y, sizeof(T));
+                memcpy(&x[2], &v.z, sizeof(T)); memcpy(&x[3], &v.w, sizeof(T));
+#pragma unroll
+                for (int j = 0; j < 4; ++j) {
+                    const T xv = active ? x[j] : big;
+                    if (xv < r.ds) {
+                        const A xa = (A)xv;
+                        if (xv < r.dn) { accp[cl0 + j] += xa - (A)r.dn; accs[cl0 + j] += (A)r.dn - (A)r.ds; }
+                        else { accs[cl0 + j] += xa - (A)r.ds; }
+                    }
+                }
+            }
+            named_bar_sync(1, NCT);
+            if (warp == 0 && lane == 0) ptx::mbar_arrive(&empty[s]);
+        }
+    }
+    // end of the part: the open segment is the tail (or the head)
+    A tail[4];
+    if (first) {
+#pragma unroll
+        for (int j = 0; j < 4; ++j) { head[j] = accs[cl0 + j]; tail[j] = 0; }
+    } else {
+#pragma unroll
+        for (int j = 0; j < 4; ++j) tail[j] = accs[cl0 + j];
+    }
+    if (!active) return;
+    const int64_t base = (int64_t)q * w;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+        const int c = cb + j;
+        if (c < w) {
+            out_plus[base + c] = accp[cl0 + j];
+            out_head[base + c] = head[j];
+            out_tail[base + c] = tail[j];
+            out_imin[base + c] = imin[j];
+            out_islot[base + c] = islot[j];
         }
     }
 }

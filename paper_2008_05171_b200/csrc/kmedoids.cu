@@ -60,6 +60,14 @@ constexpr int MAX_K = 8192;
 // (~100 KB shared memory, 2 CTAs per SM).
 constexpr int TMA_NC = 7, TMA_RB = 4, TMA_S = 7;
 constexpr int TMA_COLS = TMA_NC * 128;
+// Warp-autonomous TMA stream kernel (default): 4 warps x 128 columns per CTA,
+// each warp with its own 6-stage x 4-row ring (~12.7 KB), 4 CTAs per SM.
+constexpr int WT_NW = 4, WT_RB = 4, WT_S = 6;
+// TMA ring + compacted hit lists (default): 7 consumer warps + 1 producer,
+// 4 rows per stage, 6 stages, per-column fp64 partials in shared memory.
+constexpr int CMP_NC = 7, CMP_RB = 4, CMP_S = 6;
+constexpr int WT_COLS = WT_NW * 128;
+constexpr int WT_RESIDENT = 4;
 constexpr int TMA_RESIDENT = 2;
 
 int64_t cdiv(int64_t a, int64_t b) { return (a + b - 1) / b; }
@@ -124,7 +132,9 @@ struct Impl : ImplBase {
     int nranks = 1;
     int wpad = 0;
     bool use_tma = true;
+    int stream_kind = 2;
     int debug_natural = 0;
+    int debug_nocompute = 0;
     bool ready = false;     // medoids + cache valid
 
     std::vector<void*> bufs;        // every device allocation, freed in the destructor
@@ -171,10 +181,24 @@ struct Impl : ImplBase {
         w = (int)(c1 - c0);
         sharded = !(c0 == 0 && c1 == n);
         const char* ev = getenv("KM_STREAM");
-        use_tma = !(ev && strcmp(ev, "ldg") == 0);
+        stream_kind = 6;                                        // TMA ring + compacted hits (default)
+        if (ev && strcmp(ev, "tma") == 0) stream_kind = 1;
+        if (ev && strcmp(ev, "ldg") == 0) stream_kind = 0;
+        if (ev && strcmp(ev, "wtma") == 0) stream_kind = 2;
+        if (ev && strcmp(ev, "wtma1") == 0) stream_kind = 3;
+        if (ev && strcmp(ev, "wtma1d") == 0) stream_kind = 4;
+        if (ev && strcmp(ev, "wtma2") == 0) stream_kind = 5;
+        use_tma = stream_kind == 1;
         const char* dbg = getenv("KM_DEBUG_NATURAL_ORDER");   // perf experiment only: wrong results
         debug_natural = (dbg && dbg[0] == '1') ? 1 : 0;
-        P = use_tma ? choose_parts(n, w, TMA_COLS, TMA_RESIDENT) : choose_parts(n, w, STREAM_COLS, RESIDENT_CTAS);
+        const char* dnc = getenv("KM_DEBUG_NOCOMPUTE");        // perf experiment only: wrong results
+        debug_nocompute = (dnc && dnc[0] == '1') ? 1 : 0;
+        P = stream_kind == 6 ? choose_parts(n, w, CMP_NC * 128, 2)
+            : stream_kind == 1 ? choose_parts(n, w, TMA_COLS, TMA_RESIDENT)
+            : stream_kind == 2 ? choose_parts(n, w, WT_COLS, WT_RESIDENT)
+            : stream_kind == 3 || stream_kind == 4 ? choose_parts(n, w, 128, 16)
+            : stream_kind == 5 ? choose_parts(n, w, 256, 8)
+                               : choose_parts(n, w, STREAM_COLS, RESIDENT_CTAS);
         Pb = choose_parts(n, w, STREAM_COLS, RESIDENT_CTAS);
         wpad = (int)((w + 3) / 4 * 4);
         B = (int)cdiv(n, km::SORT_CHUNK);
@@ -237,6 +261,7 @@ struct Impl : ImplBase {
     }
     bool pending_prof = false;
     bool tma_attr_set = false;
+    bool cmp_attr_set = false;
 
     km_status assign_full_and_td() {
         const int nb = (int)cdiv(n, 256);
@@ -300,7 +325,25 @@ struct Impl : ImplBase {
     km_status eval_local() {
         KM_TRY(prep());
         if (profiling) KM_CK(cudaEventRecord(ev0, st));
-        if (use_tma) {
+        if (stream_kind == 6) {
+            using C = km::CmpCfg<T, A, CMP_NC, CMP_RB, CMP_S>;
+            auto kern = km::k_swap_stream_cmp<T, A, CMP_NC, CMP_RB, CMP_S>;
+            if (!cmp_attr_set) {
+                KM_CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM));
+                cmp_attr_set = true;
+            }
+            dim3 g((unsigned)cdiv(w, C::COLS), P);
+            kern<<<g, C::THREADS, C::SMEM, st>>>(D, ld, w, wpad, (int)n, P, ri, R, o_plus, o_head, o_tail, o_imin,
+                                                  o_islot);
+        } else if (stream_kind == 2) {
+            KM_TRY((launch_wtma<WT_NW, WT_RB, WT_S>()));
+        } else if (stream_kind == 3) {
+            KM_TRY((launch_wtma<1, 4, 6>()));
+        } else if (stream_kind == 4) {
+            KM_TRY((launch_wtma<1, 4, 10>()));
+        } else if (stream_kind == 5) {
+            KM_TRY((launch_wtma<2, 4, 8>()));
+        } else if (use_tma) {
             using C = km::TmaCfg<T, TMA_NC, TMA_RB, TMA_S>;
             auto kern = km::k_swap_stream_tma<T, A, TMA_NC, TMA_RB, TMA_S>;
             if (!tma_attr_set) {
@@ -309,7 +352,7 @@ struct Impl : ImplBase {
             }
             dim3 g((unsigned)cdiv(w, C::COLS), P);
             kern<<<g, C::THREADS, C::SMEM, st>>>(D, ld, w, wpad, (int)n, P, ri, R, o_plus, o_head, o_tail, o_imin,
-                                                  o_islot);
+                                                  o_islot, debug_nocompute);
         } else {
             dim3 g((unsigned)cdiv(w, STREAM_COLS), P);
             km::k_swap_stream<T, A, STREAM_WARPS, STREAM_U><<<g, STREAM_WARPS * 32, 0, st>>>(
@@ -321,6 +364,17 @@ struct Impl : ImplBase {
                                                       tail_slot, R, empty_slot, point_slot, cand_v, cand_slot,
                                                       partials, counters, rec_local);
         KM_CKL();
+        return KM_OK;
+    }
+
+    template <int NW, int RB, int S>
+    km_status launch_wtma() {
+        using C = km::WTmaCfg<T, NW, RB, S>;
+        auto kern = km::k_swap_stream_wtma<T, A, NW, RB, S>;
+        KM_CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM));
+        dim3 g((unsigned)cdiv(w, NW * 128), P);
+        kern<<<g, C::THREADS, C::SMEM, st>>>(D, ld, w, wpad, (int)n, P, ri, R, o_plus, o_head, o_tail, o_imin, o_islot,
+                                              debug_nocompute);
         return KM_OK;
     }
 
