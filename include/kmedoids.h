@@ -132,6 +132,12 @@ km_status kmedoids_get_cache(km_handle* h, int32_t* nearest_out, int32_t* second
  * = its lexicographic argmin slot; medoid columns get slot -1. */
 km_status kmedoids_eval_candidates(km_handle* h, void* dtd_out, int32_t* slot_out);
 
+/* The swaps applied by the last kmedoids_swap_iter call, in application
+ * order: slots_out[j], cands_out[j] (global point index) and dtds_out[j]
+ * (int64_t / double) for j < min(*count_out, cap).  Any output may be NULL. */
+km_status kmedoids_last_swaps(km_handle* h, int32_t* slots_out, int32_t* cands_out, void* dtds_out, int32_t cap,
+                              int32_t* count_out);
+
 /* Profiling: enable (1) / disable (0) CUDA-event timing of the SWAP-delta
  * stream kernel on the handle's stream; kmedoids_stream_time returns the
  * accumulated milliseconds and launch count since the last reset. */

@@ -9,6 +9,8 @@
 //   a8     k_td_from_dn
 #pragma once
 #include "km_common.cuh"
+#include <cooperative_groups.h>
+#include <type_traits>
 
 namespace km {
 
@@ -538,14 +540,22 @@ struct StreamAcc {
             }
         }
     }
-    // The segment of slot `cur` ended; `next` starts.
+    // The segment of slot `cur` ended; `next` starts.  FastPAM2 mode
+    // (acc_out != nullptr) also stores the complete interior sums
+    // acc_c[cur] = acc_out[cur*w + c] for the lane's columns c = cb..cb+3.
     template <typename RA>
-    __device__ __forceinline__ void close_segment(int next, const RA* __restrict__ R) {
+    __device__ __forceinline__ void close_segment(int next, const RA* __restrict__ R, A* __restrict__ acc_out = nullptr,
+                                                  int w = 0, int cb = 0) {
         if (first) {
 #pragma unroll
             for (int j = 0; j < 4; ++j) head[j] = seg[j];
             first = false;
         } else {
+            if (acc_out) {
+#pragma unroll
+                for (int j = 0; j < 4; ++j)
+                    if (cb + j < w) acc_out[(int64_t)cur * w + cb + j] = seg[j];
+            }
             const A rv = R[cur];
 #pragma unroll
             for (int j = 0; j < 4; ++j) {
@@ -618,12 +628,13 @@ struct TmaCfg {
     static constexpr int THREADS = (NC + 1) * 32;
 };
 
-template <typename T, typename A, int NC, int RB, int S>
-__global__ void __launch_bounds__((NC + 1) * 32, 2)
+template <typename T, typename A, int NC, int RB, int S, int MINB = 2>
+__global__ void __launch_bounds__((NC + 1) * 32, MINB)
 k_swap_stream_tma(const T* __restrict__ D, int64_t ld, int w, int wpad, int n, int P,
                   const RowInfo<T>* __restrict__ ri, const A* __restrict__ R,
                   A* __restrict__ out_plus, A* __restrict__ out_head, A* __restrict__ out_tail,
-                  A* __restrict__ out_imin, int* __restrict__ out_islot, int debug_nocompute) {
+                  A* __restrict__ out_imin, int* __restrict__ out_islot, int debug_nocompute,
+                  A* __restrict__ out_acc = nullptr) {
     using C = TmaCfg<T, NC, RB, S>;
     using V = typename Vec4<T>::type;
     extern __shared__ __align__(128) unsigned char smem[];
@@ -708,7 +719,7 @@ k_swap_stream_tma(const T* __restrict__ D, int64_t ld, int w, int wpad, int n, i
 #pragma unroll
             for (int u = 0; u < RB; ++u) {
                 if (u < nb) {
-                    if (r[u].slot != acc.cur) acc.close_segment(r[u].slot, R);
+                    if (r[u].slot != acc.cur) acc.close_segment(r[u].slot, R, out_acc, w, cb);
                     acc.row(x[u], r[u].dn, r[u].ds);
                 }
             }
@@ -1106,7 +1117,7 @@ __global__ void k_swap_combine(int w, int64_t col_begin, int P, const A* __restr
                                const A* __restrict__ R, const int* __restrict__ empty_slot,
                                const int* __restrict__ point_slot, A* __restrict__ cand_v,
                                int* __restrict__ cand_slot, Rec<A>* partials, unsigned* counter,
-                               Rec<A>* out) {
+                               Rec<A>* out, A* __restrict__ acc_out = nullptr, A* __restrict__ plus_out = nullptr) {
     const int cl = blockIdx.x * blockDim.x + threadIdx.x;
     Rec<A> best = rec_none<A>();
     if (cl < w) {
@@ -1115,6 +1126,7 @@ __global__ void k_swap_combine(int w, int64_t col_begin, int P, const A* __restr
         const int es = *empty_slot;
         if (es != INT_MAX) { bv = 0; bs = es; }
         auto fin = [&](int s, A sum) {
+            if (acc_out) acc_out[(int64_t)s * w + cl] = sum;     // FastPAM2: complete acc_c[s]
             const A val = R[s] + sum;
             if (val < bv || (val == bv && s < bs)) { bv = val; bs = s; }
         };
@@ -1144,6 +1156,7 @@ __global__ void k_swap_combine(int w, int64_t col_begin, int P, const A* __restr
             }
         }
         fin(cs, carry);
+        if (plus_out) plus_out[cl] = plus;
         const A dtd = bv + plus;
         const int64_t c = col_begin + cl;
         const bool medoid = point_slot[c] >= 0;
@@ -1180,6 +1193,152 @@ __global__ void k_select(const Rec<A>* __restrict__ recs, int nrec, A* __restric
         point_slot[b.c] = b.slot;
         *td += b.v;
         dec->swaps += 1;
+    }
+}
+
+// ---------------------------------------------------------------------------
+// a6: FastPAM2 (reading R6)
+// ---------------------------------------------------------------------------
+
+// Per slot i: (v_i, c_i) = lexicographic min over local non-medoid candidates
+// of (dTD(m_i, x_c), c) with dTD = R_i + acc_c[i] + dTD^{+x_c}
+// (Eq. eqn:better-change3).  Slots with an empty segment have acc_c[i] = 0.
+// One block per slot; reads row i of the k x w acc matrix (coalesced).
+template <typename A>
+__global__ void k_fp2_slot_best(int w, int64_t col_begin, const A* __restrict__ acc, const A* __restrict__ plus,
+                                const A* __restrict__ R, const int* __restrict__ seg_start,
+                                const int* __restrict__ point_slot, Rec<A>* __restrict__ out) {
+    const int i = blockIdx.x;
+    const bool empty = seg_start[i] == seg_start[i + 1];
+    const A ri = R[i];
+    Rec<A> b = rec_none<A>();
+    for (int cl = threadIdx.x; cl < w; cl += blockDim.x) {
+        const int64_t c = col_begin + cl;
+        if (point_slot[c] >= 0) continue;
+        const A v = ri + (empty ? (A)0 : acc[(int64_t)i * w + cl]) + plus[cl];
+        Rec<A> r; r.v = v; r.slot = i; r.c = (int)c;
+        if (rec_less(r, b)) b = r;        // same slot: (v, c) order
+    }
+    b = block_min_rec(b);
+    if (threadIdx.x == 0) out[i] = b;
+}
+
+// The sequential phase of one FastPAM2 iteration as ONE cooperative kernel
+// (grid-wide syncs instead of ~6 launches per swap).  order[0..m) are the
+// improving slots sorted by (v_i, i) (host), best[i] = (v_i, i, c_i).
+// r = 0 applies best[order[0]] as is (it is FastPAM1's swap).  Every later
+// slot i: skipped if c_i became a medoid, else dTD(m_i, x_c_i) is recomputed
+// on the current cache in one pass over the objects,
+//    sum_o [nearest(o)=i](d_s - d_n) + [d<d_n](d - d_n)
+//        + [nearest(o)=i]([d<d_n](d_n - d_s) + [d_n<=d<d_s](d - d_s)),
+// and the swap is applied iff it still improves (reading R5).  Applying =
+// M[i] <- c, TD += dTD, MC[i] <- column c, incremental nearest/second update.
+// Applied swaps are appended to trace[] (slot, c, dTD).
+template <typename T, typename A>
+__global__ void __launch_bounds__(256)
+k_fp2_sequential(const T* __restrict__ D, int64_t ld, int n, int k, const int* __restrict__ order, int m,
+                 const Rec<A>* __restrict__ best, int* __restrict__ M, int* __restrict__ point_slot,
+                 T* __restrict__ MC, int* __restrict__ near, int* __restrict__ sec, T* __restrict__ dn,
+                 T* __restrict__ ds, T* __restrict__ colbuf, A* __restrict__ td, A* __restrict__ partials,
+                 Decision<A>* __restrict__ dec, Rec<A>* __restrict__ trace, int trace_cap) {
+    namespace cg = cooperative_groups;
+    cg::grid_group grid = cg::this_grid();
+    __shared__ A sred[8];
+    __shared__ int s_apply;
+    const int nth = gridDim.x * blockDim.x;
+    const int tid = blockIdx.x * blockDim.x + threadIdx.x;
+    for (int r = 0; r < m; ++r) {
+        const int i = order[r];
+        const int c = best[i].c;
+        // point_slot and td change only in phase 2 of a step (block 0), after
+        // every block has read them here: all blocks take the same decisions.
+        const bool skip = (r > 0) && (point_slot[c] >= 0);
+        const A tdv = __ldcg(td);
+        if (skip) continue;
+        // phase 1: gather column c, partial sums of dTD(m_i, x_c)
+        A part = 0;
+        for (int o = tid; o < n; o += nth) {
+            const T x = D[(int64_t)o * ld + c];
+            colbuf[o] = x;
+            if (r > 0) {
+                const T a = dn[o], b = ds[o];
+                const bool mine = near[o] == i;
+                A f = 0;
+                if (x < a) f += (A)x - (A)a;
+                if (mine) {
+                    f += (A)b - (A)a;
+                    if (x < a) f += (A)a - (A)b;
+                    else if (x < b) f += (A)x - (A)b;
+                }
+                part += f;
+            }
+        }
+        if (r > 0) {
+#pragma unroll
+            for (int x = 16; x >= 1; x >>= 1) part += __shfl_xor_sync(FULL, part, x);
+            if ((threadIdx.x & 31) == 0) sred[threadIdx.x >> 5] = part;
+            __syncthreads();
+            if (threadIdx.x == 0) {
+                A t = 0;
+                for (int q = 0; q < (int)(blockDim.x >> 5); ++q) t += sred[q];
+                partials[blockIdx.x] = t;
+            }
+        }
+        grid.sync();
+        // phase 2: every block reduces the partials in the same order -> same decision
+        if (threadIdx.x == 0) {
+            A v;
+            if (r == 0) {
+                v = best[i].v;
+            } else {
+                v = 0;
+                for (int b = 0; b < (int)gridDim.x; ++b) v += __ldcg(&partials[b]);
+            }
+            bool ok;
+            if (std::is_same<A, double>::value) ok = (double)v < -1e-12 * fabs((double)tdv);
+            else ok = v < 0;
+            s_apply = ok ? 1 : 0;
+            if (ok && blockIdx.x == 0) {
+                const int old = M[i];
+                M[i] = c;
+                point_slot[old] = -1;
+                point_slot[c] = i;
+                *td = tdv + v;
+                const int sw = dec->swaps;
+                if (sw < trace_cap) { Rec<A> t; t.v = v; t.slot = i; t.c = c; trace[sw] = t; }
+                dec->swaps = sw + 1;
+                dec->apply = 1;
+                dec->slot = i;
+                dec->c = c;
+                dec->dtd = v;
+                dec->old_m = old;
+            }
+        }
+        __syncthreads();
+        if (s_apply) {
+            // phase 3: MC[i] <- column c, incremental nearest/second update (own objects only)
+            for (int o = tid; o < n; o += nth) {
+                const T x = colbuf[o];
+                MC[(int64_t)i * n + o] = x;
+                int j1 = near[o], j2 = sec[o];
+                if (j1 == i || j2 == i) {
+                    T a0 = MC[o], b0 = MC[(int64_t)n + o];
+                    T d1, d2;
+                    if (b0 < a0) { d1 = b0; j1 = 1; d2 = a0; j2 = 0; } else { d1 = a0; j1 = 0; d2 = b0; j2 = 1; }
+                    for (int j = 2; j < k; ++j) {
+                        const T d = (j == i) ? x : MC[(int64_t)j * n + o];
+                        if (d < d1) { d2 = d1; j2 = j1; d1 = d; j1 = j; }
+                        else if (d < d2) { d2 = d; j2 = j; }
+                    }
+                    near[o] = j1; sec[o] = j2; dn[o] = d1; ds[o] = d2;
+                } else {
+                    const T d1 = dn[o], d2 = ds[o];
+                    if (x < d1 || (x == d1 && i < j1)) { near[o] = i; dn[o] = x; sec[o] = j1; ds[o] = d1; }
+                    else if (x < d2 || (x == d2 && i < j2)) { sec[o] = i; ds[o] = x; }
+                }
+            }
+        }
+        grid.sync();
     }
 }
 

@@ -9,6 +9,8 @@
 #include <cstring>
 #include <memory>
 #include <string>
+#include <algorithm>
+#include <cmath>
 #include <type_traits>
 #include <vector>
 
@@ -102,6 +104,7 @@ struct ImplBase {
     virtual km_status build_eval(int32_t step) = 0;
     virtual km_status build_select(const int64_t* rcb, int32_t* cand, int32_t* owner, void* gain) = 0;
     virtual km_status build_apply(int32_t step) = 0;
+    virtual km_status last_swaps_out(int32_t* slots, int32_t* cands, void* dtds, int32_t cap, int32_t* count) = 0;
     bool profiling = false;
     double prof_ms = 0.0;
     int64_t prof_launches = 0;
@@ -153,6 +156,18 @@ struct Impl : ImplBase {
     A *td = nullptr, *td_partials = nullptr;
     Dec* dec = nullptr;
     Dec* h_dec = nullptr;           // pinned mirror
+    // FastPAM2 state (allocated on first use)
+    A* fp2_acc = nullptr;           // [k][w] complete acc_c[i]
+    A* fp2_plus = nullptr;          // [w]    dTD^{+x_c}
+    Rec* fp2_best = nullptr;        // [k]    per-slot (v_i, i, c_i)
+    int* fp2_order = nullptr;       // [k]
+    A* fp2_partials = nullptr;      // cooperative-kernel block partials
+    int fp2_blocks = 0;
+    std::vector<Rec> h_best;
+    // swaps of the last iteration (slot, c, dTD)
+    Rec* trace = nullptr;
+    int trace_cap = 0;
+    std::vector<Rec> last_swaps;
     cudaEvent_t ev0 = nullptr, ev1 = nullptr;
 
     ~Impl() override {
@@ -181,23 +196,25 @@ struct Impl : ImplBase {
         w = (int)(c1 - c0);
         sharded = !(c0 == 0 && c1 == n);
         const char* ev = getenv("KM_STREAM");
-        stream_kind = 6;                                        // TMA ring + compacted hits (default)
-        if (ev && strcmp(ev, "tma") == 0) stream_kind = 1;
+        // Stream kernel selection (KM_STREAM overrides for
+        // measurements): tma = TMA bulk-copy ring (default), ldg = register
+        // pipelined loads, wtma = warp-autonomous rings, cmp = compacted hits.
+        stream_kind = 1;
+        if (ev && strcmp(ev, "cmp") == 0) stream_kind = 6;
         if (ev && strcmp(ev, "ldg") == 0) stream_kind = 0;
         if (ev && strcmp(ev, "wtma") == 0) stream_kind = 2;
-        if (ev && strcmp(ev, "wtma1") == 0) stream_kind = 3;
-        if (ev && strcmp(ev, "wtma1d") == 0) stream_kind = 4;
-        if (ev && strcmp(ev, "wtma2") == 0) stream_kind = 5;
+
+
         use_tma = stream_kind == 1;
         const char* dbg = getenv("KM_DEBUG_NATURAL_ORDER");   // perf experiment only: wrong results
         debug_natural = (dbg && dbg[0] == '1') ? 1 : 0;
         const char* dnc = getenv("KM_DEBUG_NOCOMPUTE");        // perf experiment only: wrong results
         debug_nocompute = (dnc && dnc[0] == '1') ? 1 : 0;
         P = stream_kind == 6 ? choose_parts(n, w, CMP_NC * 128, 2)
+
             : stream_kind == 1 ? choose_parts(n, w, TMA_COLS, TMA_RESIDENT)
             : stream_kind == 2 ? choose_parts(n, w, WT_COLS, WT_RESIDENT)
-            : stream_kind == 3 || stream_kind == 4 ? choose_parts(n, w, 128, 16)
-            : stream_kind == 5 ? choose_parts(n, w, 256, 8)
+
                                : choose_parts(n, w, STREAM_COLS, RESIDENT_CTAS);
         Pb = choose_parts(n, w, STREAM_COLS, RESIDENT_CTAS);
         wpad = (int)((w + 3) / 4 * 4);
@@ -325,7 +342,7 @@ struct Impl : ImplBase {
     km_status eval_local() {
         KM_TRY(prep());
         if (profiling) KM_CK(cudaEventRecord(ev0, st));
-        if (stream_kind == 6) {
+        if (stream_kind == 6) {   // compacted hits
             using C = km::CmpCfg<T, A, CMP_NC, CMP_RB, CMP_S>;
             auto kern = km::k_swap_stream_cmp<T, A, CMP_NC, CMP_RB, CMP_S>;
             if (!cmp_attr_set) {
@@ -337,12 +354,6 @@ struct Impl : ImplBase {
                                                   o_islot);
         } else if (stream_kind == 2) {
             KM_TRY((launch_wtma<WT_NW, WT_RB, WT_S>()));
-        } else if (stream_kind == 3) {
-            KM_TRY((launch_wtma<1, 4, 6>()));
-        } else if (stream_kind == 4) {
-            KM_TRY((launch_wtma<1, 4, 10>()));
-        } else if (stream_kind == 5) {
-            KM_TRY((launch_wtma<2, 4, 8>()));
         } else if (use_tma) {
             using C = km::TmaCfg<T, TMA_NC, TMA_RB, TMA_S>;
             auto kern = km::k_swap_stream_tma<T, A, TMA_NC, TMA_RB, TMA_S>;
@@ -352,7 +363,7 @@ struct Impl : ImplBase {
             }
             dim3 g((unsigned)cdiv(w, C::COLS), P);
             kern<<<g, C::THREADS, C::SMEM, st>>>(D, ld, w, wpad, (int)n, P, ri, R, o_plus, o_head, o_tail, o_imin,
-                                                  o_islot, debug_nocompute);
+                                                  o_islot, debug_nocompute, nullptr);
         } else {
             dim3 g((unsigned)cdiv(w, STREAM_COLS), P);
             km::k_swap_stream<T, A, STREAM_WARPS, STREAM_U><<<g, STREAM_WARPS * 32, 0, st>>>(
@@ -364,6 +375,17 @@ struct Impl : ImplBase {
                                                       tail_slot, R, empty_slot, point_slot, cand_v, cand_slot,
                                                       partials, counters, rec_local);
         KM_CKL();
+        return KM_OK;
+    }
+
+    template <int NC, int RB, int S, int MINB>
+    km_status launch_tma() {
+        using C = km::TmaCfg<T, NC, RB, S>;
+        auto kern = km::k_swap_stream_tma<T, A, NC, RB, S, MINB>;
+        KM_CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM));
+        dim3 g((unsigned)cdiv(w, C::COLS), P);
+        kern<<<g, C::THREADS, C::SMEM, st>>>(D, ld, w, wpad, (int)n, P, ri, R, o_plus, o_head, o_tail, o_imin, o_islot,
+                                              debug_nocompute, nullptr);
         return KM_OK;
     }
 
@@ -404,13 +426,119 @@ struct Impl : ImplBase {
         KM_CKL();
         KM_TRY(apply_local());
         KM_TRY(sync_dec());
+        last_swaps.clear();
+        if (h_dec->apply) {
+            Rec r; r.v = h_dec->dtd; r.slot = h_dec->slot; r.c = h_dec->c;
+            last_swaps.push_back(r);
+        }
         if (swaps) *swaps = h_dec->apply;
         copy_td(td_out);
         return h_dec->apply ? KM_OK : KM_CONVERGED;
     }
 
-    km_status swap_iter_fp2(int32_t*, void*) {
-        return fail(KM_EINVAL, "FastPAM2 is not implemented yet");
+    km_status fp2_alloc() {
+        if (fp2_acc) return KM_OK;
+        KM_TRY(alloc(&fp2_acc, (size_t)k * w));
+        KM_TRY(alloc(&fp2_plus, w));
+        KM_TRY(alloc(&fp2_best, k));
+        KM_TRY(alloc(&fp2_order, k));
+        int dev = 0, per_sm = 0, nsm = 0;
+        KM_CK(cudaGetDevice(&dev));
+        KM_CK(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
+        KM_CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, km::k_fp2_sequential<T, A>, 256, 0));
+        fp2_blocks = (int)std::min<int64_t>((int64_t)nsm * std::max(per_sm, 1), std::max<int64_t>(1, cdiv(n, 256)));
+        KM_TRY(alloc(&fp2_partials, fp2_blocks));
+        trace_cap = k;
+        KM_TRY(alloc(&trace, trace_cap));
+        h_best.resize(k);
+        return KM_OK;
+    }
+
+    // One FastPAM2 iteration (reading R6): per-slot best candidates from one
+    // stream pass, then the sequential multi-swap phase on the device.
+    km_status swap_iter_fp2(int32_t* swaps_out, void* td_out) {
+        KM_TRY(fp2_alloc());
+        KM_TRY(prep());
+        using C = km::TmaCfg<T, TMA_NC, TMA_RB, TMA_S>;
+        auto kern = km::k_swap_stream_tma<T, A, TMA_NC, TMA_RB, TMA_S>;
+        if (!tma_attr_set) {
+            KM_CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM));
+            tma_attr_set = true;
+        }
+        const int Pt = choose_parts(n, w, TMA_COLS, TMA_RESIDENT);
+        if (Pt != P) return fail(KM_EINVAL, "internal: FastPAM2 needs the TMA stream partition");
+        if (profiling) KM_CK(cudaEventRecord(ev0, st));
+        dim3 g((unsigned)cdiv(w, C::COLS), P);
+        kern<<<g, C::THREADS, C::SMEM, st>>>(D, ld, w, wpad, (int)n, P, ri, R, o_plus, o_head, o_tail, o_imin,
+                                              o_islot, 0, fp2_acc);
+        KM_CKL();
+        if (profiling) { KM_CK(cudaEventRecord(ev1, st)); pending_prof = true; }
+        km::k_swap_combine<A><<<ncomb, 256, 0, st>>>(w, c0, P, o_plus, o_head, o_tail, o_imin, o_islot, head_slot,
+                                                      tail_slot, R, empty_slot, point_slot, cand_v, cand_slot,
+                                                      partials, counters, rec_local, fp2_acc, fp2_plus);
+        KM_CKL();
+        km::k_fp2_slot_best<A><<<k, 256, 0, st>>>(w, c0, fp2_acc, fp2_plus, R, seg_start, point_slot, fp2_best);
+        KM_CKL();
+        A tdh;
+        KM_CK(cudaMemcpyAsync(h_best.data(), fp2_best, k * sizeof(Rec), cudaMemcpyDeviceToHost, st));
+        KM_CK(cudaMemcpyAsync(&tdh, td, sizeof(A), cudaMemcpyDeviceToHost, st));
+        KM_CK(cudaMemcpyAsync(h_dec, dec, sizeof(Dec), cudaMemcpyDeviceToHost, st));
+        KM_CK(cudaStreamSynchronize(st));
+        if (profiling && pending_prof) {
+            float ms = 0.f;
+            KM_CK(cudaEventElapsedTime(&ms, ev0, ev1));
+            prof_ms += ms; prof_launches += 1; pending_prof = false;
+        }
+        // steps 4-5: improving slots ordered by (v_i, i)
+        std::vector<int> order;
+        for (int i = 0; i < k; ++i) {
+            const Rec& b = h_best[i];
+            if (b.slot == INT_MAX) continue;
+            const bool imp = km::Acc<T>::is_float ? ((double)b.v < -1e-12 * fabs((double)tdh)) : (b.v < 0);
+            if (imp) order.push_back(i);
+        }
+        std::stable_sort(order.begin(), order.end(), [&](int a, int b) {
+            return h_best[a].v < h_best[b].v || (h_best[a].v == h_best[b].v && a < b);
+        });
+        Dec hd = *h_dec;
+        hd.iters += 1;
+        hd.apply = 0;
+        const int swaps0 = hd.swaps;
+        last_swaps.clear();
+        if (order.empty()) {
+            KM_CK(cudaMemcpyAsync(dec, &hd, sizeof(Dec), cudaMemcpyHostToDevice, st));
+            KM_CK(cudaStreamSynchronize(st));
+            if (swaps_out) *swaps_out = 0;
+            copy_td(td_out);
+            return KM_CONVERGED;
+        }
+        hd.swaps = 0;                       // the kernel counts this iteration's swaps from 0
+        KM_CK(cudaMemcpyAsync(dec, &hd, sizeof(Dec), cudaMemcpyHostToDevice, st));
+        KM_CK(cudaMemcpyAsync(fp2_order, order.data(), order.size() * sizeof(int), cudaMemcpyHostToDevice, st));
+        int m = (int)order.size();
+        const T* Dp = D; int64_t ldv = ld; int nn = (int)n; int kk = k;
+        int* Mp = M; int* psp = point_slot; T* MCp = MC; int* nr = near; int* sc = sec; T* dnp = dn; T* dsp = ds;
+        T* cb = colbuf; A* tdp = td; A* pp = fp2_partials; Dec* dp = dec; Rec* tr = trace; int tc = trace_cap;
+        int* op = fp2_order; Rec* bp = fp2_best;
+        void* args[] = {&Dp, &ldv, &nn, &kk, &op, &m, &bp, &Mp, &psp, &MCp, &nr, &sc, &dnp, &dsp, &cb, &tdp, &pp,
+                        &dp, &tr, &tc};
+        KM_CK(cudaLaunchCooperativeKernel((void*)km::k_fp2_sequential<T, A>, dim3(fp2_blocks), dim3(256), args, 0,
+                                          st));
+        ++launches;
+        KM_CK(cudaMemcpyAsync(h_dec, dec, sizeof(Dec), cudaMemcpyDeviceToHost, st));
+        KM_CK(cudaStreamSynchronize(st));
+        const int done = h_dec->swaps;
+        last_swaps.resize(std::min(done, trace_cap));
+        if (!last_swaps.empty())
+            KM_CK(cudaMemcpy(last_swaps.data(), trace, last_swaps.size() * sizeof(Rec), cudaMemcpyDeviceToHost));
+        hd = *h_dec;
+        hd.swaps = swaps0 + done;
+        KM_CK(cudaMemcpyAsync(dec, &hd, sizeof(Dec), cudaMemcpyHostToDevice, st));
+        KM_CK(cudaStreamSynchronize(st));
+        *h_dec = hd;
+        if (swaps_out) *swaps_out = done;
+        copy_td(td_out);
+        return KM_OK;
     }
 
     // ---- BUILD ---------------------------------------------------------------
@@ -458,6 +586,17 @@ struct Impl : ImplBase {
         KM_CK(cudaStreamSynchronize(st));
         if (M_out) KM_CK(cudaMemcpy(M_out, M, k * sizeof(int32_t), cudaMemcpyDeviceToHost));
         copy_td(td_out);
+        return KM_OK;
+    }
+
+    km_status last_swaps_out(int32_t* slots, int32_t* cands, void* dtds, int32_t cap, int32_t* count) override {
+        const int m = (int)last_swaps.size();
+        if (count) *count = m;
+        for (int j = 0; j < m && j < cap; ++j) {
+            if (slots) slots[j] = last_swaps[j].slot;
+            if (cands) cands[j] = last_swaps[j].c;
+            if (dtds) memcpy((char*)dtds + j * sizeof(A), &last_swaps[j].v, sizeof(A));
+        }
         return KM_OK;
     }
 
@@ -722,6 +861,12 @@ km_status kmedoids_get_cache(km_handle* h, int32_t* nearest_out, int32_t* second
 km_status kmedoids_eval_candidates(km_handle* h, void* dtd_out, int32_t* slot_out) {
     KM_H();
     return h->impl->eval_candidates(dtd_out, slot_out);
+}
+
+km_status kmedoids_last_swaps(km_handle* h, int32_t* slots_out, int32_t* cands_out, void* dtds_out, int32_t cap,
+                              int32_t* count_out) {
+    KM_H();
+    return h->impl->last_swaps_out(slots_out, cands_out, dtds_out, cap, count_out);
 }
 
 km_status kmedoids_set_profiling(km_handle* h, int32_t enable) {

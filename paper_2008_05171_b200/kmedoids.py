@@ -64,6 +64,7 @@ def load_library() -> ctypes.CDLL:
         "kmedoids_get_cache": [vp, vp, vp, vp, vp],
         "kmedoids_eval_candidates": [vp, vp, vp],
         "kmedoids_set_profiling": [vp, i32],
+        "kmedoids_last_swaps": [vp, vp, vp, vp, i32, vp],
         "kmedoids_stream_time": [vp, vp, vp, i32],
         "kmedoids_launch_count": [vp, vp],
         "kmedoids_shard_exchange": [vp, i32, ctypes.POINTER(_Exchange)],
@@ -206,6 +207,15 @@ class KMedoids:
         v = np.zeros(w, self.acc); s = np.zeros(w, np.int32)
         _check(load_library().kmedoids_eval_candidates(self.h, _p(v), _p(s)))
         return v, s
+
+    def last_swaps(self):
+        """[(slot, candidate, dTD)] applied by the last swap_iter call."""
+        cnt = np.zeros(1, np.int32)
+        _check(load_library().kmedoids_last_swaps(self.h, None, None, None, 0, _p(cnt)))
+        m = int(cnt[0])
+        sl = np.zeros(max(m, 1), np.int32); cd = np.zeros(max(m, 1), np.int32); dv = np.zeros(max(m, 1), self.acc)
+        _check(load_library().kmedoids_last_swaps(self.h, _p(sl), _p(cd), _p(dv), m, _p(cnt)))
+        return [(int(sl[j]), int(cd[j]), dv[j].item()) for j in range(m)]
 
     def set_profiling(self, on=True):
         _check(load_library().kmedoids_set_profiling(self.h, int(on)))

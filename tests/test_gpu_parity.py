@@ -281,3 +281,81 @@ def test_float_per_candidate_values():
         srt = np.sort(full)
         if srt[1] - srt[0] > 1e-9 * td:
             assert s[x] == int(np.argmin(full))
+
+
+# ---------------- FastPAM2 (reading R6) ----------------
+
+def gpu_swaps(km, variant, max_iter=2000):
+    """Run SWAP iterations to convergence; return the full swap trace."""
+    trace = []
+    for _ in range(max_iter):
+        conv, swaps, td = km.swap_iter(variant)
+        got = km.last_swaps()
+        assert len(got) == swaps
+        trace += got
+        if conv:
+            break
+    return trace
+
+
+@pytest.mark.parametrize("seed", range(10))
+def test_fastpam2_int_trace_exact(seed):
+    rng = np.random.default_rng(500 + seed)
+    n = int(rng.choice([9, 64, 257, 700]))
+    k = int(rng.integers(2, min(16, n - 1) + 1))
+    D = rand_int(rng, n, int(rng.choice([3, 40, 10000])), symmetric=bool(seed % 2))
+    M0 = rng.choice(n, size=k, replace=False).astype(np.int32)
+    ref = oracle.swap_run(D, M0, oracle.FASTPAM2)
+    km = KM(to_dev(D), n, k)
+    km.set_medoids(M0)
+    tr = gpu_swaps(km, "fastpam2")
+    assert [(i, c, int(v)) for i, c, v in tr] == [(i, c, int(v)) for i, c, v in ref.trace]
+    st = km.get_state()
+    assert st.medoids.tolist() == ref.medoids.tolist()
+    assert st.assignment.tolist() == ref.assignment.tolist()
+    assert st.td == ref.td and st.n_iter == ref.n_iter and st.n_swaps == ref.n_swaps
+    near, sec, dn, ds = km.get_cache()
+    c = oracle.assign(D, ref.medoids)
+    assert near.tolist() == c.nearest.tolist() and sec.tolist() == c.second.tolist()
+
+
+def test_fastpam1_last_swaps_trace():
+    rng = np.random.default_rng(42)
+    n, k = 300, 6
+    D = rand_int(rng, n, 500)
+    M0 = rng.choice(n, size=k, replace=False)
+    ref = oracle.swap_run(D, M0, oracle.FASTPAM1)
+    km = KM(to_dev(D), n, k)
+    km.set_medoids(M0)
+    tr = gpu_swaps(km, "fastpam1")
+    assert [(i, c, int(v)) for i, c, v in tr] == [(i, c, int(v)) for i, c, v in ref.trace]
+
+
+def test_fastpam2_float_c3_prefix():
+    """C3 recipe (oracle-sized prefix): FastPAM2 final TD within 1e-5 of the
+    oracle, every applied dTD exact up to fp64 rounding, final state a local
+    optimum (a GPU FastPAM1 pass finds nothing improving)."""
+    cfg = kmsynth.CONFIGS[3]
+    n, k = 1500, 30
+    X = kmsynth.make_points(cfg, n=n)
+    Dt = kmsynth.dist_cuda(X, cfg.metric)
+    D = kmsynth.as_numpy_D(Dt)[:, :n]
+    M0 = kmsynth.random_medoids(cfg, k=k, n=n)
+    ref = oracle.swap_run(D, M0, oracle.FASTPAM2)
+    km = KM(Dt, n, k)
+    km.set_medoids(M0)
+    M = list(M0)
+    for _ in range(500):
+        conv, swaps, td = km.swap_iter("fastpam2")
+        for (i, c, v) in km.last_swaps():
+            td_before = oracle.td(D, M)
+            M[i] = c
+            assert v == pytest.approx(oracle.td(D, M) - td_before, rel=1e-9, abs=1e-9 * td_before)
+        if conv:
+            break
+    st = km.get_state()
+    assert st.medoids.tolist() == M
+    assert st.td == pytest.approx(ref.td, rel=FTOL)
+    assert st.td == pytest.approx(oracle.td(D, M), rel=1e-12)
+    v, s = km.eval_candidates()
+    assert np.nanmin(np.where(s >= 0, v, np.inf)) >= -1e-9 * st.td
