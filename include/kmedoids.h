@@ -178,6 +178,8 @@ km_status kmedoids_shard_eval(km_handle* h);
  * or double*).  Returns KM_CONVERGED when nothing improves. */
 km_status kmedoids_shard_select(km_handle* h, const int64_t* rank_col_begin, int32_t* found, int32_t* slot,
                                 int32_t* cand, int32_t* owner, void* dtd);
+/* The owner of point `cand` (col_begin <= cand < col_end) copies column
+ * d(., x_cand) into the exchange column buffer (n elements). */
 km_status kmedoids_shard_pack_column(km_handle* h, int32_t cand);
 km_status kmedoids_shard_apply(km_handle* h);
 

@@ -136,6 +136,14 @@ __global__ void k_gather_decided_col(const T* __restrict__ D, int64_t ld, int n,
     if (colbuf) colbuf[o] = v;
 }
 
+// Sharded: column c (global index, local to this rank) -> colbuf[o] = d(x_o, x_c).
+template <typename T>
+__global__ void k_gather_col(const T* __restrict__ D, int64_t ld, int n, int64_t col_begin, int c,
+                             T* __restrict__ colbuf) {
+    const int o = blockIdx.x * blockDim.x + threadIdx.x;
+    if (o < n) colbuf[o] = D[(int64_t)o * ld + (c - col_begin)];
+}
+
 // Sharded: copy the broadcast column into MC[slot].
 template <typename T, typename A>
 __global__ void k_column_to_mc(const T* __restrict__ colbuf, int n, const Decision<A>* __restrict__ dec,

@@ -685,7 +685,7 @@ struct Impl : ImplBase {
     km_status shard_pack_column(int32_t cand) override {
         if (cand < c0 || cand >= c1) return fail(KM_ECOMM, "candidate %d is not in this rank's columns", cand);
         const int nb = (int)cdiv(n, 256);
-        km::k_gather_decided_col<T, A><<<nb, 256, 0, st>>>(D, ld, (int)n, c0, c1, dec, nullptr, colbuf);
+        km::k_gather_col<T><<<nb, 256, 0, st>>>(D, ld, (int)n, c0, cand, colbuf);
         KM_CKL();
         KM_CK(cudaStreamSynchronize(st));
         return KM_OK;

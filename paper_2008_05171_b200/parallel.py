@@ -1,0 +1,301 @@
+"""Column-sharded multi-GPU SWAP / BUILD.
+
+Rank r of R holds the column slab [cb[r], cb[r+1]) of the n x n matrix D
+(all n rows): its candidates are those columns.  Every rank keeps the full
+nearest/second cache and the k medoid columns MC (replicated), so after the
+one exchange per step every rank updates its own copy and no symmetry of D
+is needed.  One SWAP iteration (FastPAM1, Alg.3) is:
+
+  1. kmedoids_shard_eval      local stream over the slab -> 16-byte record (dTD, slot, c)
+  2. all-gather the R records (NCCL over NVLink; 16*R bytes)
+  3. kmedoids_shard_select    identical lexicographic min on every rank (reading R1)
+  4. owner of c*: kmedoids_shard_pack_column; broadcast the n-element column
+  5. kmedoids_shard_apply     M, TD and the nearest/second cache (identical on every rank)
+
+BUILD (Alg.1) uses the same gather / pack / broadcast pattern per step.
+
+The protocol is written once over ``handles`` (the shard handles this process
+drives) and a ``comm``:
+  * ``TorchComm``  one handle per process, torch.distributed (nccl on GPUs,
+                    gloo for the CPU tests of this host logic);
+  * ``LocalComm``  all R handles in one process (virtual ranks on one GPU,
+                    sequential, no kernels waiting on each other).
+The exchange buffers are whatever ``h.exchange_tensors(R)`` returns (device
+memory owned by the library handle for the CUDA path).
+"""
+from __future__ import annotations
+
+import os
+import time
+
+import numpy as np
+
+RECORD_BYTES = 16
+
+
+def column_bounds(n: int, world: int) -> np.ndarray:
+    """Contiguous column slabs: rank r owns [cb[r], cb[r+1]) (multiples of 4 except the last)."""
+    cb = np.zeros(world + 1, np.int64)
+    for r in range(1, world):
+        cb[r] = min(n, (r * n // world + 3) // 4 * 4)
+    cb[world] = n
+    if np.any(np.diff(cb) <= 0):
+        raise ValueError(f"n={n} too small for {world} ranks")
+    return cb
+
+
+def decode_records(raw: np.ndarray, acc_dtype) -> list:
+    """(R*16,) uint8 -> [(v, slot, c)] in rank order."""
+    R = raw.size // RECORD_BYTES
+    rec = raw.reshape(R, RECORD_BYTES)
+    v = rec[:, 0:8].copy().view(acc_dtype).ravel()
+    slot = rec[:, 8:12].copy().view(np.int32).ravel()
+    c = rec[:, 12:16].copy().view(np.int32).ravel()
+    return [(v[r].item(), int(slot[r]), int(c[r])) for r in range(R)]
+
+
+def lexmin_records(recs):
+    """Reading R1: the lexicographic minimum of (dTD, slot, candidate)."""
+    return min(recs, key=lambda t: (t[0], t[1], t[2]))
+
+
+class LocalComm:
+    """All ranks' handles in one process (virtual ranks)."""
+
+    def __init__(self, world: int):
+        self.world = world
+
+    def allgather_records(self, handles):
+        xs = [h.exchange_tensors(self.world) for h in handles]
+        cat = [x[0] for x in xs]
+        for (send, recv, col) in xs:
+            for r, s in enumerate(cat):
+                recv[r * RECORD_BYTES:(r + 1) * RECORD_BYTES].copy_(s)
+
+    def broadcast_column(self, handles, owner: int):
+        xs = [h.exchange_tensors(self.world) for h in handles]
+        src = xs[owner][2]
+        for r, (_, _, col) in enumerate(xs):
+            if r != owner:
+                col.copy_(src)
+
+    def max_over_ranks(self, x: float) -> float:
+        return x
+
+
+class TorchComm:
+    """One handle per process; torch.distributed collectives (nccl or gloo)."""
+
+    def __init__(self, group=None):
+        import torch.distributed as dist
+        self.dist = dist
+        self.group = group
+        self.world = dist.get_world_size(group)
+        self.rank = dist.get_rank(group)
+
+    def allgather_records(self, handles):
+        (h,) = handles
+        send, recv, _ = h.exchange_tensors(self.world)
+        self.dist.all_gather_into_tensor(recv, send, group=self.group)
+
+    def broadcast_column(self, handles, owner: int):
+        (h,) = handles
+        _, _, col = h.exchange_tensors(self.world)
+        self.dist.broadcast(col, src=owner, group=self.group)
+
+    def max_over_ranks(self, x: float) -> float:
+        import torch
+        dev = "cuda" if self.dist.get_backend(self.group) == "nccl" else "cpu"
+        t = torch.tensor([x], dtype=torch.float64, device=dev)
+        self.dist.all_reduce(t, op=self.dist.ReduceOp.MAX, group=self.group)
+        return float(t.item())
+
+
+# ---------------------------------------------------------------------------
+# the protocol (identical on every rank)
+# ---------------------------------------------------------------------------
+def set_medoids(handles, comm, cb, medoids, n: int):
+    """Gather the k medoid columns from their owners (k broadcasts) and set them."""
+    import torch
+    M = np.asarray(medoids, dtype=np.int64)
+    k = len(M)
+    cols = []
+    for h in handles:
+        _, _, col = h.exchange_tensors(comm.world)
+        cols.append(torch.empty((k, col.numel()), dtype=col.dtype, device=col.device))
+    for j, m in enumerate(M):
+        owner = int(np.searchsorted(cb, m, side="right") - 1)
+        for h in handles:
+            if h.rank == owner:
+                h.shard_pack_column(int(m))
+        comm.broadcast_column(handles, owner)
+        for h, buf in zip(handles, cols):
+            buf[j].copy_(h.exchange_tensors(comm.world)[2])
+    for h, buf in zip(handles, cols):
+        h.shard_set_medoids(M.astype(np.int32), buf)
+
+
+def swap_iter(handles, comm, cb):
+    """One sharded FastPAM1 SWAP iteration; returns (converged, (slot, c, dTD) or None)."""
+    for h in handles:
+        h.shard_eval()
+    comm.allgather_records(handles)
+    sel = [h.shard_select(cb) for h in handles]
+    found, slot, cand, owner, dtd = sel[0]
+    if any(s != sel[0] for s in sel):
+        raise RuntimeError(f"ranks disagree on the swap: {sel}")
+    if not found:
+        return True, None
+    for h in handles:
+        if h.rank == owner:
+            h.shard_pack_column(cand)
+    comm.broadcast_column(handles, owner)
+    for h in handles:
+        h.shard_apply()
+    return False, (slot, cand, dtd)
+
+
+def build(handles, comm, cb, k: int):
+    """Sharded PAM BUILD (Alg.1): k steps of local eval / gather / select / broadcast."""
+    chosen = []
+    for step in range(k):
+        for h in handles:
+            h.build_eval(step)
+        comm.allgather_records(handles)
+        sel = [h.build_select(cb) for h in handles]
+        cand, owner, gain = sel[0]
+        if any(s != sel[0] for s in sel):
+            raise RuntimeError(f"ranks disagree on the BUILD step: {sel}")
+        for h in handles:
+            if h.rank == owner:
+                h.shard_pack_column(cand)
+        comm.broadcast_column(handles, owner)
+        for h in handles:
+            h.build_apply(step)
+        chosen.append((cand, gain))
+    return chosen
+
+
+def run(handles, comm, cb, max_iter: int = 2000):
+    trace = []
+    it = 0
+    while it < max_iter:
+        it += 1
+        conv, sw = swap_iter(handles, comm, cb)
+        if conv:
+            return trace, it, True
+        trace.append(sw)
+    return trace, it, False
+
+
+# ---------------------------------------------------------------------------
+# CUDA shard handle: KMedoids on a column slab + exchange tensors
+# ---------------------------------------------------------------------------
+class _DevBytes:
+    def __init__(self, ptr: int, nbytes: int):
+        self.__cuda_array_interface__ = {"shape": (nbytes,), "typestr": "|u1", "data": (ptr, False),
+                                         "version": 3, "strides": None}
+
+
+class CudaShard:
+    """A KMedoids handle on columns [cb[rank], cb[rank+1]) of D."""
+
+    def __init__(self, D_slab, n: int, k: int, rank: int, cb, stream=None):
+        from .kmedoids import KMedoids
+        self.rank = rank
+        self.km = KMedoids(D_slab, n, k, int(cb[rank]), int(cb[rank + 1]), stream=stream)
+        self._x = None
+
+    def exchange_tensors(self, world: int):
+        import torch
+        if self._x is None:
+            x = self.km.shard_exchange(world)
+            dev = self.km.D.device
+            send = torch.as_tensor(_DevBytes(x.record_send, x.record_bytes), device=dev)
+            recv = torch.as_tensor(_DevBytes(x.record_recv, x.record_bytes * world), device=dev)
+            col = torch.as_tensor(_DevBytes(x.column, x.column_bytes), device=dev)
+            self._x = (send, recv, col)
+        return self._x
+
+    def __getattr__(self, name):       # shard_eval, shard_select, ... -> the handle
+        return getattr(self.km, name)
+
+
+# ---------------------------------------------------------------------------
+# bench entry (torchrun, one rank per GPU)
+# ---------------------------------------------------------------------------
+def bench_main(args):
+    import json
+
+    import torch
+    import torch.distributed as dist
+
+    import kmsynth
+
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    if not dist.is_initialized():
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    comm = TorchComm()
+    cfg = kmsynth.CONFIGS[args.config]
+    n, k = cfg.n, cfg.k
+    cb = column_bounds(n, world)
+    X = kmsynth.make_points(cfg)
+    Dt = kmsynth.dist_cuda(X, cfg.metric, int(cb[rank]), int(cb[rank + 1]))
+    stream = torch.cuda.current_stream()
+    h = CudaShard(Dt, n, k, rank, cb, stream=stream)
+    hs = [h]
+    torch.cuda.synchronize()
+    dist.barrier()
+    t0 = time.perf_counter()
+    if cfg.init == "build":
+        build(hs, comm, cb, k)
+    else:
+        set_medoids(hs, comm, cb, kmsynth.random_medoids(cfg), n)
+    torch.cuda.synchronize()
+    init_s = comm.max_over_ranks(time.perf_counter() - t0)
+    for _ in range(args.warmup):
+        swap_iter(hs, comm, cb)
+    h.km.set_profiling(True)
+    h.km.stream_time(reset=True)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    dist.barrier()
+    e0.record(stream)
+    for _ in range(args.steps):
+        swap_iter(hs, comm, cb)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    dist.barrier()
+    ms = comm.max_over_ranks(e0.elapsed_time(e1))
+    k1_ms, k1_n = h.km.stream_time(reset=True)
+    k1_ms = comm.max_over_ranks(k1_ms)
+    ms_step = ms / args.steps
+    pairs = k * (n - k)
+    value = pairs / (ms_step / 1e3)
+    if rank == 0:
+        peak = 6551.4
+        try:
+            peak = json.load(open(os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))),
+                                               "MEASURED_PEAKS.json")))["hbm_gbs"]
+        except Exception:
+            pass
+        slab_bytes = 4.0 * n * (int(cb[1]) - int(cb[0]))
+        k1_avg = k1_ms / max(1, k1_n)
+        ach = slab_bytes / (k1_avg / 1e3) / 1e9
+        line = {"metric": "swap_pair_evals_per_s", "value": value, "unit": "pair-evals/s", "n_gpus": world,
+                "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
+                "scaling": "strong", "vs_baseline": None,
+                "dtype": "f32->f64" if cfg.metric == kmsynth.L2_F32 else "u32->int64", "data": "synthetic",
+                "config": {"workload": f"{cfg.name} n={n} k={k} column-sharded over {world} GPUs",
+                           "n": n, "k": k, "variant": "fastpam1", "parallelism": f"column-shard x{world}"},
+                "s_per_iteration": ms_step / 1e3,
+                "roofline": {"bound": "hbm", "achieved": ach, "peak": peak, "unit": "GB/s", "frac": ach / peak,
+                             "traffic": None, "kernel": "k_swap_stream (rank 0 slab)", "kernel_ms": k1_avg},
+                "init_s": init_s, "e2e": None, "cpu_baseline": None,
+                "gpu_launches": h.km.launch_count()}
+        print(json.dumps(line), flush=True)
+    dist.barrier()
+    dist.destroy_process_group()

@@ -1,0 +1,201 @@
+"""Host logic of the column-sharded path (paper_2008_05171_b200.parallel) on
+the CPU: world_size-2 torch.distributed over gloo, with a mock shard whose
+per-rank arithmetic comes from the oracle.  The real collectives, the
+protocol order, the 16-byte record format and the column broadcast are the
+product code; the result must equal the single-process oracle run exactly."""
+import multiprocessing as mp
+import os
+import socket
+
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+
+import oracle  # noqa: E402
+from paper_2008_05171_b200 import parallel  # noqa: E402
+
+
+def rand_int(rng, n, hi):
+    A = rng.integers(0, hi, size=(n, n)).astype(np.uint32)
+    A = np.triu(A, 1)
+    A = A + A.T
+    np.fill_diagonal(A, 0)
+    return A
+
+
+class MockShard:
+    """Mirrors the CudaShard phase API on the CPU (int64 records)."""
+
+    def __init__(self, D, rank, cb, k):
+        self.D, self.rank, self.cb, self.k = D, rank, cb, k
+        self.n = D.shape[0]
+        self.c0, self.c1 = int(cb[rank]), int(cb[rank + 1])
+        self._x = None
+        self.exchange_tensors(len(cb) - 1)
+        self.M = None
+        self.td = 0
+
+    def exchange_tensors(self, world):
+        if self._x is None:
+            self._x = (torch.zeros(16, dtype=torch.uint8), torch.zeros(16 * world, dtype=torch.uint8),
+                       torch.zeros(4 * self.n, dtype=torch.uint8))
+        return self._x
+
+    def _write(self, v, slot, c):
+        rec = np.zeros(16, np.uint8)
+        rec[0:8] = np.array([v], np.int64).view(np.uint8)
+        rec[8:12] = np.array([slot], np.int32).view(np.uint8)
+        rec[12:16] = np.array([c], np.int32).view(np.uint8)
+        self._x[0].copy_(torch.from_numpy(rec))
+
+    def _recs(self):
+        return parallel.decode_records(self._x[1].numpy(), np.int64)
+
+    def _col(self):
+        return self._x[2].numpy().view(np.uint32)
+
+    # --- SWAP ---
+    def shard_set_medoids(self, M, cols):
+        self.M = [int(m) for m in M]
+        self.MC = cols.numpy().view(np.uint32).reshape(self.k, self.n).copy()
+        self.cache = oracle.assign_cols(self.MC)
+        self.td = int(self.cache.dn.sum())
+
+    def shard_pack_column(self, c):
+        assert self.c0 <= c < self.c1
+        self._col()[:] = self.D[:, c]
+
+    def shard_eval(self):
+        R = oracle.removal_loss(self.cache, self.k)
+        best = (np.iinfo(np.int64).max, 2**31 - 1, 2**31 - 1)
+        for c in range(self.c0, self.c1):
+            if c in self.M:
+                continue
+            vec, plus = oracle.fastpam1_candidate_col(self.D[:, c], self.cache, R)
+            i = int(np.argmin(vec))
+            best = min(best, (int(vec[i] + plus), i, c))
+        self._write(*best)
+
+    def shard_select(self, cb):
+        v, slot, c = parallel.lexmin_records(self._recs())
+        found = slot != 2**31 - 1 and v < 0
+        owner = int(np.searchsorted(cb, c, side="right") - 1) if found else -1
+        if found:
+            self.M[slot] = c
+            self.td += v
+            self._pending = slot
+        return found, slot, c, owner, v
+
+    def shard_apply(self):
+        self.MC[self._pending] = self._col()
+        self.cache = oracle.assign_cols(self.MC)
+
+    # --- BUILD ---
+    def build_eval(self, step):
+        if step == 0:
+            self.M = []
+            self.dnear = None
+        best = (np.iinfo(np.int64).max, 0, 2**31 - 1)
+        for c in range(self.c0, self.c1):
+            if c in self.M:
+                continue
+            col = self.D[:, c].astype(np.int64)
+            if step == 0:
+                g = int(col.sum() - col[c])
+            else:
+                d = col - self.dnear
+                g = int(np.minimum(d, 0).sum())
+            best = min(best, (g, 0, c))
+        self._write(*best)
+
+    def build_select(self, cb):
+        g, _, c = parallel.lexmin_records(self._recs())
+        owner = int(np.searchsorted(cb, c, side="right") - 1)
+        self._pending = c
+        self._gain = g
+        return c, owner, g
+
+    def build_apply(self, step):
+        col = self._col().astype(np.int64)
+        self.M.append(self._pending)
+        if step == 0:
+            self.dnear = col.copy()
+        else:
+            self.dnear = np.minimum(self.dnear, col)
+        self.dnear[self.M] = 0
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _worker(rank, world, port, seed, q):
+    import torch.distributed as dist
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        rng = np.random.default_rng(seed)
+        n, k = 57, 4
+        D = rand_int(rng, n, 300)
+        cb = parallel.column_bounds(n, world)
+        comm = parallel.TorchComm()
+        h = MockShard(D, rank, cb, k)
+        chosen = parallel.build([h], comm, cb, k)
+        M = [c for c, _ in chosen]
+        parallel.set_medoids([h], comm, cb, M, n)
+        trace, iters, conv = parallel.run([h], comm, cb)
+        q.put((rank, M, trace, iters, conv, h.M, h.td))
+    except Exception as e:  # report instead of hanging the parent
+        q.put((rank, "error", repr(e), 0, 0, 0, 0))
+        raise
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("seed", [0, 1])
+def test_gloo_world2_sharded_protocol_equals_oracle(seed):
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    ps = [ctx.Process(target=_worker, args=(r, 2, port, seed, q)) for r in range(2)]
+    for p in ps:
+        p.start()
+    out = [q.get(timeout=240) for _ in ps]
+    for p in ps:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    out.sort(key=lambda t: t[0])
+    assert all(t[1] != "error" for t in out), out
+    rng = np.random.default_rng(seed)
+    D = rand_int(rng, 57, 300)
+    Mb, _, _ = oracle.build_init(D, 4)
+    ref = oracle.swap_run(D, Mb, oracle.FASTPAM1)
+    for (rank, M, trace, iters, conv, Mf, td) in out:
+        assert M == Mb.tolist()
+        assert [(s, c, int(v)) for s, c, v in trace] == [(s, c, int(v)) for s, c, v in ref.trace]
+        assert iters == ref.n_iter and conv
+        assert Mf == ref.medoids.tolist() and td == ref.td
+
+
+def test_column_bounds_and_records():
+    cb = parallel.column_bounds(50000, 8)
+    assert cb[0] == 0 and cb[-1] == 50000 and all(int(x) % 4 == 0 for x in cb[:-1])
+    assert np.all(np.diff(cb) > 0)
+    with pytest.raises(ValueError):
+        parallel.column_bounds(3, 8)
+    raw = np.zeros(32, np.uint8)
+    raw[0:8] = np.array([-5], np.int64).view(np.uint8)
+    raw[8:12] = np.array([2], np.int32).view(np.uint8)
+    raw[12:16] = np.array([40], np.int32).view(np.uint8)
+    raw[16:24] = np.array([-5], np.int64).view(np.uint8)
+    raw[24:28] = np.array([1], np.int32).view(np.uint8)
+    raw[28:32] = np.array([99], np.int32).view(np.uint8)
+    recs = parallel.decode_records(raw, np.int64)
+    assert recs == [(-5, 2, 40), (-5, 1, 99)]
+    assert parallel.lexmin_records(recs) == (-5, 1, 99)     # smaller slot wins (reading R1)
