@@ -120,6 +120,21 @@ class ClockSampler:
                 "source": "nvml" if self._nvml is not None else "nvidia-smi"}
 
 
+def committed_traffic(tag):
+    """dram__bytes_read+write per launch of the stream kernel from the committed
+    `ncu --set full` capture (profiles/r*_traffic.json), if one matches the workload."""
+    import glob
+    best = None
+    for p in sorted(glob.glob(os.path.join(ROOT, "profiles", "r*_traffic.json"))):
+        try:
+            d = json.load(open(p))
+        except Exception:
+            continue
+        if tag in d:
+            best = d[tag]
+    return best
+
+
 def host_info():
     cores = len(os.sched_getaffinity(0))
     model = ""
@@ -315,7 +330,9 @@ def run_ours(args):
                    "l2": f"inputs larger than L2 ({4 * n * n / 1e9:.1f} GB D vs 126 MB L2), no flush needed"},
         "s_per_iteration": ms_step / 1e3,
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
-                     "traffic": None, "kernel": "k_swap_stream_tma", "kernel_ms": k1_avg,
+                     "traffic": (committed_traffic(cfg.name) or {}).get("traffic_bytes"),
+                     "traffic_source": (committed_traffic(cfg.name) or {}).get("source"),
+                     "kernel": "k_swap_stream_tma", "kernel_ms": k1_avg,
                      "alg_bytes_per_launch": alg_bytes, "peak_kind": peak_kind},
         "stream_share_of_step": k1_ms / total_ms,
         "gpu_launches": launches,
