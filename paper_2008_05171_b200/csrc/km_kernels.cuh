@@ -598,13 +598,15 @@ __device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
 __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
     asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(sa(bar)) : "memory");
 }
+// try_wait with a suspend-time hint: the warp sleeps until the phase
+// completes (or the hint expires) instead of spinning through issue slots.
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
     asm volatile(
         "{\n\t.reg .pred P;\n"
         "KM_WAIT_%=:\n\t"
-        "mbarrier.try_wait.parity.shared::cta.b64 P, [%0], %1;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 P, [%0], %1, %2;\n\t"
         "@!P bra KM_WAIT_%=;\n}" ::"r"(sa(bar)),
-        "r"(parity)
+        "r"(parity), "r"(0x989680u)
         : "memory");
 }
 __device__ __forceinline__ uint64_t policy_evict_first() {
@@ -1108,6 +1110,461 @@ k_swap_stream_cmp(const T* __restrict__ D, int64_t ld, int w, int wpad, int n, i
             out_plus[base + c] = accp[cl0 + j];
             out_head[base + c] = head[j];
             out_tail[base + c] = tail[j];
+            out_imin[base + c] = imin[j];
+            out_islot[base + c] = islot[j];
+        }
+    }
+}
+
+// ---------------------------------------------------------------------------
+// a3, TMA ring + per-warp hit queues (k_swap_stream_tmaq).
+//
+// Producer and ring as in k_swap_stream_tma.  The (d < d_s) hits of a stage
+// concentrate on the few candidate columns near the current slot's cluster,
+// i.e. on one or two warps of the CTA; with register accumulators such a
+// warp executes every hit column's fp64 update for all 32 lanes (SIMT
+// efficiency ~1/32) and the shared ring then advances at its pace.  Here each
+// warp compacts its hit columns of the stage (one entry = column + row mask)
+// into a warp-private queue and processes the queue lane-parallel, updating
+// per-column partial sums in shared memory (one owner per column and stage,
+// rows in order: deterministic).  Heavy and light warps now cost about the
+// same; no barrier couples the warps beyond the ring itself.
+// ---------------------------------------------------------------------------
+template <typename T, typename A, int NC, int RB, int S>
+struct TmaqCfg {
+    static constexpr int COLS = NC * 128;
+    static constexpr int ROWB = COLS * (int)sizeof(T);
+    static constexpr int DATAB = S * RB * ROWB;
+    static constexpr int RIB = S * RB * 16;
+    static constexpr int BARB = 2 * S * 8;
+    static constexpr int ACCB = 2 * COLS * (int)sizeof(A);   // plus, seg per column
+    static constexpr int QB = COLS * 4;                        // per-warp queues (128 entries each)
+    static constexpr int SMEM = DATAB + RIB + BARB + ACCB + QB;
+    static constexpr int THREADS = (NC + 1) * 32;
+};
+
+template <typename T, typename A, int NC, int RB, int S>
+__global__ void __launch_bounds__((NC + 1) * 32, 2)
+k_swap_stream_tmaq(const T* __restrict__ D, int64_t ld, int w, int wpad, int n, int P,
+                   const RowInfo<T>* __restrict__ ri, const A* __restrict__ R,
+                   A* __restrict__ out_plus, A* __restrict__ out_head, A* __restrict__ out_tail,
+                   A* __restrict__ out_imin, int* __restrict__ out_islot, A* __restrict__ out_acc) {
+    using C = TmaqCfg<T, A, NC, RB, S>;
+    using V = typename Vec4<T>::type;
+    extern __shared__ __align__(128) unsigned char smem[];
+    T* sdata = reinterpret_cast<T*>(smem);
+    RowInfo<T>* sri = reinterpret_cast<RowInfo<T>*>(smem + C::DATAB);
+    uint64_t* full = reinterpret_cast<uint64_t*>(smem + C::DATAB + C::RIB);
+    uint64_t* empty = full + S;
+    A* accp = reinterpret_cast<A*>(smem + C::DATAB + C::RIB + C::BARB);
+    A* accs = accp + C::COLS;
+    int* queue = reinterpret_cast<int*>(smem + C::DATAB + C::RIB + C::BARB + C::ACCB);
+
+    const int q = blockIdx.y;
+    const int64_t p0 = (int64_t)q * n / P, p1 = (int64_t)(q + 1) * n / P;
+    const int nstages = (int)((p1 - p0 + RB - 1) / RB);
+    const int ctacol = blockIdx.x * C::COLS;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+
+    if (threadIdx.x == 0) {
+        for (int st = 0; st < S; ++st) {
+            ptx::mbar_init(&full[st], 1);
+            ptx::mbar_init(&empty[st], NC);
+        }
+        ptx::fence_mbar_init();
+    }
+    for (int i = threadIdx.x; i < C::COLS; i += blockDim.x) { accp[i] = 0; accs[i] = 0; }
+    __syncthreads();
+
+    if (warp == NC) {
+        // ---------------- producer warp ----------------
+        const uint32_t cbytes = (uint32_t)min(C::COLS, wpad - ctacol) * (uint32_t)sizeof(T);
+        const uint64_t pol = ptx::policy_evict_first();
+        int o_next = (lane < RB && p0 + lane < p1) ? ri[p0 + lane].o : 0;
+        for (int st = 0; st < nstages; ++st) {
+            const int s = st % S;
+            if (st >= S) ptx::mbar_wait(&empty[s], ((st / S) & 1) ^ 1);
+            const int64_t pr = p0 + (int64_t)st * RB;
+            const int nb = (int)min((int64_t)RB, p1 - pr);
+            const int o = o_next;
+            const int64_t pn = pr + RB + lane;
+            if (lane < RB && pn < p1) o_next = ri[pn].o;
+            if (lane == 0) ptx::mbar_expect_tx(&full[s], (uint32_t)nb * (cbytes + 16u));
+            __syncwarp();
+            if (lane < nb)
+                ptx::bulk_g2s(sdata + (size_t)(s * RB + lane) * C::COLS, D + (int64_t)o * ld + ctacol, cbytes,
+                              &full[s], pol);
+            if (lane == 0) ptx::bulk_g2s(sri + s * RB, ri + pr, (uint32_t)nb * 16u, &full[s]);
+        }
+        return;
+    }
+
+    // ---------------- consumer warps ----------------
+    const int wc0 = warp * 128;                 // this warp's first column within the tile
+    const int cl0 = wc0 + lane * 4;             // this lane's first column within the tile
+    const int cb = ctacol + cl0;
+    const bool active = cb < w;
+    int* wq = queue + warp * 128;
+    A head[4], imin[4];
+    int islot[4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) { head[j] = 0; imin[j] = amax<A>(); islot[j] = -1; }
+    int cur = ri[p0].slot;
+    bool first = true;
+
+    auto close_segment = [&](int next) {        // the lane's own 4 columns
+        __syncwarp();                           // queue updates of other lanes are visible
+        if (first) {
+#pragma unroll
+            for (int j = 0; j < 4; ++j) head[j] = accs[cl0 + j];
+            first = false;
+        } else {
+            if (out_acc) {
+#pragma unroll
+                for (int j = 0; j < 4; ++j)
+                    if (cb + j < w) out_acc[(int64_t)cur * w + cb + j] = accs[cl0 + j];
+            }
+            const A rv = R[cur];
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+                const A val = rv + accs[cl0 + j];
+                if (val < imin[j]) { imin[j] = val; islot[j] = cur; }
+            }
+        }
+#pragma unroll
+        for (int j = 0; j < 4; ++j) accs[cl0 + j] = 0;
+        cur = next;
+        __syncwarp();
+    };
+
+    // compacted update of the rows [u0, u1) of the current stage
+    auto process = [&](const T* srow, const RowInfo<T>* srii, int u0, int u1) {
+        unsigned colmask[4] = {0, 0, 0, 0};
+        for (int u = u0; u < u1; ++u) {
+            const T ds = srii[u].ds;
+            const V v = *reinterpret_cast<const V*>(srow + (size_t)u * C::COLS + cl0);
+            T x[4];
+            memcpy(&x[0], &v.x, sizeof(T)); memcpy(&x[1], &v.y, sizeof(T));
+            memcpy(&x[2], &v.z, sizeof(T)); memcpy(&x[3], &v.w, sizeof(T));
+#pragma unroll
+            for (int j = 0; j < 4; ++j) colmask[j] |= (unsigned)(active && x[j] < ds) << u;
+        }
+        const int hc = (colmask[0] != 0) + (colmask[1] != 0) + (colmask[2] != 0) + (colmask[3] != 0);
+        if (__ballot_sync(FULL, hc != 0) == 0) return;
+        int incl = hc;
+#pragma unroll
+        for (int d = 1; d < 32; d <<= 1) {
+            const int y = __shfl_up_sync(FULL, incl, d);
+            if (lane >= d) incl += y;
+        }
+        const int H = __shfl_sync(FULL, incl, 31);
+        int pos = incl - hc;
+#pragma unroll
+        for (int j = 0; j < 4; ++j)
+            if (colmask[j]) wq[pos++] = (lane * 4 + j) | (int)(colmask[j] << 16);
+        __syncwarp();
+        for (int e = lane; e < H; e += 32) {
+            const int ent = wq[e];
+            const int c = wc0 + (ent & 0xffff);
+            const unsigned rm = (unsigned)ent >> 16;
+            A pp = 0, sg = 0;
+#pragma unroll
+            for (int u = 0; u < RB; ++u) {
+                if (rm & (1u << u)) {
+                    const T xv = srow[(size_t)u * C::COLS + c];
+                    const T dn = srii[u].dn, ds = srii[u].ds;
+                    const A xa = (A)xv;
+                    if (xv < dn) { pp += xa - (A)dn; sg += (A)dn - (A)ds; }
+                    else { sg += xa - (A)ds; }
+                }
+            }
+            accp[c] += pp;
+            accs[c] += sg;
+        }
+        __syncwarp();
+    };
+
+    for (int st = 0; st < nstages; ++st) {
+        const int s = st % S;
+        ptx::mbar_wait(&full[s], (st / S) & 1);
+        const int64_t pr = p0 + (int64_t)st * RB;
+        const int nb = (int)min((int64_t)RB, p1 - pr);
+        const T* srow = sdata + (size_t)(s * RB) * C::COLS;
+        const RowInfo<T>* srii = sri + s * RB;
+        if (nb == RB && srii[RB - 1].slot == cur) {
+            process(srow, srii, 0, RB);
+        } else {
+            int u = 0;
+            while (u < nb) {                     // split the stage at slot changes
+                if (srii[u].slot != cur) close_segment(srii[u].slot);
+                int v = u + 1;
+                while (v < nb && srii[v].slot == cur) ++v;
+                process(srow, srii, u, v);
+                u = v;
+            }
+        }
+        if (lane == 0) ptx::mbar_arrive(&empty[s]);
+    }
+    __syncwarp();
+    A tail[4];
+    if (first) {
+#pragma unroll
+        for (int j = 0; j < 4; ++j) { head[j] = accs[cl0 + j]; tail[j] = 0; }
+    } else {
+#pragma unroll
+        for (int j = 0; j < 4; ++j) tail[j] = accs[cl0 + j];
+    }
+    if (!active) return;
+    const int64_t base = (int64_t)q * w;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+        const int c = cb + j;
+        if (c < w) {
+            out_plus[base + c] = accp[cl0 + j];
+            out_head[base + c] = head[j];
+            out_tail[base + c] = tail[j];
+            out_imin[base + c] = imin[j];
+            out_islot[base + c] = islot[j];
+        }
+    }
+}
+
+// ---------------------------------------------------------------------------
+// a3, TMA ring with segment-aligned stages (k_swap_stream_seg, default).
+//
+// As k_swap_stream_tma, but the producer never lets a stage straddle two
+// slots: a stage holds up to RB rows of ONE segment (it is cut where the
+// slot changes; the cut costs ~1 short stage per segment).  The consumer
+// therefore closes a segment only between stages (one warp-uniform check)
+// and every stage takes the same branch-light path:
+//   * 16 compares d < d_s folded into a 4-bit "column j has a hit" mask per
+//     lane (setp.or chains), one REDUX.OR over the warp;
+//   * for the (few) columns with a hit somewhere in the warp, the RB row
+//     terms in fp64/int64, branch-free, tree-summed.
+// ---------------------------------------------------------------------------
+// A threshold no value compares below (uint32: 0; float: -inf, false even for NaN).
+template <typename T> __device__ __forceinline__ T never_lt();
+template <> __device__ __forceinline__ uint32_t never_lt<uint32_t>() { return 0u; }
+template <> __device__ __forceinline__ float never_lt<float>() { return -INFINITY; }
+
+template <typename T> struct CmpLt;
+template <> struct CmpLt<float> {
+    // 1 if any a_u < b_u (u = 0..3)
+    __device__ __forceinline__ static unsigned any4(float a0, float b0, float a1, float b1, float a2, float b2,
+                                                    float a3, float b3) {
+        unsigned r;
+        asm("{\n\t.reg .pred p;\n\t"
+            "setp.lt.f32 p, %1, %2;\n\t"
+            "setp.lt.or.f32 p, %3, %4, p;\n\t"
+            "setp.lt.or.f32 p, %5, %6, p;\n\t"
+            "setp.lt.or.f32 p, %7, %8, p;\n\t"
+            "selp.u32 %0, 1, 0, p;\n\t}"
+            : "=r"(r)
+            : "f"(a0), "f"(b0), "f"(a1), "f"(b1), "f"(a2), "f"(b2), "f"(a3), "f"(b3));
+        return r;
+    }
+};
+template <> struct CmpLt<uint32_t> {
+    __device__ __forceinline__ static unsigned any4(uint32_t a0, uint32_t b0, uint32_t a1, uint32_t b1, uint32_t a2,
+                                                    uint32_t b2, uint32_t a3, uint32_t b3) {
+        unsigned r;
+        asm("{\n\t.reg .pred p;\n\t"
+            "setp.lt.u32 p, %1, %2;\n\t"
+            "setp.lt.or.u32 p, %3, %4, p;\n\t"
+            "setp.lt.or.u32 p, %5, %6, p;\n\t"
+            "setp.lt.or.u32 p, %7, %8, p;\n\t"
+            "selp.u32 %0, 1, 0, p;\n\t}"
+            : "=r"(r)
+            : "r"(a0), "r"(b0), "r"(a1), "r"(b1), "r"(a2), "r"(b2), "r"(a3), "r"(b3));
+        return r;
+    }
+};
+
+template <typename T, int NC, int RB, int S>
+struct SegCfg {
+    static constexpr int COLS = NC * 128;
+    static constexpr int ROWB = COLS * (int)sizeof(T);
+    static constexpr int DATAB = S * RB * ROWB;
+    static constexpr int RIB = S * RB * 16;
+    static constexpr int NBB = S * 4;                   // rows in each stage
+    static constexpr int BARB = 2 * S * 8;
+    static constexpr int SMEM = DATAB + RIB + 16 * ((NBB + 15) / 16) + BARB;
+    static constexpr int THREADS = (NC + 1) * 32;
+};
+
+template <typename T, typename A, int NC, int RB, int S>
+__global__ void __launch_bounds__((NC + 1) * 32, 2)
+k_swap_stream_seg(const T* __restrict__ D, int64_t ld, int w, int wpad, int n, int P,
+                  const RowInfo<T>* __restrict__ ri, const A* __restrict__ R,
+                  A* __restrict__ out_plus, A* __restrict__ out_head, A* __restrict__ out_tail,
+                  A* __restrict__ out_imin, int* __restrict__ out_islot, A* __restrict__ out_acc) {
+    using C = SegCfg<T, NC, RB, S>;
+    using V = typename Vec4<T>::type;
+    extern __shared__ __align__(128) unsigned char smem[];
+    T* sdata = reinterpret_cast<T*>(smem);
+    RowInfo<T>* sri = reinterpret_cast<RowInfo<T>*>(smem + C::DATAB);
+    int* snb = reinterpret_cast<int*>(smem + C::DATAB + C::RIB);
+    uint64_t* full = reinterpret_cast<uint64_t*>(smem + C::DATAB + C::RIB + 16 * ((C::NBB + 15) / 16));
+    uint64_t* empty = full + S;
+
+    const int q = blockIdx.y;
+    const int64_t p0 = (int64_t)q * n / P, p1 = (int64_t)(q + 1) * n / P;
+    const int ctacol = blockIdx.x * C::COLS;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+
+    if (threadIdx.x == 0) {
+        for (int st = 0; st < S; ++st) {
+            ptx::mbar_init(&full[st], 1);
+            ptx::mbar_init(&empty[st], NC);
+        }
+        ptx::fence_mbar_init();
+    }
+    __syncthreads();
+
+    if (warp == NC) {
+        // ---------------- producer warp ----------------
+        // Stage = up to RB rows of one slot.  nb = 0 marks the end of the part.
+        const uint32_t cbytes = (uint32_t)min(C::COLS, wpad - ctacol) * (uint32_t)sizeof(T);
+        const uint64_t pol = ptx::policy_evict_first();
+        int64_t pr = p0;
+        int st = 0;
+        // lane u < RB holds (o, slot) of row pr + u
+        int o_l = 0, sl_l = -1;
+        if (lane < RB && pr + lane < p1) { const RowInfo<T> r = ri[pr + lane]; o_l = r.o; sl_l = r.slot; }
+        while (true) {
+            const int s = st % S;
+            if (st >= S) ptx::mbar_wait(&empty[s], ((st / S) & 1) ^ 1);
+            if (pr >= p1) {                      // terminator stage
+                if (lane == 0) {
+                    snb[s] = 0;
+                    ptx::mbar_arrive(&full[s]);
+                }
+                break;
+            }
+            const int slot0 = __shfl_sync(FULL, sl_l, 0);
+            const unsigned same = __ballot_sync(FULL, lane < RB && sl_l == slot0 && pr + lane < p1);
+            const int nb = __ffs(~same) - 1;     // rows of slot0 at the head of the window (>= 1)
+            if (lane == 0) {
+                snb[s] = nb;
+                ptx::mbar_expect_tx(&full[s], (uint32_t)nb * (cbytes + 16u));
+            }
+            __syncwarp();
+            if (lane < nb)
+                ptx::bulk_g2s(sdata + (size_t)(s * RB + lane) * C::COLS, D + (int64_t)o_l * ld + ctacol, cbytes,
+                              &full[s], pol);
+            if (lane == 0) ptx::bulk_g2s(sri + s * RB, ri + pr, (uint32_t)nb * 16u, &full[s]);
+            pr += nb;
+            // slide the row window by nb (rows already loaded move down, new ones are fetched)
+            const int o_sh = __shfl_down_sync(FULL, o_l, nb);
+            const int s_sh = __shfl_down_sync(FULL, sl_l, nb);
+            if (lane < RB) {
+                if (lane + nb < RB) { o_l = o_sh; sl_l = s_sh; }
+                else if (pr + lane < p1) { const RowInfo<T> r = ri[pr + lane]; o_l = r.o; sl_l = r.slot; }
+                else { sl_l = -1; }
+            }
+            ++st;
+        }
+        return;
+    }
+
+    // ---------------- consumer warps ----------------
+    const int cb = ctacol + warp * 128 + lane * 4;
+    const bool active = cb < w;
+    const T big = dmax<T>();
+    A plus[4], seg[4], head[4], imin[4];
+    int islot[4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) { plus[j] = 0; seg[j] = 0; head[j] = 0; imin[j] = amax<A>(); islot[j] = -1; }
+    int cur = ri[p0].slot;
+    bool first = true;
+
+    for (int st = 0;; ++st) {
+        const int s = st % S;
+        ptx::mbar_wait(&full[s], (st / S) & 1);
+        const int nb = snb[s];
+        if (nb == 0) break;
+        const RowInfo<T>* srii = sri + s * RB;
+        const int slot = srii[0].slot;
+        if (slot != cur) {                       // segment boundary (warp-uniform, ~1 in 60 stages)
+            if (first) {
+#pragma unroll
+                for (int j = 0; j < 4; ++j) head[j] = seg[j];
+                first = false;
+            } else {
+                if (out_acc) {
+#pragma unroll
+                    for (int j = 0; j < 4; ++j)
+                        if (cb + j < w) out_acc[(int64_t)cur * w + cb + j] = seg[j];
+                }
+                const A rv = R[cur];
+#pragma unroll
+                for (int j = 0; j < 4; ++j) {
+                    const A val = rv + seg[j];
+                    if (val < imin[j]) { imin[j] = val; islot[j] = cur; }
+                }
+            }
+#pragma unroll
+            for (int j = 0; j < 4; ++j) seg[j] = 0;
+            cur = slot;
+        }
+        T x[RB][4], dn[RB], ds[RB];
+        const T* srow = sdata + (size_t)(s * RB) * C::COLS + (warp * 128 + lane * 4);
+#pragma unroll
+        for (int u = 0; u < RB; ++u) {
+            const V v = *reinterpret_cast<const V*>(srow + (size_t)u * C::COLS);
+            memcpy(&x[u][0], &v.x, sizeof(T)); memcpy(&x[u][1], &v.y, sizeof(T));
+            memcpy(&x[u][2], &v.z, sizeof(T)); memcpy(&x[u][3], &v.w, sizeof(T));
+            const bool valid = u < nb;           // rows >= nb hold stale (possibly never written) bytes:
+            dn[u] = valid ? srii[u].dn : never_lt<T>();   // a threshold nothing is below
+            ds[u] = valid ? srii[u].ds : never_lt<T>();
+        }
+        __syncwarp();
+        if (lane == 0) ptx::mbar_arrive(&empty[s]);
+        if (!active) {
+#pragma unroll
+            for (int u = 0; u < RB; ++u)
+#pragma unroll
+                for (int j = 0; j < 4; ++j) x[u][j] = big;
+        }
+        static_assert(RB == 4, "mask folding assumes 4 rows per stage");
+        unsigned m = 0;
+#pragma unroll
+        for (int j = 0; j < 4; ++j)
+            m |= CmpLt<T>::any4(x[0][j], ds[0], x[1][j], ds[1], x[2][j], ds[2], x[3][j], ds[3]) << j;
+        const unsigned wm = __reduce_or_sync(FULL, m);
+        if (wm == 0) continue;
+        A dnA[RB], dsA[RB], dnds[RB];
+#pragma unroll
+        for (int u = 0; u < RB; ++u) { dnA[u] = (A)dn[u]; dsA[u] = (A)ds[u]; dnds[u] = dnA[u] - dsA[u]; }
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            if (wm & (1u << j)) {
+                A tp[RB], ts[RB];
+#pragma unroll
+                for (int u = 0; u < RB; ++u) {
+                    const bool c1 = x[u][j] < dn[u], c2 = x[u][j] < ds[u];
+                    const A t = (A)x[u][j] - (c1 ? dnA[u] : dsA[u]);
+                    tp[u] = c1 ? t : (A)0;
+                    ts[u] = c1 ? dnds[u] : (c2 ? t : (A)0);
+                }
+                plus[j] += (tp[0] + tp[1]) + (tp[2] + tp[3]);
+                seg[j] += (ts[0] + ts[1]) + (ts[2] + ts[3]);
+            }
+        }
+    }
+    if (first) {
+#pragma unroll
+        for (int j = 0; j < 4; ++j) { head[j] = seg[j]; seg[j] = 0; }
+    }
+    if (!active) return;
+    const int64_t base = (int64_t)q * w;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+        const int c = cb + j;
+        if (c < w) {
+            out_plus[base + c] = plus[j];
+            out_head[base + c] = head[j];
+            out_tail[base + c] = seg[j];
             out_imin[base + c] = imin[j];
             out_islot[base + c] = islot[j];
         }

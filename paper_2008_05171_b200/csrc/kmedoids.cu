@@ -68,6 +68,10 @@ constexpr int WT_NW = 4, WT_RB = 4, WT_S = 6;
 // TMA ring + compacted hit lists (default): 7 consumer warps + 1 producer,
 // 4 rows per stage, 6 stages, per-column fp64 partials in shared memory.
 constexpr int CMP_NC = 7, CMP_RB = 4, CMP_S = 6;
+// TMA ring + per-warp hit queues: 7 consumer warps + 1 producer, 4 rows x 6 stages.
+constexpr int TQ_NC = 7, TQ_RB = 4, TQ_S = 6;
+// TMA ring with segment-aligned stages: 7 consumer warps + 1 producer, 4 rows x 7 stages.
+constexpr int SG_NC = 7, SG_RB = 4, SG_S = 7;
 constexpr int WT_COLS = WT_NW * 128;
 constexpr int WT_RESIDENT = 4;
 constexpr int TMA_RESIDENT = 2;
@@ -197,10 +201,15 @@ struct Impl : ImplBase {
         sharded = !(c0 == 0 && c1 == n);
         const char* ev = getenv("KM_STREAM");
         // Stream kernel selection (KM_STREAM overrides for
-        // measurements): tma = TMA bulk-copy ring (default), ldg = register
-        // pipelined loads, wtma = warp-autonomous rings, cmp = compacted hits.
-        stream_kind = 1;
+        // measurements): seg = TMA bulk-copy ring with segment-aligned stages
+        // (default), tma = the same ring with stages across segments, ldg =
+        // register-pipelined loads, wtma = warp-autonomous rings, cmp / tmaq =
+        // compacted hit lists (CTA-wide / per warp).
+        stream_kind = 10;
+        if (ev && strcmp(ev, "tma") == 0) stream_kind = 1;
         if (ev && strcmp(ev, "cmp") == 0) stream_kind = 6;
+        if (ev && strcmp(ev, "tmaq") == 0) stream_kind = 9;
+        if (ev && strcmp(ev, "seg") == 0) stream_kind = 10;
         if (ev && strcmp(ev, "ldg") == 0) stream_kind = 0;
         if (ev && strcmp(ev, "wtma") == 0) stream_kind = 2;
 
@@ -210,7 +219,9 @@ struct Impl : ImplBase {
         debug_natural = (dbg && dbg[0] == '1') ? 1 : 0;
         const char* dnc = getenv("KM_DEBUG_NOCOMPUTE");        // perf experiment only: wrong results
         debug_nocompute = (dnc && dnc[0] == '1') ? 1 : 0;
-        P = stream_kind == 6 ? choose_parts(n, w, CMP_NC * 128, 2)
+        P = stream_kind == 10 ? choose_parts(n, w, SG_NC * 128, 2)
+            : stream_kind == 9 ? choose_parts(n, w, TQ_NC * 128, 2)
+            : stream_kind == 6 ? choose_parts(n, w, CMP_NC * 128, 2)
 
             : stream_kind == 1 ? choose_parts(n, w, TMA_COLS, TMA_RESIDENT)
             : stream_kind == 2 ? choose_parts(n, w, WT_COLS, WT_RESIDENT)
@@ -279,6 +290,8 @@ struct Impl : ImplBase {
     bool pending_prof = false;
     bool tma_attr_set = false;
     bool cmp_attr_set = false;
+    bool tmaq_attr_set = false;
+    bool seg_attr_set = false;
 
     km_status assign_full_and_td() {
         const int nb = (int)cdiv(n, 256);
@@ -342,7 +355,11 @@ struct Impl : ImplBase {
     km_status eval_local() {
         KM_TRY(prep());
         if (profiling) KM_CK(cudaEventRecord(ev0, st));
-        if (stream_kind == 6) {   // compacted hits
+        if (stream_kind == 10) {  // TMA ring, segment-aligned stages
+            KM_TRY((launch_seg<SG_NC, SG_RB, SG_S>(nullptr)));
+        } else if (stream_kind == 9) {   // TMA ring + per-warp hit queues
+            KM_TRY((launch_tmaq<TQ_NC, TQ_RB, TQ_S>(nullptr)));
+        } else if (stream_kind == 6) {   // compacted hits
             using C = km::CmpCfg<T, A, CMP_NC, CMP_RB, CMP_S>;
             auto kern = km::k_swap_stream_cmp<T, A, CMP_NC, CMP_RB, CMP_S>;
             if (!cmp_attr_set) {
@@ -375,6 +392,34 @@ struct Impl : ImplBase {
                                                       tail_slot, R, empty_slot, point_slot, cand_v, cand_slot,
                                                       partials, counters, rec_local);
         KM_CKL();
+        return KM_OK;
+    }
+
+    template <int NC, int RB, int S>
+    km_status launch_seg(A* acc_out) {
+        using C = km::SegCfg<T, NC, RB, S>;
+        auto kern = km::k_swap_stream_seg<T, A, NC, RB, S>;
+        if (!seg_attr_set) {
+            KM_CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM));
+            seg_attr_set = true;
+        }
+        dim3 g((unsigned)cdiv(w, C::COLS), P);
+        kern<<<g, C::THREADS, C::SMEM, st>>>(D, ld, w, wpad, (int)n, P, ri, R, o_plus, o_head, o_tail, o_imin, o_islot,
+                                              acc_out);
+        return KM_OK;
+    }
+
+    template <int NC, int RB, int S>
+    km_status launch_tmaq(A* acc_out) {
+        using C = km::TmaqCfg<T, A, NC, RB, S>;
+        auto kern = km::k_swap_stream_tmaq<T, A, NC, RB, S>;
+        if (!tmaq_attr_set) {
+            KM_CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM));
+            tmaq_attr_set = true;
+        }
+        dim3 g((unsigned)cdiv(w, C::COLS), P);
+        kern<<<g, C::THREADS, C::SMEM, st>>>(D, ld, w, wpad, (int)n, P, ri, R, o_plus, o_head, o_tail, o_imin, o_islot,
+                                              acc_out);
         return KM_OK;
     }
 
@@ -459,18 +504,9 @@ struct Impl : ImplBase {
     km_status swap_iter_fp2(int32_t* swaps_out, void* td_out) {
         KM_TRY(fp2_alloc());
         KM_TRY(prep());
-        using C = km::TmaCfg<T, TMA_NC, TMA_RB, TMA_S>;
-        auto kern = km::k_swap_stream_tma<T, A, TMA_NC, TMA_RB, TMA_S>;
-        if (!tma_attr_set) {
-            KM_CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM));
-            tma_attr_set = true;
-        }
-        const int Pt = choose_parts(n, w, TMA_COLS, TMA_RESIDENT);
-        if (Pt != P) return fail(KM_EINVAL, "internal: FastPAM2 needs the TMA stream partition");
+        // FastPAM2 always uses the segment-aligned TMA stream (it stores acc_c[i]).
         if (profiling) KM_CK(cudaEventRecord(ev0, st));
-        dim3 g((unsigned)cdiv(w, C::COLS), P);
-        kern<<<g, C::THREADS, C::SMEM, st>>>(D, ld, w, wpad, (int)n, P, ri, R, o_plus, o_head, o_tail, o_imin,
-                                              o_islot, 0, fp2_acc);
+        KM_TRY((launch_seg<SG_NC, SG_RB, SG_S>(fp2_acc)));
         KM_CKL();
         if (profiling) { KM_CK(cudaEventRecord(ev1, st)); pending_prof = true; }
         km::k_swap_combine<A><<<ncomb, 256, 0, st>>>(w, c0, P, o_plus, o_head, o_tail, o_imin, o_islot, head_slot,
