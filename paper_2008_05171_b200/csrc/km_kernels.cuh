@@ -1470,7 +1470,6 @@ k_swap_stream_seg(const T* __restrict__ D, int64_t ld, int w, int wpad, int n, i
     // ---------------- consumer warps ----------------
     const int cb = ctacol + warp * 128 + lane * 4;
     const bool active = cb < w;
-    const T big = dmax<T>();
     A plus[4], seg[4], head[4], imin[4];
     int islot[4];
 #pragma unroll
@@ -1514,17 +1513,24 @@ k_swap_stream_seg(const T* __restrict__ D, int64_t ld, int w, int wpad, int n, i
             const V v = *reinterpret_cast<const V*>(srow + (size_t)u * C::COLS);
             memcpy(&x[u][0], &v.x, sizeof(T)); memcpy(&x[u][1], &v.y, sizeof(T));
             memcpy(&x[u][2], &v.z, sizeof(T)); memcpy(&x[u][3], &v.w, sizeof(T));
-            const bool valid = u < nb;           // rows >= nb hold stale (possibly never written) bytes:
-            dn[u] = valid ? srii[u].dn : never_lt<T>();   // a threshold nothing is below
-            ds[u] = valid ? srii[u].ds : never_lt<T>();
+            dn[u] = srii[u].dn;
+            ds[u] = srii[u].ds;
         }
         __syncwarp();
         if (lane == 0) ptx::mbar_arrive(&empty[s]);
-        if (!active) {
+        // Rows >= nb (the short stage at a segment end) hold stale, possibly
+        // never-written bytes, and columns >= w of the last tile are padding:
+        // give them thresholds nothing compares below (a per-lane select; the
+        // loaded values themselves are left untouched).
+        if (nb < RB) {
 #pragma unroll
-            for (int u = 0; u < RB; ++u)
+            for (int u = 1; u < RB; ++u)
+                if (u >= nb) { dn[u] = never_lt<T>(); ds[u] = never_lt<T>(); }
+        }
 #pragma unroll
-                for (int j = 0; j < 4; ++j) x[u][j] = big;
+        for (int u = 0; u < RB; ++u) {
+            dn[u] = active ? dn[u] : never_lt<T>();
+            ds[u] = active ? ds[u] : never_lt<T>();
         }
         static_assert(RB == 4, "mask folding assumes 4 rows per stage");
         unsigned m = 0;
