@@ -255,9 +255,10 @@ __global__ void k_slot_hist(const int* __restrict__ near, int n, int k, int* __r
 // Exclusive scan of counts (slot-major) -> offsets; seg_start[s] = first
 // sorted position of slot s, seg_start[k] = n.  Single block of 1024.
 __global__ void k_scan_counts(const int* __restrict__ counts, int total, int B, int k,
-                              int* __restrict__ offsets, int* __restrict__ seg_start) {
+                              int* __restrict__ offsets, int* __restrict__ seg_start, int* __restrict__ empty_slot) {
     __shared__ int sums[1024];
     const int t = threadIdx.x, nt = blockDim.x;
+    if (t == 0) *empty_slot = INT_MAX;      // reset for k_removal_loss (runs after this kernel)
     const int per = (total + nt - 1) / nt;
     const int a = t * per, z = min(total, a + per);
     int s = 0;

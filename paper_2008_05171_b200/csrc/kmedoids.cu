@@ -175,6 +175,8 @@ struct Impl : ImplBase {
     cudaEvent_t ev0 = nullptr, ev1 = nullptr;
 
     ~Impl() override {
+        if (fp1_exec) cudaGraphExecDestroy(fp1_exec);
+        if (cap_st) cudaStreamDestroy(cap_st);
         for (void* p : bufs) cudaFree(p);
         if (h_dec) cudaFreeHost(h_dec);
         if (ev0) cudaEventDestroy(ev0);
@@ -217,6 +219,8 @@ struct Impl : ImplBase {
         use_tma = stream_kind == 1;
         const char* dbg = getenv("KM_DEBUG_NATURAL_ORDER");   // perf experiment only: wrong results
         debug_natural = (dbg && dbg[0] == '1') ? 1 : 0;
+        const char* eg = getenv("KM_GRAPH");
+        use_graph = !(eg && eg[0] == '0');
         const char* dnc = getenv("KM_DEBUG_NOCOMPUTE");        // perf experiment only: wrong results
         debug_nocompute = (dnc && dnc[0] == '1') ? 1 : 0;
         P = stream_kind == 10 ? choose_parts(n, w, SG_NC * 128, 2)
@@ -275,6 +279,12 @@ struct Impl : ImplBase {
     }
 
     // ---- pieces of the hot path -------------------------------------------
+    // inside a graph capture the event must be an external record node
+    bool capturing = false;
+    cudaError_t record_ev(cudaEvent_t e) {
+        return capturing ? cudaEventRecordWithFlags(e, st, cudaEventRecordExternal) : cudaEventRecord(e, st);
+    }
+
     km_status sync_dec() {
         KM_CK(cudaMemcpyAsync(h_dec, dec, sizeof(Dec), cudaMemcpyDeviceToHost, st));
         KM_CK(cudaStreamSynchronize(st));
@@ -289,6 +299,12 @@ struct Impl : ImplBase {
     }
     bool pending_prof = false;
     bool tma_attr_set = false;
+    // CUDA graph of the FastPAM1 iteration (KM_GRAPH=0 disables)
+    bool use_graph = true;
+    cudaGraphExec_t fp1_exec = nullptr;
+    cudaStream_t cap_st = nullptr;
+    int64_t fp1_graph_kernels = 0;
+    int64_t fp1_iters = 0;
     bool cmp_attr_set = false;
     bool tmaq_attr_set = false;
     bool seg_attr_set = false;
@@ -338,10 +354,8 @@ struct Impl : ImplBase {
     km_status prep() {
         km::k_slot_hist<<<B, 256, k * sizeof(int), st>>>(near, (int)n, k, counts);
         KM_CKL();
-        km::k_scan_counts<<<1, 1024, 0, st>>>(counts, k * B, B, k, offsets, seg_start);
+        km::k_scan_counts<<<1, 1024, 0, st>>>(counts, k * B, B, k, offsets, seg_start, empty_slot);
         KM_CKL();
-        const int big = INT_MAX;
-        KM_CK(cudaMemcpyAsync(empty_slot, &big, sizeof(int), cudaMemcpyHostToDevice, st));
         km::k_slot_scatter<T><<<B, 32, k * sizeof(int), st>>>(near, dn, ds, (int)n, k, offsets, ri, debug_natural);
         KM_CKL();
         km::k_removal_loss<T, A><<<(unsigned)cdiv((int64_t)k * 32, 256), 256, 0, st>>>(ri, seg_start, k, R, empty_slot);
@@ -354,7 +368,7 @@ struct Impl : ImplBase {
     // a3 + a4 (local): stream the slab, combine into the local best record.
     km_status eval_local() {
         KM_TRY(prep());
-        if (profiling) KM_CK(cudaEventRecord(ev0, st));
+        if (profiling) KM_CK(record_ev(ev0));
         if (stream_kind == 10) {  // TMA ring, segment-aligned stages
             KM_TRY((launch_seg<SG_NC, SG_RB, SG_S>(nullptr)));
         } else if (stream_kind == 9) {   // TMA ring + per-warp hit queues
@@ -387,7 +401,7 @@ struct Impl : ImplBase {
                 D, ld, w, (int)n, P, ri, R, o_plus, o_head, o_tail, o_imin, o_islot);
         }
         KM_CKL();
-        if (profiling) { KM_CK(cudaEventRecord(ev1, st)); pending_prof = true; }
+        if (profiling) { KM_CK(record_ev(ev1)); pending_prof = true; }
         km::k_swap_combine<A><<<ncomb, 256, 0, st>>>(w, c0, P, o_plus, o_head, o_tail, o_imin, o_islot, head_slot,
                                                       tail_slot, R, empty_slot, point_slot, cand_v, cand_slot,
                                                       partials, counters, rec_local);
@@ -461,16 +475,65 @@ struct Impl : ImplBase {
         memcpy(td_out, &v, sizeof(A));
     }
 
+    // One FastPAM1 iteration, enqueued on st (graph-capturable: fixed pointers,
+    // no host-side memory other than the pinned decision mirror).
+    km_status enqueue_fp1_iteration() {
+        const bool prof_save = profiling;
+        if (use_graph) profiling = true;      // the graph always carries the stream events
+        km_status s = eval_local();
+        profiling = prof_save;
+        if (s != KM_OK) return s;
+        km::k_select<A><<<1, 1, 0, st>>>(rec_local, 1, td, M, point_slot, dec);
+        KM_CKL();
+        KM_TRY(apply_local());
+        KM_CK(cudaMemcpyAsync(h_dec, dec, sizeof(Dec), cudaMemcpyDeviceToHost, st));
+        return KM_OK;
+    }
+
     km_status swap_iter(km_variant v, int32_t* swaps, void* td_out) override {
         if (sharded) return fail(KM_EINVAL, "swap_iter on a sharded handle; use the kmedoids_shard_* phases");
         if (!ready) return fail(KM_EINVAL, "no medoids: call kmedoids_set_medoids or kmedoids_init_build first");
         if (v != KM_FASTPAM1 && v != KM_FASTPAM2) return fail(KM_EINVAL, "unknown variant %d", (int)v);
         if (v == KM_FASTPAM2) return swap_iter_fp2(swaps, td_out);
-        KM_TRY(eval_local());
-        km::k_select<A><<<1, 1, 0, st>>>(rec_local, 1, td, M, point_slot, dec);
-        KM_CKL();
-        KM_TRY(apply_local());
-        KM_TRY(sync_dec());
+        if (use_graph && fp1_iters >= 1) {
+            // the whole iteration (11 kernels + the 32-byte decision copy) as one CUDA graph
+            if (!fp1_exec) {
+                const int64_t l0 = launches;
+                // capture on a private stream (the caller's may be the legacy
+                // default stream, which cannot capture); launch on the caller's.
+                if (!cap_st) KM_CK(cudaStreamCreateWithFlags(&cap_st, cudaStreamNonBlocking));
+                cudaStream_t user_st = st;
+                st = cap_st;
+                cudaError_t be = cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal);
+                if (be != cudaSuccess) { st = user_st; return fail(KM_ECUDA, "begin capture: %s", cudaGetErrorString(be)); }
+                capturing = true;
+                km_status cs = enqueue_fp1_iteration();
+                capturing = false;
+                cudaGraph_t g = nullptr;
+                cudaError_t ce = cudaStreamEndCapture(st, &g);
+                st = user_st;
+                if (cs != KM_OK) { if (g) cudaGraphDestroy(g); return cs; }
+                if (ce != cudaSuccess) return fail(KM_ECUDA, "graph capture failed: %s", cudaGetErrorString(ce));
+                ce = cudaGraphInstantiate(&fp1_exec, g, 0);
+                cudaGraphDestroy(g);
+                if (ce != cudaSuccess) { fp1_exec = nullptr; return fail(KM_ECUDA, "graph instantiate: %s", cudaGetErrorString(ce)); }
+                fp1_graph_kernels = launches - l0;
+                launches = l0;
+            }
+            KM_CK(cudaGraphLaunch(fp1_exec, st));
+            launches += fp1_graph_kernels;
+            KM_CK(cudaStreamSynchronize(st));
+            if (profiling) {
+                float ms = 0.f;
+                KM_CK(cudaEventElapsedTime(&ms, ev0, ev1));
+                prof_ms += ms; prof_launches += 1;
+            }
+            pending_prof = false;
+        } else {
+            KM_TRY(enqueue_fp1_iteration());
+            KM_TRY(sync_dec());
+        }
+        ++fp1_iters;
         last_swaps.clear();
         if (h_dec->apply) {
             Rec r; r.v = h_dec->dtd; r.slot = h_dec->slot; r.c = h_dec->c;
@@ -505,10 +568,10 @@ struct Impl : ImplBase {
         KM_TRY(fp2_alloc());
         KM_TRY(prep());
         // FastPAM2 always uses the segment-aligned TMA stream (it stores acc_c[i]).
-        if (profiling) KM_CK(cudaEventRecord(ev0, st));
+        if (profiling) KM_CK(record_ev(ev0));
         KM_TRY((launch_seg<SG_NC, SG_RB, SG_S>(fp2_acc)));
         KM_CKL();
-        if (profiling) { KM_CK(cudaEventRecord(ev1, st)); pending_prof = true; }
+        if (profiling) { KM_CK(record_ev(ev1)); pending_prof = true; }
         km::k_swap_combine<A><<<ncomb, 256, 0, st>>>(w, c0, P, o_plus, o_head, o_tail, o_imin, o_islot, head_slot,
                                                       tail_slot, R, empty_slot, point_slot, cand_v, cand_slot,
                                                       partials, counters, rec_local, fp2_acc, fp2_plus);
