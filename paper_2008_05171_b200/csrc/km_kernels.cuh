@@ -174,28 +174,23 @@ __global__ void k_assign_full(const T* __restrict__ MC, int n, int k, int* __res
 }
 
 // Incremental update after slot i = dec->slot received a new medoid whose
-// column is MC[i]: objects whose nearest or second was slot i rescan all k
-// slots; every other object only compares the new medoid against its current
-// (nearest, second) pair.  Equal to k_assign_full on the new medoid set.
+// column is MC[i]: every object not served by slot i only compares the new
+// medoid against its current (nearest, second) pair; objects whose nearest or
+// second WAS slot i (about 2n/k of them) are appended to `rescan` and handled
+// by k_assign_rescan (one warp per object).  Together equal to k_assign_full
+// on the new medoid set (tested).  *rescan_count is reset by k_select.
 template <typename T, typename A>
 __global__ void k_assign_incremental(const T* __restrict__ MC, int n, int k,
                                      const Decision<A>* __restrict__ dec, int* __restrict__ near,
-                                     int* __restrict__ sec, T* __restrict__ dn, T* __restrict__ ds) {
+                                     int* __restrict__ sec, T* __restrict__ dn, T* __restrict__ ds,
+                                     int* __restrict__ rescan, int* __restrict__ rescan_count) {
     if (!dec->apply) return;
     const int o = blockIdx.x * blockDim.x + threadIdx.x;
     if (o >= n) return;
     const int i = dec->slot;
-    int j1 = near[o], j2 = sec[o];
+    const int j1 = near[o], j2 = sec[o];
     if (j1 == i || j2 == i) {
-        T a = MC[o], b = MC[(int64_t)n + o];
-        T d1, d2;
-        if (b < a) { d1 = b; j1 = 1; d2 = a; j2 = 0; } else { d1 = a; j1 = 0; d2 = b; j2 = 1; }
-        for (int j = 2; j < k; ++j) {
-            T d = MC[(int64_t)j * n + o];
-            if (d < d1) { d2 = d1; j2 = j1; d1 = d; j1 = j; }
-            else if (d < d2) { d2 = d; j2 = j; }
-        }
-        near[o] = j1; sec[o] = j2; dn[o] = d1; ds[o] = d2;
+        rescan[atomicAdd(rescan_count, 1)] = o;
         return;
     }
     const T x = MC[(int64_t)i * n + o];
@@ -204,6 +199,47 @@ __global__ void k_assign_incremental(const T* __restrict__ MC, int n, int k,
         near[o] = i; dn[o] = x; sec[o] = j1; ds[o] = d1;
     } else if (x < d2 || (x == d2 && i < j2)) {
         sec[o] = i; ds[o] = x;
+    }
+}
+
+// (d, j) lexicographic top-2 of the k medoid columns for one object, one
+// warp per listed object: lanes scan slots j = lane, lane+32, ... and the
+// per-lane top-2 lists are merged with shuffles (result independent of the
+// merge order, so deterministic).
+template <typename T>
+__device__ __forceinline__ bool lex_lt(T a, int ja, T b, int jb) { return a < b || (a == b && ja < jb); }
+
+template <typename T, typename A>
+__global__ void k_assign_rescan(const T* __restrict__ MC, int n, int k, const Decision<A>* __restrict__ dec,
+                                const int* __restrict__ rescan, const int* __restrict__ rescan_count,
+                                int* __restrict__ near, int* __restrict__ sec, T* __restrict__ dn,
+                                T* __restrict__ ds) {
+    if (!dec->apply) return;
+    const int lane = threadIdx.x & 31;
+    const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, nw = (gridDim.x * blockDim.x) >> 5;
+    const int cnt = *rescan_count;
+    for (int e = gw; e < cnt; e += nw) {
+        const int o = rescan[e];
+        T d1 = dmax<T>(), d2 = dmax<T>();
+        int j1 = INT_MAX, j2 = INT_MAX;
+        for (int j = lane; j < k; j += 32) {
+            const T d = MC[(int64_t)j * n + o];
+            if (lex_lt(d, j, d1, j1)) { d2 = d1; j2 = j1; d1 = d; j1 = j; }
+            else if (lex_lt(d, j, d2, j2)) { d2 = d; j2 = j; }
+        }
+#pragma unroll
+        for (int x = 16; x >= 1; x >>= 1) {
+            const T e1 = __shfl_xor_sync(FULL, d1, x), e2 = __shfl_xor_sync(FULL, d2, x);
+            const int f1 = __shfl_xor_sync(FULL, j1, x), f2 = __shfl_xor_sync(FULL, j2, x);
+            // merge (d1,j1) <= (d2,j2) with (e1,f1) <= (e2,f2)
+            if (lex_lt(e1, f1, d1, j1)) {
+                if (lex_lt(d1, j1, e2, f2)) { d2 = d1; j2 = j1; } else { d2 = e2; j2 = f2; }
+                d1 = e1; j1 = f1;
+            } else if (lex_lt(e1, f1, d2, j2)) {
+                d2 = e1; j2 = f1;
+            }
+        }
+        if (lane == 0) { near[o] = j1; sec[o] = j2; dn[o] = d1; ds[o] = d2; }
     }
 }
 
@@ -1604,27 +1640,38 @@ __global__ void k_swap_combine(int w, int64_t col_begin, int P, const A* __restr
         };
         A plus = 0, carry = 0;
         int cs = -1;
-        for (int q = 0; q < P; ++q) {
-            const int64_t idx = (int64_t)q * w + cl;
-            plus += in_plus[idx];
-            const int h = head_slot[q], t = tail_slot[q];
-            const A hv = in_head[idx];
-            if (h == cs) {
-                carry += hv;
-            } else {
-                if (cs >= 0) fin(cs, carry);
-                cs = h;
-                carry = hv;
+        constexpr int QU = 4;                  // parts loaded ahead (memory-level parallelism)
+        for (int q0 = 0; q0 < P; q0 += QU) {
+            A pl[QU], hv[QU], tv[QU], iv[QU];
+            int isl[QU], hs[QU], ts[QU];
+#pragma unroll
+            for (int u = 0; u < QU; ++u) {
+                const int q = q0 + u;
+                if (q < P) {
+                    const int64_t idx = (int64_t)q * w + cl;
+                    pl[u] = in_plus[idx]; hv[u] = in_head[idx]; tv[u] = in_tail[idx];
+                    iv[u] = in_imin[idx]; isl[u] = in_islot[idx];
+                    hs[u] = head_slot[q]; ts[u] = tail_slot[q];
+                }
             }
-            const int is = in_islot[idx];
-            if (is >= 0) {
-                const A iv = in_imin[idx];
-                if (iv < bv || (iv == bv && is < bs)) { bv = iv; bs = is; }
-            }
-            if (t != h) {
-                fin(cs, carry);
-                cs = t;
-                carry = in_tail[idx];
+#pragma unroll
+            for (int u = 0; u < QU; ++u) {
+                if (q0 + u >= P) break;
+                plus += pl[u];
+                const int h = hs[u], t = ts[u];
+                if (h == cs) {
+                    carry += hv[u];
+                } else {
+                    if (cs >= 0) fin(cs, carry);
+                    cs = h;
+                    carry = hv[u];
+                }
+                if (isl[u] >= 0 && (iv[u] < bv || (iv[u] == bv && isl[u] < bs))) { bv = iv[u]; bs = isl[u]; }
+                if (t != h) {
+                    fin(cs, carry);
+                    cs = t;
+                    carry = tv[u];
+                }
             }
         }
         fin(cs, carry);
@@ -1644,7 +1691,8 @@ __global__ void k_swap_combine(int w, int64_t col_begin, int P, const A* __restr
 // TD <- TD + dTD*.  Runs as one thread; identical on every rank.
 template <typename A>
 __global__ void k_select(const Rec<A>* __restrict__ recs, int nrec, A* __restrict__ td, int* __restrict__ M,
-                         int* __restrict__ point_slot, Decision<A>* __restrict__ dec) {
+                         int* __restrict__ point_slot, Decision<A>* __restrict__ dec, int* __restrict__ rescan_count) {
+    *rescan_count = 0;
     Rec<A> b = rec_none<A>();
     for (int r = 0; r < nrec; ++r)
         if (rec_less(recs[r], b)) b = recs[r];

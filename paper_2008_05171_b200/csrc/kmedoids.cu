@@ -147,6 +147,7 @@ struct Impl : ImplBase {
     std::vector<void*> bufs;        // every device allocation, freed in the destructor
     int *M = nullptr, *point_slot = nullptr, *near = nullptr, *sec = nullptr;
     T *MC = nullptr, *dn = nullptr, *ds = nullptr, *colbuf = nullptr;
+    int *rescan = nullptr, *rescan_count = nullptr;   // objects whose nearest/second slot was swapped
     RI* ri = nullptr;
     int *counts = nullptr, *offsets = nullptr, *seg_start = nullptr, *empty_slot = nullptr;
     int *head_slot = nullptr, *tail_slot = nullptr;
@@ -234,7 +235,7 @@ struct Impl : ImplBase {
         Pb = choose_parts(n, w, STREAM_COLS, RESIDENT_CTAS);
         wpad = (int)((w + 3) / 4 * 4);
         B = (int)cdiv(n, km::SORT_CHUNK);
-        ncomb = (int)cdiv(w, 256);
+        ncomb = (int)cdiv(w, 128);
         ntd = (int)std::min<int64_t>(cdiv(n, 256), 1024);
         KM_TRY(alloc(&M, k));
         KM_TRY(alloc(&point_slot, n));
@@ -244,6 +245,8 @@ struct Impl : ImplBase {
         KM_TRY(alloc(&dn, n));
         KM_TRY(alloc(&ds, n));
         KM_TRY(alloc(&colbuf, n));
+        KM_TRY(alloc(&rescan, n));
+        KM_TRY(alloc(&rescan_count, 1));
         KM_TRY(alloc(&ri, n));
         KM_TRY(alloc(&counts, (size_t)k * B));
         KM_TRY(alloc(&offsets, (size_t)k * B));
@@ -402,7 +405,7 @@ struct Impl : ImplBase {
         }
         KM_CKL();
         if (profiling) { KM_CK(record_ev(ev1)); pending_prof = true; }
-        km::k_swap_combine<A><<<ncomb, 256, 0, st>>>(w, c0, P, o_plus, o_head, o_tail, o_imin, o_islot, head_slot,
+        km::k_swap_combine<A><<<ncomb, 128, 0, st>>>(w, c0, P, o_plus, o_head, o_tail, o_imin, o_islot, head_slot,
                                                       tail_slot, R, empty_slot, point_slot, cand_v, cand_slot,
                                                       partials, counters, rec_local);
         KM_CKL();
@@ -459,12 +462,22 @@ struct Impl : ImplBase {
         return KM_OK;
     }
 
+    km_status assign_incremental() {
+        const int nb = (int)cdiv(n, 256);
+        km::k_assign_incremental<T, A><<<nb, 256, 0, st>>>(MC, (int)n, k, dec, near, sec, dn, ds, rescan,
+                                                            rescan_count);
+        KM_CKL();
+        km::k_assign_rescan<T, A><<<NUM_SMS, 256, 0, st>>>(MC, (int)n, k, dec, rescan, rescan_count, near, sec, dn,
+                                                           ds);
+        KM_CKL();
+        return KM_OK;
+    }
+
     km_status apply_local() {
         const int nb = (int)cdiv(n, 256);
         km::k_gather_decided_col<T, A><<<nb, 256, 0, st>>>(D, ld, (int)n, c0, c1, dec, MC, nullptr);
         KM_CKL();
-        km::k_assign_incremental<T, A><<<nb, 256, 0, st>>>(MC, (int)n, k, dec, near, sec, dn, ds);
-        KM_CKL();
+        KM_TRY(assign_incremental());
         return KM_OK;
     }
 
@@ -483,7 +496,7 @@ struct Impl : ImplBase {
         km_status s = eval_local();
         profiling = prof_save;
         if (s != KM_OK) return s;
-        km::k_select<A><<<1, 1, 0, st>>>(rec_local, 1, td, M, point_slot, dec);
+        km::k_select<A><<<1, 1, 0, st>>>(rec_local, 1, td, M, point_slot, dec, rescan_count);
         KM_CKL();
         KM_TRY(apply_local());
         KM_CK(cudaMemcpyAsync(h_dec, dec, sizeof(Dec), cudaMemcpyDeviceToHost, st));
@@ -572,7 +585,7 @@ struct Impl : ImplBase {
         KM_TRY((launch_seg<SG_NC, SG_RB, SG_S>(fp2_acc)));
         KM_CKL();
         if (profiling) { KM_CK(record_ev(ev1)); pending_prof = true; }
-        km::k_swap_combine<A><<<ncomb, 256, 0, st>>>(w, c0, P, o_plus, o_head, o_tail, o_imin, o_islot, head_slot,
+        km::k_swap_combine<A><<<ncomb, 128, 0, st>>>(w, c0, P, o_plus, o_head, o_tail, o_imin, o_islot, head_slot,
                                                       tail_slot, R, empty_slot, point_slot, cand_v, cand_slot,
                                                       partials, counters, rec_local, fp2_acc, fp2_plus);
         KM_CKL();
@@ -770,7 +783,7 @@ struct Impl : ImplBase {
     km_status shard_select(const int64_t* rcb, int32_t* found, int32_t* slot, int32_t* cand, int32_t* owner,
                            void* dtd) override {
         if (!rec_recv) return fail(KM_ECOMM, "call kmedoids_shard_exchange first");
-        km::k_select<A><<<1, 1, 0, st>>>(rec_recv, nranks, td, M, point_slot, dec);
+        km::k_select<A><<<1, 1, 0, st>>>(rec_recv, nranks, td, M, point_slot, dec, rescan_count);
         KM_CKL();
         KM_TRY(sync_dec());
         if (found) *found = h_dec->apply;
@@ -794,8 +807,7 @@ struct Impl : ImplBase {
         const int nb = (int)cdiv(n, 256);
         km::k_column_to_mc<T, A><<<nb, 256, 0, st>>>(colbuf, (int)n, dec, MC);
         KM_CKL();
-        km::k_assign_incremental<T, A><<<nb, 256, 0, st>>>(MC, (int)n, k, dec, near, sec, dn, ds);
-        KM_CKL();
+        KM_TRY(assign_incremental());
         KM_CK(cudaStreamSynchronize(st));
         return KM_OK;
     }
