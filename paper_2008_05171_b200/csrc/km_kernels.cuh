@@ -15,7 +15,7 @@
 namespace km {
 
 constexpr unsigned FULL = 0xffffffffu;
-constexpr int SORT_CHUNK = 1024;   // objects per block of the stable counting sort
+constexpr int SORT_CHUNK = 256;    // objects per block of the stable counting sort
 
 // ---------------------------------------------------------------------------
 // small helpers

@@ -355,7 +355,7 @@ struct Impl : ImplBase {
 
     // a2: sort rows by nearest slot, removal loss, part metadata.
     km_status prep() {
-        km::k_slot_hist<<<B, 256, k * sizeof(int), st>>>(near, (int)n, k, counts);
+        km::k_slot_hist<<<B, 128, k * sizeof(int), st>>>(near, (int)n, k, counts);
         KM_CKL();
         km::k_scan_counts<<<1, 1024, 0, st>>>(counts, k * B, B, k, offsets, seg_start, empty_slot);
         KM_CKL();
