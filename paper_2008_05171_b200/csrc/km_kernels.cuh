@@ -1505,12 +1505,20 @@ k_swap_stream_seg(const T* __restrict__ D, int64_t ld, int w, int wpad, int n, i
     }
 
     // ---------------- consumer warps ----------------
+    // Registers hold only plus[4] and seg[4] (the hot accumulators).  The
+    // per-column segment bookkeeping -- head (first, possibly cut, segment),
+    // the running lexicographic min of R_i + acc_c[i] and its slot -- lives in
+    // this part's output rows in global memory: each is touched only by its
+    // own lane and only at a segment end (~1 in 60 stages).
     const int cb = ctacol + warp * 128 + lane * 4;
     const bool active = cb < w;
-    A plus[4], seg[4], head[4], imin[4];
-    int islot[4];
+    const int64_t obase = (int64_t)q * w + cb;
+    int jmax = active ? min(4, w - cb) : 0;       // valid columns of this lane
+    A plus[4], seg[4];
 #pragma unroll
-    for (int j = 0; j < 4; ++j) { plus[j] = 0; seg[j] = 0; head[j] = 0; imin[j] = amax<A>(); islot[j] = -1; }
+    for (int j = 0; j < 4; ++j) { plus[j] = 0; seg[j] = 0; }
+    #pragma unroll
+    for (int j = 0; j < 4; ++j) if (j < jmax) { out_imin[obase + j] = amax<A>(); out_islot[obase + j] = -1; out_head[obase + j] = 0; }
     int cur = ri[p0].slot;
     bool first = true;
 
@@ -1524,19 +1532,16 @@ k_swap_stream_seg(const T* __restrict__ D, int64_t ld, int w, int wpad, int n, i
         if (slot != cur) {                       // segment boundary (warp-uniform, ~1 in 60 stages)
             if (first) {
 #pragma unroll
-                for (int j = 0; j < 4; ++j) head[j] = seg[j];
+                for (int j = 0; j < 4; ++j) if (j < jmax) out_head[obase + j] = seg[j];
                 first = false;
             } else {
-                if (out_acc) {
-#pragma unroll
-                    for (int j = 0; j < 4; ++j)
-                        if (cb + j < w) out_acc[(int64_t)cur * w + cb + j] = seg[j];
-                }
                 const A rv = R[cur];
 #pragma unroll
                 for (int j = 0; j < 4; ++j) {
+                    if (j >= jmax) continue;
+                    if (out_acc) out_acc[(int64_t)cur * w + cb + j] = seg[j];
                     const A val = rv + seg[j];
-                    if (val < imin[j]) { imin[j] = val; islot[j] = cur; }
+                    if (val < out_imin[obase + j]) { out_imin[obase + j] = val; out_islot[obase + j] = cur; }
                 }
             }
 #pragma unroll
@@ -1557,8 +1562,8 @@ k_swap_stream_seg(const T* __restrict__ D, int64_t ld, int w, int wpad, int n, i
         if (lane == 0) ptx::mbar_arrive(&empty[s]);
         // Rows >= nb (the short stage at a segment end) hold stale, possibly
         // never-written bytes, and columns >= w of the last tile are padding:
-        // give them thresholds nothing compares below (a per-lane select; the
-        // loaded values themselves are left untouched).
+        // give them thresholds nothing compares below (the loaded values are
+        // left untouched).
         if (nb < RB) {
 #pragma unroll
             for (int u = 1; u < RB; ++u)
@@ -1582,6 +1587,8 @@ k_swap_stream_seg(const T* __restrict__ D, int64_t ld, int w, int wpad, int n, i
 #pragma unroll
         for (int j = 0; j < 4; ++j) {
             if (wm & (1u << j)) {
+                // Alg.3 P:883-889 per row in select form (independent rows, no
+                // data-dependent branches), tree-summed: a short fp64 chain.
                 A tp[RB], ts[RB];
 #pragma unroll
                 for (int u = 0; u < RB; ++u) {
@@ -1595,22 +1602,13 @@ k_swap_stream_seg(const T* __restrict__ D, int64_t ld, int w, int wpad, int n, i
             }
         }
     }
-    if (first) {
-#pragma unroll
-        for (int j = 0; j < 4; ++j) { head[j] = seg[j]; seg[j] = 0; }
-    }
     if (!active) return;
-    const int64_t base = (int64_t)q * w;
 #pragma unroll
     for (int j = 0; j < 4; ++j) {
-        const int c = cb + j;
-        if (c < w) {
-            out_plus[base + c] = plus[j];
-            out_head[base + c] = head[j];
-            out_tail[base + c] = seg[j];
-            out_imin[base + c] = imin[j];
-            out_islot[base + c] = islot[j];
-        }
+        if (j >= jmax) continue;
+        if (first) { out_head[obase + j] = seg[j]; out_tail[obase + j] = 0; }
+        else out_tail[obase + j] = seg[j];
+        out_plus[obase + j] = plus[j];
     }
 }
 
