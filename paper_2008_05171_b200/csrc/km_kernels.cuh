@@ -1429,8 +1429,8 @@ struct SegCfg {
     static constexpr int THREADS = (NC + 1) * 32;
 };
 
-template <typename T, typename A, int NC, int RB, int S>
-__global__ void __launch_bounds__((NC + 1) * 32, 2)
+template <typename T, typename A, int NC, int RB, int S, int MINB = 2>
+__global__ void __launch_bounds__((NC + 1) * 32, MINB)
 k_swap_stream_seg(const T* __restrict__ D, int64_t ld, int w, int wpad, int n, int P,
                   const RowInfo<T>* __restrict__ ri, const A* __restrict__ R,
                   A* __restrict__ out_plus, A* __restrict__ out_head, A* __restrict__ out_tail,

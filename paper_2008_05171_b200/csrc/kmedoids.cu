@@ -70,8 +70,9 @@ constexpr int WT_NW = 4, WT_RB = 4, WT_S = 6;
 constexpr int CMP_NC = 7, CMP_RB = 4, CMP_S = 6;
 // TMA ring + per-warp hit queues: 7 consumer warps + 1 producer, 4 rows x 6 stages.
 constexpr int TQ_NC = 7, TQ_RB = 4, TQ_S = 6;
-// TMA ring with segment-aligned stages: 7 consumer warps + 1 producer, 4 rows x 7 stages.
-constexpr int SG_NC = 7, SG_RB = 4, SG_S = 7;
+// TMA ring with segment-aligned stages: 7 consumer warps + 1 producer, 4 rows x
+// 5 stages (~72 KB shared memory), 3 CTAs = 24 warps per SM (<= 80 registers).
+constexpr int SG_NC = 7, SG_RB = 4, SG_S = 5, SG_MINB = 3;
 constexpr int WT_COLS = WT_NW * 128;
 constexpr int WT_RESIDENT = 4;
 constexpr int TMA_RESIDENT = 2;
@@ -213,6 +214,8 @@ struct Impl : ImplBase {
         if (ev && strcmp(ev, "cmp") == 0) stream_kind = 6;
         if (ev && strcmp(ev, "tmaq") == 0) stream_kind = 9;
         if (ev && strcmp(ev, "seg") == 0) stream_kind = 10;
+        if (ev && strcmp(ev, "seg6") == 0) stream_kind = 11;
+        if (ev && strcmp(ev, "seg5") == 0) stream_kind = 12;
         if (ev && strcmp(ev, "ldg") == 0) stream_kind = 0;
         if (ev && strcmp(ev, "wtma") == 0) stream_kind = 2;
 
@@ -224,7 +227,9 @@ struct Impl : ImplBase {
         use_graph = !(eg && eg[0] == '0');
         const char* dnc = getenv("KM_DEBUG_NOCOMPUTE");        // perf experiment only: wrong results
         debug_nocompute = (dnc && dnc[0] == '1') ? 1 : 0;
-        P = stream_kind == 10 ? choose_parts(n, w, SG_NC * 128, 2)
+        P = stream_kind == 10 ? choose_parts(n, w, SG_NC * 128, SG_MINB)
+            : stream_kind == 11 ? choose_parts(n, w, 6 * 128, 3)
+            : stream_kind == 12 ? choose_parts(n, w, 5 * 128, 4)
             : stream_kind == 9 ? choose_parts(n, w, TQ_NC * 128, 2)
             : stream_kind == 6 ? choose_parts(n, w, CMP_NC * 128, 2)
 
@@ -373,7 +378,11 @@ struct Impl : ImplBase {
         KM_TRY(prep());
         if (profiling) KM_CK(record_ev(ev0));
         if (stream_kind == 10) {  // TMA ring, segment-aligned stages
-            KM_TRY((launch_seg<SG_NC, SG_RB, SG_S>(nullptr)));
+            KM_TRY((launch_seg<SG_NC, SG_RB, SG_S, SG_MINB>(nullptr)));
+        } else if (stream_kind == 11) {
+            KM_TRY((launch_seg<6, 4, 6, 3>(nullptr)));
+        } else if (stream_kind == 12) {
+            KM_TRY((launch_seg<5, 4, 5, 4>(nullptr)));
         } else if (stream_kind == 9) {   // TMA ring + per-warp hit queues
             KM_TRY((launch_tmaq<TQ_NC, TQ_RB, TQ_S>(nullptr)));
         } else if (stream_kind == 6) {   // compacted hits
@@ -412,10 +421,10 @@ struct Impl : ImplBase {
         return KM_OK;
     }
 
-    template <int NC, int RB, int S>
+    template <int NC, int RB, int S, int MINB = 2>
     km_status launch_seg(A* acc_out) {
         using C = km::SegCfg<T, NC, RB, S>;
-        auto kern = km::k_swap_stream_seg<T, A, NC, RB, S>;
+        auto kern = km::k_swap_stream_seg<T, A, NC, RB, S, MINB>;
         if (!seg_attr_set) {
             KM_CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM));
             seg_attr_set = true;
@@ -582,7 +591,7 @@ struct Impl : ImplBase {
         KM_TRY(prep());
         // FastPAM2 always uses the segment-aligned TMA stream (it stores acc_c[i]).
         if (profiling) KM_CK(record_ev(ev0));
-        KM_TRY((launch_seg<SG_NC, SG_RB, SG_S>(fp2_acc)));
+        KM_TRY((launch_seg<SG_NC, SG_RB, SG_S, SG_MINB>(fp2_acc)));
         KM_CKL();
         if (profiling) { KM_CK(record_ev(ev1)); pending_prof = true; }
         km::k_swap_combine<A><<<ncomb, 128, 0, st>>>(w, c0, P, o_plus, o_head, o_tail, o_imin, o_islot, head_slot,
