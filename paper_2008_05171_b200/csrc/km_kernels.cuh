@@ -15,7 +15,7 @@
 namespace km {
 
 constexpr unsigned FULL = 0xffffffffu;
-constexpr int SORT_CHUNK = 256;    // objects per block of the stable counting sort
+constexpr int SORT_CHUNK_MIN = 256;   // objects per block of the stable counting sort (at least)
 
 // ---------------------------------------------------------------------------
 // small helpers
@@ -277,12 +277,12 @@ __global__ void k_td_from_dn(const T* __restrict__ dn, int n, A* __restrict__ pa
 // ---------------------------------------------------------------------------
 
 // counts[s*B + b] = #objects of chunk b with nearest slot s.
-__global__ void k_slot_hist(const int* __restrict__ near, int n, int k, int* __restrict__ counts) {
+__global__ void k_slot_hist(const int* __restrict__ near, int n, int k, int chunk, int* __restrict__ counts) {
     extern __shared__ int h[];
     const int B = gridDim.x, b = blockIdx.x;
     for (int s = threadIdx.x; s < k; s += blockDim.x) h[s] = 0;
     __syncthreads();
-    const int e0 = b * SORT_CHUNK, e1 = min(n, e0 + SORT_CHUNK);
+    const int e0 = b * chunk, e1 = min(n, e0 + chunk);
     for (int e = e0 + threadIdx.x; e < e1; e += blockDim.x) atomicAdd(&h[near[e]], 1);
     __syncthreads();
     for (int s = threadIdx.x; s < k; s += blockDim.x) counts[(int64_t)s * B + b] = h[s];
@@ -323,13 +323,13 @@ __global__ void k_scan_counts(const int* __restrict__ counts, int total, int B, 
 // given cache, so every sum over it is deterministic.
 template <typename T>
 __global__ void k_slot_scatter(const int* __restrict__ near, const T* __restrict__ dn,
-                               const T* __restrict__ ds, int n, int k, const int* __restrict__ offsets,
+                               const T* __restrict__ ds, int n, int k, int chunk, const int* __restrict__ offsets,
                                RowInfo<T>* __restrict__ ri, int natural_order) {
     extern __shared__ int cnt[];
     const int B = gridDim.x, b = blockIdx.x, lane = threadIdx.x;
     for (int s = lane; s < k; s += 32) cnt[s] = offsets[(int64_t)s * B + b];
     __syncwarp();
-    const int e0 = b * SORT_CHUNK, e1 = min(n, e0 + SORT_CHUNK);
+    const int e0 = b * chunk, e1 = min(n, e0 + chunk);
     const unsigned lt = (1u << lane) - 1u;
     for (int base = e0; base < e1; base += 32) {
         const int e = base + lane;
@@ -1725,12 +1725,14 @@ __global__ void k_select(const Rec<A>* __restrict__ recs, int nrec, A* __restric
 template <typename A>
 __global__ void k_fp2_slot_best(int w, int64_t col_begin, const A* __restrict__ acc, const A* __restrict__ plus,
                                 const A* __restrict__ R, const int* __restrict__ seg_start,
-                                const int* __restrict__ point_slot, Rec<A>* __restrict__ out) {
-    const int i = blockIdx.x;
+                                const int* __restrict__ point_slot, Rec<A>* __restrict__ part) {
+    // grid (k, FP2_SPLIT): block (i, y) scans columns [y*w/SPLIT, (y+1)*w/SPLIT) of row i
+    const int i = blockIdx.x, y = blockIdx.y;
     const bool empty = seg_start[i] == seg_start[i + 1];
     const A ri = R[i];
+    const int a = (int)((int64_t)y * w / gridDim.y), z = (int)((int64_t)(y + 1) * w / gridDim.y);
     Rec<A> b = rec_none<A>();
-    for (int cl = threadIdx.x; cl < w; cl += blockDim.x) {
+    for (int cl = a + threadIdx.x; cl < z; cl += blockDim.x) {
         const int64_t c = col_begin + cl;
         if (point_slot[c] >= 0) continue;
         const A v = ri + (empty ? (A)0 : acc[(int64_t)i * w + cl]) + plus[cl];
@@ -1738,7 +1740,20 @@ __global__ void k_fp2_slot_best(int w, int64_t col_begin, const A* __restrict__ 
         if (rec_less(r, b)) b = r;        // same slot: (v, c) order
     }
     b = block_min_rec(b);
-    if (threadIdx.x == 0) out[i] = b;
+    if (threadIdx.x == 0) part[(int64_t)i * gridDim.y + y] = b;
+}
+
+// Per slot: lexicographic min over the FP2_SPLIT partials (fixed order).
+template <typename A>
+__global__ void k_fp2_slot_reduce(int k, int split, const Rec<A>* __restrict__ part, Rec<A>* __restrict__ out) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= k) return;
+    Rec<A> b = rec_none<A>();
+    for (int y = 0; y < split; ++y) {
+        const Rec<A> r = part[(int64_t)i * split + y];
+        if (rec_less(r, b)) b = r;
+    }
+    out[i] = b;
 }
 
 // The sequential phase of one FastPAM2 iteration as ONE cooperative kernel

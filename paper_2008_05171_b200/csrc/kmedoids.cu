@@ -73,6 +73,7 @@ constexpr int TQ_NC = 7, TQ_RB = 4, TQ_S = 6;
 // TMA ring with segment-aligned stages: 7 consumer warps + 1 producer, 4 rows x
 // 5 stages (~72 KB shared memory), 3 CTAs = 24 warps per SM (<= 80 registers).
 constexpr int SG_NC = 7, SG_RB = 4, SG_S = 5, SG_MINB = 3;
+constexpr int FP2_SPLIT = 8;   // column splits of the FastPAM2 per-slot reduction
 constexpr int WT_COLS = WT_NW * 128;
 constexpr int WT_RESIDENT = 4;
 constexpr int TMA_RESIDENT = 2;
@@ -136,13 +137,14 @@ struct Impl : ImplBase {
     int64_t ld = 0, c0 = 0, c1 = 0;
     int w = 0;
     cudaStream_t st = nullptr;
-    int P = 1, Pb = 1, B = 1, ncomb = 1, ntd = 1;
+    int P = 1, Pb = 1, B = 1, ncomb = 1, ntd = 1, sort_chunk = 256;
     int nranks = 1;
     int wpad = 0;
     bool use_tma = true;
     int stream_kind = 2;
     int debug_natural = 0;
     int debug_nocompute = 0;
+    int debug_fp2 = 0;
     bool ready = false;     // medoids + cache valid
 
     std::vector<void*> bufs;        // every device allocation, freed in the destructor
@@ -166,6 +168,7 @@ struct Impl : ImplBase {
     A* fp2_acc = nullptr;           // [k][w] complete acc_c[i]
     A* fp2_plus = nullptr;          // [w]    dTD^{+x_c}
     Rec* fp2_best = nullptr;        // [k]    per-slot (v_i, i, c_i)
+    Rec* fp2_part = nullptr;        // [k][FP2_SPLIT] partial per-slot bests
     int* fp2_order = nullptr;       // [k]
     A* fp2_partials = nullptr;      // cooperative-kernel block partials
     int fp2_blocks = 0;
@@ -223,6 +226,8 @@ struct Impl : ImplBase {
         use_tma = stream_kind == 1;
         const char* dbg = getenv("KM_DEBUG_NATURAL_ORDER");   // perf experiment only: wrong results
         debug_natural = (dbg && dbg[0] == '1') ? 1 : 0;
+        const char* df = getenv("KM_DEBUG_FP2");
+        debug_fp2 = (df && df[0] == '1') ? 1 : 0;
         const char* eg = getenv("KM_GRAPH");
         use_graph = !(eg && eg[0] == '0');
         const char* dnc = getenv("KM_DEBUG_NOCOMPUTE");        // perf experiment only: wrong results
@@ -239,7 +244,10 @@ struct Impl : ImplBase {
                                : choose_parts(n, w, STREAM_COLS, RESIDENT_CTAS);
         Pb = choose_parts(n, w, STREAM_COLS, RESIDENT_CTAS);
         wpad = (int)((w + 3) / 4 * 4);
-        B = (int)cdiv(n, km::SORT_CHUNK);
+        // counting-sort chunk: >= 256 objects and at most 128 chunks (keeps the
+        // k x B count matrix of the one-block scan small)
+        sort_chunk = (int)std::max<int64_t>(km::SORT_CHUNK_MIN, cdiv(cdiv(n, 128), 32) * 32);
+        B = (int)cdiv(n, sort_chunk);
         ncomb = (int)cdiv(w, 128);
         ntd = (int)std::min<int64_t>(cdiv(n, 256), 1024);
         KM_TRY(alloc(&M, k));
@@ -360,11 +368,11 @@ struct Impl : ImplBase {
 
     // a2: sort rows by nearest slot, removal loss, part metadata.
     km_status prep() {
-        km::k_slot_hist<<<B, 128, k * sizeof(int), st>>>(near, (int)n, k, counts);
+        km::k_slot_hist<<<B, 256, k * sizeof(int), st>>>(near, (int)n, k, sort_chunk, counts);
         KM_CKL();
         km::k_scan_counts<<<1, 1024, 0, st>>>(counts, k * B, B, k, offsets, seg_start, empty_slot);
         KM_CKL();
-        km::k_slot_scatter<T><<<B, 32, k * sizeof(int), st>>>(near, dn, ds, (int)n, k, offsets, ri, debug_natural);
+        km::k_slot_scatter<T><<<B, 32, k * sizeof(int), st>>>(near, dn, ds, (int)n, k, sort_chunk, offsets, ri, debug_natural);
         KM_CKL();
         km::k_removal_loss<T, A><<<(unsigned)cdiv((int64_t)k * 32, 256), 256, 0, st>>>(ri, seg_start, k, R, empty_slot);
         KM_CKL();
@@ -571,11 +579,15 @@ struct Impl : ImplBase {
         KM_TRY(alloc(&fp2_acc, (size_t)k * w));
         KM_TRY(alloc(&fp2_plus, w));
         KM_TRY(alloc(&fp2_best, k));
+        KM_TRY(alloc(&fp2_part, (size_t)k * FP2_SPLIT));
         KM_TRY(alloc(&fp2_order, k));
         int dev = 0, per_sm = 0, nsm = 0;
         KM_CK(cudaGetDevice(&dev));
         KM_CK(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
         KM_CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, km::k_fp2_sequential<T, A>, 256, 0));
+        // all co-resident blocks: a re-evaluation step is a strided gather of one
+        // column (n sectors) and wants every SM's load units (measured: one
+        // block per SM is ~1.6x slower despite cheaper grid syncs)
         fp2_blocks = (int)std::min<int64_t>((int64_t)nsm * std::max(per_sm, 1), std::max<int64_t>(1, cdiv(n, 256)));
         KM_TRY(alloc(&fp2_partials, fp2_blocks));
         trace_cap = k;
@@ -588,7 +600,11 @@ struct Impl : ImplBase {
     // stream pass, then the sequential multi-swap phase on the device.
     km_status swap_iter_fp2(int32_t* swaps_out, void* td_out) {
         KM_TRY(fp2_alloc());
+        cudaEvent_t dbg[6];
+        if (debug_fp2) for (auto& e : dbg) cudaEventCreate(&e);
+        if (debug_fp2) cudaEventRecord(dbg[0], st);
         KM_TRY(prep());
+        if (debug_fp2) cudaEventRecord(dbg[1], st);
         // FastPAM2 always uses the segment-aligned TMA stream (it stores acc_c[i]).
         if (profiling) KM_CK(record_ev(ev0));
         KM_TRY((launch_seg<SG_NC, SG_RB, SG_S, SG_MINB>(fp2_acc)));
@@ -598,8 +614,13 @@ struct Impl : ImplBase {
                                                       tail_slot, R, empty_slot, point_slot, cand_v, cand_slot,
                                                       partials, counters, rec_local, fp2_acc, fp2_plus);
         KM_CKL();
-        km::k_fp2_slot_best<A><<<k, 256, 0, st>>>(w, c0, fp2_acc, fp2_plus, R, seg_start, point_slot, fp2_best);
+        if (debug_fp2) cudaEventRecord(dbg[2], st);
+        km::k_fp2_slot_best<A><<<dim3(k, FP2_SPLIT), 256, 0, st>>>(w, c0, fp2_acc, fp2_plus, R, seg_start, point_slot,
+                                                                     fp2_part);
         KM_CKL();
+        km::k_fp2_slot_reduce<A><<<(unsigned)cdiv(k, 128), 128, 0, st>>>(k, FP2_SPLIT, fp2_part, fp2_best);
+        KM_CKL();
+        if (debug_fp2) cudaEventRecord(dbg[3], st);
         A tdh;
         KM_CK(cudaMemcpyAsync(h_best.data(), fp2_best, k * sizeof(Rec), cudaMemcpyDeviceToHost, st));
         KM_CK(cudaMemcpyAsync(&tdh, td, sizeof(A), cudaMemcpyDeviceToHost, st));
@@ -637,15 +658,26 @@ struct Impl : ImplBase {
         KM_CK(cudaMemcpyAsync(dec, &hd, sizeof(Dec), cudaMemcpyHostToDevice, st));
         KM_CK(cudaMemcpyAsync(fp2_order, order.data(), order.size() * sizeof(int), cudaMemcpyHostToDevice, st));
         int m = (int)order.size();
+        if (debug_fp2) fprintf(stderr, "[fp2] improving slots m=%d\n", m);
         const T* Dp = D; int64_t ldv = ld; int nn = (int)n; int kk = k;
         int* Mp = M; int* psp = point_slot; T* MCp = MC; int* nr = near; int* sc = sec; T* dnp = dn; T* dsp = ds;
         T* cb = colbuf; A* tdp = td; A* pp = fp2_partials; Dec* dp = dec; Rec* tr = trace; int tc = trace_cap;
         int* op = fp2_order; Rec* bp = fp2_best;
         void* args[] = {&Dp, &ldv, &nn, &kk, &op, &m, &bp, &Mp, &psp, &MCp, &nr, &sc, &dnp, &dsp, &cb, &tdp, &pp,
                         &dp, &tr, &tc};
+        if (debug_fp2) cudaEventRecord(dbg[4], st);
         KM_CK(cudaLaunchCooperativeKernel((void*)km::k_fp2_sequential<T, A>, dim3(fp2_blocks), dim3(256), args, 0,
                                           st));
         ++launches;
+        if (debug_fp2) {
+            cudaEventRecord(dbg[5], st);
+            cudaEventSynchronize(dbg[5]);
+            float t[5];
+            for (int q = 0; q < 5; ++q) cudaEventElapsedTime(&t[q], dbg[q], dbg[q + 1]);
+            fprintf(stderr, "[fp2] prep %.3f stream+combine %.3f slot_best %.3f host %.3f sequential %.3f ms (m=%d)\n",
+                    t[0], t[1], t[2], t[3], t[4], m);
+            for (auto& e : dbg) cudaEventDestroy(e);
+        }
         KM_CK(cudaMemcpyAsync(h_dec, dec, sizeof(Dec), cudaMemcpyDeviceToHost, st));
         KM_CK(cudaStreamSynchronize(st));
         const int done = h_dec->swaps;
