@@ -183,6 +183,34 @@ km_status kmedoids_shard_select(km_handle* h, const int64_t* rank_col_begin, int
 km_status kmedoids_shard_pack_column(km_handle* h, int32_t cand);
 km_status kmedoids_shard_apply(km_handle* h);
 
+/* Sharded FastPAM2 (reading R6) iteration, on every rank:
+ *   1. kmedoids_fp2_shard_eval(h)      per-slot best (v_i, i, c_i) over the local
+ *                                      candidates -> record_send (k records)
+ *   2. all-gather the records           (caller; k*16 bytes per rank)
+ *   3. kmedoids_fp2_shard_plan(h, rcb, &m, &maxcnt)
+ *                                      per-slot min over ranks, improving slots in
+ *                                      (v_i, i) order (m of them; 0 = converged),
+ *                                      this rank's planned candidate columns
+ *                                      packed into col_send (maxcnt columns)
+ *   4. if m > 0: all-gather maxcnt*n elements per rank from col_send into
+ *      col_recv (rank order), then kmedoids_fp2_shard_apply(h, ...) runs the
+ *      sequential phase redundantly on every rank (identical results).
+ * Buffers are device memory owned by the handle. */
+typedef struct {
+    void* record_send;          /* k records of 16 bytes */
+    void* record_recv;          /* R*k records, rank order */
+    size_t record_bytes;        /* k*16 */
+    void* col_send;             /* col_capacity columns of n elements */
+    void* col_recv;             /* R*col_capacity columns (use R*maxcnt) */
+    size_t col_bytes_per_column;
+    int32_t col_capacity;       /* = k */
+} km_fp2_exchange;
+
+km_status kmedoids_fp2_shard_exchange(km_handle* h, int32_t nranks, km_fp2_exchange* out);
+km_status kmedoids_fp2_shard_eval(km_handle* h);
+km_status kmedoids_fp2_shard_plan(km_handle* h, const int64_t* rank_col_begin, int32_t* m_out, int32_t* maxcnt_out);
+km_status kmedoids_fp2_shard_apply(km_handle* h, int32_t* swaps_done_out, void* td_out);
+
 /* Sharded BUILD: step 0 evaluates the distance sums (first medoid), steps
  * 1..k-1 the BUILD gains of the local candidates into record_send; after the
  * gather, kmedoids_build_select picks the global (value, c) minimum, the

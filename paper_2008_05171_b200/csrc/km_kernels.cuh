@@ -1769,7 +1769,8 @@ __global__ void k_fp2_slot_reduce(int k, int split, const Rec<A>* __restrict__ p
 // Applied swaps are appended to trace[] (slot, c, dTD).
 template <typename T, typename A>
 __global__ void __launch_bounds__(256)
-k_fp2_sequential(const T* __restrict__ D, int64_t ld, int n, int k, const int* __restrict__ order, int m,
+k_fp2_sequential(const T* __restrict__ D, int64_t ld, const T* __restrict__ colsrc, const int* __restrict__ colidx,
+                 int n, int k, const int* __restrict__ order, int m,
                  const Rec<A>* __restrict__ best, int* __restrict__ M, int* __restrict__ point_slot,
                  T* __restrict__ MC, int* __restrict__ near, int* __restrict__ sec, T* __restrict__ dn,
                  T* __restrict__ ds, T* __restrict__ colbuf, A* __restrict__ td, A* __restrict__ partials,
@@ -1791,7 +1792,8 @@ k_fp2_sequential(const T* __restrict__ D, int64_t ld, int n, int k, const int* _
         // phase 1: gather column c, partial sums of dTD(m_i, x_c)
         A part = 0;
         for (int o = tid; o < n; o += nth) {
-            const T x = D[(int64_t)o * ld + c];
+            // candidate column: gathered (sharded) or read from D (single GPU)
+            const T x = colsrc ? colsrc[(int64_t)colidx[r] * n + o] : D[(int64_t)o * ld + c];
             colbuf[o] = x;
             if (r > 0) {
                 const T a = dn[o], b = ds[o];

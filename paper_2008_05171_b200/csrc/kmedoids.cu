@@ -111,6 +111,10 @@ struct ImplBase {
     virtual km_status build_select(const int64_t* rcb, int32_t* cand, int32_t* owner, void* gain) = 0;
     virtual km_status build_apply(int32_t step) = 0;
     virtual km_status last_swaps_out(int32_t* slots, int32_t* cands, void* dtds, int32_t cap, int32_t* count) = 0;
+    virtual km_status fp2_shard_exchange(int32_t nranks, km_fp2_exchange* out) = 0;
+    virtual km_status fp2_shard_eval() = 0;
+    virtual km_status fp2_shard_plan(const int64_t* rcb, int32_t* m_out, int32_t* maxcnt_out) = 0;
+    virtual km_status fp2_shard_apply(int32_t* swaps_out, void* td_out) = 0;
     bool profiling = false;
     double prof_ms = 0.0;
     int64_t prof_launches = 0;
@@ -596,15 +600,11 @@ struct Impl : ImplBase {
         return KM_OK;
     }
 
-    // One FastPAM2 iteration (reading R6): per-slot best candidates from one
-    // stream pass, then the sequential multi-swap phase on the device.
-    km_status swap_iter_fp2(int32_t* swaps_out, void* td_out) {
+    // FastPAM2 step 1-3 (reading R6), local part: per-slot best over this
+    // handle's candidates into fp2_best (device).
+    km_status fp2_eval_local() {
         KM_TRY(fp2_alloc());
-        cudaEvent_t dbg[6];
-        if (debug_fp2) for (auto& e : dbg) cudaEventCreate(&e);
-        if (debug_fp2) cudaEventRecord(dbg[0], st);
         KM_TRY(prep());
-        if (debug_fp2) cudaEventRecord(dbg[1], st);
         // FastPAM2 always uses the segment-aligned TMA stream (it stores acc_c[i]).
         if (profiling) KM_CK(record_ev(ev0));
         KM_TRY((launch_seg<SG_NC, SG_RB, SG_S, SG_MINB>(fp2_acc)));
@@ -614,24 +614,17 @@ struct Impl : ImplBase {
                                                       tail_slot, R, empty_slot, point_slot, cand_v, cand_slot,
                                                       partials, counters, rec_local, fp2_acc, fp2_plus);
         KM_CKL();
-        if (debug_fp2) cudaEventRecord(dbg[2], st);
         km::k_fp2_slot_best<A><<<dim3(k, FP2_SPLIT), 256, 0, st>>>(w, c0, fp2_acc, fp2_plus, R, seg_start, point_slot,
                                                                      fp2_part);
         KM_CKL();
         km::k_fp2_slot_reduce<A><<<(unsigned)cdiv(k, 128), 128, 0, st>>>(k, FP2_SPLIT, fp2_part, fp2_best);
         KM_CKL();
-        if (debug_fp2) cudaEventRecord(dbg[3], st);
-        A tdh;
-        KM_CK(cudaMemcpyAsync(h_best.data(), fp2_best, k * sizeof(Rec), cudaMemcpyDeviceToHost, st));
-        KM_CK(cudaMemcpyAsync(&tdh, td, sizeof(A), cudaMemcpyDeviceToHost, st));
-        KM_CK(cudaMemcpyAsync(h_dec, dec, sizeof(Dec), cudaMemcpyDeviceToHost, st));
-        KM_CK(cudaStreamSynchronize(st));
-        if (profiling && pending_prof) {
-            float ms = 0.f;
-            KM_CK(cudaEventElapsedTime(&ms, ev0, ev1));
-            prof_ms += ms; prof_launches += 1; pending_prof = false;
-        }
-        // steps 4-5: improving slots ordered by (v_i, i)
+        return KM_OK;
+    }
+
+    // Steps 4-5 on the host (identical on every rank): improving slots of the
+    // global per-slot bests h_best ordered by (v_i, i).
+    std::vector<int> fp2_order_slots(A tdh) {
         std::vector<int> order;
         for (int i = 0; i < k; ++i) {
             const Rec& b = h_best[i];
@@ -642,6 +635,25 @@ struct Impl : ImplBase {
         std::stable_sort(order.begin(), order.end(), [&](int a, int b) {
             return h_best[a].v < h_best[b].v || (h_best[a].v == h_best[b].v && a < b);
         });
+        return order;
+    }
+
+    km_status fp2_finish_profiling() {
+        if (profiling && pending_prof) {
+            float ms = 0.f;
+            KM_CK(cudaEventElapsedTime(&ms, ev0, ev1));
+            prof_ms += ms; prof_launches += 1; pending_prof = false;
+        }
+        return KM_OK;
+    }
+
+    // Steps 6-7: the sequential phase (one cooperative kernel).  colsrc/colidx
+    // give each order entry's candidate column (sharded: gathered columns);
+    // nullptr = read the column from D.  Counts the iteration.
+    km_status fp2_sequential(const std::vector<int>& order, const T* colsrc, const int* colidx_dev,
+                             int32_t* swaps_out, void* td_out) {
+        KM_CK(cudaMemcpyAsync(h_dec, dec, sizeof(Dec), cudaMemcpyDeviceToHost, st));
+        KM_CK(cudaStreamSynchronize(st));
         Dec hd = *h_dec;
         hd.iters += 1;
         hd.apply = 0;
@@ -650,6 +662,7 @@ struct Impl : ImplBase {
         if (order.empty()) {
             KM_CK(cudaMemcpyAsync(dec, &hd, sizeof(Dec), cudaMemcpyHostToDevice, st));
             KM_CK(cudaStreamSynchronize(st));
+            *h_dec = hd;
             if (swaps_out) *swaps_out = 0;
             copy_td(td_out);
             return KM_CONVERGED;
@@ -663,21 +676,12 @@ struct Impl : ImplBase {
         int* Mp = M; int* psp = point_slot; T* MCp = MC; int* nr = near; int* sc = sec; T* dnp = dn; T* dsp = ds;
         T* cb = colbuf; A* tdp = td; A* pp = fp2_partials; Dec* dp = dec; Rec* tr = trace; int tc = trace_cap;
         int* op = fp2_order; Rec* bp = fp2_best;
-        void* args[] = {&Dp, &ldv, &nn, &kk, &op, &m, &bp, &Mp, &psp, &MCp, &nr, &sc, &dnp, &dsp, &cb, &tdp, &pp,
-                        &dp, &tr, &tc};
-        if (debug_fp2) cudaEventRecord(dbg[4], st);
+        const T* csp = colsrc; const int* cip = colidx_dev;
+        void* args[] = {&Dp, &ldv, &csp, &cip, &nn, &kk, &op, &m, &bp, &Mp, &psp, &MCp, &nr, &sc, &dnp, &dsp, &cb,
+                        &tdp, &pp, &dp, &tr, &tc};
         KM_CK(cudaLaunchCooperativeKernel((void*)km::k_fp2_sequential<T, A>, dim3(fp2_blocks), dim3(256), args, 0,
                                           st));
         ++launches;
-        if (debug_fp2) {
-            cudaEventRecord(dbg[5], st);
-            cudaEventSynchronize(dbg[5]);
-            float t[5];
-            for (int q = 0; q < 5; ++q) cudaEventElapsedTime(&t[q], dbg[q], dbg[q + 1]);
-            fprintf(stderr, "[fp2] prep %.3f stream+combine %.3f slot_best %.3f host %.3f sequential %.3f ms (m=%d)\n",
-                    t[0], t[1], t[2], t[3], t[4], m);
-            for (auto& e : dbg) cudaEventDestroy(e);
-        }
         KM_CK(cudaMemcpyAsync(h_dec, dec, sizeof(Dec), cudaMemcpyDeviceToHost, st));
         KM_CK(cudaStreamSynchronize(st));
         const int done = h_dec->swaps;
@@ -692,6 +696,120 @@ struct Impl : ImplBase {
         if (swaps_out) *swaps_out = done;
         copy_td(td_out);
         return KM_OK;
+    }
+
+    // One single-GPU FastPAM2 iteration (reading R6).
+    km_status swap_iter_fp2(int32_t* swaps_out, void* td_out) {
+        KM_TRY(fp2_eval_local());
+        A tdh;
+        KM_CK(cudaMemcpyAsync(h_best.data(), fp2_best, k * sizeof(Rec), cudaMemcpyDeviceToHost, st));
+        KM_CK(cudaMemcpyAsync(&tdh, td, sizeof(A), cudaMemcpyDeviceToHost, st));
+        KM_CK(cudaStreamSynchronize(st));
+        KM_TRY(fp2_finish_profiling());
+        const std::vector<int> order = fp2_order_slots(tdh);
+        return fp2_sequential(order, nullptr, nullptr, swaps_out, td_out);
+    }
+
+    // ---- sharded FastPAM2 ------------------------------------------------------
+    // record_send: this rank's k per-slot bests; record_recv: R x k gathered.
+    // col_send: the columns of the planned candidates this rank owns
+    // (cap x n); col_recv: R x cap x n gathered (rank r's block at r*maxcnt).
+    Rec* f2_rec_recv = nullptr;
+    T* f2_col_send = nullptr;
+    T* f2_col_recv = nullptr;
+    int* f2_colidx = nullptr;
+    int f2_ranks = 0, f2_maxcnt = 0;
+    std::vector<int> f2_order;
+
+    km_status fp2_shard_exchange(int32_t nr, km_fp2_exchange* out) override {
+        if (nr < 1) return fail(KM_EINVAL, "nranks must be >= 1");
+        KM_TRY(fp2_alloc());
+        if (f2_ranks != nr) {
+            if (f2_ranks != 0) return fail(KM_ECOMM, "fp2 exchange already sized for %d ranks", f2_ranks);
+            f2_ranks = nr;
+            KM_TRY(alloc(&f2_rec_recv, (size_t)nr * k));
+            KM_TRY(alloc(&f2_col_send, (size_t)k * n));
+            KM_TRY(alloc(&f2_col_recv, (size_t)nr * k * n));
+            KM_TRY(alloc(&f2_colidx, k));
+        }
+        out->record_send = fp2_best;
+        out->record_recv = f2_rec_recv;
+        out->record_bytes = (size_t)k * sizeof(Rec);
+        out->col_send = f2_col_send;
+        out->col_recv = f2_col_recv;
+        out->col_bytes_per_column = (size_t)n * sizeof(T);
+        out->col_capacity = k;
+        return KM_OK;
+    }
+
+    km_status fp2_shard_eval() override {
+        if (!ready) return fail(KM_EINVAL, "no medoids set");
+        if (!f2_ranks) return fail(KM_ECOMM, "call kmedoids_fp2_shard_exchange first");
+        return fp2_eval_local();
+    }
+
+    km_status fp2_shard_plan(const int64_t* rcb, int32_t* m_out, int32_t* maxcnt_out) override {
+        if (!f2_ranks) return fail(KM_ECOMM, "call kmedoids_fp2_shard_exchange first");
+        const int nr = f2_ranks;
+        int me = -1;
+        for (int r = 0; r < nr; ++r)
+            if (rcb[r] == c0 && rcb[r + 1] == c1) me = r;
+        if (me < 0) return fail(KM_ECOMM, "rank_col_begin does not contain this handle's columns");
+        std::vector<Rec> all((size_t)nr * k);
+        A tdh;
+        KM_CK(cudaMemcpyAsync(all.data(), f2_rec_recv, all.size() * sizeof(Rec), cudaMemcpyDeviceToHost, st));
+        KM_CK(cudaMemcpyAsync(&tdh, td, sizeof(A), cudaMemcpyDeviceToHost, st));
+        KM_CK(cudaStreamSynchronize(st));
+        KM_TRY(fp2_finish_profiling());
+        for (int i = 0; i < k; ++i) {                // lexicographic min over ranks, rank order
+            Rec b = km::rec_none<A>();
+            for (int r = 0; r < nr; ++r)
+                if (km::rec_less(all[(size_t)r * k + i], b)) b = all[(size_t)r * k + i];
+            h_best[i] = b;
+        }
+        KM_CK(cudaMemcpyAsync(fp2_best, h_best.data(), k * sizeof(Rec), cudaMemcpyHostToDevice, st));
+        f2_order = fp2_order_slots(tdh);
+        // distinct candidates in order of first use, grouped by owner rank
+        std::vector<std::vector<int>> owned(nr);
+        std::vector<int> pos_of(f2_order.size()), own_of(f2_order.size());
+        std::vector<std::pair<int, int>> seen;    // (candidate, index in owner list)
+        for (size_t r = 0; r < f2_order.size(); ++r) {
+            const int c = h_best[f2_order[r]].c;
+            int ow = -1;
+            for (int q = 0; q < nr; ++q)
+                if (c >= rcb[q] && c < rcb[q + 1]) ow = q;
+            if (ow < 0) return fail(KM_ECOMM, "candidate %d has no owner", c);
+            int pos = -1;
+            for (auto& sp : seen)
+                if (sp.first == c) pos = sp.second;
+            if (pos < 0) {
+                pos = (int)owned[ow].size();
+                owned[ow].push_back(c);
+                seen.push_back({c, pos});
+            }
+            pos_of[r] = pos;
+            own_of[r] = ow;
+        }
+        int maxcnt = 0;
+        for (auto& v : owned) maxcnt = std::max(maxcnt, (int)v.size());
+        f2_maxcnt = maxcnt;
+        std::vector<int> colidx(f2_order.size());
+        for (size_t r = 0; r < f2_order.size(); ++r) colidx[r] = own_of[r] * maxcnt + pos_of[r];
+        if (!colidx.empty())
+            KM_CK(cudaMemcpyAsync(f2_colidx, colidx.data(), colidx.size() * sizeof(int), cudaMemcpyHostToDevice, st));
+        const int nb = (int)cdiv(n, 256);
+        for (size_t j = 0; j < owned[me].size(); ++j) {
+            km::k_gather_col<T><<<nb, 256, 0, st>>>(D, ld, (int)n, c0, owned[me][j], f2_col_send + j * (size_t)n);
+            KM_CKL();
+        }
+        KM_CK(cudaStreamSynchronize(st));
+        if (m_out) *m_out = (int)f2_order.size();
+        if (maxcnt_out) *maxcnt_out = maxcnt;
+        return KM_OK;
+    }
+
+    km_status fp2_shard_apply(int32_t* swaps_out, void* td_out) override {
+        return fp2_sequential(f2_order, f2_col_recv, f2_colidx, swaps_out, td_out);
     }
 
     // ---- BUILD ---------------------------------------------------------------
@@ -1073,6 +1191,28 @@ km_status kmedoids_shard_pack_column(km_handle* h, int32_t cand) {
 km_status kmedoids_shard_apply(km_handle* h) {
     KM_H();
     return h->impl->shard_apply();
+}
+
+km_status kmedoids_fp2_shard_exchange(km_handle* h, int32_t nranks, km_fp2_exchange* out) {
+    KM_H();
+    if (!out) return fail(KM_EINVAL, "out is NULL");
+    return h->impl->fp2_shard_exchange(nranks, out);
+}
+
+km_status kmedoids_fp2_shard_eval(km_handle* h) {
+    KM_H();
+    return h->impl->fp2_shard_eval();
+}
+
+km_status kmedoids_fp2_shard_plan(km_handle* h, const int64_t* rank_col_begin, int32_t* m_out, int32_t* maxcnt_out) {
+    KM_H();
+    if (!rank_col_begin) return fail(KM_EINVAL, "rank_col_begin is NULL");
+    return h->impl->fp2_shard_plan(rank_col_begin, m_out, maxcnt_out);
+}
+
+km_status kmedoids_fp2_shard_apply(km_handle* h, int32_t* swaps_done_out, void* td_out) {
+    KM_H();
+    return h->impl->fp2_shard_apply(swaps_done_out, td_out);
 }
 
 km_status kmedoids_build_eval(km_handle* h, int32_t step) {

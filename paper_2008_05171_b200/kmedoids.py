@@ -40,6 +40,13 @@ class _Exchange(ctypes.Structure):
                 ("column_bytes", ctypes.c_size_t)]
 
 
+class _Fp2Exchange(ctypes.Structure):
+    _fields_ = [("record_send", ctypes.c_void_p), ("record_recv", ctypes.c_void_p),
+                ("record_bytes", ctypes.c_size_t), ("col_send", ctypes.c_void_p),
+                ("col_recv", ctypes.c_void_p), ("col_bytes_per_column", ctypes.c_size_t),
+                ("col_capacity", ctypes.c_int32)]
+
+
 _lib = None
 
 
@@ -73,6 +80,10 @@ def load_library() -> ctypes.CDLL:
         "kmedoids_shard_select": [vp, vp, vp, vp, vp, vp, vp],
         "kmedoids_shard_pack_column": [vp, i32],
         "kmedoids_shard_apply": [vp],
+        "kmedoids_fp2_shard_exchange": [vp, i32, ctypes.POINTER(_Fp2Exchange)],
+        "kmedoids_fp2_shard_eval": [vp],
+        "kmedoids_fp2_shard_plan": [vp, vp, vp, vp],
+        "kmedoids_fp2_shard_apply": [vp, vp, vp],
         "kmedoids_build_eval": [vp, i32],
         "kmedoids_build_select": [vp, vp, vp, vp, vp],
         "kmedoids_build_apply": [vp, i32],
@@ -256,6 +267,25 @@ class KMedoids:
 
     def shard_apply(self):
         _check(load_library().kmedoids_shard_apply(self.h))
+
+    def fp2_shard_exchange(self, nranks: int) -> _Fp2Exchange:
+        x = _Fp2Exchange()
+        _check(load_library().kmedoids_fp2_shard_exchange(self.h, int(nranks), ctypes.byref(x)))
+        return x
+
+    def fp2_shard_eval(self):
+        _check(load_library().kmedoids_fp2_shard_eval(self.h))
+
+    def fp2_shard_plan(self, rank_col_begin):
+        rcb = np.ascontiguousarray(np.asarray(rank_col_begin, dtype=np.int64))
+        m = np.zeros(1, np.int32); mx = np.zeros(1, np.int32)
+        _check(load_library().kmedoids_fp2_shard_plan(self.h, _p(rcb), _p(m), _p(mx)))
+        return int(m[0]), int(mx[0])
+
+    def fp2_shard_apply(self):
+        sw = np.zeros(1, np.int32); td = np.zeros(1, self.acc)
+        s = _check(load_library().kmedoids_fp2_shard_apply(self.h, _p(sw), _p(td)), ok=(KM_OK, KM_CONVERGED))
+        return s == KM_CONVERGED, int(sw[0]), td[0].item()
 
     def build_eval(self, step: int):
         _check(load_library().kmedoids_build_eval(self.h, int(step)))

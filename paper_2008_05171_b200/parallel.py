@@ -79,6 +79,20 @@ class LocalComm:
             if r != owner:
                 col.copy_(src)
 
+    def allgather_fp2_records(self, handles):
+        xs = [h.fp2_exchange_tensors(self.world) for h in handles]
+        nb = xs[0][0].numel()
+        for x in xs:
+            for r, y in enumerate(xs):
+                x[1][r * nb:(r + 1) * nb].copy_(y[0])
+
+    def allgather_fp2_columns(self, handles, maxcnt: int):
+        xs = [h.fp2_exchange_tensors(self.world) for h in handles]
+        cb = xs[0][4] * maxcnt                     # bytes per rank
+        for x in xs:
+            for r, y in enumerate(xs):
+                x[3][r * cb:(r + 1) * cb].copy_(y[2][:cb])
+
     def max_over_ranks(self, x: float) -> float:
         return x
 
@@ -102,6 +116,17 @@ class TorchComm:
         (h,) = handles
         _, _, col = h.exchange_tensors(self.world)
         self.dist.broadcast(col, src=owner, group=self.group)
+
+    def allgather_fp2_records(self, handles):
+        (h,) = handles
+        send, recv, _, _, _ = h.fp2_exchange_tensors(self.world)
+        self.dist.all_gather_into_tensor(recv, send, group=self.group)
+
+    def allgather_fp2_columns(self, handles, maxcnt: int):
+        (h,) = handles
+        _, _, csend, crecv, colb = h.fp2_exchange_tensors(self.world)
+        cb = colb * maxcnt
+        self.dist.all_gather_into_tensor(crecv[:cb * self.world], csend[:cb], group=self.group)
 
     def max_over_ranks(self, x: float) -> float:
         import torch
@@ -176,6 +201,30 @@ def build(handles, comm, cb, k: int):
     return chosen
 
 
+def fp2_iter(handles, comm, cb):
+    """One sharded FastPAM2 iteration (reading R6); returns (converged, swaps).
+
+    per-slot bests of the local candidates -> all-gather (k*16 B per rank) ->
+    identical plan on every rank -> all-gather of the planned candidates'
+    columns (each rank sends the ones it owns) -> every rank runs the
+    sequential phase redundantly on the gathered columns."""
+    for h in handles:
+        h.fp2_exchange_tensors(comm.world)      # sizes the exchange buffers once
+        h.fp2_shard_eval()
+    comm.allgather_fp2_records(handles)
+    plans = [h.fp2_shard_plan(cb) for h in handles]
+    m, maxcnt = plans[0]
+    if any(p != plans[0] for p in plans):
+        raise RuntimeError(f"ranks disagree on the FastPAM2 plan: {plans}")
+    if m > 0:
+        comm.allgather_fp2_columns(handles, maxcnt)
+    res = [h.fp2_shard_apply() for h in handles]
+    if any(r[:2] != res[0][:2] for r in res):
+        raise RuntimeError(f"ranks disagree on the FastPAM2 swaps: {res}")
+    conv, swaps, td = res[0]
+    return conv, swaps
+
+
 def run(handles, comm, cb, max_iter: int = 2000):
     trace = []
     it = 0
@@ -216,6 +265,20 @@ class CudaShard:
             col = torch.as_tensor(_DevBytes(x.column, x.column_bytes), device=dev)
             self._x = (send, recv, col)
         return self._x
+
+    def fp2_exchange_tensors(self, world: int):
+        """(record_send, record_recv, col_send, col_recv, bytes per column) as uint8 tensors."""
+        import torch
+        if getattr(self, "_f2", None) is None:
+            x = self.km.fp2_shard_exchange(world)
+            dev = self.km.D.device
+            cap = x.col_capacity * x.col_bytes_per_column
+            self._f2 = (torch.as_tensor(_DevBytes(x.record_send, x.record_bytes), device=dev),
+                        torch.as_tensor(_DevBytes(x.record_recv, x.record_bytes * world), device=dev),
+                        torch.as_tensor(_DevBytes(x.col_send, cap), device=dev),
+                        torch.as_tensor(_DevBytes(x.col_recv, cap * world), device=dev),
+                        int(x.col_bytes_per_column))
+        return self._f2
 
     def __getattr__(self, name):       # shard_eval, shard_select, ... -> the handle
         return getattr(self.km, name)
@@ -260,8 +323,13 @@ def bench_main(args):
         set_medoids(hs, comm, cb, kmsynth.random_medoids(cfg), n)
     torch.cuda.synchronize()
     init_s = comm.max_over_ranks(time.perf_counter() - t0)
+    fp2 = getattr(args, "variant", "fastpam1") == "fastpam2"
+
+    def step():
+        return fp2_iter(hs, comm, cb) if fp2 else swap_iter(hs, comm, cb)
+
     for _ in range(args.warmup):
-        swap_iter(hs, comm, cb)
+        step()
     h.km.set_profiling(True)
     h.km.stream_time(reset=True)
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -269,7 +337,7 @@ def bench_main(args):
     dist.barrier()
     e0.record(stream)
     for _ in range(args.steps):
-        swap_iter(hs, comm, cb)
+        step()
     e1.record(stream)
     torch.cuda.synchronize()
     dist.barrier()
@@ -293,8 +361,9 @@ def bench_main(args):
                 "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
                 "scaling": "strong", "vs_baseline": None,
                 "dtype": "f32->f64" if cfg.metric == kmsynth.L2_F32 else "u32->int64", "data": "synthetic",
-                "config": {"workload": f"{cfg.name} n={n} k={k} column-sharded over {world} GPUs",
-                           "n": n, "k": k, "variant": "fastpam1", "parallelism": f"column-shard x{world}"},
+                "config": {"workload": f"{cfg.name} n={n} k={k} ({'f32 Euclidean' if cfg.metric else 'u32 L1 x100'}, "
+                                       f"{cfg.init} init, {args.variant}) column-sharded over {world} GPUs",
+                           "n": n, "k": k, "variant": args.variant, "parallelism": f"column-shard x{world}"},
                 "s_per_iteration": ms_step / 1e3,
                 "roofline": {"bound": "hbm", "achieved": ach, "peak": peak, "unit": "GB/s", "frac": ach / peak,
                              "traffic": None, "kernel": "k_swap_stream (rank 0 slab)", "kernel_ms": k1_avg},

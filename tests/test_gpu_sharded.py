@@ -81,3 +81,43 @@ def test_sharded_random_init_set_medoids():
     st = hs[1].km.get_state()
     assert st.medoids.tolist() == ref.medoids.tolist() and st.td == ref.td
     assert st.assignment.tolist() == ref.assignment.tolist()
+
+
+@pytest.mark.parametrize("world,cid,n,k", [(2, 5, 900, 11), (3, 5, 1300, 17), (4, 3, 800, 9)])
+def test_sharded_fastpam2_equals_single_gpu(world, cid, n, k):
+    from paper_2008_05171_b200 import KMedoids, parallel
+    cfg = kmsynth.CONFIGS[cid]
+    X = kmsynth.make_points(cfg, n=n)
+    Dt = kmsynth.dist_cuda(X, cfg.metric)
+    M0 = kmsynth.random_medoids(cfg, k=k, n=n)
+    single = KMedoids(Dt, n, k)
+    single.set_medoids(M0)
+    tr1 = []
+    while True:
+        conv, sw, td = single.swap_iter("fastpam2")
+        tr1.append(single.last_swaps())
+        if conv:
+            break
+    st1 = single.get_state()
+    hs, cb = shards(Dt, n, k, world)
+    comm = parallel.LocalComm(world)
+    parallel.set_medoids(hs, comm, cb, M0, n)
+    tr2 = []
+    while True:
+        conv, sw = parallel.fp2_iter(hs, comm, cb)
+        tr2.append(hs[0].km.last_swaps())
+        if conv:
+            break
+    if cfg.metric == kmsynth.L1_INT:
+        assert tr2 == tr1
+    else:
+        assert [[t[:2] for t in it] for it in tr2] == [[t[:2] for t in it] for it in tr1]
+    for h in hs:
+        st = h.km.get_state()
+        assert st.medoids.tolist() == st1.medoids.tolist()
+        assert st.assignment.tolist() == st1.assignment.tolist()
+        assert st.n_iter == st1.n_iter and st.n_swaps == st1.n_swaps
+    if cfg.metric == kmsynth.L1_INT:
+        D = kmsynth.as_numpy_D(Dt)[:, :n]
+        ref = oracle.swap_run(D, M0, oracle.FASTPAM2)
+        assert st1.medoids.tolist() == ref.medoids.tolist() and st1.td == ref.td

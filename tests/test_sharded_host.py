@@ -199,3 +199,57 @@ def test_column_bounds_and_records():
     recs = parallel.decode_records(raw, np.int64)
     assert recs == [(-5, 2, 40), (-5, 1, 99)]
     assert parallel.lexmin_records(recs) == (-5, 1, 99)     # smaller slot wins (reading R1)
+
+
+class BufShard:
+    """Only the FastPAM2 exchange buffers (CPU tensors), rank-tagged contents."""
+
+    def __init__(self, rank, world, k, n):
+        self.rank = rank
+        colb = 4 * n
+        self.x = (torch.full((16 * k,), rank + 1, dtype=torch.uint8), torch.zeros(16 * k * world, dtype=torch.uint8),
+                  torch.zeros(k * colb, dtype=torch.uint8), torch.zeros(k * colb * world, dtype=torch.uint8), colb)
+        for j in range(k):
+            self.x[2][j * colb:(j + 1) * colb] = (10 * rank + j) % 251
+
+    def fp2_exchange_tensors(self, world):
+        return self.x
+
+
+def _fp2_worker(rank, world, port, q):
+    import torch.distributed as dist
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        k, n, maxcnt = 5, 7, 3
+        h = BufShard(rank, world, k, n)
+        comm = parallel.TorchComm()
+        comm.allgather_fp2_records([h])
+        comm.allgather_fp2_columns([h], maxcnt)
+        q.put((rank, h.x[1].numpy().copy(), h.x[3].numpy().copy()))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_gloo_world2_fp2_exchange_layout():
+    """Records land in rank order; rank r's first maxcnt columns land at
+    [r*maxcnt*colbytes, (r+1)*maxcnt*colbytes) -- the layout
+    kmedoids_fp2_shard_plan's column indices assume."""
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    ps = [ctx.Process(target=_fp2_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in ps:
+        p.start()
+    out = sorted([q.get(timeout=120) for _ in ps], key=lambda t: t[0])
+    for p in ps:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    k, n, maxcnt, colb = 5, 7, 3, 28
+    for rank, rec, cols in out:
+        assert (rec[:16 * k] == 1).all() and (rec[16 * k:] == 2).all()
+        for r in range(2):
+            for j in range(maxcnt):
+                blk = cols[(r * maxcnt + j) * colb:(r * maxcnt + j + 1) * colb]
+                assert (blk == (10 * r + j) % 251).all()
