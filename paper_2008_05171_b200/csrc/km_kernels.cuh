@@ -2,7 +2,7 @@
 //
 // Kernel map:
 //   a1/a5  k_gather_medoid_cols, k_gather_decided_col, k_assign_full, k_assign_incremental
-//   a2     k_slot_hist, k_scan_counts, k_slot_scatter, k_removal_loss, k_part_meta
+//   a2     k_slot_hist, k_scan_within_slot, k_scan_slots, k_slot_scatter, k_removal_loss, k_part_meta
 //   a3     k_swap_stream   (the HBM stream; Alg.3, Eq. eqn:better-change3)
 //   a4     k_swap_combine  (per-candidate argmin over slots) + k_select
 //   a7     k_build_stream / k_build_combine / k_build_select / k_build_apply (Alg.1)
@@ -288,33 +288,54 @@ __global__ void k_slot_hist(const int* __restrict__ near, int n, int k, int chun
     for (int s = threadIdx.x; s < k; s += blockDim.x) counts[(int64_t)s * B + b] = h[s];
 }
 
-// Exclusive scan of counts (slot-major) -> offsets; seg_start[s] = first
-// sorted position of slot s, seg_start[k] = n.  Single block of 1024.
-__global__ void k_scan_counts(const int* __restrict__ counts, int total, int B, int k,
-                              int* __restrict__ offsets, int* __restrict__ seg_start, int* __restrict__ empty_slot) {
+// Within-slot exclusive scan of the chunk counts, one warp per slot:
+// offsets[s*B + b] = #objects of slot s in chunks < b; tot[s] = slot total.
+__global__ void k_scan_within_slot(const int* __restrict__ counts, int B, int k, int* __restrict__ offsets,
+                                   int* __restrict__ tot) {
+    const int s = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+    if (s >= k) return;
+    int run = 0;
+    for (int b0 = 0; b0 < B; b0 += 32) {
+        const int b = b0 + lane;
+        const int c = b < B ? counts[(int64_t)s * B + b] : 0;
+        int incl = c;
+#pragma unroll
+        for (int d = 1; d < 32; d <<= 1) {
+            const int y = __shfl_up_sync(FULL, incl, d);
+            if (lane >= d) incl += y;
+        }
+        if (b < B) offsets[(int64_t)s * B + b] = run + incl - c;
+        run += __shfl_sync(FULL, incl, 31);
+    }
+    if (lane == 0) tot[s] = run;
+}
+
+// Exclusive scan of the k slot totals (one block): seg_start[s] = first
+// sorted position of slot s, seg_start[k] = n.  Also resets *empty_slot for
+// k_removal_loss, which runs after this kernel.
+__global__ void k_scan_slots(const int* __restrict__ tot, int k, int* __restrict__ seg_start,
+                             int* __restrict__ empty_slot) {
     __shared__ int sums[1024];
     const int t = threadIdx.x, nt = blockDim.x;
-    if (t == 0) *empty_slot = INT_MAX;      // reset for k_removal_loss (runs after this kernel)
-    const int per = (total + nt - 1) / nt;
-    const int a = t * per, z = min(total, a + per);
+    if (t == 0) *empty_slot = INT_MAX;
+    const int per = (k + nt - 1) / nt;
+    const int a = t * per, z = min(k, a + per);
     int s = 0;
-    for (int i = a; i < z; ++i) s += counts[i];
+    for (int i = a; i < z; ++i) s += tot[i];
     sums[t] = s;
     __syncthreads();
     for (int off = 1; off < nt; off <<= 1) {     // Hillis-Steele inclusive scan
-        int v = (t >= off) ? sums[t - off] : 0;
+        const int v = (t >= off) ? sums[t - off] : 0;
         __syncthreads();
         sums[t] += v;
         __syncthreads();
     }
     int run = sums[t] - s;
     for (int i = a; i < z; ++i) {
-        offsets[i] = run;
-        run += counts[i];
+        seg_start[i] = run;
+        run += tot[i];
     }
-    __syncthreads();
-    for (int sl = t; sl < k; sl += nt) seg_start[sl] = offsets[(int64_t)sl * B];
-    if (t == 0) seg_start[k] = sums[nt - 1];
+    if (t == nt - 1) seg_start[k] = sums[nt - 1];
 }
 
 // Stable scatter: one warp per chunk walks its objects in index order and
@@ -324,10 +345,10 @@ __global__ void k_scan_counts(const int* __restrict__ counts, int total, int B, 
 template <typename T>
 __global__ void k_slot_scatter(const int* __restrict__ near, const T* __restrict__ dn,
                                const T* __restrict__ ds, int n, int k, int chunk, const int* __restrict__ offsets,
-                               RowInfo<T>* __restrict__ ri, int natural_order) {
+                               const int* __restrict__ seg_start, RowInfo<T>* __restrict__ ri, int natural_order) {
     extern __shared__ int cnt[];
     const int B = gridDim.x, b = blockIdx.x, lane = threadIdx.x;
-    for (int s = lane; s < k; s += 32) cnt[s] = offsets[(int64_t)s * B + b];
+    for (int s = lane; s < k; s += 32) cnt[s] = seg_start[s] + offsets[(int64_t)s * B + b];
     __syncwarp();
     const int e0 = b * chunk, e1 = min(n, e0 + chunk);
     const unsigned lt = (1u << lane) - 1u;

@@ -156,7 +156,7 @@ struct Impl : ImplBase {
     T *MC = nullptr, *dn = nullptr, *ds = nullptr, *colbuf = nullptr;
     int *rescan = nullptr, *rescan_count = nullptr;   // objects whose nearest/second slot was swapped
     RI* ri = nullptr;
-    int *counts = nullptr, *offsets = nullptr, *seg_start = nullptr, *empty_slot = nullptr;
+    int *counts = nullptr, *offsets = nullptr, *seg_start = nullptr, *empty_slot = nullptr, *slot_tot = nullptr;
     int *head_slot = nullptr, *tail_slot = nullptr;
     A *R = nullptr, *o_plus = nullptr, *o_head = nullptr, *o_tail = nullptr, *o_imin = nullptr;
     int* o_islot = nullptr;
@@ -268,6 +268,7 @@ struct Impl : ImplBase {
         KM_TRY(alloc(&counts, (size_t)k * B));
         KM_TRY(alloc(&offsets, (size_t)k * B));
         KM_TRY(alloc(&seg_start, k + 1));
+        KM_TRY(alloc(&slot_tot, k));
         KM_TRY(alloc(&empty_slot, 1));
         KM_TRY(alloc(&head_slot, P));
         KM_TRY(alloc(&tail_slot, P));
@@ -374,9 +375,11 @@ struct Impl : ImplBase {
     km_status prep() {
         km::k_slot_hist<<<B, 256, k * sizeof(int), st>>>(near, (int)n, k, sort_chunk, counts);
         KM_CKL();
-        km::k_scan_counts<<<1, 1024, 0, st>>>(counts, k * B, B, k, offsets, seg_start, empty_slot);
+        km::k_scan_within_slot<<<(unsigned)cdiv((int64_t)k * 32, 256), 256, 0, st>>>(counts, B, k, offsets, slot_tot);
         KM_CKL();
-        km::k_slot_scatter<T><<<B, 32, k * sizeof(int), st>>>(near, dn, ds, (int)n, k, sort_chunk, offsets, ri, debug_natural);
+        km::k_scan_slots<<<1, 1024, 0, st>>>(slot_tot, k, seg_start, empty_slot);
+        KM_CKL();
+        km::k_slot_scatter<T><<<B, 32, k * sizeof(int), st>>>(near, dn, ds, (int)n, k, sort_chunk, offsets, seg_start, ri, debug_natural);
         KM_CKL();
         km::k_removal_loss<T, A><<<(unsigned)cdiv((int64_t)k * 32, 256), 256, 0, st>>>(ri, seg_start, k, R, empty_slot);
         KM_CKL();
