@@ -345,7 +345,8 @@ __global__ void k_scan_slots(const int* __restrict__ tot, int k, int* __restrict
 template <typename T>
 __global__ void k_slot_scatter(const int* __restrict__ near, const T* __restrict__ dn,
                                const T* __restrict__ ds, int n, int k, int chunk, const int* __restrict__ offsets,
-                               const int* __restrict__ seg_start, RowInfo<T>* __restrict__ ri, int natural_order) {
+                               const int* __restrict__ seg_start, RowInfo<T>* __restrict__ ri, int natural_order,
+                               double2* __restrict__ rowd) {
     extern __shared__ int cnt[];
     const int B = gridDim.x, b = blockIdx.x, lane = threadIdx.x;
     for (int s = lane; s < k; s += 32) cnt[s] = seg_start[s] + offsets[(int64_t)s * B + b];
@@ -368,7 +369,9 @@ __global__ void k_slot_scatter(const int* __restrict__ near, const T* __restrict
         if (valid) {
             RowInfo<T> r;
             r.o = e; r.slot = s; r.dn = dn[e]; r.ds = ds[e];
-            ri[natural_order ? e : bp + rank] = r;
+            const int pos = natural_order ? e : bp + rank;
+            ri[pos] = r;
+            if (rowd) rowd[pos] = make_double2((double)r.dn, (double)r.ds);
         }
     }
 }
@@ -1446,7 +1449,8 @@ struct SegCfg {
     static constexpr int RIB = S * RB * 16;
     static constexpr int NBB = S * 4;                   // rows in each stage
     static constexpr int BARB = 2 * S * 8;
-    static constexpr int SMEM = DATAB + RIB + 16 * ((NBB + 15) / 16) + BARB;
+    static constexpr int RDB = S * RB * 16;             // float path: (double dn, double ds) per row
+    static constexpr int SMEM = DATAB + RIB + RDB + 16 * ((NBB + 15) / 16) + BARB;
     static constexpr int THREADS = (NC + 1) * 32;
 };
 
@@ -1455,14 +1459,16 @@ __global__ void __launch_bounds__((NC + 1) * 32, MINB)
 k_swap_stream_seg(const T* __restrict__ D, int64_t ld, int w, int wpad, int n, int P,
                   const RowInfo<T>* __restrict__ ri, const A* __restrict__ R,
                   A* __restrict__ out_plus, A* __restrict__ out_head, A* __restrict__ out_tail,
-                  A* __restrict__ out_imin, int* __restrict__ out_islot, A* __restrict__ out_acc) {
+                  A* __restrict__ out_imin, int* __restrict__ out_islot, A* __restrict__ out_acc,
+                  const double2* __restrict__ rowd) {
     using C = SegCfg<T, NC, RB, S>;
     using V = typename Vec4<T>::type;
     extern __shared__ __align__(128) unsigned char smem[];
     T* sdata = reinterpret_cast<T*>(smem);
     RowInfo<T>* sri = reinterpret_cast<RowInfo<T>*>(smem + C::DATAB);
-    int* snb = reinterpret_cast<int*>(smem + C::DATAB + C::RIB);
-    uint64_t* full = reinterpret_cast<uint64_t*>(smem + C::DATAB + C::RIB + 16 * ((C::NBB + 15) / 16));
+    double2* srd = reinterpret_cast<double2*>(smem + C::DATAB + C::RIB);
+    int* snb = reinterpret_cast<int*>(smem + C::DATAB + C::RIB + C::RDB);
+    uint64_t* full = reinterpret_cast<uint64_t*>(smem + C::DATAB + C::RIB + C::RDB + 16 * ((C::NBB + 15) / 16));
     uint64_t* empty = full + S;
 
     const int q = blockIdx.y;
@@ -1504,13 +1510,14 @@ k_swap_stream_seg(const T* __restrict__ D, int64_t ld, int w, int wpad, int n, i
             const int nb = __ffs(~same) - 1;     // rows of slot0 at the head of the window (>= 1)
             if (lane == 0) {
                 snb[s] = nb;
-                ptx::mbar_expect_tx(&full[s], (uint32_t)nb * (cbytes + 16u));
+                ptx::mbar_expect_tx(&full[s], (uint32_t)nb * (cbytes + (rowd ? 32u : 16u)));
             }
             __syncwarp();
             if (lane < nb)
                 ptx::bulk_g2s(sdata + (size_t)(s * RB + lane) * C::COLS, D + (int64_t)o_l * ld + ctacol, cbytes,
                               &full[s], pol);
             if (lane == 0) ptx::bulk_g2s(sri + s * RB, ri + pr, (uint32_t)nb * 16u, &full[s]);
+            if (lane == 1 && rowd) ptx::bulk_g2s(srd + s * RB, rowd + pr, (uint32_t)nb * 16u, &full[s]);
             pr += nb;
             // slide the row window by nb (rows already loaded move down, new ones are fetched)
             const int o_sh = __shfl_down_sync(FULL, o_l, nb);
@@ -1603,8 +1610,14 @@ k_swap_stream_seg(const T* __restrict__ D, int64_t ld, int w, int wpad, int n, i
         const unsigned wm = __reduce_or_sync(FULL, m);
         if (wm == 0) continue;
         A dnA[RB], dsA[RB], dnds[RB];
+        if constexpr (Acc<T>::is_float) {       // widened thresholds staged by the producer (no F2F)
+            const double2* sr = srd + s * RB;
 #pragma unroll
-        for (int u = 0; u < RB; ++u) { dnA[u] = (A)dn[u]; dsA[u] = (A)ds[u]; dnds[u] = dnA[u] - dsA[u]; }
+            for (int u = 0; u < RB; ++u) { const double2 q = sr[u]; dnA[u] = q.x; dsA[u] = q.y; dnds[u] = dnA[u] - dsA[u]; }
+        } else {
+#pragma unroll
+            for (int u = 0; u < RB; ++u) { dnA[u] = (A)dn[u]; dsA[u] = (A)ds[u]; dnds[u] = dnA[u] - dsA[u]; }
+        }
 #pragma unroll
         for (int j = 0; j < 4; ++j) {
             if (wm & (1u << j)) {

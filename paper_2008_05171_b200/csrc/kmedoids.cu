@@ -156,6 +156,7 @@ struct Impl : ImplBase {
     T *MC = nullptr, *dn = nullptr, *ds = nullptr, *colbuf = nullptr;
     int *rescan = nullptr, *rescan_count = nullptr;   // objects whose nearest/second slot was swapped
     RI* ri = nullptr;
+    double2* rowd = nullptr;        // float path: (double dn, double ds) in sorted order
     int *counts = nullptr, *offsets = nullptr, *seg_start = nullptr, *empty_slot = nullptr, *slot_tot = nullptr;
     int *head_slot = nullptr, *tail_slot = nullptr;
     A *R = nullptr, *o_plus = nullptr, *o_head = nullptr, *o_tail = nullptr, *o_imin = nullptr;
@@ -265,6 +266,7 @@ struct Impl : ImplBase {
         KM_TRY(alloc(&rescan, n));
         KM_TRY(alloc(&rescan_count, 1));
         KM_TRY(alloc(&ri, n));
+        if (km::Acc<T>::is_float) KM_TRY(alloc(&rowd, n));
         KM_TRY(alloc(&counts, (size_t)k * B));
         KM_TRY(alloc(&offsets, (size_t)k * B));
         KM_TRY(alloc(&seg_start, k + 1));
@@ -379,7 +381,7 @@ struct Impl : ImplBase {
         KM_CKL();
         km::k_scan_slots<<<1, 1024, 0, st>>>(slot_tot, k, seg_start, empty_slot);
         KM_CKL();
-        km::k_slot_scatter<T><<<B, 32, k * sizeof(int), st>>>(near, dn, ds, (int)n, k, sort_chunk, offsets, seg_start, ri, debug_natural);
+        km::k_slot_scatter<T><<<B, 32, k * sizeof(int), st>>>(near, dn, ds, (int)n, k, sort_chunk, offsets, seg_start, ri, debug_natural, rowd);
         KM_CKL();
         km::k_removal_loss<T, A><<<(unsigned)cdiv((int64_t)k * 32, 256), 256, 0, st>>>(ri, seg_start, k, R, empty_slot);
         KM_CKL();
@@ -446,7 +448,7 @@ struct Impl : ImplBase {
         }
         dim3 g((unsigned)cdiv(w, C::COLS), P);
         kern<<<g, C::THREADS, C::SMEM, st>>>(D, ld, w, wpad, (int)n, P, ri, R, o_plus, o_head, o_tail, o_imin, o_islot,
-                                              acc_out);
+                                              acc_out, rowd);
         return KM_OK;
     }
 
