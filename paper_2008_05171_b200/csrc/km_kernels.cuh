@@ -1965,6 +1965,112 @@ k_build_stream(const T* __restrict__ D, int64_t ld, int w, int n, int P, const T
         if (cb + j < w) out[base + cb + j] = acc[j];
 }
 
+// BUILD stream, TMA variant (default): the producer / ring of
+// k_swap_stream_seg with rows in natural order; per stage the consumers
+// fold "d < d_n" over the 4 rows x 4 columns into a REDUX.OR mask and
+// update only the columns with a hit (MODE 1), or sum every element with a
+// 4-row tree (MODE 0).  3 CTAs x 8 warps per SM.
+template <typename T, typename A, int NC, int RB, int S, int MINB, int MODE>
+__global__ void __launch_bounds__((NC + 1) * 32, MINB)
+k_build_tma(const T* __restrict__ D, int64_t ld, int w, int wpad, int n, int P, const T* __restrict__ dnear,
+            A* __restrict__ out) {
+    using C = SegCfg<T, NC, RB, S>;
+    using V = typename Vec4<T>::type;
+    extern __shared__ __align__(128) unsigned char smem[];
+    T* sdata = reinterpret_cast<T*>(smem);
+    uint64_t* full = reinterpret_cast<uint64_t*>(smem + C::DATAB);
+    uint64_t* empty = full + S;
+    const int q = blockIdx.y;
+    const int64_t p0 = (int64_t)q * n / P, p1 = (int64_t)(q + 1) * n / P;
+    const int nstages = (int)((p1 - p0 + RB - 1) / RB);
+    const int ctacol = blockIdx.x * C::COLS;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    if (threadIdx.x == 0) {
+        for (int st = 0; st < S; ++st) {
+            ptx::mbar_init(&full[st], 1);
+            ptx::mbar_init(&empty[st], NC);
+        }
+        ptx::fence_mbar_init();
+    }
+    __syncthreads();
+    if (warp == NC) {
+        const uint32_t cbytes = (uint32_t)min(C::COLS, wpad - ctacol) * (uint32_t)sizeof(T);
+        const uint64_t pol = ptx::policy_evict_first();
+        for (int st = 0; st < nstages; ++st) {
+            const int s = st % S;
+            if (st >= S) ptx::mbar_wait(&empty[s], ((st / S) & 1) ^ 1);
+            const int64_t pr = p0 + (int64_t)st * RB;
+            const int nb = (int)min((int64_t)RB, p1 - pr);
+            if (lane == 0) ptx::mbar_expect_tx(&full[s], (uint32_t)nb * cbytes);
+            __syncwarp();
+            if (lane < nb)
+                ptx::bulk_g2s(sdata + (size_t)(s * RB + lane) * C::COLS, D + (pr + lane) * ld + ctacol, cbytes,
+                              &full[s], pol);
+        }
+        return;
+    }
+    const int cb = ctacol + warp * 128 + lane * 4;
+    const bool active = cb < w;
+    A acc[4] = {0, 0, 0, 0};
+    for (int st = 0; st < nstages; ++st) {
+        const int s = st % S;
+        const int64_t pr = p0 + (int64_t)st * RB;
+        const int nb = (int)min((int64_t)RB, p1 - pr);
+        T dv[RB];
+#pragma unroll
+        for (int u = 0; u < RB; ++u)        // d_nearest of the stage's rows (uniform loads, L1)
+            dv[u] = (MODE == 1 && u < nb) ? dnear[pr + u] : never_lt<T>();
+        ptx::mbar_wait(&full[s], (st / S) & 1);
+        T x[RB][4];
+        const T* srow = sdata + (size_t)(s * RB) * C::COLS + (warp * 128 + lane * 4);
+#pragma unroll
+        for (int u = 0; u < RB; ++u) {
+            const V v = *reinterpret_cast<const V*>(srow + (size_t)u * C::COLS);
+            memcpy(&x[u][0], &v.x, sizeof(T)); memcpy(&x[u][1], &v.y, sizeof(T));
+            memcpy(&x[u][2], &v.z, sizeof(T)); memcpy(&x[u][3], &v.w, sizeof(T));
+        }
+        __syncwarp();
+        if (lane == 0) ptx::mbar_arrive(&empty[s]);
+        if (MODE == 0) {
+            if (!active) continue;
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+                A t[RB];
+#pragma unroll
+                for (int u = 0; u < RB; ++u) t[u] = (u < nb) ? (A)x[u][j] : (A)0;
+                acc[j] += (t[0] + t[1]) + (t[2] + t[3]);
+            }
+        } else {
+#pragma unroll
+            for (int u = 0; u < RB; ++u) dv[u] = active ? dv[u] : never_lt<T>();
+            static_assert(RB == 4, "mask folding assumes 4 rows per stage");
+            unsigned m = 0;
+#pragma unroll
+            for (int j = 0; j < 4; ++j)
+                m |= CmpLt<T>::any4(x[0][j], dv[0], x[1][j], dv[1], x[2][j], dv[2], x[3][j], dv[3]) << j;
+            const unsigned wm = __reduce_or_sync(FULL, m);
+            if (wm == 0) continue;
+            A dA[RB];
+#pragma unroll
+            for (int u = 0; u < RB; ++u) dA[u] = (A)dv[u];
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+                if (wm & (1u << j)) {
+                    A t[RB];
+#pragma unroll
+                    for (int u = 0; u < RB; ++u) t[u] = (x[u][j] < dv[u]) ? (A)x[u][j] - dA[u] : (A)0;
+                    acc[j] += (t[0] + t[1]) + (t[2] + t[3]);
+                }
+            }
+        }
+    }
+    if (!active) return;
+    const int64_t base = (int64_t)q * w;
+#pragma unroll
+    for (int j = 0; j < 4; ++j)
+        if (cb + j < w) out[base + cb + j] = acc[j];
+}
+
 // Per candidate: sum the parts in order; MODE 0 removes the x_o = x_c term
 // (Alg.1 P:288 "x_o != x_c"); non-medoids enter a (value, c) min (slot = 0).
 template <typename T, typename A, int MODE>

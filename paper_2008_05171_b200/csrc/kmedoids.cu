@@ -141,7 +141,8 @@ struct Impl : ImplBase {
     int64_t ld = 0, c0 = 0, c1 = 0;
     int w = 0;
     cudaStream_t st = nullptr;
-    int P = 1, Pb = 1, B = 1, ncomb = 1, ntd = 1, sort_chunk = 256;
+    int P = 1, Pb = 1, Pbt = 1, B = 1, ncomb = 1, ntd = 1, sort_chunk = 256;
+    bool build_tma = true;          // KM_BUILD=ldg selects the register-pipelined BUILD stream
     int nranks = 1;
     int wpad = 0;
     bool use_tma = true;
@@ -248,6 +249,9 @@ struct Impl : ImplBase {
 
                                : choose_parts(n, w, STREAM_COLS, RESIDENT_CTAS);
         Pb = choose_parts(n, w, STREAM_COLS, RESIDENT_CTAS);
+        Pbt = choose_parts(n, w, SG_NC * 128, SG_MINB);
+        const char* eb = getenv("KM_BUILD");
+        build_tma = !(eb && strcmp(eb, "ldg") == 0);
         wpad = (int)((w + 3) / 4 * 4);
         // counting-sort chunk: >= 256 objects and at most 128 chunks (keeps the
         // k x B count matrix of the one-block scan small)
@@ -275,7 +279,7 @@ struct Impl : ImplBase {
         KM_TRY(alloc(&head_slot, P));
         KM_TRY(alloc(&tail_slot, P));
         KM_TRY(alloc(&R, k));
-        const size_t pw = (size_t)std::max(P, Pb) * w;
+        const size_t pw = (size_t)std::max(P, std::max(Pb, Pbt)) * w;
         KM_TRY(alloc(&o_plus, pw));
         KM_TRY(alloc(&o_head, pw));
         KM_TRY(alloc(&o_tail, pw));
@@ -818,18 +822,33 @@ struct Impl : ImplBase {
     }
 
     // ---- BUILD ---------------------------------------------------------------
+    template <int MODE>
+    km_status launch_build_tma() {
+        using C = km::SegCfg<T, SG_NC, SG_RB, SG_S>;
+        auto kern = km::k_build_tma<T, A, SG_NC, SG_RB, SG_S, SG_MINB, MODE>;
+        KM_CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM));
+        dim3 g((unsigned)cdiv(w, C::COLS), Pbt);
+        kern<<<g, C::THREADS, C::SMEM, st>>>(D, ld, w, wpad, (int)n, Pbt, dn, b_out);
+        KM_CKL();
+        km::k_build_combine<T, A, MODE><<<ncomb, 128, 0, st>>>(D, ld, w, c0, Pbt, b_out, point_slot, partials,
+                                                                counters, rec_local);
+        KM_CKL();
+        return KM_OK;
+    }
+
     km_status build_eval(int32_t step) override {
         if (step < 0 || step >= k) return fail(KM_EINVAL, "build step %d out of range", step);
+        if (build_tma) return step == 0 ? launch_build_tma<0>() : launch_build_tma<1>();
         dim3 g((unsigned)cdiv(w, STREAM_COLS), Pb);
         if (step == 0) {
             km::k_build_stream<T, A, STREAM_WARPS, STREAM_U, 0><<<g, STREAM_WARPS * 32, 0, st>>>(D, ld, w, (int)n, Pb, dn, b_out);
             KM_CKL();
-            km::k_build_combine<T, A, 0><<<ncomb, 256, 0, st>>>(D, ld, w, c0, Pb, b_out, point_slot, partials, counters, rec_local);
+            km::k_build_combine<T, A, 0><<<ncomb, 128, 0, st>>>(D, ld, w, c0, Pb, b_out, point_slot, partials, counters, rec_local);
             KM_CKL();
         } else {
             km::k_build_stream<T, A, STREAM_WARPS, STREAM_U, 1><<<g, STREAM_WARPS * 32, 0, st>>>(D, ld, w, (int)n, Pb, dn, b_out);
             KM_CKL();
-            km::k_build_combine<T, A, 1><<<ncomb, 256, 0, st>>>(D, ld, w, c0, Pb, b_out, point_slot, partials, counters, rec_local);
+            km::k_build_combine<T, A, 1><<<ncomb, 128, 0, st>>>(D, ld, w, c0, Pb, b_out, point_slot, partials, counters, rec_local);
             KM_CKL();
         }
         return KM_OK;
