@@ -247,6 +247,29 @@ def swap_run(D: np.ndarray, M0, variant: int = FASTPAM1, max_iter: int = 2000) -
     return RunResult(M, asg, tdo[0].item(), int(it[0]), ns, rc == 0, trace)
 
 
+def fasterpam_run(D: np.ndarray, M0, max_iter: int = 2000) -> RunResult:
+    """FasterPAM, Alg.4 with readings F1-F5 (oracle_impl.h).
+
+    ``trace`` entries are (slot, candidate, dTD, scan position t)."""
+    f, acc = _fn(D, "oracle_fasterpam_run")
+    f.restype = ctypes.c_int
+    M = _i32(M0).copy()
+    n, k = D.shape[0], len(M)
+    cap = 1 << 20
+    ti = np.zeros(cap, np.int32); tc = np.zeros(cap, np.int32); tdv = np.zeros(cap, acc)
+    tp = np.zeros(cap, np.int64)
+    it = np.zeros(1, np.int32); sw = np.zeros(1, np.int32); tdo = np.zeros(1, acc)
+    asg = np.zeros(n, np.int32)
+    rc = f(_ptr(D), ctypes.c_int64(_ld(D)), ctypes.c_int32(n), _ptr(M), ctypes.c_int32(k),
+           ctypes.c_int32(max_iter), _ptr(ti), _ptr(tc), _ptr(tdv), _ptr(tp), ctypes.c_int32(cap),
+           _ptr(it), _ptr(sw), _ptr(tdo), _ptr(asg))
+    if rc < 0:
+        raise ValueError("fasterpam_run needs 2 <= k < n")
+    ns = int(sw[0])
+    trace = [(int(ti[j]), int(tc[j]), tdv[j].item(), int(tp[j])) for j in range(min(ns, cap))]
+    return RunResult(M, asg, tdo[0].item(), int(it[0]), ns, rc == 0, trace)
+
+
 def build_init(D: np.ndarray, k: int):
     """PAM BUILD, Alg.1 with readings R3/R4.
 

@@ -22,6 +22,8 @@
  *   R4 BUILD ties: smallest point index; no early stop           (c6)
  *   R5 acceptance: int dTD < 0; float dTD < -EPS_REL*|TD|        (c7)
  *   R6 FastPAM2 per-iteration procedure                           (c10)
+ *   F1-F5 FasterPAM scan order, termination, pass count, slot choice,
+ *         swap target (oracle_fasterpam_run)                       (c12)
  */
 
 #define CAT2(a, b) a##b
@@ -312,6 +314,75 @@ int FN(oracle_swap_run)(const D_T* D, int64_t ld, int32_t n, int32_t* M, int32_t
         for (int32_t o = 0; o < n; ++o) assignment[o] = nearest[o];
     free(nearest); free(second); free(dn); free(ds); free(R); free(vec);
     free(sv); free(sc); free(order);
+    return status;
+}
+
+/* FasterPAM: FastPAM1 with eager swapping, Alg.4 (section
+ * "FasterPAM").  Readings (F1-F5):
+ *   F1 candidates are visited in ascending point index, cyclically
+ *      (c = t mod n for the scan position t = 0, 1, 2, ...); medoids are
+ *      skipped ("x_c not in {m_1..m_k}").
+ *   F2 "break outer loop if x_c = x_last" is tested at every
+ *      position BEFORE the medoid skip (x_last is itself a medoid right
+ *      after its swap); with x_last still invalid, the scan stops after one
+ *      whole pass without a swap.  Both are "stop at the first position t
+ *      with t - t_last = n", t_last = the position of the last swap (0
+ *      before any swap).
+ *   F3 iterations = passes begun = ceil(t_stop / n) ("multiple
+ *      swaps per pass"); max_iter caps the passes begun.
+ *   F4 i = argmin_i dTD_i, smaller slot on ties (as Alg.3),
+ *      then dTD_i += dTD^{+x_c} (the garbled
+ *      "dTD^{+nearest(o)}" accumulators of P:1008-1013 are read as
+ *      dTD_{nearest(o)}).
+ *   F5 acceptance as R5; the swap exchanges m_i with x_c (P:1019 and
+ *      P:1022 write x_o); the nearest/second cache and the
+ *      removal losses are then recomputed from scratch ("update").
+ * trace_* as in oracle_swap_run; trace_pos (may be NULL) receives the scan
+ * position t of every swap.  Returns 0 converged, 1 max_iter reached. */
+int FN(oracle_fasterpam_run)(const D_T* D, int64_t ld, int32_t n, int32_t* M, int32_t k, int32_t max_iter,
+                             int32_t* trace_i, int32_t* trace_c, ACC_T* trace_dtd, int64_t* trace_pos,
+                             int32_t trace_cap, int32_t* n_iter, int32_t* n_swaps, ACC_T* td_out,
+                             int32_t* assignment) {
+    if (k < 2 || k >= n) return -1;
+    int32_t* nearest = (int32_t*)malloc(sizeof(int32_t) * (size_t)n);
+    int32_t* second = (int32_t*)malloc(sizeof(int32_t) * (size_t)n);
+    ACC_T* dn = (ACC_T*)malloc(sizeof(ACC_T) * (size_t)n);
+    ACC_T* ds = (ACC_T*)malloc(sizeof(ACC_T) * (size_t)n);
+    ACC_T* R = (ACC_T*)malloc(sizeof(ACC_T) * (size_t)k);
+    ACC_T* vec = (ACC_T*)malloc(sizeof(ACC_T) * (size_t)k);
+    int32_t swaps = 0, status = 0;
+    int64_t t = 0, t_last = 0;
+    ACC_T td = FN(oracle_td)(D, ld, n, M, k);
+    FN(oracle_assign)(D, ld, n, M, k, nearest, second, dn, ds);
+    FN(oracle_removal_loss)(n, k, nearest, dn, ds, R);
+    for (;; ++t) {
+        if (t - t_last == n) break;                                 /* F2 */
+        if (t % n == 0 && t / n >= max_iter) { status = 1; break; } /* F3 cap */
+        const int32_t c = (int32_t)(t % n);
+        if (FN(is_medoid)(M, k, c)) continue;                       /* F1 */
+        ACC_T plus;
+        FN(oracle_fastpam1_candidate)(D, ld, n, k, c, nearest, dn, ds, R, vec, &plus);
+        int32_t i = 0;
+        for (int32_t j = 1; j < k; ++j)
+            if (vec[j] < vec[i]) i = j;                             /* F4 */
+        const ACC_T v = vec[i] + plus;
+        if (!FN(improving)(v, td)) continue;                        /* F5 */
+        if (swaps < trace_cap) {
+            trace_i[swaps] = i; trace_c[swaps] = c; trace_dtd[swaps] = v;
+            if (trace_pos) trace_pos[swaps] = t;
+        }
+        swaps++;
+        M[i] = c;
+        td += v;
+        FN(oracle_assign)(D, ld, n, M, k, nearest, second, dn, ds);
+        FN(oracle_removal_loss)(n, k, nearest, dn, ds, R);
+        t_last = t;
+    }
+    *n_iter = (int32_t)((t + n - 1) / n);
+    *n_swaps = swaps; *td_out = td;
+    if (assignment)
+        for (int32_t o = 0; o < n; ++o) assignment[o] = nearest[o];
+    free(nearest); free(second); free(dn); free(ds); free(R); free(vec);
     return status;
 }
 

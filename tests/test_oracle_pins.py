@@ -332,3 +332,115 @@ def test_fastpam2_reading_properties():
                 if x not in M:
                     assert bf_delta(D, M, i, x) >= 0
         assert r2.converged and r2.n_iter >= 1
+
+
+# ---------- FasterPAM (Alg.4; readings F1-F5) ----------
+
+def bf_eager(D, M0, max_iter=2000, eps_rel=None):
+    """Eager swapping written from the definitions only: for every scan
+    position t (candidate c = t mod n, medoids skipped), the change of TD for
+    replacing each slot i by c is recomputed from scratch (Eq. eqn:td); the
+    best slot (smaller slot on ties) is swapped in if it lowers TD.  Stops at
+    the first position n past the last swap (readings F1-F3)."""
+    n = D.shape[0]
+    Dw = D.astype(np.int64) if D.dtype == np.uint32 else D.astype(np.float64)
+    M = list(M0)
+
+    def td_of(MM):
+        return Dw[:, MM].min(axis=1).sum()
+
+    td = td_of(M)
+    t = t_last = 0
+    trace = []
+    converged = True
+    while True:
+        if t - t_last == n:
+            break
+        if t % n == 0 and t // n >= max_iter:
+            converged = False
+            break
+        c = t % n
+        if c not in M:
+            deltas = []
+            for i in range(len(M)):
+                M2 = list(M)
+                M2[i] = c
+                deltas.append(td_of(M2) - td)
+            i = int(np.argmin(deltas))      # first minimum = smaller slot
+            v = deltas[i]
+            ok = v < 0 if eps_rel is None else v < -eps_rel * abs(td)
+            if ok:
+                trace.append((i, c, v, t))
+                M[i] = c
+                td = td_of(M)
+                t_last = t
+        t += 1
+    return M, td, (t + n - 1) // n, trace, converged
+
+
+def _check_eager(D, M0, float_tol=None, **kw):
+    r = oracle.fasterpam_run(D, M0, **kw)
+    M, td, iters, trace, conv = bf_eager(D, M0, eps_rel=None if float_tol is None else oracle.EPS_REL, **kw)
+    assert r.medoids.tolist() == M
+    assert [(a, b, d) for a, b, _, d in r.trace] == [(a, b, d) for a, b, _, d in trace]
+    if float_tol is None:
+        assert [v for _, _, v, _ in r.trace] == [v for _, _, v, _ in trace]
+        assert r.td == td
+    else:
+        assert np.allclose([v for _, _, v, _ in r.trace], [v for _, _, v, _ in trace], rtol=0, atol=float_tol)
+        assert abs(r.td - td) <= float_tol
+    assert r.n_iter == iters and r.n_swaps == len(trace) and r.converged == conv
+    return r
+
+
+@pytest.mark.parametrize("symmetric", [True, False])
+def test_fasterpam_equals_bruteforce_eager(symmetric):
+    rng = np.random.default_rng(41 + symmetric)
+    for _ in range(60):
+        n = int(rng.integers(6, 28))
+        k = int(rng.integers(2, min(6, n - 1) + 1))
+        D = rand_int_matrix(rng, n, hi=int(rng.choice([4, 30, 1000])), symmetric=symmetric)
+        M0 = rng.choice(n, k, replace=False).tolist()
+        r = _check_eager(D, M0)
+        # P:1703-1706: several swaps per pass; the result is a local optimum
+        for i in range(k):
+            for c in range(n):
+                if c not in r.medoids.tolist():
+                    assert bf_delta(D, r.medoids.tolist(), i, c) >= 0
+        assert oracle.td(D, r.medoids) == r.td
+        assert r.assignment.tolist() == oracle.assign(D, r.medoids).nearest.tolist()
+
+
+def test_fasterpam_float_equals_bruteforce_eager():
+    rng = np.random.default_rng(7)
+    for _ in range(30):
+        n = int(rng.integers(8, 26))
+        k = int(rng.integers(2, 5))
+        X = rng.normal(size=(n, 3))
+        D = np.sqrt(((X[:, None, :] - X[None, :, :]) ** 2).sum(-1)).astype(np.float32)
+        M0 = rng.choice(n, k, replace=False).tolist()
+        _check_eager(D, M0, float_tol=1e-9)
+
+
+def test_fasterpam_max_iter_and_termination():
+    rng = np.random.default_rng(3)
+    D = rand_int_matrix(rng, 40, hi=1000)
+    M0 = [0, 1, 2, 3]
+    full = _check_eager(D, M0)
+    assert full.converged and full.n_swaps >= full.n_iter - 1
+    capped = _check_eager(D, M0, max_iter=1)
+    assert capped.n_iter == 1 and not capped.converged
+    # a start at the optimum: one pass, no swap (F2 with x_last invalid)
+    again = _check_eager(D, full.medoids.tolist())
+    assert again.n_swaps == 0 and again.n_iter == 1 and again.converged
+
+
+def test_fasterpam_fig1_reaches_the_optimum():
+    """SPEC fasterpam_swap example: the Fig.1 instance (reading R7),
+    started at its 'Loss: 10' configuration, ends at the exhaustive optimum."""
+    g = _gold("fig1_alternating.json")
+    D = line_matrix(g["points"])
+    r = _check_eager(D, g["medoids"])
+    best = min(bf_td(D, list(S)) for S in itertools.combinations(range(len(g["points"])), 2))
+    assert best == g["losses"][-1]
+    assert r.td == best
