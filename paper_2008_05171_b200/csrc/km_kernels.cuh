@@ -1364,6 +1364,7 @@ k_swap_stream_tmaq(const T* __restrict__ D, int64_t ld, int w, int wpad, int n, 
                 u = v;
             }
         }
+        __syncwarp();
         if (lane == 0) ptx::mbar_arrive(&empty[s]);
     }
     __syncwarp();
@@ -1586,8 +1587,6 @@ k_swap_stream_seg(const T* __restrict__ D, int64_t ld, int w, int wpad, int n, i
             dn[u] = srii[u].dn;
             ds[u] = srii[u].ds;
         }
-        __syncwarp();
-        if (lane == 0) ptx::mbar_arrive(&empty[s]);
         // Rows >= nb (the short stage at a segment end) hold stale, possibly
         // never-written bytes, and columns >= w of the last tile are padding:
         // give them thresholds nothing compares below (the loaded values are
@@ -1608,7 +1607,12 @@ k_swap_stream_seg(const T* __restrict__ D, int64_t ld, int w, int wpad, int n, i
         for (int j = 0; j < 4; ++j)
             m |= CmpLt<T>::any4(x[0][j], ds[0], x[1][j], ds[1], x[2][j], ds[2], x[3][j], ds[3]) << j;
         const unsigned wm = __reduce_or_sync(FULL, m);
-        if (wm == 0) continue;
+        if (wm == 0) {
+            // every lane has its stage values in registers: release the stage
+            __syncwarp();
+            if (lane == 0) ptx::mbar_arrive(&empty[s]);
+            continue;
+        }
         A dnA[RB], dsA[RB], dnds[RB];
         if constexpr (Acc<T>::is_float) {       // widened thresholds staged by the producer (no F2F)
             const double2* sr = srd + s * RB;
@@ -1618,6 +1622,10 @@ k_swap_stream_seg(const T* __restrict__ D, int64_t ld, int w, int wpad, int n, i
 #pragma unroll
             for (int u = 0; u < RB; ++u) { dnA[u] = (A)dn[u]; dsA[u] = (A)ds[u]; dnds[u] = dnA[u] - dsA[u]; }
         }
+        // the stage is released only after the staged fp64 thresholds are in
+        // registers: the producer refills srd together with the data
+        __syncwarp();
+        if (lane == 0) ptx::mbar_arrive(&empty[s]);
 #pragma unroll
         for (int j = 0; j < 4; ++j) {
             if (wm & (1u << j)) {

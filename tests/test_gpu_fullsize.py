@@ -154,3 +154,50 @@ def test_c3_fullsize_fastpam1_lockstep_prefix():
         assert gdtd == pytest.approx(vec[gi] + plus, rel=1e-9, abs=1e-9 * td_ref)
         M[gi] = gc
         assert td == pytest.approx(oracle.td(D, M), rel=1e-9)
+
+
+def test_c4_every_candidate_exact_and_deterministic():
+    """C4 at full size, EVERY candidate of an iteration: the per-candidate
+    (min_i dTD, argmin) equals the oracle's Alg.3 evaluation (reading R9:
+    fp64 sums in another order, 1e-9 relative), two evaluations of the same
+    state are bitwise identical, and the TD tracked over a whole run to
+    convergence equals TD recomputed from its definition (Eq. eqn:td)."""
+    from paper_2008_05171_b200 import KMedoids
+    cfg = kmsynth.CONFIGS[4]
+    n, k = cfg.n, cfg.k
+    X = kmsynth.make_points(cfg)
+    Dt = kmsynth.dist_cuda(X, cfg.metric)
+    km = KMedoids(Dt, n, k)
+    M, td = km.init_build()
+    for _ in range(3):
+        km.swap_iter()
+    M = km.get_state().medoids
+    v1, s1 = km.eval_candidates()
+    v2, s2 = km.eval_candidates()
+    assert np.array_equal(v1, v2) and np.array_equal(s1, s2)
+    cache = oracle.assign_cols(cols(Dt, M, n))
+    R = oracle.removal_loss(cache, k)
+    tdr = float(cache.dn.sum())
+    med = set(M.tolist())
+    bad = []
+    for c0 in range(0, n, 2500):
+        idx = np.arange(c0, min(n, c0 + 2500))
+        C = cols(Dt, idx, n)
+        for c, col in zip(idx, C):
+            if c in med:
+                assert s1[c] == -1
+                continue
+            vec, plus = oracle.fastpam1_candidate_col(col, cache, R)
+            full = vec + plus
+            i = int(np.argmin(full))
+            srt = np.partition(full, 1)
+            ok = abs(v1[c] - full[i]) <= 1e-9 * tdr and (s1[c] == i or srt[1] - srt[0] <= 1e-9 * tdr)
+            if not ok:
+                bad.append((int(c), float(v1[c]), int(s1[c]), float(full[i]), i))
+    assert not bad, bad[:10]
+    r = km.run(use_build=False)
+    assert r.converged
+    td_def = float(cols(Dt, r.medoids, n).astype(np.float64).min(axis=0).sum())
+    assert r.td == pytest.approx(td_def, rel=1e-9)
+    v, s = km.eval_candidates()
+    assert np.min(np.where(s >= 0, v, np.inf)) >= -1e-12 * abs(r.td)
