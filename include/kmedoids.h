@@ -56,7 +56,10 @@ typedef enum {
 } km_status;
 
 typedef enum { KM_U32 = 0, KM_F32 = 1 } km_dtype;
-typedef enum { KM_FASTPAM1 = 0, KM_FASTPAM2 = 1 } km_variant;
+/* KM_FASTERPAM: FasterPAM's eager swapping (Alg.4; readings
+ * F1-F5 in DESIGN.md), evaluated exactly on the GPU by speculative candidate
+ * batches. */
+typedef enum { KM_FASTPAM1 = 0, KM_FASTPAM2 = 1, KM_FASTERPAM = 2 } km_variant;
 
 typedef struct km_handle km_handle;  /* opaque; owns only its scratch buffers */
 
@@ -87,10 +90,14 @@ km_status kmedoids_set_medoids(km_handle* h, const int32_t* medoids);
  * driven through kmedoids_build_step*). */
 km_status kmedoids_init_build(km_handle* h, int32_t* medoids_out, void* td_out);
 
-/* One SWAP iteration (FastPAM1: Alg.3; FastPAM2: reading R6) from
- * the current state.  *swaps_done_out (may be NULL) receives the number of
- * swaps applied (0 or 1 for FastPAM1, 0..k for FastPAM2); *td_out the TD
- * after the iteration.  Returns KM_CONVERGED when no swap improves.
+/* One SWAP iteration (FastPAM1: Alg.3; FastPAM2: reading R6;
+ * FasterPAM: one pass of Alg.4's candidate scan) from the
+ * current state.  *swaps_done_out (may be NULL) receives the number of
+ * swaps applied (0 or 1 for FastPAM1, 0..k for FastPAM2, 0..n-k for a
+ * FasterPAM pass); *td_out the TD after the iteration.  Returns KM_CONVERGED
+ * when no swap improves (FasterPAM: when n consecutive scan positions
+ * passed without a swap, reading F2; a pass that ends that way returns
+ * KM_CONVERGED, and later calls return KM_CONVERGED without work).
  * Single GPU only. */
 km_status kmedoids_swap_iter(km_handle* h, km_variant variant, int32_t* swaps_done_out, void* td_out);
 

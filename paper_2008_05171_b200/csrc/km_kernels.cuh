@@ -1757,6 +1757,54 @@ __global__ void k_select(const Rec<A>* __restrict__ recs, int nrec, A* __restric
 }
 
 // ---------------------------------------------------------------------------
+// FasterPAM (Alg.4; readings F1-F5): eager acceptance inside a
+// speculative candidate batch.  cand_v/cand_slot hold (min_i dTD(m_i, x_c),
+// argmin) of every candidate of the batch window, evaluated on the current
+// state (k_swap_combine).  The scan visits the window's positions lo..hi-1
+// in ascending order (F1); the first improving candidate (F5 / R5) is the
+// one Alg.4 swaps, because every earlier one was evaluated on exactly the
+// state the sequential scan would see and found non-improving.  Later
+// candidates of the batch are discarded (the host resumes behind the swap).
+// One block; also resets the rescan counter and counts a pass (F3).
+// ---------------------------------------------------------------------------
+template <typename A>
+__global__ void k_fp3_pick(const A* __restrict__ cand_v, const int* __restrict__ cand_slot, int lo, int hi,
+                           int64_t win_begin, A* __restrict__ td, int* __restrict__ M, int* __restrict__ point_slot,
+                           Decision<A>* __restrict__ dec, int* __restrict__ rescan_count, int new_pass) {
+    __shared__ int first;
+    if (threadIdx.x == 0) first = INT_MAX;
+    __syncthreads();
+    const A tdv = *td;
+    for (int j = lo + (int)threadIdx.x; j < hi; j += blockDim.x) {
+        if (cand_slot[j] < 0) continue;                       // medoid column (F1 skip)
+        const A v = cand_v[j];
+        bool imp;
+        if (std::is_same<A, double>::value) imp = (double)v < -1e-12 * fabs((double)tdv);
+        else imp = v < 0;
+        if (imp) { atomicMin(&first, j); break; }             // this thread's first = its minimum
+    }
+    __syncthreads();
+    if (threadIdx.x != 0) return;
+    *rescan_count = 0;
+    if (new_pass) dec->iters += 1;
+    if (first == INT_MAX) { dec->apply = 0; return; }
+    const int slot = cand_slot[first];
+    const int c = (int)(win_begin + first);
+    const A v = cand_v[first];
+    const int old = M[slot];
+    dec->apply = 1;
+    dec->dtd = v;
+    dec->slot = slot;
+    dec->c = c;
+    dec->old_m = old;
+    M[slot] = c;
+    point_slot[old] = -1;
+    point_slot[c] = slot;
+    *td = tdv + v;
+    dec->swaps += 1;
+}
+
+// ---------------------------------------------------------------------------
 // a6: FastPAM2 (reading R6)
 // ---------------------------------------------------------------------------
 

@@ -374,6 +374,7 @@ struct Impl : ImplBase {
         KM_TRY(reset_counters());
         KM_CK(cudaStreamSynchronize(st));
         ready = true;
+        fp3_reset();
         return KM_OK;
     }
 
@@ -444,15 +445,23 @@ struct Impl : ImplBase {
 
     template <int NC, int RB, int S, int MINB = 2>
     km_status launch_seg(A* acc_out) {
+        return launch_seg_win<NC, RB, S, MINB>(D, w, wpad, P, o_plus, o_head, o_tail, o_imin, o_islot, acc_out);
+    }
+
+    // The stream over the column window [Dw, Dw + ww) of the slab (Dw 16-byte
+    // aligned) with Pw row parts; outputs indexed [part][column of window].
+    template <int NC, int RB, int S, int MINB = 2>
+    km_status launch_seg_win(const T* Dw, int ww, int wpadw, int Pw, A* plus_o, A* head_o, A* tail_o, A* imin_o,
+                             int* islot_o, A* acc_out) {
         using C = km::SegCfg<T, NC, RB, S>;
         auto kern = km::k_swap_stream_seg<T, A, NC, RB, S, MINB>;
         if (!seg_attr_set) {
             KM_CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM));
             seg_attr_set = true;
         }
-        dim3 g((unsigned)cdiv(w, C::COLS), P);
-        kern<<<g, C::THREADS, C::SMEM, st>>>(D, ld, w, wpad, (int)n, P, ri, R, o_plus, o_head, o_tail, o_imin, o_islot,
-                                              acc_out, rowd);
+        dim3 g((unsigned)cdiv(ww, C::COLS), Pw);
+        kern<<<g, C::THREADS, C::SMEM, st>>>(Dw, ld, ww, wpadw, (int)n, Pw, ri, R, plus_o, head_o, tail_o, imin_o,
+                                              islot_o, acc_out, rowd);
         return KM_OK;
     }
 
@@ -536,8 +545,10 @@ struct Impl : ImplBase {
     km_status swap_iter(km_variant v, int32_t* swaps, void* td_out) override {
         if (sharded) return fail(KM_EINVAL, "swap_iter on a sharded handle; use the kmedoids_shard_* phases");
         if (!ready) return fail(KM_EINVAL, "no medoids: call kmedoids_set_medoids or kmedoids_init_build first");
-        if (v != KM_FASTPAM1 && v != KM_FASTPAM2) return fail(KM_EINVAL, "unknown variant %d", (int)v);
+        if (v != KM_FASTPAM1 && v != KM_FASTPAM2 && v != KM_FASTERPAM)
+            return fail(KM_EINVAL, "unknown variant %d", (int)v);
         if (v == KM_FASTPAM2) return swap_iter_fp2(swaps, td_out);
+        if (v == KM_FASTERPAM) return swap_iter_fp3(swaps, td_out);
         if (use_graph && fp1_iters >= 1) {
             // the whole iteration (11 kernels + the 32-byte decision copy) as one CUDA graph
             if (!fp1_exec) {
@@ -719,6 +730,117 @@ struct Impl : ImplBase {
         return fp2_sequential(order, nullptr, nullptr, swaps_out, td_out);
     }
 
+    // ---- FasterPAM (Alg.4; readings F1-F5) -------------------------
+    // Exact eager scan by speculative batches: evaluate the candidates of the
+    // next scan positions [t, hi) on the current state in one stream pass,
+    // accept the FIRST improving one (every candidate before it was evaluated
+    // on exactly the state Alg.4's sequential loop sees), apply it, resume
+    // at the position behind it.  Positions run t = 0, 1, 2, ... with
+    // candidate c = t mod n (F1); the scan stops once n consecutive
+    // positions passed without a swap (F2); a pass = n positions (F3).
+    int64_t fp3_t = 0, fp3_tlast = 0;
+    bool fp3_dirty = true;          // cache changed since the last prep()
+    int fp3_wmax = 0, fp3_w0 = 0, fp3_pmax = 0;
+    A *f3_plus = nullptr, *f3_head = nullptr, *f3_tail = nullptr, *f3_imin = nullptr, *f3_v = nullptr;
+    int *f3_islot = nullptr, *f3_hs = nullptr, *f3_ts = nullptr, *f3_s = nullptr;
+    int64_t fp3_batches = 0;
+
+    void fp3_reset() { fp3_t = 0; fp3_tlast = 0; fp3_dirty = true; }
+
+    // row parts for a window of ww columns: one wave of 3 CTAs per SM
+    int fp3_parts(int ww) const {
+        const int64_t ncb = cdiv(ww, SG_NC * 128);
+        int64_t p = cdiv((int64_t)NUM_SMS * SG_MINB, ncb);
+        p = std::min<int64_t>(p, std::max<int64_t>(1, n / 64));
+        return (int)std::max<int64_t>(p, 1);
+    }
+
+    km_status fp3_alloc() {
+        if (f3_plus) return KM_OK;
+        const int tile = SG_NC * 128;
+        const char* ew = getenv("KM_FASTER_WMAX");
+        const char* e0 = getenv("KM_FASTER_W0");
+        fp3_wmax = ew ? std::max(tile, atoi(ew) / tile * tile) : 16 * tile;
+        fp3_w0 = e0 ? std::max(tile, atoi(e0) / tile * tile) : 2 * tile;
+        fp3_w0 = std::min(fp3_w0, fp3_wmax);
+        size_t cap = 0;
+        for (int64_t nc = 1; nc <= cdiv(fp3_wmax + 3, tile); ++nc) {
+            const int ww = (int)std::min<int64_t>(nc * tile, fp3_wmax + 3);
+            cap = std::max(cap, (size_t)fp3_parts(ww) * ww);
+        }
+        fp3_pmax = fp3_parts(1);
+        KM_TRY(alloc(&f3_plus, cap));
+        KM_TRY(alloc(&f3_head, cap));
+        KM_TRY(alloc(&f3_tail, cap));
+        KM_TRY(alloc(&f3_imin, cap));
+        KM_TRY(alloc(&f3_islot, cap));
+        KM_TRY(alloc(&f3_hs, fp3_pmax));
+        KM_TRY(alloc(&f3_ts, fp3_pmax));
+        KM_TRY(alloc(&f3_v, fp3_wmax + 4));
+        KM_TRY(alloc(&f3_s, fp3_wmax + 4));
+        return KM_OK;
+    }
+
+    // One batch: scan positions [t, hi) of the pass starting at pass_base.
+    km_status fp3_batch(int64_t pass_base, int64_t t, int64_t hi, bool new_pass) {
+        const int clo = (int)(t - pass_base), chi = (int)(hi - pass_base);
+        const int a = clo & ~3;                       // 16-byte aligned window start
+        const int ww = chi - a, wpadw = (int)std::min<int64_t>(cdiv(ww, 4) * 4, ld - a);
+        const int Pw = fp3_parts(ww);
+        if (fp3_dirty) { KM_TRY(prep()); fp3_dirty = false; }
+        km::k_part_meta<T><<<(unsigned)cdiv(Pw, 128), 128, 0, st>>>(ri, (int)n, Pw, f3_hs, f3_ts);
+        KM_CKL();
+        if (profiling) KM_CK(record_ev(ev0));
+        KM_TRY((launch_seg_win<SG_NC, SG_RB, SG_S, SG_MINB>(D + a, ww, wpadw, Pw, f3_plus, f3_head, f3_tail, f3_imin,
+                                                             f3_islot, nullptr)));
+        KM_CKL();
+        if (profiling) { KM_CK(record_ev(ev1)); pending_prof = true; }
+        km::k_swap_combine<A><<<(unsigned)cdiv(ww, 128), 128, 0, st>>>(
+            ww, c0 + a, Pw, f3_plus, f3_head, f3_tail, f3_imin, f3_islot, f3_hs, f3_ts, R, empty_slot, point_slot,
+            f3_v, f3_s, partials, counters, rec_local);
+        KM_CKL();
+        km::k_fp3_pick<A><<<1, 1024, 0, st>>>(f3_v, f3_s, clo - a, chi - a, c0 + a, td, M, point_slot, dec,
+                                              rescan_count, new_pass ? 1 : 0);
+        KM_CKL();
+        KM_TRY(apply_local());                        // no-ops unless a swap was picked
+        ++fp3_batches;
+        return sync_dec();
+    }
+
+    // One pass of Alg.4's scan (or its remainder up to the stop, F2).
+    km_status swap_iter_fp3(int32_t* swaps_out, void* td_out) {
+        KM_TRY(fp3_alloc());
+        fp3_dirty = true;           // another variant may have changed the cache
+        last_swaps.clear();
+        if (swaps_out) *swaps_out = 0;
+        if (fp3_t - fp3_tlast >= n) { copy_td(td_out); return KM_CONVERGED; }
+        const int64_t pass_base = fp3_t - fp3_t % n, pass_end = pass_base + n;
+        int64_t wcur = fp3_w0;
+        bool first = true;
+        int done = 0;
+        while (fp3_t < pass_end && fp3_t - fp3_tlast < n) {
+            const int64_t hi = std::min(std::min(pass_end, fp3_tlast + n), fp3_t + wcur);
+            KM_TRY(fp3_batch(pass_base, fp3_t, hi, first));
+            first = false;
+            if (h_dec->apply) {
+                const int64_t pos = pass_base + h_dec->c;
+                Rec r; r.v = h_dec->dtd; r.slot = h_dec->slot; r.c = h_dec->c;
+                last_swaps.push_back(r);
+                ++done;
+                fp3_tlast = pos;
+                fp3_t = pos + 1;
+                fp3_dirty = true;
+                wcur = fp3_w0;
+            } else {
+                fp3_t = hi;
+                wcur = std::min<int64_t>(wcur * 2, fp3_wmax);
+            }
+        }
+        if (swaps_out) *swaps_out = done;
+        copy_td(td_out);
+        return (fp3_t - fp3_tlast >= n) ? KM_CONVERGED : KM_OK;
+    }
+
     // ---- sharded FastPAM2 ------------------------------------------------------
     // record_send: this rank's k per-slot bests; record_recv: R x k gathered.
     // col_send: the columns of the planned candidates this rank owns
@@ -858,6 +980,7 @@ struct Impl : ImplBase {
         if (k >= 2) {
             KM_TRY(assign_full_and_td());
             ready = true;
+            fp3_reset();
         }
         KM_TRY(reset_counters());
         return KM_OK;
@@ -949,6 +1072,7 @@ struct Impl : ImplBase {
         KM_TRY(reset_counters());
         KM_CK(cudaStreamSynchronize(st));
         ready = true;
+        fp3_reset();
         return KM_OK;
     }
 
