@@ -68,7 +68,10 @@ def full(rep, out, tjson, tag):
         dur = val("gpu__time_duration.sum", 1)
         f.write(f"DRAM traffic per launch: {traffic / 1e9:.3f} GB; duration {dur * 1e3:.3f} ms; "
                 f"{traffic / dur / 1e9:.0f} GB/s under ncu.\n")
-    json.dump({tag: {"traffic_bytes": traffic, "ncu_duration_s": dur, "source": rep}}, open(tjson, "w"), indent=1)
+    import os
+    d = json.load(open(tjson)) if os.path.exists(tjson) else {}
+    d[tag] = {"traffic_bytes": traffic, "ncu_duration_s": dur, "source": "profiles/" + os.path.basename(rep)}
+    json.dump(d, open(tjson, "w"), indent=1)
     print(open(out).read())
 
 
