@@ -298,6 +298,28 @@ def run_ours(args):
                          f"k={k} slots) on the state before the timed region, 1 thread, {used:.1f} s",
                "host_cores": cores, "cpu_model": model}
 
+    # NEXT-1: FasterPAM (Alg.4, eager swaps) vs FastPAM1 to convergence from the
+    # same initial medoids, D resident in HBM, CUDA events on the library's stream.
+    fpm = None
+    if not args.no_fasterpam:
+        def to_converge(variant):
+            km.set_medoids(M0)
+            torch.cuda.synchronize()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            r = km.run(use_build=False, variant=variant)
+            e1.record(stream)
+            torch.cuda.synchronize()
+            return r, e0.elapsed_time(e1) / 1e3
+        to_converge("fasterpam")                     # warm-up (allocations, first launches)
+        rf, sf = to_converge("fasterpam")
+        r1, s1 = to_converge("fastpam1")
+        fpm = {"variant": "fasterpam (Alg.4 P:988-1027, exact eager scan)", "s_to_converge": sf,
+               "passes": rf.n_iter, "swaps": rf.n_swaps, "td": rf.td,
+               "fastpam1_s_to_converge": s1, "fastpam1_iterations": r1.n_iter, "fastpam1_td": r1.td,
+               "speedup_vs_fastpam1": s1 / sf,
+               "start": "the initial medoids of the timed run (after " + cfg.init + ")"}
+
     # e2e: the public host-buffer call kmedoids_run_host (H2D of D, init, SWAP to
     # convergence, D2H of medoids/assignment/TD) -- one whole job per e2e step.
     e2e = None
@@ -342,6 +364,7 @@ def run_ours(args):
         "datagen_s": gen_s,
         "e2e": e2e,
         "cpu_baseline": cpu,
+        "fasterpam": fpm,
     }
     print(json.dumps(line), flush=True)
 
@@ -357,6 +380,7 @@ def main():
     ap.add_argument("--sharded", action="store_true", help="use the column-sharded path even on 1 GPU")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-fasterpam", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
     ap.add_argument("--cpu-candidates", type=int, default=2000)
     ap.add_argument("--ref-candidates", type=int, default=400)

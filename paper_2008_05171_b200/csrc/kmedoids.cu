@@ -10,12 +10,14 @@
 #include <memory>
 #include <string>
 #include <algorithm>
+#include <chrono>
 #include <cmath>
 #include <type_traits>
 #include <vector>
 
 #include "../../include/kmedoids.h"
 #include "km_kernels.cuh"
+#include "km_fasterpam.cuh"
 
 namespace {
 
@@ -807,8 +809,128 @@ struct Impl : ImplBase {
         return sync_dec();
     }
 
+    // ---- FasterPAM, cooperative window scan (default; KM_FASTER=batch selects
+    // the speculative batch path above).  A window is streamed once; one
+    // cooperative kernel (km_fasterpam.cuh) scans it, swapping eagerly and
+    // correcting the values ahead of each swap instead of re-streaming.
+    int fp3_mode = -1;              // 1 = cooperative window scan, 0 = speculative batches
+    int fp3c_ww = 0, fp3c_L = 0, fp3c_blocks = 0;
+    A *f3_acc = nullptr, *f3_wplus = nullptr, *f3_pacc = nullptr, *f3_pplus = nullptr, *f3_pR = nullptr;
+    int *f3_flag = nullptr, *f3_oldnear = nullptr, *f3_rescan = nullptr, *f3_blk = nullptr;
+    T *f3_olddn = nullptr, *f3_oldds = nullptr, *f3_mct = nullptr;
+    int *f3_tflag = nullptr, *f3_tmap = nullptr, *f3_tlist = nullptr;
+    km::Fp3Chg<T>* f3_chg = nullptr;
+    km::Fp3Ctl *f3_ctl = nullptr, *h_f3ctl = nullptr;
+    Rec* f3_trace = nullptr;
+    int64_t fp3_windows = 0, fp3_stale = 0;
+    unsigned long long fp3_tphase[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    long long fp3_stat[3] = {0, 0, 0};
+    double fp3_host_ms = 0;
+
+    km_status fp3c_alloc() {
+        if (f3_acc) return KM_OK;
+        const int tile = SG_NC * 128;
+        const char* ew = getenv("KM_FASTER_COOP_W");
+        const char* el = getenv("KM_FASTER_L");
+        fp3c_ww = ew ? std::max(tile, atoi(ew) / tile * tile) : 8 * tile;
+        fp3c_L = el ? std::max(32, atoi(el) / 32 * 32) : 4096;
+        fp3c_ww = std::min(fp3c_ww, fp3_wmax);     // the stream's part buffers are sized for fp3_wmax
+        fp3c_L = std::min(fp3c_L, fp3c_ww);
+        const size_t wcap = (size_t)fp3c_ww + 4;
+        KM_TRY(alloc(&f3_acc, (size_t)k * wcap));
+        KM_TRY(alloc(&f3_wplus, wcap));
+        KM_TRY(alloc(&f3_pacc, (size_t)km::FP3_G * km::FP3_TMAX * fp3c_L));
+        KM_TRY(alloc(&f3_pplus, (size_t)km::FP3_G * fp3c_L));
+        KM_TRY(alloc(&f3_pR, (size_t)km::FP3_G * km::FP3_TMAX));
+        KM_TRY(alloc(&f3_flag, n));
+        KM_TRY(alloc(&f3_oldnear, n));
+        KM_TRY(alloc(&f3_olddn, n));
+        KM_TRY(alloc(&f3_oldds, n));
+        KM_TRY(alloc(&f3_rescan, n));
+        KM_TRY(alloc(&f3_chg, n));
+        KM_TRY(alloc(&f3_mct, (size_t)n * k));
+        KM_TRY(alloc(&f3_tflag, k));
+        KM_TRY(alloc(&f3_tmap, k));
+        KM_TRY(alloc(&f3_tlist, km::FP3_TMAX));
+        KM_TRY(alloc(&f3_ctl, 1));
+        KM_TRY(alloc(&f3_trace, wcap));
+        KM_CK(cudaMemsetAsync(f3_tflag, 0, k * sizeof(int), st));
+        KM_CK(cudaMallocHost((void**)&h_f3ctl, sizeof(km::Fp3Ctl)));
+        auto kern = km::k_fp3_window<T, A>;
+        KM_CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, km::FP3_SMEM));
+        int dev = 0, per_sm = 0, nsm = 0;
+        KM_CK(cudaGetDevice(&dev));
+        KM_CK(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
+        KM_CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, km::FP3_THREADS, km::FP3_SMEM));
+        if (per_sm < 1) return fail(KM_ECUDA, "k_fp3_window cannot be resident");
+        fp3c_blocks = nsm * per_sm;
+        KM_TRY(alloc(&f3_blk, fp3c_blocks));
+        return KM_OK;
+    }
+
+    // One window of the scan: positions [t, hi) of the pass at pass_base.
+    km_status fp3_window_coop(int64_t pass_base, int64_t t, int64_t hi, bool new_pass) {
+        const int clo = (int)(t - pass_base), chi = (int)(hi - pass_base);
+        const int a = clo & ~3;
+        const int ww = chi - a, wpadw = (int)std::min<int64_t>(cdiv(ww, 4) * 4, ld - a);
+        const int Pw = fp3_parts(ww);
+        if (fp3_dirty) { KM_TRY(prep()); fp3_dirty = false; }
+        KM_CK(cudaMemsetAsync(f3_acc, 0, (size_t)k * ww * sizeof(A), st));
+        km::k_part_meta<T><<<(unsigned)cdiv(Pw, 128), 128, 0, st>>>(ri, (int)n, Pw, f3_hs, f3_ts);
+        KM_CKL();
+        if (profiling) KM_CK(record_ev(ev0));
+        KM_TRY((launch_seg_win<SG_NC, SG_RB, SG_S, SG_MINB>(D + a, ww, wpadw, Pw, f3_plus, f3_head, f3_tail, f3_imin,
+                                                             f3_islot, f3_acc)));
+        KM_CKL();
+        if (profiling) { KM_CK(record_ev(ev1)); pending_prof = true; }
+        km::k_swap_combine<A><<<(unsigned)cdiv(ww, 128), 128, 0, st>>>(
+            ww, c0 + a, Pw, f3_plus, f3_head, f3_tail, f3_imin, f3_islot, f3_hs, f3_ts, R, empty_slot, point_slot,
+            f3_v, f3_s, partials, counters, rec_local, f3_acc, f3_wplus);
+        KM_CKL();
+        km::Fp3Ctl hc;
+        memset(&hc, 0, sizeof(hc));
+        hc.first[0] = hc.first[1] = hc.first[2] = INT_MAX;
+        *h_f3ctl = hc;
+        KM_CK(cudaMemcpyAsync(f3_ctl, h_f3ctl, sizeof(hc), cudaMemcpyHostToDevice, st));
+        km::Fp3Args<T, A> g;
+        g.D = D; g.ld = ld; g.n = (int)n; g.k = k; g.c0 = c0; g.a = a; g.ww = ww;
+        g.lo = clo - a; g.hi = chi - a; g.L = fp3c_L;
+        g.acc = f3_acc; g.plus = f3_wplus; g.R = R; g.M = M; g.point_slot = point_slot; g.MC = MC; g.MCt = f3_mct;
+        g.near = near; g.sec = sec; g.dn = dn; g.ds = ds; g.td = td; g.dec = dec;
+        g.trace = f3_trace; g.trace_cap = fp3c_ww + 4;
+        g.cand_v = f3_v; g.cand_s = f3_s; g.flag = f3_flag; g.old_near = f3_oldnear; g.old_dn = f3_olddn;
+        g.old_ds = f3_oldds; g.rescan = f3_rescan; g.blk_cnt = f3_blk; g.chg = f3_chg; g.chg_cap = (int)n;
+        g.touched_flag = f3_tflag; g.touched_map = f3_tmap; g.touched = f3_tlist;
+        g.part_acc = f3_pacc; g.part_plus = f3_pplus; g.part_R = f3_pR; g.ctl = f3_ctl; g.new_pass = new_pass ? 1 : 0;
+        void* args[] = {&g};
+        KM_CK(cudaLaunchCooperativeKernel((void*)km::k_fp3_window<T, A>, dim3(fp3c_blocks), dim3(km::FP3_THREADS),
+                                          args, km::FP3_SMEM, st));
+        ++launches;
+        KM_CK(cudaMemcpyAsync(h_f3ctl, f3_ctl, sizeof(km::Fp3Ctl), cudaMemcpyDeviceToHost, st));
+        KM_TRY(sync_dec());
+        ++fp3_windows;
+        const km::Fp3Ctl r = *h_f3ctl;
+        if (r.status == km::FP3_STALE) ++fp3_stale;
+        for (int q = 0; q < 8; ++q) fp3_tphase[q] += r.tphase[q];
+        for (int q = 0; q < 3; ++q) fp3_stat[q] += r.pad[q];
+        if (r.swaps > 0) {
+            std::vector<Rec> tr((size_t)r.swaps);
+            KM_CK(cudaMemcpy(tr.data(), f3_trace, tr.size() * sizeof(Rec), cudaMemcpyDeviceToHost));
+            for (const Rec& x : tr) last_swaps.push_back(x);
+            fp3_tlast = pass_base + (tr.back().c - c0);
+            fp3_dirty = true;
+        }
+        fp3_t = pass_base + a + r.p_end;
+        return KM_OK;
+    }
+
     // One pass of Alg.4's scan (or its remainder up to the stop, F2).
     km_status swap_iter_fp3(int32_t* swaps_out, void* td_out) {
+        if (fp3_mode < 0) {
+            const char* e = getenv("KM_FASTER");
+            fp3_mode = (e && strcmp(e, "batch") == 0) ? 0 : 1;
+        }
+        if (fp3_mode == 1) return swap_iter_fp3_coop(swaps_out, td_out);
         KM_TRY(fp3_alloc());
         fp3_dirty = true;           // another variant may have changed the cache
         last_swaps.clear();
@@ -838,6 +960,37 @@ struct Impl : ImplBase {
         }
         if (swaps_out) *swaps_out = done;
         copy_td(td_out);
+        return (fp3_t - fp3_tlast >= n) ? KM_CONVERGED : KM_OK;
+    }
+
+    km_status swap_iter_fp3_coop(int32_t* swaps_out, void* td_out) {
+        KM_TRY(fp3_alloc());
+        KM_TRY(fp3c_alloc());
+        fp3_dirty = true;           // another variant may have changed the cache
+        last_swaps.clear();
+        if (swaps_out) *swaps_out = 0;
+        if (fp3_t - fp3_tlast >= n) { copy_td(td_out); return KM_CONVERGED; }
+        const int64_t pass_base = fp3_t - fp3_t % n, pass_end = pass_base + n;
+        bool first = true;
+        km::k_fp3_transpose_mc<T><<<dim3((unsigned)cdiv(n, 32), (unsigned)cdiv(k, 32)), dim3(32, 8), 0, st>>>(
+            MC, (int)n, k, f3_mct);
+        KM_CKL();
+        while (fp3_t < pass_end && fp3_t - fp3_tlast < n) {
+            const int64_t hi = std::min(std::min(pass_end, fp3_tlast + n), fp3_t + (int64_t)fp3c_ww - 3);
+            const auto h0 = std::chrono::steady_clock::now();
+            KM_TRY(fp3_window_coop(pass_base, fp3_t, hi, first));
+            fp3_host_ms += std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - h0).count();
+            first = false;
+        }
+        if (swaps_out) *swaps_out = (int32_t)last_swaps.size();
+        copy_td(td_out);
+        const char* ep = getenv("KM_FASTER_PROF");
+        if (ep && ep[0] == '1')
+            fprintf(stderr, "[fasterpam] pass: swaps %zu windows %lld stale %lld | ms pick %.2f apply %.2f rescan %.2f "
+                    "compact %.2f correct %.2f fold %.2f | sum nres %lld m %lld T %lld | window host ms %.2f\n",
+                    last_swaps.size(), (long long)fp3_windows, (long long)fp3_stale, fp3_tphase[0] * 1e-6,
+                    fp3_tphase[1] * 1e-6, fp3_tphase[2] * 1e-6, fp3_tphase[4] * 1e-6, fp3_tphase[5] * 1e-6,
+                    fp3_tphase[6] * 1e-6, fp3_stat[0], fp3_stat[1], fp3_stat[2], fp3_host_ms);
         return (fp3_t - fp3_tlast >= n) ? KM_CONVERGED : KM_OK;
     }
 

@@ -195,6 +195,61 @@ def test_fasterpam_fig1_instance():
     assert (r.n_iter, r.n_swaps) == (ref.n_iter, ref.n_swaps)
 
 
+def check_float_against_oracle(D, Dt, n, k, M0):
+    """GPU FasterPAM vs oracle.fasterpam_run on float data: identical swaps
+    until a near tie (1e-5*TD), every applied dTD = TD change from the
+    definition, final local optimum, TD within 1e-5; returns the GPU trace."""
+    ref = oracle.fasterpam_run(D, M0)
+    km = KM(Dt, n, k)
+    km.set_medoids(M0)
+    tr, passes, conv = gpu_passes(km)
+    assert conv
+    M = np.array(M0, np.int32)
+    diverged = False
+    for j, (i, c, v) in enumerate(tr):
+        td_before = oracle.td(D, M)
+        if not diverged:
+            ri, rc, rv, _ = ref.trace[j] if j < len(ref.trace) else (-1, -1, 0.0, -1)
+            if (ri, rc) != (i, c):
+                cache = oracle.assign(D, M)
+                R = oracle.removal_loss(cache, k)
+                vec, plus = oracle.fastpam1_candidate(D, c, cache, R)
+                full = np.sort(vec + plus)
+                near_tie = abs(full[0]) <= FTOL * td_before or full[1] - full[0] <= FTOL * td_before
+                if rc >= 0:
+                    vr, pr = oracle.fastpam1_candidate(D, rc, cache, R)
+                    near_tie |= abs(np.min(vr + pr)) <= FTOL * td_before
+                assert near_tie, (j, (i, c, v), ref.trace[j] if j < len(ref.trace) else None)
+                diverged = True
+        M[i] = c
+        assert v == pytest.approx(oracle.td(D, M) - td_before, rel=1e-9, abs=1e-9 * td_before)
+    st = km.get_state()
+    assert st.medoids.tolist() == M.tolist()
+    assert st.td == pytest.approx(oracle.td(D, M), rel=1e-12)
+    assert st.td == pytest.approx(ref.td, rel=FTOL)
+    if not diverged:
+        assert len(tr) == len(ref.trace) and st.n_iter == ref.n_iter
+    v, s = km.eval_candidates()
+    assert np.min(np.where(s >= 0, v, np.inf)) >= -1e-9 * st.td
+    return tr
+
+
+def test_fasterpam_float_c4_recipe_from_build_deterministic():
+    """C4 recipe (32-D mixture, f32 Euclidean) at n=12000, k=200, GPU BUILD
+    start: oracle agreement as above, and two GPU runs are bitwise equal."""
+    cfg = kmsynth.CONFIGS[4]
+    n, k = 12000, 200
+    X = kmsynth.make_points(cfg, n=n)
+    Dt = kmsynth.dist_cuda(X, cfg.metric)
+    D = kmsynth.as_numpy_D(Dt)[:, :n]
+    M0, _ = KM(Dt, n, k).init_build()
+    tr = check_float_against_oracle(D, Dt, n, k, M0)
+    km = KM(Dt, n, k)
+    km.set_medoids(M0)
+    tr2, _, _ = gpu_passes(km)
+    assert tr2 == tr
+
+
 @pytest.mark.parametrize("windows", [ONE_TILE, DEFAULT], indirect=True)
 def test_fasterpam_float_c2_recipe(windows):
     """C2 recipe (f32 Euclidean), oracle-sized: the GPU's swap sequence equals
