@@ -250,6 +250,8 @@ struct Impl : ImplBase {
             : stream_kind == 2 ? choose_parts(n, w, WT_COLS, WT_RESIDENT)
 
                                : choose_parts(n, w, STREAM_COLS, RESIDENT_CTAS);
+        const char* ep = getenv("KM_PARTS");          // measurement override of the stream's row parts
+        if (ep && atoi(ep) > 0) P = std::min<int>(atoi(ep), (int)std::max<int64_t>(1, n / 64));
         Pb = choose_parts(n, w, STREAM_COLS, RESIDENT_CTAS);
         Pbt = choose_parts(n, w, SG_NC * 128, SG_MINB);
         const char* eb = getenv("KM_BUILD");
