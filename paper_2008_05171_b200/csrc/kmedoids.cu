@@ -92,6 +92,20 @@ int choose_parts(int64_t n, int64_t w, int cols_per_cta, int resident) {
 }
 
 
+// Row parts of the segment stream (measured): about 1000
+// rows per part, but between 3 and 8 waves of resident CTAs (3 per SM) --
+// more, shorter CTAs balance the Poisson-lumpy hit work across SMs; very
+// short parts cost ring fill/drain and combine bytes.
+int choose_parts_seg(int64_t n, int64_t w) {
+    const int64_t ncb = cdiv(w, SG_NC * 128);
+    const int64_t slots = (int64_t)NUM_SMS * SG_MINB;
+    int64_t P = n / 1000;
+    P = std::max<int64_t>(P, cdiv(3 * slots, ncb));
+    P = std::min<int64_t>(P, std::max<int64_t>(1, 8 * slots / ncb));
+    P = std::min<int64_t>(P, std::max<int64_t>(1, n / 64));
+    return (int)std::max<int64_t>(P, 1);
+}
+
 }  // namespace
 
 struct ImplBase {
@@ -220,13 +234,14 @@ struct Impl : ImplBase {
         // (default), tma = the same ring with stages across segments, ldg =
         // register-pipelined loads, wtma = warp-autonomous rings, cmp / tmaq =
         // compacted hit lists (CTA-wide / per warp).
-        stream_kind = 10;
+        stream_kind = 13;
         if (ev && strcmp(ev, "tma") == 0) stream_kind = 1;
         if (ev && strcmp(ev, "cmp") == 0) stream_kind = 6;
         if (ev && strcmp(ev, "tmaq") == 0) stream_kind = 9;
         if (ev && strcmp(ev, "seg") == 0) stream_kind = 10;
         if (ev && strcmp(ev, "seg6") == 0) stream_kind = 11;
         if (ev && strcmp(ev, "seg5") == 0) stream_kind = 12;
+        if (ev && strcmp(ev, "seg2") == 0) stream_kind = 13;
         if (ev && strcmp(ev, "ldg") == 0) stream_kind = 0;
         if (ev && strcmp(ev, "wtma") == 0) stream_kind = 2;
 
@@ -240,7 +255,7 @@ struct Impl : ImplBase {
         use_graph = !(eg && eg[0] == '0');
         const char* dnc = getenv("KM_DEBUG_NOCOMPUTE");        // perf experiment only: wrong results
         debug_nocompute = (dnc && dnc[0] == '1') ? 1 : 0;
-        P = stream_kind == 10 ? choose_parts(n, w, SG_NC * 128, SG_MINB)
+        P = (stream_kind == 10 || stream_kind == 13) ? choose_parts_seg(n, w)
             : stream_kind == 11 ? choose_parts(n, w, 6 * 128, 3)
             : stream_kind == 12 ? choose_parts(n, w, 5 * 128, 4)
             : stream_kind == 9 ? choose_parts(n, w, TQ_NC * 128, 2)
@@ -260,6 +275,8 @@ struct Impl : ImplBase {
         // counting-sort chunk: >= 256 objects and at most 128 chunks (keeps the
         // k x B count matrix of the one-block scan small)
         sort_chunk = (int)std::max<int64_t>(km::SORT_CHUNK_MIN, cdiv(cdiv(n, 128), 32) * 32);
+        if (const char* ec = getenv("KM_SORT_CHUNKS"))   // measurement override: target number of chunks
+            if (atoi(ec) > 0) sort_chunk = (int)std::max<int64_t>(32, cdiv(cdiv(n, atoi(ec)), 32) * 32);
         B = (int)cdiv(n, sort_chunk);
         ncomb = (int)cdiv(w, 128);
         ntd = (int)std::min<int64_t>(cdiv(n, 256), 1024);
@@ -405,6 +422,9 @@ struct Impl : ImplBase {
         if (profiling) KM_CK(record_ev(ev0));
         if (stream_kind == 10) {  // TMA ring, segment-aligned stages
             KM_TRY((launch_seg<SG_NC, SG_RB, SG_S, SG_MINB>(nullptr)));
+        } else if (stream_kind == 13) {
+            KM_TRY((launch_seg2<SG_NC, SG_RB, SG_S, SG_MINB>(D, w, wpad, P, o_plus, o_head, o_tail, o_imin, o_islot,
+                                                              nullptr)));
         } else if (stream_kind == 11) {
             KM_TRY((launch_seg<6, 4, 6, 3>(nullptr)));
         } else if (stream_kind == 12) {
@@ -457,11 +477,29 @@ struct Impl : ImplBase {
     template <int NC, int RB, int S, int MINB = 2>
     km_status launch_seg_win(const T* Dw, int ww, int wpadw, int Pw, A* plus_o, A* head_o, A* tail_o, A* imin_o,
                              int* islot_o, A* acc_out) {
+        if (stream_kind != 10)
+            return launch_seg2<NC, RB, S, MINB>(Dw, ww, wpadw, Pw, plus_o, head_o, tail_o, imin_o, islot_o, acc_out);
         using C = km::SegCfg<T, NC, RB, S>;
         auto kern = km::k_swap_stream_seg<T, A, NC, RB, S, MINB>;
         if (!seg_attr_set) {
             KM_CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM));
             seg_attr_set = true;
+        }
+        dim3 g((unsigned)cdiv(ww, C::COLS), Pw);
+        kern<<<g, C::THREADS, C::SMEM, st>>>(Dw, ld, ww, wpadw, (int)n, Pw, ri, R, plus_o, head_o, tail_o, imin_o,
+                                              islot_o, acc_out, rowd);
+        return KM_OK;
+    }
+
+    bool seg2_attr_set = false;
+    template <int NC, int RB, int S, int MINB = 2>
+    km_status launch_seg2(const T* Dw, int ww, int wpadw, int Pw, A* plus_o, A* head_o, A* tail_o, A* imin_o,
+                          int* islot_o, A* acc_out) {
+        using C = km::SegCfg<T, NC, RB, S>;
+        auto kern = km::k_swap_stream_seg2<T, A, NC, RB, S, MINB>;
+        if (!seg2_attr_set) {
+            KM_CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM));
+            seg2_attr_set = true;
         }
         dim3 g((unsigned)cdiv(ww, C::COLS), Pw);
         kern<<<g, C::THREADS, C::SMEM, st>>>(Dw, ld, ww, wpadw, (int)n, Pw, ri, R, plus_o, head_o, tail_o, imin_o,
