@@ -354,7 +354,9 @@ def run_ours(args):
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
                      "traffic": (committed_traffic(cfg.name) or {}).get("traffic_bytes"),
                      "traffic_source": (committed_traffic(cfg.name) or {}).get("source"),
-                     "kernel": "k_swap_stream_seg", "kernel_ms": k1_avg,
+                     "kernel": {"seg": "k_swap_stream_seg"}.get(os.environ.get("KM_STREAM", ""), "k_swap_stream_seg2")
+                     if not os.environ.get("KM_STREAM") or os.environ.get("KM_STREAM") in ("seg", "seg2")
+                     else os.environ["KM_STREAM"], "kernel_ms": k1_avg,
                      "alg_bytes_per_launch": alg_bytes, "peak_kind": peak_kind},
         "stream_share_of_step": k1_ms / total_ms,
         "gpu_launches": launches,

@@ -1934,6 +1934,113 @@ __global__ void k_swap_combine(int w, int64_t col_begin, int P, const A* __restr
     grid_min_rec(best, partials, counter, out);
 }
 
+// a4, parallel over parts: the same result as k_swap_combine (up to the
+// association of fp64 sums, reading R9), with CG thread groups per column.
+// Block = 32 columns x CG warps; warp g folds the contiguous part range g of
+// its column into a range state (head segment, tail segment, best completed
+// segment, plus); warp 0 merges the CG states in order (deterministic).
+// A segment is complete once a later range starts another slot; the head
+// segment of the whole column and its tail segment are complete at the end.
+template <typename A>
+struct CombState {
+    int hs, ts;          // slot of the first / last segment of the range (hs < 0: empty range)
+    A hsum, tsum;        // their partial sums (single segment: hsum only)
+    A plus;
+    A bv;                // best completed (R_s + acc_s, s) inside the range
+    int bs;
+};
+
+// Append range b to range a (rows sorted by slot, so a slot is one run).
+// fin(slot, sum) receives every segment that becomes complete.
+template <typename A, typename Fin>
+__device__ __forceinline__ void comb_merge(CombState<A>& a, const CombState<A>& b, Fin&& fin) {
+    if (b.hs < 0) return;
+    if (a.hs < 0) { a = b; return; }
+    a.plus += b.plus;
+    if (b.bv < a.bv || (b.bv == a.bv && b.bs < a.bs)) { a.bv = b.bv; a.bs = b.bs; }
+    const bool sa = a.hs == a.ts, sb = b.hs == b.ts;
+    if (a.ts == b.hs) {                       // the boundary segment continues into b
+        const A joined = (sa ? a.hsum : a.tsum) + b.hsum;
+        if (sa && sb) { a.hsum = joined; }
+        else if (sa) { a.hsum = joined; a.ts = b.ts; a.tsum = b.tsum; }
+        else if (sb) { a.tsum = joined; }
+        else { fin(a.ts, joined); a.ts = b.ts; a.tsum = b.tsum; }
+    } else {
+        if (!sa) fin(a.ts, a.tsum);           // a's last segment ends at the boundary
+        if (!sb) fin(b.hs, b.hsum);           // b's first segment ends inside b
+        a.ts = b.ts;
+        a.tsum = sb ? b.hsum : b.tsum;
+    }
+}
+
+template <typename A, int CG>
+__global__ void __launch_bounds__(32 * CG)
+k_swap_combine_par(int w, int64_t col_begin, int P, const A* __restrict__ in_plus,
+                   const A* __restrict__ in_head, const A* __restrict__ in_tail,
+                   const A* __restrict__ in_imin, const int* __restrict__ in_islot,
+                   const int* __restrict__ head_slot, const int* __restrict__ tail_slot,
+                   const A* __restrict__ R, const int* __restrict__ empty_slot,
+                   const int* __restrict__ point_slot, A* __restrict__ cand_v,
+                   int* __restrict__ cand_slot, Rec<A>* partials, unsigned* counter,
+                   Rec<A>* out, A* __restrict__ acc_out = nullptr, A* __restrict__ plus_out = nullptr) {
+    __shared__ CombState<A> sst[CG][32];
+    const int lane = threadIdx.x & 31, g = threadIdx.x >> 5;
+    const int cl = blockIdx.x * 32 + lane;
+    CombState<A> st;
+    st.hs = -1; st.ts = -1; st.hsum = 0; st.tsum = 0; st.plus = 0; st.bv = amax<A>(); st.bs = INT_MAX;
+    auto fin = [&](int sl, A sum) {
+        if (acc_out) acc_out[(int64_t)sl * w + cl] = sum;
+        const A val = R[sl] + sum;
+        if (val < st.bv || (val == st.bv && sl < st.bs)) { st.bv = val; st.bs = sl; }
+    };
+    if (cl < w) {
+        const int q0 = (int)((int64_t)g * P / CG), q1 = (int)((int64_t)(g + 1) * P / CG);
+        constexpr int QU = 4;
+        for (int qb = q0; qb < q1; qb += QU) {
+            A pl[QU], hv[QU], tv[QU], iv[QU];
+            int isl[QU], hs[QU], ts[QU];
+#pragma unroll
+            for (int u = 0; u < QU; ++u) {
+                const int q = qb + u;
+                if (q < q1) {
+                    const int64_t idx = (int64_t)q * w + cl;
+                    pl[u] = in_plus[idx]; hv[u] = in_head[idx]; tv[u] = in_tail[idx];
+                    iv[u] = in_imin[idx]; isl[u] = in_islot[idx];
+                    hs[u] = head_slot[q]; ts[u] = tail_slot[q];
+                }
+            }
+#pragma unroll
+            for (int u = 0; u < QU; ++u) {
+                if (qb + u >= q1) break;
+                CombState<A> b;
+                b.hs = hs[u]; b.ts = ts[u]; b.hsum = hv[u]; b.tsum = (ts[u] != hs[u]) ? tv[u] : (A)0;
+                b.plus = pl[u];
+                if (isl[u] >= 0) { b.bv = iv[u]; b.bs = isl[u]; } else { b.bv = amax<A>(); b.bs = INT_MAX; }
+                comb_merge(st, b, fin);
+            }
+        }
+    }
+    sst[g][lane] = st;
+    __syncthreads();
+    Rec<A> best = rec_none<A>();
+    if (g == 0 && cl < w) {
+        for (int gg = 1; gg < CG; ++gg) comb_merge(st, sst[gg][lane], fin);
+        // the column's first and last segments are complete
+        fin(st.hs, st.hsum);
+        if (st.ts != st.hs) fin(st.ts, st.tsum);
+        const int es = *empty_slot;
+        if (es != INT_MAX && (0 < st.bv || (0 == st.bv && es < st.bs))) { st.bv = 0; st.bs = es; }
+        if (plus_out) plus_out[cl] = st.plus;
+        const A dtd = st.bv + st.plus;
+        const int64_t c = col_begin + cl;
+        const bool medoid = point_slot[c] >= 0;
+        cand_v[cl] = dtd;
+        cand_slot[cl] = medoid ? -1 : st.bs;
+        if (!medoid) { best.v = dtd; best.slot = st.bs; best.c = (int)c; }
+    }
+    grid_min_rec(best, partials, counter, out);
+}
+
 // Acceptance (reading R5) and bookkeeping of the chosen swap (Alg.3):
 // lexicographic min over the gathered per-rank records, then M[i*] <- c*,
 // TD <- TD + dTD*.  Runs as one thread; identical on every rank.

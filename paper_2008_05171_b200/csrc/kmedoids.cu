@@ -75,7 +75,8 @@ constexpr int TQ_NC = 7, TQ_RB = 4, TQ_S = 6;
 // TMA ring with segment-aligned stages: 7 consumer warps + 1 producer, 4 rows x
 // 5 stages (~72 KB shared memory), 3 CTAs = 24 warps per SM (<= 80 registers).
 constexpr int SG_NC = 7, SG_RB = 4, SG_S = 5, SG_MINB = 3;
-constexpr int FP2_SPLIT = 8;   // column splits of the FastPAM2 per-slot reduction
+constexpr int FP2_SPLIT = 8;
+constexpr int COMB_G = 8;      // warps (part groups) per column block of k_swap_combine_par   // column splits of the FastPAM2 per-slot reduction
 constexpr int WT_COLS = WT_NW * 128;
 constexpr int WT_RESIDENT = 4;
 constexpr int TMA_RESIDENT = 2;
@@ -309,7 +310,7 @@ struct Impl : ImplBase {
         b_out = o_plus;   // BUILD partial sums reuse the plus buffer (sized for max(P, Pb))
         KM_TRY(alloc(&cand_v, w));
         KM_TRY(alloc(&cand_slot, w));
-        KM_TRY(alloc(&partials, std::max(ncomb, 1)));
+        KM_TRY(alloc(&partials, std::max<int64_t>(cdiv(w, 32), 1)));
         KM_TRY(alloc(&rec_local, 1));
         KM_TRY(alloc(&counters, 2));
         KM_TRY(alloc(&td, 1));
@@ -460,9 +461,29 @@ struct Impl : ImplBase {
         }
         KM_CKL();
         if (profiling) { KM_CK(record_ev(ev1)); pending_prof = true; }
-        km::k_swap_combine<A><<<ncomb, 128, 0, st>>>(w, c0, P, o_plus, o_head, o_tail, o_imin, o_islot, head_slot,
-                                                      tail_slot, R, empty_slot, point_slot, cand_v, cand_slot,
-                                                      partials, counters, rec_local);
+        KM_TRY(launch_combine(w, c0, P, o_plus, o_head, o_tail, o_imin, o_islot, head_slot, tail_slot, cand_v, cand_slot,
+                              nullptr, nullptr));
+        return KM_OK;
+    }
+
+    // a4: per-candidate combine of the stream's part outputs: one thread per
+    // column (default); KM_COMBINE=par folds part groups in parallel warps and
+    // merges them (measured 10-30 us SLOWER per step at C4/C5, kept for A/B)
+    int combine_kind = -1;
+    km_status launch_combine(int ww, int64_t colb, int Pw, const A* pl, const A* hd, const A* tl, const A* im,
+                             const int* isl, const int* hsl, const int* tsl, A* cv, int* cs, A* acc_o, A* plus_o) {
+        if (combine_kind < 0) {
+            const char* e = getenv("KM_COMBINE");
+            combine_kind = (e && strcmp(e, "par") == 0) ? 1 : 0;
+        }
+        if (combine_kind == 0)
+            km::k_swap_combine<A><<<(unsigned)cdiv(ww, 128), 128, 0, st>>>(ww, colb, Pw, pl, hd, tl, im, isl, hsl, tsl, R,
+                                                                            empty_slot, point_slot, cv, cs, partials,
+                                                                            counters, rec_local, acc_o, plus_o);
+        else
+            km::k_swap_combine_par<A, COMB_G><<<(unsigned)cdiv(ww, 32), 32 * COMB_G, 0, st>>>(
+                ww, colb, Pw, pl, hd, tl, im, isl, hsl, tsl, R, empty_slot, point_slot, cv, cs, partials, counters,
+                rec_local, acc_o, plus_o);
         KM_CKL();
         return KM_OK;
     }
@@ -672,10 +693,8 @@ struct Impl : ImplBase {
         KM_TRY((launch_seg<SG_NC, SG_RB, SG_S, SG_MINB>(fp2_acc)));
         KM_CKL();
         if (profiling) { KM_CK(record_ev(ev1)); pending_prof = true; }
-        km::k_swap_combine<A><<<ncomb, 128, 0, st>>>(w, c0, P, o_plus, o_head, o_tail, o_imin, o_islot, head_slot,
-                                                      tail_slot, R, empty_slot, point_slot, cand_v, cand_slot,
-                                                      partials, counters, rec_local, fp2_acc, fp2_plus);
-        KM_CKL();
+        KM_TRY(launch_combine(w, c0, P, o_plus, o_head, o_tail, o_imin, o_islot, head_slot, tail_slot, cand_v, cand_slot,
+                              fp2_acc, fp2_plus));
         km::k_fp2_slot_best<A><<<dim3(k, FP2_SPLIT), 256, 0, st>>>(w, c0, fp2_acc, fp2_plus, R, seg_start, point_slot,
                                                                      fp2_part);
         KM_CKL();
@@ -837,10 +856,8 @@ struct Impl : ImplBase {
                                                              f3_islot, nullptr)));
         KM_CKL();
         if (profiling) { KM_CK(record_ev(ev1)); pending_prof = true; }
-        km::k_swap_combine<A><<<(unsigned)cdiv(ww, 128), 128, 0, st>>>(
-            ww, c0 + a, Pw, f3_plus, f3_head, f3_tail, f3_imin, f3_islot, f3_hs, f3_ts, R, empty_slot, point_slot,
-            f3_v, f3_s, partials, counters, rec_local);
-        KM_CKL();
+        KM_TRY(launch_combine(ww, c0 + a, Pw, f3_plus, f3_head, f3_tail, f3_imin, f3_islot, f3_hs, f3_ts, f3_v, f3_s,
+                              nullptr, nullptr));
         km::k_fp3_pick<A><<<1, 1024, 0, st>>>(f3_v, f3_s, clo - a, chi - a, c0 + a, td, M, point_slot, dec,
                                               rescan_count, new_pass ? 1 : 0);
         KM_CKL();
@@ -923,10 +940,8 @@ struct Impl : ImplBase {
                                                              f3_islot, f3_acc)));
         KM_CKL();
         if (profiling) { KM_CK(record_ev(ev1)); pending_prof = true; }
-        km::k_swap_combine<A><<<(unsigned)cdiv(ww, 128), 128, 0, st>>>(
-            ww, c0 + a, Pw, f3_plus, f3_head, f3_tail, f3_imin, f3_islot, f3_hs, f3_ts, R, empty_slot, point_slot,
-            f3_v, f3_s, partials, counters, rec_local, f3_acc, f3_wplus);
-        KM_CKL();
+        KM_TRY(launch_combine(ww, c0 + a, Pw, f3_plus, f3_head, f3_tail, f3_imin, f3_islot, f3_hs, f3_ts, f3_v, f3_s,
+                              f3_acc, f3_wplus));
         km::Fp3Ctl hc;
         memset(&hc, 0, sizeof(hc));
         hc.first[0] = hc.first[1] = hc.first[2] = INT_MAX;
