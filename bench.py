@@ -229,8 +229,7 @@ def run_ours(args):
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     if world > 1 or args.gpus > 1 or args.sharded:
-        from paper_2008_05171_b200 import parallel
-        return parallel.bench_main(args)
+        return run_sharded(args)
 
     torch.cuda.set_device(0)
     cfg = kmsynth.CONFIGS[args.config]
@@ -369,6 +368,128 @@ def run_ours(args):
         "fasterpam": fpm,
     }
     print(json.dumps(line), flush=True)
+
+
+# ------------------------------------------------------------------------------------------
+# N > 1: column-sharded path (paper_2008_05171_b200.parallel), one rank per GPU over NCCL
+# ------------------------------------------------------------------------------------------
+def run_sharded(args):
+    import torch
+    import torch.distributed as dist
+
+    import kmsynth
+    from paper_2008_05171_b200 import parallel
+    from paper_2008_05171_b200.kmedoids import pinned_empty
+
+    os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+    os.environ.setdefault("MASTER_PORT", "29517")
+    os.environ.setdefault("RANK", "0")
+    os.environ.setdefault("WORLD_SIZE", "1")
+    rank = int(os.environ["RANK"])
+    world = int(os.environ["WORLD_SIZE"])
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    if not dist.is_initialized():
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    comm = parallel.TorchComm()
+    cfg = kmsynth.CONFIGS[args.config]
+    n, k = cfg.n, cfg.k
+    cb = parallel.column_bounds(n, world)
+    X = kmsynth.make_points(cfg)
+    Dt = kmsynth.dist_cuda(X, cfg.metric, int(cb[rank]), int(cb[rank + 1]))
+    stream = torch.cuda.current_stream()
+    fp2 = args.variant == "fastpam2"
+
+    def job(D_slab):
+        h = parallel.CudaShard(D_slab, n, k, rank, cb, stream=stream)
+        if cfg.init == "build":
+            parallel.build([h], comm, cb, k)
+        else:
+            parallel.set_medoids([h], comm, cb, kmsynth.random_medoids(cfg), n)
+        return h
+
+    torch.cuda.synchronize()
+    dist.barrier()
+    t0 = time.perf_counter()
+    h = job(Dt)
+    torch.cuda.synchronize()
+    init_s = comm.max_over_ranks(time.perf_counter() - t0)
+
+    def step(hh):
+        return parallel.fp2_iter([hh], comm, cb) if fp2 else parallel.swap_iter([hh], comm, cb)
+
+    for _ in range(args.warmup):
+        step(h)
+    h.km.set_profiling(True)
+    h.km.stream_time(reset=True)
+    l0 = h.km.launch_count()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    dist.barrier()
+    with ClockSampler(local) as clk:
+        e0.record(stream)
+        for _ in range(args.steps):
+            step(h)
+        e1.record(stream)
+        torch.cuda.synchronize()
+    dist.barrier()
+    ms = comm.max_over_ranks(e0.elapsed_time(e1))
+    launches = h.km.launch_count() - l0
+    k1_ms, k1_n = h.km.stream_time(reset=True)
+    k1_ms = comm.max_over_ranks(k1_ms)
+    h.km.set_profiling(False)
+    ms_step = ms / args.steps
+    pairs = k * (n - k)
+    value = pairs / (ms_step / 1e3)
+
+    # e2e: every rank copies its slab from pinned host memory, then the whole
+    # sharded job (init + SWAP to convergence) and the D2H of the result
+    e2e = None
+    if not args.no_e2e:
+        Dh, Dh_t = pinned_empty(tuple(Dt.shape), cfg.dtype)
+        Dh_t.copy_(Dt)
+        h.km.close()
+        del h
+        torch.cuda.synchronize()
+        dist.barrier()
+        t1 = time.perf_counter()
+        Dd = Dh_t.to(Dt.device, non_blocking=True)
+        h2 = job(Dd)
+        it = 0
+        while it < 2000:
+            it += 1
+            res = step(h2)
+            if res[0]:
+                break
+        st = h2.km.get_state()
+        torch.cuda.synchronize()
+        e2e_s = comm.max_over_ranks(time.perf_counter() - t1)
+        e2e = {"value": it * pairs / e2e_s, "unit": "pair-evals/s", "h2d_bytes_per_step": int(Dh.nbytes) * world,
+               "d2h_bytes_per_step": int(4 * (k + n) + 8),
+               "job": f"every rank: H2D of its {Dh.nbytes / 1e9:.2f} GB slab (pinned) + {cfg.init} init + {it} SWAP "
+                      f"iterations to convergence + D2H of medoids/assignment/TD; max over ranks",
+               "seconds": e2e_s, "n_iter": it, "td": st.td}
+    if rank == 0:
+        peak, peak_kind = measured_peaks()
+        slab_bytes = 4.0 * n * (int(cb[1]) - int(cb[0]))
+        k1_avg = k1_ms / max(1, k1_n)
+        ach = slab_bytes / (k1_avg / 1e3) / 1e9
+        line = {"metric": "swap_pair_evals_per_s", "value": value, "unit": "pair-evals/s", "n_gpus": world,
+                "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
+                "scaling": "strong", "vs_baseline": None,
+                "dtype": "f32->f64" if cfg.metric == kmsynth.L2_F32 else "u32->int64", "data": "synthetic",
+                "config": {"workload": workload_name(cfg, args.variant) + f", column-sharded over {world} GPUs",
+                           "n": n, "k": k, "variant": args.variant, "parallelism": f"column-shard x{world}",
+                           "l2": "inputs larger than L2, no flush needed"},
+                "s_per_iteration": ms_step / 1e3,
+                "roofline": {"bound": "hbm", "achieved": ach, "peak": peak, "unit": "GB/s", "frac": ach / peak,
+                             "traffic": None, "kernel": "k_swap_stream_seg2 (rank 0 slab)", "kernel_ms": k1_avg,
+                             "alg_bytes_per_launch": slab_bytes, "peak_kind": peak_kind},
+                "gpu_launches": launches, "clocks": clk.summary(), "init": {"kind": cfg.init, "s": init_s},
+                "e2e": e2e, "cpu_baseline": None}
+        print(json.dumps(line), flush=True)
+    dist.barrier()
+    dist.destroy_process_group()
 
 
 def main():

@@ -18,6 +18,7 @@
 #include "../../include/kmedoids.h"
 #include "km_kernels.cuh"
 #include "km_fasterpam.cuh"
+#include "km_post.cuh"
 
 namespace {
 
@@ -187,6 +188,7 @@ struct Impl : ImplBase {
     A *td = nullptr, *td_partials = nullptr;
     Dec* dec = nullptr;
     Dec* h_dec = nullptr;           // pinned mirror
+    A* h_td = nullptr;              // pinned mirror of TD (FastPAM1 iteration)
     // FastPAM2 state (allocated on first use)
     A* fp2_acc = nullptr;           // [k][w] complete acc_c[i]
     A* fp2_plus = nullptr;          // [w]    dTD^{+x_c}
@@ -207,6 +209,7 @@ struct Impl : ImplBase {
         if (cap_st) cudaStreamDestroy(cap_st);
         for (void* p : bufs) cudaFree(p);
         if (h_dec) cudaFreeHost(h_dec);
+        if (h_td) cudaFreeHost(h_td);
         if (ev0) cudaEventDestroy(ev0);
         if (ev1) cudaEventDestroy(ev1);
     }
@@ -321,6 +324,7 @@ struct Impl : ImplBase {
         KM_CK(cudaMemsetAsync(point_slot, 0xff, n * sizeof(int), st));
         KM_CK(cudaMallocHost((void**)&h_dec, sizeof(Dec)));
         memset(h_dec, 0, sizeof(Dec));
+        KM_CK(cudaMallocHost((void**)&h_td, sizeof(A)));
         KM_CK(cudaEventCreate(&ev0));
         KM_CK(cudaEventCreate(&ev1));
         KM_CK(cudaStreamSynchronize(st));
@@ -397,6 +401,7 @@ struct Impl : ImplBase {
         KM_CK(cudaStreamSynchronize(st));
         ready = true;
         fp3_reset();
+        fp1_prepped = false;
         return KM_OK;
     }
 
@@ -418,8 +423,8 @@ struct Impl : ImplBase {
     }
 
     // a3 + a4 (local): stream the slab, combine into the local best record.
-    km_status eval_local() {
-        KM_TRY(prep());
+    km_status eval_local(bool do_prep = true) {
+        if (do_prep) KM_TRY(prep());
         if (profiling) KM_CK(record_ev(ev0));
         if (stream_kind == 10) {  // TMA ring, segment-aligned stages
             KM_TRY((launch_seg<SG_NC, SG_RB, SG_S, SG_MINB>(nullptr)));
@@ -590,14 +595,59 @@ struct Impl : ImplBase {
         memcpy(td_out, &v, sizeof(A));
     }
 
+    // ---- fused post-stream kernel (km_post.cuh; KM_POST=0 disables) -----------
+    int use_post = -1;
+    bool fp1_prepped = false;       // slot sort / R / part metadata valid for the current cache
+    int post_blocks = 0;
+    int *post_counts = nullptr, *post_offsets = nullptr;
+
+    km_status post_alloc() {
+        if (post_counts) return KM_OK;
+        auto kern = km::k_fp1_post<T, A>;
+        const size_t sm = (size_t)k * sizeof(int);
+        if (sm > 48 * 1024) KM_CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+        int dev = 0, per_sm = 0, nsm = 0;
+        KM_CK(cudaGetDevice(&dev));
+        KM_CK(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
+        KM_CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, km::POST_THREADS, sm));
+        if (per_sm < 1) return fail(KM_ECUDA, "k_fp1_post cannot be resident");
+        post_blocks = nsm * std::min(per_sm, 4);
+        post_blocks = (int)std::min<int64_t>(post_blocks, std::max<int64_t>(1, cdiv(n, 64)));
+        KM_TRY(alloc(&post_counts, (size_t)k * post_blocks));
+        KM_TRY(alloc(&post_offsets, (size_t)k * post_blocks));
+        return KM_OK;
+    }
+
+    km_status launch_post() {
+        km::PostArgs<T, A> g;
+        g.D = D; g.ld = ld; g.n = (int)n; g.k = k; g.c0 = c0; g.c1 = c1; g.recs = rec_local; g.nrec = 1;
+        g.td = td; g.M = M; g.point_slot = point_slot; g.dec = dec; g.MC = MC; g.near = near; g.sec = sec;
+        g.dn = dn; g.ds = ds; g.rescan = rescan; g.rescan_count = rescan_count; g.counts = post_counts;
+        g.offsets = post_offsets; g.slot_tot = slot_tot; g.seg_start = seg_start; g.empty_slot = empty_slot;
+        g.ri = ri; g.rowd = rowd; g.R = R; g.P = P; g.head_slot = head_slot; g.tail_slot = tail_slot;
+        void* args[] = {&g};
+        KM_CK(cudaLaunchCooperativeKernel((void*)km::k_fp1_post<T, A>, dim3(post_blocks), dim3(km::POST_THREADS), args,
+                                          (size_t)k * sizeof(int), st));
+        ++launches;
+        return KM_OK;
+    }
+
     // One FastPAM1 iteration, enqueued on st (graph-capturable: fixed pointers,
-    // no host-side memory other than the pinned decision mirror).
+    // no host-side memory other than the pinned decision mirror).  With the
+    // post kernel the slot sort of this iteration was done by the previous
+    // one (or by swap_iter before the first).
     km_status enqueue_fp1_iteration() {
         const bool prof_save = profiling;
         if (use_graph) profiling = true;      // the graph always carries the stream events
-        km_status s = eval_local();
+        km_status s = eval_local(use_post != 1);
         profiling = prof_save;
         if (s != KM_OK) return s;
+        if (use_post == 1) {
+            KM_TRY(launch_post());
+            KM_CK(cudaMemcpyAsync(h_dec, dec, sizeof(Dec), cudaMemcpyDeviceToHost, st));
+            KM_CK(cudaMemcpyAsync(h_td, td, sizeof(A), cudaMemcpyDeviceToHost, st));
+            return KM_OK;
+        }
         km::k_select<A><<<1, 1, 0, st>>>(rec_local, 1, td, M, point_slot, dec, rescan_count);
         KM_CKL();
         KM_TRY(apply_local());
@@ -612,6 +662,16 @@ struct Impl : ImplBase {
             return fail(KM_EINVAL, "unknown variant %d", (int)v);
         if (v == KM_FASTPAM2) return swap_iter_fp2(swaps, td_out);
         if (v == KM_FASTERPAM) return swap_iter_fp3(swaps, td_out);
+        if (use_post < 0) {
+            const char* e = getenv("KM_POST");
+            use_post = (e && e[0] == '0') ? 0 : 1;
+            if (use_post == 1 && (stream_kind != 10 && stream_kind != 13)) use_post = 0;
+            if (use_post == 1) KM_TRY(post_alloc());
+        }
+        if (use_post == 1 && !fp1_prepped) {
+            KM_TRY(prep());
+            KM_CK(cudaMemsetAsync(rescan_count, 0, sizeof(int), st));
+        }
         if (use_graph && fp1_iters >= 1) {
             // the whole iteration (11 kernels + the 32-byte decision copy) as one CUDA graph
             if (!fp1_exec) {
@@ -629,13 +689,26 @@ struct Impl : ImplBase {
                 cudaGraph_t g = nullptr;
                 cudaError_t ce = cudaStreamEndCapture(st, &g);
                 st = user_st;
-                if (cs != KM_OK) { if (g) cudaGraphDestroy(g); return cs; }
-                if (ce != cudaSuccess) return fail(KM_ECUDA, "graph capture failed: %s", cudaGetErrorString(ce));
-                ce = cudaGraphInstantiate(&fp1_exec, g, 0);
-                cudaGraphDestroy(g);
-                if (ce != cudaSuccess) { fp1_exec = nullptr; return fail(KM_ECUDA, "graph instantiate: %s", cudaGetErrorString(ce)); }
-                fp1_graph_kernels = launches - l0;
+                bool graph_ok = (cs == KM_OK && ce == cudaSuccess);
+                if (graph_ok) {
+                    ce = cudaGraphInstantiate(&fp1_exec, g, 0);
+                    if (ce != cudaSuccess) { fp1_exec = nullptr; graph_ok = false; }
+                }
+                if (g) cudaGraphDestroy(g);
+                const int64_t captured = launches - l0;
                 launches = l0;
+                if (!graph_ok) {
+                    // e.g. a cooperative launch the capture does not accept: run the
+                    // iteration directly from now on
+                    const cudaError_t le = cudaGetLastError();
+                    fprintf(stderr, "[kmedoids] FastPAM1 iteration graph unavailable (%s / %s); launching directly\n",
+                            cudaGetErrorString(ce), cudaGetErrorString(le));
+                    use_graph = false;
+                    KM_TRY(enqueue_fp1_iteration());
+                    KM_TRY(sync_dec());
+                    goto iteration_done;
+                }
+                fp1_graph_kernels = captured;
             }
             KM_CK(cudaGraphLaunch(fp1_exec, st));
             launches += fp1_graph_kernels;
@@ -650,14 +723,17 @@ struct Impl : ImplBase {
             KM_TRY(enqueue_fp1_iteration());
             KM_TRY(sync_dec());
         }
+    iteration_done:
         ++fp1_iters;
+        fp1_prepped = (use_post == 1);
         last_swaps.clear();
         if (h_dec->apply) {
             Rec r; r.v = h_dec->dtd; r.slot = h_dec->slot; r.c = h_dec->c;
             last_swaps.push_back(r);
         }
         if (swaps) *swaps = h_dec->apply;
-        copy_td(td_out);
+        if (use_post == 1) { if (td_out) memcpy(td_out, h_td, sizeof(A)); }   // mirrored in the iteration
+        else copy_td(td_out);
         return h_dec->apply ? KM_OK : KM_CONVERGED;
     }
 
@@ -781,6 +857,7 @@ struct Impl : ImplBase {
 
     // One single-GPU FastPAM2 iteration (reading R6).
     km_status swap_iter_fp2(int32_t* swaps_out, void* td_out) {
+        fp1_prepped = false;
         KM_TRY(fp2_eval_local());
         A tdh;
         KM_CK(cudaMemcpyAsync(h_best.data(), fp2_best, k * sizeof(Rec), cudaMemcpyDeviceToHost, st));
@@ -981,6 +1058,7 @@ struct Impl : ImplBase {
 
     // One pass of Alg.4's scan (or its remainder up to the stop, F2).
     km_status swap_iter_fp3(int32_t* swaps_out, void* td_out) {
+        fp1_prepped = false;
         if (fp3_mode < 0) {
             const char* e = getenv("KM_FASTER");
             fp3_mode = (e && strcmp(e, "batch") == 0) ? 0 : 1;
@@ -1189,6 +1267,7 @@ struct Impl : ImplBase {
             KM_TRY(assign_full_and_td());
             ready = true;
             fp3_reset();
+            fp1_prepped = false;
         }
         KM_TRY(reset_counters());
         return KM_OK;
@@ -1281,6 +1360,7 @@ struct Impl : ImplBase {
         KM_CK(cudaStreamSynchronize(st));
         ready = true;
         fp3_reset();
+        fp1_prepped = false;
         return KM_OK;
     }
 

@@ -181,10 +181,12 @@ class KMedoids:
         return M, td[0].item()
 
     def swap_iter(self, variant="fastpam1"):
-        sw = np.zeros(1, np.int32)
-        td = np.zeros(1, self.acc)
-        s = _check(load_library().kmedoids_swap_iter(self.h, VARIANTS[variant], _p(sw), _p(td)),
-                   ok=(KM_OK, KM_CONVERGED))
+        if getattr(self, "_it_bufs", None) is None:        # reused: keeps the per-call host work small
+            sw = np.zeros(1, np.int32)
+            td = np.zeros(1, self.acc)
+            self._it_bufs = (sw, td, _p(sw), _p(td))
+        sw, td, psw, ptd = self._it_bufs
+        s = _check(load_library().kmedoids_swap_iter(self.h, VARIANTS[variant], psw, ptd), ok=(KM_OK, KM_CONVERGED))
         return s == KM_CONVERGED, int(sw[0]), td[0].item()
 
     def run(self, use_build=True, variant="fastpam1", max_iter=2000) -> Result:

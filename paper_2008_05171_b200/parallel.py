@@ -282,93 +282,3 @@ class CudaShard:
 
     def __getattr__(self, name):       # shard_eval, shard_select, ... -> the handle
         return getattr(self.km, name)
-
-
-# ---------------------------------------------------------------------------
-# bench entry (torchrun, one rank per GPU)
-# ---------------------------------------------------------------------------
-def bench_main(args):
-    import json
-
-    import torch
-    import torch.distributed as dist
-
-    import kmsynth
-
-    os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
-    os.environ.setdefault("MASTER_PORT", "29517")
-    os.environ.setdefault("RANK", "0")
-    os.environ.setdefault("WORLD_SIZE", "1")
-    rank = int(os.environ.get("RANK", "0"))
-    world = int(os.environ.get("WORLD_SIZE", "1"))
-    local = int(os.environ.get("LOCAL_RANK", "0"))
-    torch.cuda.set_device(local)
-    if not dist.is_initialized():
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    comm = TorchComm()
-    cfg = kmsynth.CONFIGS[args.config]
-    n, k = cfg.n, cfg.k
-    cb = column_bounds(n, world)
-    X = kmsynth.make_points(cfg)
-    Dt = kmsynth.dist_cuda(X, cfg.metric, int(cb[rank]), int(cb[rank + 1]))
-    stream = torch.cuda.current_stream()
-    h = CudaShard(Dt, n, k, rank, cb, stream=stream)
-    hs = [h]
-    torch.cuda.synchronize()
-    dist.barrier()
-    t0 = time.perf_counter()
-    if cfg.init == "build":
-        build(hs, comm, cb, k)
-    else:
-        set_medoids(hs, comm, cb, kmsynth.random_medoids(cfg), n)
-    torch.cuda.synchronize()
-    init_s = comm.max_over_ranks(time.perf_counter() - t0)
-    fp2 = getattr(args, "variant", "fastpam1") == "fastpam2"
-
-    def step():
-        return fp2_iter(hs, comm, cb) if fp2 else swap_iter(hs, comm, cb)
-
-    for _ in range(args.warmup):
-        step()
-    h.km.set_profiling(True)
-    h.km.stream_time(reset=True)
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    torch.cuda.synchronize()
-    dist.barrier()
-    e0.record(stream)
-    for _ in range(args.steps):
-        step()
-    e1.record(stream)
-    torch.cuda.synchronize()
-    dist.barrier()
-    ms = comm.max_over_ranks(e0.elapsed_time(e1))
-    k1_ms, k1_n = h.km.stream_time(reset=True)
-    k1_ms = comm.max_over_ranks(k1_ms)
-    ms_step = ms / args.steps
-    pairs = k * (n - k)
-    value = pairs / (ms_step / 1e3)
-    if rank == 0:
-        peak = 6551.4
-        try:
-            peak = json.load(open(os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))),
-                                               "MEASURED_PEAKS.json")))["hbm_gbs"]
-        except Exception:
-            pass
-        slab_bytes = 4.0 * n * (int(cb[1]) - int(cb[0]))
-        k1_avg = k1_ms / max(1, k1_n)
-        ach = slab_bytes / (k1_avg / 1e3) / 1e9
-        line = {"metric": "swap_pair_evals_per_s", "value": value, "unit": "pair-evals/s", "n_gpus": world,
-                "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
-                "scaling": "strong", "vs_baseline": None,
-                "dtype": "f32->f64" if cfg.metric == kmsynth.L2_F32 else "u32->int64", "data": "synthetic",
-                "config": {"workload": f"{cfg.name} n={n} k={k} ({'f32 Euclidean' if cfg.metric else 'u32 L1 x100'}, "
-                                       f"{cfg.init} init, {args.variant}) column-sharded over {world} GPUs",
-                           "n": n, "k": k, "variant": args.variant, "parallelism": f"column-shard x{world}"},
-                "s_per_iteration": ms_step / 1e3,
-                "roofline": {"bound": "hbm", "achieved": ach, "peak": peak, "unit": "GB/s", "frac": ach / peak,
-                             "traffic": None, "kernel": "k_swap_stream (rank 0 slab)", "kernel_ms": k1_avg},
-                "init_s": init_s, "e2e": None, "cpu_baseline": None,
-                "gpu_launches": h.km.launch_count()}
-        print(json.dumps(line), flush=True)
-    dist.barrier()
-    dist.destroy_process_group()
