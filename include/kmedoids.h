@@ -154,6 +154,24 @@ km_status kmedoids_stream_time(km_handle* h, double* ms_out, int64_t* launches_o
 /* Number of CUDA kernel launches this handle has issued (all kernels). */
 km_status kmedoids_launch_count(km_handle* h, int64_t* count_out);
 
+/* ---------------- dissimilarity materialisation -----
+ * The dissimilarity matrix the method starts from ("computed in
+ * advance"; its cost dominates FasterPAM on MNIST), written
+ * directly in the layout a handle borrows: the column slab
+ * [col_begin, col_end) of all n rows, D[o*ld + (c - col_begin)].
+ *   KM_METRIC_L2_F32: X float32 (n x d, row-major, device), D float32,
+ *     d(x, y) = sqrt(max(0, |x|^2 + |y|^2 - 2 <x, y>)), inner products on the
+ *     tensor cores (tcgen05, tf32 hi/lo split: ~f32 accuracy), d <= 64,
+ *     D 16-byte aligned, ld % 4 == 0.  Diagonal exactly 0.  Accuracy: the
+ *     squared distance is within ~4 * 2^-22 (|x|^2 + |y|^2) of the exact one.
+ *   KM_METRIC_L1_U32: X int32 integer coordinates (n x d), D uint32,
+ *     d(x, y) = sum_t |x_t - y_t| exactly (caller keeps sums < 2^32).
+ * Asynchronous on cuda_stream; X and D are borrowed.  Errors: KM_EINVAL
+ * (sizes, alignment, d > 64 for L2), KM_ENOMEM, KM_ECUDA. */
+typedef enum { KM_METRIC_L2_F32 = 0, KM_METRIC_L1_U32 = 1 } km_metric;
+km_status kmedoids_dissimilarity(const void* X, km_metric metric, int64_t n, int32_t d, void* D, int64_t ld,
+                                 int64_t col_begin, int64_t col_end, void* cuda_stream);
+
 /* ---------------- sharded (column-slab) phase API ----------------------
  * A sharded SWAP iteration on R ranks is, on every rank:
  *   1. kmedoids_shard_eval(h)          local candidates -> 16-byte record

@@ -283,3 +283,21 @@ def build_init(D: np.ndarray, k: int):
     if rc != 0:
         raise ValueError("build needs 1 <= k < n")
     return M, tdo[0].item(), gains
+
+
+def dist_l2(X: np.ndarray) -> np.ndarray:
+    """Euclidean dissimilarities by definition, fp64 (oracle_dist_l2)."""
+    X = np.ascontiguousarray(X, dtype=np.float32)
+    n, d = X.shape
+    D = np.empty((n, n), np.float64)
+    _load().oracle_dist_l2(_ptr(X), ctypes.c_int32(n), ctypes.c_int32(d), _ptr(D))
+    return D
+
+
+def dist_l1(Xq: np.ndarray) -> np.ndarray:
+    """Manhattan dissimilarities of integer coordinates by definition, int64 (oracle_dist_l1)."""
+    Xq = np.ascontiguousarray(Xq, dtype=np.int32)
+    n, d = Xq.shape
+    D = np.empty((n, n), np.int64)
+    _load().oracle_dist_l1(_ptr(Xq), ctypes.c_int32(n), ctypes.c_int32(d), _ptr(D))
+    return D

@@ -1,0 +1,326 @@
+// km_dist.cuh -- dissimilarity-matrix materialisation (
+// PAPER P:272-278 "a dissimilarity matrix D ... is computed in advance",
+// computing it dominates FasterPAM's time on MNIST).
+//
+// Writes the column slab [c0, c1) of all n rows of D, row stride ld, i.e.
+// directly in the layout a (possibly sharded) kmedoids handle borrows.
+//
+//   L2 (float32): d(x_i, x_j) = sqrt(max(0, |x_i|^2 + |x_j|^2 - 2 <x_i, x_j>)).
+//     The inner products are a contraction and run on the 5th-generation
+//     tensor cores: tcgen05.mma kind::tf32, M = 128 rows x N = 128 columns
+//     per tile, accumulator in TMEM, operands in shared memory (K-major,
+//     no-swizzle core matrices).  f32 accuracy from tf32 inputs by the
+//     3-term split x = hi + lo (hi = tf32(x), lo = tf32(x - hi)):
+//     <x,y> ~ hi.hi + hi.lo + lo.hi, fp32 accumulation (the dropped lo.lo
+//     term is < 2^-22 |x||y|).  Norms are exact fp64 sums rounded to f32.
+//     The diagonal is set to 0 exactly (d(x, x) = 0).
+//   L1 (uint32): d(x_i, x_j) = sum_t |x_it - x_jt| on integer coordinates
+//     (the C1/C5 "L1 of round(100 x)" dissimilarities), exact, CUDA cores
+//     (an absolute-difference sum is not a contraction).
+#pragma once
+#include "km_kernels.cuh"
+
+namespace km {
+
+constexpr int DT_M = 128;       // rows per tile (TMEM lanes)
+constexpr int DT_N = 128;       // columns per tile (TMEM columns, fp32)
+
+__device__ __forceinline__ uint32_t dt_smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+
+__device__ __forceinline__ float dt_tf32(float x) {
+    uint32_t r;
+    asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(x));
+    return __uint_as_float(r);
+}
+
+// Shared-memory matrix descriptor, K-major, no swizzle (canonical layout
+// ((8, m), (T, 2)) : ((1T, SBO), (1, LBO)) in 16-byte units): core matrices of
+// 8 rows x 16 bytes; LBO = byte distance between the two K-adjacent core
+// matrices of one instruction, SBO = byte distance between 8-row groups.
+__device__ __forceinline__ uint64_t dt_desc(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
+    uint64_t d = 0;
+    d |= (uint64_t)((saddr >> 4) & 0x3FFF);
+    d |= (uint64_t)((lbo >> 4) & 0x3FFF) << 16;
+    d |= (uint64_t)((sbo >> 4) & 0x3FFF) << 32;
+    d |= (uint64_t)1 << 46;          // descriptor version (sm_100)
+    // base offset 0, LBO mode 0, layout type 0 = SWIZZLE_NONE (bits 61-63)
+    return d;
+}
+
+// Instruction descriptor: D f32, A/B tf32, both K-major, M x N.
+__host__ __device__ constexpr uint32_t dt_idesc(int M, int N) {
+    return (1u << 4)                       // c_format = F32
+         | (2u << 7)                       // a_format = TF32
+         | (2u << 10)                      // b_format = TF32
+         | ((uint32_t)(N >> 3) << 17)      // n_dim
+         | ((uint32_t)(M >> 4) << 24);     // m_dim
+}
+
+__device__ __forceinline__ void dt_mma_tf32(uint32_t tmem_d, uint64_t da, uint64_t db, uint32_t idesc, uint32_t acc) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t}\n"
+        :: "r"(tmem_d), "l"(da), "l"(db), "r"(idesc), "r"(acc));
+}
+
+// Element (r, k) of a K-major no-swizzle tile with kc = Kpad/4 chunks of 4
+// tf32 per 8-row group: core matrix (r/8, k/4), 8 rows x 4 floats each.
+__device__ __forceinline__ int dt_off(int r, int k, int kc) {
+    return (((r >> 3) * kc + (k >> 2)) << 5) + ((r & 7) << 2) + (k & 3);
+}
+
+// fp64 squared norms rounded to f32: nrm[i] = |x_i|^2
+__global__ void k_dist_norms(const float* __restrict__ X, int n, int d, float* __restrict__ nrm) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    double s = 0;
+    for (int t = 0; t < d; ++t) { const double v = X[(int64_t)i * d + t]; s += v * v; }
+    nrm[i] = (float)s;
+}
+
+// Operand pre-pass: rows [r0, r1) of X as 128-row tiles in exactly the
+// shared-memory image the MMA reads -- [hi core matrices (128 x dpad)][lo
+// core matrices][128 squared norms] -- so that one TMA bulk copy moves a
+// whole tile.  Rows beyond r1 and columns beyond d are zero.
+__host__ __device__ inline int64_t dt_tile_floats(int dpad) { return 2LL * DT_M * dpad + DT_M; }
+
+__global__ void k_dist_pack(const float* __restrict__ X, const float* __restrict__ nrm, int d, int dpad, int64_t r0,
+                            int64_t r1, float* __restrict__ out) {
+    const int kc = dpad / 4;
+    const int64_t tile = blockIdx.x;
+    float* o = out + tile * dt_tile_floats(dpad);
+    for (int idx = threadIdx.x; idx < DT_M * dpad; idx += blockDim.x) {
+        const int r = idx / dpad, k = idx - r * dpad;
+        const int64_t j = r0 + tile * DT_M + r;
+        const float v = (j < r1 && k < d) ? X[j * d + k] : 0.f;
+        const float hi = dt_tf32(v);
+        o[dt_off(r, k, kc)] = hi;
+        o[DT_M * dpad + dt_off(r, k, kc)] = dt_tf32(v - hi);
+    }
+    for (int r = threadIdx.x; r < DT_M; r += blockDim.x) {
+        const int64_t j = r0 + tile * DT_M + r;
+        o[2 * DT_M * dpad + r] = j < r1 ? nrm[j] : 0.f;
+    }
+}
+
+// Persistent CTAs (one per SM, 8 warps) over work items (128-row tile,
+// range of 128-column tiles).  Per column tile: one thread issues
+// 3 * dpad/8 tcgen05.mma (hi.hi, hi.lo, lo.hi) into a TMEM accumulator
+// (128 lanes x 128 fp32 columns) and commits to an mbarrier; as soon as the
+// MMAs are done the next B tile is fetched by a TMA bulk copy (it lands
+// while the epilogue runs); the 8 warps read the accumulator (warp w: lanes
+// 32(w%4).., columns 64(w/4)..), form the distances and stage the tile in
+// shared memory; one thread writes it with 128 TMA bulk copies (a 512-byte
+// row segment each) that overlap the next tile (two staging buffers when
+// they fit).  Requires d <= 64 (dpad = roundup(d, 8)).
+constexpr int DT_WARPS = 8;
+constexpr int DT_THREADS = DT_WARPS * 32;
+constexpr int DT_SROW = DT_N + 4;                   // staging row stride (floats): 528 B, 4-way bank spread
+
+__host__ __device__ inline size_t dt_smem_bytes(int dpad, int nstage) {
+    return (size_t)2 * dt_tile_floats(dpad) * sizeof(float) + (size_t)nstage * DT_M * DT_SROW * sizeof(float);
+}
+
+__device__ __forceinline__ void dt_bulk_load(void* sdst, const void* gsrc, uint32_t bytes, uint64_t* bar) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" :: "r"(dt_smem_u32(bar)), "r"(bytes) : "memory");
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+                 :: "r"(dt_smem_u32(sdst)), "l"(gsrc), "r"(bytes), "r"(dt_smem_u32(bar)) : "memory");
+}
+
+__device__ __forceinline__ void dt_wait(uint64_t* bar, uint32_t phase) {
+    uint32_t done = 0;
+    while (!done) {
+        asm volatile("{\n\t.reg .pred p;\n\t"
+                     "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+                     "selp.u32 %0, 1, 0, p;\n\t}\n"
+                     : "=r"(done) : "r"(dt_smem_u32(bar)), "r"(phase) : "memory");
+    }
+}
+
+__global__ void __launch_bounds__(DT_THREADS, 1)
+k_dist_l2_tc(const float* __restrict__ PA, const float* __restrict__ PB, int n, int dpad, int nstage, int nsplit,
+             float* __restrict__ D, int64_t ld, int64_t c0, int64_t c1) {
+    extern __shared__ __align__(1024) unsigned char dsm[];
+    const int64_t TF = dt_tile_floats(dpad);
+    const uint32_t tbytes = (uint32_t)(TF * sizeof(float));
+    float* sA = reinterpret_cast<float*>(dsm);
+    float* sB = sA + TF;
+    float* stage0 = sB + TF;                            // nstage x [128][DT_SROW]
+    const float* sny = sB + 2 * DT_M * dpad;            // |x_j|^2 of the B tile
+    __shared__ __align__(8) uint64_t bar_mma, bar_a, bar_b;
+    __shared__ uint32_t tmem_base_s;
+    __shared__ float sny_keep[DT_N];
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const int q = warp & 3, half = warp >> 2;           // TMEM lane quarter, column half
+
+    if (warp == 0) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;"
+                     :: "r"(dt_smem_u32(&tmem_base_s)), "n"(DT_N));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
+    if (tid == 0) {
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" :: "r"(dt_smem_u32(&bar_mma)));
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" :: "r"(dt_smem_u32(&bar_a)));
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" :: "r"(dt_smem_u32(&bar_b)));
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;");
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;");
+    const uint32_t tmem = tmem_base_s;
+    const uint32_t idesc = dt_idesc(DT_M, DT_N);
+    const uint32_t lbo = 128, sbo = (uint32_t)(dpad / 4) * 128;
+    const int64_t ntile_c = (c1 - c0 + DT_N - 1) / DT_N;
+    const int64_t nm = (n + DT_M - 1) / DT_M;
+    const int64_t items = nm * nsplit;
+    uint32_t ph_mma = 0, ph_a = 0, ph_b = 0;
+    int64_t tcount = 0;                                  // tiles done by this CTA (staging rotation)
+
+    for (int64_t item = blockIdx.x; item < items; item += gridDim.x) {
+        const int64_t mt = item / nsplit;
+        const int m0 = (int)(mt * DT_M);
+        const int sp = (int)(item % nsplit);
+        const int64_t t0 = ntile_c * sp / nsplit, t1 = ntile_c * (sp + 1) / nsplit;
+        if (t0 >= t1) continue;
+        if (tid == 0) {                                  // A tile and the first B tile of the item
+            dt_bulk_load(sA, PA + mt * TF, tbytes, &bar_a);
+            dt_bulk_load(sB, PB + t0 * TF, tbytes, &bar_b);
+        }
+        dt_wait(&bar_a, ph_a); ph_a ^= 1;
+        const int rowq = m0 + q * 32 + lane;             // this thread's row (TMEM lane q*32+lane)
+        const float nx = sA[2 * DT_M * dpad + q * 32 + lane];
+        for (int64_t tc = t0; tc < t1; ++tc, ++tcount) {
+            const int64_t n0 = c0 + tc * DT_N;
+            if (tid == 0) {
+                dt_wait(&bar_b, ph_b);
+                asm volatile("tcgen05.fence::after_thread_sync;");
+                const uint32_t sa_hi = dt_smem_u32(sA), sa_lo = sa_hi + DT_M * dpad * 4;
+                const uint32_t sb_hi = dt_smem_u32(sB), sb_lo = sb_hi + DT_N * dpad * 4;
+                for (int s = 0; s < dpad / 8; ++s) {
+                    const uint32_t ko = (uint32_t)s * 2 * 128;   // two 16-byte K chunks per instruction
+                    dt_mma_tf32(tmem, dt_desc(sa_hi + ko, lbo, sbo), dt_desc(sb_hi + ko, lbo, sbo), idesc, s > 0);
+                    dt_mma_tf32(tmem, dt_desc(sa_hi + ko, lbo, sbo), dt_desc(sb_lo + ko, lbo, sbo), idesc, 1);
+                    dt_mma_tf32(tmem, dt_desc(sa_lo + ko, lbo, sbo), dt_desc(sb_hi + ko, lbo, sbo), idesc, 1);
+                }
+                asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];"
+                             :: "r"(dt_smem_u32(&bar_mma)) : "memory");
+            }
+            ph_b ^= 1;
+            dt_wait(&bar_mma, ph_mma); ph_mma ^= 1;      // accumulator ready, B consumed
+            asm volatile("tcgen05.fence::after_thread_sync;");
+            // the B norms are needed by the epilogue: copy them out before B is refilled
+            if (tid < DT_N) sny_keep[tid] = sny[tid];
+            __syncthreads();
+            if (tid == 0 && tc + 1 < t1) dt_bulk_load(sB, PB + (tc + 1) * TF, tbytes, &bar_b);   // lands during the epilogue
+            if (warp == 0) {
+                // the staging buffer of this tile was last read by the bulk
+                // stores of tile tcount - nstage (issued by the lanes of warp 0)
+                if (nstage == 2) asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+                else asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+            }
+            __syncthreads();
+            float* stg = stage0 + (size_t)(tcount % nstage) * DT_M * DT_SROW;
+#pragma unroll 1
+            for (int cc = 0; cc < 2; ++cc) {
+                const int col0 = half * 64 + cc * 32;
+                uint32_t v[32];
+                const uint32_t taddr = tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)col0;
+                asm volatile(
+                    "tcgen05.ld.sync.aligned.32x32b.x32.b32 "
+                    "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+                    "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+                    : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]),
+                      "=r"(v[7]), "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]),
+                      "=r"(v[14]), "=r"(v[15]), "=r"(v[16]), "=r"(v[17]), "=r"(v[18]), "=r"(v[19]), "=r"(v[20]),
+                      "=r"(v[21]), "=r"(v[22]), "=r"(v[23]), "=r"(v[24]), "=r"(v[25]), "=r"(v[26]), "=r"(v[27]),
+                      "=r"(v[28]), "=r"(v[29]), "=r"(v[30]), "=r"(v[31])
+                    : "r"(taddr));
+                asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+                float* srow = stg + (size_t)(q * 32 + lane) * DT_SROW + col0;
+#pragma unroll
+                for (int j = 0; j < 32; j += 4) {
+                    float o4[4];
+#pragma unroll
+                    for (int u = 0; u < 4; ++u) {
+                        const float dot = __uint_as_float(v[j + u]);
+                        const float d2 = fmaf(-2.f, dot, nx + sny_keep[col0 + j + u]);
+                        o4[u] = (n0 + col0 + j + u == rowq) ? 0.f : sqrtf(fmaxf(d2, 0.f));
+                    }
+                    *reinterpret_cast<float4*>(srow + j) = make_float4(o4[0], o4[1], o4[2], o4[3]);
+                }
+            }
+            // staging -> global: 128 row segments by bulk copies (async proxy)
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            asm volatile("tcgen05.fence::before_thread_sync;");
+            __syncthreads();                             // also: TMEM free for the next MMA
+            const int wcols = (int)((c1 - n0) < (int64_t)DT_N ? (c1 - n0) : (int64_t)DT_N);
+            if ((wcols & 3) == 0) {
+                if (warp == 0) {                         // 4 row copies per lane of warp 0
+                    const uint32_t bytes = (uint32_t)wcols * 4;
+                    for (int r = lane; r < DT_M && m0 + r < n; r += 32) {
+                        float* g = D + (int64_t)(m0 + r) * ld + (n0 - c0);
+                        asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;"
+                                     :: "l"(g), "r"(dt_smem_u32(stg + (size_t)r * DT_SROW)), "r"(bytes) : "memory");
+                    }
+                    asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+                }
+            } else {                                     // ragged last tile: plain stores
+                for (int idx = tid; idx < DT_M * wcols; idx += DT_THREADS) {
+                    const int r = idx / wcols, cidx = idx - r * wcols;
+                    if (m0 + r < n) D[(int64_t)(m0 + r) * ld + (n0 - c0) + cidx] = stg[(size_t)r * DT_SROW + cidx];
+                }
+                __syncthreads();
+            }
+        }
+    }
+    if (warp == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+    asm volatile("tcgen05.fence::after_thread_sync;");
+    __syncthreads();
+    if (warp == 0)
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" :: "r"(tmem), "n"(DT_N));
+}
+
+// L1 on integer coordinates: 64 x 64 output tile per block, 256 threads
+// (each 4 x 4 outputs), coordinates staged through shared memory.
+__global__ void __launch_bounds__(256)
+k_dist_l1_u32(const int32_t* __restrict__ Xq, int n, int d, uint32_t* __restrict__ D, int64_t ld, int64_t c0,
+              int64_t c1) {
+    constexpr int TB = 64, KB = 32;
+    __shared__ int32_t sa[KB][TB + 1], sb[KB][TB + 1];
+    const int i0 = blockIdx.y * TB;
+    const int64_t j0 = c0 + (int64_t)blockIdx.x * TB;
+    const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
+    uint32_t acc[4][4] = {};
+    for (int k0 = 0; k0 < d; k0 += KB) {
+        for (int idx = threadIdx.x; idx < TB * KB; idx += 256) {
+            const int r = idx / KB, k = idx % KB;
+            sa[k][r] = (i0 + r < n && k0 + k < d) ? Xq[(int64_t)(i0 + r) * d + k0 + k] : 0;
+            sb[k][r] = (j0 + r < c1 && k0 + k < d) ? Xq[(j0 + r) * d + k0 + k] : 0;
+        }
+        __syncthreads();
+        const int kn = min(KB, d - k0);
+        for (int k = 0; k < kn; ++k) {
+            int32_t a[4], b[4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) { a[u] = sa[k][ty * 4 + u]; b[u] = sb[k][tx * 4 + u]; }
+#pragma unroll
+            for (int u = 0; u < 4; ++u)
+#pragma unroll
+                for (int v = 0; v < 4; ++v) acc[u][v] += (uint32_t)abs(a[u] - b[v]);
+        }
+        __syncthreads();
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+        const int i = i0 + ty * 4 + u;
+        if (i >= n) continue;
+#pragma unroll
+        for (int v = 0; v < 4; ++v) {
+            const int64_t j = j0 + tx * 4 + v;
+            if (j < c1) D[(int64_t)i * ld + (j - c0)] = (j == i) ? 0u : acc[u][v];
+        }
+    }
+}
+
+}  // namespace km

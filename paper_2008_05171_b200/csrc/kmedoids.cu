@@ -19,6 +19,7 @@
 #include "km_kernels.cuh"
 #include "km_fasterpam.cuh"
 #include "km_post.cuh"
+#include "km_dist.cuh"
 
 namespace {
 
@@ -1587,6 +1588,62 @@ km_status kmedoids_stream_time(km_handle* h, double* ms_out, int64_t* launches_o
     if (launches_out) *launches_out = h->impl->prof_launches;
     if (reset) { h->impl->prof_ms = 0.0; h->impl->prof_launches = 0; }
     return KM_OK;
+}
+
+km_status kmedoids_dissimilarity(const void* X, km_metric metric, int64_t n, int32_t d, void* D, int64_t ld,
+                                 int64_t col_begin, int64_t col_end, void* cuda_stream) {
+    g_err.clear();
+    if (!X || !D) return fail(KM_EINVAL, "X and D must be device pointers");
+    if (n < 1 || n >= (int64_t)INT32_MAX) return fail(KM_EINVAL, "n=%lld out of range", (long long)n);
+    if (d < 1) return fail(KM_EINVAL, "d=%d must be >= 1", d);
+    if (col_begin < 0 || col_end > n || col_begin >= col_end)
+        return fail(KM_EINVAL, "column range [%lld,%lld) invalid for n=%lld", (long long)col_begin, (long long)col_end,
+                    (long long)n);
+    if (ld < col_end - col_begin) return fail(KM_EINVAL, "ld=%lld smaller than the slab width", (long long)ld);
+    cudaStream_t st = (cudaStream_t)cuda_stream;
+    if (metric == KM_METRIC_L2_F32) {
+        if (d > 64) return fail(KM_EINVAL, "L2 on tensor cores supports d <= 64 (d=%d)", d);
+        if (ld % 4 != 0 || ((uintptr_t)D) % 16 != 0) return fail(KM_EINVAL, "D must be 16-byte aligned, ld % 4 == 0");
+        const int dpad = (d + 7) / 8 * 8;
+        const int64_t nm = cdiv(n, km::DT_M), ntc = cdiv(col_end - col_begin, km::DT_N);
+        const int64_t TF = km::dt_tile_floats(dpad);
+        const bool same = (col_begin == 0);
+        const size_t nrm_floats = (size_t)cdiv(n, 64) * 64;          // keeps the packed tiles 256-byte aligned
+        const size_t scratch = nrm_floats + (size_t)nm * TF + (same ? 0 : (size_t)ntc * TF);
+        float* nrm = nullptr;
+        cudaError_t e = cudaMallocAsync((void**)&nrm, scratch * sizeof(float), st);
+        if (e != cudaSuccess) return fail(KM_ENOMEM, "dissimilarity scratch: %s", cudaGetErrorString(e));
+        float* PA = nrm + nrm_floats;
+        float* PB = same ? PA : PA + nm * TF;
+        km::k_dist_norms<<<(unsigned)cdiv(n, 256), 256, 0, st>>>((const float*)X, (int)n, d, nrm);
+        km::k_dist_pack<<<(unsigned)nm, 256, 0, st>>>((const float*)X, nrm, d, dpad, 0, n, PA);
+        if (!same) km::k_dist_pack<<<(unsigned)ntc, 256, 0, st>>>((const float*)X, nrm, d, dpad, col_begin, col_end, PB);
+        int dev = 0, nsm = 0, smax = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+        cudaDeviceGetAttribute(&smax, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+        const int nstage = km::dt_smem_bytes(dpad, 2) + 1024 <= (size_t)smax ? 2 : 1;
+        const size_t smem = km::dt_smem_bytes(dpad, nstage);
+        e = cudaFuncSetAttribute(km::k_dist_l2_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if (e != cudaSuccess) { cudaFreeAsync(nrm, st); return fail(KM_ECUDA, "smem attribute: %s", cudaGetErrorString(e)); }
+        // work items (row tile x column range): at least 8 per SM for balance
+        const int nsplit = (int)std::max<int64_t>(1, std::min<int64_t>(ntc, cdiv((int64_t)nsm * 8, nm)));
+        const int grid = (int)std::min<int64_t>(nsm, nm * nsplit);
+        km::k_dist_l2_tc<<<grid, km::DT_THREADS, smem, st>>>(PA, PB, (int)n, dpad, nstage, nsplit, (float*)D, ld,
+                                                              col_begin, col_end);
+        e = cudaGetLastError();
+        cudaFreeAsync(nrm, st);
+        if (e != cudaSuccess) return fail(KM_ECUDA, "k_dist_l2_tc: %s", cudaGetErrorString(e));
+        return KM_OK;
+    }
+    if (metric == KM_METRIC_L1_U32) {
+        dim3 g((unsigned)cdiv(col_end - col_begin, 64), (unsigned)cdiv(n, 64));
+        km::k_dist_l1_u32<<<g, 256, 0, st>>>((const int32_t*)X, (int)n, d, (uint32_t*)D, ld, col_begin, col_end);
+        cudaError_t e = cudaGetLastError();
+        if (e != cudaSuccess) return fail(KM_ECUDA, "k_dist_l1_u32: %s", cudaGetErrorString(e));
+        return KM_OK;
+    }
+    return fail(KM_EINVAL, "unknown metric %d", (int)metric);
 }
 
 km_status kmedoids_launch_count(km_handle* h, int64_t* count_out) {

@@ -87,6 +87,7 @@ def load_library() -> ctypes.CDLL:
         "kmedoids_build_eval": [vp, i32],
         "kmedoids_build_select": [vp, vp, vp, vp, vp],
         "kmedoids_build_apply": [vp, i32],
+        "kmedoids_dissimilarity": [vp, ctypes.c_int, i64, i32, vp, i64, i64, i64, vp],
     }
     for name, args in sig.items():
         f = getattr(lib, name)
@@ -367,3 +368,31 @@ def pinned_empty(shape, dtype):
     a = t.numpy()
     a = a.view(np.uint32) if np.dtype(dtype) == np.uint32 else a
     return a, t
+
+
+KM_METRIC_L2_F32, KM_METRIC_L1_U32 = 0, 1
+
+
+def kmedoids_dissimilarity(X, metric="l2", D=None, col_begin=0, col_end=None, stream=None):
+    """Materialise the column slab [col_begin, col_end) of the dissimilarity
+    matrix of the points X (torch CUDA tensor, n x d) into D (n x ld; allocated
+    if None): "l2" float32 X -> float32 Euclidean on the tensor cores, "l1"
+    int32 X -> uint32 (int32 storage) Manhattan.  Returns D."""
+    import torch
+    lib = load_library()
+    if not X.is_cuda or X.dim() != 2:
+        raise ValueError("X must be a 2-D CUDA tensor")
+    X = X.contiguous()
+    n, d = X.shape
+    col_end = n if col_end is None else int(col_end)
+    code = {"l2": KM_METRIC_L2_F32, "l1": KM_METRIC_L1_U32}[metric]
+    want = torch.float32 if code == KM_METRIC_L2_F32 else torch.int32
+    if X.dtype != want:
+        raise TypeError(f"metric {metric} needs X of dtype {want}")
+    if D is None:
+        w = col_end - col_begin
+        D = torch.empty((n, (w + 3) // 4 * 4), dtype=want, device=X.device)
+    st = stream if stream is not None else torch.cuda.current_stream(X.device)
+    _check(lib.kmedoids_dissimilarity(ctypes.c_void_p(X.data_ptr()), code, n, d, ctypes.c_void_p(D.data_ptr()),
+                                      int(D.stride(0)), int(col_begin), int(col_end), ctypes.c_void_p(st.cuda_stream)))
+    return D

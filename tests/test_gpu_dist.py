@@ -1,0 +1,103 @@
+"""NEXT-2: dissimilarity materialisation (kmedoids_dissimilarity) vs the
+oracle's plain definitions.  L1 on integer coordinates is exact; L2 runs on
+the tensor cores (tcgen05 kind::tf32 with a hi/lo split) and is checked on
+squared distances against the bound its arithmetic gives (header of
+csrc/km_dist.cuh): |d2_gpu - d2| <= (6d + 16) 2^-24 (|x|^2 + |y|^2) plus the
+f32 output rounding."""
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+import kmsynth  # noqa: E402
+import oracle  # noqa: E402
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _cuda():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    torch.cuda.set_device(0)
+
+
+def l2_bound(X, d):
+    nrm = (X.astype(np.float64) ** 2).sum(axis=1)
+    return (6 * d + 16) * 2.0 ** -24 * (nrm[:, None] + nrm[None, :])
+
+
+@pytest.mark.parametrize("n,d,c0,c1", [(1, 1, 0, 1), (7, 2, 0, 7), (129, 10, 0, 129), (300, 27, 0, 300),
+                                       (1000, 32, 0, 1000), (513, 64, 0, 513), (700, 33, 128, 515),
+                                       (260, 5, 256, 260)])
+def test_l2_tensor_core_matches_definition(n, d, c0, c1):
+    from paper_2008_05171_b200 import kmedoids_dissimilarity
+    rng = np.random.default_rng(n * 100 + d)
+    X = (rng.normal(size=(n, d)) * rng.choice([0.1, 1.0, 8.0]) + rng.normal(size=d) * 3).astype(np.float32)
+    Dg = kmedoids_dissimilarity(torch.from_numpy(X).cuda(), "l2", col_begin=c0, col_end=c1)
+    Dg = Dg[:, :c1 - c0].double().cpu().numpy()
+    Dx = oracle.dist_l2(X)[:, c0:c1]
+    tol = l2_bound(X, d)[:, c0:c1] + 2.0 ** -22 * Dx ** 2
+    err = np.abs(Dg ** 2 - Dx ** 2)
+    assert (err <= tol).all(), (err.max(), np.unravel_index(np.argmax(err - tol), err.shape))
+    for i in range(max(c0, 0), min(c1, n)):
+        assert Dg[i, i - c0] == 0.0
+    assert (Dg >= 0).all()
+
+
+@pytest.mark.parametrize("n,d,c0,c1", [(1, 1, 0, 1), (65, 2, 0, 65), (300, 64, 0, 300), (257, 3, 64, 200)])
+def test_l1_exact(n, d, c0, c1):
+    from paper_2008_05171_b200 import kmedoids_dissimilarity
+    rng = np.random.default_rng(7 + n)
+    Xq = rng.integers(-20000, 20000, size=(n, d)).astype(np.int32)
+    Dg = kmedoids_dissimilarity(torch.from_numpy(Xq).cuda(), "l1", col_begin=c0, col_end=c1)
+    Dg = Dg[:, :c1 - c0].cpu().numpy().view(np.uint32).astype(np.int64)
+    assert (Dg == oracle.dist_l1(Xq)[:, c0:c1]).all()
+
+
+def test_l2_config_points_close_to_generator_and_swap_runs():
+    """C4 recipe points (n=2000): the tensor-core D is within the bound of the
+    definition; FastPAM1 on it (through the C ABI) equals the oracle's
+    FastPAM1 on the same (downloaded) D."""
+    from paper_2008_05171_b200 import KMedoids, kmedoids_dissimilarity
+    cfg = kmsynth.CONFIGS[4]
+    n, k = 2000, 20
+    X = kmsynth.make_points(cfg, n=n).astype(np.float32)
+    Dt = kmedoids_dissimilarity(torch.from_numpy(X).cuda(), "l2")
+    D = Dt[:, :n].cpu().numpy()
+    Dx = oracle.dist_l2(X)
+    assert (np.abs(D.astype(np.float64) ** 2 - Dx ** 2) <= l2_bound(X, X.shape[1]) + 2.0 ** -22 * Dx ** 2).all()
+    M0 = kmsynth.random_medoids(cfg, k=k, n=n)
+    km = KMedoids(Dt, n, k)
+    km.set_medoids(M0)
+    r = km.run(use_build=False)
+    ref = oracle.swap_run(np.ascontiguousarray(D), M0, oracle.FASTPAM1)
+    assert r.td == pytest.approx(ref.td, rel=1e-9)
+    assert r.medoids.tolist() == ref.medoids.tolist()
+
+
+def test_l1_config_points_exact_pipeline():
+    """C5 recipe points quantised x100 (n=1500): the GPU L1 matrix equals the
+    oracle's; FastPAM1 on it is bit-exact to the oracle."""
+    from paper_2008_05171_b200 import KMedoids, kmedoids_dissimilarity
+    cfg = kmsynth.CONFIGS[5]
+    n, k = 1500, 12
+    Xq = np.ascontiguousarray(kmsynth.make_points(cfg, n=n), dtype=np.int32)   # already x100-quantised
+    Dt = kmedoids_dissimilarity(torch.from_numpy(Xq).cuda(), "l1")
+    D = Dt[:, :n].cpu().numpy().view(np.uint32)
+    assert (D.astype(np.int64) == oracle.dist_l1(Xq)).all()
+    M0 = kmsynth.random_medoids(cfg, k=k, n=n)
+    km = KMedoids(Dt, n, k)
+    km.set_medoids(M0)
+    r = km.run(use_build=False)
+    ref = oracle.swap_run(np.ascontiguousarray(D), M0, oracle.FASTPAM1)
+    assert r.medoids.tolist() == ref.medoids.tolist() and r.td == ref.td
+    assert r.assignment.tolist() == ref.assignment.tolist()
+
+
+def test_dissimilarity_argument_errors():
+    from paper_2008_05171_b200 import KMError, kmedoids_dissimilarity
+    X = torch.zeros((10, 65), dtype=torch.float32, device="cuda")
+    with pytest.raises(KMError):
+        kmedoids_dissimilarity(X, "l2")                   # d > 64 on the tensor-core path
+    with pytest.raises(KMError):
+        kmedoids_dissimilarity(X[:, :4].contiguous(), "l2", col_begin=5, col_end=3)

@@ -444,3 +444,28 @@ def test_fasterpam_fig1_reaches_the_optimum():
     best = min(bf_td(D, list(S)) for S in itertools.combinations(range(len(g["points"])), 2))
     assert best == g["losses"][-1]
     assert r.td == best
+
+
+# ---------- dissimilarity matrix from points (NEXT-2) ----------
+
+def test_dist_oracle_closed_forms_and_library():
+    """oracle.dist_l2 / dist_l1 against closed forms (3-4-5, unit square) and
+    scipy's cdist (a library routine of the same definitions), plus the metric
+    axioms: zero diagonal, symmetry, triangle inequality."""
+    from scipy.spatial.distance import cdist
+    X = np.array([[0, 0], [3, 4], [0, 1], [1, 0]], np.float32)
+    D = oracle.dist_l2(X)
+    assert D[0, 1] == 5.0 and D[2, 3] == np.sqrt(2.0) and D[1, 2] == np.sqrt(9 + 9)
+    Xq = np.array([[0, 0], [3, -4], [-1, 2]], np.int32)
+    assert oracle.dist_l1(Xq).tolist() == [[0, 7, 3], [7, 0, 10], [3, 10, 0]]
+    rng = np.random.default_rng(17)
+    for n, d in [(1, 3), (40, 1), (57, 13), (80, 64)]:
+        X = rng.normal(size=(n, d)).astype(np.float32)
+        D = oracle.dist_l2(X)
+        assert np.allclose(D, cdist(X.astype(np.float64), X.astype(np.float64)), rtol=1e-12, atol=1e-12)
+        assert (np.diag(D) == 0).all() and (D == D.T).all()
+        if n >= 3:
+            i, j, l = rng.integers(0, n, size=(3, 200))
+            assert (D[i, j] <= D[i, l] + D[l, j] + 1e-12).all()
+        Xq = rng.integers(-5000, 5000, size=(n, d)).astype(np.int32)
+        assert (oracle.dist_l1(Xq) == cdist(Xq, Xq, "cityblock").astype(np.int64)).all()
