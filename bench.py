@@ -319,6 +319,36 @@ def run_ours(args):
                "speedup_vs_fastpam1": s1 / sf,
                "start": "the initial medoids of the timed run (after " + cfg.init + ")"}
 
+    # NEXT-2: the dissimilarity matrix of the config materialised by the product
+    # (kmedoids_dissimilarity: tensor-core L2 / exact integer L1), written into
+    # a second buffer of the same shape, CUDA events on the current stream.
+    dis = None
+    if not args.no_dissimilarity:
+        from paper_2008_05171_b200 import kmedoids_dissimilarity
+        metric = "l2" if cfg.metric == kmsynth.L2_F32 else "l1"
+        Xt = torch.from_numpy(np.ascontiguousarray(X, dtype=np.float32 if metric == "l2" else np.int32)).cuda()
+        D2 = torch.empty_like(Dt)
+        kmedoids_dissimilarity(Xt, metric, D=D2)
+        torch.cuda.synchronize()
+        d0, d1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        reps = 3
+        d0.record(stream)
+        for _ in range(reps):
+            kmedoids_dissimilarity(Xt, metric, D=D2)
+        d1.record(stream)
+        torch.cuda.synchronize()
+        dms = d0.elapsed_time(d1) / reps
+        wb = n * D2.stride(0) * 4
+        dpad = (Xt.shape[1] + 7) // 8 * 8
+        dis = {"metric": metric, "engine": "tcgen05 kind::tf32 (hi/lo split)" if metric == "l2" else "CUDA cores",
+               "ms": dms, "bytes_written": wb, "write_GBps": wb / (dms / 1e3) / 1e9,
+               "frac_of_hbm_peak": wb / (dms / 1e3) / 1e9 / peak,
+               "tensor_TFLOPs": (3 * 2 * n * n * dpad / (dms / 1e3) / 1e12) if metric == "l2" else None,
+               "max_abs_diff_vs_generator": float((D2[:, :n].double() - Dt[:, :n].double()).abs().max().item())
+               if metric == "l2" else int((D2[:, :n] != Dt[:, :n]).sum().item())}
+        del D2, Xt
+        torch.cuda.empty_cache()
+
     # e2e: the public host-buffer call kmedoids_run_host (H2D of D, init, SWAP to
     # convergence, D2H of medoids/assignment/TD) -- one whole job per e2e step.
     e2e = None
@@ -366,6 +396,7 @@ def run_ours(args):
         "e2e": e2e,
         "cpu_baseline": cpu,
         "fasterpam": fpm,
+        "dissimilarity": dis,
     }
     print(json.dumps(line), flush=True)
 
@@ -504,6 +535,7 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-fasterpam", action="store_true")
+    ap.add_argument("--no-dissimilarity", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
     ap.add_argument("--cpu-candidates", type=int, default=2000)
     ap.add_argument("--ref-candidates", type=int, default=400)
