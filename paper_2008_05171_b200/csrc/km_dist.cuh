@@ -18,6 +18,7 @@
 //     (the C1/C5 "L1 of round(100 x)" dissimilarities), exact, CUDA cores
 //     (an absolute-difference sum is not a contraction).
 #pragma once
+#include <cuda.h>
 #include "km_kernels.cuh"
 
 namespace km {
@@ -279,6 +280,250 @@ k_dist_l2_tc(const float* __restrict__ PA, const float* __restrict__ PB, int n, 
     __syncthreads();
     if (warp == 0)
         asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" :: "r"(tmem), "n"(DT_N));
+}
+
+// ---------------------------------------------------------------------------
+// Warp-specialised L2 kernel (default).  9 warps per CTA, one CTA per SM,
+// persistent over (128-row tile, column range) items:
+//   warp 8, one lane: TMA bulk loads of the packed A / B operand tiles (B in a
+//     2-stage ring), tcgen05.mma (3 * dpad/8 per tile) into one of TWO TMEM
+//     accumulators (2 x 128 columns), tcgen05.commit to the epilogue's
+//     "full" barrier and to the B stage's "empty" barrier;
+//   warps 0-7: epilogue -- tcgen05.ld of 32 lanes x 64 columns each, release
+//     the accumulator, d = sqrt(max(0, |x|^2 + |y|^2 - 2 dot)) (norms from
+//     global memory, L1/L2 resident), 128B-swizzled staging, and four 2-D TMA
+//     tensor stores (32 x 128 boxes) per tile issued by one lane; the
+//     stores run while the next tile is computed.
+// The MMA of tile t+1 overlaps the epilogue of tile t (TMEM double buffer);
+// the B tile of t+2 is fetched as soon as the MMAs of t are done.  Edges
+// (rows beyond n, columns beyond the slab) are clipped by the tensor store.
+// ---------------------------------------------------------------------------
+constexpr int DW_EPI_WARPS = 16;                     // 4 per TMEM lane quarter
+constexpr int DW_CPW = DT_N / (DW_EPI_WARPS / 4);    // accumulator columns per epilogue warp
+constexpr int DW_THREADS = (DW_EPI_WARPS + 1) * 32;
+
+__host__ __device__ inline int64_t dw_tile_floats(int dpad) { return 2LL * DT_M * dpad; }
+__host__ __device__ inline size_t dw_smem_bytes(int dpad, int nstage) {
+    // A + 2 B stages + nstage x 64 KB staging (4 boxes of 128 rows x 128 B), 1 KB alignment slack
+    return (size_t)3 * dw_tile_floats(dpad) * sizeof(float) + (size_t)nstage * 4 * DT_M * 128 + 1024;
+}
+
+// hi / lo core matrices of rows [r0, r1), 128-row tiles (no norms appended)
+__global__ void k_dist_pack2(const float* __restrict__ X, int d, int dpad, int64_t r0, int64_t r1,
+                             float* __restrict__ out) {
+    const int kc = dpad / 4;
+    const int64_t tile = blockIdx.x;
+    float* o = out + tile * dw_tile_floats(dpad);
+    for (int idx = threadIdx.x; idx < DT_M * dpad; idx += blockDim.x) {
+        const int r = idx / dpad, k = idx - r * dpad;
+        const int64_t j = r0 + tile * DT_M + r;
+        const float v = (j < r1 && k < d) ? X[j * d + k] : 0.f;
+        const float hi = dt_tf32(v);
+        o[dt_off(r, k, kc)] = hi;
+        o[DT_M * dpad + dt_off(r, k, kc)] = dt_tf32(v - hi);
+    }
+}
+
+__device__ __forceinline__ void dw_arrive(uint64_t* bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" :: "r"(dt_smem_u32(bar)) : "memory");
+}
+
+__device__ __forceinline__ float dw_sqrt(float x) {
+    float r;
+    asm("sqrt.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+    return r;
+}
+
+__global__ void __launch_bounds__(DW_THREADS, 1)
+k_dist_l2_ws(const __grid_constant__ CUtensorMap tmap, const float* __restrict__ PA, const float* __restrict__ PB,
+             const float* __restrict__ nrm, int n, int dpad, int nsplit, int nstage, int64_t c0, int64_t c1) {
+    extern __shared__ __align__(1024) unsigned char dsm_raw[];
+    // 1 KB alignment for the 128B-swizzled staging boxes
+    unsigned char* dsm = dsm_raw + ((1024 - (dt_smem_u32(dsm_raw) & 1023)) & 1023);
+    const int64_t TF = dw_tile_floats(dpad);
+    const uint32_t tbytes = (uint32_t)(TF * sizeof(float));
+    unsigned char* stage0 = dsm;                         // nstage x 4 boxes x 16 KB (1 KB aligned)
+    float* sA = reinterpret_cast<float*>(dsm + (size_t)nstage * 4 * DT_M * 128);
+    float* sB0 = sA + TF;                                // 2 stages
+    __shared__ __align__(8) uint64_t bar_a, bar_bfull[2], bar_bempty[2], bar_tfull[2], bar_tempty[2];
+    __shared__ uint32_t tmem_base_s;
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+
+    if (warp == DW_EPI_WARPS) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;"
+                     :: "r"(dt_smem_u32(&tmem_base_s)), "n"(2 * DT_N));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
+    if (tid == 0) {
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" :: "r"(dt_smem_u32(&bar_a)));
+        for (int i = 0; i < 2; ++i) {
+            asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" :: "r"(dt_smem_u32(&bar_bfull[i])));
+            asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" :: "r"(dt_smem_u32(&bar_bempty[i])));
+            asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" :: "r"(dt_smem_u32(&bar_tfull[i])));
+            asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" :: "r"(dt_smem_u32(&bar_tempty[i])), "r"(DW_EPI_WARPS));
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;");
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;");
+    const uint32_t tmem = tmem_base_s;
+    const int64_t ntile_c = (c1 - c0 + DT_N - 1) / DT_N;
+    const int64_t nm = (n + DT_M - 1) / DT_M;
+    const int64_t items = nm * nsplit;
+
+    if (warp == DW_EPI_WARPS) {
+        // ====================== TMA + MMA (one lane) ======================
+        if (lane == 0) {
+            const uint32_t idesc = dt_idesc(DT_M, DT_N);
+            const uint32_t lbo = 128, sbo = (uint32_t)(dpad / 4) * 128;
+            uint32_t ph_a = 0, ph_bf[2] = {0, 0}, ph_be[2] = {0, 0}, ph_te[2] = {0, 0};
+            int64_t t = 0;                               // tiles issued by this CTA
+            bool pending[2] = {false, false};            // B stage has an MMA commit not yet waited for
+            for (int64_t item = blockIdx.x; item < items; item += gridDim.x) {
+                const int64_t mt = item / nsplit;
+                const int sp = (int)(item % nsplit);
+                const int64_t t0 = ntile_c * sp / nsplit, t1 = ntile_c * (sp + 1) / nsplit;
+                if (t0 >= t1) continue;
+                // the A tile is rewritten: every MMA issued so far must be complete
+                for (int s = 0; s < 2; ++s)
+                    if (pending[s]) { dt_wait(&bar_bempty[s], ph_be[s]); ph_be[s] ^= 1; pending[s] = false; }
+                dt_bulk_load(sA, PA + mt * TF, tbytes, &bar_a);
+                // the first two B tiles of the item
+                for (int64_t k = 0; k < 2 && t0 + k < t1; ++k) {
+                    const int s = (int)((t + k) & 1);
+                    dt_bulk_load(sB0 + s * TF, PB + (t0 + k) * TF, tbytes, &bar_bfull[s]);
+                }
+                dt_wait(&bar_a, ph_a); ph_a ^= 1;
+                for (int64_t tc = t0; tc < t1; ++tc, ++t) {
+                    const int s = (int)(t & 1);
+                    dt_wait(&bar_bfull[s], ph_bf[s]); ph_bf[s] ^= 1;
+                    if (t >= 2) { dt_wait(&bar_tempty[s], ph_te[s]); ph_te[s] ^= 1; }   // accumulator s drained
+                    asm volatile("tcgen05.fence::after_thread_sync;");
+                    const uint32_t sa_hi = dt_smem_u32(sA), sa_lo = sa_hi + DT_M * dpad * 4;
+                    const uint32_t sb_hi = dt_smem_u32(sB0 + s * TF), sb_lo = sb_hi + DT_N * dpad * 4;
+                    const uint32_t acc = tmem + (uint32_t)(s * DT_N);
+                    for (int kk = 0; kk < dpad / 8; ++kk) {
+                        const uint32_t ko = (uint32_t)kk * 2 * 128;
+                        dt_mma_tf32(acc, dt_desc(sa_hi + ko, lbo, sbo), dt_desc(sb_hi + ko, lbo, sbo), idesc, kk > 0);
+                        dt_mma_tf32(acc, dt_desc(sa_hi + ko, lbo, sbo), dt_desc(sb_lo + ko, lbo, sbo), idesc, 1);
+                        dt_mma_tf32(acc, dt_desc(sa_lo + ko, lbo, sbo), dt_desc(sb_hi + ko, lbo, sbo), idesc, 1);
+                    }
+                    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];"
+                                 :: "r"(dt_smem_u32(&bar_tfull[s])) : "memory");
+                    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];"
+                                 :: "r"(dt_smem_u32(&bar_bempty[s])) : "memory");
+                    pending[s] = true;
+                    // B stage s is refilled with tile tc + 2 once these MMAs are done
+                    if (tc + 2 < t1) {
+                        dt_wait(&bar_bempty[s], ph_be[s]); ph_be[s] ^= 1; pending[s] = false;
+                        dt_bulk_load(sB0 + s * TF, PB + (tc + 2) * TF, tbytes, &bar_bfull[s]);
+                    }
+                }
+            }
+            for (int s = 0; s < 2; ++s)
+                if (pending[s]) { dt_wait(&bar_bempty[s], ph_be[s]); ph_be[s] ^= 1; }
+        }
+    } else {
+        // ====================== epilogue warps 0-7 ======================
+        const int q = warp & 3, part = warp >> 2;       // TMEM lane quarter, column part
+        uint32_t ph_tf[2] = {0, 0};
+        int64_t t = 0;
+        for (int64_t item = blockIdx.x; item < items; item += gridDim.x) {
+            const int64_t mt = item / nsplit;
+            const int m0 = (int)(mt * DT_M);
+            const int sp = (int)(item % nsplit);
+            const int64_t t0 = ntile_c * sp / nsplit, t1 = ntile_c * (sp + 1) / nsplit;
+            const int row = m0 + q * 32 + lane;
+            const float nx = row < n ? nrm[row] : 0.f;
+            for (int64_t tc = t0; tc < t1; ++tc, ++t) {
+                const int s = (int)(t & 1);
+                const int64_t n0 = c0 + tc * DT_N;
+                dt_wait(&bar_tfull[s], ph_tf[s]); ph_tf[s] ^= 1;
+                asm volatile("tcgen05.fence::after_thread_sync;");
+                uint32_t v[DW_CPW];
+#pragma unroll
+                for (int ch = 0; ch < DW_CPW / 32; ++ch) {
+                    const uint32_t taddr = tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(s * DT_N + part * DW_CPW + ch * 32);
+                    uint32_t* w = v + ch * 32;
+                    asm volatile(
+                        "tcgen05.ld.sync.aligned.32x32b.x32.b32 "
+                        "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+                        "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+                        : "=r"(w[0]), "=r"(w[1]), "=r"(w[2]), "=r"(w[3]), "=r"(w[4]), "=r"(w[5]), "=r"(w[6]),
+                          "=r"(w[7]), "=r"(w[8]), "=r"(w[9]), "=r"(w[10]), "=r"(w[11]), "=r"(w[12]), "=r"(w[13]),
+                          "=r"(w[14]), "=r"(w[15]), "=r"(w[16]), "=r"(w[17]), "=r"(w[18]), "=r"(w[19]), "=r"(w[20]),
+                          "=r"(w[21]), "=r"(w[22]), "=r"(w[23]), "=r"(w[24]), "=r"(w[25]), "=r"(w[26]), "=r"(w[27]),
+                          "=r"(w[28]), "=r"(w[29]), "=r"(w[30]), "=r"(w[31])
+                        : "r"(taddr));
+                }
+                asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+                asm volatile("tcgen05.fence::before_thread_sync;");
+                __syncwarp();
+                if (lane == 0) dw_arrive(&bar_tempty[s]);  // accumulator s may be overwritten
+                // distances (norms of the columns: same addresses across the warp -> broadcast)
+                const int64_t cb = n0 + part * DW_CPW;
+                const bool diag = (cb <= (int64_t)m0 + DT_M - 1) && ((int64_t)m0 <= cb + DW_CPW - 1);
+#pragma unroll
+                for (int j = 0; j < DW_CPW; j += 4) {
+                    float4 ny4 = make_float4(0.f, 0.f, 0.f, 0.f);
+                    if (cb + j + 3 < c1 && ((cb + j) & 3) == 0) ny4 = __ldg(reinterpret_cast<const float4*>(nrm + cb + j));
+                    else {
+                        if (cb + j + 3 < c1) ny4.w = nrm[cb + j + 3];
+                        if (cb + j < c1) ny4.x = nrm[cb + j];
+                        if (cb + j + 1 < c1) ny4.y = nrm[cb + j + 1];
+                        if (cb + j + 2 < c1) ny4.z = nrm[cb + j + 2];
+                    }
+                    const float ny[4] = {ny4.x, ny4.y, ny4.z, ny4.w};
+#pragma unroll
+                    for (int u = 0; u < 4; ++u) {
+                        const float d2 = fmaf(-2.f, __uint_as_float(v[j + u]), nx + ny[u]);
+                        float dd = dw_sqrt(fmaxf(d2, 0.f));
+                        if (diag && cb + j + u == row) dd = 0.f;
+                        v[j + u] = __float_as_uint(dd);
+                    }
+                }
+                // the staging boxes were last read by the tensor stores of tile t - nstage
+                unsigned char* stage = stage0 + (size_t)(t % nstage) * 4 * DT_M * 128;
+                if (tid == 0) {
+                    if (nstage == 2) asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+                    else asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+                }
+                asm volatile("bar.sync 1, %0;" :: "n"(DW_EPI_WARPS * 32) : "memory");
+                // box b (32 columns) = 128 rows x 128 B, 128B swizzle: 16-byte chunk c of row r at c ^ (r & 7)
+                const int r = q * 32 + lane;
+#pragma unroll
+                for (int bb = 0; bb < DW_CPW / 32; ++bb) {
+                    unsigned char* box = stage + (part * (DW_CPW / 32) + bb) * (DT_M * 128);
+#pragma unroll
+                    for (int c = 0; c < 8; ++c) {
+                        const int jj = bb * 32 + c * 4;
+                        *reinterpret_cast<uint4*>(box + r * 128 + ((c ^ (r & 7)) << 4)) =
+                            make_uint4(v[jj], v[jj + 1], v[jj + 2], v[jj + 3]);
+                    }
+                }
+                asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                asm volatile("bar.sync 1, %0;" :: "n"(DW_EPI_WARPS * 32) : "memory");
+                if (tid == 0) {
+#pragma unroll
+                    for (int bb = 0; bb < 4; ++bb) {
+                        const int x = (int)(n0 - c0) + bb * 32;
+                        asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%1, %2}], [%3];"
+                                     :: "l"(reinterpret_cast<uint64_t>(&tmap)), "r"(x), "r"(m0),
+                                        "r"(dt_smem_u32(stage + bb * (DT_M * 128)))
+                                     : "memory");
+                    }
+                    asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+                }
+            }
+        }
+        if (tid == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;");
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;");
+    if (warp == DW_EPI_WARPS)
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" :: "r"(tmem), "n"(2 * DT_N));
 }
 
 // L1 on integer coordinates: 64 x 64 output tile per block, 256 threads

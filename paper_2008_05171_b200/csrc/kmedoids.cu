@@ -14,6 +14,7 @@
 #include <cmath>
 #include <type_traits>
 #include <vector>
+#include <cudaTypedefs.h>
 
 #include "../../include/kmedoids.h"
 #include "km_kernels.cuh"
@@ -1606,8 +1607,17 @@ km_status kmedoids_dissimilarity(const void* X, km_metric metric, int64_t n, int
         if (ld % 4 != 0 || ((uintptr_t)D) % 16 != 0) return fail(KM_EINVAL, "D must be 16-byte aligned, ld % 4 == 0");
         const int dpad = (d + 7) / 8 * 8;
         const int64_t nm = cdiv(n, km::DT_M), ntc = cdiv(col_end - col_begin, km::DT_N);
-        const int64_t TF = km::dt_tile_floats(dpad);
+        int dev = 0, nsm = 0, smax = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+        cudaDeviceGetAttribute(&smax, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+        const char* ek = getenv("KM_DIST_KERNEL");     // "simple": the single-role kernel
+        const bool ws = !(ek && strcmp(ek, "simple") == 0) && km::dw_smem_bytes(dpad, 1) <= (size_t)smax;
+        int wstage = 1;                                 // measured: a second staging buffer is slower (L1 carve-out)
+        if (const char* es = getenv("KM_DIST_STAGES"))
+            if (atoi(es) == 2 && km::dw_smem_bytes(dpad, 2) <= (size_t)smax) wstage = 2;
         const bool same = (col_begin == 0);
+        const int64_t TF = ws ? km::dw_tile_floats(dpad) : km::dt_tile_floats(dpad);
         const size_t nrm_floats = (size_t)cdiv(n, 64) * 64;          // keeps the packed tiles 256-byte aligned
         const size_t scratch = nrm_floats + (size_t)nm * TF + (same ? 0 : (size_t)ntc * TF);
         float* nrm = nullptr;
@@ -1616,21 +1626,44 @@ km_status kmedoids_dissimilarity(const void* X, km_metric metric, int64_t n, int
         float* PA = nrm + nrm_floats;
         float* PB = same ? PA : PA + nm * TF;
         km::k_dist_norms<<<(unsigned)cdiv(n, 256), 256, 0, st>>>((const float*)X, (int)n, d, nrm);
-        km::k_dist_pack<<<(unsigned)nm, 256, 0, st>>>((const float*)X, nrm, d, dpad, 0, n, PA);
-        if (!same) km::k_dist_pack<<<(unsigned)ntc, 256, 0, st>>>((const float*)X, nrm, d, dpad, col_begin, col_end, PB);
-        int dev = 0, nsm = 0, smax = 0;
-        cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
-        cudaDeviceGetAttribute(&smax, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
-        const int nstage = km::dt_smem_bytes(dpad, 2) + 1024 <= (size_t)smax ? 2 : 1;
-        const size_t smem = km::dt_smem_bytes(dpad, nstage);
-        e = cudaFuncSetAttribute(km::k_dist_l2_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        if (e != cudaSuccess) { cudaFreeAsync(nrm, st); return fail(KM_ECUDA, "smem attribute: %s", cudaGetErrorString(e)); }
         // work items (row tile x column range): at least 8 per SM for balance
         const int nsplit = (int)std::max<int64_t>(1, std::min<int64_t>(ntc, cdiv((int64_t)nsm * 8, nm)));
         const int grid = (int)std::min<int64_t>(nsm, nm * nsplit);
-        km::k_dist_l2_tc<<<grid, km::DT_THREADS, smem, st>>>(PA, PB, (int)n, dpad, nstage, nsplit, (float*)D, ld,
-                                                              col_begin, col_end);
+        if (ws) {
+            km::k_dist_pack2<<<(unsigned)nm, 256, 0, st>>>((const float*)X, d, dpad, 0, n, PA);
+            if (!same) km::k_dist_pack2<<<(unsigned)ntc, 256, 0, st>>>((const float*)X, d, dpad, col_begin, col_end, PB);
+            static PFN_cuTensorMapEncodeTiled_v12000 encode = nullptr;
+            if (!encode) {
+                void* fn = nullptr;
+                cudaDriverEntryPointQueryResult qr;
+                e = cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &qr);
+                if (e != cudaSuccess || !fn) { cudaFreeAsync(nrm, st); return fail(KM_ECUDA, "cuTensorMapEncodeTiled unavailable"); }
+                encode = (PFN_cuTensorMapEncodeTiled_v12000)fn;
+            }
+            CUtensorMap tm;
+            cuuint64_t gdim[2] = {(cuuint64_t)(col_end - col_begin), (cuuint64_t)n};
+            cuuint64_t gstride[1] = {(cuuint64_t)ld * sizeof(float)};
+            cuuint32_t box[2] = {32, (cuuint32_t)km::DT_M};
+            cuuint32_t estr[2] = {1, 1};
+            CUresult cr = encode(&tm, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, D, gdim, gstride, box, estr,
+                                 CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                                 CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+            if (cr != CUDA_SUCCESS) { cudaFreeAsync(nrm, st); return fail(KM_ECUDA, "tensor map encode failed (%d)", (int)cr); }
+            const size_t smem = km::dw_smem_bytes(dpad, wstage);
+            e = cudaFuncSetAttribute(km::k_dist_l2_ws, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+            if (e != cudaSuccess) { cudaFreeAsync(nrm, st); return fail(KM_ECUDA, "smem attribute: %s", cudaGetErrorString(e)); }
+            km::k_dist_l2_ws<<<grid, km::DW_THREADS, smem, st>>>(tm, PA, PB, nrm, (int)n, dpad, nsplit, wstage,
+                                                                  col_begin, col_end);
+        } else {
+            km::k_dist_pack<<<(unsigned)nm, 256, 0, st>>>((const float*)X, nrm, d, dpad, 0, n, PA);
+            if (!same) km::k_dist_pack<<<(unsigned)ntc, 256, 0, st>>>((const float*)X, nrm, d, dpad, col_begin, col_end, PB);
+            const int nstage = km::dt_smem_bytes(dpad, 2) + 1024 <= (size_t)smax ? 2 : 1;
+            const size_t smem = km::dt_smem_bytes(dpad, nstage);
+            e = cudaFuncSetAttribute(km::k_dist_l2_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+            if (e != cudaSuccess) { cudaFreeAsync(nrm, st); return fail(KM_ECUDA, "smem attribute: %s", cudaGetErrorString(e)); }
+            km::k_dist_l2_tc<<<grid, km::DT_THREADS, smem, st>>>(PA, PB, (int)n, dpad, nstage, nsplit, (float*)D, ld,
+                                                                  col_begin, col_end);
+        }
         e = cudaGetLastError();
         cudaFreeAsync(nrm, st);
         if (e != cudaSuccess) return fail(KM_ECUDA, "k_dist_l2_tc: %s", cudaGetErrorString(e));

@@ -28,7 +28,7 @@ def l2_bound(X, d):
 
 @pytest.mark.parametrize("n,d,c0,c1", [(1, 1, 0, 1), (7, 2, 0, 7), (129, 10, 0, 129), (300, 27, 0, 300),
                                        (1000, 32, 0, 1000), (513, 64, 0, 513), (700, 33, 128, 515),
-                                       (260, 5, 256, 260)])
+                                       (260, 5, 256, 260), (3001, 17, 0, 3001), (900, 8, 300, 899)])
 def test_l2_tensor_core_matches_definition(n, d, c0, c1):
     from paper_2008_05171_b200 import kmedoids_dissimilarity
     rng = np.random.default_rng(n * 100 + d)
@@ -36,7 +36,7 @@ def test_l2_tensor_core_matches_definition(n, d, c0, c1):
     Dg = kmedoids_dissimilarity(torch.from_numpy(X).cuda(), "l2", col_begin=c0, col_end=c1)
     Dg = Dg[:, :c1 - c0].double().cpu().numpy()
     Dx = oracle.dist_l2(X)[:, c0:c1]
-    tol = l2_bound(X, d)[:, c0:c1] + 2.0 ** -22 * Dx ** 2
+    tol = l2_bound(X, d)[:, c0:c1] + 2.0 ** -20 * Dx ** 2
     err = np.abs(Dg ** 2 - Dx ** 2)
     assert (err <= tol).all(), (err.max(), np.unravel_index(np.argmax(err - tol), err.shape))
     for i in range(max(c0, 0), min(c1, n)):
@@ -65,7 +65,7 @@ def test_l2_config_points_close_to_generator_and_swap_runs():
     Dt = kmedoids_dissimilarity(torch.from_numpy(X).cuda(), "l2")
     D = Dt[:, :n].cpu().numpy()
     Dx = oracle.dist_l2(X)
-    assert (np.abs(D.astype(np.float64) ** 2 - Dx ** 2) <= l2_bound(X, X.shape[1]) + 2.0 ** -22 * Dx ** 2).all()
+    assert (np.abs(D.astype(np.float64) ** 2 - Dx ** 2) <= l2_bound(X, X.shape[1]) + 2.0 ** -20 * Dx ** 2).all()
     M0 = kmsynth.random_medoids(cfg, k=k, n=n)
     km = KMedoids(Dt, n, k)
     km.set_medoids(M0)
