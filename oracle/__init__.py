@@ -301,3 +301,40 @@ def dist_l1(Xq: np.ndarray) -> np.ndarray:
     D = np.empty((n, n), np.int64)
     _load().oracle_dist_l1(_ptr(Xq), ctypes.c_int32(n), ctypes.c_int32(d), _ptr(D))
     return D
+
+
+def init_weighted(D: np.ndarray, k: int, u) -> np.ndarray:
+    """Distance-weighted seeding (reading I1) with the uniforms u[k]."""
+    f, acc = _fn(D, "oracle_init_weighted")
+    f.restype = ctypes.c_int
+    M = np.zeros(k, np.int32)
+    uu = np.ascontiguousarray(u, np.float64)
+    if f(_ptr(D), ctypes.c_int64(_ld(D)), ctypes.c_int32(D.shape[0]), ctypes.c_int32(k), _ptr(uu), _ptr(M)) != 0:
+        raise ValueError("init_weighted needs 1 <= k <= n")
+    return M
+
+
+def init_lab(D: np.ndarray, k: int, s: int, seq) -> np.ndarray:
+    """LAB (reading I2) with the per-step index rows seq[k][s+k]."""
+    f, acc = _fn(D, "oracle_init_lab")
+    f.restype = ctypes.c_int
+    M = np.zeros(k, np.int32)
+    q = np.ascontiguousarray(seq, np.int32)
+    if f(_ptr(D), ctypes.c_int64(_ld(D)), ctypes.c_int32(D.shape[0]), ctypes.c_int32(k), ctypes.c_int32(s),
+         _ptr(q), _ptr(M)) != 0:
+        raise ValueError("init_lab needs 1 <= k <= n, s >= 1")
+    return M
+
+
+def lab_sample_rows(n: int, k: int, seed: int, s: int | None = None):
+    """The caller-side random input of LAB: s = 10 + ceil(sqrt(n)) and, per step,
+    s + k distinct uniform indices (numpy Generator(PCG64(seed)))."""
+    import math
+    s = s if s is not None else 10 + math.ceil(math.sqrt(n))
+    s = min(s, n)
+    rng = np.random.Generator(np.random.PCG64(seed))
+    w = min(n, s + k)
+    rows = np.stack([rng.choice(n, size=w, replace=False) for _ in range(k)]).astype(np.int32)
+    if w < s + k:                                   # fewer than s + k points: pad with -1 (skipped)
+        rows = np.concatenate([rows, np.full((k, s + k - w), -1, np.int32)], axis=1)
+    return s, rows

@@ -433,6 +433,89 @@ int FN(oracle_build)(const D_T* D, int64_t ld, int32_t n, int32_t k, int32_t* M,
     return 0;
 }
 
+/* NEXT-4 initialisations.  Random numbers are INPUTS (drawn
+ * by the caller, identical for the oracle and the GPU).
+ *
+ * Distance-weighted ("k-means++" adapted to arbitrary dissimilarities,
+ * P:1046-1059; reading I1): the first seed is
+ * min(n-1, floor(u[0] n)); seed i > 0 is the smallest index c whose running
+ * sum of w(o) = min_j d(x_o, m_j) over o = 0..c exceeds u[i] * W, W = sum
+ * of all w (sequential sums in index order, ACC_T); if W = 0 the smallest
+ * non-medoid is taken.  d(x_o, m_j) = D[o][m_j] (reading R0). */
+int FN(oracle_init_weighted)(const D_T* D, int64_t ld, int32_t n, int32_t k, const double* u, int32_t* M) {
+    if (k < 1 || k > n) return -1;
+    ACC_T* w = (ACC_T*)malloc(sizeof(ACC_T) * (size_t)n);
+    int32_t c = (int32_t)(u[0] * (double)n);
+    if (c >= n) c = n - 1;
+    M[0] = c;
+    for (int32_t o = 0; o < n; ++o) w[o] = DIST(o, c);
+    for (int32_t i = 1; i < k; ++i) {
+        ACC_T W = 0;
+        for (int32_t o = 0; o < n; ++o) W += w[o];
+        int32_t pick = -1;
+        if (W > 0) {
+            const double r = u[i] * (double)W;
+            ACC_T run = 0;
+            for (int32_t o = 0; o < n; ++o) {
+                run += w[o];
+                if ((double)run > r) { pick = o; break; }
+            }
+        }
+        if (pick < 0)                       /* W = 0 (or r rounded to W): smallest non-medoid */
+            for (int32_t o = 0; o < n && pick < 0; ++o)
+                if (!FN(is_medoid)(M, i, o)) pick = o;
+        M[i] = pick;
+        for (int32_t o = 0; o < n; ++o) {
+            const ACC_T d = DIST(o, pick);
+            if (d < w[o]) w[o] = d;
+        }
+    }
+    free(w);
+    return 0;
+}
+
+/* LAB, Linear Approximative BUILD (the SISAP'19 paper that
+ * defines it is not in the container: reading I2).  Step i draws the
+ * sample S_i = the first s entries of seq[i*(s+k) ...] that are not yet
+ * medoids (the caller supplies distinct indices per row, -1 = padding); for each
+ * candidate c in S_i (in order) g(c) = sum over o in S_i (in order) of
+ * d(x_o, x_c) for i = 0 (BUILD's first step, Alg.1) and of
+ * min(d(x_o, x_c) - d_nearest(o), 0) for i > 0 (Alg.1 P:300-310 restricted
+ * to the subsample, self term included as reading R3); the smallest
+ * (g, c) is the next medoid; d_nearest is then updated for all objects. */
+int FN(oracle_init_lab)(const D_T* D, int64_t ld, int32_t n, int32_t k, int32_t s, const int32_t* seq, int32_t* M) {
+    if (k < 1 || k > n || s < 1) return -1;
+    ACC_T* dnear = (ACC_T*)malloc(sizeof(ACC_T) * (size_t)n);
+    int32_t* S = (int32_t*)malloc(sizeof(int32_t) * (size_t)s);
+    for (int32_t i = 0; i < k; ++i) {
+        const int32_t* row = seq + (int64_t)i * (s + k);
+        int32_t m = 0;
+        for (int32_t j = 0; j < s + k && m < s; ++j)
+            if (row[j] >= 0 && !FN(is_medoid)(M, i, row[j])) S[m++] = row[j];
+        ACC_T bg = 0; int32_t bc = -1;
+        for (int32_t a = 0; a < m; ++a) {
+            const int32_t c = S[a];
+            ACC_T g = 0;
+            for (int32_t b = 0; b < m; ++b) {
+                const int32_t o = S[b];
+                if (i == 0) g += DIST(o, c);
+                else {
+                    const ACC_T delta = DIST(o, c) - dnear[o];
+                    if (delta < 0) g += delta;
+                }
+            }
+            if (bc < 0 || g < bg || (g == bg && c < bc)) { bg = g; bc = c; }
+        }
+        M[i] = bc;
+        for (int32_t o = 0; o < n; ++o) {
+            const ACC_T d = DIST(o, bc);
+            if (i == 0 || d < dnear[o]) dnear[o] = d;
+        }
+    }
+    free(dnear); free(S);
+    return 0;
+}
+
 #undef DIST
 #undef FN
 #undef CAT

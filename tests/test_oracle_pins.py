@@ -469,3 +469,44 @@ def test_dist_oracle_closed_forms_and_library():
             assert (D[i, j] <= D[i, l] + D[l, j] + 1e-12).all()
         Xq = rng.integers(-5000, 5000, size=(n, d)).astype(np.int32)
         assert (oracle.dist_l1(Xq) == cdist(Xq, Xq, "cityblock").astype(np.int64)).all()
+
+
+# ---------- NEXT-4 initialisations (readings I1, I2) ----------
+
+def test_init_weighted_hand_example_and_intervals():
+    """Distance-weighted seeding: the 1-D example by hand, and for every
+    candidate c the uniform u at the middle of its interval
+    [prefix(c-1), prefix(c)) / W picks exactly c (sampling proportional to
+    the distance to the nearest seed)."""
+    x = np.array([0, 1, 2, 10, 11, 30])
+    D = np.abs(x[:, None] - x[None, :]).astype(np.uint32)
+    assert oracle.init_weighted(D, 3, [0.0, 0.5, 0.99]).tolist() == [0, 5, 4]
+    rng = np.random.default_rng(4)
+    D = rand_int_matrix(rng, 40, 100)
+    first = 7
+    w = D[:, first].astype(np.int64)
+    pref = np.cumsum(w)
+    for c in range(40):
+        if w[c] == 0:
+            continue
+        u1 = (pref[c] - w[c] / 2) / pref[-1]
+        M = oracle.init_weighted(D, 2, [(first + 0.5) / 40, u1])
+        assert M.tolist() == [first, c]
+    # all points identical: W = 0 -> smallest non-medoids
+    Z = np.zeros((6, 6), np.uint32)
+    assert oracle.init_weighted(Z, 3, [0.5, 0.3, 0.3]).tolist() == [3, 0, 1]
+
+
+@pytest.mark.parametrize("seed", range(4))
+def test_init_lab_with_full_samples_equals_build(seed):
+    """LAB restricted to a sample equal to all points is PAM BUILD (Alg.1,
+    P:281-318, reading R3): same medoids for integer and float inputs."""
+    rng = np.random.default_rng(900 + seed)
+    n, k = int(rng.integers(8, 60)), int(rng.integers(1, 6))
+    D = rand_int_matrix(rng, n, int(rng.choice([5, 1000])), symmetric=bool(seed % 2))
+    rows = np.stack([np.concatenate([rng.permutation(n), -np.ones(k, np.int64)]) for _ in range(k)]).astype(np.int32)
+    Mb, _, _ = oracle.build_init(D, k)
+    assert oracle.init_lab(D, k, n, rows).tolist() == Mb.tolist()
+    Df = (D.astype(np.float32) * 0.37).astype(np.float32)
+    Mbf, _, _ = oracle.build_init(Df, k)
+    assert oracle.init_lab(Df, k, n, rows).tolist() == Mbf.tolist()
