@@ -90,6 +90,22 @@ km_status kmedoids_set_medoids(km_handle* h, const int32_t* medoids);
  * driven through kmedoids_build_step*). */
 km_status kmedoids_init_build(km_handle* h, int32_t* medoids_out, void* td_out);
 
+/* NEXT-4 initialisations, single GPU.  Random numbers are
+ * caller inputs (the oracle uses the same), so runs are reproducible.
+ *  kmedoids_init_weighted: distance-weighted seeding ("k-means++" adapted to
+ *    arbitrary dissimilarities; reading I1).  u: host
+ *    array of k uniforms in [0, 1): seed 0 = floor(u[0] n); seed i = the first
+ *    object whose running sum of w(o) = min_j d(x_o, m_j) exceeds u[i] * W.
+ *  kmedoids_init_lab: LAB (reading I2).  seq: host array of k
+ *    rows of (s + k) indices in [0, n) or -1 (padding), distinct per row;
+ *    step i samples the first s non-medoids of row i and takes BUILD's choice
+ *    on that sample (s = 10 + ceil(sqrt(n))).
+ * Both leave the handle ready for SWAP (cache and TD as kmedoids_set_medoids);
+ * medoids_out[k] / td_out may be NULL.  Errors: KM_EINVAL (k < 2, u outside
+ * [0, 1), s outside [1, n], indices out of range, sharded handle). */
+km_status kmedoids_init_weighted(km_handle* h, const double* u, int32_t* medoids_out, void* td_out);
+km_status kmedoids_init_lab(km_handle* h, int32_t s, const int32_t* seq, int32_t* medoids_out, void* td_out);
+
 /* One SWAP iteration (FastPAM1: Alg.3; FastPAM2: reading R6;
  * FasterPAM: one pass of Alg.4's candidate scan) from the
  * current state.  *swaps_done_out (may be NULL) receives the number of

@@ -21,6 +21,7 @@
 #include "km_fasterpam.cuh"
 #include "km_post.cuh"
 #include "km_dist.cuh"
+#include "km_init.cuh"
 
 namespace {
 
@@ -135,6 +136,8 @@ struct ImplBase {
     virtual km_status fp2_shard_eval() = 0;
     virtual km_status fp2_shard_plan(const int64_t* rcb, int32_t* m_out, int32_t* maxcnt_out) = 0;
     virtual km_status fp2_shard_apply(int32_t* swaps_out, void* td_out) = 0;
+    virtual km_status init_weighted(const double* u, int32_t* M_out, void* td_out) = 0;
+    virtual km_status init_lab(int32_t s, const int32_t* seq, int32_t* M_out, void* td_out) = 0;
     bool profiling = false;
     double prof_ms = 0.0;
     int64_t prof_launches = 0;
@@ -1231,6 +1234,62 @@ struct Impl : ImplBase {
         return fp2_sequential(f2_order, f2_col_recv, f2_colidx, swaps_out, td_out);
     }
 
+    // ---- NEXT-4 initialisations (km_init.cuh) ----------------------------------
+    km_status init_common_alloc(T** w, int** flags) {
+        if (!init_w) { KM_TRY(alloc(&init_w, n)); KM_TRY(alloc(&init_flags, n)); }
+        KM_CK(cudaMemsetAsync(init_flags, 0, n * sizeof(int), st));
+        *w = init_w; *flags = init_flags;
+        return KM_OK;
+    }
+    T* init_w = nullptr;
+    int* init_flags = nullptr;
+
+    km_status finish_init(int32_t* M_out, void* td_out) {
+        std::vector<int32_t> Mh((size_t)k);
+        KM_CK(cudaMemcpyAsync(Mh.data(), M, k * sizeof(int32_t), cudaMemcpyDeviceToHost, st));
+        KM_CK(cudaStreamSynchronize(st));
+        KM_TRY(set_medoids(Mh.data()));
+        if (M_out) memcpy(M_out, Mh.data(), k * sizeof(int32_t));
+        copy_td(td_out);
+        return KM_OK;
+    }
+
+    km_status init_weighted(const double* u, int32_t* M_out, void* td_out) override {
+        if (sharded) return fail(KM_EINVAL, "init_weighted on a sharded handle");
+        if (k < 2) return fail(KM_EINVAL, "SWAP needs k >= 2");
+        for (int i = 0; i < k; ++i)
+            if (!(u[i] >= 0.0 && u[i] < 1.0)) return fail(KM_EINVAL, "u[%d] = %g not in [0, 1)", i, u[i]);
+        T* w; int* fl;
+        KM_TRY(init_common_alloc(&w, &fl));
+        double* ud = nullptr;
+        KM_CK(cudaMallocAsync((void**)&ud, k * sizeof(double), st));
+        KM_CK(cudaMemcpyAsync(ud, u, k * sizeof(double), cudaMemcpyHostToDevice, st));
+        km::k_init_weighted<T, A><<<1, km::INIT_THREADS, 0, st>>>(D, ld, (int)n, k, ud, M, w, fl);
+        KM_CKL();
+        ++launches;
+        KM_CK(cudaFreeAsync(ud, st));
+        return finish_init(M_out, td_out);
+    }
+
+    km_status init_lab(int32_t s, const int32_t* seq, int32_t* M_out, void* td_out) override {
+        if (sharded) return fail(KM_EINVAL, "init_lab on a sharded handle");
+        if (k < 2) return fail(KM_EINVAL, "SWAP needs k >= 2");
+        if (s < 1 || s > n) return fail(KM_EINVAL, "sample size s=%d must be in [1, n]", s);
+        const size_t cnt = (size_t)k * (s + k);
+        for (size_t j = 0; j < cnt; ++j)
+            if (seq[j] < -1 || seq[j] >= n) return fail(KM_EINVAL, "seq[%zu] = %d out of range", j, seq[j]);
+        T* w; int* fl;
+        KM_TRY(init_common_alloc(&w, &fl));
+        int* sd = nullptr;
+        KM_CK(cudaMallocAsync((void**)&sd, (cnt + (size_t)s) * sizeof(int), st));
+        KM_CK(cudaMemcpyAsync(sd, seq, cnt * sizeof(int), cudaMemcpyHostToDevice, st));
+        km::k_init_lab<T, A><<<1, km::INIT_THREADS, 0, st>>>(D, ld, (int)n, k, s, sd, M, w, fl, sd + cnt);
+        KM_CKL();
+        ++launches;
+        KM_CK(cudaFreeAsync(sd, st));
+        return finish_init(M_out, td_out);
+    }
+
     // ---- BUILD ---------------------------------------------------------------
     template <int MODE>
     km_status launch_build_tma() {
@@ -1502,6 +1561,18 @@ km_status kmedoids_set_medoids(km_handle* h, const int32_t* medoids) {
 km_status kmedoids_init_build(km_handle* h, int32_t* medoids_out, void* td_out) {
     KM_H();
     return h->impl->init_build(medoids_out, td_out);
+}
+
+km_status kmedoids_init_weighted(km_handle* h, const double* u, int32_t* medoids_out, void* td_out) {
+    KM_H();
+    if (!u) return fail(KM_EINVAL, "u is NULL");
+    return h->impl->init_weighted(u, medoids_out, td_out);
+}
+
+km_status kmedoids_init_lab(km_handle* h, int32_t s, const int32_t* seq, int32_t* medoids_out, void* td_out) {
+    KM_H();
+    if (!seq) return fail(KM_EINVAL, "seq is NULL");
+    return h->impl->init_lab(s, seq, medoids_out, td_out);
 }
 
 km_status kmedoids_swap_iter(km_handle* h, km_variant variant, int32_t* swaps_done_out, void* td_out) {

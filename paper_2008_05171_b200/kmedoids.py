@@ -88,6 +88,8 @@ def load_library() -> ctypes.CDLL:
         "kmedoids_build_select": [vp, vp, vp, vp, vp],
         "kmedoids_build_apply": [vp, i32],
         "kmedoids_dissimilarity": [vp, ctypes.c_int, i64, i32, vp, i64, i64, i64, vp],
+        "kmedoids_init_weighted": [vp, vp, vp, vp],
+        "kmedoids_init_lab": [vp, i32, vp, vp, vp],
     }
     for name, args in sig.items():
         f = getattr(lib, name)
@@ -179,6 +181,26 @@ class KMedoids:
         M = np.zeros(self.k, np.int32)
         td = np.zeros(1, self.acc)
         _check(load_library().kmedoids_init_build(self.h, _p(M), _p(td)))
+        return M, td[0].item()
+
+    def init_weighted(self, u):
+        """Distance-weighted seeding with the caller's uniforms u[k] (NEXT-4)."""
+        uu = np.ascontiguousarray(np.asarray(u, np.float64))
+        if uu.shape != (self.k,):
+            raise ValueError(f"expected {self.k} uniforms")
+        M = np.zeros(self.k, np.int32)
+        td = np.zeros(1, self.acc)
+        _check(load_library().kmedoids_init_weighted(self.h, _p(uu), _p(M), _p(td)))
+        return M, td[0].item()
+
+    def init_lab(self, s: int, seq):
+        """LAB with the caller's per-step index rows seq[k][s+k] (NEXT-4)."""
+        q = np.ascontiguousarray(np.asarray(seq, np.int32))
+        if q.shape != (self.k, s + self.k):
+            raise ValueError(f"expected seq of shape ({self.k}, {s + self.k})")
+        M = np.zeros(self.k, np.int32)
+        td = np.zeros(1, self.acc)
+        _check(load_library().kmedoids_init_lab(self.h, int(s), _p(q), _p(M), _p(td)))
         return M, td[0].item()
 
     def swap_iter(self, variant="fastpam1"):
