@@ -1243,6 +1243,9 @@ struct Impl : ImplBase {
     }
     T* init_w = nullptr;
     int* init_flags = nullptr;
+    double* init_u = nullptr;
+    int* init_seq = nullptr;
+    size_t init_seq_cap = 0;
 
     km_status finish_init(int32_t* M_out, void* td_out) {
         std::vector<int32_t> Mh((size_t)k);
@@ -1261,13 +1264,11 @@ struct Impl : ImplBase {
             if (!(u[i] >= 0.0 && u[i] < 1.0)) return fail(KM_EINVAL, "u[%d] = %g not in [0, 1)", i, u[i]);
         T* w; int* fl;
         KM_TRY(init_common_alloc(&w, &fl));
-        double* ud = nullptr;
-        KM_CK(cudaMallocAsync((void**)&ud, k * sizeof(double), st));
-        KM_CK(cudaMemcpyAsync(ud, u, k * sizeof(double), cudaMemcpyHostToDevice, st));
-        km::k_init_weighted<T, A><<<1, km::INIT_THREADS, 0, st>>>(D, ld, (int)n, k, ud, M, w, fl);
+        if (!init_u) KM_TRY(alloc(&init_u, k));
+        KM_CK(cudaMemcpyAsync(init_u, u, k * sizeof(double), cudaMemcpyHostToDevice, st));
+        km::k_init_weighted<T, A><<<1, km::INIT_THREADS, 0, st>>>(D, ld, (int)n, k, init_u, M, w, fl);
         KM_CKL();
         ++launches;
-        KM_CK(cudaFreeAsync(ud, st));
         return finish_init(M_out, td_out);
     }
 
@@ -1280,13 +1281,14 @@ struct Impl : ImplBase {
             if (seq[j] < -1 || seq[j] >= n) return fail(KM_EINVAL, "seq[%zu] = %d out of range", j, seq[j]);
         T* w; int* fl;
         KM_TRY(init_common_alloc(&w, &fl));
-        int* sd = nullptr;
-        KM_CK(cudaMallocAsync((void**)&sd, (cnt + (size_t)s) * sizeof(int), st));
-        KM_CK(cudaMemcpyAsync(sd, seq, cnt * sizeof(int), cudaMemcpyHostToDevice, st));
-        km::k_init_lab<T, A><<<1, km::INIT_THREADS, 0, st>>>(D, ld, (int)n, k, s, sd, M, w, fl, sd + cnt);
+        if (cnt + (size_t)s > init_seq_cap) {       // grows only (the handle owns its scratch)
+            KM_TRY(alloc(&init_seq, cnt + (size_t)s));
+            init_seq_cap = cnt + (size_t)s;
+        }
+        KM_CK(cudaMemcpyAsync(init_seq, seq, cnt * sizeof(int), cudaMemcpyHostToDevice, st));
+        km::k_init_lab<T, A><<<1, km::INIT_THREADS, 0, st>>>(D, ld, (int)n, k, s, init_seq, M, w, fl, init_seq + cnt);
         KM_CKL();
         ++launches;
-        KM_CK(cudaFreeAsync(sd, st));
         return finish_init(M_out, td_out);
     }
 
