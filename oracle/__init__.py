@@ -338,3 +338,22 @@ def lab_sample_rows(n: int, k: int, seed: int, s: int | None = None):
     if w < s + k:                                   # fewer than s + k points: pad with -1 (skipped)
         rows = np.concatenate([rows, np.full((k, s + k - w), -1, np.int32)], axis=1)
     return s, rows
+
+
+def clara(D: np.ndarray, k: int, samples, variant: str = "fastpam1"):
+    """FastCLARA (reading C1): PAM (BUILD, Alg.1, then SWAP:
+    FastPAM1 Alg.3 or FasterPAM Alg.4) on the sub-matrix D[S][S] of every
+    sample S (caller-drawn, distinct indices), medoids mapped back to point
+    indices, TD over ALL points (Eq. eqn:td); the sample with the smallest
+    (TD, sample index) wins.  Returns (TD, best sample index, medoids)."""
+    best = None
+    for j, S in enumerate(samples):
+        S = np.asarray(S, np.int64)
+        Dj = np.ascontiguousarray(D[np.ix_(S, S)])
+        Mb, _, _ = build_init(Dj, k)
+        r = swap_run(Dj, Mb, FASTPAM1) if variant == "fastpam1" else fasterpam_run(Dj, Mb)
+        M = S[r.medoids].astype(np.int32)
+        t = td(D, M)
+        if best is None or t < best[0]:
+            best = (t, j, M)
+    return best

@@ -510,3 +510,27 @@ def test_init_lab_with_full_samples_equals_build(seed):
     Df = (D.astype(np.float32) * 0.37).astype(np.float32)
     Mbf, _, _ = oracle.build_init(Df, k)
     assert oracle.init_lab(Df, k, n, rows).tolist() == Mbf.tolist()
+
+
+# ---------- NEXT-3 FastCLARA (reading C1) ----------
+
+def test_clara_full_sample_is_pam_and_best_sample_wins():
+    """A single sample holding every point makes CLARA the PAM of the whole
+    set (BUILD + FastPAM1, pinned above); with several samples the returned
+    TD is the definition's TD of the returned medoids and no sample's
+    solution has a smaller TD."""
+    rng = np.random.default_rng(61)
+    n, k = 90, 4
+    D = rand_int_matrix(rng, n, 300)
+    t, j, M = oracle.clara(D, k, [np.arange(n)])
+    Mb, _, _ = oracle.build_init(D, k)
+    ref = oracle.swap_run(D, Mb, oracle.FASTPAM1)
+    assert j == 0 and M.tolist() == ref.medoids.tolist() and t == ref.td
+    samples = [rng.choice(n, size=30, replace=False) for _ in range(5)]
+    t, j, M = oracle.clara(D, k, samples)
+    assert t == bf_td(D, M)
+    for S in samples:
+        Dj = np.ascontiguousarray(D[np.ix_(S, S)])
+        Mj, _, _ = oracle.build_init(Dj, k)
+        rj = oracle.swap_run(Dj, Mj, oracle.FASTPAM1)
+        assert bf_td(D, S[rj.medoids]) >= t
