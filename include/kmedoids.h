@@ -106,6 +106,18 @@ km_status kmedoids_init_build(km_handle* h, int32_t* medoids_out, void* td_out);
 km_status kmedoids_init_weighted(km_handle* h, const double* u, int32_t* medoids_out, void* td_out);
 km_status kmedoids_init_lab(km_handle* h, int32_t s, const int32_t* seq, int32_t* medoids_out, void* td_out);
 
+/* NEXT-3 FastCLARA (reading C1), single GPU.  For each
+ * of the nsamples caller-drawn samples (host array samples[nsamples][s] of
+ * distinct indices in [0, n); P:1122 suggests s = 80 + 4k): PAM on the s x s
+ * sub-matrix (BUILD, then SWAP with `variant` to convergence), medoids mapped
+ * back to point indices, TD over all n objects; the sample with the smallest
+ * (TD, sample index) wins.  The handle is left on the winning medoids (cache,
+ * TD); medoids_out[k], td_out, best_sample_out may be NULL.  Scratch: s x s
+ * sub-matrix + one nested handle (allocated on first use; s fixed per handle).
+ * Errors: KM_EINVAL (s <= k or s > n, bad or duplicate indices, sharded). */
+km_status kmedoids_clara(km_handle* h, int32_t nsamples, int32_t s, const int32_t* samples, km_variant variant,
+                         int32_t* medoids_out, void* td_out, int32_t* best_sample_out);
+
 /* One SWAP iteration (FastPAM1: Alg.3; FastPAM2: reading R6;
  * FasterPAM: one pass of Alg.4's candidate scan) from the
  * current state.  *swaps_done_out (may be NULL) receives the number of

@@ -147,4 +147,14 @@ k_init_lab(const T* __restrict__ D, int64_t ld, int n, int k, int s, const int* 
     }
 }
 
+// FastCLARA (NEXT-3): the sub-matrix of a sample, sub[a][b] = d(x_S[a], x_S[b])
+// = D[S[a]][S[b]] (reading R0 orientation), row stride lds.
+template <typename T>
+__global__ void k_gather_submatrix(const T* __restrict__ D, int64_t ld, const int* __restrict__ S, int s,
+                                   T* __restrict__ sub, int64_t lds) {
+    const int b = blockIdx.x * blockDim.x + threadIdx.x, a = blockIdx.y;
+    if (b >= s) return;
+    sub[(int64_t)a * lds + b] = D[(int64_t)S[a] * ld + S[b]];
+}
+
 }  // namespace km

@@ -138,6 +138,8 @@ struct ImplBase {
     virtual km_status fp2_shard_apply(int32_t* swaps_out, void* td_out) = 0;
     virtual km_status init_weighted(const double* u, int32_t* M_out, void* td_out) = 0;
     virtual km_status init_lab(int32_t s, const int32_t* seq, int32_t* M_out, void* td_out) = 0;
+    virtual km_status clara(int32_t ns, int32_t s, const int32_t* samples, km_variant v, int32_t* M_out,
+                            void* td_out, int32_t* best_out) = 0;
     bool profiling = false;
     double prof_ms = 0.0;
     int64_t prof_launches = 0;
@@ -1292,6 +1294,78 @@ struct Impl : ImplBase {
         return finish_init(M_out, td_out);
     }
 
+    // ---- NEXT-3 FastCLARA (reading C1) ------------------------------
+    // Per sample: gather the s x s sub-matrix, PAM on it (BUILD + SWAP with
+    // the requested variant, one nested handle reused for every sample), map
+    // the medoids back and evaluate TD over ALL n objects with this handle's
+    // cache kernels; keep the smallest (TD, sample).  Leaves this handle on
+    // the winning medoids.
+    T* clara_buf = nullptr;
+    int* clara_idx = nullptr;
+    int64_t clara_s = 0;
+    std::unique_ptr<Impl<T>> clara_sub;
+
+    km_status clara(int32_t ns, int32_t s, const int32_t* samples, km_variant v, int32_t* M_out, void* td_out,
+                    int32_t* best_out) override {
+        if (sharded) return fail(KM_EINVAL, "clara on a sharded handle");
+        if (k < 2) return fail(KM_EINVAL, "CLARA needs k >= 2");
+        if (ns < 1) return fail(KM_EINVAL, "nsamples must be >= 1");
+        if (s <= k || s > n) return fail(KM_EINVAL, "sample size s=%d must satisfy k < s <= n", s);
+        if (v != KM_FASTPAM1 && v != KM_FASTPAM2 && v != KM_FASTERPAM) return fail(KM_EINVAL, "unknown variant");
+        std::vector<char> seen((size_t)n, 0);
+        for (int j = 0; j < ns; ++j) {
+            const int32_t* S = samples + (size_t)j * s;
+            for (int a = 0; a < s; ++a) {
+                if (S[a] < 0 || S[a] >= n) return fail(KM_EINVAL, "sample %d: index %d out of range", j, S[a]);
+                if (seen[S[a]]) return fail(KM_EINVAL, "sample %d: duplicate index %d", j, S[a]);
+                seen[S[a]] = 1;
+            }
+            for (int a = 0; a < s; ++a) seen[S[a]] = 0;
+        }
+        const int64_t lds = cdiv(s, 4) * 4;
+        if (clara_s != s) {
+            if (clara_s != 0) return fail(KM_EINVAL, "this handle already ran CLARA with s=%lld", (long long)clara_s);
+            KM_TRY(alloc(&clara_buf, (size_t)s * lds));
+            KM_TRY(alloc(&clara_idx, s));
+            KM_CK(cudaMemsetAsync(clara_buf, 0, (size_t)s * lds * sizeof(T), st));
+            clara_sub.reset(new Impl<T>());
+            KM_TRY(clara_sub->init(clara_buf, s, lds, 0, s, k, st));
+            clara_s = s;
+        }
+        A best_td = km::amax<A>();
+        int best_j = -1;
+        std::vector<int32_t> Mloc((size_t)k), Mg((size_t)k), Mbest((size_t)k);
+        for (int j = 0; j < ns; ++j) {
+            const int32_t* S = samples + (size_t)j * s;
+            KM_CK(cudaMemcpyAsync(clara_idx, S, s * sizeof(int32_t), cudaMemcpyHostToDevice, st));
+            km::k_gather_submatrix<T><<<dim3((unsigned)cdiv(s, 256), (unsigned)s), 256, 0, st>>>(D, ld, clara_idx, s,
+                                                                                                 clara_buf, lds);
+            KM_CKL();
+            ++launches;
+            Impl<T>& sub = *clara_sub;
+            KM_TRY(sub.init_build(nullptr, nullptr));
+            km_status rs = KM_OK;
+            for (int it = 0; it < 2000; ++it) {
+                rs = sub.swap_iter(v, nullptr, nullptr);
+                if (rs == KM_CONVERGED) break;
+                if (rs != KM_OK) return rs;
+            }
+            launches += sub.launches;
+            sub.launches = 0;
+            KM_TRY(sub.get_state(Mloc.data(), nullptr, nullptr, nullptr, nullptr));
+            for (int i = 0; i < k; ++i) Mg[i] = S[Mloc[i]];
+            KM_TRY(set_medoids(Mg.data()));            // TD over all n objects (Eq. eqn:td)
+            A tdj;
+            KM_CK(cudaMemcpy(&tdj, td, sizeof(A), cudaMemcpyDeviceToHost));
+            if (best_j < 0 || tdj < best_td) { best_td = tdj; best_j = j; Mbest = Mg; }
+        }
+        KM_TRY(set_medoids(Mbest.data()));
+        if (M_out) memcpy(M_out, Mbest.data(), k * sizeof(int32_t));
+        if (best_out) *best_out = best_j;
+        copy_td(td_out);
+        return KM_OK;
+    }
+
     // ---- BUILD ---------------------------------------------------------------
     template <int MODE>
     km_status launch_build_tma() {
@@ -1575,6 +1649,13 @@ km_status kmedoids_init_lab(km_handle* h, int32_t s, const int32_t* seq, int32_t
     KM_H();
     if (!seq) return fail(KM_EINVAL, "seq is NULL");
     return h->impl->init_lab(s, seq, medoids_out, td_out);
+}
+
+km_status kmedoids_clara(km_handle* h, int32_t nsamples, int32_t s, const int32_t* samples, km_variant variant,
+                         int32_t* medoids_out, void* td_out, int32_t* best_sample_out) {
+    KM_H();
+    if (!samples) return fail(KM_EINVAL, "samples is NULL");
+    return h->impl->clara(nsamples, s, samples, variant, medoids_out, td_out, best_sample_out);
 }
 
 km_status kmedoids_swap_iter(km_handle* h, km_variant variant, int32_t* swaps_done_out, void* td_out) {

@@ -90,6 +90,7 @@ def load_library() -> ctypes.CDLL:
         "kmedoids_dissimilarity": [vp, ctypes.c_int, i64, i32, vp, i64, i64, i64, vp],
         "kmedoids_init_weighted": [vp, vp, vp, vp],
         "kmedoids_init_lab": [vp, i32, vp, vp, vp],
+        "kmedoids_clara": [vp, i32, i32, vp, ctypes.c_int, vp, vp, vp],
     }
     for name, args in sig.items():
         f = getattr(lib, name)
@@ -202,6 +203,18 @@ class KMedoids:
         td = np.zeros(1, self.acc)
         _check(load_library().kmedoids_init_lab(self.h, int(s), _p(q), _p(M), _p(td)))
         return M, td[0].item()
+
+    def clara(self, samples, variant="fastpam1"):
+        """FastCLARA over the caller's samples[nsamples][s] (NEXT-3): (medoids, TD, best sample)."""
+        q = np.ascontiguousarray(np.asarray(samples, np.int32))
+        if q.ndim != 2:
+            raise ValueError("samples must be (nsamples, s)")
+        M = np.zeros(self.k, np.int32)
+        td = np.zeros(1, self.acc)
+        b = np.zeros(1, np.int32)
+        _check(load_library().kmedoids_clara(self.h, q.shape[0], q.shape[1], _p(q), VARIANTS[variant], _p(M), _p(td),
+                                             _p(b)))
+        return M, td[0].item(), int(b[0])
 
     def swap_iter(self, variant="fastpam1"):
         if getattr(self, "_it_bufs", None) is None:        # reused: keeps the per-call host work small
