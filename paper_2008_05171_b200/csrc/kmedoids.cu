@@ -15,6 +15,7 @@
 #include <type_traits>
 #include <vector>
 #include <cudaTypedefs.h>
+#include <thread>
 
 #include "../../include/kmedoids.h"
 #include "km_kernels.cuh"
@@ -212,6 +213,7 @@ struct Impl : ImplBase {
     cudaEvent_t ev0 = nullptr, ev1 = nullptr;
 
     ~Impl() override {
+        for (auto& sl : clara_slots) { sl.sub.reset(); if (sl.stream) cudaStreamDestroy(sl.stream); }
         if (fp1_exec) cudaGraphExecDestroy(fp1_exec);
         if (cap_st) cudaStreamDestroy(cap_st);
         for (void* p : bufs) cudaFree(p);
@@ -1300,10 +1302,20 @@ struct Impl : ImplBase {
     // the medoids back and evaluate TD over ALL n objects with this handle's
     // cache kernels; keep the smallest (TD, sample).  Leaves this handle on
     // the winning medoids.
-    T* clara_buf = nullptr;
-    int* clara_idx = nullptr;
+    // The samples are independent: up to CLARA_CONC of them run concurrently,
+    // each on its own CUDA stream with its own nested handle and sub-matrix,
+    // driven by its own host thread (the GPU overlaps the small, launch-bound
+    // sub-problems).  The TD over all objects is then evaluated per sample on
+    // this handle, in sample order.
+    static constexpr int CLARA_CONC = 8;
+    struct ClaraSlot {
+        T* buf = nullptr;
+        int* idx = nullptr;
+        cudaStream_t stream = nullptr;
+        std::unique_ptr<Impl<T>> sub;
+    };
+    std::vector<ClaraSlot> clara_slots;
     int64_t clara_s = 0;
-    std::unique_ptr<Impl<T>> clara_sub;
 
     km_status clara(int32_t ns, int32_t s, const int32_t* samples, km_variant v, int32_t* M_out, void* td_out,
                     int32_t* best_out) override {
@@ -1323,44 +1335,69 @@ struct Impl : ImplBase {
             for (int a = 0; a < s; ++a) seen[S[a]] = 0;
         }
         const int64_t lds = cdiv(s, 4) * 4;
-        if (clara_s != s) {
-            if (clara_s != 0) return fail(KM_EINVAL, "this handle already ran CLARA with s=%lld", (long long)clara_s);
-            KM_TRY(alloc(&clara_buf, (size_t)s * lds));
-            KM_TRY(alloc(&clara_idx, s));
-            KM_CK(cudaMemsetAsync(clara_buf, 0, (size_t)s * lds * sizeof(T), st));
-            clara_sub.reset(new Impl<T>());
-            KM_TRY(clara_sub->init(clara_buf, s, lds, 0, s, k, st));
-            clara_s = s;
+        if (clara_s != 0 && clara_s != s) return fail(KM_EINVAL, "this handle already ran CLARA with s=%lld", (long long)clara_s);
+        clara_s = s;
+        const int conc = std::min(ns, CLARA_CONC);
+        KM_CK(cudaStreamSynchronize(st));              // D and the cache are settled before other streams read D
+        while ((int)clara_slots.size() < conc) {
+            ClaraSlot sl;
+            KM_TRY(alloc(&sl.buf, (size_t)s * lds));
+            KM_TRY(alloc(&sl.idx, s));
+            KM_CK(cudaStreamCreateWithFlags(&sl.stream, cudaStreamNonBlocking));
+            KM_CK(cudaMemsetAsync(sl.buf, 0, (size_t)s * lds * sizeof(T), sl.stream));
+            sl.sub.reset(new Impl<T>());
+            KM_TRY(sl.sub->init(sl.buf, s, lds, 0, s, k, sl.stream));
+            clara_slots.push_back(std::move(sl));
         }
+        std::vector<std::vector<int32_t>> Mg((size_t)ns, std::vector<int32_t>((size_t)k));
+        std::vector<km_status> res((size_t)ns, KM_OK);
+        std::vector<std::string> errs((size_t)ns);
+        auto worker = [&](int slot) {
+            ClaraSlot& sl = clara_slots[slot];
+            Impl<T>& sub = *sl.sub;
+            for (int j = slot; j < ns; j += conc) {
+                const int32_t* S = samples + (size_t)j * s;
+                km_status r = KM_OK;
+                if (cudaMemcpyAsync(sl.idx, S, s * sizeof(int32_t), cudaMemcpyHostToDevice, sl.stream) != cudaSuccess)
+                    r = KM_ECUDA;
+                if (r == KM_OK) {
+                    km::k_gather_submatrix<T><<<dim3((unsigned)cdiv(s, 256), (unsigned)s), 256, 0, sl.stream>>>(
+                        D, ld, sl.idx, s, sl.buf, lds);
+                    if (cudaGetLastError() != cudaSuccess) r = KM_ECUDA;
+                }
+                if (r == KM_OK) r = sub.init_build(nullptr, nullptr);
+                for (int it = 0; r == KM_OK && it < 2000; ++it) {
+                    const km_status q = sub.swap_iter(v, nullptr, nullptr);
+                    if (q == KM_CONVERGED) break;
+                    if (q != KM_OK) r = q;
+                }
+                std::vector<int32_t> Mloc((size_t)k);
+                if (r == KM_OK) r = sub.get_state(Mloc.data(), nullptr, nullptr, nullptr, nullptr);
+                if (r == KM_OK)
+                    for (int i = 0; i < k; ++i) Mg[j][i] = S[Mloc[i]];
+                res[j] = r;
+                if (r != KM_OK) errs[j] = g_err;
+            }
+        };
+        {
+            std::vector<std::thread> th;
+            for (int t = 1; t < conc; ++t) th.emplace_back(worker, t);
+            worker(0);
+            for (auto& x : th) x.join();
+        }
+        for (int j = 0; j < ns; ++j)
+            if (res[j] != KM_OK) return fail(res[j], "CLARA sample %d: %s", j, errs[j].c_str());
+        for (auto& sl : clara_slots) { launches += sl.sub->launches + 1; sl.sub->launches = 0; }
         A best_td = km::amax<A>();
         int best_j = -1;
-        std::vector<int32_t> Mloc((size_t)k), Mg((size_t)k), Mbest((size_t)k);
         for (int j = 0; j < ns; ++j) {
-            const int32_t* S = samples + (size_t)j * s;
-            KM_CK(cudaMemcpyAsync(clara_idx, S, s * sizeof(int32_t), cudaMemcpyHostToDevice, st));
-            km::k_gather_submatrix<T><<<dim3((unsigned)cdiv(s, 256), (unsigned)s), 256, 0, st>>>(D, ld, clara_idx, s,
-                                                                                                 clara_buf, lds);
-            KM_CKL();
-            ++launches;
-            Impl<T>& sub = *clara_sub;
-            KM_TRY(sub.init_build(nullptr, nullptr));
-            km_status rs = KM_OK;
-            for (int it = 0; it < 2000; ++it) {
-                rs = sub.swap_iter(v, nullptr, nullptr);
-                if (rs == KM_CONVERGED) break;
-                if (rs != KM_OK) return rs;
-            }
-            launches += sub.launches;
-            sub.launches = 0;
-            KM_TRY(sub.get_state(Mloc.data(), nullptr, nullptr, nullptr, nullptr));
-            for (int i = 0; i < k; ++i) Mg[i] = S[Mloc[i]];
-            KM_TRY(set_medoids(Mg.data()));            // TD over all n objects (Eq. eqn:td)
+            KM_TRY(set_medoids(Mg[j].data()));          // TD over all n objects (Eq. eqn:td)
             A tdj;
             KM_CK(cudaMemcpy(&tdj, td, sizeof(A), cudaMemcpyDeviceToHost));
-            if (best_j < 0 || tdj < best_td) { best_td = tdj; best_j = j; Mbest = Mg; }
+            if (best_j < 0 || tdj < best_td) { best_td = tdj; best_j = j; }
         }
-        KM_TRY(set_medoids(Mbest.data()));
-        if (M_out) memcpy(M_out, Mbest.data(), k * sizeof(int32_t));
+        KM_TRY(set_medoids(Mg[best_j].data()));
+        if (M_out) memcpy(M_out, Mg[best_j].data(), k * sizeof(int32_t));
         if (best_out) *best_out = best_j;
         copy_td(td_out);
         return KM_OK;

@@ -12,7 +12,7 @@ s = min(n, 80 + 4 * k)
 rng = np.random.Generator(np.random.PCG64(cfg.seed + 5000))
 S = np.stack([rng.choice(n, size=s, replace=False) for _ in range(5)]).astype(np.int32)
 km = KMedoids(Dt, n, k, stream=st)
-km.clara(S[:1], "fasterpam")          # warm-up (nested handle, graphs)
+km.clara(S, "fastpam1"); km.clara(S, "fasterpam")          # warm-up (nested handles, scratch, graphs)
 for variant in ["fastpam1", "fasterpam"]:
     torch.cuda.synchronize(); e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record(st); M, td, j = km.clara(S, variant); e1.record(st); torch.cuda.synchronize()
