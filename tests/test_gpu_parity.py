@@ -359,3 +359,27 @@ def test_fastpam2_float_c3_prefix():
     assert st.td == pytest.approx(oracle.td(D, M), rel=1e-12)
     v, s = km.eval_candidates()
     assert np.nanmin(np.where(s >= 0, v, np.inf)) >= -1e-9 * st.td
+
+
+@pytest.mark.parametrize("variant", ["fastpam1", "fastpam2", "fasterpam"])
+def test_large_k_and_tiny_n(variant):
+    """Many slots (k = 900 of n = 2501: segments of ~3 rows, many empty-slot
+    and part-boundary cases) and the smallest problems (n = 3, k = 2)."""
+    rng = np.random.default_rng(8080)
+    n, k = 2501, 900
+    D = rand_int(rng, n, 1 << 20)
+    M0 = rng.choice(n, size=k, replace=False).astype(np.int32)
+    ref = (oracle.fasterpam_run(D, M0) if variant == "fasterpam"
+           else oracle.swap_run(D, M0, oracle.FASTPAM1 if variant == "fastpam1" else oracle.FASTPAM2, max_iter=6))
+    km = KM(to_dev(D), n, k)
+    km.set_medoids(M0)
+    r = km.run(use_build=False, variant=variant, max_iter=2000 if variant == "fasterpam" else 6)
+    assert r.medoids.tolist() == ref.medoids.tolist() and r.td == ref.td
+    assert (r.n_iter, r.n_swaps) == (ref.n_iter, ref.n_swaps)
+    D3 = np.array([[0, 5, 1], [5, 0, 4], [1, 4, 0]], np.uint32)
+    ref3 = (oracle.fasterpam_run(D3, [1, 2]) if variant == "fasterpam"
+            else oracle.swap_run(D3, [1, 2], oracle.FASTPAM1 if variant == "fastpam1" else oracle.FASTPAM2))
+    km3 = KM(to_dev(D3), 3, 2)
+    km3.set_medoids([1, 2])
+    r3 = km3.run(use_build=False, variant=variant)
+    assert r3.medoids.tolist() == ref3.medoids.tolist() and r3.td == ref3.td
