@@ -23,6 +23,7 @@
 #include "km_post.cuh"
 #include "km_dist.cuh"
 #include "km_init.cuh"
+#include "km_build_delta.cuh"
 
 namespace {
 
@@ -1447,19 +1448,91 @@ struct Impl : ImplBase {
         return KM_OK;
     }
 
+    // ---- incremental BUILD (km_build_delta.cuh; KM_BUILD=full recomputes every step)
+    int bd_mode = -1;               // 1: incremental gains, 0: a full pass per step
+    A* bd_gain = nullptr;
+    T *bd_dnold = nullptr, *bd_lold = nullptr, *bd_lnew = nullptr;
+    int *bd_flag = nullptr, *bd_cnt = nullptr, *bd_off = nullptr, *bd_lo = nullptr, *bd_m = nullptr;
+    int bd_B = 1, bd_chunk = 1;
+
+    km_status bd_alloc() {
+        if (bd_gain) return KM_OK;
+        bd_B = (int)std::min<int64_t>(1024, cdiv(n, km::BD_CHUNK_THREADS));
+        bd_chunk = (int)cdiv(n, bd_B);
+        KM_TRY(alloc(&bd_gain, w));
+        KM_TRY(alloc(&bd_dnold, n));
+        KM_TRY(alloc(&bd_lold, n));
+        KM_TRY(alloc(&bd_lnew, n));
+        KM_TRY(alloc(&bd_flag, n));
+        KM_TRY(alloc(&bd_lo, n));
+        KM_TRY(alloc(&bd_cnt, bd_B));
+        KM_TRY(alloc(&bd_off, bd_B));
+        KM_TRY(alloc(&bd_m, 1));
+        return KM_OK;
+    }
+
+    // step >= 1 gains into bd_gain and the best record into rec_local:
+    // a full pass (step 1) or the delta pass over the objects changed by the
+    // previous step
+    km_status bd_eval(int step) {
+        using C = km::SegCfg<T, SG_NC, SG_RB, SG_S>;
+        if (step == 1) {
+            auto kern = km::k_build_tma<T, A, SG_NC, SG_RB, SG_S, SG_MINB, 1>;
+            KM_CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM));
+            dim3 g((unsigned)cdiv(w, C::COLS), Pbt);
+            kern<<<g, C::THREADS, C::SMEM, st>>>(D, ld, w, wpad, (int)n, Pbt, dn, b_out);
+        } else {
+            auto kern = km::k_build_delta_tma<T, A, SG_NC, SG_RB, SG_S, SG_MINB>;
+            KM_CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM));
+            dim3 g((unsigned)cdiv(w, C::COLS), Pbt);
+            kern<<<g, C::THREADS, C::SMEM, st>>>(D, ld, w, wpad, Pbt, bd_m, bd_lo, bd_lold, bd_lnew, b_out);
+        }
+        KM_CKL();
+        ++launches;
+        km::k_build_gain_combine<A><<<ncomb, 128, 0, st>>>(w, c0, Pbt, b_out, step == 1 ? 0 : 1, bd_gain, point_slot,
+                                                            partials, counters, rec_local);
+        KM_CKL();
+        ++launches;
+        return KM_OK;
+    }
+
     km_status init_build(int32_t* M_out, void* td_out) override {
         if (sharded) return fail(KM_EINVAL, "init_build on a sharded handle; use kmedoids_build_* phases");
+        if (bd_mode < 0) {
+            const char* e = getenv("KM_BUILD");
+            bd_mode = (e && (strcmp(e, "full") == 0 || strcmp(e, "ldg") == 0)) ? 0 : 1;
+            if (!build_tma) bd_mode = 0;
+        }
+        if (bd_mode == 1) KM_TRY(bd_alloc());
         KM_CK(cudaMemsetAsync(point_slot, 0xff, n * sizeof(int), st));
         ready = false;
         const int nb = (int)cdiv(n, 256);
         for (int step = 0; step < k; ++step) {
-            KM_TRY(build_eval(step));
+            if (bd_mode == 1 && step >= 1) KM_TRY(bd_eval(step));
+            else KM_TRY(build_eval(step));
             km::k_build_select<A><<<1, 1, 0, st>>>(rec_local, 1, step, td, M, point_slot, dec);
             KM_CKL();
-            km::k_gather_decided_col<T, A><<<nb, 256, 0, st>>>(D, ld, (int)n, c0, c1, dec, MC, nullptr);
-            KM_CKL();
-            km::k_build_dn<T, A><<<nb, 256, 0, st>>>(MC, (int)n, dec, point_slot, dn);
-            KM_CKL();
+            if (bd_mode == 1 && step >= 1) {
+                if (step + 1 < k) {
+                    km::k_build_dn_delta<T, A><<<bd_B, km::BD_CHUNK_THREADS, 0, st>>>(
+                        D, ld, (int)n, c0, dec, MC, point_slot, dn, bd_dnold, bd_flag, bd_chunk, bd_cnt);
+                    KM_CKL();
+                    km::k_chunk_scan<<<1, 1024, 0, st>>>(bd_cnt, bd_B, bd_off, bd_m);
+                    KM_CKL();
+                    km::k_changed_scatter<T><<<bd_B, km::BD_CHUNK_THREADS, 0, st>>>(
+                        (int)n, bd_flag, bd_dnold, dn, bd_chunk, bd_off, bd_lo, bd_lold, bd_lnew);
+                    KM_CKL();
+                    launches += 3;
+                } else {                                 // last step: only MC is needed
+                    km::k_gather_decided_col<T, A><<<nb, 256, 0, st>>>(D, ld, (int)n, c0, c1, dec, MC, nullptr);
+                    KM_CKL();
+                }
+            } else {
+                km::k_gather_decided_col<T, A><<<nb, 256, 0, st>>>(D, ld, (int)n, c0, c1, dec, MC, nullptr);
+                KM_CKL();
+                km::k_build_dn<T, A><<<nb, 256, 0, st>>>(MC, (int)n, dec, point_slot, dn);
+                KM_CKL();
+            }
         }
         KM_TRY(build_finish());
         KM_CK(cudaStreamSynchronize(st));
