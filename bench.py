@@ -311,12 +311,17 @@ def run_ours(args):
             torch.cuda.synchronize()
             return r, e0.elapsed_time(e1) / 1e3
         to_converge("fasterpam")                     # warm-up (allocations, first launches)
+        to_converge("fastpam1_inc")
         rf, sf = to_converge("fasterpam")
+        ri, si = to_converge("fastpam1_inc")
         r1, s1 = to_converge("fastpam1")
         fpm = {"variant": "fasterpam (Alg.4 P:988-1027, exact eager scan)", "s_to_converge": sf,
                "passes": rf.n_iter, "swaps": rf.n_swaps, "td": rf.td,
                "fastpam1_s_to_converge": s1, "fastpam1_iterations": r1.n_iter, "fastpam1_td": r1.td,
                "speedup_vs_fastpam1": s1 / sf,
+               "fastpam1_incremental_s_to_converge": si, "fastpam1_incremental_iterations": ri.n_iter,
+               "fastpam1_incremental_td": ri.td, "fastpam1_incremental_same_medoids":
+                   bool(ri.medoids.tolist() == r1.medoids.tolist()),
                "start": "the initial medoids of the timed run (after " + cfg.init + ")"}
 
     # NEXT-2: the dissimilarity matrix of the config materialised by the product

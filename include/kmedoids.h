@@ -59,7 +59,13 @@ typedef enum { KM_U32 = 0, KM_F32 = 1 } km_dtype;
 /* KM_FASTERPAM: FasterPAM's eager swapping (Alg.4; readings
  * F1-F5 in DESIGN.md), evaluated exactly on the GPU by speculative candidate
  * batches. */
-typedef enum { KM_FASTPAM1 = 0, KM_FASTPAM2 = 1, KM_FASTERPAM = 2 } km_variant;
+/* KM_FASTPAM1_INC: the same swaps as KM_FASTPAM1 (Alg.3's best swap per
+ * iteration, reading R1; bit-exact on U32), computed incrementally: the
+ * k-vectors of every candidate are kept (one FastPAM2-mode stream of D) and
+ * corrected after each swap from the rows of the objects whose nearest /
+ * second changed, instead of re-streaming D (DESIGN.md "incremental
+ * FastPAM1"; extra device memory k*n*8 bytes).  Single GPU. */
+typedef enum { KM_FASTPAM1 = 0, KM_FASTPAM2 = 1, KM_FASTERPAM = 2, KM_FASTPAM1_INC = 3 } km_variant;
 
 typedef struct km_handle km_handle;  /* opaque; owns only its scratch buffers */
 

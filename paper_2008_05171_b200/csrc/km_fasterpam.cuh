@@ -101,12 +101,15 @@ struct Fp3Args {
     int chg_cap;
     int* touched_flag;   // [k], zero between steps
     int* touched_map;    // [k] slot -> touched index
-    int* touched;        // [FP3_TMAX]
+    int* touched;        // [k]
     A* part_acc;         // [FP3_G][FP3_TMAX][L]
     A* part_plus;        // [FP3_G][L]
     A* part_R;           // [FP3_G][FP3_TMAX]
     Fp3Ctl* ctl;
     int new_pass;        // count a pass in dec->iters (F3)
+    // GLOBAL mode (incremental FastPAM1): best swap over all candidates per iteration
+    int max_iters;
+    Rec<A>* gpart;       // [gridDim] per-block best records
 };
 
 template <typename T>
@@ -176,7 +179,12 @@ __global__ void k_fp3_transpose_mc(const T* __restrict__ MC, int n, int k, T* __
     }
 }
 
-template <typename T, typename A>
+// GLOBAL = false: FasterPAM's eager scan of one window (Alg.4).
+// GLOBAL = true: incremental FastPAM1 (Alg.3's best swap per iteration, key
+// R1) over ALL candidates: the stored k-vectors acc[i][c] / plus[c] (a
+// FastPAM2-mode stream pass) are corrected after every swap for every
+// candidate, so an iteration reads the changed objects' rows instead of D.
+template <typename T, typename A, bool GLOBAL>
 __global__ void __launch_bounds__(FP3_THREADS)
 k_fp3_window(Fp3Args<T, A> g) {
     namespace cg = cooperative_groups;
@@ -195,12 +203,16 @@ k_fp3_window(Fp3Args<T, A> g) {
     if (g.new_pass && blockIdx.x == 0 && threadIdx.x == 0) g.dec->iters += 1;
     unsigned long long tlast = fp3_now();
 
-    while (p < vhi) {
+    int iters_done = 0;
+    bool converged = false;
+    while (GLOBAL ? (iters_done < g.max_iters) : (p < vhi)) {
         // ------------------------------------------------------------ pick
         if (blockIdx.x == 0 && threadIdx.x == 0) ctl->nres = 0;
         for (int b = tid; b < (int)gridDim.x; b += nth) g.blk_cnt[b] = 0;
         int found = INT_MAX;
         const A tdv = __ldcg(g.td);
+        int gslot = 0;
+        A gv = 0;
         // R_i staged in shared memory for the pick (the correction's buffer is idle here)
         A* sR = reinterpret_cast<A*>(fp3_smem);
         const bool r_smem = (size_t)k * sizeof(A) <= (size_t)FP3_SMEM;
@@ -208,6 +220,53 @@ k_fp3_window(Fp3Args<T, A> g) {
             for (int i = threadIdx.x; i < k; i += blockDim.x) sR[i] = __ldcg(&g.R[i]);
             __syncthreads();
         }
+        if constexpr (GLOBAL) {
+            // lexicographic min of (dTD, slot, c) over every non-medoid candidate (R1);
+            // one thread per candidate, slots in ascending order (strict <): the
+            // acc[i][j .. j+31] reads of a warp are contiguous
+            __shared__ Rec<A> sbest[FP3_WARPS];
+            Rec<A> best = rec_none<A>();
+            for (int j = tid; j < g.hi; j += nth) {
+                const int64_t cc = g.c0 + g.a + j;
+                if (__ldcg(&g.point_slot[cc]) >= 0) continue;
+                A bv = amax<A>();
+                int bs = INT_MAX;
+                const A* aj = g.acc + j;
+#pragma unroll 8
+                for (int i = 0; i < k; ++i) {
+                    const A v = (r_smem ? sR[i] : __ldcg(&g.R[i])) + __ldcg(aj + (int64_t)i * g.ww);
+                    if (v < bv) { bv = v; bs = i; }
+                }
+                Rec<A> r; r.v = bv + __ldcg(&g.plus[j]); r.slot = bs; r.c = (int)cc;
+                if (rec_less(r, best)) best = r;
+            }
+            best = warp_min_rec(best);
+            if (lane == 0) sbest[warp] = best;
+            __syncthreads();
+            if (threadIdx.x == 0) {
+                Rec<A> b = rec_none<A>();
+                for (int w2 = 0; w2 < FP3_WARPS; ++w2) if (rec_less(sbest[w2], b)) b = sbest[w2];
+                g.gpart[blockIdx.x] = b;
+            }
+            if (blockIdx.x == 0 && threadIdx.x == 0) g.dec->iters += 1;   // a pass
+            grid.sync();
+            Rec<A> b = rec_none<A>();
+            for (int q2 = threadIdx.x; q2 < (int)gridDim.x; q2 += blockDim.x) {
+                Rec<A> r;
+                r.v = __ldcg(&g.gpart[q2].v); r.slot = __ldcg(&g.gpart[q2].slot); r.c = __ldcg(&g.gpart[q2].c);
+                if (rec_less(r, b)) b = r;
+            }
+            b = block_min_rec(b);
+            __shared__ Rec<A> sfin;
+            if (threadIdx.x == 0) sfin = b;
+            __syncthreads();
+            b = sfin;
+            ++iters_done;
+            if (b.slot == INT_MAX || !fp3_improving(b.v, tdv)) { converged = true; break; }
+            found = (int)(b.c - g.c0 - g.a);
+            gslot = b.slot;
+            gv = b.v;
+        } else
         for (int base = p; base < vhi; base += nwarps) {
             const int slot_now = rnd % 3;
             // first[(rnd+1)%3] was last read before the previous round's sync
@@ -244,8 +303,8 @@ k_fp3_window(Fp3Args<T, A> g) {
 
         // ------------------------------------------------------------ apply
         const int j = found;
-        const int slot = __ldcg(&g.cand_s[j]);
-        const A v = __ldcg(&g.cand_v[j]);
+        const int slot = GLOBAL ? gslot : __ldcg(&g.cand_s[j]);
+        const A v = GLOBAL ? gv : __ldcg(&g.cand_v[j]);
         const int64_t c = g.c0 + g.a + j;
         if (blockIdx.x == 0 && threadIdx.x == 0) {
             const int old = g.M[slot];
@@ -369,7 +428,7 @@ k_fp3_window(Fp3Args<T, A> g) {
                     int bt;
                     const int r = fp3_block_scan(f, &bt);
                     if (f) {
-                        if (tb + r < FP3_TMAX) g.touched[tb + r] = s;
+                        g.touched[tb + r] = s;
                         g.touched_map[s] = tb + r;
                     }
                     tb += bt;
@@ -383,9 +442,9 @@ k_fp3_window(Fp3Args<T, A> g) {
         if (blockIdx.x == 0 && threadIdx.x == 0) {
             ctl->pad[0] += __ldcg(&ctl->nres); ctl->pad[1] += m; ctl->pad[2] += T_;
         }
-        const int cl0 = j + 1;
-        const int cl1 = min(vhi, j + 1 + g.L);
-        if (m > g.chg_cap || T_ > FP3_TMAX) {
+        const int cl0 = GLOBAL ? 0 : j + 1;              // GLOBAL: every candidate is corrected
+        const int cl1 = GLOBAL ? vhi : min(vhi, j + 1 + g.L);
+        if (m > g.chg_cap) {
             // too many changes for the correction step: the rest of the
             // window is stale; the host re-streams from j + 1
             status = FP3_STALE;
@@ -395,6 +454,10 @@ k_fp3_window(Fp3Args<T, A> g) {
             break;
         }
         // ------------------------------------------------------------ correct
+        // touched slots are handled FP3_TMAX at a time (per-warp shared-memory
+        // accumulators); plus / R deltas of the non-slot terms in the first slice
+        for (int tb = 0; tb < T_; tb += FP3_TMAX) {
+        const int TS = min(FP3_TMAX, T_ - tb);
         __syncthreads();
         // warp item = (event group q, 32-column tile u) of [cl0, cl1).  The
         // group's events are loaded 32 at a time (one per lane) and
@@ -412,7 +475,7 @@ k_fp3_window(Fp3Args<T, A> g) {
                 const int col = u * 32 + lane;          // offset in [0, L)
                 const bool act = col < ncols;
                 const int64_t dcol = (int64_t)g.a + (act ? cl0 + col : 0);
-                for (int t = 0; t < T_; ++t) sacc[t * 32 + lane] = 0;
+                for (int t = 0; t < TS; ++t) sacc[t * 32 + lane] = 0;
                 if (lane < FP3_TMAX) srs[lane] = 0;
                 __syncwarp();
                 A pl = 0;
@@ -424,8 +487,8 @@ k_fp3_window(Fp3Args<T, A> g) {
                     if (lane < nb) {
                         const Fp3Chg<T> ch = fp3_ld_chg(&g.chg[eb + lane]);
                         o_l = ch.o;
-                        to_l = __ldcg(&g.touched_map[ch.near_old]);
-                        tn_l = __ldcg(&g.touched_map[ch.near_new]);
+                        to_l = __ldcg(&g.touched_map[ch.near_old]) - tb;   // slice-local, may be outside
+                        tn_l = __ldcg(&g.touched_map[ch.near_new]) - tb;
                         dno = ch.dn_old; dso = ch.ds_old; dnn = ch.dn_new; dsn = ch.ds_new;
                     }
                     for (int e8 = 0; e8 < nb; e8 += 16) {
@@ -445,12 +508,13 @@ k_fp3_window(Fp3Args<T, A> g) {
                                 A tpo, tao, tpn, tan_;
                                 fp3_terms<T, A>(x[v8], a_dno, a_dso, tpo, tao);
                                 fp3_terms<T, A>(x[v8], a_dnn, a_dsn, tpn, tan_);
-                                pl += tpn - tpo;
-                                sacc[a_to * 32 + lane] -= tao;
-                                sacc[a_tn * 32 + lane] += tan_;
+                                if (tb == 0) pl += tpn - tpo;
+                                const bool io = (unsigned)a_to < (unsigned)TS, in_ = (unsigned)a_tn < (unsigned)TS;
+                                if (io) sacc[a_to * 32 + lane] -= tao;
+                                if (in_) sacc[a_tn * 32 + lane] += tan_;
                                 if (u == 0 && lane == 0) {
-                                    srs[a_to] -= (A)a_dso - (A)a_dno;
-                                    srs[a_tn] += (A)a_dsn - (A)a_dnn;
+                                    if (io) srs[a_to] -= (A)a_dso - (A)a_dno;
+                                    if (in_) srs[a_tn] += (A)a_dsn - (A)a_dnn;
                                 }
                             }
                         }
@@ -458,11 +522,11 @@ k_fp3_window(Fp3Args<T, A> g) {
                 }
                 __syncwarp();
                 if (act) {
-                    for (int t = 0; t < T_; ++t)
+                    for (int t = 0; t < TS; ++t)
                         g.part_acc[((int64_t)q * FP3_TMAX + t) * g.L + col] = sacc[t * 32 + lane];
-                    g.part_plus[(int64_t)q * g.L + col] = pl;
+                    if (tb == 0) g.part_plus[(int64_t)q * g.L + col] = pl;
                 }
-                if (u == 0 && lane < T_) g.part_R[q * FP3_TMAX + lane] = srs[lane];
+                if (u == 0 && lane < TS) g.part_R[q * FP3_TMAX + lane] = srs[lane];
                 __syncwarp();
             }
         }
@@ -472,38 +536,41 @@ k_fp3_window(Fp3Args<T, A> g) {
             const int ncols = cl1 - cl0;
             const int G = min(FP3_G, max(1, nwarps / max((ncols + 31) / 32, 1)));
             // acc[slot_t][col] += sum_q part_acc[q][t][col]  (fixed order)
-            for (int it = tid; it < T_ * ncols; it += nth) {
+            for (int it = tid; it < TS * ncols; it += nth) {
                 const int t = it / ncols, col = it % ncols;
                 A s = 0;
 #pragma unroll 8
                 for (int q = 0; q < G; ++q) s += __ldcg(&g.part_acc[((int64_t)q * FP3_TMAX + t) * g.L + col]);
-                A* dst = &g.acc[(int64_t)__ldcg(&g.touched[t]) * g.ww + cl0 + col];
+                A* dst = &g.acc[(int64_t)__ldcg(&g.touched[tb + t]) * g.ww + cl0 + col];
                 *dst = __ldcg(dst) + s;
             }
-            for (int col = tid; col < ncols; col += nth) {
+            for (int col = tid; tb == 0 && col < ncols; col += nth) {
                 A s = 0;
 #pragma unroll 8
                 for (int q = 0; q < G; ++q) s += __ldcg(&g.part_plus[(int64_t)q * g.L + col]);
                 g.plus[cl0 + col] = __ldcg(&g.plus[cl0 + col]) + s;
             }
             // R_s += sum over changed objects of the change of (d_s - d_n) in slot s
-            for (int t = tid; t < T_; t += nth) {
+            for (int t = tid; t < TS; t += nth) {
                 A rs = 0;
                 for (int q = 0; q < G; ++q) rs += __ldcg(&g.part_R[q * FP3_TMAX + t]);
-                const int sl = __ldcg(&g.touched[t]);
+                const int sl = __ldcg(&g.touched[tb + t]);
                 g.R[sl] = __ldcg(&g.R[sl]) + rs;
             }
-            for (int s = tid; s < k; s += nth) g.touched_flag[s] = 0;
+            if (tb + FP3_TMAX >= T_)
+                for (int s = tid; s < k; s += nth) g.touched_flag[s] = 0;
         }
         grid.sync();
+        }   // slices of touched slots
         if (blockIdx.x == 0 && threadIdx.x == 0) { const unsigned long long tn = fp3_now(); ctl->tphase[6] += tn - tlast; tlast = tn; }
-        p = j + 1;
-        vhi = cl1;
+        if (!GLOBAL) { p = j + 1; vhi = cl1; }
     }
     if (blockIdx.x == 0 && threadIdx.x == 0) {
         ctl->status = status;
         ctl->p_end = p;
         ctl->swaps = swaps;
+        ctl->pad[3] = converged ? 1 : 0;
+        ctl->pad[4] = iters_done;
     }
 }
 

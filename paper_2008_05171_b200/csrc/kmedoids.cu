@@ -142,6 +142,8 @@ struct ImplBase {
     virtual km_status init_lab(int32_t s, const int32_t* seq, int32_t* M_out, void* td_out) = 0;
     virtual km_status clara(int32_t ns, int32_t s, const int32_t* samples, km_variant v, int32_t* M_out,
                             void* td_out, int32_t* best_out) = 0;
+    virtual km_status inc_iters(int32_t max_iters, int32_t* swaps, void* td_out, int32_t* iters_done,
+                                bool* converged) = 0;
     bool profiling = false;
     double prof_ms = 0.0;
     int64_t prof_launches = 0;
@@ -412,6 +414,7 @@ struct Impl : ImplBase {
         ready = true;
         fp3_reset();
         fp1_prepped = false;
+        inc_valid = false;
         return KM_OK;
     }
 
@@ -668,10 +671,12 @@ struct Impl : ImplBase {
     km_status swap_iter(km_variant v, int32_t* swaps, void* td_out) override {
         if (sharded) return fail(KM_EINVAL, "swap_iter on a sharded handle; use the kmedoids_shard_* phases");
         if (!ready) return fail(KM_EINVAL, "no medoids: call kmedoids_set_medoids or kmedoids_init_build first");
-        if (v != KM_FASTPAM1 && v != KM_FASTPAM2 && v != KM_FASTERPAM)
+        if (v != KM_FASTPAM1 && v != KM_FASTPAM2 && v != KM_FASTERPAM && v != KM_FASTPAM1_INC)
             return fail(KM_EINVAL, "unknown variant %d", (int)v);
         if (v == KM_FASTPAM2) return swap_iter_fp2(swaps, td_out);
         if (v == KM_FASTERPAM) return swap_iter_fp3(swaps, td_out);
+        if (v == KM_FASTPAM1_INC) return inc_iters(1, swaps, td_out, nullptr, nullptr);
+        inc_valid = false;
         if (use_post < 0) {
             const char* e = getenv("KM_POST");
             use_post = (e && e[0] == '0') ? 0 : 1;
@@ -868,6 +873,7 @@ struct Impl : ImplBase {
     // One single-GPU FastPAM2 iteration (reading R6).
     km_status swap_iter_fp2(int32_t* swaps_out, void* td_out) {
         fp1_prepped = false;
+        inc_valid = false;
         KM_TRY(fp2_eval_local());
         A tdh;
         KM_CK(cudaMemcpyAsync(h_best.data(), fp2_best, k * sizeof(Rec), cudaMemcpyDeviceToHost, st));
@@ -995,13 +1001,15 @@ struct Impl : ImplBase {
         KM_TRY(alloc(&f3_mct, (size_t)n * k));
         KM_TRY(alloc(&f3_tflag, k));
         KM_TRY(alloc(&f3_tmap, k));
-        KM_TRY(alloc(&f3_tlist, km::FP3_TMAX));
+        KM_TRY(alloc(&f3_tlist, k));
         KM_TRY(alloc(&f3_ctl, 1));
         KM_TRY(alloc(&f3_trace, wcap));
         KM_CK(cudaMemsetAsync(f3_tflag, 0, k * sizeof(int), st));
         KM_CK(cudaMallocHost((void**)&h_f3ctl, sizeof(km::Fp3Ctl)));
-        auto kern = km::k_fp3_window<T, A>;
+        auto kern = km::k_fp3_window<T, A, false>;
         KM_CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, km::FP3_SMEM));
+        KM_CK(cudaFuncSetAttribute(km::k_fp3_window<T, A, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   km::FP3_SMEM));
         int dev = 0, per_sm = 0, nsm = 0;
         KM_CK(cudaGetDevice(&dev));
         KM_CK(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
@@ -1044,8 +1052,9 @@ struct Impl : ImplBase {
         g.old_ds = f3_oldds; g.rescan = f3_rescan; g.blk_cnt = f3_blk; g.chg = f3_chg; g.chg_cap = (int)n;
         g.touched_flag = f3_tflag; g.touched_map = f3_tmap; g.touched = f3_tlist;
         g.part_acc = f3_pacc; g.part_plus = f3_pplus; g.part_R = f3_pR; g.ctl = f3_ctl; g.new_pass = new_pass ? 1 : 0;
+        g.max_iters = 0; g.gpart = nullptr;
         void* args[] = {&g};
-        KM_CK(cudaLaunchCooperativeKernel((void*)km::k_fp3_window<T, A>, dim3(fp3c_blocks), dim3(km::FP3_THREADS),
+        KM_CK(cudaLaunchCooperativeKernel((void*)km::k_fp3_window<T, A, false>, dim3(fp3c_blocks), dim3(km::FP3_THREADS),
                                           args, km::FP3_SMEM, st));
         ++launches;
         KM_CK(cudaMemcpyAsync(h_f3ctl, f3_ctl, sizeof(km::Fp3Ctl), cudaMemcpyDeviceToHost, st));
@@ -1069,6 +1078,7 @@ struct Impl : ImplBase {
     // One pass of Alg.4's scan (or its remainder up to the stop, F2).
     km_status swap_iter_fp3(int32_t* swaps_out, void* td_out) {
         fp1_prepped = false;
+        inc_valid = false;
         if (fp3_mode < 0) {
             const char* e = getenv("KM_FASTER");
             fp3_mode = (e && strcmp(e, "batch") == 0) ? 0 : 1;
@@ -1135,6 +1145,105 @@ struct Impl : ImplBase {
                     fp3_tphase[1] * 1e-6, fp3_tphase[2] * 1e-6, fp3_tphase[4] * 1e-6, fp3_tphase[5] * 1e-6,
                     fp3_tphase[6] * 1e-6, fp3_stat[0], fp3_stat[1], fp3_stat[2], fp3_host_ms);
         return (fp3_t - fp3_tlast >= n) ? KM_CONVERGED : KM_OK;
+    }
+
+    // ---- incremental FastPAM1 (KM_FASTPAM1_INC; km_fasterpam.cuh GLOBAL mode) ---
+    // The complete k-vectors of every candidate (acc[i][c], plus[c]) come from
+    // one FastPAM2-mode stream; every iteration then takes Alg.3's best swap
+    // over all candidates (key R1) from them and corrects them for the objects
+    // whose (nearest, d_n, d_s) changed -- the same swaps as the streaming
+    // FastPAM1 (bit-exact on u32), reading the changed rows instead of D.
+    bool inc_valid = false;
+    int64_t inc_restreams = 0;
+    unsigned long long inc_tphase[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    long long inc_stat[3] = {0, 0, 0};
+    A *inc_pacc = nullptr, *inc_pplus = nullptr, *inc_pR = nullptr;
+    Rec* inc_gpart = nullptr;
+    Rec* inc_trace = nullptr;
+    int inc_trace_cap = 0;
+
+    km_status inc_alloc() {
+        if (inc_pacc) return KM_OK;
+        KM_TRY(fp2_alloc());
+        KM_TRY(fp3_alloc());
+        KM_TRY(fp3c_alloc());
+        const int64_t nwarps = (int64_t)fp3c_blocks * km::FP3_WARPS;
+        const int64_t G = std::min<int64_t>(km::FP3_G, std::max<int64_t>(1, nwarps / cdiv(w, 32)));
+        KM_TRY(alloc(&inc_pacc, (size_t)G * km::FP3_TMAX * w));
+        KM_TRY(alloc(&inc_pplus, (size_t)G * w));
+        KM_TRY(alloc(&inc_pR, (size_t)km::FP3_G * km::FP3_TMAX));
+        KM_TRY(alloc(&inc_gpart, fp3c_blocks));
+        inc_trace_cap = 4096;
+        KM_TRY(alloc(&inc_trace, inc_trace_cap));
+        return KM_OK;
+    }
+
+    km_status inc_iters(int32_t max_iters, int32_t* swaps_out, void* td_out, int32_t* iters_out,
+                        bool* conv_out) override {
+        if (sharded) return fail(KM_EINVAL, "incremental FastPAM1 on a sharded handle");
+        if (!ready) return fail(KM_EINVAL, "no medoids: call kmedoids_set_medoids or kmedoids_init_build first");
+        KM_TRY(inc_alloc());
+        fp1_prepped = false;
+        last_swaps.clear();
+        int done_iters = 0, done_swaps = 0;
+        bool conv = false;
+        while (done_iters < max_iters && !conv) {
+            if (!inc_valid) {                         // exact k-vectors of the current state
+                KM_CK(cudaMemsetAsync(fp2_acc, 0, (size_t)k * w * sizeof(A), st));
+                KM_TRY(fp2_eval_local());
+                KM_TRY(fp2_finish_profiling());
+                km::k_fp3_transpose_mc<T><<<dim3((unsigned)cdiv(n, 32), (unsigned)cdiv(k, 32)), dim3(32, 8), 0, st>>>(
+                    MC, (int)n, k, f3_mct);
+                KM_CKL();
+                inc_valid = true;
+            }
+            km::Fp3Ctl hc;
+            memset(&hc, 0, sizeof(hc));
+            hc.first[0] = hc.first[1] = hc.first[2] = INT_MAX;
+            *h_f3ctl = hc;
+            KM_CK(cudaMemcpyAsync(f3_ctl, h_f3ctl, sizeof(hc), cudaMemcpyHostToDevice, st));
+            km::Fp3Args<T, A> g;
+            g.D = D; g.ld = ld; g.n = (int)n; g.k = k; g.c0 = c0; g.a = 0; g.ww = w;
+            g.lo = 0; g.hi = w; g.L = w;
+            g.acc = fp2_acc; g.plus = fp2_plus; g.R = R; g.M = M; g.point_slot = point_slot; g.MC = MC; g.MCt = f3_mct;
+            g.near = near; g.sec = sec; g.dn = dn; g.ds = ds; g.td = td; g.dec = dec;
+            g.trace = inc_trace; g.trace_cap = inc_trace_cap;
+            g.cand_v = f3_v; g.cand_s = f3_s; g.flag = f3_flag; g.old_near = f3_oldnear; g.old_dn = f3_olddn;
+            g.old_ds = f3_oldds; g.rescan = f3_rescan; g.blk_cnt = f3_blk; g.chg = f3_chg; g.chg_cap = (int)n;
+            g.touched_flag = f3_tflag; g.touched_map = f3_tmap; g.touched = f3_tlist;
+            g.part_acc = inc_pacc; g.part_plus = inc_pplus; g.part_R = inc_pR; g.ctl = f3_ctl; g.new_pass = 0;
+            g.max_iters = max_iters - done_iters; g.gpart = inc_gpart;
+            void* args[] = {&g};
+            KM_CK(cudaLaunchCooperativeKernel((void*)km::k_fp3_window<T, A, true>, dim3(fp3c_blocks),
+                                              dim3(km::FP3_THREADS), args, km::FP3_SMEM, st));
+            ++launches;
+            KM_CK(cudaMemcpyAsync(h_f3ctl, f3_ctl, sizeof(km::Fp3Ctl), cudaMemcpyDeviceToHost, st));
+            KM_TRY(sync_dec());
+            const km::Fp3Ctl r = *h_f3ctl;
+            if (r.swaps > 0) {
+                std::vector<Rec> tr((size_t)std::min(r.swaps, inc_trace_cap));
+                KM_CK(cudaMemcpy(tr.data(), inc_trace, tr.size() * sizeof(Rec), cudaMemcpyDeviceToHost));
+                for (const Rec& x : tr) last_swaps.push_back(x);
+            }
+            done_swaps += r.swaps;
+            done_iters += r.pad[4];
+            conv = r.pad[3] != 0;
+            if (r.status == km::FP3_STALE) { inc_valid = false; ++inc_restreams; }   // re-stream next
+            for (int q = 0; q < 8; ++q) inc_tphase[q] += r.tphase[q];
+            for (int q = 0; q < 3; ++q) inc_stat[q] += r.pad[q];
+        }
+        const char* ep = getenv("KM_FASTER_PROF");
+        if (ep && ep[0] == '1')
+            fprintf(stderr, "[fastpam1_inc] iters %d swaps %d restreams %lld | ms pick %.2f apply %.2f rescan %.2f "
+                    "compact %.2f correct %.2f fold %.2f | sum nres %lld m %lld T %lld\n", done_iters, done_swaps,
+                    (long long)inc_restreams, inc_tphase[0] * 1e-6, inc_tphase[1] * 1e-6, inc_tphase[2] * 1e-6,
+                    inc_tphase[4] * 1e-6, inc_tphase[5] * 1e-6, inc_tphase[6] * 1e-6, inc_stat[0], inc_stat[1],
+                    inc_stat[2]);
+        if (swaps_out) *swaps_out = done_swaps;
+        if (iters_out) *iters_out = done_iters;
+        if (conv_out) *conv_out = conv;
+        copy_td(td_out);
+        return conv ? KM_CONVERGED : KM_OK;
     }
 
     // ---- sharded FastPAM2 ------------------------------------------------------
@@ -1443,6 +1552,7 @@ struct Impl : ImplBase {
             ready = true;
             fp3_reset();
             fp1_prepped = false;
+            inc_valid = false;
         }
         KM_TRY(reset_counters());
         return KM_OK;
@@ -1608,6 +1718,7 @@ struct Impl : ImplBase {
         ready = true;
         fp3_reset();
         fp1_prepped = false;
+        inc_valid = false;
         return KM_OK;
     }
 
@@ -1780,6 +1891,13 @@ km_status kmedoids_run(km_handle* h, int32_t use_build, km_variant variant, int3
     if (max_iter <= 0) max_iter = 2000;
     if (use_build) KM_TRY(h->impl->init_build(nullptr, nullptr));
     km_status st = KM_NOT_CONVERGED;
+    if (variant == KM_FASTPAM1_INC) {              // all iterations in cooperative launches
+        bool conv = false;
+        const km_status s = h->impl->inc_iters(max_iter, nullptr, nullptr, nullptr, &conv);
+        if (s != KM_OK && s != KM_CONVERGED) return s;
+        KM_TRY(h->impl->get_state(medoids_out, assignment_out, td_out, n_iter_out, n_swaps_out));
+        return conv ? KM_OK : KM_NOT_CONVERGED;
+    }
     for (int it = 0; it < max_iter; ++it) {
         km_status s = h->impl->swap_iter(variant, nullptr, nullptr);
         if (s == KM_CONVERGED) { st = KM_OK; break; }

@@ -24,8 +24,9 @@ LIB_PATH = os.path.join(_HERE, "libkmedoids.so")
 KM_OK, KM_CONVERGED, KM_NOT_CONVERGED = 0, 1, 2
 KM_EINVAL, KM_ENOMEM, KM_ECUDA, KM_ECOMM = 10, 11, 12, 13
 KM_U32, KM_F32 = 0, 1
-KM_FASTPAM1, KM_FASTPAM2, KM_FASTERPAM = 0, 1, 2
-VARIANTS = {"fastpam1": KM_FASTPAM1, "fastpam2": KM_FASTPAM2, "fasterpam": KM_FASTERPAM}
+KM_FASTPAM1, KM_FASTPAM2, KM_FASTERPAM, KM_FASTPAM1_INC = 0, 1, 2, 3
+VARIANTS = {"fastpam1": KM_FASTPAM1, "fastpam2": KM_FASTPAM2, "fasterpam": KM_FASTERPAM,
+            "fastpam1_inc": KM_FASTPAM1_INC}
 
 
 class KMError(RuntimeError):
