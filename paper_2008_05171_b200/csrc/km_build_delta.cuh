@@ -32,7 +32,8 @@ template <typename T, typename A>
 __global__ void __launch_bounds__(BD_CHUNK_THREADS)
 k_build_dn_delta(const T* __restrict__ D, int64_t ld, int n, int64_t col_begin, const Decision<A>* __restrict__ dec,
                  T* __restrict__ MC, const int* __restrict__ point_slot, T* __restrict__ dn,
-                 T* __restrict__ dn_old, int* __restrict__ flag, int chunk, int* __restrict__ cnt) {
+                 T* __restrict__ dn_old, int* __restrict__ flag, int chunk, int* __restrict__ cnt,
+                 int from_mc /* sharded: the column is already in MC (broadcast) */) {
     const int step = dec->slot;
     const int64_t c = dec->c;
     const int o0 = min(n, (int)blockIdx.x * chunk), o1 = min(n, o0 + chunk);
@@ -41,8 +42,9 @@ k_build_dn_delta(const T* __restrict__ D, int64_t ld, int n, int64_t col_begin, 
         const int o = ob + threadIdx.x;
         int f = 0;
         if (o < o1) {
-            const T x = D[(int64_t)o * ld + (c - col_begin)];
-            MC[(int64_t)step * n + o] = x;
+            T x;
+            if (from_mc) x = MC[(int64_t)step * n + o];
+            else { x = D[(int64_t)o * ld + (c - col_begin)]; MC[(int64_t)step * n + o] = x; }
             const T old = dn[o];
             const T nw = point_slot[o] >= 0 ? (T)0 : (x < old ? x : old);
             if (nw != old) { f = 1; dn_old[o] = old; dn[o] = nw; }

@@ -1530,6 +1530,10 @@ struct Impl : ImplBase {
 
     km_status build_eval(int32_t step) override {
         if (step < 0 || step >= k) return fail(KM_EINVAL, "build step %d out of range", step);
+        if (sharded) {                             // the sharded BUILD is incremental too (own slab's gains)
+            KM_TRY(bd_init());
+            if (bd_mode == 1 && step >= 1) return bd_eval(step);
+        }
         if (build_tma) return step == 0 ? launch_build_tma<0>() : launch_build_tma<1>();
         dim3 g((unsigned)cdiv(w, STREAM_COLS), Pb);
         if (step == 0) {
@@ -1606,14 +1610,33 @@ struct Impl : ImplBase {
         return KM_OK;
     }
 
-    km_status init_build(int32_t* M_out, void* td_out) override {
-        if (sharded) return fail(KM_EINVAL, "init_build on a sharded handle; use kmedoids_build_* phases");
+    km_status bd_init() {
         if (bd_mode < 0) {
             const char* e = getenv("KM_BUILD");
             bd_mode = (e && (strcmp(e, "full") == 0 || strcmp(e, "ldg") == 0)) ? 0 : 1;
             if (!build_tma) bd_mode = 0;
         }
         if (bd_mode == 1) KM_TRY(bd_alloc());
+        return KM_OK;
+    }
+
+    // changed-object list of the step just applied (its column is in MC)
+    km_status bd_changed_list(int from_mc) {
+        km::k_build_dn_delta<T, A><<<bd_B, km::BD_CHUNK_THREADS, 0, st>>>(
+            D, ld, (int)n, c0, dec, MC, point_slot, dn, bd_dnold, bd_flag, bd_chunk, bd_cnt, from_mc);
+        KM_CKL();
+        km::k_chunk_scan<<<1, 1024, 0, st>>>(bd_cnt, bd_B, bd_off, bd_m);
+        KM_CKL();
+        km::k_changed_scatter<T><<<bd_B, km::BD_CHUNK_THREADS, 0, st>>>(
+            (int)n, bd_flag, bd_dnold, dn, bd_chunk, bd_off, bd_lo, bd_lold, bd_lnew);
+        KM_CKL();
+        launches += 3;
+        return KM_OK;
+    }
+
+    km_status init_build(int32_t* M_out, void* td_out) override {
+        if (sharded) return fail(KM_EINVAL, "init_build on a sharded handle; use kmedoids_build_* phases");
+        KM_TRY(bd_init());
         KM_CK(cudaMemsetAsync(point_slot, 0xff, n * sizeof(int), st));
         ready = false;
         const int nb = (int)cdiv(n, 256);
@@ -1624,15 +1647,7 @@ struct Impl : ImplBase {
             KM_CKL();
             if (bd_mode == 1 && step >= 1) {
                 if (step + 1 < k) {
-                    km::k_build_dn_delta<T, A><<<bd_B, km::BD_CHUNK_THREADS, 0, st>>>(
-                        D, ld, (int)n, c0, dec, MC, point_slot, dn, bd_dnold, bd_flag, bd_chunk, bd_cnt);
-                    KM_CKL();
-                    km::k_chunk_scan<<<1, 1024, 0, st>>>(bd_cnt, bd_B, bd_off, bd_m);
-                    KM_CKL();
-                    km::k_changed_scatter<T><<<bd_B, km::BD_CHUNK_THREADS, 0, st>>>(
-                        (int)n, bd_flag, bd_dnold, dn, bd_chunk, bd_off, bd_lo, bd_lold, bd_lnew);
-                    KM_CKL();
-                    launches += 3;
+                    KM_TRY(bd_changed_list(0));
                 } else {                                 // last step: only MC is needed
                     km::k_gather_decided_col<T, A><<<nb, 256, 0, st>>>(D, ld, (int)n, c0, c1, dec, MC, nullptr);
                     KM_CKL();
@@ -1785,8 +1800,12 @@ struct Impl : ImplBase {
         const int nb = (int)cdiv(n, 256);
         km::k_column_to_mc<T, A><<<nb, 256, 0, st>>>(colbuf, (int)n, dec, MC);
         KM_CKL();
-        km::k_build_dn<T, A><<<nb, 256, 0, st>>>(MC, (int)n, dec, point_slot, dn);
-        KM_CKL();
+        if (bd_mode == 1 && step >= 1) {
+            if (step + 1 < k) KM_TRY(bd_changed_list(1));   // column from MC (broadcast)
+        } else {
+            km::k_build_dn<T, A><<<nb, 256, 0, st>>>(MC, (int)n, dec, point_slot, dn);
+            KM_CKL();
+        }
         build_step = step + 1;
         if (step == k - 1) {
             KM_TRY(build_finish());
