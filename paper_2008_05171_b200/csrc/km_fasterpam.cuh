@@ -501,8 +501,12 @@ k_fp3_window(Fp3Args<T, A> g) {
 #pragma unroll
                         for (int v8 = 0; v8 < 16; ++v8) {
                             const int src = (e8 + v8) & 31;
-                            const T a_dno = __shfl_sync(FULL, dno, src), a_dso = __shfl_sync(FULL, dso, src);
-                            const T a_dnn = __shfl_sync(FULL, dnn, src), a_dsn = __shfl_sync(FULL, dsn, src);
+                            const T a_dso = __shfl_sync(FULL, dso, src), a_dsn = __shfl_sync(FULL, dsn, src);
+                            // a term is non-zero only where d < d_s (old or new): most (o, c)
+                            // pairs miss both, and the warp skips them together
+                            const bool any_hit = __any_sync(FULL, act && (x[v8] < a_dso || x[v8] < a_dsn));
+                            if (!any_hit && u != 0) continue;  // u == 0 items also carry the R deltas
+                            const T a_dno = __shfl_sync(FULL, dno, src), a_dnn = __shfl_sync(FULL, dnn, src);
                             const int a_to = __shfl_sync(FULL, to_l, src), a_tn = __shfl_sync(FULL, tn_l, src);
                             if (e8 + v8 < nb) {
                                 A tpo, tao, tpn, tan_;

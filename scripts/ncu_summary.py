@@ -24,7 +24,9 @@ def launches(path, out):
         agg[name][0] += 1
         agg[name][1] += float(r[iv].replace(",", "")) * scale.get(r[iu], 1.0)
     tot = sum(v for _, v in agg.values())
-    swap = [k for k in agg if k.startswith("km::") and "build" not in k and k not in ("km::k_assign_full", "km::k_td_from_dn")]
+    init_only = ("km::k_assign_full", "km::k_td_from_dn", "km::k_chunk_scan", "km::k_gather_medoid_cols")
+    swap = [k for k in agg if k.startswith("km::") and "build" not in k and "changed_scatter" not in k
+            and not k.startswith(init_only)]
     swap_tot = sum(agg[k][1] for k in swap)
     with open(out, "w") as f:
         f.write(f"# ncu launch list summary: `{path}`\n\n")
