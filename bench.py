@@ -281,6 +281,8 @@ def run_ours(args):
     alg_bytes = 4.0 * n * (n - k)
     k1_avg = k1_ms / max(1, k1_launches)
     achieved = alg_bytes / (k1_avg / 1e3) / 1e9
+    # a read-only stream over the same D in the same job (a second denominator)
+    read_peak = kmsynth.read_peak_gbs(Dt, reps=5, stream=stream)
 
     # CPU oracle baseline on the state of the first timed iteration (rank 0, N=1 only)
     cpu = None
@@ -391,7 +393,9 @@ def run_ours(args):
                      "kernel": {"seg": "k_swap_stream_seg"}.get(os.environ.get("KM_STREAM", ""), "k_swap_stream_seg2")
                      if not os.environ.get("KM_STREAM") or os.environ.get("KM_STREAM") in ("seg", "seg2")
                      else os.environ["KM_STREAM"], "kernel_ms": k1_avg,
-                     "alg_bytes_per_launch": alg_bytes, "peak_kind": peak_kind},
+                     "alg_bytes_per_launch": alg_bytes, "peak_kind": peak_kind,
+                     "read_only_peak_same_job": read_peak, "frac_of_read_only_peak": achieved / read_peak,
+                     "frac_of_nominal_7700": achieved / 7700.0},
         "stream_share_of_step": k1_ms / total_ms,
         "gpu_launches": launches,
         "clocks": clk.summary(),

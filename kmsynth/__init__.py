@@ -207,3 +207,18 @@ def as_numpy_D(t) -> np.ndarray:
     """Host numpy view of a dist_cuda tensor with the right element type."""
     a = t.cpu().numpy()
     return a.view(np.uint32) if a.dtype == np.int32 else a
+
+
+def read_peak_gbs(t, reps: int = 5, stream=None) -> float:
+    """Read-only HBM bandwidth (GB/s, best of reps) over the bytes of the CUDA tensor t
+    (measurement helper for bench.py's roofline; not part of the method)."""
+    import torch
+    global _lib
+    if _lib is None:
+        _lib = ctypes.CDLL(build_lib())
+    f = _lib.kmsynth_read_peak
+    f.restype = ctypes.c_double
+    f.argtypes = [ctypes.c_void_p, ctypes.c_int64, ctypes.c_int, ctypes.c_void_p]
+    st = stream if stream is not None else torch.cuda.current_stream(t.device)
+    return float(f(ctypes.c_void_p(t.data_ptr()), int(t.numel() * t.element_size()) // 16 * 16, int(reps),
+                   ctypes.c_void_p(st.cuda_stream)))

@@ -70,3 +70,57 @@ extern "C" int kmsynth_dist(const void* pts_dev, int metric, int n, int d, int64
     else k_dist<1, double><<<grd, blk, 0, st>>>((const double*)pts_dev, n, d, c0, c1, ld, out_dev);
     return (int)cudaGetLastError();
 }
+
+// ---------------------------------------------------------------------------
+// Measurement helper (bench.py): the read-only HBM bandwidth of this GPU in the
+// same job -- a grid-stride 128-bit load stream over `bytes` of a buffer,
+// XOR-folded into one word so the loads cannot be removed.  Not part of the
+// method; a denominator for the stream kernel's roofline besides the copy peak.
+// ---------------------------------------------------------------------------
+namespace {
+__global__ void k_read_stream(const uint4* __restrict__ p, int64_t n16, unsigned* __restrict__ sink) {
+    uint4 acc = make_uint4(0, 0, 0, 0);
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    for (; i + 3 * stride < n16; i += 4 * stride) {
+        uint4 a, b, c, e;
+        asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];" : "=r"(a.x), "=r"(a.y), "=r"(a.z), "=r"(a.w) : "l"(p + i));
+        asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];" : "=r"(b.x), "=r"(b.y), "=r"(b.z), "=r"(b.w) : "l"(p + i + stride));
+        asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];" : "=r"(c.x), "=r"(c.y), "=r"(c.z), "=r"(c.w) : "l"(p + i + 2 * stride));
+        asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];" : "=r"(e.x), "=r"(e.y), "=r"(e.z), "=r"(e.w) : "l"(p + i + 3 * stride));
+        acc.x ^= a.x ^ b.x ^ c.x ^ e.x; acc.y ^= a.y ^ b.y ^ c.y ^ e.y;
+        acc.z ^= a.z ^ b.z ^ c.z ^ e.z; acc.w ^= a.w ^ b.w ^ c.w ^ e.w;
+    }
+    for (; i < n16; i += stride) { const uint4 a = p[i]; acc.x ^= a.x; acc.y ^= a.y; acc.z ^= a.z; acc.w ^= a.w; }
+    const unsigned v = acc.x ^ acc.y ^ acc.z ^ acc.w;
+    if (v == 0x9e3779b9u) atomicXor(sink, v);   // practically never taken; keeps the loads alive
+}
+}  // namespace
+
+// Best of `reps` timed passes (CUDA events); returns GB/s (read bytes / time).
+extern "C" double kmsynth_read_peak(const void* buf, int64_t bytes, int reps, void* stream) {
+    cudaStream_t st = (cudaStream_t)stream;
+    unsigned* sink = nullptr;
+    if (cudaMalloc(&sink, sizeof(unsigned)) != cudaSuccess) return -1.0;
+    int dev = 0, nsm = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+    const int64_t n16 = bytes / 16;
+    cudaEvent_t a, b;
+    cudaEventCreate(&a); cudaEventCreate(&b);
+    k_read_stream<<<nsm * 8, 256, 0, st>>>((const uint4*)buf, n16, sink);     // warm-up
+    double best = 0.0;
+    for (int r = 0; r < reps; ++r) {
+        cudaEventRecord(a, st);
+        k_read_stream<<<nsm * 8, 256, 0, st>>>((const uint4*)buf, n16, sink);
+        cudaEventRecord(b, st);
+        cudaEventSynchronize(b);
+        float ms = 0.f;
+        cudaEventElapsedTime(&ms, a, b);
+        const double gbs = (double)n16 * 16 / (ms * 1e-3) / 1e9;
+        if (gbs > best) best = gbs;
+    }
+    cudaEventDestroy(a); cudaEventDestroy(b);
+    cudaFree(sink);
+    return best;
+}
