@@ -116,7 +116,7 @@ k_build_delta_tma(const T* __restrict__ D, int64_t ld, int w, int wpad, int P, c
     uint64_t* empty = full + S;
     const int m = *m_dev;
     const int q = blockIdx.y;
-    const int64_t p0 = (int64_t)q * m / P, p1 = (int64_t)(q + 1) * m / P;
+    const int64_t p0 = part_lo_uniform(q, m, P), p1 = part_lo_uniform(q + 1, m, P);   // a few changed rows: no tilt
     const int nstages = (int)((p1 - p0 + RB - 1) / RB);
     const int ctacol = blockIdx.x * C::COLS;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;

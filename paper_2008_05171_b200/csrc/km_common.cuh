@@ -73,4 +73,17 @@ template <typename A> struct alignas(16) Decision {
     int32_t swaps;   // swaps so far
 };
 
+// Row parts of the SWAP / BUILD streams: part q of P covers slot-sorted
+// positions [part_lo(q), part_lo(q + 1)).  The sizes tilt linearly from
+// (1 + a) n/P (first part) to (1 - a) n/P (last), a = c_part_skew / 16:
+// blocks are dispatched part-major, so the last wave of a bandwidth-bound
+// stream holds its smallest CTAs and the tail in which SMs fall idle is
+// shorter.  a = 0 gives the uniform split q*n/P.
+__constant__ int c_part_skew;
+__device__ __forceinline__ int64_t part_lo(int q, int64_t n, int P) {
+    const int64_t a = c_part_skew, PP = P;
+    return (int64_t)q * n * ((16 + a) * PP - a * q) / (16 * PP * PP);
+}
+__device__ __forceinline__ int64_t part_lo_uniform(int q, int64_t n, int P) { return (int64_t)q * n / P; }
+
 }  // namespace km

@@ -396,14 +396,14 @@ __global__ void k_removal_loss(const RowInfo<T>* __restrict__ ri, const int* __r
     }
 }
 
-// Row parts of the stream: part q covers sorted positions [q*n/P, (q+1)*n/P);
+// Row parts of the stream: part q covers sorted positions [part_lo(q), part_lo(q+1));
 // head/tail slot = slot of its first/last row.
 template <typename T>
 __global__ void k_part_meta(const RowInfo<T>* __restrict__ ri, int n, int P, int* __restrict__ head_slot,
                             int* __restrict__ tail_slot) {
     const int q = blockIdx.x * blockDim.x + threadIdx.x;
     if (q >= P) return;
-    const int64_t p0 = (int64_t)q * n / P, p1 = (int64_t)(q + 1) * n / P;
+    const int64_t p0 = part_lo(q, n, P), p1 = part_lo(q + 1, n, P);
     head_slot[q] = ri[p0].slot;
     tail_slot[q] = ri[p1 - 1].slot;
 }
@@ -433,7 +433,7 @@ k_swap_stream(const T* __restrict__ D, int64_t ld, int w, int n, int P,
               A* __restrict__ out_imin, int* __restrict__ out_islot) {
     using V = typename Vec4<T>::type;
     const int q = blockIdx.y;
-    const int64_t p0 = (int64_t)q * n / P, p1 = (int64_t)(q + 1) * n / P;
+    const int64_t p0 = part_lo(q, n, P), p1 = part_lo(q + 1, n, P);
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int cb = (blockIdx.x * WARPS + warp) * 128 + lane * 4;
     const bool active = cb < w;
@@ -715,7 +715,7 @@ k_swap_stream_tma(const T* __restrict__ D, int64_t ld, int w, int wpad, int n, i
     uint64_t* empty = full + S;
 
     const int q = blockIdx.y;
-    const int64_t p0 = (int64_t)q * n / P, p1 = (int64_t)(q + 1) * n / P;
+    const int64_t p0 = part_lo(q, n, P), p1 = part_lo(q + 1, n, P);
     const int nstages = (int)((p1 - p0 + RB - 1) / RB);
     const int ctacol = blockIdx.x * C::COLS;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -844,7 +844,7 @@ k_swap_stream_wtma(const T* __restrict__ D, int64_t ld, int w, int wpad, int n, 
     uint64_t* full = reinterpret_cast<uint64_t*>(wbase + S * RB * (C::ROWB + 16));
 
     const int q = blockIdx.y;
-    const int64_t p0 = (int64_t)q * n / P, p1 = (int64_t)(q + 1) * n / P;
+    const int64_t p0 = part_lo(q, n, P), p1 = part_lo(q + 1, n, P);
     const int nstages = (int)((p1 - p0 + RB - 1) / RB);
     const int cw = (blockIdx.x * NW + warp) * 128;          // first column of this warp
     if (cw >= w) return;                                     // no warp-collective op spans warps
@@ -994,7 +994,7 @@ k_swap_stream_cmp(const T* __restrict__ D, int64_t ld, int w, int wpad, int n, i
     int* hitcnt = hits + C::COLS;
 
     const int q = blockIdx.y;
-    const int64_t p0 = (int64_t)q * n / P, p1 = (int64_t)(q + 1) * n / P;
+    const int64_t p0 = part_lo(q, n, P), p1 = part_lo(q + 1, n, P);
     const int nstages = (int)((p1 - p0 + RB - 1) / RB);
     const int ctacol = blockIdx.x * C::COLS;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -1222,7 +1222,7 @@ k_swap_stream_tmaq(const T* __restrict__ D, int64_t ld, int w, int wpad, int n, 
     int* queue = reinterpret_cast<int*>(smem + C::DATAB + C::RIB + C::BARB + C::ACCB);
 
     const int q = blockIdx.y;
-    const int64_t p0 = (int64_t)q * n / P, p1 = (int64_t)(q + 1) * n / P;
+    const int64_t p0 = part_lo(q, n, P), p1 = part_lo(q + 1, n, P);
     const int nstages = (int)((p1 - p0 + RB - 1) / RB);
     const int ctacol = blockIdx.x * C::COLS;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -1473,7 +1473,7 @@ k_swap_stream_seg(const T* __restrict__ D, int64_t ld, int w, int wpad, int n, i
     uint64_t* empty = full + S;
 
     const int q = blockIdx.y;
-    const int64_t p0 = (int64_t)q * n / P, p1 = (int64_t)(q + 1) * n / P;
+    const int64_t p0 = part_lo(q, n, P), p1 = part_lo(q + 1, n, P);
     const int ctacol = blockIdx.x * C::COLS;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 
@@ -1691,7 +1691,7 @@ k_swap_stream_seg2(const T* __restrict__ D, int64_t ld, int w, int wpad, int n, 
     uint64_t* empty = full + S;
 
     const int q = blockIdx.y;
-    const int64_t p0 = (int64_t)q * n / P, p1 = (int64_t)(q + 1) * n / P;
+    const int64_t p0 = part_lo(q, n, P), p1 = part_lo(q + 1, n, P);
     const int ctacol = blockIdx.x * C::COLS;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 
@@ -2296,7 +2296,7 @@ k_build_stream(const T* __restrict__ D, int64_t ld, int w, int n, int P, const T
                A* __restrict__ out) {
     using V = typename Vec4<T>::type;
     const int q = blockIdx.y;
-    const int64_t p0 = (int64_t)q * n / P, p1 = (int64_t)(q + 1) * n / P;
+    const int64_t p0 = part_lo(q, n, P), p1 = part_lo(q + 1, n, P);
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int cb = (blockIdx.x * WARPS + warp) * 128 + lane * 4;
     if (cb >= w) return;                      // no warp-collective ops below
@@ -2352,7 +2352,7 @@ k_build_tma(const T* __restrict__ D, int64_t ld, int w, int wpad, int n, int P, 
     uint64_t* full = reinterpret_cast<uint64_t*>(smem + C::DATAB);
     uint64_t* empty = full + S;
     const int q = blockIdx.y;
-    const int64_t p0 = (int64_t)q * n / P, p1 = (int64_t)(q + 1) * n / P;
+    const int64_t p0 = part_lo(q, n, P), p1 = part_lo(q + 1, n, P);
     const int nstages = (int)((p1 - p0 + RB - 1) / RB);
     const int ctacol = blockIdx.x * C::COLS;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;

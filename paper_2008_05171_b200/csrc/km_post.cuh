@@ -265,7 +265,7 @@ k_fp1_post(PostArgs<T, A> g) {
         }
     }
     for (int q = tid; q < g.P; q += nth) {
-        const int64_t p0 = (int64_t)q * n / g.P, p1 = (int64_t)(q + 1) * n / g.P;
+        const int64_t p0 = part_lo(q, n, g.P), p1 = part_lo(q + 1, n, g.P);
         g.head_slot[q] = post_ld_ri(&g.ri[p0]).slot;
         g.tail_slot[q] = post_ld_ri(&g.ri[p1 - 1]).slot;
     }

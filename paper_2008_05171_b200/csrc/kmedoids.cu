@@ -103,6 +103,8 @@ int choose_parts(int64_t n, int64_t w, int cols_per_cta, int resident) {
 // rows per part, but between 3 and 8 waves of resident CTAs (3 per SM) --
 // more, shorter CTAs balance the Poisson-lumpy hit work across SMs; very
 // short parts cost ring fill/drain and combine bytes.
+constexpr int PART_SKEW_DEFAULT = 15;  // 16ths; see km::part_lo (C4 stream 1.565 -> 1.478 ms)
+
 int choose_parts_seg(int64_t n, int64_t w) {
     const int64_t ncb = cdiv(w, SG_NC * 128);
     const int64_t slots = (int64_t)NUM_SMS * SG_MINB;
@@ -283,6 +285,13 @@ struct Impl : ImplBase {
                                : choose_parts(n, w, STREAM_COLS, RESIDENT_CTAS);
         const char* ep = getenv("KM_PARTS");          // measurement override of the stream's row parts
         if (ep && atoi(ep) > 0) P = std::min<int>(atoi(ep), (int)std::max<int64_t>(1, n / 64));
+        {
+            // part-size tilt of the streams (km_common.cuh part_lo); one value
+            // per process (a __constant__ of this device), KM_PART_SKEW in 16ths
+            int skew = PART_SKEW_DEFAULT;
+            if (const char* es = getenv("KM_PART_SKEW")) skew = std::min(15, std::max(0, atoi(es)));
+            KM_CK(cudaMemcpyToSymbol(km::c_part_skew, &skew, sizeof(int)));
+        }
         Pb = choose_parts(n, w, STREAM_COLS, RESIDENT_CTAS);
         Pbt = choose_parts(n, w, SG_NC * 128, SG_MINB);
         const char* eb = getenv("KM_BUILD");
