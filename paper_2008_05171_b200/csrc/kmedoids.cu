@@ -8,6 +8,7 @@
 #include <cstdio>
 #include <cstring>
 #include <memory>
+#include <mutex>
 #include <string>
 #include <algorithm>
 #include <chrono>
@@ -2001,6 +2002,37 @@ km_status kmedoids_stream_time(km_handle* h, double* ms_out, int64_t* launches_o
     return KM_OK;
 }
 
+namespace {
+std::mutex g_dist_mu;
+struct DistScratch { void* p = nullptr; size_t bytes = 0; cudaEvent_t done = nullptr; };
+DistScratch g_dist_scr[64];
+// Grow-only scratch of device dev; a larger request waits for the stream
+// (earlier launches may still read the old buffer) before replacing it.
+cudaError_t dist_scratch(int dev, size_t bytes, cudaStream_t st, float** out) {
+    if (dev < 0 || dev >= 64) return cudaErrorInvalidDevice;
+    DistScratch& s = g_dist_scr[dev];
+    if (s.bytes < bytes) {
+        cudaError_t e = cudaStreamSynchronize(st);
+        if (e != cudaSuccess) return e;
+        if (s.p) cudaFree(s.p);
+        s.p = nullptr; s.bytes = 0;
+        e = cudaMalloc(&s.p, bytes);
+        if (e != cudaSuccess) { cudaGetLastError(); return e; }
+        s.bytes = bytes;
+    }
+    if (!s.done) {
+        cudaError_t e = cudaEventCreateWithFlags(&s.done, cudaEventDisableTiming);
+        if (e != cudaSuccess) return e;
+    } else {
+        // a call on another stream may still use the scratch
+        cudaError_t e = cudaStreamWaitEvent(st, s.done, 0);
+        if (e != cudaSuccess) return e;
+    }
+    *out = (float*)s.p;
+    return cudaSuccess;
+}
+}  // namespace
+
 km_status kmedoids_dissimilarity(const void* X, km_metric metric, int64_t n, int32_t d, void* D, int64_t ld,
                                  int64_t col_begin, int64_t col_end, void* cuda_stream) {
     g_err.clear();
@@ -2021,6 +2053,7 @@ km_status kmedoids_dissimilarity(const void* X, km_metric metric, int64_t n, int
         cudaGetDevice(&dev);
         cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
         cudaDeviceGetAttribute(&smax, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+        std::lock_guard<std::mutex> lock(g_dist_mu);   // one scratch per device
         const char* ek = getenv("KM_DIST_KERNEL");     // "simple": the single-role kernel
         const bool ws = !(ek && strcmp(ek, "simple") == 0) && km::dw_smem_bytes(dpad, 1) <= (size_t)smax;
         int wstage = 1;                                 // measured: a second staging buffer is slower (L1 carve-out)
@@ -2030,8 +2063,11 @@ km_status kmedoids_dissimilarity(const void* X, km_metric metric, int64_t n, int
         const int64_t TF = ws ? km::dw_tile_floats(dpad) : km::dt_tile_floats(dpad);
         const size_t nrm_floats = (size_t)cdiv(n, 64) * 64;          // keeps the packed tiles 256-byte aligned
         const size_t scratch = nrm_floats + (size_t)nm * TF + (same ? 0 : (size_t)ntc * TF);
+        // persistent per-device scratch (norms + packed operands), grown on
+        // demand: a stream-ordered allocation per call pays the pool's page
+        // mapping again whenever the pool was trimmed at a synchronisation
         float* nrm = nullptr;
-        cudaError_t e = cudaMallocAsync((void**)&nrm, scratch * sizeof(float), st);
+        cudaError_t e = dist_scratch(dev, scratch * sizeof(float), st, &nrm);
         if (e != cudaSuccess) return fail(KM_ENOMEM, "dissimilarity scratch: %s", cudaGetErrorString(e));
         float* PA = nrm + nrm_floats;
         float* PB = same ? PA : PA + nm * TF;
@@ -2047,7 +2083,7 @@ km_status kmedoids_dissimilarity(const void* X, km_metric metric, int64_t n, int
                 void* fn = nullptr;
                 cudaDriverEntryPointQueryResult qr;
                 e = cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &qr);
-                if (e != cudaSuccess || !fn) { cudaFreeAsync(nrm, st); return fail(KM_ECUDA, "cuTensorMapEncodeTiled unavailable"); }
+                if (e != cudaSuccess || !fn) { return fail(KM_ECUDA, "cuTensorMapEncodeTiled unavailable"); }
                 encode = (PFN_cuTensorMapEncodeTiled_v12000)fn;
             }
             CUtensorMap tm;
@@ -2058,10 +2094,10 @@ km_status kmedoids_dissimilarity(const void* X, km_metric metric, int64_t n, int
             CUresult cr = encode(&tm, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, D, gdim, gstride, box, estr,
                                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
                                  CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-            if (cr != CUDA_SUCCESS) { cudaFreeAsync(nrm, st); return fail(KM_ECUDA, "tensor map encode failed (%d)", (int)cr); }
+            if (cr != CUDA_SUCCESS) { return fail(KM_ECUDA, "tensor map encode failed (%d)", (int)cr); }
             const size_t smem = km::dw_smem_bytes(dpad, wstage);
             e = cudaFuncSetAttribute(km::k_dist_l2_ws, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-            if (e != cudaSuccess) { cudaFreeAsync(nrm, st); return fail(KM_ECUDA, "smem attribute: %s", cudaGetErrorString(e)); }
+            if (e != cudaSuccess) { return fail(KM_ECUDA, "smem attribute: %s", cudaGetErrorString(e)); }
             km::k_dist_l2_ws<<<grid, km::DW_THREADS, smem, st>>>(tm, PA, PB, nrm, (int)n, dpad, nsplit, wstage,
                                                                   col_begin, col_end);
         } else {
@@ -2070,12 +2106,12 @@ km_status kmedoids_dissimilarity(const void* X, km_metric metric, int64_t n, int
             const int nstage = km::dt_smem_bytes(dpad, 2) + 1024 <= (size_t)smax ? 2 : 1;
             const size_t smem = km::dt_smem_bytes(dpad, nstage);
             e = cudaFuncSetAttribute(km::k_dist_l2_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-            if (e != cudaSuccess) { cudaFreeAsync(nrm, st); return fail(KM_ECUDA, "smem attribute: %s", cudaGetErrorString(e)); }
+            if (e != cudaSuccess) { return fail(KM_ECUDA, "smem attribute: %s", cudaGetErrorString(e)); }
             km::k_dist_l2_tc<<<grid, km::DT_THREADS, smem, st>>>(PA, PB, (int)n, dpad, nstage, nsplit, (float*)D, ld,
                                                                   col_begin, col_end);
         }
         e = cudaGetLastError();
-        cudaFreeAsync(nrm, st);
+        if (e == cudaSuccess) e = cudaEventRecord(g_dist_scr[dev].done, st);
         if (e != cudaSuccess) return fail(KM_ECUDA, "k_dist_l2_tc: %s", cudaGetErrorString(e));
         return KM_OK;
     }
