@@ -530,7 +530,8 @@ k_dist_l2_ws(const __grid_constant__ CUtensorMap tmap, const float* __restrict__
 // (each 4 x 4 outputs), coordinates staged through shared memory.
 __global__ void __launch_bounds__(256)
 k_dist_l1_u32(const int32_t* __restrict__ Xq, int n, int d, uint32_t* __restrict__ D, int64_t ld, int64_t c0,
-              int64_t c1) {
+              int64_t c1, const int* __restrict__ exact_f32 = nullptr) {
+    if (exact_f32 && *exact_f32) return;      // k_dist_l1_f32x produces this matrix
     constexpr int TB = 64, KB = 32;
     __shared__ int32_t sa[KB][TB + 1], sb[KB][TB + 1];
     const int i0 = blockIdx.y * TB;
@@ -564,6 +565,134 @@ k_dist_l1_u32(const int32_t* __restrict__ Xq, int n, int d, uint32_t* __restrict
         for (int v = 0; v < 4; ++v) {
             const int64_t j = j0 + tx * 4 + v;
             if (j < c1) D[(int64_t)i * ld + (j - c0)] = (j == i) ? 0u : acc[u][v];
+        }
+    }
+}
+
+// Per-dimension coordinate range of the L1 input (decides whether the fp32
+// kernel below is exact): rng[2t] = min_t, rng[2t+1] = max_t (pre-set by
+// k_dist_l1_range_init), then k_dist_l1_decide sets rng[2d] = 1 iff every
+// sum_t (max_t - min_t) < 2^24 (computed in int64).
+__global__ void k_dist_l1_range_init(int d, int* __restrict__ rng) {
+    for (int t = threadIdx.x; t < d; t += blockDim.x) { rng[2 * t] = INT_MAX; rng[2 * t + 1] = INT_MIN; }
+}
+__global__ void k_dist_l1_decide(int d, int* __restrict__ rng) {
+    __shared__ long long tot;
+    if (threadIdx.x == 0) tot = 0;
+    __syncthreads();
+    constexpr long long LIM = 1ll << 24;
+    for (int t = threadIdx.x; t < d; t += blockDim.x) {
+        const long long lo = rng[2 * t], hi = rng[2 * t + 1];
+        atomicAdd((unsigned long long*)&tot, (unsigned long long)(hi - lo));
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) rng[2 * d] = tot < LIM ? 1 : 0;
+}
+__global__ void k_dist_l1_range(const int32_t* __restrict__ Xq, int n, int d, int* __restrict__ rng) {
+    const int t = blockIdx.y;
+    int lo = INT_MAX, hi = INT_MIN;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        const int v = Xq[i * d + t];
+        lo = min(lo, v); hi = max(hi, v);
+    }
+    lo = __reduce_min_sync(0xffffffffu, lo);
+    hi = __reduce_max_sync(0xffffffffu, hi);
+    if ((threadIdx.x & 31) == 0) { atomicMin(&rng[2 * t], lo); atomicMax(&rng[2 * t + 1], hi); }
+}
+
+// L1 in fp32 arithmetic, exact: with coordinates translated per dimension
+// to y_t = x_t - min_t >= 0 (L1 is translation invariant) and
+// S_i = sum_t y_it,
+//     sum_t |y_it - y_jt| = S_i + S_j - 2 sum_t min(y_it, y_jt).
+// The kernel accumulates 2 min(.,.) in fp32; when sum_t (max_t - min_t) <
+// 2^24 (decided on the device by k_dist_l1_decide) every partial sum is an
+// even integer below 2^25, which fp32 represents exactly, so the result
+// equals the integer definition bit for bit.  Per element one FMNMX (ALU
+// pipe) and one FFMA with an immediate operand (FMA pipe), i.e. both issue
+// pipes in parallel, instead of three integer-ALU instructions.  128 x 128
+// tile per block, 8 x 8 outputs per thread (rows ty*4 + {0..3} and
+// 64 + ty*4 + {0..3}, likewise columns), operands transposed into shared
+// memory as [dim][row] floats and read as float4.
+constexpr int L1F_TB = 128, L1F_KB = 32, L1F_LD = L1F_TB + 4;
+
+// S_i of the translated coordinates (only when the fp32 kernel is used).
+__global__ void k_dist_l1_rowsum(const int32_t* __restrict__ Xq, int n, int d, const int* __restrict__ rng,
+                                 int* __restrict__ rowsum) {
+    if (!rng[2 * d]) return;
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    int sum = 0;
+    for (int t = 0; t < d; ++t) sum += Xq[(int64_t)i * d + t] - __ldg(&rng[2 * t]);
+    rowsum[i] = sum;
+}
+
+__global__ void __launch_bounds__(256, 2)
+k_dist_l1_f32x(const int32_t* __restrict__ Xq, int n, int d, uint32_t* __restrict__ D, int64_t ld, int64_t c0,
+               int64_t c1, bool vec, const int* __restrict__ rng, const int* __restrict__ rowsum) {
+    if (!rng[2 * d]) return;                  // not exact in fp32: k_dist_l1_u32 runs instead
+    __shared__ __align__(16) float sa[L1F_KB][L1F_LD], sb[L1F_KB][L1F_LD];
+    const int i0 = blockIdx.y * L1F_TB;
+    const int64_t j0 = c0 + (int64_t)blockIdx.x * L1F_TB;
+    const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
+    float acc[8][8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u)
+#pragma unroll
+        for (int v = 0; v < 8; ++v) acc[u][v] = 0.f;
+    for (int k0 = 0; k0 < d; k0 += L1F_KB) {
+        // 128 rows x 32 dims per operand: consecutive threads take consecutive
+        // dims of one row (coalesced), written transposed; padding is 0
+        for (int idx = threadIdx.x; idx < L1F_TB * L1F_KB; idx += 256) {
+            const int r = idx / L1F_KB, k = idx % L1F_KB;
+            const bool kin = k0 + k < d;
+            const int lo = kin ? __ldg(&rng[2 * (k0 + k)]) : 0;
+            sa[k][r] = (i0 + r < n && kin) ? (float)(Xq[(int64_t)(i0 + r) * d + k0 + k] - lo) : 0.f;
+            sb[k][r] = (j0 + r < c1 && kin) ? (float)(Xq[(j0 + r) * d + k0 + k] - lo) : 0.f;
+        }
+        __syncthreads();
+        const int kn = min(L1F_KB, d - k0);
+#pragma unroll 4
+        for (int k = 0; k < kn; ++k) {
+            const float4 a0 = *reinterpret_cast<const float4*>(&sa[k][ty * 4]);
+            const float4 a1 = *reinterpret_cast<const float4*>(&sa[k][64 + ty * 4]);
+            const float4 b0 = *reinterpret_cast<const float4*>(&sb[k][tx * 4]);
+            const float4 b1 = *reinterpret_cast<const float4*>(&sb[k][64 + tx * 4]);
+            const float a[8] = {a0.x, a0.y, a0.z, a0.w, a1.x, a1.y, a1.z, a1.w};
+            const float b[8] = {b0.x, b0.y, b0.z, b0.w, b1.x, b1.y, b1.z, b1.w};
+#pragma unroll
+            for (int u = 0; u < 8; ++u)
+#pragma unroll
+                for (int v = 0; v < 8; ++v) acc[u][v] = fmaf(fminf(a[u], b[v]), 2.0f, acc[u][v]);
+        }
+        __syncthreads();
+    }
+    int sj[8];
+#pragma unroll
+    for (int h = 0; h < 2; ++h)
+#pragma unroll
+        for (int v = 0; v < 4; ++v) {
+            const int64_t j = j0 + h * 64 + tx * 4 + v;
+            sj[h * 4 + v] = j < c1 ? __ldg(&rowsum[j]) : 0;
+        }
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+        const int i = i0 + (u < 4 ? ty * 4 + u : 64 + ty * 4 + (u - 4));
+        if (i >= n) continue;
+        const int si = __ldg(&rowsum[i]);
+        uint32_t* Drow = D + (int64_t)i * ld - c0;
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+            const int64_t j = j0 + h * 64 + tx * 4;
+            uint32_t o[4];
+#pragma unroll
+            for (int v = 0; v < 4; ++v)
+                o[v] = (j + v == i) ? 0u : (uint32_t)(si + sj[h * 4 + v] - (int)acc[u][h * 4 + v]);
+            if (vec && j + 3 < c1) {
+                *reinterpret_cast<uint4*>(Drow + j) = make_uint4(o[0], o[1], o[2], o[3]);
+            } else {
+#pragma unroll
+                for (int v = 0; v < 4; ++v) if (j + v < c1) Drow[j + v] = o[v];
+            }
         }
     }
 }

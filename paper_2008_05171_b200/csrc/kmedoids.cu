@@ -2116,10 +2116,36 @@ km_status kmedoids_dissimilarity(const void* X, km_metric metric, int64_t n, int
         return KM_OK;
     }
     if (metric == KM_METRIC_L1_U32) {
+        // Exactness of the fp32 kernel is decided on the device (coordinate
+        // ranges), and both kernels are launched: the one not chosen exits at
+        // its first instruction, so the call never waits for the GPU.
+        int dev = 0;
+        cudaGetDevice(&dev);
+        std::lock_guard<std::mutex> lock(g_dist_mu);
+        float* scr = nullptr;
+        cudaError_t e = dist_scratch(dev, (size_t)(2 * d + 1 + n) * sizeof(int), st, &scr);
+        if (e != cudaSuccess) return fail(KM_ENOMEM, "dissimilarity scratch: %s", cudaGetErrorString(e));
+        int* rng = (int*)scr;
+        const char* ek = getenv("KM_DIST_L1");          // "int": the integer kernel only
+        const bool try_f32 = !(ek && strcmp(ek, "int") == 0);
+        if (try_f32) {
+            km::k_dist_l1_range_init<<<1, 256, 0, st>>>(d, rng);
+            km::k_dist_l1_range<<<dim3((unsigned)std::min<int64_t>(cdiv(n, 256), 64), (unsigned)d), 256, 0, st>>>(
+                (const int32_t*)X, (int)n, d, rng);
+            km::k_dist_l1_decide<<<1, 256, 0, st>>>(d, rng);
+            km::k_dist_l1_rowsum<<<(unsigned)cdiv(n, 256), 256, 0, st>>>((const int32_t*)X, (int)n, d, rng,
+                                                                        rng + 2 * d + 1);
+            const bool vec = (ld % 4 == 0) && (((uintptr_t)D) % 16 == 0);
+            dim3 gf((unsigned)cdiv(col_end - col_begin, km::L1F_TB), (unsigned)cdiv(n, km::L1F_TB));
+            km::k_dist_l1_f32x<<<gf, 256, 0, st>>>((const int32_t*)X, (int)n, d, (uint32_t*)D, ld, col_begin, col_end,
+                                                    vec, rng, rng + 2 * d + 1);
+        }
         dim3 g((unsigned)cdiv(col_end - col_begin, 64), (unsigned)cdiv(n, 64));
-        km::k_dist_l1_u32<<<g, 256, 0, st>>>((const int32_t*)X, (int)n, d, (uint32_t*)D, ld, col_begin, col_end);
-        cudaError_t e = cudaGetLastError();
-        if (e != cudaSuccess) return fail(KM_ECUDA, "k_dist_l1_u32: %s", cudaGetErrorString(e));
+        km::k_dist_l1_u32<<<g, 256, 0, st>>>((const int32_t*)X, (int)n, d, (uint32_t*)D, ld, col_begin, col_end,
+                                             try_f32 ? rng + 2 * d : nullptr);
+        e = cudaGetLastError();
+        if (e == cudaSuccess) e = cudaEventRecord(g_dist_scr[dev].done, st);
+        if (e != cudaSuccess) return fail(KM_ECUDA, "k_dist_l1: %s", cudaGetErrorString(e));
         return KM_OK;
     }
     return fail(KM_EINVAL, "unknown metric %d", (int)metric);

@@ -101,3 +101,35 @@ def test_dissimilarity_argument_errors():
         kmedoids_dissimilarity(X, "l2")                   # d > 64 on the tensor-core path
     with pytest.raises(KMError):
         kmedoids_dissimilarity(X[:, :4].contiguous(), "l2", col_begin=5, col_end=3)
+
+
+@pytest.mark.parametrize("n,d,lo,hi,c0,c1", [
+    (300, 2, 0, 2 ** 23 - 1, 0, 300),           # sum of ranges 2^24 - 2: the fp32 kernel, at its limit
+    (300, 3, 0, 2 ** 23 - 1, 0, 300),           # 1.5 x 2^24: the integer kernel
+    (200, 4, -2 ** 25, 2 ** 25, 0, 200),        # ranges 2^26: the integer kernel
+    (150, 3, 2 ** 30, 2 ** 30 + 1000, 0, 150),  # large |x|, small ranges: fp32 after translation
+    (1000, 5, -3000, 3000, 3, 997),             # ragged 128-tiles, unaligned slab start
+    (385, 64, 0, 5000, 0, 385),                 # C5-like range, three row tiles + 1 row
+    (129, 40, -100, 100, 1, 2),                 # one column
+])
+def test_l1_fp32_path_exact_and_integer_fallback(n, d, lo, hi, c0, c1):
+    """The fp32 L1 kernel (translated coordinates, S_i + S_j - 2 sum min) is
+    used only when sum_t (max_t - min_t) < 2^24 (decided on the device); both
+    sides of that limit must equal the integer definition exactly."""
+    from paper_2008_05171_b200 import kmedoids_dissimilarity
+    rng = np.random.default_rng(n + d)
+    Xq = rng.integers(lo, hi, size=(n, d), endpoint=True).astype(np.int32)
+    Xq[0, :] = lo                              # the extremes occur
+    Xq[-1, :] = hi
+    Dg = kmedoids_dissimilarity(torch.from_numpy(Xq).cuda(), "l1", col_begin=c0, col_end=c1)
+    Dg = Dg[:, :c1 - c0].cpu().numpy().view(np.uint32).astype(np.int64)
+    assert (Dg == oracle.dist_l1(Xq)[:, c0:c1]).all()
+
+
+def test_l1_integer_kernel_forced(monkeypatch):
+    from paper_2008_05171_b200 import kmedoids_dissimilarity
+    monkeypatch.setenv("KM_DIST_L1", "int")
+    rng = np.random.default_rng(5)
+    Xq = rng.integers(-5000, 5000, size=(333, 17)).astype(np.int32)
+    Dg = kmedoids_dissimilarity(torch.from_numpy(Xq).cuda(), "l1")
+    assert (Dg[:, :333].cpu().numpy().view(np.uint32).astype(np.int64) == oracle.dist_l1(Xq)).all()
