@@ -1888,7 +1888,7 @@ __global__ void k_swap_combine(int w, int64_t col_begin, int P, const A* __restr
         };
         A plus = 0, carry = 0;
         int cs = -1;
-        constexpr int QU = 4;                  // parts loaded ahead (memory-level parallelism)
+        constexpr int QU = 8;                  // parts loaded ahead (memory-level parallelism)
         for (int q0 = 0; q0 < P; q0 += QU) {
             A pl[QU], hv[QU], tv[QU], iv[QU];
             int isl[QU], hs[QU], ts[QU];

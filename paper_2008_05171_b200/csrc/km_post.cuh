@@ -24,6 +24,8 @@
 namespace km {
 
 constexpr int POST_THREADS = 256;
+constexpr int POST_MAX_BLOCKS = 768;                  // chunk counts per slot scanned in registers
+constexpr int POST_MAX_PER = POST_MAX_BLOCKS / 32;
 
 template <typename T, typename A>
 struct PostArgs {
@@ -52,7 +54,18 @@ struct PostArgs {
     A* R;
     int P;
     int *head_slot, *tail_slot;
+    Decision<A>* h_dec;        // pinned host mirrors written at the end (or null)
+    A* h_td;
+    unsigned long long* tph;   // measurement aid (KM_STEP_PROF): globaltimer after each phase, or null
 };
+
+__device__ __forceinline__ void post_stamp(unsigned long long* tph, int i) {
+    if (tph && blockIdx.x == 0 && threadIdx.x == 0) {
+        unsigned long long t;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+        tph[i] = t;
+    }
+}
 
 template <typename T>
 __device__ __forceinline__ RowInfo<T> post_ld_ri(const RowInfo<T>* p) {
@@ -73,6 +86,7 @@ k_fp1_post(PostArgs<T, A> g) {
     const int tid = blockIdx.x * blockDim.x + threadIdx.x, nth = gridDim.x * blockDim.x;
     const int gwarp = tid >> 5, nwarps = nth >> 5;
     const int n = g.n, k = g.k, B = gridDim.x, b = blockIdx.x;
+    post_stamp(g.tph, 0);
 
     // ---- 0 select (every block decides identically; block 0 records)
     if (threadIdx.x == 0) {
@@ -100,7 +114,7 @@ k_fp1_post(PostArgs<T, A> g) {
     }
     __syncthreads();
     const Decision<A> d = sdec;
-    grid.sync();                                 // every block has read M / td / dec
+    grid.sync(); post_stamp(g.tph, 1);                                 // every block has read M / td / dec
     if (b == 0 && threadIdx.x == 0) {
         *g.dec = d;
         if (d.apply) {
@@ -133,7 +147,7 @@ k_fp1_post(PostArgs<T, A> g) {
                 g.sec[o] = i; g.ds[o] = x;
             }
         }
-        grid.sync();
+        grid.sync(); post_stamp(g.tph, 2);
         // ---- 2 rescan
         const int cnt = __ldcg(g.rescan_count);
         for (int e = gwarp; e < cnt; e += nwarps) {
@@ -159,7 +173,7 @@ k_fp1_post(PostArgs<T, A> g) {
             }
             if (lane == 0) { g.near[o] = j1; g.sec[o] = j2; g.dn[o] = d1; g.ds[o] = d2; }
         }
-        grid.sync();
+        grid.sync(); post_stamp(g.tph, 3);
     }
 
     // ---- 3 histogram of the block's chunk
@@ -171,26 +185,37 @@ k_fp1_post(PostArgs<T, A> g) {
     for (int e = e0 + threadIdx.x; e < e1; e += blockDim.x) atomicAdd(&h[__ldcg(&g.near[e])], 1);
     __syncthreads();
     for (int s = threadIdx.x; s < k; s += blockDim.x) g.counts[(int64_t)s * B + b] = h[s];
-    grid.sync();
+    grid.sync(); post_stamp(g.tph, 4);
 
-    // ---- 4 within-slot exclusive scan over the chunks, warp per slot
+    // ---- 4 within-slot exclusive scan over the chunks, warp per slot: all
+    // B counts of the slot loaded first (coalesced, one memory round trip),
+    // then B/32 register-only warp scans
     for (int s = gwarp; s < k; s += nwarps) {
+        const int* cs = g.counts + (int64_t)s * B;
+        int cv[POST_MAX_PER];
+#pragma unroll
+        for (int i = 0; i < POST_MAX_PER; ++i) {
+            const int bb = i * 32 + lane;
+            cv[i] = bb < B ? __ldcg(&cs[bb]) : 0;
+        }
         int run = 0;
-        for (int b0 = 0; b0 < B; b0 += 32) {
-            const int bb = b0 + lane;
-            const int c = bb < B ? __ldcg(&g.counts[(int64_t)s * B + bb]) : 0;
-            int incl = c;
+        int* os = g.offsets + (int64_t)s * B;
+#pragma unroll
+        for (int i = 0; i < POST_MAX_PER; ++i) {
+            if (i * 32 >= B) break;
+            int incl = cv[i];
 #pragma unroll
             for (int dd = 1; dd < 32; dd <<= 1) {
                 const int y = __shfl_up_sync(FULL, incl, dd);
                 if (lane >= dd) incl += y;
             }
-            if (bb < B) g.offsets[(int64_t)s * B + bb] = run + incl - c;
+            const int bb = i * 32 + lane;
+            if (bb < B) os[bb] = run + incl - cv[i];
             run += __shfl_sync(FULL, incl, 31);
         }
         if (lane == 0) g.slot_tot[s] = run;
     }
-    grid.sync();
+    grid.sync(); post_stamp(g.tph, 5);
 
     // ---- 5 exclusive scan of the slot totals (block 0)
     if (b == 0) {
@@ -217,7 +242,7 @@ k_fp1_post(PostArgs<T, A> g) {
         if (threadIdx.x == blockDim.x - 1) g.seg_start[k] = run;
         if (threadIdx.x == 0) *g.empty_slot = INT_MAX;
     }
-    grid.sync();
+    grid.sync(); post_stamp(g.tph, 6);
 
     // ---- 6 stable scatter into (slot, o) order: warp 0 of each block
     if (threadIdx.x < 32) {
@@ -247,7 +272,7 @@ k_fp1_post(PostArgs<T, A> g) {
             }
         }
     }
-    grid.sync();
+    grid.sync(); post_stamp(g.tph, 7);
 
     // ---- 7 removal loss (warp per slot, fixed tree) and part metadata
     for (int s = gwarp; s < k; s += nwarps) {
@@ -269,7 +294,16 @@ k_fp1_post(PostArgs<T, A> g) {
         g.head_slot[q] = post_ld_ri(&g.ri[p0]).slot;
         g.tail_slot[q] = post_ld_ri(&g.ri[p1 - 1]).slot;
     }
-    if (b == 0 && threadIdx.x == 0) *g.rescan_count = 0;
+    if (b == 0 && threadIdx.x == 0) {
+        *g.rescan_count = 0;
+        // the decision and TD straight into pinned host memory (visible to the
+        // host once the stream is synchronised): no copy nodes after the kernel
+        if (g.h_dec) {
+            *g.h_dec = d;
+            *g.h_td = *g.td;
+        }
+    }
+    post_stamp(g.tph, 8);
 }
 
 }  // namespace km

@@ -225,6 +225,7 @@ struct Impl : ImplBase {
         for (void* p : bufs) cudaFree(p);
         if (h_dec) cudaFreeHost(h_dec);
         if (h_td) cudaFreeHost(h_td);
+        for (auto e : sp_ev) if (e) cudaEventDestroy(e);
         if (ev0) cudaEventDestroy(ev0);
         if (ev1) cudaEventDestroy(ev1);
     }
@@ -349,6 +350,9 @@ struct Impl : ImplBase {
         KM_CK(cudaMallocHost((void**)&h_td, sizeof(A)));
         KM_CK(cudaEventCreate(&ev0));
         KM_CK(cudaEventCreate(&ev1));
+        if (const char* es = getenv("KM_STEP_PROF")) step_prof = es[0] == '1';
+        if (step_prof)
+            for (auto& e : sp_ev) KM_CK(cudaEventCreate(&e));
         KM_CK(cudaStreamSynchronize(st));
         return KM_OK;
     }
@@ -373,6 +377,10 @@ struct Impl : ImplBase {
         return KM_OK;
     }
     bool pending_prof = false;
+    bool step_prof = false;
+    cudaEvent_t sp_ev[5] = {};
+    double sp_sum[5] = {};
+    int sp_n = 0;
     bool tma_attr_set = false;
     // CUDA graph of the FastPAM1 iteration (KM_GRAPH=0 disables)
     bool use_graph = true;
@@ -623,6 +631,8 @@ struct Impl : ImplBase {
     bool fp1_prepped = false;       // slot sort / R / part metadata valid for the current cache
     int post_blocks = 0;
     int *post_counts = nullptr, *post_offsets = nullptr;
+    unsigned long long* post_tph = nullptr;   // KM_STEP_PROF: phase stamps of k_fp1_post
+    double post_ph_sum[8] = {};
 
     km_status post_alloc() {
         if (post_counts) return KM_OK;
@@ -634,10 +644,11 @@ struct Impl : ImplBase {
         KM_CK(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
         KM_CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, km::POST_THREADS, sm));
         if (per_sm < 1) return fail(KM_ECUDA, "k_fp1_post cannot be resident");
-        post_blocks = nsm * std::min(per_sm, 4);
+        post_blocks = std::min(nsm * std::min(per_sm, 4), km::POST_MAX_BLOCKS);
         post_blocks = (int)std::min<int64_t>(post_blocks, std::max<int64_t>(1, cdiv(n, 64)));
         KM_TRY(alloc(&post_counts, (size_t)k * post_blocks));
         KM_TRY(alloc(&post_offsets, (size_t)k * post_blocks));
+        if (step_prof) KM_TRY(alloc(&post_tph, 16));
         return KM_OK;
     }
 
@@ -648,6 +659,8 @@ struct Impl : ImplBase {
         g.dn = dn; g.ds = ds; g.rescan = rescan; g.rescan_count = rescan_count; g.counts = post_counts;
         g.offsets = post_offsets; g.slot_tot = slot_tot; g.seg_start = seg_start; g.empty_slot = empty_slot;
         g.ri = ri; g.rowd = rowd; g.R = R; g.P = P; g.head_slot = head_slot; g.tail_slot = tail_slot;
+        g.tph = post_tph;
+        g.h_dec = h_dec; g.h_td = h_td;
         void* args[] = {&g};
         KM_CK(cudaLaunchCooperativeKernel((void*)km::k_fp1_post<T, A>, dim3(post_blocks), dim3(km::POST_THREADS), args,
                                           (size_t)k * sizeof(int), st));
@@ -666,9 +679,10 @@ struct Impl : ImplBase {
         profiling = prof_save;
         if (s != KM_OK) return s;
         if (use_post == 1) {
-            KM_TRY(launch_post());
-            KM_CK(cudaMemcpyAsync(h_dec, dec, sizeof(Dec), cudaMemcpyDeviceToHost, st));
-            KM_CK(cudaMemcpyAsync(h_td, td, sizeof(A), cudaMemcpyDeviceToHost, st));
+            if (step_prof) KM_CK(record_ev(sp_ev[2]));
+            KM_TRY(launch_post());          // writes the pinned h_dec / h_td mirrors itself
+            if (step_prof) KM_CK(record_ev(sp_ev[3]));
+            if (step_prof) KM_CK(record_ev(sp_ev[4]));
             return KM_OK;
         }
         km::k_select<A><<<1, 1, 0, st>>>(rec_local, 1, td, M, point_slot, dec, rescan_count);
@@ -735,9 +749,37 @@ struct Impl : ImplBase {
                 }
                 fp1_graph_kernels = captured;
             }
+            if (step_prof) KM_CK(cudaEventRecord(sp_ev[0], st));
             KM_CK(cudaGraphLaunch(fp1_exec, st));
             launches += fp1_graph_kernels;
             KM_CK(cudaStreamSynchronize(st));
+            if (step_prof) {
+                // phases of the iteration graph (KM_STEP_PROF=1, measurement aid):
+                // launch -> stream start, stream, combine, post, decision copies
+                float t[5];
+                KM_CK(cudaEventElapsedTime(&t[0], sp_ev[0], ev0));
+                KM_CK(cudaEventElapsedTime(&t[1], ev0, ev1));
+                KM_CK(cudaEventElapsedTime(&t[2], ev1, sp_ev[2]));
+                KM_CK(cudaEventElapsedTime(&t[3], sp_ev[2], sp_ev[3]));
+                KM_CK(cudaEventElapsedTime(&t[4], sp_ev[3], sp_ev[4]));
+                for (int i = 0; i < 5; ++i) sp_sum[i] += t[i];
+                if (post_tph) {
+                    unsigned long long h[9];
+                    KM_CK(cudaMemcpy(h, post_tph, sizeof(h), cudaMemcpyDeviceToHost));
+                    for (int i = 0; i < 8; ++i) post_ph_sum[i] += 1e-3 * (double)(h[i + 1] - h[i]);
+                }
+                if (++sp_n % 50 == 0) {
+                    fprintf(stderr, "[kmedoids] step phases over %d iterations (us): launch %.1f stream %.1f combine %.1f "
+                            "post %.1f copies %.1f\n", sp_n, 1e3 * sp_sum[0] / sp_n, 1e3 * sp_sum[1] / sp_n,
+                            1e3 * sp_sum[2] / sp_n, 1e3 * sp_sum[3] / sp_n, 1e3 * sp_sum[4] / sp_n);
+                    if (post_tph)
+                        fprintf(stderr, "[kmedoids] post phases (us): select %.1f apply %.1f rescan %.1f hist %.1f "
+                                "slotscan %.1f scan %.1f scatter %.1f R/parts %.1f\n", post_ph_sum[0] / sp_n,
+                                post_ph_sum[1] / sp_n, post_ph_sum[2] / sp_n, post_ph_sum[3] / sp_n,
+                                post_ph_sum[4] / sp_n, post_ph_sum[5] / sp_n, post_ph_sum[6] / sp_n,
+                                post_ph_sum[7] / sp_n);
+                }
+            }
             if (profiling) {
                 float ms = 0.f;
                 KM_CK(cudaEventElapsedTime(&ms, ev0, ev1));
