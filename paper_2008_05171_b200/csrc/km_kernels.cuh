@@ -1873,7 +1873,20 @@ __global__ void k_swap_combine(int w, int64_t col_begin, int P, const A* __restr
                                const A* __restrict__ R, const int* __restrict__ empty_slot,
                                const int* __restrict__ point_slot, A* __restrict__ cand_v,
                                int* __restrict__ cand_slot, Rec<A>* partials, unsigned* counter,
-                               Rec<A>* out, A* __restrict__ acc_out = nullptr, A* __restrict__ plus_out = nullptr) {
+                               Rec<A>* out, A* __restrict__ acc_out = nullptr, A* __restrict__ plus_out = nullptr,
+                               int k = 0, bool stage = false) {
+    // R and the part head/tail slots staged in shared memory (when they fit):
+    // the fold's R[s] lookups and slot compares then wait ~30 cycles, not an
+    // L1/L2 round trip each (ncu: stalls on the DADD after every R load)
+    extern __shared__ __align__(16) unsigned char comb_smem[];
+    if (stage) {
+        A* sR = reinterpret_cast<A*>(comb_smem);
+        int* shs = reinterpret_cast<int*>(comb_smem + (size_t)k * sizeof(A));
+        for (int i = threadIdx.x; i < k; i += blockDim.x) sR[i] = R[i];
+        for (int i = threadIdx.x; i < P; i += blockDim.x) { shs[i] = head_slot[i]; shs[P + i] = tail_slot[i]; }
+        __syncthreads();
+        R = sR; head_slot = shs; tail_slot = shs + P;
+    }
     const int cl = blockIdx.x * blockDim.x + threadIdx.x;
     Rec<A> best = rec_none<A>();
     if (cl < w) {
@@ -1982,8 +1995,18 @@ k_swap_combine_par(int w, int64_t col_begin, int P, const A* __restrict__ in_plu
                    const A* __restrict__ R, const int* __restrict__ empty_slot,
                    const int* __restrict__ point_slot, A* __restrict__ cand_v,
                    int* __restrict__ cand_slot, Rec<A>* partials, unsigned* counter,
-                   Rec<A>* out, A* __restrict__ acc_out = nullptr, A* __restrict__ plus_out = nullptr) {
+                   Rec<A>* out, A* __restrict__ acc_out = nullptr, A* __restrict__ plus_out = nullptr,
+                   int k = 0, bool stage = false) {
     __shared__ CombState<A> sst[CG][32];
+    extern __shared__ __align__(16) unsigned char comb_smem[];
+    if (stage) {                               // as k_swap_combine
+        A* sR = reinterpret_cast<A*>(comb_smem);
+        int* shs = reinterpret_cast<int*>(comb_smem + (size_t)k * sizeof(A));
+        for (int i = threadIdx.x; i < k; i += blockDim.x) sR[i] = R[i];
+        for (int i = threadIdx.x; i < P; i += blockDim.x) { shs[i] = head_slot[i]; shs[P + i] = tail_slot[i]; }
+        __syncthreads();
+        R = sR; head_slot = shs; tail_slot = shs + P;
+    }
     const int lane = threadIdx.x & 31, g = threadIdx.x >> 5;
     const int cl = blockIdx.x * 32 + lane;
     CombState<A> st;
@@ -1995,7 +2018,7 @@ k_swap_combine_par(int w, int64_t col_begin, int P, const A* __restrict__ in_plu
     };
     if (cl < w) {
         const int q0 = (int)((int64_t)g * P / CG), q1 = (int)((int64_t)(g + 1) * P / CG);
-        constexpr int QU = 4;
+        constexpr int QU = 8;
         for (int qb = q0; qb < q1; qb += QU) {
             A pl[QU], hv[QU], tv[QU], iv[QU];
             int isl[QU], hs[QU], ts[QU];

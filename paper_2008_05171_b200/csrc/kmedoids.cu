@@ -510,16 +510,23 @@ struct Impl : ImplBase {
                              const int* isl, const int* hsl, const int* tsl, A* cv, int* cs, A* acc_o, A* plus_o) {
         if (combine_kind < 0) {
             const char* e = getenv("KM_COMBINE");
-            combine_kind = (e && strcmp(e, "par") == 0) ? 1 : 0;
+            combine_kind = (e && strcmp(e, "par") == 0) ? 1 : (e && strcmp(e, "par4") == 0) ? 2 : 0;
         }
-        if (combine_kind == 0)
-            km::k_swap_combine<A><<<(unsigned)cdiv(ww, 128), 128, 0, st>>>(ww, colb, Pw, pl, hd, tl, im, isl, hsl, tsl, R,
-                                                                            empty_slot, point_slot, cv, cs, partials,
-                                                                            counters, rec_local, acc_o, plus_o);
-        else
-            km::k_swap_combine_par<A, COMB_G><<<(unsigned)cdiv(ww, 32), 32 * COMB_G, 0, st>>>(
+        const size_t sm = (size_t)k * sizeof(A) + 2 * (size_t)Pw * sizeof(int);
+        const bool stage = sm <= 32 * 1024;
+        if (combine_kind == 0) {
+            km::k_swap_combine<A><<<(unsigned)cdiv(ww, 128), 128, stage ? sm : 0, st>>>(
                 ww, colb, Pw, pl, hd, tl, im, isl, hsl, tsl, R, empty_slot, point_slot, cv, cs, partials, counters,
-                rec_local, acc_o, plus_o);
+                rec_local, acc_o, plus_o, k, stage);
+        }
+        else if (combine_kind == 2)
+            km::k_swap_combine_par<A, 4><<<(unsigned)cdiv(ww, 32), 32 * 4, stage ? sm : 0, st>>>(
+                ww, colb, Pw, pl, hd, tl, im, isl, hsl, tsl, R, empty_slot, point_slot, cv, cs, partials, counters,
+                rec_local, acc_o, plus_o, k, stage);
+        else
+            km::k_swap_combine_par<A, COMB_G><<<(unsigned)cdiv(ww, 32), 32 * COMB_G, stage ? sm : 0, st>>>(
+                ww, colb, Pw, pl, hd, tl, im, isl, hsl, tsl, R, empty_slot, point_slot, cv, cs, partials, counters,
+                rec_local, acc_o, plus_o, k, stage);
         KM_CKL();
         return KM_OK;
     }
