@@ -281,6 +281,19 @@ def run_ours(args):
     alg_bytes = 4.0 * n * (n - k)
     k1_avg = k1_ms / max(1, k1_launches)
     achieved = alg_bytes / (k1_avg / 1e3) / 1e9
+    # per-iteration distribution (median, mean, count): a separate
+    # pass after the timed region with events around every iteration
+    it_ms = []
+    for _ in range(min(args.steps, 30)):
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        km.swap_iter(args.variant)
+        b.record(stream)
+        b.synchronize()
+        it_ms.append(a.elapsed_time(b))
+    iteration_ms = {"median": float(np.median(it_ms)), "mean": float(np.mean(it_ms)), "min": float(np.min(it_ms)),
+                    "max": float(np.max(it_ms)), "n": len(it_ms),
+                    "note": "events around each swap_iter call in a pass after the timed region"}
     # a read-only stream over the same D in the same job (a second denominator)
     read_peak = kmsynth.read_peak_gbs(Dt, reps=5, stream=stream)
 
@@ -396,6 +409,7 @@ def run_ours(args):
                      "alg_bytes_per_launch": alg_bytes, "peak_kind": peak_kind,
                      "read_only_peak_same_job": read_peak, "frac_of_read_only_peak": achieved / read_peak,
                      "frac_of_nominal_7700": achieved / 7700.0},
+        "iteration_ms": iteration_ms,
         "stream_share_of_step": k1_ms / total_ms,
         "gpu_launches": launches,
         "clocks": clk.summary(),

@@ -439,6 +439,7 @@ k_dist_l2_ws(const __grid_constant__ CUtensorMap tmap, const float* __restrict__
             for (int64_t tc = t0; tc < t1; ++tc, ++t) {
                 const int s = (int)(t & 1);
                 const int64_t n0 = c0 + tc * DT_N;
+                const int64_t cb = n0 + part * DW_CPW;
                 dt_wait(&bar_tfull[s], ph_tf[s]); ph_tf[s] ^= 1;
                 asm volatile("tcgen05.fence::after_thread_sync;");
                 uint32_t v[DW_CPW];
@@ -462,8 +463,6 @@ k_dist_l2_ws(const __grid_constant__ CUtensorMap tmap, const float* __restrict__
                 __syncwarp();
                 if (lane == 0) dw_arrive(&bar_tempty[s]);  // accumulator s may be overwritten
                 // distances (norms of the columns: same addresses across the warp -> broadcast)
-                const int64_t cb = n0 + part * DW_CPW;
-                const bool diag = (cb <= (int64_t)m0 + DT_M - 1) && ((int64_t)m0 <= cb + DW_CPW - 1);
 #pragma unroll
                 for (int j = 0; j < DW_CPW; j += 4) {
                     float4 ny4 = make_float4(0.f, 0.f, 0.f, 0.f);
@@ -476,13 +475,10 @@ k_dist_l2_ws(const __grid_constant__ CUtensorMap tmap, const float* __restrict__
                     }
                     const float ny[4] = {ny4.x, ny4.y, ny4.z, ny4.w};
 #pragma unroll
-                    for (int u = 0; u < 4; ++u) {
-                        const float d2 = fmaf(-2.f, __uint_as_float(v[j + u]), nx + ny[u]);
-                        float dd = dw_sqrt(fmaxf(d2, 0.f));
-                        if (diag && cb + j + u == row) dd = 0.f;
-                        v[j + u] = __float_as_uint(dd);
-                    }
+                    for (int u = 0; u < 4; ++u)
+                        v[j + u] = __float_as_uint(dw_sqrt(fmaxf(fmaf(-2.f, __uint_as_float(v[j + u]), nx + ny[u]), 0.f)));
                 }
+                const int64_t dj = (int64_t)row - cb;       // this lane's diagonal column, if in its part
                 // the staging boxes were last read by the tensor stores of tile t - nstage
                 unsigned char* stage = stage0 + (size_t)(t % nstage) * 4 * DT_M * 128;
                 if (tid == 0) {
@@ -501,6 +497,13 @@ k_dist_l2_ws(const __grid_constant__ CUtensorMap tmap, const float* __restrict__
                         *reinterpret_cast<uint4*>(box + r * 128 + ((c ^ (r & 7)) << 4)) =
                             make_uint4(v[jj], v[jj + 1], v[jj + 2], v[jj + 3]);
                     }
+                }
+                // d(x, x) = 0 exactly: one scalar overwrite in the staging box, only
+                // in tiles that cross the diagonal (kept out of the per-element loop)
+                if (dj >= 0 && dj < DW_CPW) {
+                    const int jj = (int)dj;
+                    unsigned char* box = stage + (part * (DW_CPW / 32) + (jj >> 5)) * (DT_M * 128);
+                    *reinterpret_cast<float*>(box + r * 128 + ((((jj & 31) >> 2) ^ (r & 7)) << 4) + (jj & 3) * 4) = 0.f;
                 }
                 asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
                 asm volatile("bar.sync 1, %0;" :: "n"(DW_EPI_WARPS * 32) : "memory");
