@@ -479,48 +479,40 @@ k_dist_l2_ws(const __grid_constant__ CUtensorMap tmap, const float* __restrict__
                         v[j + u] = __float_as_uint(dw_sqrt(fmaxf(fmaf(-2.f, __uint_as_float(v[j + u]), nx + ny[u]), 0.f)));
                 }
                 const int64_t dj = (int64_t)row - cb;       // this lane's diagonal column, if in its part
-                // the staging boxes were last read by the tensor stores of tile t - nstage
-                unsigned char* stage = stage0 + (size_t)(t % nstage) * 4 * DT_M * 128;
-                if (tid == 0) {
+                // Each warp stages its own 32 rows x 32 columns (one 4 KB box, 128B
+                // swizzle: 16-byte chunk c of row r at c ^ (r & 7)) and lane 0 issues
+                // its tensor store: no CTA-wide barrier in the epilogue.  The box was
+                // last read by this lane's store of tile t - nstage.
+                static_assert(DW_CPW == 32, "one 32-column box per warp");
+                unsigned char* box = stage0 + (size_t)(t % nstage) * DW_EPI_WARPS * 4096 + (size_t)warp * 4096;
+                if (lane == 0) {
                     if (nstage == 2) asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
                     else asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
                 }
-                asm volatile("bar.sync 1, %0;" :: "n"(DW_EPI_WARPS * 32) : "memory");
-                // box b (32 columns) = 128 rows x 128 B, 128B swizzle: 16-byte chunk c of row r at c ^ (r & 7)
-                const int r = q * 32 + lane;
+                __syncwarp();
 #pragma unroll
-                for (int bb = 0; bb < DW_CPW / 32; ++bb) {
-                    unsigned char* box = stage + (part * (DW_CPW / 32) + bb) * (DT_M * 128);
-#pragma unroll
-                    for (int c = 0; c < 8; ++c) {
-                        const int jj = bb * 32 + c * 4;
-                        *reinterpret_cast<uint4*>(box + r * 128 + ((c ^ (r & 7)) << 4)) =
-                            make_uint4(v[jj], v[jj + 1], v[jj + 2], v[jj + 3]);
-                    }
-                }
+                for (int c = 0; c < 8; ++c)
+                    *reinterpret_cast<uint4*>(box + lane * 128 + ((c ^ (lane & 7)) << 4)) =
+                        make_uint4(v[c * 4], v[c * 4 + 1], v[c * 4 + 2], v[c * 4 + 3]);
                 // d(x, x) = 0 exactly: one scalar overwrite in the staging box, only
                 // in tiles that cross the diagonal (kept out of the per-element loop)
                 if (dj >= 0 && dj < DW_CPW) {
                     const int jj = (int)dj;
-                    unsigned char* box = stage + (part * (DW_CPW / 32) + (jj >> 5)) * (DT_M * 128);
-                    *reinterpret_cast<float*>(box + r * 128 + ((((jj & 31) >> 2) ^ (r & 7)) << 4) + (jj & 3) * 4) = 0.f;
+                    *reinterpret_cast<float*>(box + lane * 128 + (((jj >> 2) ^ (lane & 7)) << 4) + (jj & 3) * 4) = 0.f;
                 }
                 asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-                asm volatile("bar.sync 1, %0;" :: "n"(DW_EPI_WARPS * 32) : "memory");
-                if (tid == 0) {
-#pragma unroll
-                    for (int bb = 0; bb < 4; ++bb) {
-                        const int x = (int)(n0 - c0) + bb * 32;
-                        asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%1, %2}], [%3];"
-                                     :: "l"(reinterpret_cast<uint64_t>(&tmap)), "r"(x), "r"(m0),
-                                        "r"(dt_smem_u32(stage + bb * (DT_M * 128)))
-                                     : "memory");
-                    }
+                __syncwarp();
+                if (lane == 0) {
+                    const int x = (int)(n0 - c0) + part * DW_CPW;
+                    asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%1, %2}], [%3];"
+                                 :: "l"(reinterpret_cast<uint64_t>(&tmap)), "r"(x), "r"(m0 + q * 32),
+                                    "r"(dt_smem_u32(box))
+                                 : "memory");
                     asm volatile("cp.async.bulk.commit_group;" ::: "memory");
                 }
             }
         }
-        if (tid == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+        if (lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
     }
     asm volatile("tcgen05.fence::before_thread_sync;");
     __syncthreads();

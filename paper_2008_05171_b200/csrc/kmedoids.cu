@@ -2138,7 +2138,7 @@ km_status kmedoids_dissimilarity(const void* X, km_metric metric, int64_t n, int
             CUtensorMap tm;
             cuuint64_t gdim[2] = {(cuuint64_t)(col_end - col_begin), (cuuint64_t)n};
             cuuint64_t gstride[1] = {(cuuint64_t)ld * sizeof(float)};
-            cuuint32_t box[2] = {32, (cuuint32_t)km::DT_M};
+            cuuint32_t box[2] = {32, 32};                 // one warp's 32 x 32 staging box
             cuuint32_t estr[2] = {1, 1};
             CUresult cr = encode(&tm, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, D, gdim, gstride, box, estr,
                                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
