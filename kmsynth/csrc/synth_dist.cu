@@ -95,7 +95,40 @@ __global__ void k_read_stream(const uint4* __restrict__ p, int64_t n16, unsigned
     const unsigned v = acc.x ^ acc.y ^ acc.z ^ acc.w;
     if (v == 0x9e3779b9u) atomicXor(sink, v);   // practically never taken; keeps the loads alive
 }
+__global__ void k_write_stream(uint4* __restrict__ p, int64_t n16, unsigned v) {
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    const uint4 w = make_uint4(v, v, v, v);
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n16; i += stride)
+        asm volatile("st.global.L1::no_allocate.v4.u32 [%0], {%1,%2,%3,%4};" :: "l"(p + i), "r"(w.x), "r"(w.y),
+                     "r"(w.z), "r"(w.w) : "memory");
+}
 }  // namespace
+
+// Best of `reps` timed write-only passes over buf (its contents are
+// overwritten); returns GB/s (written bytes / time).
+extern "C" double kmsynth_write_peak(void* buf, int64_t bytes, int reps, void* stream) {
+    cudaStream_t st = (cudaStream_t)stream;
+    int dev = 0, nsm = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+    const int64_t n16 = bytes / 16;
+    cudaEvent_t a, b;
+    cudaEventCreate(&a); cudaEventCreate(&b);
+    k_write_stream<<<nsm * 8, 256, 0, st>>>((uint4*)buf, n16, 0u);     // warm-up
+    double best = 0.0;
+    for (int r = 0; r < reps; ++r) {
+        cudaEventRecord(a, st);
+        k_write_stream<<<nsm * 8, 256, 0, st>>>((uint4*)buf, n16, (unsigned)r);
+        cudaEventRecord(b, st);
+        cudaEventSynchronize(b);
+        float ms = 0.f;
+        cudaEventElapsedTime(&ms, a, b);
+        const double gbs = (double)n16 * 16 / (ms * 1e-3) / 1e9;
+        if (gbs > best) best = gbs;
+    }
+    cudaEventDestroy(a); cudaEventDestroy(b);
+    return best;
+}
 
 // Best of `reps` timed passes (CUDA events); returns GB/s (read bytes / time).
 extern "C" double kmsynth_read_peak(const void* buf, int64_t bytes, int reps, void* stream) {

@@ -463,15 +463,18 @@ k_dist_l2_ws(const __grid_constant__ CUtensorMap tmap, const float* __restrict__
                 __syncwarp();
                 if (lane == 0) dw_arrive(&bar_tempty[s]);  // accumulator s may be overwritten
                 // distances (norms of the columns: same addresses across the warp -> broadcast)
+                // column norms: 16-byte loads with no per-element bounds in whole,
+                // aligned parts (all but the slab's last part when c0 % 4 == 0)
+                const bool whole = (cb + DW_CPW <= c1) && ((cb & 3) == 0);
 #pragma unroll
                 for (int j = 0; j < DW_CPW; j += 4) {
-                    float4 ny4 = make_float4(0.f, 0.f, 0.f, 0.f);
-                    if (cb + j + 3 < c1 && ((cb + j) & 3) == 0) ny4 = __ldg(reinterpret_cast<const float4*>(nrm + cb + j));
+                    float4 ny4;
+                    if (whole) ny4 = __ldg(reinterpret_cast<const float4*>(nrm + cb + j));
                     else {
-                        if (cb + j + 3 < c1) ny4.w = nrm[cb + j + 3];
-                        if (cb + j < c1) ny4.x = nrm[cb + j];
-                        if (cb + j + 1 < c1) ny4.y = nrm[cb + j + 1];
-                        if (cb + j + 2 < c1) ny4.z = nrm[cb + j + 2];
+                        ny4.x = cb + j < c1 ? nrm[cb + j] : 0.f;
+                        ny4.y = cb + j + 1 < c1 ? nrm[cb + j + 1] : 0.f;
+                        ny4.z = cb + j + 2 < c1 ? nrm[cb + j + 2] : 0.f;
+                        ny4.w = cb + j + 3 < c1 ? nrm[cb + j + 3] : 0.f;
                     }
                     const float ny[4] = {ny4.x, ny4.y, ny4.z, ny4.w};
 #pragma unroll
