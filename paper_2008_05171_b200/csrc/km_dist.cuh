@@ -529,7 +529,7 @@ k_dist_l2_ws(const __grid_constant__ CUtensorMap tmap, const float* __restrict__
 __global__ void __launch_bounds__(256)
 k_dist_l1_u32(const int32_t* __restrict__ Xq, int n, int d, uint32_t* __restrict__ D, int64_t ld, int64_t c0,
               int64_t c1, const int* __restrict__ exact_f32 = nullptr) {
-    if (exact_f32 && *exact_f32) return;      // k_dist_l1_f32x produces this matrix
+    if (exact_f32 && *exact_f32) return;      // k_dist_l1_f32x / u16x2 produces this matrix
     constexpr int TB = 64, KB = 32;
     __shared__ int32_t sa[KB][TB + 1], sb[KB][TB + 1];
     const int i0 = blockIdx.y * TB;
@@ -574,17 +574,20 @@ k_dist_l1_u32(const int32_t* __restrict__ Xq, int n, int d, uint32_t* __restrict
 __global__ void k_dist_l1_range_init(int d, int* __restrict__ rng) {
     for (int t = threadIdx.x; t < d; t += blockDim.x) { rng[2 * t] = INT_MAX; rng[2 * t + 1] = INT_MIN; }
 }
-__global__ void k_dist_l1_decide(int d, int* __restrict__ rng) {
-    __shared__ long long tot;
-    if (threadIdx.x == 0) tot = 0;
+// rng[2d] = 2: every range < 2^16 (k_dist_l1_u16x2, exact in 32-bit integer
+// arithmetic); 1: sum of ranges < 2^24 (k_dist_l1_f32x); 0: k_dist_l1_u32.
+__global__ void k_dist_l1_decide(int d, int* __restrict__ rng, int allow_packed) {
+    __shared__ long long tot, mx;
+    if (threadIdx.x == 0) { tot = 0; mx = 0; }
     __syncthreads();
     constexpr long long LIM = 1ll << 24;
     for (int t = threadIdx.x; t < d; t += blockDim.x) {
         const long long lo = rng[2 * t], hi = rng[2 * t + 1];
         atomicAdd((unsigned long long*)&tot, (unsigned long long)(hi - lo));
+        atomicMax((unsigned long long*)&mx, (unsigned long long)(hi - lo));
     }
     __syncthreads();
-    if (threadIdx.x == 0) rng[2 * d] = tot < LIM ? 1 : 0;
+    if (threadIdx.x == 0) rng[2 * d] = (allow_packed && mx < 65536) ? 2 : tot < LIM ? 1 : 0;
 }
 __global__ void k_dist_l1_range(const int32_t* __restrict__ Xq, int n, int d, int* __restrict__ rng) {
     const int t = blockIdx.y;
@@ -616,7 +619,7 @@ constexpr int L1F_TB = 128, L1F_KB = 32, L1F_LD = L1F_TB + 4;
 // S_i of the translated coordinates (only when the fp32 kernel is used).
 __global__ void k_dist_l1_rowsum(const int32_t* __restrict__ Xq, int n, int d, const int* __restrict__ rng,
                                  int* __restrict__ rowsum) {
-    if (!rng[2 * d]) return;
+    if (!rng[2 * d]) return;                  // the integer kernel needs no row sums
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= n) return;
     int sum = 0;
@@ -627,7 +630,7 @@ __global__ void k_dist_l1_rowsum(const int32_t* __restrict__ Xq, int n, int d, c
 __global__ void __launch_bounds__(256, 2)
 k_dist_l1_f32x(const int32_t* __restrict__ Xq, int n, int d, uint32_t* __restrict__ D, int64_t ld, int64_t c0,
                int64_t c1, bool vec, const int* __restrict__ rng, const int* __restrict__ rowsum) {
-    if (!rng[2 * d]) return;                  // not exact in fp32: k_dist_l1_u32 runs instead
+    if (rng[2 * d] != 1) return;              // another L1 kernel produces this matrix
     __shared__ __align__(16) float sa[L1F_KB][L1F_LD], sb[L1F_KB][L1F_LD];
     const int i0 = blockIdx.y * L1F_TB;
     const int64_t j0 = c0 + (int64_t)blockIdx.x * L1F_TB;
@@ -685,6 +688,96 @@ k_dist_l1_f32x(const int32_t* __restrict__ Xq, int n, int d, uint32_t* __restric
 #pragma unroll
             for (int v = 0; v < 4; ++v)
                 o[v] = (j + v == i) ? 0u : (uint32_t)(si + sj[h * 4 + v] - (int)acc[u][h * 4 + v]);
+            if (vec && j + 3 < c1) {
+                *reinterpret_cast<uint4*>(Drow + j) = make_uint4(o[0], o[1], o[2], o[3]);
+            } else {
+#pragma unroll
+                for (int v = 0; v < 4; ++v) if (j + v < c1) Drow[j + v] = o[v];
+            }
+        }
+    }
+}
+
+// L1 in packed 16-bit integer arithmetic, exact: with translated coordinates
+// y_t = x_t - min_t < 2^16 (every range below 2^16, decided on the device),
+//     sum_t |y_it - y_jt| = S_i + S_j - 2 sum_t min(y_it, y_jt)   (mod 2^32).
+// Two consecutive dimensions of a row are packed in one 32-bit word; ONE
+// VIMNMX.U16x2 gives both minima of a (row, column) pair and ONE IDP.2A
+// (dp2a with weights (1, 1)) adds them into a 32-bit accumulator: one
+// instruction per element instead of two (k_dist_l1_f32x), no overflow
+// (the accumulator is 32-bit), no flushes.  Tile and thread layout as
+// k_dist_l1_f32x; operands in shared memory as [dim pair][row] words.
+constexpr int L1P_KP = 16;                     // dim pairs per shared-memory chunk
+__global__ void __launch_bounds__(256, 2)
+k_dist_l1_u16x2(const int32_t* __restrict__ Xq, int n, int d, uint32_t* __restrict__ D, int64_t ld, int64_t c0,
+                int64_t c1, bool vec, const int* __restrict__ rng, const int* __restrict__ rowsum) {
+    if (rng[2 * d] != 2) return;              // another L1 kernel produces this matrix
+    __shared__ __align__(16) uint32_t sa[L1P_KP][L1F_LD], sb[L1P_KP][L1F_LD];
+    const int i0 = blockIdx.y * L1F_TB;
+    const int64_t j0 = c0 + (int64_t)blockIdx.x * L1F_TB;
+    const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
+    uint32_t acc[8][8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u)
+#pragma unroll
+        for (int v = 0; v < 8; ++v) acc[u][v] = 0u;
+    const int dp = (d + 1) >> 1;                  // dimension pairs
+    for (int p0 = 0; p0 < dp; p0 += L1P_KP) {
+        for (int idx = threadIdx.x; idx < L1F_TB * L1P_KP; idx += 256) {
+            const int r = idx / L1P_KP, kp = idx % L1P_KP;
+            const int t0 = 2 * (p0 + kp), t1 = t0 + 1;
+            const int lo0 = t0 < d ? __ldg(&rng[2 * t0]) : 0, lo1 = t1 < d ? __ldg(&rng[2 * t1]) : 0;
+            uint32_t wa = 0u, wb = 0u;
+            if (i0 + r < n) {
+                const int32_t* xr = Xq + (int64_t)(i0 + r) * d;
+                const uint32_t y0 = t0 < d ? (uint32_t)(xr[t0] - lo0) : 0u, y1 = t1 < d ? (uint32_t)(xr[t1] - lo1) : 0u;
+                wa = y0 | (y1 << 16);
+            }
+            if (j0 + r < c1) {
+                const int32_t* xr = Xq + (j0 + r) * d;
+                const uint32_t y0 = t0 < d ? (uint32_t)(xr[t0] - lo0) : 0u, y1 = t1 < d ? (uint32_t)(xr[t1] - lo1) : 0u;
+                wb = y0 | (y1 << 16);
+            }
+            sa[kp][r] = wa;
+            sb[kp][r] = wb;
+        }
+        __syncthreads();
+        const int kn = min(L1P_KP, dp - p0);
+#pragma unroll 4
+        for (int kp = 0; kp < kn; ++kp) {
+            const uint4 a0 = *reinterpret_cast<const uint4*>(&sa[kp][ty * 4]);
+            const uint4 a1 = *reinterpret_cast<const uint4*>(&sa[kp][64 + ty * 4]);
+            const uint4 b0 = *reinterpret_cast<const uint4*>(&sb[kp][tx * 4]);
+            const uint4 b1 = *reinterpret_cast<const uint4*>(&sb[kp][64 + tx * 4]);
+            const uint32_t a[8] = {a0.x, a0.y, a0.z, a0.w, a1.x, a1.y, a1.z, a1.w};
+            const uint32_t b[8] = {b0.x, b0.y, b0.z, b0.w, b1.x, b1.y, b1.z, b1.w};
+#pragma unroll
+            for (int u = 0; u < 8; ++u)
+#pragma unroll
+                for (int v = 0; v < 8; ++v) acc[u][v] = __dp2a_lo(__vminu2(a[u], b[v]), 0x0101u, acc[u][v]);
+        }
+        __syncthreads();
+    }
+    uint32_t sj[8];
+#pragma unroll
+    for (int h = 0; h < 2; ++h)
+#pragma unroll
+        for (int v = 0; v < 4; ++v) {
+            const int64_t j = j0 + h * 64 + tx * 4 + v;
+            sj[h * 4 + v] = j < c1 ? (uint32_t)__ldg(&rowsum[j]) : 0u;
+        }
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+        const int i = i0 + (u < 4 ? ty * 4 + u : 64 + ty * 4 + (u - 4));
+        if (i >= n) continue;
+        const uint32_t si = (uint32_t)__ldg(&rowsum[i]);
+        uint32_t* Drow = D + (int64_t)i * ld - c0;
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+            const int64_t j = j0 + h * 64 + tx * 4;
+            uint32_t o[4];
+#pragma unroll
+            for (int v = 0; v < 4; ++v) o[v] = (j + v == i) ? 0u : si + sj[h * 4 + v] - 2u * acc[u][h * 4 + v];
             if (vec && j + 3 < c1) {
                 *reinterpret_cast<uint4*>(Drow + j) = make_uint4(o[0], o[1], o[2], o[3]);
             } else {

@@ -2175,17 +2175,22 @@ km_status kmedoids_dissimilarity(const void* X, km_metric metric, int64_t n, int
         cudaError_t e = dist_scratch(dev, (size_t)(2 * d + 1 + n) * sizeof(int), st, &scr);
         if (e != cudaSuccess) return fail(KM_ENOMEM, "dissimilarity scratch: %s", cudaGetErrorString(e));
         int* rng = (int*)scr;
-        const char* ek = getenv("KM_DIST_L1");          // "int": the integer kernel only
+        // measurement / test override: "int" = the integer kernel only, "f32" =
+        // no packed 16-bit kernel
+        const char* ek = getenv("KM_DIST_L1");
         const bool try_f32 = !(ek && strcmp(ek, "int") == 0);
+        const int allow_packed = (ek && (strcmp(ek, "int") == 0 || strcmp(ek, "f32") == 0)) ? 0 : 1;
         if (try_f32) {
             km::k_dist_l1_range_init<<<1, 256, 0, st>>>(d, rng);
             km::k_dist_l1_range<<<dim3((unsigned)std::min<int64_t>(cdiv(n, 256), 64), (unsigned)d), 256, 0, st>>>(
                 (const int32_t*)X, (int)n, d, rng);
-            km::k_dist_l1_decide<<<1, 256, 0, st>>>(d, rng);
+            km::k_dist_l1_decide<<<1, 256, 0, st>>>(d, rng, allow_packed);
             km::k_dist_l1_rowsum<<<(unsigned)cdiv(n, 256), 256, 0, st>>>((const int32_t*)X, (int)n, d, rng,
                                                                         rng + 2 * d + 1);
             const bool vec = (ld % 4 == 0) && (((uintptr_t)D) % 16 == 0);
             dim3 gf((unsigned)cdiv(col_end - col_begin, km::L1F_TB), (unsigned)cdiv(n, km::L1F_TB));
+            km::k_dist_l1_u16x2<<<gf, 256, 0, st>>>((const int32_t*)X, (int)n, d, (uint32_t*)D, ld, col_begin,
+                                                     col_end, vec, rng, rng + 2 * d + 1);
             km::k_dist_l1_f32x<<<gf, 256, 0, st>>>((const int32_t*)X, (int)n, d, (uint32_t*)D, ld, col_begin, col_end,
                                                     vec, rng, rng + 2 * d + 1);
         }

@@ -111,11 +111,14 @@ def test_dissimilarity_argument_errors():
     (1000, 5, -3000, 3000, 3, 997),             # ragged 128-tiles, unaligned slab start
     (385, 64, 0, 5000, 0, 385),                 # C5-like range, three row tiles + 1 row
     (129, 40, -100, 100, 1, 2),                 # one column
+    (260, 7, 0, 65535, 0, 260),                 # ranges 2^16 - 1: the packed 16-bit kernel at its limit
+    (260, 7, 0, 65536, 0, 260),                 # ranges 2^16: the fp32 kernel
 ])
 def test_l1_fp32_path_exact_and_integer_fallback(n, d, lo, hi, c0, c1):
-    """The fp32 L1 kernel (translated coordinates, S_i + S_j - 2 sum min) is
-    used only when sum_t (max_t - min_t) < 2^24 (decided on the device); both
-    sides of that limit must equal the integer definition exactly."""
+    """The translated-coordinate L1 kernels (S_i + S_j - 2 sum min) are used
+    only where exact: packed 16-bit when every range < 2^16, fp32 when the
+    sum of ranges < 2^24 (decided on the device), else the integer kernel;
+    every side of both limits must equal the integer definition exactly."""
     from paper_2008_05171_b200 import kmedoids_dissimilarity
     rng = np.random.default_rng(n + d)
     Xq = rng.integers(lo, hi, size=(n, d), endpoint=True).astype(np.int32)
@@ -133,3 +136,14 @@ def test_l1_integer_kernel_forced(monkeypatch):
     Xq = rng.integers(-5000, 5000, size=(333, 17)).astype(np.int32)
     Dg = kmedoids_dissimilarity(torch.from_numpy(Xq).cuda(), "l1")
     assert (Dg[:, :333].cpu().numpy().view(np.uint32).astype(np.int64) == oracle.dist_l1(Xq)).all()
+
+
+@pytest.mark.parametrize("n,d,c0,c1", [(333, 17, 0, 333), (1000, 5, 3, 997), (129, 64, 0, 129)])
+def test_l1_fp32_kernel_forced(monkeypatch, n, d, c0, c1):
+    """KM_DIST_L1=f32 disables the packed kernel: the fp32 one on small ranges."""
+    from paper_2008_05171_b200 import kmedoids_dissimilarity
+    monkeypatch.setenv("KM_DIST_L1", "f32")
+    rng = np.random.default_rng(n + 3 * d)
+    Xq = rng.integers(-5000, 5000, size=(n, d)).astype(np.int32)
+    Dg = kmedoids_dissimilarity(torch.from_numpy(Xq).cuda(), "l1", col_begin=c0, col_end=c1)
+    assert (Dg[:, :c1 - c0].cpu().numpy().view(np.uint32).astype(np.int64) == oracle.dist_l1(Xq)[:, c0:c1]).all()
