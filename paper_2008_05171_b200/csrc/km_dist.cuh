@@ -643,7 +643,9 @@ k_dist_l1_f32x(const int32_t* __restrict__ Xq, int n, int d, uint32_t* __restric
     for (int k0 = 0; k0 < d; k0 += L1F_KB) {
         // 128 rows x 32 dims per operand: consecutive threads take consecutive
         // dims of one row (coalesced), written transposed; padding is 0
-        for (int idx = threadIdx.x; idx < L1F_TB * L1F_KB; idx += 256) {
+#pragma unroll
+        for (int it = 0; it < L1F_TB * L1F_KB / 256; ++it) {
+            const int idx = it * 256 + threadIdx.x;
             const int r = idx / L1F_KB, k = idx % L1F_KB;
             const bool kin = k0 + k < d;
             const int lo = kin ? __ldg(&rng[2 * (k0 + k)]) : 0;
@@ -705,44 +707,73 @@ k_dist_l1_f32x(const int32_t* __restrict__ Xq, int n, int d, uint32_t* __restric
 // VIMNMX.U16x2 gives both minima of a (row, column) pair and ONE IDP.2A
 // (dp2a with weights (1, 1)) adds them into a 32-bit accumulator: one
 // instruction per element instead of two (k_dist_l1_f32x), no overflow
-// (the accumulator is 32-bit), no flushes.  Tile and thread layout as
-// k_dist_l1_f32x; operands in shared memory as [dim pair][row] words.
-constexpr int L1P_KP = 16;                     // dim pairs per shared-memory chunk
+// (the accumulator is 32-bit), no flushes.
+//
+// The words are packed once (k_dist_l1_pack16) in the exact shared-memory
+// image a tile uses -- [128-row tile][dim pair][row] -- so a block fetches its
+// A and B operands with two bulk copies (no per-element loads, no
+// registers: the first version spent most stall samples waiting on its
+// element loads).  Tile and thread layout as k_dist_l1_f32x.
+constexpr int L1P_KP = 32;                     // dim pairs per shared-memory chunk (d <= 64: one chunk)
+
+// packed operand tiles of the rows [r0, r1): out[(tile * dp + p) * 128 + r]
+__global__ void k_dist_l1_pack16(const int32_t* __restrict__ Xq, int d, int64_t r0, int64_t r1,
+                                 const int* __restrict__ rng, uint32_t* __restrict__ out) {
+    if (rng[2 * d] != 2) return;
+    const int dp = (d + 1) >> 1;
+    const int64_t tile = blockIdx.x;
+    for (int idx = threadIdx.x; idx < dp * L1F_TB; idx += blockDim.x) {
+        const int p = idx / L1F_TB, r = idx % L1F_TB;
+        const int64_t row = r0 + tile * L1F_TB + r;
+        const int t0 = 2 * p, t1 = t0 + 1;
+        uint32_t w = 0u;
+        if (row < r1) {
+            const int32_t* xr = Xq + row * d;
+            const uint32_t y0 = (uint32_t)(xr[t0] - __ldg(&rng[2 * t0]));
+            const uint32_t y1 = t1 < d ? (uint32_t)(xr[t1] - __ldg(&rng[2 * t1])) : 0u;
+            w = y0 | (y1 << 16);
+        }
+        out[(tile * dp + p) * L1F_TB + r] = w;
+    }
+}
+
 __global__ void __launch_bounds__(256, 2)
-k_dist_l1_u16x2(const int32_t* __restrict__ Xq, int n, int d, uint32_t* __restrict__ D, int64_t ld, int64_t c0,
-                int64_t c1, bool vec, const int* __restrict__ rng, const int* __restrict__ rowsum) {
+k_dist_l1_u16x2(const uint32_t* __restrict__ PA, const uint32_t* __restrict__ PB, int n, int d,
+                uint32_t* __restrict__ D, int64_t ld, int64_t c0, int64_t c1, bool vec, const int* __restrict__ rng,
+                const int* __restrict__ rowsum) {
     if (rng[2 * d] != 2) return;              // another L1 kernel produces this matrix
-    __shared__ __align__(16) uint32_t sa[L1P_KP][L1F_LD], sb[L1P_KP][L1F_LD];
+    __shared__ __align__(128) uint32_t sa[L1P_KP][L1F_TB], sb[L1P_KP][L1F_TB];
+    __shared__ __align__(8) uint64_t bar;
     const int i0 = blockIdx.y * L1F_TB;
     const int64_t j0 = c0 + (int64_t)blockIdx.x * L1F_TB;
     const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
+    const int dp = (d + 1) >> 1;
+    if (threadIdx.x == 0) {
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" :: "r"(dt_smem_u32(&bar)));
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
     uint32_t acc[8][8];
 #pragma unroll
     for (int u = 0; u < 8; ++u)
 #pragma unroll
         for (int v = 0; v < 8; ++v) acc[u][v] = 0u;
-    const int dp = (d + 1) >> 1;                  // dimension pairs
+    uint32_t ph = 0;
     for (int p0 = 0; p0 < dp; p0 += L1P_KP) {
-        for (int idx = threadIdx.x; idx < L1F_TB * L1P_KP; idx += 256) {
-            const int r = idx / L1P_KP, kp = idx % L1P_KP;
-            const int t0 = 2 * (p0 + kp), t1 = t0 + 1;
-            const int lo0 = t0 < d ? __ldg(&rng[2 * t0]) : 0, lo1 = t1 < d ? __ldg(&rng[2 * t1]) : 0;
-            uint32_t wa = 0u, wb = 0u;
-            if (i0 + r < n) {
-                const int32_t* xr = Xq + (int64_t)(i0 + r) * d;
-                const uint32_t y0 = t0 < d ? (uint32_t)(xr[t0] - lo0) : 0u, y1 = t1 < d ? (uint32_t)(xr[t1] - lo1) : 0u;
-                wa = y0 | (y1 << 16);
-            }
-            if (j0 + r < c1) {
-                const int32_t* xr = Xq + (j0 + r) * d;
-                const uint32_t y0 = t0 < d ? (uint32_t)(xr[t0] - lo0) : 0u, y1 = t1 < d ? (uint32_t)(xr[t1] - lo1) : 0u;
-                wb = y0 | (y1 << 16);
-            }
-            sa[kp][r] = wa;
-            sb[kp][r] = wb;
-        }
-        __syncthreads();
         const int kn = min(L1P_KP, dp - p0);
+        if (threadIdx.x == 0) {
+            // one arrival announcing both copies' bytes, then the two copies
+            const uint32_t bytes = (uint32_t)kn * L1F_TB * 4u;
+            asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;"
+                         :: "r"(dt_smem_u32(&bar)), "r"(2u * bytes) : "memory");
+            asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+                         :: "r"(dt_smem_u32(&sa[0][0])), "l"(PA + ((int64_t)blockIdx.y * dp + p0) * L1F_TB),
+                            "r"(bytes), "r"(dt_smem_u32(&bar)) : "memory");
+            asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+                         :: "r"(dt_smem_u32(&sb[0][0])), "l"(PB + ((int64_t)blockIdx.x * dp + p0) * L1F_TB),
+                            "r"(bytes), "r"(dt_smem_u32(&bar)) : "memory");
+        }
+        dt_wait(&bar, ph); ph ^= 1;
 #pragma unroll 4
         for (int kp = 0; kp < kn; ++kp) {
             const uint4 a0 = *reinterpret_cast<const uint4*>(&sa[kp][ty * 4]);
@@ -756,7 +787,7 @@ k_dist_l1_u16x2(const int32_t* __restrict__ Xq, int n, int d, uint32_t* __restri
 #pragma unroll
                 for (int v = 0; v < 8; ++v) acc[u][v] = __dp2a_lo(__vminu2(a[u], b[v]), 0x0101u, acc[u][v]);
         }
-        __syncthreads();
+        __syncthreads();                          // the tiles are overwritten by the next chunk
     }
     uint32_t sj[8];
 #pragma unroll

@@ -2172,7 +2172,14 @@ km_status kmedoids_dissimilarity(const void* X, km_metric metric, int64_t n, int
         cudaGetDevice(&dev);
         std::lock_guard<std::mutex> lock(g_dist_mu);
         float* scr = nullptr;
-        cudaError_t e = dist_scratch(dev, (size_t)(2 * d + 1 + n) * sizeof(int), st, &scr);
+        // scratch: ranges + flag [2d + 1], row sums [n], packed 16-bit operand
+        // tiles of the rows (A) and of the slab's columns (B; shared when c0 == 0)
+        const int dp = (d + 1) / 2;
+        const int64_t ntr = cdiv(n, km::L1F_TB), ntc = cdiv(col_end - col_begin, km::L1F_TB);
+        const size_t off_pa = (size_t)cdiv(2 * d + 1 + n, 32) * 32;            // 128-byte aligned
+        const size_t pa_words = (size_t)ntr * dp * km::L1F_TB;
+        const size_t pb_words = col_begin == 0 ? 0 : (size_t)ntc * dp * km::L1F_TB;
+        cudaError_t e = dist_scratch(dev, (off_pa + pa_words + pb_words) * sizeof(int), st, &scr);
         if (e != cudaSuccess) return fail(KM_ENOMEM, "dissimilarity scratch: %s", cudaGetErrorString(e));
         int* rng = (int*)scr;
         // measurement / test override: "int" = the integer kernel only, "f32" =
@@ -2189,8 +2196,13 @@ km_status kmedoids_dissimilarity(const void* X, km_metric metric, int64_t n, int
                                                                         rng + 2 * d + 1);
             const bool vec = (ld % 4 == 0) && (((uintptr_t)D) % 16 == 0);
             dim3 gf((unsigned)cdiv(col_end - col_begin, km::L1F_TB), (unsigned)cdiv(n, km::L1F_TB));
-            km::k_dist_l1_u16x2<<<gf, 256, 0, st>>>((const int32_t*)X, (int)n, d, (uint32_t*)D, ld, col_begin,
-                                                     col_end, vec, rng, rng + 2 * d + 1);
+            uint32_t* PA = (uint32_t*)scr + off_pa;
+            uint32_t* PB = col_begin == 0 ? PA : PA + pa_words;
+            km::k_dist_l1_pack16<<<(unsigned)ntr, 256, 0, st>>>((const int32_t*)X, d, 0, n, rng, PA);
+            if (col_begin != 0)
+                km::k_dist_l1_pack16<<<(unsigned)ntc, 256, 0, st>>>((const int32_t*)X, d, col_begin, col_end, rng, PB);
+            km::k_dist_l1_u16x2<<<gf, 256, 0, st>>>(PA, PB, (int)n, d, (uint32_t*)D, ld, col_begin, col_end, vec, rng,
+                                                     rng + 2 * d + 1);
             km::k_dist_l1_f32x<<<gf, 256, 0, st>>>((const int32_t*)X, (int)n, d, (uint32_t*)D, ld, col_begin, col_end,
                                                     vec, rng, rng + 2 * d + 1);
         }
