@@ -2202,13 +2202,16 @@ k_fp2_sequential(const T* __restrict__ D, int64_t ld, const T* __restrict__ cols
                  const Rec<A>* __restrict__ best, int* __restrict__ M, int* __restrict__ point_slot,
                  T* __restrict__ MC, int* __restrict__ near, int* __restrict__ sec, T* __restrict__ dn,
                  T* __restrict__ ds, T* __restrict__ colbuf, A* __restrict__ td, A* __restrict__ partials,
-                 Decision<A>* __restrict__ dec, Rec<A>* __restrict__ trace, int trace_cap) {
+                 Decision<A>* __restrict__ dec, Rec<A>* __restrict__ trace, int trace_cap,
+                 int* __restrict__ rescan, int* __restrict__ rescan_count) {
     namespace cg = cooperative_groups;
     cg::grid_group grid = cg::this_grid();
     __shared__ A sred[8];
     __shared__ int s_apply;
     const int nth = gridDim.x * blockDim.x;
     const int tid = blockIdx.x * blockDim.x + threadIdx.x;
+    const int lane = threadIdx.x & 31;
+    const int gwarp = tid >> 5, nwarps = nth >> 5;
     for (int r = 0; r < m; ++r) {
         const int i = order[r];
         const int c = best[i].c;
@@ -2217,6 +2220,8 @@ k_fp2_sequential(const T* __restrict__ D, int64_t ld, const T* __restrict__ cols
         const bool skip = (r > 0) && (point_slot[c] >= 0);
         const A tdv = __ldcg(td);
         if (skip) continue;
+        // (the previous swap's rescan list was consumed before the last grid sync)
+        if (tid == 0) *rescan_count = 0;
         // phase 1: gather column c, partial sums of dTD(m_i, x_c)
         A part = 0;
         for (int o = tid; o < n; o += nth) {
@@ -2248,20 +2253,25 @@ k_fp2_sequential(const T* __restrict__ D, int64_t ld, const T* __restrict__ cols
             }
         }
         grid.sync();
-        // phase 2: every block reduces the partials in the same order -> same decision
-        if (threadIdx.x == 0) {
+        // phase 2: every block reduces the partials in the same order -> same
+        // decision (warp 0: strided loads, all in flight, then an xor butterfly,
+        // whose result is the same bits in every lane and every block)
+        if (threadIdx.x < 32) {
             A v;
             if (r == 0) {
                 v = best[i].v;
             } else {
-                v = 0;
-                for (int b = 0; b < (int)gridDim.x; ++b) v += __ldcg(&partials[b]);
+                A t = 0;
+                for (int b = lane; b < (int)gridDim.x; b += 32) t += __ldcg(&partials[b]);
+#pragma unroll
+                for (int x = 16; x >= 1; x >>= 1) t += __shfl_xor_sync(FULL, t, x);
+                v = t;
             }
             bool ok;
             if (std::is_same<A, double>::value) ok = (double)v < -1e-12 * fabs((double)tdv);
             else ok = v < 0;
-            s_apply = ok ? 1 : 0;
-            if (ok && blockIdx.x == 0) {
+            if (lane == 0) s_apply = ok ? 1 : 0;
+            if (ok && blockIdx.x == 0 && lane == 0) {
                 const int old = M[i];
                 M[i] = c;
                 point_slot[old] = -1;
@@ -2279,26 +2289,46 @@ k_fp2_sequential(const T* __restrict__ D, int64_t ld, const T* __restrict__ cols
         }
         __syncthreads();
         if (s_apply) {
-            // phase 3: MC[i] <- column c, incremental nearest/second update (own objects only)
+            // phase 3: MC[i] <- column c, incremental nearest/second update;
+            // objects whose nearest/second was slot i are listed for a rescan
             for (int o = tid; o < n; o += nth) {
                 const T x = colbuf[o];
                 MC[(int64_t)i * n + o] = x;
-                int j1 = near[o], j2 = sec[o];
+                const int j1 = near[o], j2 = sec[o];
                 if (j1 == i || j2 == i) {
-                    T a0 = MC[o], b0 = MC[(int64_t)n + o];
-                    T d1, d2;
-                    if (b0 < a0) { d1 = b0; j1 = 1; d2 = a0; j2 = 0; } else { d1 = a0; j1 = 0; d2 = b0; j2 = 1; }
-                    for (int j = 2; j < k; ++j) {
-                        const T d = (j == i) ? x : MC[(int64_t)j * n + o];
-                        if (d < d1) { d2 = d1; j2 = j1; d1 = d; j1 = j; }
-                        else if (d < d2) { d2 = d; j2 = j; }
-                    }
-                    near[o] = j1; sec[o] = j2; dn[o] = d1; ds[o] = d2;
+                    rescan[atomicAdd(rescan_count, 1)] = o;
                 } else {
                     const T d1 = dn[o], d2 = ds[o];
                     if (x < d1 || (x == d1 && i < j1)) { near[o] = i; dn[o] = x; sec[o] = j1; ds[o] = d1; }
                     else if (x < d2 || (x == d2 && i < j2)) { sec[o] = i; ds[o] = x; }
                 }
+            }
+            grid.sync();
+            // phase 4: (d, j) lexicographic top-2 of the listed objects, one warp
+            // each (lanes over the slots, all loads in flight; as k_assign_rescan)
+            const int cnt = __ldcg(rescan_count);
+            for (int e = gwarp; e < cnt; e += nwarps) {
+                const int o = __ldcg(&rescan[e]);
+                T d1 = dmax<T>(), d2 = dmax<T>();
+                int j1 = INT_MAX, j2 = INT_MAX;
+#pragma unroll 8
+                for (int j = lane; j < k; j += 32) {
+                    const T d = __ldcg(&MC[(int64_t)j * n + o]);
+                    if (lex_lt(d, j, d1, j1)) { d2 = d1; j2 = j1; d1 = d; j1 = j; }
+                    else if (lex_lt(d, j, d2, j2)) { d2 = d; j2 = j; }
+                }
+#pragma unroll
+                for (int x = 16; x >= 1; x >>= 1) {
+                    const T e1 = __shfl_xor_sync(FULL, d1, x), e2 = __shfl_xor_sync(FULL, d2, x);
+                    const int f1 = __shfl_xor_sync(FULL, j1, x), f2 = __shfl_xor_sync(FULL, j2, x);
+                    if (lex_lt(e1, f1, d1, j1)) {
+                        if (lex_lt(d1, j1, e2, f2)) { d2 = d1; j2 = j1; } else { d2 = e2; j2 = f2; }
+                        d1 = e1; j1 = f1;
+                    } else if (lex_lt(e1, f1, d2, j2)) {
+                        d2 = e1; j2 = f1;
+                    }
+                }
+                if (lane == 0) { near[o] = j1; sec[o] = j2; dn[o] = d1; ds[o] = d2; }
             }
         }
         grid.sync();

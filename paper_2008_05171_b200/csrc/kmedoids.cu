@@ -908,8 +908,9 @@ struct Impl : ImplBase {
         T* cb = colbuf; A* tdp = td; A* pp = fp2_partials; Dec* dp = dec; Rec* tr = trace; int tc = trace_cap;
         int* op = fp2_order; Rec* bp = fp2_best;
         const T* csp = colsrc; const int* cip = colidx_dev;
+        int* rsp = rescan; int* rcp = rescan_count;
         void* args[] = {&Dp, &ldv, &csp, &cip, &nn, &kk, &op, &m, &bp, &Mp, &psp, &MCp, &nr, &sc, &dnp, &dsp, &cb,
-                        &tdp, &pp, &dp, &tr, &tc};
+                        &tdp, &pp, &dp, &tr, &tc, &rsp, &rcp};
         KM_CK(cudaLaunchCooperativeKernel((void*)km::k_fp2_sequential<T, A>, dim3(fp2_blocks), dim3(256), args, 0,
                                           st));
         ++launches;
