@@ -2184,154 +2184,208 @@ __global__ void k_fp2_slot_reduce(int k, int split, const Rec<A>* __restrict__ p
     out[i] = b;
 }
 
-// The sequential phase of one FastPAM2 iteration as ONE cooperative kernel
-// (grid-wide syncs instead of ~6 launches per swap).  order[0..m) are the
-// improving slots sorted by (v_i, i) (host), best[i] = (v_i, i, c_i).
-// r = 0 applies best[order[0]] as is (it is FastPAM1's swap).  Every later
-// slot i: skipped if c_i became a medoid, else dTD(m_i, x_c_i) is recomputed
-// on the current cache in one pass over the objects,
+// The sequential phase of one FastPAM2 iteration as ONE cooperative kernel.
+// order[0..m) are the improving slots sorted by (v_i, i) (host), best[i] =
+// (v_i, i, c_i).  r = 0 applies best[order[0]] as is (it is FastPAM1's swap).
+// Every later slot i (in order): skipped if c_i became a medoid, else
+// dTD(m_i, x_c_i) is recomputed on the current cache in one pass over the
+// objects,
 //    sum_o [nearest(o)=i](d_s - d_n) + [d<d_n](d - d_n)
 //        + [nearest(o)=i]([d<d_n](d_n - d_s) + [d_n<=d<d_s](d - d_s)),
 // and the swap is applied iff it still improves (reading R5).  Applying =
-// M[i] <- c, TD += dTD, MC[i] <- column c, incremental nearest/second update.
+// M[i] <- c, TD += dTD, MC[i] <- column c, incremental nearest/second update
+// (+ warp rescans of the objects whose nearest/second was slot i).
+//
+// Speculative batches: the state changes only when a swap is applied (a few
+// per iteration, while m is up to k), so the next FP2_B unskipped entries are
+// re-evaluated TOGETHER on the current state in one pass over the objects
+// (their columns land in cols[b][o]); the first improving entry of the batch
+// is exactly the one the sequential loop applies next (every earlier entry
+// was evaluated on the same state and rejected).  It is applied; entries
+// after it were evaluated on a stale state and start the next batch.  Two
+// grid syncs per batch (plus two per applied swap) instead of two per entry.
 // Applied swaps are appended to trace[] (slot, c, dTD).
+constexpr int FP2_B = 32;
 template <typename T, typename A>
 __global__ void __launch_bounds__(256)
 k_fp2_sequential(const T* __restrict__ D, int64_t ld, const T* __restrict__ colsrc, const int* __restrict__ colidx,
                  int n, int k, const int* __restrict__ order, int m,
                  const Rec<A>* __restrict__ best, int* __restrict__ M, int* __restrict__ point_slot,
                  T* __restrict__ MC, int* __restrict__ near, int* __restrict__ sec, T* __restrict__ dn,
-                 T* __restrict__ ds, T* __restrict__ colbuf, A* __restrict__ td, A* __restrict__ partials,
+                 T* __restrict__ ds, T* __restrict__ cols, A* __restrict__ td, A* __restrict__ partials,
                  Decision<A>* __restrict__ dec, Rec<A>* __restrict__ trace, int trace_cap,
                  int* __restrict__ rescan, int* __restrict__ rescan_count) {
     namespace cg = cooperative_groups;
     cg::grid_group grid = cg::this_grid();
-    __shared__ A sred[8];
-    __shared__ int s_apply;
+    __shared__ A sred[8][FP2_B];
+    __shared__ int s_r[FP2_B], s_c[FP2_B], s_i[FP2_B];
+    __shared__ int s_nb, s_next, s_pick;
+    __shared__ A s_v;
     const int nth = gridDim.x * blockDim.x;
     const int tid = blockIdx.x * blockDim.x + threadIdx.x;
-    const int lane = threadIdx.x & 31;
+    const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
     const int gwarp = tid >> 5, nwarps = nth >> 5;
-    for (int r = 0; r < m; ++r) {
-        const int i = order[r];
-        const int c = best[i].c;
-        // point_slot and td change only in phase 2 of a step (block 0), after
-        // every block has read them here: all blocks take the same decisions.
-        const bool skip = (r > 0) && (point_slot[c] >= 0);
-        const A tdv = __ldcg(td);
-        if (skip) continue;
-        // (the previous swap's rescan list was consumed before the last grid sync)
-        if (tid == 0) *rescan_count = 0;
-        // phase 1: gather column c, partial sums of dTD(m_i, x_c)
-        A part = 0;
-        for (int o = tid; o < n; o += nth) {
-            // candidate column: gathered (sharded) or read from D (single GPU)
-            const T x = colsrc ? colsrc[(int64_t)colidx[r] * n + o] : D[(int64_t)o * ld + c];
-            colbuf[o] = x;
-            if (r > 0) {
-                const T a = dn[o], b = ds[o];
-                const bool mine = near[o] == i;
-                A f = 0;
-                if (x < a) f += (A)x - (A)a;
-                if (mine) {
-                    f += (A)b - (A)a;
-                    if (x < a) f += (A)a - (A)b;
-                    else if (x < b) f += (A)x - (A)b;
+    int r = 0, round = 0;
+    while (r < m) {
+        // ---- batch (every block identically: the state is the same everywhere);
+        // the barrier keeps thread 0 from overwriting the shared batch / pick
+        // values before every thread of the block has read the last ones
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            int nb = 0, q = r;
+            if (r == 0) {                            // FastPAM1's swap, applied as is
+                s_r[0] = 0; s_i[0] = order[0]; s_c[0] = best[order[0]].c; nb = 1; q = 1;
+            } else {
+                for (; q < m && nb < FP2_B; ++q) {
+                    const int i = order[q], c = best[i].c;
+                    if (point_slot[c] >= 0) continue;   // c became a medoid: skipped
+                    s_r[nb] = q; s_i[nb] = i; s_c[nb] = c; ++nb;
                 }
-                part += f;
+            }
+            s_nb = nb; s_next = q;
+        }
+        __syncthreads();
+        const int nb = s_nb;
+        if (nb == 0) break;                          // (uniform across blocks)
+        const A tdv = __ldcg(td);
+        if (tid == 0) *rescan_count = 0;             // the last rescan list was consumed before a grid sync
+        // ---- phase 1: columns of the batch, partial re-evaluations
+        A part[FP2_B];
+#pragma unroll
+        for (int b = 0; b < FP2_B; ++b) part[b] = 0;
+        for (int o = tid; o < n; o += nth) {
+            const T a = dn[o], bb = ds[o];
+            const int no = near[o];
+#pragma unroll
+            for (int b = 0; b < FP2_B; ++b) {
+                if (b >= nb) continue;               // (fully unrolled: part[] stays in registers)
+                const T x = colsrc ? colsrc[(int64_t)colidx[s_r[b]] * n + o] : D[(int64_t)o * ld + s_c[b]];
+                cols[(int64_t)b * n + o] = x;
+                if (r > 0) {
+                    A f = 0;
+                    if (x < a) f += (A)x - (A)a;
+                    if (no == s_i[b]) {
+                        f += (A)bb - (A)a;
+                        if (x < a) f += (A)a - (A)bb;
+                        else if (x < bb) f += (A)x - (A)bb;
+                    }
+                    part[b] += f;
+                }
             }
         }
+        A* pbuf = partials + (size_t)(round & 1) * gridDim.x * FP2_B;   // double-buffered across batches
         if (r > 0) {
 #pragma unroll
-            for (int x = 16; x >= 1; x >>= 1) part += __shfl_xor_sync(FULL, part, x);
-            if ((threadIdx.x & 31) == 0) sred[threadIdx.x >> 5] = part;
+            for (int b = 0; b < FP2_B; ++b) {
+                if (b >= nb) continue;
+                A t = part[b];
+#pragma unroll
+                for (int x = 16; x >= 1; x >>= 1) t += __shfl_xor_sync(FULL, t, x);
+                if (lane == 0) sred[wib][b] = t;
+            }
             __syncthreads();
-            if (threadIdx.x == 0) {
+            if (threadIdx.x < FP2_B && threadIdx.x < nb) {
                 A t = 0;
-                for (int q = 0; q < (int)(blockDim.x >> 5); ++q) t += sred[q];
-                partials[blockIdx.x] = t;
+                for (int w = 0; w < (int)(blockDim.x >> 5); ++w) t += sred[w][threadIdx.x];
+                pbuf[(size_t)blockIdx.x * FP2_B + threadIdx.x] = t;
             }
         }
         grid.sync();
-        // phase 2: every block reduces the partials in the same order -> same
-        // decision (warp 0: strided loads, all in flight, then an xor butterfly,
-        // whose result is the same bits in every lane and every block)
-        if (threadIdx.x < 32) {
-            A v;
-            if (r == 0) {
-                v = best[i].v;
-            } else {
+        // ---- phase 2: every block reduces the partials in the same order (warp
+        // w: entries b = w, w+8, ...; strided loads + xor butterfly, identical
+        // bits everywhere) and picks the first improving entry
+        if (r == 0) {
+            if (threadIdx.x == 0) { s_pick = 0; s_v = best[s_i[0]].v; }
+        } else {
+            for (int b = wib; b < nb; b += (int)(blockDim.x >> 5)) {
                 A t = 0;
-                for (int b = lane; b < (int)gridDim.x; b += 32) t += __ldcg(&partials[b]);
+                for (int q = lane; q < (int)gridDim.x; q += 32) t += __ldcg(&pbuf[(size_t)q * FP2_B + b]);
 #pragma unroll
                 for (int x = 16; x >= 1; x >>= 1) t += __shfl_xor_sync(FULL, t, x);
-                v = t;
+                if (lane == 0) sred[0][b] = t;       // sred rows are free again
             }
-            bool ok;
-            if (std::is_same<A, double>::value) ok = (double)v < -1e-12 * fabs((double)tdv);
-            else ok = v < 0;
-            if (lane == 0) s_apply = ok ? 1 : 0;
-            if (ok && blockIdx.x == 0 && lane == 0) {
-                const int old = M[i];
-                M[i] = c;
-                point_slot[old] = -1;
-                point_slot[c] = i;
-                *td = tdv + v;
-                const int sw = dec->swaps;
-                if (sw < trace_cap) { Rec<A> t; t.v = v; t.slot = i; t.c = c; trace[sw] = t; }
-                dec->swaps = sw + 1;
-                dec->apply = 1;
-                dec->slot = i;
-                dec->c = c;
-                dec->dtd = v;
-                dec->old_m = old;
+            __syncthreads();
+            if (threadIdx.x == 0) {
+                int pick = -1;
+                for (int b = 0; b < nb && pick < 0; ++b) {
+                    const A v = sred[0][b];
+                    bool ok;
+                    if (std::is_same<A, double>::value) ok = (double)v < -1e-12 * fabs((double)tdv);
+                    else ok = v < 0;
+                    if (ok) { pick = b; s_v = v; }
+                }
+                s_pick = pick;
             }
         }
         __syncthreads();
-        if (s_apply) {
-            // phase 3: MC[i] <- column c, incremental nearest/second update;
-            // objects whose nearest/second was slot i are listed for a rescan
-            for (int o = tid; o < n; o += nth) {
-                const T x = colbuf[o];
-                MC[(int64_t)i * n + o] = x;
-                const int j1 = near[o], j2 = sec[o];
-                if (j1 == i || j2 == i) {
-                    rescan[atomicAdd(rescan_count, 1)] = o;
-                } else {
-                    const T d1 = dn[o], d2 = ds[o];
-                    if (x < d1 || (x == d1 && i < j1)) { near[o] = i; dn[o] = x; sec[o] = j1; ds[o] = d1; }
-                    else if (x < d2 || (x == d2 && i < j2)) { sec[o] = i; ds[o] = x; }
-                }
-            }
-            grid.sync();
-            // phase 4: (d, j) lexicographic top-2 of the listed objects, one warp
-            // each (lanes over the slots, all loads in flight; as k_assign_rescan)
-            const int cnt = __ldcg(rescan_count);
-            for (int e = gwarp; e < cnt; e += nwarps) {
-                const int o = __ldcg(&rescan[e]);
-                T d1 = dmax<T>(), d2 = dmax<T>();
-                int j1 = INT_MAX, j2 = INT_MAX;
-#pragma unroll 8
-                for (int j = lane; j < k; j += 32) {
-                    const T d = __ldcg(&MC[(int64_t)j * n + o]);
-                    if (lex_lt(d, j, d1, j1)) { d2 = d1; j2 = j1; d1 = d; j1 = j; }
-                    else if (lex_lt(d, j, d2, j2)) { d2 = d; j2 = j; }
-                }
-#pragma unroll
-                for (int x = 16; x >= 1; x >>= 1) {
-                    const T e1 = __shfl_xor_sync(FULL, d1, x), e2 = __shfl_xor_sync(FULL, d2, x);
-                    const int f1 = __shfl_xor_sync(FULL, j1, x), f2 = __shfl_xor_sync(FULL, j2, x);
-                    if (lex_lt(e1, f1, d1, j1)) {
-                        if (lex_lt(d1, j1, e2, f2)) { d2 = d1; j2 = j1; } else { d2 = e2; j2 = f2; }
-                        d1 = e1; j1 = f1;
-                    } else if (lex_lt(e1, f1, d2, j2)) {
-                        d2 = e1; j2 = f1;
-                    }
-                }
-                if (lane == 0) { near[o] = j1; sec[o] = j2; dn[o] = d1; ds[o] = d2; }
+        const int pick = s_pick;
+        if (pick < 0) {                              // no entry of the batch improves
+            r = s_next;
+            ++round;
+            continue;
+        }
+        const int i = s_i[pick], c = s_c[pick];
+        if (blockIdx.x == 0 && threadIdx.x == 0) {
+            const A v = s_v;
+            const int old = M[i];
+            M[i] = c;
+            point_slot[old] = -1;
+            point_slot[c] = i;
+            *td = tdv + v;
+            const int sw = dec->swaps;
+            if (sw < trace_cap) { Rec<A> t; t.v = v; t.slot = i; t.c = c; trace[sw] = t; }
+            dec->swaps = sw + 1;
+            dec->apply = 1;
+            dec->slot = i;
+            dec->c = c;
+            dec->dtd = v;
+            dec->old_m = old;
+        }
+        // ---- phase 3: MC[i] <- column c, incremental nearest/second update;
+        // objects whose nearest/second was slot i are listed for a rescan
+        const T* colp = cols + (int64_t)pick * n;
+        for (int o = tid; o < n; o += nth) {
+            const T x = colp[o];
+            MC[(int64_t)i * n + o] = x;
+            const int j1 = near[o], j2 = sec[o];
+            if (j1 == i || j2 == i) {
+                rescan[atomicAdd(rescan_count, 1)] = o;
+            } else {
+                const T d1 = dn[o], d2 = ds[o];
+                if (x < d1 || (x == d1 && i < j1)) { near[o] = i; dn[o] = x; sec[o] = j1; ds[o] = d1; }
+                else if (x < d2 || (x == d2 && i < j2)) { sec[o] = i; ds[o] = x; }
             }
         }
         grid.sync();
+        // ---- phase 4: (d, j) lexicographic top-2 of the listed objects, one warp
+        // each (lanes over the slots; as k_assign_rescan)
+        const int cnt = __ldcg(rescan_count);
+        for (int e = gwarp; e < cnt; e += nwarps) {
+            const int o = __ldcg(&rescan[e]);
+            T d1 = dmax<T>(), d2 = dmax<T>();
+            int j1 = INT_MAX, j2 = INT_MAX;
+#pragma unroll 8
+            for (int j = lane; j < k; j += 32) {
+                const T d = __ldcg(&MC[(int64_t)j * n + o]);
+                if (lex_lt(d, j, d1, j1)) { d2 = d1; j2 = j1; d1 = d; j1 = j; }
+                else if (lex_lt(d, j, d2, j2)) { d2 = d; j2 = j; }
+            }
+#pragma unroll
+            for (int x = 16; x >= 1; x >>= 1) {
+                const T e1 = __shfl_xor_sync(FULL, d1, x), e2 = __shfl_xor_sync(FULL, d2, x);
+                const int f1 = __shfl_xor_sync(FULL, j1, x), f2 = __shfl_xor_sync(FULL, j2, x);
+                if (lex_lt(e1, f1, d1, j1)) {
+                    if (lex_lt(d1, j1, e2, f2)) { d2 = d1; j2 = j1; } else { d2 = e2; j2 = f2; }
+                    d1 = e1; j1 = f1;
+                } else if (lex_lt(e1, f1, d2, j2)) {
+                    d2 = e1; j2 = f1;
+                }
+            }
+            if (lane == 0) { near[o] = j1; sec[o] = j2; dn[o] = d1; ds[o] = d2; }
+        }
+        grid.sync();
+        r = s_r[pick] + 1;
+        ++round;
     }
 }
 

@@ -187,6 +187,7 @@ struct Impl : ImplBase {
     std::vector<void*> bufs;        // every device allocation, freed in the destructor
     int *M = nullptr, *point_slot = nullptr, *near = nullptr, *sec = nullptr;
     T *MC = nullptr, *dn = nullptr, *ds = nullptr, *colbuf = nullptr;
+    T* fp2_cols = nullptr;          // FastPAM2: columns of a speculative batch [FP2_B][n]
     int *rescan = nullptr, *rescan_count = nullptr;   // objects whose nearest/second slot was swapped
     RI* ri = nullptr;
     double2* rowd = nullptr;        // float path: (double dn, double ds) in sorted order
@@ -826,7 +827,8 @@ struct Impl : ImplBase {
         // column (n sectors) and wants every SM's load units (measured: one
         // block per SM is ~1.6x slower despite cheaper grid syncs)
         fp2_blocks = (int)std::min<int64_t>((int64_t)nsm * std::max(per_sm, 1), std::max<int64_t>(1, cdiv(n, 256)));
-        KM_TRY(alloc(&fp2_partials, fp2_blocks));
+        KM_TRY(alloc(&fp2_partials, (size_t)2 * fp2_blocks * km::FP2_B));
+        KM_TRY(alloc(&fp2_cols, (size_t)km::FP2_B * n));
         trace_cap = k;
         KM_TRY(alloc(&trace, trace_cap));
         h_best.resize(k);
@@ -905,7 +907,7 @@ struct Impl : ImplBase {
         if (debug_fp2) fprintf(stderr, "[fp2] improving slots m=%d\n", m);
         const T* Dp = D; int64_t ldv = ld; int nn = (int)n; int kk = k;
         int* Mp = M; int* psp = point_slot; T* MCp = MC; int* nr = near; int* sc = sec; T* dnp = dn; T* dsp = ds;
-        T* cb = colbuf; A* tdp = td; A* pp = fp2_partials; Dec* dp = dec; Rec* tr = trace; int tc = trace_cap;
+        T* cb = fp2_cols; A* tdp = td; A* pp = fp2_partials; Dec* dp = dec; Rec* tr = trace; int tc = trace_cap;
         int* op = fp2_order; Rec* bp = fp2_best;
         const T* csp = colsrc; const int* cip = colidx_dev;
         int* rsp = rescan; int* rcp = rescan_count;
