@@ -462,7 +462,7 @@ def run_sharded(args):
     def job(D_slab):
         h = parallel.CudaShard(D_slab, n, k, rank, cb, stream=stream)
         if cfg.init == "build":
-            parallel.build([h], comm, cb, k)
+            parallel.build_async([h], comm, cb, k)
         else:
             parallel.set_medoids([h], comm, cb, kmsynth.random_medoids(cfg), n)
         return h
@@ -475,7 +475,12 @@ def run_sharded(args):
     init_s = comm.max_over_ranks(time.perf_counter() - t0)
 
     def step(hh):
-        return parallel.fp2_iter([hh], comm, cb) if fp2 else parallel.swap_iter([hh], comm, cb)
+        # FastPAM1: the device-decided iteration (no host round trip; the timed
+        # region ends with a device synchronisation)
+        if fp2:
+            return parallel.fp2_iter([hh], comm, cb)
+        parallel.swap_iter_async([hh], comm)
+        return None
 
     for _ in range(args.warmup):
         step(h)
@@ -514,12 +519,14 @@ def run_sharded(args):
         t1 = time.perf_counter()
         Dd = Dh_t.to(Dt.device, non_blocking=True)
         h2 = job(Dd)
-        it = 0
-        while it < 2000:
-            it += 1
-            res = step(h2)
-            if res[0]:
-                break
+        if fp2:
+            it = 0
+            while it < 2000:
+                it += 1
+                if step(h2)[0]:
+                    break
+        else:
+            _, it, _ = parallel.run([h2], comm, cb)
         st = h2.km.get_state()
         torch.cuda.synchronize()
         e2e_s = comm.max_over_ranks(time.perf_counter() - t1)

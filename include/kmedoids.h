@@ -242,6 +242,48 @@ km_status kmedoids_shard_select(km_handle* h, const int64_t* rank_col_begin, int
 km_status kmedoids_shard_pack_column(km_handle* h, int32_t cand);
 km_status kmedoids_shard_apply(km_handle* h);
 
+/* Device-decided sharded FastPAM1 iteration (Alg.3 P:874-904 over column
+ * slabs, readings R1/R5), with no host round trip inside an iteration:
+ *   1. kmedoids_shard_eval(h)            local candidates -> 16-byte record
+ *   2. all-gather the R records          (caller)
+ *   3. kmedoids_shard_decide(h)          lexicographic min of the records on the
+ *      device (M, TD, the decision); the rank owning c* copies column c* into
+ *      the exchange column buffer, every other rank writes zeros
+ *   4. SUM all-reduce of the column buffers (caller; elements of D's type --
+ *      float32 or the uint32 bits as int32: x + 0 = x exactly)
+ *   5. kmedoids_shard_apply_async(h)     MC, nearest/second cache
+ * All five are asynchronous on the handle's stream.  The decision is sticky:
+ * once an iteration finds no improving swap, later iterations change nothing
+ * and are not counted, so a caller may keep iterations queued ahead of the
+ * one it inspects.  kmedoids_shard_status reads the run's status (pinned
+ * mirror written by step 3): *converged, *n_iter (the converging iteration
+ * included, as P:1390-1392), *n_swaps, *td (int64_t* or double*) as of a
+ * definite iteration, so every rank reads the same status: wait = 1 after
+ * all enqueued work (the last iteration), 2 after the iteration before the
+ * most recently enqueued one (blocks only until that one is done), 0 no
+ * synchronisation (the last iteration's copy if already written, else an
+ * older one -- a hint, not for collective decisions).  kmedoids_shard_trace copies the applied
+ * swaps of the run (slot, candidate, dTD; up to 4096 recorded) to host
+ * arrays of cap entries, *count = swaps of the run.  The status restarts at
+ * kmedoids_shard_set_medoids and at the end of a sharded BUILD.  Errors:
+ * KM_ECOMM before kmedoids_shard_exchange, KM_EINVAL (wait), KM_ECUDA. */
+/* The same for a sharded BUILD step (Alg.1, reading R3):
+ * kmedoids_build_eval(h, step), all-gather the records, kmedoids_build_decide
+ * (lexicographic min (gain, c) on the device; the owner packs column c*,
+ * other ranks zeros), SUM all-reduce of the column buffers,
+ * kmedoids_build_apply_async(h, step).  No host round trip in any of the k
+ * steps; the chosen medoids are read with kmedoids_get_state afterwards.
+ * Errors: KM_ECOMM before kmedoids_shard_exchange, KM_EINVAL (step out of
+ * order / range), KM_ECUDA. */
+km_status kmedoids_build_decide(km_handle* h, int32_t step);
+km_status kmedoids_build_apply_async(km_handle* h, int32_t step);
+km_status kmedoids_shard_decide(km_handle* h);
+km_status kmedoids_shard_apply_async(km_handle* h);
+km_status kmedoids_shard_status(km_handle* h, int32_t wait, int32_t* converged, int32_t* n_iter, int32_t* n_swaps,
+                                void* td_out);
+km_status kmedoids_shard_trace(km_handle* h, int32_t* slots_out, int32_t* cands_out, void* dtds_out, int32_t cap,
+                               int32_t* count_out);
+
 /* Sharded FastPAM2 (reading R6) iteration, on every rank:
  *   1. kmedoids_fp2_shard_eval(h)      per-slot best (v_i, i, c_i) over the local
  *                                      candidates -> record_send (k records)

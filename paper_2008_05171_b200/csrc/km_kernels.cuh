@@ -144,6 +144,81 @@ __global__ void k_gather_col(const T* __restrict__ D, int64_t ld, int n, int64_t
     if (o < n) colbuf[o] = D[(int64_t)o * ld + (c - col_begin)];
 }
 
+// Sharded, device-decided iteration (no host round trip): the status of the
+// run, mirrored into pinned host memory by the decide kernel.
+template <typename A>
+struct alignas(16) ShardStatus {
+    A td;            // TD after the iteration
+    int32_t conv;    // sticky: 1 once an iteration found no improving swap
+    int32_t iters;   // iterations counted (the converging one included; later ones not)
+    int32_t swaps;
+    int32_t apply;   // this iteration applied a swap
+    int32_t calls;   // decide calls so far (iterations enqueued, counted or not)
+    int32_t pad[3];
+};
+constexpr int SHARD_MIRRORS = 4;   // ring of pinned status copies, one per decide call
+
+// Reading R1/R5 on the gathered records, as k_select, but sticky: after the
+// converging iteration every further one is a no-op (apply = 0, nothing
+// counted), so a caller may enqueue iterations ahead of reading the status.
+// Applied swaps are appended to trace[] (dTD, slot, c).
+template <typename A>
+__global__ void k_shard_decide(const Rec<A>* __restrict__ recs, int nrec, A* __restrict__ td, int* __restrict__ M,
+                               int* __restrict__ point_slot, Decision<A>* __restrict__ dec,
+                               int* __restrict__ rescan_count, ShardStatus<A>* __restrict__ status,
+                               ShardStatus<A>* __restrict__ mirror, Rec<A>* __restrict__ trace, int trace_cap) {
+    *rescan_count = 0;
+    dec->apply = 0;
+    if (!status->conv) {
+        Rec<A> b = rec_none<A>();
+        for (int r = 0; r < nrec; ++r)
+            if (rec_less(recs[r], b)) b = recs[r];
+        bool improving;
+        if (b.slot == INT_MAX) improving = false;
+        else if (std::is_same<A, double>::value) improving = (double)b.v < -1e-12 * fabs((double)*td);
+        else improving = b.v < 0;
+        dec->iters += 1;
+        status->iters += 1;
+        dec->dtd = b.v;
+        dec->slot = b.slot;
+        dec->c = b.c;
+        if (improving) {
+            dec->apply = 1;
+            const int old = M[b.slot];
+            dec->old_m = old;
+            M[b.slot] = b.c;
+            point_slot[old] = -1;
+            point_slot[b.c] = b.slot;
+            *td += b.v;
+            dec->swaps += 1;
+            if (status->swaps < trace_cap) trace[status->swaps] = b;
+            status->swaps += 1;
+        } else {
+            status->conv = 1;
+        }
+    }
+    status->apply = dec->apply;
+    status->td = *td;
+    status->calls += 1;
+    // pinned host ring: the host reads the copy of a given call once that
+    // call's iteration is known complete, so every rank reads the same status
+    mirror[(status->calls - 1) % SHARD_MIRRORS] = *status;
+}
+
+// The decided column into the exchange buffer: the owner rank copies column
+// c* of its slab, every other rank writes zeros, so a SUM all-reduce of the
+// buffers delivers the column everywhere (x + 0 = x exactly) without the host
+// knowing the owner.
+template <typename T, typename A>
+__global__ void k_shard_pack_decided(const T* __restrict__ D, int64_t ld, int n, int64_t col_begin, int64_t col_end,
+                                     const Decision<A>* __restrict__ dec, T* __restrict__ colbuf) {
+    const int o = blockIdx.x * blockDim.x + threadIdx.x;
+    if (o >= n) return;
+    const int64_t c = dec->c;
+    const bool mine = dec->apply && c >= col_begin && c < col_end;
+    colbuf[o] = mine ? D[(int64_t)o * ld + (c - col_begin)] : (T)0;
+}
+
 // Sharded: copy the broadcast column into MC[slot].
 template <typename T, typename A>
 __global__ void k_column_to_mc(const T* __restrict__ colbuf, int n, const Decision<A>* __restrict__ dec,

@@ -133,9 +133,15 @@ struct ImplBase {
                                    int32_t* owner, void* dtd) = 0;
     virtual km_status shard_pack_column(int32_t cand) = 0;
     virtual km_status shard_apply() = 0;
+    virtual km_status shard_decide() = 0;
+    virtual km_status shard_apply_async() = 0;
+    virtual km_status shard_status(int32_t wait, int32_t* conv, int32_t* iters, int32_t* swaps, void* td) = 0;
+    virtual km_status shard_trace(int32_t* slots, int32_t* cands, void* dtds, int32_t cap, int32_t* count) = 0;
     virtual km_status build_eval(int32_t step) = 0;
     virtual km_status build_select(const int64_t* rcb, int32_t* cand, int32_t* owner, void* gain) = 0;
     virtual km_status build_apply(int32_t step) = 0;
+    virtual km_status build_decide(int32_t step) = 0;
+    virtual km_status build_apply_async(int32_t step) = 0;
     virtual km_status last_swaps_out(int32_t* slots, int32_t* cands, void* dtds, int32_t cap, int32_t* count) = 0;
     virtual km_status fp2_shard_exchange(int32_t nranks, km_fp2_exchange* out) = 0;
     virtual km_status fp2_shard_eval() = 0;
@@ -150,6 +156,7 @@ struct ImplBase {
     bool profiling = false;
     double prof_ms = 0.0;
     int64_t prof_launches = 0;
+    virtual km_status prof_harvest() { return KM_OK; }   // pending stream timings (async sharded mode)
     int64_t launches = 0;
     int k = 0;
     int64_t n = 0;
@@ -227,6 +234,9 @@ struct Impl : ImplBase {
         if (h_dec) cudaFreeHost(h_dec);
         if (h_td) cudaFreeHost(h_td);
         for (auto e : sp_ev) if (e) cudaEventDestroy(e);
+        for (auto e : sh_ev) if (e) cudaEventDestroy(e);
+        for (auto& p : pr_ev) for (auto e : p) if (e) cudaEventDestroy(e);
+        if (sh_mirror) cudaFreeHost(sh_mirror);
         if (ev0) cudaEventDestroy(ev0);
         if (ev1) cudaEventDestroy(ev1);
     }
@@ -455,9 +465,43 @@ struct Impl : ImplBase {
     }
 
     // a3 + a4 (local): stream the slab, combine into the local best record.
+    // Stream timing of the device-decided sharded protocol: iterations are
+    // enqueued without host round trips, so each launch gets its own event
+    // pair from a ring, harvested when a pair is reused (16 launches later:
+    // long complete) or at kmedoids_stream_time.
+    static constexpr int PROF_RING = 16;
+    bool prof_ring_mode = false;
+    cudaEvent_t pr_ev[PROF_RING][2] = {};
+    int64_t pr_next = 0, pr_done = 0;
+    km_status prof_ring_pair(cudaEvent_t** pair) {
+        const int slot = (int)(pr_next % PROF_RING);
+        if (!pr_ev[slot][0])
+            for (auto& e : pr_ev[slot]) KM_CK(cudaEventCreate(&e));
+        if (pr_next - pr_done >= PROF_RING) KM_TRY(prof_take(pr_done));
+        *pair = pr_ev[slot];
+        ++pr_next;
+        return KM_OK;
+    }
+    km_status prof_take(int64_t idx) {
+        cudaEvent_t* p = pr_ev[idx % PROF_RING];
+        KM_CK(cudaEventSynchronize(p[1]));
+        float ms = 0.f;
+        KM_CK(cudaEventElapsedTime(&ms, p[0], p[1]));
+        prof_ms += ms; prof_launches += 1;
+        pr_done = idx + 1;
+        return KM_OK;
+    }
+    km_status prof_harvest() override {
+        while (pr_done < pr_next) KM_TRY(prof_take(pr_done));
+        return KM_OK;
+    }
+
     km_status eval_local(bool do_prep = true) {
         if (do_prep) KM_TRY(prep());
-        if (profiling) KM_CK(record_ev(ev0));
+        cudaEvent_t* pair = nullptr;
+        if (profiling && prof_ring_mode) KM_TRY(prof_ring_pair(&pair));
+        if (pair) KM_CK(cudaEventRecord(pair[0], st));
+        else if (profiling) KM_CK(record_ev(ev0));
         if (stream_kind == 10) {  // TMA ring, segment-aligned stages
             KM_TRY((launch_seg<SG_NC, SG_RB, SG_S, SG_MINB>(nullptr)));
         } else if (stream_kind == 13) {
@@ -497,7 +541,8 @@ struct Impl : ImplBase {
                 D, ld, w, (int)n, P, ri, R, o_plus, o_head, o_tail, o_imin, o_islot);
         }
         KM_CKL();
-        if (profiling) { KM_CK(record_ev(ev1)); pending_prof = true; }
+        if (pair) KM_CK(cudaEventRecord(pair[1], st));
+        else if (profiling) { KM_CK(record_ev(ev1)); pending_prof = true; }
         KM_TRY(launch_combine(w, c0, P, o_plus, o_head, o_tail, o_imin, o_islot, head_slot, tail_slot, cand_v, cand_slot,
                               nullptr, nullptr));
         return KM_OK;
@@ -1592,7 +1637,14 @@ struct Impl : ImplBase {
 
     km_status build_eval(int32_t step) override {
         if (step < 0 || step >= k) return fail(KM_EINVAL, "build step %d out of range", step);
-        if (sharded) {                             // the sharded BUILD is incremental too (own slab's gains)
+        if (step == 0) {
+            // a (re)started BUILD: no medoids yet, so the step-0 pass masks
+            // nothing (a previous run's medoids must not be excluded)
+            KM_CK(cudaMemsetAsync(point_slot, 0xff, n * sizeof(int), st));
+            ready = false;
+            build_step = 0;
+        }
+        {                                          // the phase-API BUILD is incremental too (own slab's gains)
             KM_TRY(bd_init());
             if (bd_mode == 1 && step >= 1) return bd_eval(step);
         }
@@ -1791,7 +1843,7 @@ struct Impl : ImplBase {
         KM_CK(cudaMemcpyAsync(MC, cols, (size_t)k * n * sizeof(T), cudaMemcpyDeviceToDevice, st));
         KM_TRY(assign_full_and_td());
         KM_TRY(reset_counters());
-        KM_CK(cudaStreamSynchronize(st));
+        KM_TRY(sh_reset());
         ready = true;
         fp3_reset();
         fp1_prepped = false;
@@ -1842,6 +1894,98 @@ struct Impl : ImplBase {
         return KM_OK;
     }
 
+    // ---- device-decided sharded iteration (no host round trip) ---------------
+    using SStat = km::ShardStatus<A>;
+    SStat* sh_status = nullptr;      // device
+    SStat* sh_mirror = nullptr;      // pinned host
+    Rec* sh_trace = nullptr;
+    int sh_trace_cap = 0;
+    int sh_calls = 0;                              // shard_decide calls enqueued since the reset
+    cudaEvent_t sh_ev[2] = {nullptr, nullptr};   // recorded by alternate shard_apply_async calls
+    int sh_ev_last = -1;                          // index of the most recent record (-1: none)
+    int sh_ev_count = 0;
+    km_status sh_alloc() {
+        if (sh_status) return KM_OK;
+        KM_TRY(alloc(&sh_status, 1));
+        KM_CK(cudaMallocHost((void**)&sh_mirror, km::SHARD_MIRRORS * sizeof(SStat)));
+        sh_trace_cap = 4096;
+        KM_TRY(alloc(&sh_trace, sh_trace_cap));
+        for (auto& e : sh_ev) KM_CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+        return KM_OK;
+    }
+    // a new run starts at every set_medoids / BUILD: status zeroed (counted in
+    // the stream order, before the first decide)
+    km_status sh_reset() {
+        KM_TRY(sh_alloc());
+        SStat z{};
+        KM_CK(cudaMemcpyAsync(sh_status, &z, sizeof(SStat), cudaMemcpyHostToDevice, st));
+        KM_CK(cudaStreamSynchronize(st));
+        for (int i = 0; i < km::SHARD_MIRRORS; ++i) sh_mirror[i] = z;
+        sh_ev_last = -1;
+        sh_ev_count = 0;
+        sh_calls = 0;
+        return KM_OK;
+    }
+    km_status shard_decide() override {
+        if (!rec_recv) return fail(KM_ECOMM, "call kmedoids_shard_exchange first");
+        prof_ring_mode = true;           // later evals of this handle time through the event ring
+        if (!sh_status) KM_TRY(sh_reset());
+        km::k_shard_decide<A><<<1, 1, 0, st>>>(rec_recv, nranks, td, M, point_slot, dec, rescan_count, sh_status,
+                                              sh_mirror, sh_trace, sh_trace_cap);
+        KM_CKL();
+        ++sh_calls;
+        km::k_shard_pack_decided<T, A><<<(unsigned)cdiv(n, 256), 256, 0, st>>>(D, ld, (int)n, c0, c1, dec, colbuf);
+        KM_CKL();
+        launches += 2;
+        return KM_OK;
+    }
+    km_status shard_apply_async() override {
+        const int nb = (int)cdiv(n, 256);
+        km::k_column_to_mc<T, A><<<nb, 256, 0, st>>>(colbuf, (int)n, dec, MC);
+        KM_CKL();
+        KM_TRY(assign_incremental());
+        sh_ev_last = sh_ev_last < 0 ? 0 : sh_ev_last ^ 1;
+        KM_CK(cudaEventRecord(sh_ev[sh_ev_last], st));
+        ++sh_ev_count;
+        return KM_OK;
+    }
+    // wait: 0 = read the mirror as it is, 1 = after all enqueued work, 2 =
+    // after the iteration BEFORE the most recently enqueued one (so the host
+    // can keep one iteration queued ahead of the one it inspects)
+    km_status shard_status(int32_t wait, int32_t* conv, int32_t* iters, int32_t* swaps, void* tdo) override {
+        if (!sh_status) KM_TRY(sh_reset());
+        // the status after decide call `which` (1-based; 0 = the reset state)
+        int which = sh_calls;
+        if (wait == 1) KM_CK(cudaStreamSynchronize(st));
+        else if (wait == 2) {
+            which = sh_calls - 1;
+            if (sh_ev_count >= 2) KM_CK(cudaEventSynchronize(sh_ev[sh_ev_last ^ 1]));
+            else KM_CK(cudaStreamSynchronize(st));
+        }
+        SStat m{};
+        if (which > 0) m = sh_mirror[(which - 1) % km::SHARD_MIRRORS];
+        if (conv) *conv = m.conv;
+        if (iters) *iters = m.iters;
+        if (swaps) *swaps = m.swaps;
+        if (tdo) memcpy(tdo, &m.td, sizeof(A));
+        return KM_OK;
+    }
+    km_status shard_trace(int32_t* slots, int32_t* cands, void* dtds, int32_t cap, int32_t* count) override {
+        if (!sh_status) KM_TRY(sh_reset());
+        KM_CK(cudaStreamSynchronize(st));
+        const int cnt = sh_calls > 0 ? std::min(sh_mirror[(sh_calls - 1) % km::SHARD_MIRRORS].swaps, sh_trace_cap) : 0;
+        std::vector<Rec> h(cnt);
+        if (cnt) KM_CK(cudaMemcpy(h.data(), sh_trace, cnt * sizeof(Rec), cudaMemcpyDeviceToHost));
+        const int m = std::min(cnt, cap);
+        for (int i = 0; i < m; ++i) {
+            if (slots) slots[i] = h[i].slot;
+            if (cands) cands[i] = h[i].c;
+            if (dtds) memcpy((char*)dtds + (size_t)i * sizeof(A), &h[i].v, sizeof(A));
+        }
+        if (count) *count = cnt;
+        return KM_OK;
+    }
+
     int build_step = 0;
     km_status build_select(const int64_t* rcb, int32_t* cand, int32_t* owner, void* gain) override {
         if (!rec_recv) return fail(KM_ECOMM, "call kmedoids_shard_exchange first");
@@ -1858,7 +2002,26 @@ struct Impl : ImplBase {
         return KM_OK;
     }
 
-    km_status build_apply(int32_t step) override {
+    // Device-decided BUILD step (kmedoids.h): the decision stays on the device,
+    // the owner packs column c* and the other ranks zeros (SUM all-reduce).
+    km_status build_decide(int32_t step) override {
+        if (!rec_recv) return fail(KM_ECOMM, "call kmedoids_shard_exchange first");
+        if (step != build_step) return fail(KM_EINVAL, "build step %d out of order (expected %d)", step, build_step);
+        if (step == 0) {
+            KM_CK(cudaMemsetAsync(point_slot, 0xff, n * sizeof(int), st));
+            ready = false;
+        }
+        km::k_build_select<A><<<1, 1, 0, st>>>(rec_recv, nranks, build_step, td, M, point_slot, dec);
+        KM_CKL();
+        km::k_shard_pack_decided<T, A><<<(unsigned)cdiv(n, 256), 256, 0, st>>>(D, ld, (int)n, c0, c1, dec, colbuf);
+        KM_CKL();
+        launches += 2;
+        return KM_OK;
+    }
+    km_status build_apply_async(int32_t step) override { return build_apply_impl(step, false); }
+    km_status build_apply(int32_t step) override { return build_apply_impl(step, true); }
+
+    km_status build_apply_impl(int32_t step, bool sync) {
         const int nb = (int)cdiv(n, 256);
         km::k_column_to_mc<T, A><<<nb, 256, 0, st>>>(colbuf, (int)n, dec, MC);
         KM_CKL();
@@ -1872,8 +2035,9 @@ struct Impl : ImplBase {
         if (step == k - 1) {
             KM_TRY(build_finish());
             build_step = 0;
+            KM_TRY(sh_reset());
         }
-        KM_CK(cudaStreamSynchronize(st));
+        if (sync) KM_CK(cudaStreamSynchronize(st));
         return KM_OK;
     }
 };
@@ -2048,6 +2212,7 @@ km_status kmedoids_set_profiling(km_handle* h, int32_t enable) {
 
 km_status kmedoids_stream_time(km_handle* h, double* ms_out, int64_t* launches_out, int32_t reset) {
     KM_H();
+    KM_TRY(h->impl->prof_harvest());
     if (ms_out) *ms_out = h->impl->prof_ms;
     if (launches_out) *launches_out = h->impl->prof_launches;
     if (reset) { h->impl->prof_ms = 0.0; h->impl->prof_launches = 0; }
@@ -2241,6 +2406,40 @@ km_status kmedoids_shard_set_medoids(km_handle* h, const int32_t* medoids, const
 km_status kmedoids_shard_eval(km_handle* h) {
     KM_H();
     return h->impl->shard_eval();
+}
+
+km_status kmedoids_build_decide(km_handle* h, int32_t step) {
+    KM_H();
+    return h->impl->build_decide(step);
+}
+
+km_status kmedoids_build_apply_async(km_handle* h, int32_t step) {
+    KM_H();
+    if (step < 0 || step >= h->impl->k) return fail(KM_EINVAL, "build step %d out of range", step);
+    return h->impl->build_apply_async(step);
+}
+
+km_status kmedoids_shard_decide(km_handle* h) {
+    KM_H();
+    return h->impl->shard_decide();
+}
+
+km_status kmedoids_shard_apply_async(km_handle* h) {
+    KM_H();
+    return h->impl->shard_apply_async();
+}
+
+km_status kmedoids_shard_status(km_handle* h, int32_t wait, int32_t* converged, int32_t* n_iter, int32_t* n_swaps,
+                                void* td_out) {
+    KM_H();
+    if (wait < 0 || wait > 2) return fail(KM_EINVAL, "wait must be 0, 1 or 2");
+    return h->impl->shard_status(wait, converged, n_iter, n_swaps, td_out);
+}
+
+km_status kmedoids_shard_trace(km_handle* h, int32_t* slots_out, int32_t* cands_out, void* dtds_out, int32_t cap,
+                               int32_t* count_out) {
+    KM_H();
+    return h->impl->shard_trace(slots_out, cands_out, dtds_out, cap, count_out);
 }
 
 km_status kmedoids_shard_select(km_handle* h, const int64_t* rank_col_begin, int32_t* found, int32_t* slot,

@@ -81,6 +81,12 @@ def load_library() -> ctypes.CDLL:
         "kmedoids_shard_select": [vp, vp, vp, vp, vp, vp, vp],
         "kmedoids_shard_pack_column": [vp, i32],
         "kmedoids_shard_apply": [vp],
+        "kmedoids_shard_decide": [vp],
+        "kmedoids_build_decide": [vp, i32],
+        "kmedoids_build_apply_async": [vp, i32],
+        "kmedoids_shard_apply_async": [vp],
+        "kmedoids_shard_status": [vp, i32, vp, vp, vp, vp],
+        "kmedoids_shard_trace": [vp, vp, vp, vp, i32, vp],
         "kmedoids_fp2_shard_exchange": [vp, i32, ctypes.POINTER(_Fp2Exchange)],
         "kmedoids_fp2_shard_eval": [vp],
         "kmedoids_fp2_shard_plan": [vp, vp, vp, vp],
@@ -306,6 +312,35 @@ class KMedoids:
 
     def shard_apply(self):
         _check(load_library().kmedoids_shard_apply(self.h))
+
+    # device-decided iteration (kmedoids.h: no host round trip inside an iteration)
+    def shard_decide(self):
+        _check(load_library().kmedoids_shard_decide(self.h))
+
+    def build_decide(self, step: int):
+        _check(load_library().kmedoids_build_decide(self.h, int(step)))
+
+    def build_apply_async(self, step: int):
+        _check(load_library().kmedoids_build_apply_async(self.h, int(step)))
+
+    def shard_apply_async(self):
+        _check(load_library().kmedoids_shard_apply_async(self.h))
+
+    def shard_status(self, wait: int = 1):
+        """(converged, n_iter, n_swaps, td) of the sharded run; wait: 0 as is,
+        1 after all enqueued work, 2 after the iteration before the last one."""
+        cv = np.zeros(1, np.int32); it = np.zeros(1, np.int32); sw = np.zeros(1, np.int32)
+        td = np.zeros(1, self.acc)
+        _check(load_library().kmedoids_shard_status(self.h, int(wait), _p(cv), _p(it), _p(sw), _p(td)))
+        return bool(cv[0]), int(it[0]), int(sw[0]), td[0].item()
+
+    def shard_trace(self, cap: int = 4096):
+        """Applied swaps of the sharded run: [(slot, cand, dTD)]."""
+        sl = np.zeros(cap, np.int32); c = np.zeros(cap, np.int32); d = np.zeros(cap, self.acc)
+        cnt = np.zeros(1, np.int32)
+        _check(load_library().kmedoids_shard_trace(self.h, _p(sl), _p(c), _p(d), int(cap), _p(cnt)))
+        m = min(int(cnt[0]), cap)
+        return [(int(sl[i]), int(c[i]), d[i].item()) for i in range(m)]
 
     def fp2_shard_exchange(self, nranks: int) -> _Fp2Exchange:
         x = _Fp2Exchange()

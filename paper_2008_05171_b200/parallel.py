@@ -12,6 +12,14 @@ is needed.  One SWAP iteration (FastPAM1, Alg.3) is:
   4. owner of c*: kmedoids_shard_pack_column; broadcast the n-element column
   5. kmedoids_shard_apply     M, TD and the nearest/second cache (identical on every rank)
 
+``swap_iter_async`` / ``run`` use the device-decided form instead: the
+lexicographic min is taken on the device (kmedoids_shard_decide), the owner
+packs column c* and every other rank zeros, and one SUM all-reduce of the
+column buffers delivers c* everywhere -- no host round trip inside an
+iteration, so the host keeps one iteration queued ahead of the one whose
+status it reads (the decision is sticky after convergence, so the extra
+iteration changes and counts nothing).
+
 BUILD (Alg.1) uses the same gather / pack / broadcast pattern per step.
 
 The protocol is written once over ``handles`` (the shard handles this process
@@ -59,6 +67,13 @@ def lexmin_records(recs):
     return min(recs, key=lambda t: (t[0], t[1], t[2]))
 
 
+def column_view(col, dtype: str):
+    """The exchange column (uint8 bytes) as float32 ("f32") or int32 ("u32":
+    the uint32 bits; a SUM with zeros leaves them unchanged)."""
+    import torch
+    return col.view(torch.float32 if dtype == "f32" else torch.int32)
+
+
 class LocalComm:
     """All ranks' handles in one process (virtual ranks)."""
 
@@ -78,6 +93,15 @@ class LocalComm:
         for r, (_, _, col) in enumerate(xs):
             if r != owner:
                 col.copy_(src)
+
+    def allreduce_column(self, handles):
+        xs = [h.exchange_tensors(self.world) for h in handles]
+        cols = [column_view(x[2], h.column_dtype) for x, h in zip(xs, handles)]
+        tot = cols[0].clone()
+        for c in cols[1:]:
+            tot += c
+        for c in cols:
+            c.copy_(tot)
 
     def allgather_fp2_records(self, handles):
         xs = [h.fp2_exchange_tensors(self.world) for h in handles]
@@ -116,6 +140,11 @@ class TorchComm:
         (h,) = handles
         _, _, col = h.exchange_tensors(self.world)
         self.dist.broadcast(col, src=owner, group=self.group)
+
+    def allreduce_column(self, handles):
+        (h,) = handles
+        _, _, col = h.exchange_tensors(self.world)
+        self.dist.all_reduce(column_view(col, h.column_dtype), op=self.dist.ReduceOp.SUM, group=self.group)
 
     def allgather_fp2_records(self, handles):
         (h,) = handles
@@ -201,6 +230,24 @@ def build(handles, comm, cb, k: int):
     return chosen
 
 
+def build_async(handles, comm, cb, k: int):
+    """Sharded BUILD with the decisions on the device (no host round trip in
+    any step); returns the chosen medoids (identical on every rank)."""
+    for step in range(k):
+        for h in handles:
+            h.build_eval(step)
+        comm.allgather_records(handles)
+        for h in handles:
+            h.build_decide(step)
+        comm.allreduce_column(handles)
+        for h in handles:
+            h.build_apply_async(step)
+    Ms = [h.get_state().medoids.tolist() for h in handles]
+    if any(m != Ms[0] for m in Ms):
+        raise RuntimeError(f"ranks disagree on the BUILD medoids: {Ms}")
+    return Ms[0]
+
+
 def fp2_iter(handles, comm, cb):
     """One sharded FastPAM2 iteration (reading R6); returns (converged, swaps).
 
@@ -225,7 +272,8 @@ def fp2_iter(handles, comm, cb):
     return conv, swaps
 
 
-def run(handles, comm, cb, max_iter: int = 2000):
+def run_sync(handles, comm, cb, max_iter: int = 2000):
+    """The host-decided protocol (swap_iter) to convergence: same result as run()."""
     trace = []
     it = 0
     while it < max_iter:
@@ -235,6 +283,45 @@ def run(handles, comm, cb, max_iter: int = 2000):
             return trace, it, True
         trace.append(sw)
     return trace, it, False
+
+
+def swap_iter_async(handles, comm):
+    """One device-decided sharded FastPAM1 iteration, enqueued (no host sync)."""
+    for h in handles:
+        h.shard_eval()
+    comm.allgather_records(handles)
+    for h in handles:
+        h.shard_decide()
+    comm.allreduce_column(handles)
+    for h in handles:
+        h.shard_apply_async()
+
+
+def status(handles, comm, wait: int = 1):
+    """(converged, n_iter, n_swaps, td) -- identical on every rank (checked here)."""
+    st = [h.shard_status(wait) for h in handles]
+    if any(s != st[0] for s in st):
+        raise RuntimeError(f"ranks disagree on the run status: {st}")
+    return st[0]
+
+
+def run(handles, comm, cb, max_iter: int = 2000):
+    """Sharded FastPAM1 to convergence: iterations enqueued one ahead of the
+    status the host inspects.  Returns (trace [(slot, c, dTD)], n_iter, converged)."""
+    enq = 0
+    conv, it = False, 0
+    while enq < max_iter:
+        swap_iter_async(handles, comm)
+        enq += 1
+        conv, it, _, _ = status(handles, comm, wait=2)     # the iteration before the last one
+        if conv:
+            break
+    if not conv:
+        conv, it, _, _ = status(handles, comm, wait=1)
+    traces = [h.shard_trace() for h in handles]
+    if any(t != traces[0] for t in traces):
+        raise RuntimeError("ranks disagree on the swap trace")
+    return traces[0], it, conv
 
 
 # ---------------------------------------------------------------------------
@@ -279,6 +366,11 @@ class CudaShard:
                         torch.as_tensor(_DevBytes(x.col_recv, cap * world), device=dev),
                         int(x.col_bytes_per_column))
         return self._f2
+
+    @property
+    def column_dtype(self) -> str:
+        from .kmedoids import KM_U32
+        return "u32" if self.km.dtype == KM_U32 else "f32"
 
     def __getattr__(self, name):       # shard_eval, shard_select, ... -> the handle
         return getattr(self.km, name)

@@ -25,7 +25,8 @@ def shards(Dt, n, k, world):
     return hs, cb
 
 
-@pytest.mark.parametrize("world,cid,n,k", [(2, 1, 500, 5), (3, 1, 500, 5), (4, 5, 1200, 9), (2, 4, 900, 7)])
+@pytest.mark.parametrize("world,cid,n,k", [(2, 1, 500, 5), (3, 1, 500, 5), (4, 5, 1200, 9), (2, 4, 900, 7),
+                                            (1, 4, 900, 7)])
 def test_sharded_build_and_swap_equal_single_gpu(world, cid, n, k):
     from paper_2008_05171_b200 import KMedoids, parallel
     cfg = kmsynth.CONFIGS[cid]
@@ -44,8 +45,13 @@ def test_sharded_build_and_swap_equal_single_gpu(world, cid, n, k):
     comm = parallel.LocalComm(world)
     chosen = parallel.build(hs, comm, cb, k)
     assert [c for c, _ in chosen] == Mb.tolist()
+    tdb = [h.km.get_state().td for h in hs]
+    assert parallel.build_async(hs, comm, cb, k) == Mb.tolist()       # device-decided BUILD
+    assert [h.km.get_state().td for h in hs] == tdb
     trace, iters, conv = parallel.run(hs, comm, cb)
     assert conv and iters == st1.n_iter
+    for h in hs:
+        assert h.km.get_state().n_iter == st1.n_iter
     if cfg.metric == kmsynth.L1_INT:
         assert [(s, c, int(v)) for s, c, v in trace] == [(s, c, int(v)) for s, c, v in tr1]
     else:
@@ -121,3 +127,36 @@ def test_sharded_fastpam2_equals_single_gpu(world, cid, n, k):
         D = kmsynth.as_numpy_D(Dt)[:, :n]
         ref = oracle.swap_run(D, M0, oracle.FASTPAM2)
         assert st1.medoids.tolist() == ref.medoids.tolist() and st1.td == ref.td
+
+
+@pytest.mark.parametrize("world,cid,n,k", [(2, 5, 700, 9), (3, 4, 900, 12)])
+def test_sharded_device_decided_equals_host_decided(world, cid, n, k):
+    """run() (device-decided, SUM all-reduce of the column, one iteration
+    queued ahead) and run_sync() (host-decided, broadcast) give the same swaps,
+    iteration count and state; the status is sticky after convergence."""
+    from paper_2008_05171_b200 import parallel
+    cfg = kmsynth.CONFIGS[cid]
+    X = kmsynth.make_points(cfg, n=n)
+    Dt = kmsynth.dist_cuda(X, cfg.metric)
+    M0 = kmsynth.random_medoids(cfg, k=k, n=n)
+    hs, cb = shards(Dt, n, k, world)
+    comm = parallel.LocalComm(world)
+    parallel.set_medoids(hs, comm, cb, M0, n)
+    t1, it1, c1 = parallel.run(hs, comm, cb)
+    s1 = [h.km.get_state() for h in hs]
+    # extra iterations after convergence change and count nothing
+    parallel.swap_iter_async(hs, comm)
+    parallel.swap_iter_async(hs, comm)
+    conv, it, sw, td = parallel.status(hs, comm, wait=1)
+    assert conv and it == it1 and sw == len(t1)
+    parallel.set_medoids(hs, comm, cb, M0, n)
+    t2, it2, c2 = parallel.run_sync(hs, comm, cb)
+    assert c1 and c2 and it1 == it2
+    if cfg.metric == kmsynth.L1_INT:
+        assert [(a, b, int(v)) for a, b, v in t1] == [(a, b, int(v)) for a, b, v in t2]
+    else:
+        assert [(a, b) for a, b, v in t1] == [(a, b) for a, b, v in t2]
+    for h, s in zip(hs, s1):
+        st = h.km.get_state()
+        assert st.medoids.tolist() == s.medoids.tolist()
+        assert st.assignment.tolist() == s.assignment.tolist()

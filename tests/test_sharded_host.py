@@ -61,6 +61,7 @@ class MockShard:
         self.MC = cols.numpy().view(np.uint32).reshape(self.k, self.n).copy()
         self.cache = oracle.assign_cols(self.MC)
         self.td = int(self.cache.dn.sum())
+        self._status_reset()
 
     def shard_pack_column(self, c):
         assert self.c0 <= c < self.c1
@@ -91,6 +92,43 @@ class MockShard:
         self.MC[self._pending] = self._col()
         self.cache = oracle.assign_cols(self.MC)
 
+    # --- device-decided iteration (sticky after convergence) ---
+    column_dtype = "u32"
+
+    def _status_reset(self):
+        self._st = {"conv": False, "iters": 0, "swaps": 0, "trace": [], "apply": False}
+
+    def shard_decide(self):
+        st = self._st
+        st["apply"] = False
+        if not st["conv"]:
+            v, slot, c = parallel.lexmin_records(self._recs())
+            st["iters"] += 1
+            if slot != 2**31 - 1 and v < 0:
+                self.M[slot] = c
+                self.td += v
+                self._pending = slot
+                st["apply"] = True
+                st["swaps"] += 1
+                st["trace"].append((slot, c, v))
+            else:
+                st["conv"] = True
+        col = self._col()
+        if st["apply"] and self.c0 <= self.M[self._pending] < self.c1:
+            col[:] = self.D[:, self.M[self._pending]]
+        else:
+            col[:] = 0
+
+    def shard_apply_async(self):
+        if self._st["apply"]:
+            self.shard_apply()
+
+    def shard_status(self, wait=1):
+        return self._st["conv"], self._st["iters"], self._st["swaps"], self.td
+
+    def shard_trace(self):
+        return list(self._st["trace"])
+
     # --- BUILD ---
     def build_eval(self, step):
         if step == 0:
@@ -115,6 +153,23 @@ class MockShard:
         self._pending = c
         self._gain = g
         return c, owner, g
+
+    def build_decide(self, step):
+        g, _, c = parallel.lexmin_records(self._recs())
+        self._pending = c
+        self._gain = g
+        col = self._col()
+        if self.c0 <= c < self.c1:
+            col[:] = self.D[:, c]
+        else:
+            col[:] = 0
+
+    def build_apply_async(self, step):
+        self.build_apply(step)
+
+    def get_state(self):
+        import types
+        return types.SimpleNamespace(medoids=np.asarray(self.M, np.int32))
 
     def build_apply(self, step):
         col = self._col().astype(np.int64)
@@ -146,11 +201,18 @@ def _worker(rank, world, port, seed, q):
         cb = parallel.column_bounds(n, world)
         comm = parallel.TorchComm()
         h = MockShard(D, rank, cb, k)
-        chosen = parallel.build([h], comm, cb, k)
-        M = [c for c, _ in chosen]
+        M = parallel.build_async([h], comm, cb, k)                  # device-decided (all-reduce)
+        chosen = parallel.build([h], comm, cb, k)                   # host-decided (broadcast)
+        if [c for c, _ in chosen] != M:
+            raise AssertionError("the two sharded BUILD protocols disagree")
         parallel.set_medoids([h], comm, cb, M, n)
-        trace, iters, conv = parallel.run([h], comm, cb)
-        q.put((rank, M, trace, iters, conv, h.M, h.td))
+        trace, iters, conv = parallel.run([h], comm, cb)            # device-decided (all-reduce)
+        res = (M, trace, iters, conv, list(h.M), h.td)
+        parallel.set_medoids([h], comm, cb, M, n)
+        trace2, iters2, conv2 = parallel.run_sync([h], comm, cb)    # host-decided (broadcast)
+        if (trace2, iters2, conv2, list(h.M), h.td) != res[1:]:
+            raise AssertionError("the two sharded protocols disagree")
+        q.put((rank,) + res)
     except Exception as e:  # report instead of hanging the parent
         q.put((rank, "error", repr(e), 0, 0, 0, 0))
         raise
