@@ -2235,12 +2235,27 @@ __global__ void k_fp2_slot_best(int w, int64_t col_begin, const A* __restrict__ 
     const A ri = R[i];
     const int a = (int)((int64_t)y * w / gridDim.y), z = (int)((int64_t)(y + 1) * w / gridDim.y);
     Rec<A> b = rec_none<A>();
-    for (int cl = a + threadIdx.x; cl < z; cl += blockDim.x) {
-        const int64_t c = col_begin + cl;
-        if (point_slot[c] >= 0) continue;
-        const A v = ri + (empty ? (A)0 : acc[(int64_t)i * w + cl]) + plus[cl];
-        Rec<A> r; r.v = v; r.slot = i; r.c = (int)c;
-        if (rec_less(r, b)) b = r;        // same slot: (v, c) order
+    const A* arow = acc + (int64_t)i * w;
+    constexpr int U = 4;                      // columns loaded ahead per thread (memory-level parallelism)
+    for (int c0l = a + threadIdx.x; c0l < z; c0l += U * blockDim.x) {
+        A av[U], pv[U];
+        int ps[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const int cl = c0l + u * blockDim.x;
+            if (cl < z) {
+                ps[u] = point_slot[col_begin + cl];
+                av[u] = empty ? (A)0 : __ldcs(&arow[cl]);   // read once: streaming
+                pv[u] = plus[cl];
+            }
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const int cl = c0l + u * blockDim.x;
+            if (cl >= z || ps[u] >= 0) continue;
+            Rec<A> r; r.v = ri + av[u] + pv[u]; r.slot = i; r.c = (int)(col_begin + cl);
+            if (rec_less(r, b)) b = r;        // same slot: (v, c) order
+        }
     }
     b = block_min_rec(b);
     if (threadIdx.x == 0) part[(int64_t)i * gridDim.y + y] = b;
