@@ -54,6 +54,7 @@ struct PostArgs {
     A* R;
     int P;
     int *head_slot, *tail_slot;
+    int prep_only;             // 1: phases 3-7 only (slot sort, R, parts of the current cache)
     Decision<A>* h_dec;        // pinned host mirrors written at the end (or null)
     A* h_td;
     unsigned long long* tph;   // measurement aid (KM_STEP_PROF): globaltimer after each phase, or null
@@ -88,94 +89,97 @@ k_fp1_post(PostArgs<T, A> g) {
     const int n = g.n, k = g.k, B = gridDim.x, b = blockIdx.x;
     post_stamp(g.tph, 0);
 
-    // ---- 0 select (every block decides identically; block 0 records)
-    if (threadIdx.x == 0) {
-        Rec<A> best = rec_none<A>();
-        for (int r = 0; r < g.nrec; ++r) {
-            const Rec<A> x = g.recs[r];
-            if (rec_less(x, best)) best = x;
+    Decision<A> d{};
+    if (!g.prep_only) {
+        // ---- 0 select (every block decides identically; block 0 records)
+        if (threadIdx.x == 0) {
+            Rec<A> best = rec_none<A>();
+            for (int r = 0; r < g.nrec; ++r) {
+                const Rec<A> x = g.recs[r];
+                if (rec_less(x, best)) best = x;
+            }
+            const A tdv = *g.td;
+            bool improving;
+            if (best.slot == INT_MAX) improving = false;
+            else if (std::is_same<A, double>::value) improving = (double)best.v < -1e-12 * fabs((double)tdv);
+            else improving = best.v < 0;
+            Decision<A> d = *g.dec;
+            d.iters += 1;
+            d.apply = improving ? 1 : 0;
+            d.dtd = best.v;
+            d.slot = best.slot;
+            d.c = best.c;
+            if (improving) {
+                d.old_m = g.M[best.slot];
+                d.swaps += 1;
+            }
+            sdec = d;
         }
-        const A tdv = *g.td;
-        bool improving;
-        if (best.slot == INT_MAX) improving = false;
-        else if (std::is_same<A, double>::value) improving = (double)best.v < -1e-12 * fabs((double)tdv);
-        else improving = best.v < 0;
-        Decision<A> d = *g.dec;
-        d.iters += 1;
-        d.apply = improving ? 1 : 0;
-        d.dtd = best.v;
-        d.slot = best.slot;
-        d.c = best.c;
-        if (improving) {
-            d.old_m = g.M[best.slot];
-            d.swaps += 1;
+        __syncthreads();
+        d = sdec;
+        grid.sync(); post_stamp(g.tph, 1);                                 // every block has read M / td / dec
+        if (b == 0 && threadIdx.x == 0) {
+            *g.dec = d;
+            if (d.apply) {
+                g.M[d.slot] = d.c;
+                g.point_slot[d.old_m] = -1;
+                g.point_slot[d.c] = d.slot;
+                *g.td = *g.td + d.dtd;
+            }
         }
-        sdec = d;
-    }
-    __syncthreads();
-    const Decision<A> d = sdec;
-    grid.sync(); post_stamp(g.tph, 1);                                 // every block has read M / td / dec
-    if (b == 0 && threadIdx.x == 0) {
-        *g.dec = d;
-        if (d.apply) {
-            g.M[d.slot] = d.c;
-            g.point_slot[d.old_m] = -1;
-            g.point_slot[d.c] = d.slot;
-            *g.td = *g.td + d.dtd;
-        }
-    }
 
-    // ---- 1 apply: column c*, incremental nearest/second
-    if (d.apply) {
-        const int i = d.slot;
-        const bool local = d.c >= g.c0 && d.c < g.c1;
-        for (int o = tid; o < n; o += nth) {
-            if (local) g.MC[(int64_t)i * n + o] = g.D[(int64_t)o * g.ld + (d.c - g.c0)];
-        }
-        // (the column is read back below by the same thread: same o mapping)
-        for (int o = tid; o < n; o += nth) {
-            const int j1 = __ldcg(&g.near[o]), j2 = __ldcg(&g.sec[o]);
-            if (j1 == i || j2 == i) {
-                g.rescan[atomicAdd(g.rescan_count, 1)] = o;
-                continue;
+        // ---- 1 apply: column c*, incremental nearest/second
+        if (d.apply) {
+            const int i = d.slot;
+            const bool local = d.c >= g.c0 && d.c < g.c1;
+            for (int o = tid; o < n; o += nth) {
+                if (local) g.MC[(int64_t)i * n + o] = g.D[(int64_t)o * g.ld + (d.c - g.c0)];
             }
-            const T x = g.MC[(int64_t)i * n + o];
-            const T d1 = __ldcg(&g.dn[o]), d2 = __ldcg(&g.ds[o]);
-            if (x < d1 || (x == d1 && i < j1)) {
-                g.near[o] = i; g.dn[o] = x; g.sec[o] = j1; g.ds[o] = d1;
-            } else if (x < d2 || (x == d2 && i < j2)) {
-                g.sec[o] = i; g.ds[o] = x;
-            }
-        }
-        grid.sync(); post_stamp(g.tph, 2);
-        // ---- 2 rescan
-        const int cnt = __ldcg(g.rescan_count);
-        for (int e = gwarp; e < cnt; e += nwarps) {
-            const int o = __ldcg(&g.rescan[e]);
-            T d1 = dmax<T>(), d2 = dmax<T>();
-            int j1 = INT_MAX, j2 = INT_MAX;
-#pragma unroll 8
-            for (int j = lane; j < k; j += 32) {
-                const T dd = __ldcg(&g.MC[(int64_t)j * n + o]);
-                if (lex_lt(dd, j, d1, j1)) { d2 = d1; j2 = j1; d1 = dd; j1 = j; }
-                else if (lex_lt(dd, j, d2, j2)) { d2 = dd; j2 = j; }
-            }
-#pragma unroll
-            for (int x = 16; x >= 1; x >>= 1) {
-                const T e1 = __shfl_xor_sync(FULL, d1, x), e2 = __shfl_xor_sync(FULL, d2, x);
-                const int f1 = __shfl_xor_sync(FULL, j1, x), f2 = __shfl_xor_sync(FULL, j2, x);
-                if (lex_lt(e1, f1, d1, j1)) {
-                    if (lex_lt(d1, j1, e2, f2)) { d2 = d1; j2 = j1; } else { d2 = e2; j2 = f2; }
-                    d1 = e1; j1 = f1;
-                } else if (lex_lt(e1, f1, d2, j2)) {
-                    d2 = e1; j2 = f1;
+            // (the column is read back below by the same thread: same o mapping)
+            for (int o = tid; o < n; o += nth) {
+                const int j1 = __ldcg(&g.near[o]), j2 = __ldcg(&g.sec[o]);
+                if (j1 == i || j2 == i) {
+                    g.rescan[atomicAdd(g.rescan_count, 1)] = o;
+                    continue;
+                }
+                const T x = g.MC[(int64_t)i * n + o];
+                const T d1 = __ldcg(&g.dn[o]), d2 = __ldcg(&g.ds[o]);
+                if (x < d1 || (x == d1 && i < j1)) {
+                    g.near[o] = i; g.dn[o] = x; g.sec[o] = j1; g.ds[o] = d1;
+                } else if (x < d2 || (x == d2 && i < j2)) {
+                    g.sec[o] = i; g.ds[o] = x;
                 }
             }
-            if (lane == 0) { g.near[o] = j1; g.sec[o] = j2; g.dn[o] = d1; g.ds[o] = d2; }
+            grid.sync(); post_stamp(g.tph, 2);
+            // ---- 2 rescan
+            const int cnt = __ldcg(g.rescan_count);
+            for (int e = gwarp; e < cnt; e += nwarps) {
+                const int o = __ldcg(&g.rescan[e]);
+                T d1 = dmax<T>(), d2 = dmax<T>();
+                int j1 = INT_MAX, j2 = INT_MAX;
+    #pragma unroll 8
+                for (int j = lane; j < k; j += 32) {
+                    const T dd = __ldcg(&g.MC[(int64_t)j * n + o]);
+                    if (lex_lt(dd, j, d1, j1)) { d2 = d1; j2 = j1; d1 = dd; j1 = j; }
+                    else if (lex_lt(dd, j, d2, j2)) { d2 = dd; j2 = j; }
+                }
+    #pragma unroll
+                for (int x = 16; x >= 1; x >>= 1) {
+                    const T e1 = __shfl_xor_sync(FULL, d1, x), e2 = __shfl_xor_sync(FULL, d2, x);
+                    const int f1 = __shfl_xor_sync(FULL, j1, x), f2 = __shfl_xor_sync(FULL, j2, x);
+                    if (lex_lt(e1, f1, d1, j1)) {
+                        if (lex_lt(d1, j1, e2, f2)) { d2 = d1; j2 = j1; } else { d2 = e2; j2 = f2; }
+                        d1 = e1; j1 = f1;
+                    } else if (lex_lt(e1, f1, d2, j2)) {
+                        d2 = e1; j2 = f1;
+                    }
+                }
+                if (lane == 0) { g.near[o] = j1; g.sec[o] = j2; g.dn[o] = d1; g.ds[o] = d2; }
+            }
+            grid.sync(); post_stamp(g.tph, 3);
         }
-        grid.sync(); post_stamp(g.tph, 3);
-    }
 
+    }
     // ---- 3 histogram of the block's chunk
     const int chunk = (n + B - 1) / B;
     const int e0 = min(n, b * chunk), e1 = min(n, e0 + chunk);

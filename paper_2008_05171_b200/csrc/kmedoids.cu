@@ -447,8 +447,14 @@ struct Impl : ImplBase {
         return KM_OK;
     }
 
-    // a2: sort rows by nearest slot, removal loss, part metadata.
+    // a2: sort rows by nearest slot, removal loss, part metadata.  One
+    // cooperative launch (phases 3-7 of k_fp1_post) when the post kernel is
+    // available, else six small kernels (KM_POST=0).
     km_status prep() {
+        if (post_usable()) {
+            KM_TRY(post_alloc());
+            return launch_post(true);
+        }
         km::k_slot_hist<<<B, 256, k * sizeof(int), st>>>(near, (int)n, k, sort_chunk, counts);
         KM_CKL();
         km::k_scan_within_slot<<<(unsigned)cdiv((int64_t)k * 32, 256), 256, 0, st>>>(counts, B, k, offsets, slot_tot);
@@ -705,7 +711,16 @@ struct Impl : ImplBase {
         return KM_OK;
     }
 
-    km_status launch_post() {
+    int post_ok = -1;
+    bool post_usable() {
+        if (post_ok < 0) {
+            const char* e = getenv("KM_POST");
+            post_ok = ((e && e[0] == '0') || debug_natural) ? 0 : 1;
+        }
+        return post_ok == 1;
+    }
+
+    km_status launch_post(bool prep_only = false) {
         km::PostArgs<T, A> g;
         g.D = D; g.ld = ld; g.n = (int)n; g.k = k; g.c0 = c0; g.c1 = c1; g.recs = rec_local; g.nrec = 1;
         g.td = td; g.M = M; g.point_slot = point_slot; g.dec = dec; g.MC = MC; g.near = near; g.sec = sec;
@@ -713,7 +728,9 @@ struct Impl : ImplBase {
         g.offsets = post_offsets; g.slot_tot = slot_tot; g.seg_start = seg_start; g.empty_slot = empty_slot;
         g.ri = ri; g.rowd = rowd; g.R = R; g.P = P; g.head_slot = head_slot; g.tail_slot = tail_slot;
         g.tph = post_tph;
-        g.h_dec = h_dec; g.h_td = h_td;
+        g.prep_only = prep_only ? 1 : 0;
+        g.h_dec = prep_only ? nullptr : h_dec;
+        g.h_td = prep_only ? nullptr : h_td;
         void* args[] = {&g};
         KM_CK(cudaLaunchCooperativeKernel((void*)km::k_fp1_post<T, A>, dim3(post_blocks), dim3(km::POST_THREADS), args,
                                           (size_t)k * sizeof(int), st));
