@@ -35,6 +35,7 @@
 namespace km {
 
 constexpr int FP3_TMAX = 32;     // touched slots a correction step handles (else: re-stream)
+constexpr int FP3_EV = 16;      // D loads in flight per lane in the correction (events ahead; 32 measured slower)
 constexpr int FP3_G = 32;        // event groups of the correction (columns x groups warps)
 constexpr int FP3_THREADS = 256;
 constexpr int FP3_WARPS = FP3_THREADS / 32;
@@ -491,15 +492,15 @@ k_fp3_window(Fp3Args<T, A> g) {
                         tn_l = __ldcg(&g.touched_map[ch.near_new]) - tb;
                         dno = ch.dn_old; dso = ch.ds_old; dnn = ch.dn_new; dsn = ch.ds_new;
                     }
-                    for (int e8 = 0; e8 < nb; e8 += 16) {
-                        T x[16];
+                    for (int e8 = 0; e8 < nb; e8 += FP3_EV) {
+                        T x[FP3_EV];
 #pragma unroll
-                        for (int v8 = 0; v8 < 16; ++v8) {
+                        for (int v8 = 0; v8 < FP3_EV; ++v8) {
                             const int oo = __shfl_sync(FULL, o_l, (e8 + v8) & 31);
                             x[v8] = g.D[(int64_t)oo * g.ld + dcol];
                         }
 #pragma unroll
-                        for (int v8 = 0; v8 < 16; ++v8) {
+                        for (int v8 = 0; v8 < FP3_EV; ++v8) {
                             const int src = (e8 + v8) & 31;
                             const T a_dso = __shfl_sync(FULL, dso, src), a_dsn = __shfl_sync(FULL, dsn, src);
                             // a term is non-zero only where d < d_s (old or new): most (o, c)
