@@ -35,6 +35,7 @@
 namespace km {
 
 constexpr int FP3_TMAX = 32;     // touched slots a correction step handles (else: re-stream)
+constexpr int FP3_TV = 8;        // GLOBAL correction: touched slots per slice (4 columns per lane)
 constexpr int FP3_EV = 16;      // D loads in flight per lane in the correction (events ahead; 32 measured slower)
 constexpr int FP3_G = 32;        // event groups of the correction (columns x groups warps)
 constexpr int FP3_THREADS = 256;
@@ -457,9 +458,102 @@ k_fp3_window(Fp3Args<T, A> g) {
         // ------------------------------------------------------------ correct
         // touched slots are handled FP3_TMAX at a time (per-warp shared-memory
         // accumulators); plus / R deltas of the non-slot terms in the first slice
-        for (int tb = 0; tb < T_; tb += FP3_TMAX) {
-        const int TS = min(FP3_TMAX, T_ - tb);
+        constexpr int SL = GLOBAL ? FP3_TV : FP3_TMAX;      // touched slots per slice
+        for (int tb = 0; tb < T_; tb += SL) {
+        const int TS = min(SL, T_ - tb);
         __syncthreads();
+        if constexpr (GLOBAL) {
+            // GLOBAL (every candidate): warp item = (event group q, 128-column
+            // tile u), 4 columns per lane read as one 16-byte load per event
+            // (4x fewer loads and sequential batches than 32-column tiles);
+            // accumulators [slot][4][32 lanes] in shared memory (conflict-free)
+            A* sacc = reinterpret_cast<A*>(fp3_smem) + (size_t)warp * (FP3_TMAX * 32 + FP3_TMAX);
+            A* srs = sacc + FP3_TV * 128;
+            const int ncols = cl1 - cl0;
+            const int ntl = max((ncols + 127) / 128, 1);
+            const int G = min(FP3_G, max(1, nwarps / ntl));
+            const int items = G * ntl;
+            for (int it = gwarp; it < items; it += nwarps) {
+                const int q = it / ntl, u = it % ntl;
+                const int col = u * 128 + lane * 4;     // offset in [0, ncols)
+                const int nact = max(0, min(4, ncols - col));
+                const int64_t dcol = (int64_t)g.a + cl0 + (nact > 0 ? col : 0);
+                const bool vec = nact == 4 && ((dcol | g.ld) & 3) == 0;
+                for (int t = 0; t < TS * 4; ++t) sacc[t * 32 + lane] = 0;
+                if (lane < FP3_TV) srs[lane] = 0;
+                __syncwarp();
+                A pl[4] = {0, 0, 0, 0};
+                const int e0 = (int)((int64_t)q * m / G), e1 = (int)((int64_t)(q + 1) * m / G);
+                for (int eb = e0; eb < e1; eb += 32) {
+                    const int nb = min(32, e1 - eb);
+                    int o_l = 0, to_l = 0, tn_l = 0;
+                    T dno = 0, dso = 0, dnn = 0, dsn = 0;
+                    if (lane < nb) {
+                        const Fp3Chg<T> ch = fp3_ld_chg(&g.chg[eb + lane]);
+                        o_l = ch.o;
+                        to_l = __ldcg(&g.touched_map[ch.near_old]) - tb;
+                        tn_l = __ldcg(&g.touched_map[ch.near_new]) - tb;
+                        dno = ch.dn_old; dso = ch.ds_old; dnn = ch.dn_new; dsn = ch.ds_new;
+                    }
+                    constexpr int EV4 = 8;
+                    for (int e8 = 0; e8 < nb; e8 += EV4) {
+                        T x[EV4][4];
+#pragma unroll
+                        for (int v8 = 0; v8 < EV4; ++v8) {
+                            const int oo = __shfl_sync(FULL, o_l, (e8 + v8) & 31);
+                            const T* src = g.D + (int64_t)oo * g.ld + dcol;
+                            if (vec) {
+                                typename Vec4<T>::type w4 = *reinterpret_cast<const typename Vec4<T>::type*>(src);
+                                memcpy(&x[v8][0], &w4.x, sizeof(T)); memcpy(&x[v8][1], &w4.y, sizeof(T));
+                                memcpy(&x[v8][2], &w4.z, sizeof(T)); memcpy(&x[v8][3], &w4.w, sizeof(T));
+                            } else {
+#pragma unroll
+                                for (int jj = 0; jj < 4; ++jj) x[v8][jj] = jj < nact ? src[jj] : dmax<T>();
+                            }
+                        }
+#pragma unroll
+                        for (int v8 = 0; v8 < EV4; ++v8) {
+                            const int src_l = (e8 + v8) & 31;
+                            const T a_dso = __shfl_sync(FULL, dso, src_l), a_dsn = __shfl_sync(FULL, dsn, src_l);
+                            const T mx = max(a_dso, a_dsn);
+                            const bool hit = (x[v8][0] < mx) | (x[v8][1] < mx) | (x[v8][2] < mx) | (x[v8][3] < mx);
+                            const bool any_hit = __any_sync(FULL, hit);
+                            if (!any_hit && u != 0) continue;  // u == 0 items also carry the R deltas
+                            const T a_dno = __shfl_sync(FULL, dno, src_l), a_dnn = __shfl_sync(FULL, dnn, src_l);
+                            const int a_to = __shfl_sync(FULL, to_l, src_l), a_tn = __shfl_sync(FULL, tn_l, src_l);
+                            if (e8 + v8 < nb) {
+                                const bool io = (unsigned)a_to < (unsigned)TS, in_ = (unsigned)a_tn < (unsigned)TS;
+                                if (any_hit) {
+#pragma unroll
+                                    for (int jj = 0; jj < 4; ++jj) {
+                                        A tpo, tao, tpn, tan_;
+                                        fp3_terms<T, A>(x[v8][jj], a_dno, a_dso, tpo, tao);
+                                        fp3_terms<T, A>(x[v8][jj], a_dnn, a_dsn, tpn, tan_);
+                                        if (tb == 0) pl[jj] += tpn - tpo;
+                                        if (io) sacc[(a_to * 4 + jj) * 32 + lane] -= tao;
+                                        if (in_) sacc[(a_tn * 4 + jj) * 32 + lane] += tan_;
+                                    }
+                                }
+                                if (u == 0 && lane == 0) {
+                                    if (io) srs[a_to] -= (A)a_dso - (A)a_dno;
+                                    if (in_) srs[a_tn] += (A)a_dsn - (A)a_dnn;
+                                }
+                            }
+                        }
+                    }
+                }
+                __syncwarp();
+#pragma unroll
+                for (int jj = 0; jj < 4; ++jj) {
+                    if (jj >= nact) continue;
+                    for (int t = 0; t < TS; ++t)
+                        g.part_acc[((int64_t)q * FP3_TV + t) * g.L + col + jj] = sacc[(t * 4 + jj) * 32 + lane];
+                    if (tb == 0) g.part_plus[(int64_t)q * g.L + col + jj] = pl[jj];
+                }
+                if (u == 0 && lane < TS) g.part_R[q * FP3_TMAX + lane] = srs[lane];
+                __syncwarp();
+            }
+        } else
         // warp item = (event group q, 32-column tile u) of [cl0, cl1).  The
         // group's events are loaded 32 at a time (one per lane) and
         // broadcast by shuffles; D loads are issued 8 events ahead.
@@ -539,13 +633,15 @@ k_fp3_window(Fp3Args<T, A> g) {
         if (blockIdx.x == 0 && threadIdx.x == 0) { const unsigned long long tn = fp3_now(); ctl->tphase[5] += tn - tlast; tlast = tn; }
         {
             const int ncols = cl1 - cl0;
-            const int G = min(FP3_G, max(1, nwarps / max((ncols + 31) / 32, 1)));
+            const int G = GLOBAL ? min(FP3_G, max(1, nwarps / max((ncols + 127) / 128, 1)))
+                                 : min(FP3_G, max(1, nwarps / max((ncols + 31) / 32, 1)));
+            constexpr int TSTR = GLOBAL ? FP3_TV : FP3_TMAX;   // part_acc slot stride per group
             // acc[slot_t][col] += sum_q part_acc[q][t][col]  (fixed order)
             for (int it = tid; it < TS * ncols; it += nth) {
                 const int t = it / ncols, col = it % ncols;
                 A s = 0;
 #pragma unroll 8
-                for (int q = 0; q < G; ++q) s += __ldcg(&g.part_acc[((int64_t)q * FP3_TMAX + t) * g.L + col]);
+                for (int q = 0; q < G; ++q) s += __ldcg(&g.part_acc[((int64_t)q * TSTR + t) * g.L + col]);
                 A* dst = &g.acc[(int64_t)__ldcg(&g.touched[tb + t]) * g.ww + cl0 + col];
                 *dst = __ldcg(dst) + s;
             }
@@ -562,7 +658,7 @@ k_fp3_window(Fp3Args<T, A> g) {
                 const int sl = __ldcg(&g.touched[tb + t]);
                 g.R[sl] = __ldcg(&g.R[sl]) + rs;
             }
-            if (tb + FP3_TMAX >= T_)
+            if (tb + SL >= T_)
                 for (int s = tid; s < k; s += nth) g.touched_flag[s] = 0;
         }
         grid.sync();
