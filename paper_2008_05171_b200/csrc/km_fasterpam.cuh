@@ -458,11 +458,16 @@ k_fp3_window(Fp3Args<T, A> g) {
         // ------------------------------------------------------------ correct
         // touched slots are handled FP3_TMAX at a time (per-warp shared-memory
         // accumulators); plus / R deltas of the non-slot terms in the first slice
-        constexpr int SL = GLOBAL ? FP3_TV : FP3_TMAX;      // touched slots per slice
+        // GLOBAL with few touched slots (the common case): 4 columns per lane in
+        // slices of FP3_TV slots (a slice costs about a quarter of a narrow
+        // one); otherwise 1 column per lane, slices of FP3_TMAX (uniform across
+        // the grid: T_ is)
+        const bool wide = GLOBAL && T_ <= 3 * FP3_TV;
+        const int SL = wide ? FP3_TV : FP3_TMAX;             // touched slots per slice
         for (int tb = 0; tb < T_; tb += SL) {
         const int TS = min(SL, T_ - tb);
         __syncthreads();
-        if constexpr (GLOBAL) {
+        if (wide) {
             // GLOBAL (every candidate): warp item = (event group q, 128-column
             // tile u), 4 columns per lane read as one 16-byte load per event
             // (4x fewer loads and sequential batches than 32-column tiles);
@@ -633,9 +638,9 @@ k_fp3_window(Fp3Args<T, A> g) {
         if (blockIdx.x == 0 && threadIdx.x == 0) { const unsigned long long tn = fp3_now(); ctl->tphase[5] += tn - tlast; tlast = tn; }
         {
             const int ncols = cl1 - cl0;
-            const int G = GLOBAL ? min(FP3_G, max(1, nwarps / max((ncols + 127) / 128, 1)))
-                                 : min(FP3_G, max(1, nwarps / max((ncols + 31) / 32, 1)));
-            constexpr int TSTR = GLOBAL ? FP3_TV : FP3_TMAX;   // part_acc slot stride per group
+            const int G = wide ? min(FP3_G, max(1, nwarps / max((ncols + 127) / 128, 1)))
+                               : min(FP3_G, max(1, nwarps / max((ncols + 31) / 32, 1)));
+            const int TSTR = wide ? FP3_TV : FP3_TMAX;           // part_acc slot stride per group
             // acc[slot_t][col] += sum_q part_acc[q][t][col]  (fixed order)
             for (int it = tid; it < TS * ncols; it += nth) {
                 const int t = it / ncols, col = it % ncols;

@@ -1292,10 +1292,12 @@ struct Impl : ImplBase {
         KM_TRY(fp3_alloc());
         KM_TRY(fp3c_alloc());
         const int64_t nwarps = (int64_t)fp3c_blocks * km::FP3_WARPS;
-        // partials of the GLOBAL correction: G groups x FP3_TV slots x w (128-column items)
-        const int64_t G = std::min<int64_t>(km::FP3_G, std::max<int64_t>(1, nwarps / cdiv(w, 128)));
-        KM_TRY(alloc(&inc_pacc, (size_t)G * km::FP3_TV * w));
-        KM_TRY(alloc(&inc_pplus, (size_t)G * w));
+        // partials of the GLOBAL correction: G groups x slots x w, for both item
+        // shapes (128 columns x FP3_TV slots, 32 columns x FP3_TMAX slots)
+        const int64_t Gw = std::min<int64_t>(km::FP3_G, std::max<int64_t>(1, nwarps / cdiv(w, 128)));
+        const int64_t Gn = std::min<int64_t>(km::FP3_G, std::max<int64_t>(1, nwarps / cdiv(w, 32)));
+        KM_TRY(alloc(&inc_pacc, (size_t)std::max(Gw * km::FP3_TV, Gn * km::FP3_TMAX) * w));
+        KM_TRY(alloc(&inc_pplus, (size_t)std::max(Gw, Gn) * w));
         KM_TRY(alloc(&inc_pR, (size_t)km::FP3_G * km::FP3_TMAX));
         KM_TRY(alloc(&inc_gpart, fp3c_blocks));
         inc_trace_cap = 4096;
