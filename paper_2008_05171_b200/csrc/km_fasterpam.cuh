@@ -462,6 +462,8 @@ k_fp3_window(Fp3Args<T, A> g) {
         // slices of FP3_TV slots (a slice costs about a quarter of a narrow
         // one); otherwise 1 column per lane, slices of FP3_TMAX (uniform across
         // the grid: T_ is)
+        // (FasterPAM's 4096-column windows stay narrow: measured 2x slower wide,
+        // too few 128-column items to occupy the grid with <= FP3_G groups)
         const bool wide = GLOBAL && T_ <= 3 * FP3_TV;
         const int SL = wide ? FP3_TV : FP3_TMAX;             // touched slots per slice
         for (int tb = 0; tb < T_; tb += SL) {
@@ -475,15 +477,20 @@ k_fp3_window(Fp3Args<T, A> g) {
             A* sacc = reinterpret_cast<A*>(fp3_smem) + (size_t)warp * (FP3_TMAX * 32 + FP3_TMAX);
             A* srs = sacc + FP3_TV * 128;
             const int ncols = cl1 - cl0;
-            const int ntl = max((ncols + 127) / 128, 1);
+            // tiles start at the 16-byte boundary at or below column cl0 (the
+            // window start is arbitrary in FasterPAM); columns outside
+            // [cl0, cl1) are masked
+            const int sh = (int)((g.a + cl0) & 3);
+            const int ntl = max((ncols + sh + 127) / 128, 1);
             const int G = min(FP3_G, max(1, nwarps / ntl));
             const int items = G * ntl;
             for (int it = gwarp; it < items; it += nwarps) {
                 const int q = it / ntl, u = it % ntl;
-                const int col = u * 128 + lane * 4;     // offset in [0, ncols)
-                const int nact = max(0, min(4, ncols - col));
-                const int64_t dcol = (int64_t)g.a + cl0 + (nact > 0 ? col : 0);
-                const bool vec = nact == 4 && ((dcol | g.ld) & 3) == 0;
+                const int col = u * 128 + lane * 4 - sh;    // offset of column 0 of this lane (may be < 0)
+                const int jlo = max(0, -col), jhi = max(0, min(4, ncols - col));   // valid jj in [jlo, jhi)
+                const bool anyv = jlo < jhi;
+                const int64_t dcol = (int64_t)g.a + cl0 + (anyv ? col : 0);
+                const bool vec = jlo == 0 && jhi == 4 && ((dcol | g.ld) & 3) == 0;
                 for (int t = 0; t < TS * 4; ++t) sacc[t * 32 + lane] = 0;
                 if (lane < FP3_TV) srs[lane] = 0;
                 __syncwarp();
@@ -513,7 +520,7 @@ k_fp3_window(Fp3Args<T, A> g) {
                                 memcpy(&x[v8][2], &w4.z, sizeof(T)); memcpy(&x[v8][3], &w4.w, sizeof(T));
                             } else {
 #pragma unroll
-                                for (int jj = 0; jj < 4; ++jj) x[v8][jj] = jj < nact ? src[jj] : dmax<T>();
+                                for (int jj = 0; jj < 4; ++jj) x[v8][jj] = (jj >= jlo && jj < jhi) ? src[jj] : dmax<T>();
                             }
                         }
 #pragma unroll
@@ -550,7 +557,7 @@ k_fp3_window(Fp3Args<T, A> g) {
                 __syncwarp();
 #pragma unroll
                 for (int jj = 0; jj < 4; ++jj) {
-                    if (jj >= nact) continue;
+                    if (jj < jlo || jj >= jhi) continue;
                     for (int t = 0; t < TS; ++t)
                         g.part_acc[((int64_t)q * FP3_TV + t) * g.L + col + jj] = sacc[(t * 4 + jj) * 32 + lane];
                     if (tb == 0) g.part_plus[(int64_t)q * g.L + col + jj] = pl[jj];
@@ -638,7 +645,7 @@ k_fp3_window(Fp3Args<T, A> g) {
         if (blockIdx.x == 0 && threadIdx.x == 0) { const unsigned long long tn = fp3_now(); ctl->tphase[5] += tn - tlast; tlast = tn; }
         {
             const int ncols = cl1 - cl0;
-            const int G = wide ? min(FP3_G, max(1, nwarps / max((ncols + 127) / 128, 1)))
+            const int G = wide ? min(FP3_G, max(1, nwarps / max((ncols + (int)((g.a + cl0) & 3) + 127) / 128, 1)))
                                : min(FP3_G, max(1, nwarps / max((ncols + 31) / 32, 1)));
             const int TSTR = wide ? FP3_TV : FP3_TMAX;           // part_acc slot stride per group
             // acc[slot_t][col] += sum_q part_acc[q][t][col]  (fixed order)
