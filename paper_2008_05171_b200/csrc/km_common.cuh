@@ -79,9 +79,17 @@ template <typename A> struct alignas(16) Decision {
 // blocks are dispatched part-major, so the last wave of a bandwidth-bound
 // stream holds its smallest CTAs and the tail in which SMs fall idle is
 // shorter.  a = 0 gives the uniform split q*n/P.
+// c_part_skew >= 16 selects the power shape g(x) = 1 - (1 - x)^(1 + skew/16)
+// (sizes ~ (1 - x)^(skew/16): steeper still; measurement option).
 __constant__ int c_part_skew;
 __device__ __forceinline__ int64_t part_lo(int q, int64_t n, int P) {
     const int64_t a = c_part_skew, PP = P;
+    if (a >= 16) {
+        if (q >= P) return n;
+        const double r = (double)(P - q) / (double)P;
+        const int64_t v = (int64_t)((double)n * (1.0 - pow(r, 1.0 + (double)a / 16.0)));
+        return v < 0 ? 0 : (v > n ? n : v);
+    }
     return (int64_t)q * n * ((16 + a) * PP - a * q) / (16 * PP * PP);
 }
 __device__ __forceinline__ int64_t part_lo_uniform(int q, int64_t n, int P) { return (int64_t)q * n / P; }

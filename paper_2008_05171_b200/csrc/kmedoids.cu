@@ -302,7 +302,7 @@ struct Impl : ImplBase {
             // part-size tilt of the streams (km_common.cuh part_lo); one value
             // per process (a __constant__ of this device), KM_PART_SKEW in 16ths
             int skew = PART_SKEW_DEFAULT;
-            if (const char* es = getenv("KM_PART_SKEW")) skew = std::min(15, std::max(0, atoi(es)));
+            if (const char* es = getenv("KM_PART_SKEW")) skew = std::min(64, std::max(0, atoi(es)));
             KM_CK(cudaMemcpyToSymbol(km::c_part_skew, &skew, sizeof(int)));
         }
         Pb = choose_parts(n, w, STREAM_COLS, RESIDENT_CTAS);

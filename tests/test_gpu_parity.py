@@ -383,3 +383,22 @@ def test_large_k_and_tiny_n(variant):
     km3.set_medoids([1, 2])
     r3 = km3.run(use_build=False, variant=variant)
     assert r3.medoids.tolist() == ref3.medoids.tolist() and r3.td == ref3.td
+
+
+@pytest.mark.parametrize("skew", ["0", "7", "15"])
+def test_part_tilt_does_not_change_results(monkeypatch, skew):
+    """The stream's row parts are arbitrary row ranges (km::part_lo): any tilt
+    (KM_PART_SKEW, 16ths) and any part count give the oracle's exact trace."""
+    monkeypatch.setenv("KM_PART_SKEW", skew)
+    for parts in ("0", "9"):
+        monkeypatch.setenv("KM_PARTS", parts)
+        rng = np.random.default_rng(77)
+        n, k = 1500, 9
+        D = rand_int(rng, n, 5000, symmetric=True)
+        M0 = rng.choice(n, size=k, replace=False).astype(np.int32)
+        ref = oracle.swap_run(D, M0, oracle.FASTPAM1)
+        km = KM(to_dev(D), n, k)
+        km.set_medoids(M0)
+        r = km.run(use_build=False)
+        assert r.medoids.tolist() == ref.medoids.tolist() and r.td == ref.td and r.n_iter == ref.n_iter
+        km.close()
