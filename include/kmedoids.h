@@ -199,9 +199,14 @@ km_status kmedoids_launch_count(km_handle* h, int64_t* count_out);
  *     D 16-byte aligned, ld % 4 == 0.  Diagonal exactly 0.  Accuracy: the
  *     squared distance is within ~4 * 2^-22 (|x|^2 + |y|^2) of the exact one.
  *   KM_METRIC_L1_U32: X int32 integer coordinates (n x d), D uint32,
- *     d(x, y) = sum_t |x_t - y_t| exactly (caller keeps sums < 2^32).
- * Asynchronous on cuda_stream; X and D are borrowed.  Errors: KM_EINVAL
- * (sizes, alignment, d > 64 for L2), KM_ENOMEM, KM_ECUDA. */
+ *     d(x, y) = sum_t |x_t - y_t| exactly (caller keeps sums < 2^32).  The
+ *     arithmetic is chosen on the device from the coordinate ranges, always
+ *     exact: packed 16-bit (every range < 2^16), fp32 (sum of ranges < 2^24)
+ *     or 32-bit integer; KM_DIST_L1=int / f32 restricts the choice (tests).
+ * Asynchronous on cuda_stream (it never waits for the GPU); X and D are
+ * borrowed; the library keeps one grow-only scratch buffer per device,
+ * ordered across streams by an event.  Errors: KM_EINVAL (sizes,
+ * alignment, d > 64 for L2), KM_ENOMEM, KM_ECUDA. */
 typedef enum { KM_METRIC_L2_F32 = 0, KM_METRIC_L1_U32 = 1 } km_metric;
 km_status kmedoids_dissimilarity(const void* X, km_metric metric, int64_t n, int32_t d, void* D, int64_t ld,
                                  int64_t col_begin, int64_t col_end, void* cuda_stream);
