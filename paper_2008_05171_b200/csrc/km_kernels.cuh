@@ -2274,6 +2274,55 @@ __global__ void k_fp2_slot_reduce(int k, int split, const Rec<A>* __restrict__ p
     out[i] = b;
 }
 
+// FastPAM2 steps 4-5 on the device (reading R6): the improving slots of the
+// per-slot bests, ordered by (v_i, i) -- the rank of slot i is the number of
+// improving slots before it in that order (k <= a few thousand: one block).
+// Also the iteration's decision bookkeeping (the sequential kernel counts
+// this iteration's swaps from 0; k_fp2_finish adds the previous total).
+template <typename A>
+__global__ void k_fp2_plan(const Rec<A>* __restrict__ best, int k, const A* __restrict__ td,
+                           Decision<A>* __restrict__ dec, int* __restrict__ order, int* __restrict__ m_out,
+                           int* __restrict__ swaps_prev) {
+    __shared__ int s_m;
+    if (threadIdx.x == 0) s_m = 0;
+    __syncthreads();
+    const A tdv = *td;
+    auto improving = [&](const Rec<A>& b) {
+        if (b.slot == INT_MAX) return false;
+        if (std::is_same<A, double>::value) return (double)b.v < -1e-12 * fabs((double)tdv);
+        return b.v < 0;
+    };
+    for (int i = threadIdx.x; i < k; i += blockDim.x) {
+        const Rec<A> bi = best[i];
+        if (!improving(bi)) continue;
+        int rank = 0;
+        for (int j = 0; j < k; ++j) {
+            const Rec<A> bj = best[j];
+            if (j != i && improving(bj) && (bj.v < bi.v || (bj.v == bi.v && j < i))) ++rank;
+        }
+        order[rank] = i;
+        atomicAdd(&s_m, 1);
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        *m_out = s_m;
+        dec->iters += 1;
+        dec->apply = 0;
+        *swaps_prev = dec->swaps;
+        dec->swaps = 0;
+    }
+}
+
+template <typename A>
+__global__ void k_fp2_finish(Decision<A>* __restrict__ dec, const int* __restrict__ swaps_prev) {
+    dec->swaps += *swaps_prev;
+}
+
+template <typename A>
+__global__ void k_fp2_count(const Decision<A>* __restrict__ dec, int* __restrict__ swaps_iter) {
+    *swaps_iter = dec->swaps;
+}
+
 // The sequential phase of one FastPAM2 iteration as ONE cooperative kernel.
 // order[0..m) are the improving slots sorted by (v_i, i) (host), best[i] =
 // (v_i, i, c_i).  r = 0 applies best[order[0]] as is (it is FastPAM1's swap).
@@ -2299,7 +2348,7 @@ constexpr int FP2_B = 32;
 template <typename T, typename A>
 __global__ void __launch_bounds__(256)
 k_fp2_sequential(const T* __restrict__ D, int64_t ld, const T* __restrict__ colsrc, const int* __restrict__ colidx,
-                 int n, int k, const int* __restrict__ order, int m,
+                 int n, int k, const int* __restrict__ order, const int* __restrict__ m_dev,
                  const Rec<A>* __restrict__ best, int* __restrict__ M, int* __restrict__ point_slot,
                  T* __restrict__ MC, int* __restrict__ near, int* __restrict__ sec, T* __restrict__ dn,
                  T* __restrict__ ds, T* __restrict__ cols, A* __restrict__ td, A* __restrict__ partials,
@@ -2315,6 +2364,7 @@ k_fp2_sequential(const T* __restrict__ D, int64_t ld, const T* __restrict__ cols
     const int tid = blockIdx.x * blockDim.x + threadIdx.x;
     const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
     const int gwarp = tid >> 5, nwarps = nth >> 5;
+    const int m = *m_dev;
     int r = 0, round = 0;
     while (r < m) {
         // ---- batch (every block identically: the state is the same everywhere);

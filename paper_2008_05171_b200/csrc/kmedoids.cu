@@ -891,6 +891,8 @@ struct Impl : ImplBase {
         fp2_blocks = (int)std::min<int64_t>((int64_t)nsm * std::max(per_sm, 1), std::max<int64_t>(1, cdiv(n, 256)));
         KM_TRY(alloc(&fp2_partials, (size_t)2 * fp2_blocks * km::FP2_B));
         KM_TRY(alloc(&fp2_cols, (size_t)km::FP2_B * n));
+        KM_TRY(alloc(&fp2_m, 2));
+        KM_TRY(alloc(&fp2_swaps_prev, 1));
         trace_cap = k;
         KM_TRY(alloc(&trace, trace_cap));
         h_best.resize(k);
@@ -967,17 +969,8 @@ struct Impl : ImplBase {
         KM_CK(cudaMemcpyAsync(fp2_order, order.data(), order.size() * sizeof(int), cudaMemcpyHostToDevice, st));
         int m = (int)order.size();
         if (debug_fp2) fprintf(stderr, "[fp2] improving slots m=%d\n", m);
-        const T* Dp = D; int64_t ldv = ld; int nn = (int)n; int kk = k;
-        int* Mp = M; int* psp = point_slot; T* MCp = MC; int* nr = near; int* sc = sec; T* dnp = dn; T* dsp = ds;
-        T* cb = fp2_cols; A* tdp = td; A* pp = fp2_partials; Dec* dp = dec; Rec* tr = trace; int tc = trace_cap;
-        int* op = fp2_order; Rec* bp = fp2_best;
-        const T* csp = colsrc; const int* cip = colidx_dev;
-        int* rsp = rescan; int* rcp = rescan_count;
-        void* args[] = {&Dp, &ldv, &csp, &cip, &nn, &kk, &op, &m, &bp, &Mp, &psp, &MCp, &nr, &sc, &dnp, &dsp, &cb,
-                        &tdp, &pp, &dp, &tr, &tc, &rsp, &rcp};
-        KM_CK(cudaLaunchCooperativeKernel((void*)km::k_fp2_sequential<T, A>, dim3(fp2_blocks), dim3(256), args, 0,
-                                          st));
-        ++launches;
+        KM_CK(cudaMemcpyAsync(fp2_m, &m, sizeof(int), cudaMemcpyHostToDevice, st));
+        KM_TRY(launch_fp2_sequential(colsrc, colidx_dev));
         KM_CK(cudaMemcpyAsync(h_dec, dec, sizeof(Dec), cudaMemcpyDeviceToHost, st));
         KM_CK(cudaStreamSynchronize(st));
         const int done = h_dec->swaps;
@@ -995,17 +988,66 @@ struct Impl : ImplBase {
     }
 
     // One single-GPU FastPAM2 iteration (reading R6).
+    // One FastPAM2 iteration with the plan on the device (k_fp2_plan): the
+    // host waits once, at the end (KM_FP2_HOSTPLAN=1: the host orders the
+    // slots, as the sharded path does).
+    int fp2_hostplan = -1;
     km_status swap_iter_fp2(int32_t* swaps_out, void* td_out) {
         fp1_prepped = false;
         inc_valid = false;
+        if (fp2_hostplan < 0) {
+            const char* e = getenv("KM_FP2_HOSTPLAN");
+            fp2_hostplan = (e && e[0] == '1') ? 1 : 0;
+        }
         KM_TRY(fp2_eval_local());
-        A tdh;
-        KM_CK(cudaMemcpyAsync(h_best.data(), fp2_best, k * sizeof(Rec), cudaMemcpyDeviceToHost, st));
-        KM_CK(cudaMemcpyAsync(&tdh, td, sizeof(A), cudaMemcpyDeviceToHost, st));
+        if (fp2_hostplan) {
+            A tdh;
+            KM_CK(cudaMemcpyAsync(h_best.data(), fp2_best, k * sizeof(Rec), cudaMemcpyDeviceToHost, st));
+            KM_CK(cudaMemcpyAsync(&tdh, td, sizeof(A), cudaMemcpyDeviceToHost, st));
+            KM_CK(cudaStreamSynchronize(st));
+            KM_TRY(fp2_finish_profiling());
+            const std::vector<int> order = fp2_order_slots(tdh);
+            return fp2_sequential(order, nullptr, nullptr, swaps_out, td_out);
+        }
+        km::k_fp2_plan<A><<<1, 1024, 0, st>>>(fp2_best, k, td, dec, fp2_order, fp2_m, fp2_swaps_prev);
+        KM_CKL();
+        KM_TRY(launch_fp2_sequential(nullptr, nullptr));
+        km::k_fp2_finish<A><<<1, 1, 0, st>>>(dec, fp2_swaps_prev);
+        KM_CKL();
+        launches += 2;
+        KM_CK(cudaMemcpyAsync(h_dec, dec, sizeof(Dec), cudaMemcpyDeviceToHost, st));
+        KM_CK(cudaMemcpyAsync(h_td, td, sizeof(A), cudaMemcpyDeviceToHost, st));
         KM_CK(cudaStreamSynchronize(st));
         KM_TRY(fp2_finish_profiling());
-        const std::vector<int> order = fp2_order_slots(tdh);
-        return fp2_sequential(order, nullptr, nullptr, swaps_out, td_out);
+        // this iteration's swaps: the tail of the trace (dec->swaps counts all)
+        int done = 0;
+        KM_CK(cudaMemcpy(&done, fp2_m + 1, sizeof(int), cudaMemcpyDeviceToHost));
+        last_swaps.resize(std::min(done, trace_cap));
+        if (!last_swaps.empty())
+            KM_CK(cudaMemcpy(last_swaps.data(), trace, last_swaps.size() * sizeof(Rec), cudaMemcpyDeviceToHost));
+        if (swaps_out) *swaps_out = done;
+        if (td_out) memcpy(td_out, h_td, sizeof(A));
+        return done > 0 ? KM_OK : KM_CONVERGED;
+    }
+
+    int* fp2_m = nullptr;            // [2]: improving slots m; swaps of the iteration
+    int* fp2_swaps_prev = nullptr;
+    km_status launch_fp2_sequential(const T* colsrc, const int* colidx_dev) {
+        const T* Dp = D; int64_t ldv = ld; int nn = (int)n; int kk = k;
+        int* Mp = M; int* psp = point_slot; T* MCp = MC; int* nr = near; int* sc = sec; T* dnp = dn; T* dsp = ds;
+        T* cb = fp2_cols; A* tdp = td; A* pp = fp2_partials; Dec* dp = dec; Rec* tr = trace; int tc = trace_cap;
+        int* op = fp2_order; Rec* bp = fp2_best; const int* mp = fp2_m;
+        const T* csp = colsrc; const int* cip = colidx_dev;
+        int* rsp = rescan; int* rcp = rescan_count;
+        void* args[] = {&Dp, &ldv, &csp, &cip, &nn, &kk, &op, &mp, &bp, &Mp, &psp, &MCp, &nr, &sc, &dnp, &dsp, &cb,
+                        &tdp, &pp, &dp, &tr, &tc, &rsp, &rcp};
+        KM_CK(cudaLaunchCooperativeKernel((void*)km::k_fp2_sequential<T, A>, dim3(fp2_blocks), dim3(256), args, 0,
+                                          st));
+        ++launches;
+        // swaps of this iteration (the kernel counted them in dec->swaps from 0)
+        km::k_fp2_count<A><<<1, 1, 0, st>>>(dec, fp2_m + 1);
+        KM_CKL();
+        return KM_OK;
     }
 
     // ---- FasterPAM (Alg.4; readings F1-F5) -------------------------
