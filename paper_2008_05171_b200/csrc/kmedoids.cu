@@ -297,7 +297,8 @@ struct Impl : ImplBase {
 
                                : choose_parts(n, w, STREAM_COLS, RESIDENT_CTAS);
         const char* ep = getenv("KM_PARTS");          // measurement override of the stream's row parts
-        if (ep && atoi(ep) > 0) P = std::min<int>(atoi(ep), (int)std::max<int64_t>(1, n / 64));
+        // (<= 4096: km::part_lo's int64 products stay in range for any n < 2^31)
+        if (ep && atoi(ep) > 0) P = std::min<int>(std::min(atoi(ep), 4096), (int)std::max<int64_t>(1, n / 64));
         {
             // part-size tilt of the streams (km_common.cuh part_lo); one value
             // per process (a __constant__ of this device), KM_PART_SKEW in 16ths
