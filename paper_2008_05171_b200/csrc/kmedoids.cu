@@ -1530,6 +1530,11 @@ struct Impl : ImplBase {
     double* init_u = nullptr;
     int* init_seq = nullptr;
     size_t init_seq_cap = 0;
+    T* init_sub = nullptr;
+    size_t init_sub_cap = 0;
+    A* initw_bsum = nullptr;
+    int* initw_picks = nullptr;
+    int initw_blocks = 0, initw_picks_cap = 0;
 
     km_status finish_init(int32_t* M_out, void* td_out) {
         std::vector<int32_t> Mh((size_t)k);
@@ -1550,8 +1555,27 @@ struct Impl : ImplBase {
         KM_TRY(init_common_alloc(&w, &fl));
         if (!init_u) KM_TRY(alloc(&init_u, k));
         KM_CK(cudaMemcpyAsync(init_u, u, k * sizeof(double), cudaMemcpyHostToDevice, st));
-        km::k_init_weighted<T, A><<<1, km::INIT_THREADS, 0, st>>>(D, ld, (int)n, k, init_u, M, w, fl);
-        KM_CKL();
+        const char* ew = getenv("KM_INIT_WEIGHTED");       // "block": the single-block kernel
+        if (ew && strcmp(ew, "block") == 0) {
+            km::k_init_weighted<T, A><<<1, km::INIT_THREADS, 0, st>>>(D, ld, (int)n, k, init_u, M, w, fl);
+            KM_CKL();
+        } else {
+            if (!initw_bsum) {
+                int dev = 0, nsm = 0;
+                KM_CK(cudaGetDevice(&dev));
+                KM_CK(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
+                initw_blocks = nsm;
+                KM_TRY(alloc(&initw_bsum, initw_blocks));
+            }
+            if (k > initw_picks_cap) { KM_TRY(alloc(&initw_picks, k)); initw_picks_cap = k; }
+            KM_CK(cudaMemsetAsync(initw_picks, 0x7f, (size_t)k * sizeof(int), st));   // > any index
+            const int nb = (int)std::max<int64_t>(1, std::min<int64_t>(initw_blocks, cdiv(n, km::INITW_THREADS)));
+            const T* Dp = D; int64_t ldv = ld; int nn = (int)n; int kk = k; const double* up = init_u;
+            int* Mp = M; T* wp = w; int* fp = fl; A* bp = initw_bsum; int* pp = initw_picks;
+            void* args[] = {&Dp, &ldv, &nn, &kk, &up, &Mp, &wp, &fp, &bp, &pp};
+            KM_CK(cudaLaunchCooperativeKernel((void*)km::k_init_weighted_coop<T, A>, dim3(nb),
+                                              dim3(km::INITW_THREADS), args, 0, st));
+        }
         ++launches;
         return finish_init(M_out, td_out);
     }
@@ -1569,8 +1593,13 @@ struct Impl : ImplBase {
             KM_TRY(alloc(&init_seq, cnt + (size_t)s));
             init_seq_cap = cnt + (size_t)s;
         }
+        if ((size_t)s * s > init_sub_cap) {          // the sample's s x s sub-matrix (grows only)
+            KM_TRY(alloc(&init_sub, (size_t)s * s));
+            init_sub_cap = (size_t)s * s;
+        }
         KM_CK(cudaMemcpyAsync(init_seq, seq, cnt * sizeof(int), cudaMemcpyHostToDevice, st));
-        km::k_init_lab<T, A><<<1, km::INIT_THREADS, 0, st>>>(D, ld, (int)n, k, s, init_seq, M, w, fl, init_seq + cnt);
+        km::k_init_lab<T, A><<<1, km::INIT_THREADS, 0, st>>>(D, ld, (int)n, k, s, init_seq, M, w, fl, init_seq + cnt,
+                                                               init_sub);
         KM_CKL();
         ++launches;
         return finish_init(M_out, td_out);
