@@ -316,6 +316,120 @@ k_init_lab(const T* __restrict__ D, int64_t ld, int n, int k, int s, const int* 
     }
 }
 
+// LAB over the whole GPU (cooperative; default).  Per step i:
+//   block 0: the sample (first s non-medoids of row i, block scan)  | grid sync
+//   all blocks: gather the s x s sub-matrix; fold the previous step's
+//     medoid column into d_nearest (own object chunk)                | grid sync
+//   all blocks: one thread per candidate sums its column of the sub-matrix
+//     in sample order (the oracle's order: exact on float), block min | grid sync
+//   block 0: the lexicographic min over the blocks -> M[i], ismed    | grid sync
+template <typename T, typename A>
+__global__ void __launch_bounds__(INIT_THREADS)
+k_init_lab_coop(const T* __restrict__ D, int64_t ld, int n, int k, int s, const int* __restrict__ seq,
+                int* __restrict__ M, T* __restrict__ dnear, int* __restrict__ ismed, int* __restrict__ S,
+                T* __restrict__ sub, int* __restrict__ ctl, Rec<A>* __restrict__ bmin) {
+    namespace cg = cooperative_groups;
+    cg::grid_group grid = cg::this_grid();
+    __shared__ int s_base, s_total;
+    __shared__ int sh_scan[32];
+    __shared__ A sg[32];
+    __shared__ int sc[32];
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int nb = gridDim.x, b = blockIdx.x;
+    const int gt = b * INIT_THREADS + tid, nth = nb * INIT_THREADS;
+    const int ch = (n + nb - 1) / nb;
+    const int o0 = min(n, b * ch), o1 = min(n, o0 + ch);
+    const int L = s + k;
+    int prev = -1;                               // medoid of the previous step
+    for (int i = 0; i < k; ++i) {
+        if (b == 0) {
+            const int* row = seq + (int64_t)i * L;
+            if (tid == 0) s_base = 0;
+            __syncthreads();
+            for (int j0 = 0; j0 < L; j0 += INIT_THREADS) {
+                const int base = s_base;
+                if (base >= s) break;
+                const int j = j0 + tid;
+                const int c = j < L ? row[j] : -1;
+                const int f = (c >= 0 && !ismed[c]) ? 1 : 0;
+                const int pos = base + init_block_sum_prefix<int>(f, sh_scan, &s_total);
+                if (f && pos < s) S[pos] = c;
+                __syncthreads();
+                if (tid == 0) s_base = base + s_total;
+                __syncthreads();
+            }
+            if (tid == 0) ctl[0] = min(s_base, s);
+        }
+        grid.sync();
+        const int m = __ldcg(&ctl[0]);
+        for (int64_t e = gt; e < (int64_t)m * m; e += nth) {
+            const int bb = (int)(e / m), a = (int)(e - (int64_t)bb * m);
+            sub[e] = D[(int64_t)__ldcg(&S[bb]) * ld + __ldcg(&S[a])];
+        }
+        if (prev >= 0)
+            for (int o = o0 + tid; o < o1; o += INIT_THREADS) {
+                const T d = D[(int64_t)o * ld + prev];
+                if (i == 1 || d < dnear[o]) dnear[o] = d;
+            }
+        grid.sync();
+        A bg = amax<A>();
+        int bc = INT_MAX;
+        for (int a = gt; a < m; a += nth) {
+            const int c = __ldcg(&S[a]);
+            A g = 0;
+            for (int bb = 0; bb < m; ++bb) {     // sample order: the oracle's summation order
+                const A d = (A)__ldcg(&sub[(int64_t)bb * m + a]);
+                if (i == 0) g += d;
+                else {
+                    const A delta = d - (A)__ldcg(&dnear[__ldcg(&S[bb])]);
+                    if (delta < 0) g += delta;
+                }
+            }
+            if (g < bg || (g == bg && c < bc)) { bg = g; bc = c; }
+        }
+#pragma unroll
+        for (int x = 16; x >= 1; x >>= 1) {
+            const A og = __shfl_xor_sync(FULL, bg, x);
+            const int oc = __shfl_xor_sync(FULL, bc, x);
+            if (og < bg || (og == bg && oc < bc)) { bg = og; bc = oc; }
+        }
+        if (lane == 0) { sg[warp] = bg; sc[warp] = bc; }
+        __syncthreads();
+        if (warp == 0) {
+            bg = sg[lane]; bc = sc[lane];
+#pragma unroll
+            for (int x = 16; x >= 1; x >>= 1) {
+                const A og = __shfl_xor_sync(FULL, bg, x);
+                const int oc = __shfl_xor_sync(FULL, bc, x);
+                if (og < bg || (og == bg && oc < bc)) { bg = og; bc = oc; }
+            }
+            if (lane == 0) { Rec<A> r; r.v = bg; r.slot = 0; r.c = bc; bmin[b] = r; }
+        }
+        grid.sync();
+        if (b == 0 && warp == 0) {
+            Rec<A> best = rec_none<A>();
+            for (int q = lane; q < nb; q += 32) {
+                Rec<A> r; r.v = __ldcg(&bmin[q].v); r.slot = 0; r.c = __ldcg(&bmin[q].c);
+                if (r.v < best.v || (r.v == best.v && r.c < best.c)) best = r;
+            }
+#pragma unroll
+            for (int x = 16; x >= 1; x >>= 1) {
+                const A og = __shfl_xor_sync(FULL, best.v, x);
+                const int oc = __shfl_xor_sync(FULL, best.c, x);
+                if (og < best.v || (og == best.v && oc < best.c)) { best.v = og; best.c = oc; }
+            }
+            if (lane == 0) { M[i] = best.c; ismed[best.c] = 1; ctl[1] = best.c; }
+        }
+        grid.sync();
+        prev = __ldcg(&ctl[1]);
+    }
+    // the last medoid's column
+    for (int o = o0 + tid; o < o1; o += INIT_THREADS) {
+        const T d = D[(int64_t)o * ld + prev];
+        if (k == 1 || d < dnear[o]) dnear[o] = d;
+    }
+}
+
 // FastCLARA (NEXT-3): the sub-matrix of a sample, sub[a][b] = d(x_S[a], x_S[b])
 // = D[S[a]][S[b]] (reading R0 orientation), row stride lds.
 template <typename T>

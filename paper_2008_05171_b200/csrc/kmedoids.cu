@@ -1532,6 +1532,9 @@ struct Impl : ImplBase {
     size_t init_seq_cap = 0;
     T* init_sub = nullptr;
     size_t init_sub_cap = 0;
+    int* initl_ctl = nullptr;
+    Rec* initl_bmin = nullptr;
+    int initl_blocks = 0;
     A* initw_bsum = nullptr;
     int* initw_picks = nullptr;
     int initw_blocks = 0, initw_picks_cap = 0;
@@ -1598,9 +1601,28 @@ struct Impl : ImplBase {
             init_sub_cap = (size_t)s * s;
         }
         KM_CK(cudaMemcpyAsync(init_seq, seq, cnt * sizeof(int), cudaMemcpyHostToDevice, st));
-        km::k_init_lab<T, A><<<1, km::INIT_THREADS, 0, st>>>(D, ld, (int)n, k, s, init_seq, M, w, fl, init_seq + cnt,
-                                                               init_sub);
-        KM_CKL();
+        const char* el = getenv("KM_INIT_LAB");            // "block": the single-block kernel
+        if (el && strcmp(el, "block") == 0) {
+            km::k_init_lab<T, A><<<1, km::INIT_THREADS, 0, st>>>(D, ld, (int)n, k, s, init_seq, M, w, fl,
+                                                                   init_seq + cnt, init_sub);
+            KM_CKL();
+        } else {
+            if (!initl_ctl) {
+                int dev = 0, nsm = 0;
+                KM_CK(cudaGetDevice(&dev));
+                KM_CK(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
+                initl_blocks = nsm;
+                KM_TRY(alloc(&initl_ctl, 2));
+                KM_TRY(alloc(&initl_bmin, initl_blocks));
+            }
+            const int nb = (int)std::max<int64_t>(1, std::min<int64_t>(initl_blocks, cdiv(n, km::INIT_THREADS)));
+            const T* Dp = D; int64_t ldv = ld; int nn = (int)n; int kk = k; int ss = s; const int* sq = init_seq;
+            int* Mp = M; T* wp = w; int* fp = fl; int* Sp = init_seq + cnt; T* sp = init_sub; int* cp = initl_ctl;
+            Rec* bp = initl_bmin;
+            void* args[] = {&Dp, &ldv, &nn, &kk, &ss, &sq, &Mp, &wp, &fp, &Sp, &sp, &cp, &bp};
+            KM_CK(cudaLaunchCooperativeKernel((void*)km::k_init_lab_coop<T, A>, dim3(nb), dim3(km::INIT_THREADS),
+                                              args, 0, st));
+        }
         ++launches;
         return finish_init(M_out, td_out);
     }
