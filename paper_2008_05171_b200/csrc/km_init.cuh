@@ -9,8 +9,9 @@
 //                    I2): BUILD's choice restricted to a subsample of
 //                    s = 10 + ceil(sqrt(n)) non-medoids per step.
 // Both are sequential over the k steps and O(n) (weighted) / O(s^2 + n)
-// (LAB) per step -- small next to one SWAP pass -- and run as ONE block of
-// 1024 threads that loops over the steps (no launch or grid sync per step).
+// (LAB) per step -- small next to one SWAP pass.  Default: ONE cooperative
+// kernel over all SMs looping over the steps, grid syncs between a step's
+// phases (*_coop); the single-block versions are kept for comparison.
 #pragma once
 #include "km_kernels.cuh"
 
