@@ -121,3 +121,21 @@ def test_init_argument_errors():
         km.init_weighted([0.1, 1.5, 0.2])
     with pytest.raises(KMError):
         km.init_lab(3, np.full((3, 6), 11, np.int32))
+
+
+@pytest.mark.parametrize("which", ["weighted", "lab"])
+def test_single_block_and_cooperative_kernels_agree(monkeypatch, which):
+    """The cooperative seeding kernels (default) and the single-block ones
+    (KM_INIT_*=block) give the oracle's medoids on integer data."""
+    rng = np.random.default_rng(91)
+    n, k = 2100, 17
+    D = rand_int(rng, n, 3000)
+    u = rng.random(k)
+    s, rows = oracle.lab_sample_rows(n, k, seed=5)
+    ref = oracle.init_weighted(D, k, u) if which == "weighted" else oracle.init_lab(D, k, s, rows)
+    for mode in ("", "block"):
+        monkeypatch.setenv("KM_INIT_WEIGHTED" if which == "weighted" else "KM_INIT_LAB", mode)
+        km = KM(to_dev(D), n, k)
+        M, td = km.init_weighted(u) if which == "weighted" else km.init_lab(s, rows)
+        assert M.tolist() == ref.tolist(), mode
+        assert td == oracle.td(D, ref)
