@@ -229,6 +229,7 @@ struct Impl : ImplBase {
     ~Impl() override {
         for (auto& sl : clara_slots) { sl.sub.reset(); if (sl.stream) cudaStreamDestroy(sl.stream); }
         if (fp1_exec) cudaGraphExecDestroy(fp1_exec);
+        if (build_exec) cudaGraphExecDestroy(build_exec);
         if (cap_st) cudaStreamDestroy(cap_st);
         for (void* p : bufs) cudaFree(p);
         if (h_dec) cudaFreeHost(h_dec);
@@ -1739,7 +1740,7 @@ struct Impl : ImplBase {
     km_status launch_build_tma() {
         using C = km::SegCfg<T, SG_NC, SG_RB, SG_S>;
         auto kern = km::k_build_tma<T, A, SG_NC, SG_RB, SG_S, SG_MINB, MODE>;
-        KM_CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM));
+        if (!build_attr_set) KM_CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM));
         dim3 g((unsigned)cdiv(w, C::COLS), Pbt);
         kern<<<g, C::THREADS, C::SMEM, st>>>(D, ld, w, wpad, (int)n, Pbt, dn, b_out);
         KM_CKL();
@@ -1779,15 +1780,18 @@ struct Impl : ImplBase {
     }
 
     km_status build_finish() {
+        if (k >= 2) KM_TRY(assign_full_and_td());
+        KM_TRY(reset_counters());
+        build_finish_host();
+        return KM_OK;
+    }
+    void build_finish_host() {
         if (k >= 2) {
-            KM_TRY(assign_full_and_td());
             ready = true;
             fp3_reset();
             fp1_prepped = false;
             inc_valid = false;
         }
-        KM_TRY(reset_counters());
-        return KM_OK;
     }
 
     // ---- incremental BUILD (km_build_delta.cuh; KM_BUILD=full recomputes every step)
@@ -1820,12 +1824,12 @@ struct Impl : ImplBase {
         using C = km::SegCfg<T, SG_NC, SG_RB, SG_S>;
         if (step == 1) {
             auto kern = km::k_build_tma<T, A, SG_NC, SG_RB, SG_S, SG_MINB, 1>;
-            KM_CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM));
+            if (!build_attr_set) KM_CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM));
             dim3 g((unsigned)cdiv(w, C::COLS), Pbt);
             kern<<<g, C::THREADS, C::SMEM, st>>>(D, ld, w, wpad, (int)n, Pbt, dn, b_out);
         } else {
             auto kern = km::k_build_delta_tma<T, A, SG_NC, SG_RB, SG_S, SG_MINB>;
-            KM_CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM));
+            if (!build_attr_set) KM_CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM));
             dim3 g((unsigned)cdiv(w, C::COLS), Pbt);
             kern<<<g, C::THREADS, C::SMEM, st>>>(D, ld, w, wpad, Pbt, bd_m, bd_lo, bd_lold, bd_lnew, b_out);
         }
@@ -1862,9 +1866,76 @@ struct Impl : ImplBase {
         return KM_OK;
     }
 
+    // The k BUILD steps are ~6 small launches each with no host round trip;
+    // they are captured once into a CUDA graph (pointers are fixed per handle,
+    // so e.g. every CLARA sample of a nested handle replays the same graph).
+    // KM_BUILD_GRAPH=0 launches them directly.
+    cudaGraphExec_t build_exec = nullptr;
+    int build_graph = -1;
     km_status init_build(int32_t* M_out, void* td_out) override {
         if (sharded) return fail(KM_EINVAL, "init_build on a sharded handle; use kmedoids_build_* phases");
         KM_TRY(bd_init());
+        if (build_graph < 0) {
+            const char* e = getenv("KM_BUILD_GRAPH");
+            build_graph = (e && e[0] == '0') ? 0 : 1;
+        }
+        // a graph pays off only when replayed (capture + instantiate cost about
+        // one direct BUILD): capture on the second BUILD of this handle
+        const bool use_g = build_graph == 1 && (build_exec || build_calls >= 1);
+        ++build_calls;
+        if (use_g && !build_exec) {
+            // kernel attributes are set outside the capture
+            using C = km::SegCfg<T, SG_NC, SG_RB, SG_S>;
+            KM_CK(cudaFuncSetAttribute(km::k_build_tma<T, A, SG_NC, SG_RB, SG_S, SG_MINB, 0>,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM));
+            KM_CK(cudaFuncSetAttribute(km::k_build_tma<T, A, SG_NC, SG_RB, SG_S, SG_MINB, 1>,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM));
+            KM_CK(cudaFuncSetAttribute(km::k_build_delta_tma<T, A, SG_NC, SG_RB, SG_S, SG_MINB>,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM));
+            build_attr_set = true;
+            if (!cap_st) KM_CK(cudaStreamCreateWithFlags(&cap_st, cudaStreamNonBlocking));
+            cudaStream_t user_st = st;
+            st = cap_st;
+            const int64_t l0 = launches;
+            cudaError_t be = cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal);
+            km_status cs = KM_ECUDA;
+            if (be == cudaSuccess) {
+                capturing = true;
+                cs = build_steps();
+                capturing = false;
+            }
+            cudaGraph_t g = nullptr;
+            cudaError_t ce = be == cudaSuccess ? cudaStreamEndCapture(st, &g) : be;
+            st = user_st;
+            bool ok = cs == KM_OK && ce == cudaSuccess;
+            if (ok && cudaGraphInstantiate(&build_exec, g, 0) != cudaSuccess) { build_exec = nullptr; ok = false; }
+            if (g) cudaGraphDestroy(g);
+            build_graph_kernels = launches - l0;
+            launches = l0;
+            if (!ok) {
+                cudaGetLastError();
+                fprintf(stderr, "[kmedoids] BUILD graph unavailable (%s); launching directly\n", cudaGetErrorString(ce));
+                build_graph = 0;
+            }
+        }
+        if (use_g && build_graph == 1) {
+            KM_CK(cudaGraphLaunch(build_exec, st));
+            launches += build_graph_kernels;
+        } else {
+            KM_TRY(build_steps());
+        }
+        build_finish_host();                     // host-side state (not part of a graph replay)
+        KM_CK(cudaStreamSynchronize(st));
+        if (M_out) KM_CK(cudaMemcpy(M_out, M, k * sizeof(int32_t), cudaMemcpyDeviceToHost));
+        copy_td(td_out);
+        return KM_OK;
+    }
+    bool build_attr_set = false;
+    int64_t build_graph_kernels = 0;
+    int build_calls = 0;
+
+    // the k steps of Alg.1 and the cache of the result, enqueued on st
+    km_status build_steps() {
         KM_CK(cudaMemsetAsync(point_slot, 0xff, n * sizeof(int), st));
         ready = false;
         const int nb = (int)cdiv(n, 256);
@@ -1888,9 +1959,6 @@ struct Impl : ImplBase {
             }
         }
         KM_TRY(build_finish());
-        KM_CK(cudaStreamSynchronize(st));
-        if (M_out) KM_CK(cudaMemcpy(M_out, M, k * sizeof(int32_t), cudaMemcpyDeviceToHost));
-        copy_td(td_out);
         return KM_OK;
     }
 

@@ -70,3 +70,22 @@ def test_clara_argument_errors():
         km.clara(np.array([[0, 1, 2]], np.int32))            # s <= k
     with pytest.raises(KMError):
         km.clara(np.array([[0, 1, 2, 2, 5]], np.int32))      # duplicate
+
+
+@pytest.mark.parametrize("variant", ["fastpam1", "fasterpam"])
+def test_clara_many_samples_reuse_nested_handles(variant):
+    """More samples than concurrent slots: nested handles run several samples
+    (their BUILD is replayed from a captured CUDA graph from the second one
+    on); every sample must still equal the oracle exactly (int)."""
+    cfg = kmsynth.CONFIGS[5]
+    n, k = 1500, 8
+    X = kmsynth.make_points(cfg, n=n)
+    Dt = kmsynth.dist_cuda(X, cfg.metric)
+    D = kmsynth.as_numpy_D(Dt)[:, :n]
+    S = samples_for(n, k, 19, cfg.seed + 4100)
+    t, j, M = oracle.clara(D, k, S, variant)
+    km = KM(Dt, n, k)
+    Mg, tg, jg = km.clara(S, variant)
+    assert (Mg.tolist(), tg, jg) == (M.tolist(), t, j)
+    Mg2, tg2, jg2 = km.clara(S, variant)                     # the same handle again (all replays)
+    assert (Mg2.tolist(), tg2, jg2) == (M.tolist(), t, j)
