@@ -705,7 +705,9 @@ struct Impl : ImplBase {
         KM_CK(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
         KM_CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, km::POST_THREADS, sm));
         if (per_sm < 1) return fail(KM_ECUDA, "k_fp1_post cannot be resident");
-        post_blocks = std::min(nsm * std::min(per_sm, 4), km::POST_MAX_BLOCKS);
+        int bps = 4;                                    // blocks per SM (KM_POST_BPS: measurement override)
+        if (const char* e = getenv("KM_POST_BPS")) bps = std::max(1, std::min(8, atoi(e)));
+        post_blocks = std::min(nsm * std::min(per_sm, bps), km::POST_MAX_BLOCKS);
         post_blocks = (int)std::min<int64_t>(post_blocks, std::max<int64_t>(1, cdiv(n, 64)));
         KM_TRY(alloc(&post_counts, (size_t)k * post_blocks));
         KM_TRY(alloc(&post_offsets, (size_t)k * post_blocks));
