@@ -750,6 +750,21 @@ __device__ __forceinline__ uint64_t policy_evict_first() {
     asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
     return p;
 }
+__device__ __forceinline__ uint64_t policy_evict_last() {
+    uint64_t p;
+    asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+    return p;
+}
+// 8- / 4-byte stores with an L2 eviction-priority hint
+__device__ __forceinline__ void st_hint(double* p, double v, uint64_t pol) {
+    asm volatile("st.global.L2::cache_hint.f64 [%0], %1, %2;" :: "l"(p), "d"(v), "l"(pol) : "memory");
+}
+__device__ __forceinline__ void st_hint(long long* p, long long v, uint64_t pol) {
+    asm volatile("st.global.L2::cache_hint.b64 [%0], %1, %2;" :: "l"(p), "l"(v), "l"(pol) : "memory");
+}
+__device__ __forceinline__ void st_hint(int* p, int v, uint64_t pol) {
+    asm volatile("st.global.L2::cache_hint.b32 [%0], %1, %2;" :: "l"(p), "r"(v), "l"(pol) : "memory");
+}
 __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar, uint64_t pol) {
     asm volatile(
         "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;" ::"r"(
@@ -1838,11 +1853,19 @@ k_swap_stream_seg2(const T* __restrict__ D, int64_t ld, int w, int wpad, int n, 
     const bool active = cb < w;
     const int64_t obase = (int64_t)q * w + cb;
     const int jmax = active ? min(4, w - cb) : 0;
+    // the part outputs (read by the combine right after the stream) are
+    // stored with L2 evict_last, the streamed D rows are loaded evict_first
+    const uint64_t keep = ptx::policy_evict_last();
     A plus[4], seg[4];
 #pragma unroll
     for (int j = 0; j < 4; ++j) { plus[j] = 0; seg[j] = 0; }
 #pragma unroll
-    for (int j = 0; j < 4; ++j) if (j < jmax) { out_imin[obase + j] = amax<A>(); out_islot[obase + j] = -1; out_head[obase + j] = 0; }
+    for (int j = 0; j < 4; ++j)
+        if (j < jmax) {
+            ptx::st_hint(&out_imin[obase + j], amax<A>(), keep);
+            ptx::st_hint(&out_islot[obase + j], -1, keep);
+            ptx::st_hint(&out_head[obase + j], (A)0, keep);
+        }
     int cur = ri[p0].slot;
     bool first = true;
     const T* srow0 = sdata + (warp * 128 + lane * 4);
@@ -1857,7 +1880,7 @@ k_swap_stream_seg2(const T* __restrict__ D, int64_t ld, int w, int wpad, int n, 
         if (slot != cur) {                       // segment boundary (warp-uniform, rare)
             if (first) {
 #pragma unroll
-                for (int j = 0; j < 4; ++j) if (j < jmax) out_head[obase + j] = seg[j];
+                for (int j = 0; j < 4; ++j) if (j < jmax) ptx::st_hint(&out_head[obase + j], seg[j], keep);
                 first = false;
             } else {
                 const A rv = R[cur];
@@ -1866,7 +1889,10 @@ k_swap_stream_seg2(const T* __restrict__ D, int64_t ld, int w, int wpad, int n, 
                     if (j >= jmax) continue;
                     if (out_acc) out_acc[(int64_t)cur * w + cb + j] = seg[j];
                     const A val = rv + seg[j];
-                    if (val < out_imin[obase + j]) { out_imin[obase + j] = val; out_islot[obase + j] = cur; }
+                    if (val < out_imin[obase + j]) {
+                        ptx::st_hint(&out_imin[obase + j], val, keep);
+                        ptx::st_hint(&out_islot[obase + j], cur, keep);
+                    }
                 }
             }
 #pragma unroll
@@ -1931,9 +1957,9 @@ k_swap_stream_seg2(const T* __restrict__ D, int64_t ld, int w, int wpad, int n, 
 #pragma unroll
     for (int j = 0; j < 4; ++j) {
         if (j >= jmax) continue;
-        if (first) { out_head[obase + j] = seg[j]; out_tail[obase + j] = 0; }
-        else out_tail[obase + j] = seg[j];
-        out_plus[obase + j] = plus[j];
+        if (first) { ptx::st_hint(&out_head[obase + j], seg[j], keep); ptx::st_hint(&out_tail[obase + j], (A)0, keep); }
+        else ptx::st_hint(&out_tail[obase + j], seg[j], keep);
+        ptx::st_hint(&out_plus[obase + j], plus[j], keep);
     }
 }
 
