@@ -1808,6 +1808,7 @@ k_swap_stream_seg2(const T* __restrict__ D, int64_t ld, int w, int wpad, int n, 
         // ---------------- producer warp (as k_swap_stream_seg) ----------------
         const uint32_t cbytes = (uint32_t)min(C::COLS, wpad - ctacol) * (uint32_t)sizeof(T);
         const uint64_t pol = ptx::policy_evict_first();
+        const uint64_t keep = ptx::policy_evict_last();   // row metadata: re-read by every column tile
         int64_t pr = p0;
         int s = 0, ph = 0, st = 0;
         int o_l = 0, sl_l = -1;
@@ -1832,8 +1833,8 @@ k_swap_stream_seg2(const T* __restrict__ D, int64_t ld, int w, int wpad, int n, 
             if (lane < nb)
                 ptx::bulk_g2s(sdata + (size_t)(s * RB + lane) * C::COLS, D + (int64_t)o_l * ld + ctacol, cbytes,
                               &full[s], pol);
-            if (lane == 0) ptx::bulk_g2s(sri + s * RB, ri + pr, (uint32_t)nb * 16u, &full[s]);
-            if (lane == 1 && rowd) ptx::bulk_g2s(srd + s * RB, rowd + pr, (uint32_t)nb * 16u, &full[s]);
+            if (lane == 0) ptx::bulk_g2s(sri + s * RB, ri + pr, (uint32_t)nb * 16u, &full[s], keep);
+            if (lane == 1 && rowd) ptx::bulk_g2s(srd + s * RB, rowd + pr, (uint32_t)nb * 16u, &full[s], keep);
             pr += nb;
             const int o_sh = __shfl_down_sync(FULL, o_l, nb);
             const int s_sh = __shfl_down_sync(FULL, sl_l, nb);
