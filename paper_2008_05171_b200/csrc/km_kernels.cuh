@@ -1768,7 +1768,7 @@ k_swap_stream_seg2(const T* __restrict__ D, int64_t ld, int w, int wpad, int n, 
                    const RowInfo<T>* __restrict__ ri, const A* __restrict__ R,
                    A* __restrict__ out_plus, A* __restrict__ out_head, A* __restrict__ out_tail,
                    A* __restrict__ out_imin, int* __restrict__ out_islot, A* __restrict__ out_acc,
-                   const double2* __restrict__ rowd) {
+                   const double2* __restrict__ rowd, bool acc_keep = false) {
     using C = SegCfg<T, NC, RB, S>;
     using V = typename Vec4<T>::type;
     static_assert(RB == 4, "four rows per stage");
@@ -1888,7 +1888,10 @@ k_swap_stream_seg2(const T* __restrict__ D, int64_t ld, int w, int wpad, int n, 
 #pragma unroll
                 for (int j = 0; j < 4; ++j) {
                     if (j >= jmax) continue;
-                    if (out_acc) out_acc[(int64_t)cur * w + cb + j] = seg[j];
+                    if (out_acc) {
+                        if (acc_keep) ptx::st_hint(&out_acc[(int64_t)cur * w + cb + j], seg[j], keep);
+                        else out_acc[(int64_t)cur * w + cb + j] = seg[j];
+                    }
                     const A val = rv + seg[j];
                     if (val < out_imin[obase + j]) {
                         ptx::st_hint(&out_imin[obase + j], val, keep);

@@ -620,8 +620,11 @@ struct Impl : ImplBase {
             seg2_attr_set = true;
         }
         dim3 g((unsigned)cdiv(ww, C::COLS), Pw);
+        // FastPAM2 / window k-vectors kept in L2 for the per-slot reduction
+        // that follows when they fit comfortably (C3: 16 MB), else streamed
+        const bool acc_keep = acc_out && (size_t)k * ww * sizeof(A) <= ((size_t)48 << 20);
         kern<<<g, C::THREADS, C::SMEM, st>>>(Dw, ld, ww, wpadw, (int)n, Pw, ri, R, plus_o, head_o, tail_o, imin_o,
-                                              islot_o, acc_out, rowd);
+                                              islot_o, acc_out, rowd, acc_keep);
         return KM_OK;
     }
 
