@@ -189,9 +189,10 @@ k_build_delta_tma(const T* __restrict__ D, int64_t ld, int w, int wpad, int P, c
     }
     if (!active) return;
     const int64_t base = (int64_t)q * w;
+    const uint64_t keep = ptx::policy_evict_last();   // read by the gain combine right after
 #pragma unroll
     for (int j = 0; j < 4; ++j)
-        if (cb + j < w) out[base + cb + j] = acc[j];
+        if (cb + j < w) ptx::st_hint(&out[base + cb + j], acc[j], keep);
 }
 
 // gain[c] (+)= sum of the parts; lexicographic min of (gain, c) over non-medoids
