@@ -117,16 +117,10 @@ k_fp1_post(PostArgs<T, A> g) {
         }
         __syncthreads();
         d = sdec;
-        grid.sync(); post_stamp(g.tph, 1);                                 // every block has read M / td / dec
-        if (b == 0 && threadIdx.x == 0) {
-            *g.dec = d;
-            if (d.apply) {
-                g.M[d.slot] = d.c;
-                g.point_slot[d.old_m] = -1;
-                g.point_slot[d.c] = d.slot;
-                *g.td = *g.td + d.dtd;
-            }
-        }
+        post_stamp(g.tph, 1);
+        // (block 0 records the decision in M / point_slot / TD / dec after
+        // the histogram's grid sync, when every block has read them; phases
+        // 1-3 do not read them)
 
         // ---- 1 apply: column c*, incremental nearest/second
         if (d.apply) {
@@ -190,6 +184,15 @@ k_fp1_post(PostArgs<T, A> g) {
     __syncthreads();
     for (int s = threadIdx.x; s < k; s += blockDim.x) g.counts[(int64_t)s * B + b] = h[s];
     grid.sync(); post_stamp(g.tph, 4);
+    if (!g.prep_only && b == 0 && threadIdx.x == 0) {
+        *g.dec = d;
+        if (d.apply) {
+            g.M[d.slot] = d.c;
+            g.point_slot[d.old_m] = -1;
+            g.point_slot[d.c] = d.slot;
+            *g.td = *g.td + d.dtd;
+        }
+    }
 
     // ---- 4 within-slot exclusive scan over the chunks, warp per slot: all
     // B counts of the slot loaded first (coalesced, one memory round trip),
@@ -221,9 +224,12 @@ k_fp1_post(PostArgs<T, A> g) {
     }
     grid.sync(); post_stamp(g.tph, 5);
 
-    // ---- 5 exclusive scan of the slot totals (block 0)
-    if (b == 0) {
+    // ---- 5 exclusive scan of the slot totals, by EVERY block into its shared
+    // memory (no grid sync: the scatter below reads the block's own copy);
+    // block 0 also writes seg_start[] for the removal loss and the stream
+    {
         __shared__ int wsum[POST_THREADS / 32];
+        int* segs = post_smem;                   // k ints: seg_start, then the scatter cursors
         const int per = (k + blockDim.x - 1) / blockDim.x;
         const int a = threadIdx.x * per, z = min(k, a + per);
         int sum = 0;
@@ -240,18 +246,20 @@ k_fp1_post(PostArgs<T, A> g) {
         for (int w = 0; w < (int)(threadIdx.x >> 5); ++w) base += wsum[w];
         int run = base + incl - sum;
         for (int i = a; i < z; ++i) {
-            g.seg_start[i] = run;
+            segs[i] = run;
+            if (b == 0) g.seg_start[i] = run;
             run += __ldcg(&g.slot_tot[i]);
         }
-        if (threadIdx.x == blockDim.x - 1) g.seg_start[k] = run;
-        if (threadIdx.x == 0) *g.empty_slot = INT_MAX;
+        if (b == 0 && threadIdx.x == blockDim.x - 1) g.seg_start[k] = run;
+        if (b == 0 && threadIdx.x == 0) *g.empty_slot = INT_MAX;
+        __syncthreads();
     }
-    grid.sync(); post_stamp(g.tph, 6);
+    post_stamp(g.tph, 6);
 
     // ---- 6 stable scatter into (slot, o) order: warp 0 of each block
     if (threadIdx.x < 32) {
-        int* cur = post_smem;
-        for (int s = lane; s < k; s += 32) cur[s] = __ldcg(&g.seg_start[s]) + __ldcg(&g.offsets[(int64_t)s * B + b]);
+        int* cur = post_smem;                    // seg_start of this block's copy + its chunk offsets
+        for (int s = lane; s < k; s += 32) cur[s] += __ldcg(&g.offsets[(int64_t)s * B + b]);
         __syncwarp();
         const unsigned lt = (1u << lane) - 1u;
         for (int base = e0; base < e1; base += 32) {
