@@ -90,6 +90,10 @@ k_fp1_post(PostArgs<T, A> g) {
     post_stamp(g.tph, 0);
 
     Decision<A> d{};
+    // block b owns the objects [ob0, ob1) in the apply and histogram phases
+    const int ochunk = (n + B - 1) / B;
+    const int ob0 = min(n, b * ochunk), ob1 = min(n, ob0 + ochunk);
+    bool counted = false;
     if (!g.prep_only) {
         // ---- 0 select (every block decides identically; block 0 records)
         if (threadIdx.x == 0) {
@@ -122,15 +126,20 @@ k_fp1_post(PostArgs<T, A> g) {
         // the histogram's grid sync, when every block has read them; phases
         // 1-3 do not read them)
 
-        // ---- 1 apply: column c*, incremental nearest/second
+        // ---- 1 apply: column c*, incremental nearest/second, over the block's
+        // chunk of objects; the chunk's histogram of the new nearest slots is
+        // counted on the way (the rescanned objects are added in phase 2)
         if (d.apply) {
             const int i = d.slot;
             const bool local = d.c >= g.c0 && d.c < g.c1;
-            for (int o = tid; o < n; o += nth) {
+            int* hh = post_smem;
+            for (int s = threadIdx.x; s < k; s += blockDim.x) hh[s] = 0;
+            __syncthreads();
+            for (int o = ob0 + threadIdx.x; o < ob1; o += blockDim.x) {
                 if (local) g.MC[(int64_t)i * n + o] = g.D[(int64_t)o * g.ld + (d.c - g.c0)];
             }
             // (the column is read back below by the same thread: same o mapping)
-            for (int o = tid; o < n; o += nth) {
+            for (int o = ob0 + threadIdx.x; o < ob1; o += blockDim.x) {
                 const int j1 = __ldcg(&g.near[o]), j2 = __ldcg(&g.sec[o]);
                 if (j1 == i || j2 == i) {
                     g.rescan[atomicAdd(g.rescan_count, 1)] = o;
@@ -140,10 +149,14 @@ k_fp1_post(PostArgs<T, A> g) {
                 const T d1 = __ldcg(&g.dn[o]), d2 = __ldcg(&g.ds[o]);
                 if (x < d1 || (x == d1 && i < j1)) {
                     g.near[o] = i; g.dn[o] = x; g.sec[o] = j1; g.ds[o] = d1;
-                } else if (x < d2 || (x == d2 && i < j2)) {
-                    g.sec[o] = i; g.ds[o] = x;
+                    atomicAdd(&hh[i], 1);
+                } else {
+                    if (x < d2 || (x == d2 && i < j2)) { g.sec[o] = i; g.ds[o] = x; }
+                    atomicAdd(&hh[j1], 1);
                 }
             }
+            __syncthreads();
+            for (int s = threadIdx.x; s < k; s += blockDim.x) g.counts[(int64_t)s * B + b] = hh[s];
             grid.sync(); post_stamp(g.tph, 2);
             // ---- 2 rescan
             const int cnt = __ldcg(g.rescan_count);
@@ -168,22 +181,28 @@ k_fp1_post(PostArgs<T, A> g) {
                         d2 = e1; j2 = f1;
                     }
                 }
-                if (lane == 0) { g.near[o] = j1; g.sec[o] = j2; g.dn[o] = d1; g.ds[o] = d2; }
+                if (lane == 0) {
+                    g.near[o] = j1; g.sec[o] = j2; g.dn[o] = d1; g.ds[o] = d2;
+                    atomicAdd(&g.counts[(int64_t)j1 * B + o / ochunk], 1);   // the owner chunk's histogram
+                }
             }
             grid.sync(); post_stamp(g.tph, 3);
+            counted = true;
         }
 
     }
-    // ---- 3 histogram of the block's chunk
-    const int chunk = (n + B - 1) / B;
-    const int e0 = min(n, b * chunk), e1 = min(n, e0 + chunk);
-    int* h = post_smem;
-    for (int s = threadIdx.x; s < k; s += blockDim.x) h[s] = 0;
-    __syncthreads();
-    for (int e = e0 + threadIdx.x; e < e1; e += blockDim.x) atomicAdd(&h[__ldcg(&g.near[e])], 1);
-    __syncthreads();
-    for (int s = threadIdx.x; s < k; s += blockDim.x) g.counts[(int64_t)s * B + b] = h[s];
-    grid.sync(); post_stamp(g.tph, 4);
+    // ---- 3 histogram of the block's chunk (when no swap was applied, or
+    // prep only; otherwise counted in phases 1-2)
+    const int e0 = ob0, e1 = ob1;
+    if (!counted) {
+        int* h = post_smem;
+        for (int s = threadIdx.x; s < k; s += blockDim.x) h[s] = 0;
+        __syncthreads();
+        for (int e = e0 + threadIdx.x; e < e1; e += blockDim.x) atomicAdd(&h[__ldcg(&g.near[e])], 1);
+        __syncthreads();
+        for (int s = threadIdx.x; s < k; s += blockDim.x) g.counts[(int64_t)s * B + b] = h[s];
+        grid.sync(); post_stamp(g.tph, 4);
+    }
     if (!g.prep_only && b == 0 && threadIdx.x == 0) {
         *g.dec = d;
         if (d.apply) {
