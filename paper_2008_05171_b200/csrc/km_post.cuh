@@ -7,15 +7,19 @@
 // column gather, incremental update, rescan, histogram, two scans, scatter,
 // removal loss, part metadata), each latency-bound, plus a launch gap each.
 // Here they are phases of one kernel separated by grid syncs (~1.2 us each,
-// measured), with the same arithmetic and the same deterministic orders:
-//   0 select    lexicographic min of the gathered records, acceptance R5,
-//               M / point_slot / TD bookkeeping (block 0)  -- as k_select
-//   1 apply     MC[i*] <- column c*; incremental nearest/second for every
-//               object; objects whose nearest/second was slot i* listed
-//   2 rescan    warp per listed object, (d, slot) top-2     -- as k_assign_rescan
-//   3 histogram per block chunk, counts[slot][block]
+// measured; 4 of them when a swap is applied), with the same arithmetic and
+// the same deterministic orders:
+//   0 select    lexicographic min of the gathered records, acceptance R5
+//               (every block; block 0 records M / point_slot / TD / dec after
+//               the next sync that follows phase 0)     -- as k_select
+//   1 apply     MC[i*] <- column c*; incremental nearest/second for the
+//               block's chunk of objects and its histogram of the new
+//               nearest slots; objects whose nearest/second was slot i* listed
+//   2 rescan    warp per listed object, (d, slot) top-2, added to its chunk's
+//               histogram                                -- as k_assign_rescan
+//   3 histogram per block chunk (only without a swap / prep only)
 //   4 scan      warp per slot over its chunk counts; slot totals
-//   5 scan      block 0: exclusive scan of the totals -> segment starts
+//   5 scan      every block: exclusive scan of the totals -> segment starts
 //   6 scatter   stable (slot, o) order, warp-ranked        -- as k_slot_scatter
 //   7 R, parts  removal loss per slot (fixed tree), empty slot, part heads/tails
 #pragma once
