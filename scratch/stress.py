@@ -24,7 +24,8 @@ rng = np.random.default_rng(int(sys.argv[1]) if len(sys.argv) > 1 else 1)
 t0 = time.time(); fails = 0; runs = 0
 while time.time() - t0 < float(sys.argv[2]) if len(sys.argv) > 2 else 240:
     n = int(rng.choice([5, 17, 64, 129, 300, 777, 1500, 2600]))
-    k = int(rng.integers(2, min(40, n - 1) + 1))
+    kmax = int(os.environ.get("STRESS_KMAX", "40"))
+    k = int(rng.integers(2, min(kmax, n - 1) + 1))
     hi = int(rng.choice([2, 7, 1000, 10**6]))
     D = rand_int(rng, n, hi, symmetric=bool(rng.integers(0, 4)))
     M0 = rng.choice(n, size=k, replace=False).astype(np.int32)
