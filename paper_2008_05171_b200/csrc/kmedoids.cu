@@ -560,6 +560,7 @@ struct Impl : ImplBase {
     // column (default); KM_COMBINE=par folds part groups in parallel warps and
     // merges them (measured 10-30 us SLOWER per step at C4/C5, kept for A/B)
     int combine_kind = -1;
+    int comb_tpb = -1;
     km_status launch_combine(int ww, int64_t colb, int Pw, const A* pl, const A* hd, const A* tl, const A* im,
                              const int* isl, const int* hsl, const int* tsl, A* cv, int* cs, A* acc_o, A* plus_o) {
         if (combine_kind < 0) {
@@ -569,7 +570,11 @@ struct Impl : ImplBase {
         const size_t sm = (size_t)k * sizeof(A) + 2 * (size_t)Pw * sizeof(int);
         const bool stage = sm <= 32 * 1024;
         if (combine_kind == 0) {
-            km::k_swap_combine<A><<<(unsigned)cdiv(ww, 128), 128, stage ? sm : 0, st>>>(
+            if (comb_tpb < 0) {                      // threads per block (KM_COMB_TPB: measurement override)
+                const char* e = getenv("KM_COMB_TPB");
+                comb_tpb = e ? std::max(32, std::min(256, atoi(e) / 32 * 32)) : 128;
+            }
+            km::k_swap_combine<A><<<(unsigned)cdiv(ww, comb_tpb), comb_tpb, stage ? sm : 0, st>>>(
                 ww, colb, Pw, pl, hd, tl, im, isl, hsl, tsl, R, empty_slot, point_slot, cv, cs, partials, counters,
                 rec_local, acc_o, plus_o, k, stage);
         }
