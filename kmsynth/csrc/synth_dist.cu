@@ -141,18 +141,24 @@ extern "C" double kmsynth_read_peak(const void* buf, int64_t bytes, int reps, vo
     const int64_t n16 = bytes / 16;
     cudaEvent_t a, b;
     cudaEventCreate(&a); cudaEventCreate(&b);
+    // the best of several launch shapes (blocks per SM x threads), so the
+    // denominator is not an artefact of one occupancy choice
+    const int shapes[3][2] = {{8, 256}, {4, 512}, {16, 256}};
     k_read_stream<<<nsm * 8, 256, 0, st>>>((const uint4*)buf, n16, sink);     // warm-up
     double best = 0.0;
-    for (int r = 0; r < reps; ++r) {
-        cudaEventRecord(a, st);
-        k_read_stream<<<nsm * 8, 256, 0, st>>>((const uint4*)buf, n16, sink);
-        cudaEventRecord(b, st);
-        cudaEventSynchronize(b);
-        float ms = 0.f;
-        cudaEventElapsedTime(&ms, a, b);
-        const double gbs = (double)n16 * 16 / (ms * 1e-3) / 1e9;
-        if (gbs > best) best = gbs;
-    }
+    for (const auto& sh : shapes)
+        for (int r = 0; r < reps; ++r) {
+            cudaEventRecord(a, st);
+            k_read_stream<<<nsm * sh[0], sh[1], 0, st>>>((const uint4*)buf, n16, sink);
+            if (cudaGetLastError() != cudaSuccess) break;     // shape not launchable: skip it
+            cudaEventRecord(b, st);
+            cudaEventSynchronize(b);
+            float ms = 0.f;
+            cudaEventElapsedTime(&ms, a, b);
+            if (!(ms > 0.f)) continue;
+            const double gbs = (double)n16 * 16 / (ms * 1e-3) / 1e9;
+            if (gbs > best) best = gbs;
+        }
     cudaEventDestroy(a); cudaEventDestroy(b);
     cudaFree(sink);
     return best;
