@@ -224,6 +224,21 @@ def read_peak_gbs(t, reps: int = 5, stream=None) -> float:
                    ctypes.c_void_p(st.cuda_stream)))
 
 
+def read_peak_bulk_gbs(t, reps: int = 5, stream=None) -> float:
+    """Read-only HBM bandwidth (GB/s) through TMA bulk copies into shared
+    memory (measurement helper; the SWAP stream's load path without compute)."""
+    import torch
+    global _lib
+    if _lib is None:
+        _lib = ctypes.CDLL(build_lib())
+    f = _lib.kmsynth_read_peak_bulk
+    f.restype = ctypes.c_double
+    f.argtypes = [ctypes.c_void_p, ctypes.c_int64, ctypes.c_int, ctypes.c_void_p]
+    st = stream if stream is not None else torch.cuda.current_stream(t.device)
+    return float(f(ctypes.c_void_p(t.data_ptr()), int(t.numel() * t.element_size()), int(reps),
+                   ctypes.c_void_p(st.cuda_stream)))
+
+
 def write_peak_gbs(t, reps: int = 5, stream=None) -> float:
     """Write-only HBM bandwidth (GB/s, best of reps) over the bytes of the CUDA
     tensor t, whose contents are OVERWRITTEN (measurement helper for bench.py's

@@ -102,7 +102,74 @@ __global__ void k_write_stream(uint4* __restrict__ p, int64_t n16, unsigned v) {
         asm volatile("st.global.L1::no_allocate.v4.u32 [%0], {%1,%2,%3,%4};" :: "l"(p + i), "r"(w.x), "r"(w.y),
                      "r"(w.z), "r"(w.w) : "memory");
 }
+// Read-only stream through TMA bulk copies into a shared-memory ring (what
+// the SWAP stream's producer does, with no consumer work): CTA-strided 16 KB
+// chunks, RING stages in flight per CTA.
+constexpr int RB_CHUNK = 16384, RB_RING = 4;
+__global__ void __launch_bounds__(32) k_read_bulk(const unsigned char* __restrict__ p, int64_t nchunks) {
+    extern __shared__ __align__(128) unsigned char rsm[];
+    __shared__ __align__(8) unsigned long long bar[RB_RING];
+    if (threadIdx.x != 0) return;
+    for (int s = 0; s < RB_RING; ++s)
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" :: "r"((unsigned)__cvta_generic_to_shared(&bar[s])));
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    unsigned ph[RB_RING] = {0, 0, 0, 0};
+    int64_t issued = 0, done = 0;
+    const int64_t first = blockIdx.x, step = gridDim.x;
+    auto issue = [&](int64_t c, int s) {
+        const unsigned b = (unsigned)__cvta_generic_to_shared(&bar[s]);
+        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" :: "r"(b), "r"(RB_CHUNK) : "memory");
+        asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+                     :: "r"((unsigned)__cvta_generic_to_shared(rsm + s * RB_CHUNK)), "l"(p + c * RB_CHUNK),
+                        "r"(RB_CHUNK), "r"(b) : "memory");
+    };
+    for (int64_t c = first; c < nchunks && issued < RB_RING; c += step) issue(c, (int)(issued++ % RB_RING));
+    for (int64_t c = first; c < nchunks; c += step) {
+        const int s = (int)(done % RB_RING);
+        const unsigned b = (unsigned)__cvta_generic_to_shared(&bar[s]);
+        unsigned ok = 0;
+        while (!ok)
+            asm volatile("{\n\t.reg .pred q;\n\tmbarrier.try_wait.parity.shared::cta.b64 q, [%1], %2;\n\t"
+                         "selp.u32 %0, 1, 0, q;\n\t}" : "=r"(ok) : "r"(b), "r"(ph[s]) : "memory");
+        ph[s] ^= 1;
+        ++done;
+        const int64_t nxt = first + (int64_t)(done + RB_RING - 1) * step;
+        if (nxt < nchunks) issue(nxt, s);
+    }
+}
 }  // namespace
+
+// Read-only HBM bandwidth through TMA bulk copies (GB/s, best of reps).
+extern "C" double kmsynth_read_peak_bulk(const void* buf, int64_t bytes, int reps, void* stream) {
+    cudaStream_t st = (cudaStream_t)stream;
+    int dev = 0, nsm = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+    const int64_t nchunks = bytes / RB_CHUNK;
+    if (nchunks < 1) return -1.0;
+    const int smem = RB_CHUNK * RB_RING;
+    if (cudaFuncSetAttribute(k_read_bulk, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) != cudaSuccess) return -1.0;
+    cudaEvent_t a, b;
+    cudaEventCreate(&a); cudaEventCreate(&b);
+    double best = 0.0;
+    for (int per_sm : {3, 4}) {
+        k_read_bulk<<<nsm * per_sm, 32, smem, st>>>((const unsigned char*)buf, nchunks);     // warm-up
+        if (cudaGetLastError() != cudaSuccess) continue;
+        for (int r = 0; r < reps; ++r) {
+            cudaEventRecord(a, st);
+            k_read_bulk<<<nsm * per_sm, 32, smem, st>>>((const unsigned char*)buf, nchunks);
+            cudaEventRecord(b, st);
+            cudaEventSynchronize(b);
+            float ms = 0.f;
+            cudaEventElapsedTime(&ms, a, b);
+            if (!(ms > 0.f)) continue;
+            const double gbs = (double)nchunks * RB_CHUNK / (ms * 1e-3) / 1e9;
+            if (gbs > best) best = gbs;
+        }
+    }
+    cudaEventDestroy(a); cudaEventDestroy(b);
+    return best;
+}
 
 // Best of `reps` timed write-only passes over buf (its contents are
 // overwritten); returns GB/s (written bytes / time).
