@@ -1967,6 +1967,227 @@ k_swap_stream_seg2(const T* __restrict__ D, int64_t ld, int w, int wpad, int n, 
     }
 }
 
+// ---------------------------------------------------------------------------
+// a3, wide-tile variant (KM_STREAM=seg3; measurement): as k_swap_stream_seg2
+// with 8 candidate columns per lane, i.e. 7 KB bulk copies per row and
+// column tile (2 CTAs per SM, 4-stage ring).
+// ---------------------------------------------------------------------------
+template <typename T, int NC, int RB, int S>
+struct Seg8Cfg {
+    static constexpr int COLS = NC * 256;
+    static constexpr int ROWB = COLS * (int)sizeof(T);
+    static constexpr int DATAB = S * RB * ROWB;
+    static constexpr int RIB = S * RB * 16;
+    static constexpr int RDB = S * RB * 16;
+    static constexpr int NBB = S * 4;
+    static constexpr int BARB = 2 * S * 8;
+    static constexpr int SMEM = DATAB + RIB + RDB + 16 * ((NBB + 15) / 16) + BARB;
+    static constexpr int THREADS = (NC + 1) * 32;
+};
+
+template <typename T, typename A, int NC, int RB, int S, int MINB>
+__global__ void __launch_bounds__((NC + 1) * 32, MINB)
+k_swap_stream_seg3(const T* __restrict__ D, int64_t ld, int w, int wpad, int n, int P,
+                   const RowInfo<T>* __restrict__ ri, const A* __restrict__ R,
+                   A* __restrict__ out_plus, A* __restrict__ out_head, A* __restrict__ out_tail,
+                   A* __restrict__ out_imin, int* __restrict__ out_islot, A* __restrict__ out_acc,
+                   const double2* __restrict__ rowd) {
+    using C = Seg8Cfg<T, NC, RB, S>;
+    using V = typename Vec4<T>::type;
+    static_assert(RB == 4, "four rows per stage");
+    constexpr int L = 8;                              // columns per lane
+    extern __shared__ __align__(128) unsigned char smem[];
+    T* sdata = reinterpret_cast<T*>(smem);
+    RowInfo<T>* sri = reinterpret_cast<RowInfo<T>*>(smem + C::DATAB);
+    double2* srd = reinterpret_cast<double2*>(smem + C::DATAB + C::RIB);
+    int* snb = reinterpret_cast<int*>(smem + C::DATAB + C::RIB + C::RDB);
+    uint64_t* full = reinterpret_cast<uint64_t*>(smem + C::DATAB + C::RIB + C::RDB + 16 * ((C::NBB + 15) / 16));
+    uint64_t* empty = full + S;
+
+    const int q = blockIdx.y;
+    const int64_t p0 = part_lo(q, n, P), p1 = part_lo(q + 1, n, P);
+    const int ctacol = blockIdx.x * C::COLS;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+
+    if (threadIdx.x == 0) {
+        for (int st = 0; st < S; ++st) {
+            ptx::mbar_init(&full[st], 1);
+            ptx::mbar_init(&empty[st], NC);
+        }
+        ptx::fence_mbar_init();
+    }
+    if (warp < NC) {
+        const T b = dmax<T>();
+        for (int h = 0; h < 2; ++h)
+            if (ctacol + warp * 256 + lane * L + h * 4 >= wpad) {
+                V big;
+                memcpy(&big.x, &b, sizeof(T)); memcpy(&big.y, &b, sizeof(T));
+                memcpy(&big.z, &b, sizeof(T)); memcpy(&big.w, &b, sizeof(T));
+                for (int r = 0; r < S * RB; ++r)
+                    *reinterpret_cast<V*>(sdata + (size_t)r * C::COLS + warp * 256 + lane * L + h * 4) = big;
+            }
+    }
+    __syncthreads();
+
+    if (warp == NC) {
+        const uint32_t cbytes = (uint32_t)min(C::COLS, wpad - ctacol) * (uint32_t)sizeof(T);
+        const uint64_t pol = ptx::policy_evict_first();
+        const uint64_t keep = ptx::policy_evict_last();
+        int64_t pr = p0;
+        int s = 0, ph = 0, st = 0;
+        int o_l = 0, sl_l = -1;
+        if (lane < RB && pr + lane < p1) { const RowInfo<T> r = ri[pr + lane]; o_l = r.o; sl_l = r.slot; }
+        while (true) {
+            if (st >= S) ptx::mbar_wait(&empty[s], ph ^ 1);
+            if (pr >= p1) {
+                if (lane == 0) { snb[s] = 0; ptx::mbar_arrive(&full[s]); }
+                break;
+            }
+            const int slot0 = __shfl_sync(FULL, sl_l, 0);
+            const unsigned same = __ballot_sync(FULL, lane < RB && sl_l == slot0 && pr + lane < p1);
+            const int nb = __ffs(~same) - 1;
+            if (lane == 0) {
+                snb[s] = nb;
+                ptx::mbar_expect_tx(&full[s], (uint32_t)nb * (cbytes + (rowd ? 32u : 16u)));
+            }
+            __syncwarp();
+            if (lane < nb)
+                ptx::bulk_g2s(sdata + (size_t)(s * RB + lane) * C::COLS, D + (int64_t)o_l * ld + ctacol, cbytes,
+                              &full[s], pol);
+            if (lane == 0) ptx::bulk_g2s(sri + s * RB, ri + pr, (uint32_t)nb * 16u, &full[s], keep);
+            if (lane == 1 && rowd) ptx::bulk_g2s(srd + s * RB, rowd + pr, (uint32_t)nb * 16u, &full[s], keep);
+            pr += nb;
+            const int o_sh = __shfl_down_sync(FULL, o_l, nb);
+            const int s_sh = __shfl_down_sync(FULL, sl_l, nb);
+            if (lane < RB) {
+                if (lane + nb < RB) { o_l = o_sh; sl_l = s_sh; }
+                else if (pr + lane < p1) { const RowInfo<T> r = ri[pr + lane]; o_l = r.o; sl_l = r.slot; }
+                else { sl_l = -1; }
+            }
+            ++st;
+            if (++s == S) { s = 0; ph ^= 1; }
+        }
+        return;
+    }
+
+    const int cb = ctacol + warp * 256 + lane * L;
+    const bool active = cb < w;
+    const int64_t obase = (int64_t)q * w + cb;
+    const int jmax = active ? min(L, w - cb) : 0;
+    const uint64_t keep = ptx::policy_evict_last();
+    A plus[L], seg[L];
+#pragma unroll
+    for (int j = 0; j < L; ++j) { plus[j] = 0; seg[j] = 0; }
+#pragma unroll
+    for (int j = 0; j < L; ++j)
+        if (j < jmax) {
+            ptx::st_hint(&out_imin[obase + j], amax<A>(), keep);
+            ptx::st_hint(&out_islot[obase + j], -1, keep);
+            ptx::st_hint(&out_head[obase + j], (A)0, keep);
+        }
+    int cur = ri[p0].slot;
+    bool first = true;
+    const T* srow0 = sdata + (warp * 256 + lane * L);
+    int s = 0, ph = 0;
+
+    for (;;) {
+        ptx::mbar_wait(&full[s], ph);
+        const int nb = snb[s];
+        if (nb == 0) break;
+        const RowInfo<T>* srii = sri + s * RB;
+        const int slot = srii[0].slot;
+        if (slot != cur) {
+            if (first) {
+#pragma unroll
+                for (int j = 0; j < L; ++j) if (j < jmax) ptx::st_hint(&out_head[obase + j], seg[j], keep);
+                first = false;
+            } else {
+                const A rv = R[cur];
+#pragma unroll
+                for (int j = 0; j < L; ++j) {
+                    if (j >= jmax) continue;
+                    if (out_acc) out_acc[(int64_t)cur * w + cb + j] = seg[j];
+                    const A val = rv + seg[j];
+                    if (val < out_imin[obase + j]) {
+                        ptx::st_hint(&out_imin[obase + j], val, keep);
+                        ptx::st_hint(&out_islot[obase + j], cur, keep);
+                    }
+                }
+            }
+#pragma unroll
+            for (int j = 0; j < L; ++j) seg[j] = 0;
+            cur = slot;
+        }
+        T x[RB][L], dn[RB], ds[RB];
+        const T* srow = srow0 + (size_t)(s * RB) * C::COLS;
+#pragma unroll
+        for (int u = 0; u < RB; ++u) {
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+                const V v = *reinterpret_cast<const V*>(srow + (size_t)u * C::COLS + h * 4);
+                memcpy(&x[u][h * 4 + 0], &v.x, sizeof(T)); memcpy(&x[u][h * 4 + 1], &v.y, sizeof(T));
+                memcpy(&x[u][h * 4 + 2], &v.z, sizeof(T)); memcpy(&x[u][h * 4 + 3], &v.w, sizeof(T));
+            }
+            dn[u] = srii[u].dn;
+            ds[u] = srii[u].ds;
+        }
+        if (nb < RB) {
+#pragma unroll
+            for (int u = 1; u < RB; ++u)
+                if (u >= nb) { dn[u] = never_lt<T>(); ds[u] = never_lt<T>(); }
+        }
+        bool hit[L];
+        bool anyh = false;
+#pragma unroll
+        for (int j = 0; j < L; ++j) {
+            hit[j] = __any_sync(FULL, CmpLt<T>::any4(x[0][j], ds[0], x[1][j], ds[1], x[2][j], ds[2], x[3][j], ds[3]));
+            anyh |= hit[j];
+        }
+        const int cs = s;
+        if (++s == S) { s = 0; ph ^= 1; }
+        if (!anyh) {
+            __syncwarp();
+            if (lane == 0) ptx::mbar_arrive(&empty[cs]);
+            continue;
+        }
+        A dnA[RB], dsA[RB];
+        if constexpr (Acc<T>::is_float) {
+            const double2* sr = srd + cs * RB;
+#pragma unroll
+            for (int u = 0; u < RB; ++u) { const double2 qq = sr[u]; dnA[u] = qq.x; dsA[u] = qq.y; }
+        } else {
+#pragma unroll
+            for (int u = 0; u < RB; ++u) { dnA[u] = (A)dn[u]; dsA[u] = (A)ds[u]; }
+        }
+        __syncwarp();
+        if (lane == 0) ptx::mbar_arrive(&empty[cs]);
+#pragma unroll
+        for (int j = 0; j < L; ++j) {
+            if (hit[j]) {
+                A tq[RB], tt[RB];
+#pragma unroll
+                for (int u = 0; u < RB; ++u) {
+                    const A xa = (A)x[u][j];
+                    tq[u] = (x[u][j] < ds[u]) ? xa - dsA[u] : (A)0;
+                    tt[u] = (x[u][j] < dn[u]) ? xa - dnA[u] : (A)0;
+                }
+                const A sq = (tq[0] + tq[1]) + (tq[2] + tq[3]);
+                const A sp = (tt[0] + tt[1]) + (tt[2] + tt[3]);
+                plus[j] += sp;
+                seg[j] += sq - sp;
+            }
+        }
+    }
+    if (!active) return;
+#pragma unroll
+    for (int j = 0; j < L; ++j) {
+        if (j >= jmax) continue;
+        if (first) { ptx::st_hint(&out_head[obase + j], seg[j], keep); ptx::st_hint(&out_tail[obase + j], (A)0, keep); }
+        else ptx::st_hint(&out_tail[obase + j], seg[j], keep);
+        ptx::st_hint(&out_plus[obase + j], plus[j], keep);
+    }
+}
+
 // a4: complete the segments cut by part boundaries, take the lexicographic
 // min over slots of (R_i + acc_i, i) (Alg.3, smaller slot on ties), add
 // dTD^{+x_c}, mask medoids, and reduce (dTD, i, c) over the grid.

@@ -106,6 +106,18 @@ int choose_parts(int64_t n, int64_t w, int cols_per_cta, int resident) {
 // short parts cost ring fill/drain and combine bytes.
 constexpr int PART_SKEW_DEFAULT = 15;  // 16ths; see km::part_lo (C4 stream 1.565 -> 1.478 ms)
 
+// wide-tile stream (KM_STREAM=seg3): 1792-column tiles, 2 CTAs per SM
+constexpr int SG8_NC = 7, SG8_RB = 4, SG8_S = 4, SG8_MINB = 2;
+int choose_parts_seg8(int64_t n, int64_t w) {
+    const int64_t ncb = cdiv(w, SG8_NC * 256);
+    const int64_t slots = (int64_t)NUM_SMS * SG8_MINB;
+    int64_t P = n / 1000;
+    P = std::max<int64_t>(P, cdiv(3 * slots, ncb));
+    P = std::min<int64_t>(P, std::max<int64_t>(1, 8 * slots / ncb));
+    P = std::min<int64_t>(P, std::max<int64_t>(1, n / 64));
+    return (int)std::max<int64_t>(P, 1);
+}
+
 int choose_parts_seg(int64_t n, int64_t w) {
     const int64_t ncb = cdiv(w, SG_NC * 128);
     const int64_t slots = (int64_t)NUM_SMS * SG_MINB;
@@ -274,6 +286,7 @@ struct Impl : ImplBase {
         if (ev && strcmp(ev, "seg6") == 0) stream_kind = 11;
         if (ev && strcmp(ev, "seg5") == 0) stream_kind = 12;
         if (ev && strcmp(ev, "seg2") == 0) stream_kind = 13;
+        if (ev && strcmp(ev, "seg3") == 0) stream_kind = 14;
         if (ev && strcmp(ev, "ldg") == 0) stream_kind = 0;
         if (ev && strcmp(ev, "wtma") == 0) stream_kind = 2;
 
@@ -288,6 +301,7 @@ struct Impl : ImplBase {
         const char* dnc = getenv("KM_DEBUG_NOCOMPUTE");        // perf experiment only: wrong results
         debug_nocompute = (dnc && dnc[0] == '1') ? 1 : 0;
         P = (stream_kind == 10 || stream_kind == 13) ? choose_parts_seg(n, w)
+            : stream_kind == 14 ? choose_parts_seg8(n, w)
             : stream_kind == 11 ? choose_parts(n, w, 6 * 128, 3)
             : stream_kind == 12 ? choose_parts(n, w, 5 * 128, 4)
             : stream_kind == 9 ? choose_parts(n, w, TQ_NC * 128, 2)
@@ -515,6 +529,16 @@ struct Impl : ImplBase {
         } else if (stream_kind == 13) {
             KM_TRY((launch_seg2<SG_NC, SG_RB, SG_S, SG_MINB>(D, w, wpad, P, o_plus, o_head, o_tail, o_imin, o_islot,
                                                               nullptr)));
+        } else if (stream_kind == 14) {
+            using C = km::Seg8Cfg<T, SG8_NC, SG8_RB, SG8_S>;
+            auto kern = km::k_swap_stream_seg3<T, A, SG8_NC, SG8_RB, SG8_S, SG8_MINB>;
+            if (!seg3_attr_set) {
+                KM_CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM));
+                seg3_attr_set = true;
+            }
+            dim3 g((unsigned)cdiv(w, C::COLS), P);
+            kern<<<g, C::THREADS, C::SMEM, st>>>(D, ld, w, wpad, (int)n, P, ri, R, o_plus, o_head, o_tail, o_imin,
+                                                  o_islot, nullptr, rowd);
         } else if (stream_kind == 11) {
             KM_TRY((launch_seg<6, 4, 6, 3>(nullptr)));
         } else if (stream_kind == 12) {
@@ -615,6 +639,7 @@ struct Impl : ImplBase {
     }
 
     bool seg2_attr_set = false;
+    bool seg3_attr_set = false;
     template <int NC, int RB, int S, int MINB = 2>
     km_status launch_seg2(const T* Dw, int ww, int wpadw, int Pw, A* plus_o, A* head_o, A* tail_o, A* imin_o,
                           int* islot_o, A* acc_out) {
@@ -786,7 +811,7 @@ struct Impl : ImplBase {
         if (use_post < 0) {
             const char* e = getenv("KM_POST");
             use_post = (e && e[0] == '0') ? 0 : 1;
-            if (use_post == 1 && (stream_kind != 10 && stream_kind != 13)) use_post = 0;
+            if (use_post == 1 && (stream_kind != 10 && stream_kind != 13 && stream_kind != 14)) use_post = 0;
             if (use_post == 1) KM_TRY(post_alloc());
         }
         if (use_post == 1 && !fp1_prepped) {
