@@ -388,10 +388,11 @@ def run_ours(args):
         km.close()
         del km
         torch.cuda.synchronize()
-        # the whole job three times (device allocation and page mapping make a
-        # single job's time vary); the median job is reported
+        torch.cuda.empty_cache()                 # the job allocates its own device memory
+        # the whole job five times (occasionally one job stalls 0.3-0.6 s in
+        # allocation / transfer); the median job is reported
         jobs = []
-        for _ in range(3):
+        for _ in range(5):
             t1 = time.perf_counter()
             r = kmedoids_run_host(Dh, k, use_build=(cfg.init == "build"), medoids=init_M, variant=args.variant)
             jobs.append(time.perf_counter() - t1)
