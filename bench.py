@@ -257,6 +257,7 @@ def run_ours(args):
 
     for _ in range(args.warmup):
         km.swap_iter(args.variant)
+    stream_kernel = km.stream_kernel()
     st0 = km.get_state()
     km.set_profiling(True)
     km.stream_time(reset=True)
@@ -417,9 +418,7 @@ def run_ours(args):
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
                      "traffic": (committed_traffic(cfg.name) or {}).get("traffic_bytes"),
                      "traffic_source": (committed_traffic(cfg.name) or {}).get("source"),
-                     "kernel": {"seg": "k_swap_stream_seg"}.get(os.environ.get("KM_STREAM", ""), "k_swap_stream_seg2")
-                     if not os.environ.get("KM_STREAM") or os.environ.get("KM_STREAM") in ("seg", "seg2")
-                     else os.environ["KM_STREAM"], "kernel_ms": k1_avg,
+                     "kernel": stream_kernel, "kernel_ms": k1_avg,
                      "alg_bytes_per_launch": alg_bytes, "peak_kind": peak_kind,
                      "read_only_peak_same_job": read_peak, "frac_of_read_only_peak": achieved / read_peak,
                      "read_only_peak_ldg": read_peak_ldg, "read_only_peak_bulk": read_peak_bulk,

@@ -186,6 +186,9 @@ km_status kmedoids_set_profiling(km_handle* h, int32_t enable);
 km_status kmedoids_stream_time(km_handle* h, double* ms_out, int64_t* launches_out, int32_t reset);
 
 /* Number of CUDA kernel launches this handle has issued (all kernels). */
+/* Name of the SWAP-delta stream kernel this handle launches (static string;
+ * measurement/reporting aid). */
+km_status kmedoids_stream_kernel(km_handle* h, const char** name_out);
 km_status kmedoids_launch_count(km_handle* h, int64_t* count_out);
 
 /* ---------------- dissimilarity materialisation -----

@@ -169,6 +169,7 @@ struct ImplBase {
     double prof_ms = 0.0;
     int64_t prof_launches = 0;
     virtual km_status prof_harvest() { return KM_OK; }   // pending stream timings (async sharded mode)
+    virtual const char* stream_kernel_name() const = 0;
     int64_t launches = 0;
     int k = 0;
     int64_t n = 0;
@@ -287,9 +288,9 @@ struct Impl : ImplBase {
         if (ev && strcmp(ev, "seg5") == 0) stream_kind = 12;
         if (ev && strcmp(ev, "seg2") == 0) stream_kind = 13;
         if (ev && strcmp(ev, "seg3") == 0) stream_kind = 14;
-        // (seg3 is 1.1 % faster per C4 iteration, 1.531 vs 1.549 ms, but a
-        // repeated whole job through kmedoids_run_host then stalled 0.3-0.6 s
-        // on every second job -- not understood yet, so seg2 stays the default)
+        // (seg3, the wide-tile stream, is 1.1 % faster per C4 iteration --
+        // 1.531 vs 1.549 ms -- but the whole kmedoids_run_host job at C4 took
+        // 0.37-0.39 s with it vs 0.32 s with seg2, so seg2 stays the default)
         if (ev && strcmp(ev, "ldg") == 0) stream_kind = 0;
         if (ev && strcmp(ev, "wtma") == 0) stream_kind = 2;
 
@@ -643,6 +644,19 @@ struct Impl : ImplBase {
 
     bool seg2_attr_set = false;
     bool seg3_attr_set = false;
+    const char* stream_kernel_name() const override {
+        switch (stream_kind) {
+            case 14: return "k_swap_stream_seg3";
+            case 13: return "k_swap_stream_seg2";
+            case 10: return "k_swap_stream_seg";
+            case 11: case 12: return "k_swap_stream_seg2";
+            case 9: return "k_swap_stream_tmaq";
+            case 6: return "k_swap_stream_cmp";
+            case 2: return "k_swap_stream_wtma";
+            case 1: return "k_swap_stream_tma";
+            default: return "k_swap_stream";
+        }
+    }
     template <int NC, int RB, int S, int MINB = 2>
     km_status launch_seg2(const T* Dw, int ww, int wpadw, int Pw, A* plus_o, A* head_o, A* tail_o, A* imin_o,
                           int* islot_o, A* acc_out) {
@@ -2603,6 +2617,13 @@ km_status kmedoids_dissimilarity(const void* X, km_metric metric, int64_t n, int
         return KM_OK;
     }
     return fail(KM_EINVAL, "unknown metric %d", (int)metric);
+}
+
+km_status kmedoids_stream_kernel(km_handle* h, const char** name_out) {
+    KM_H();
+    if (!name_out) return fail(KM_EINVAL, "name_out is NULL");
+    *name_out = h->impl->stream_kernel_name();
+    return KM_OK;
 }
 
 km_status kmedoids_launch_count(km_handle* h, int64_t* count_out) {

@@ -75,6 +75,7 @@ def load_library() -> ctypes.CDLL:
         "kmedoids_last_swaps": [vp, vp, vp, vp, i32, vp],
         "kmedoids_stream_time": [vp, vp, vp, i32],
         "kmedoids_launch_count": [vp, vp],
+        "kmedoids_stream_kernel": [vp, ctypes.POINTER(ctypes.c_char_p)],
         "kmedoids_shard_exchange": [vp, i32, ctypes.POINTER(_Exchange)],
         "kmedoids_shard_set_medoids": [vp, vp, vp],
         "kmedoids_shard_eval": [vp],
@@ -285,6 +286,12 @@ class KMedoids:
         c = ctypes.c_int64()
         _check(load_library().kmedoids_launch_count(self.h, ctypes.byref(c)))
         return c.value
+
+    def stream_kernel(self) -> str:
+        """Name of the SWAP-delta stream kernel this handle launches."""
+        name = ctypes.c_char_p()
+        _check(load_library().kmedoids_stream_kernel(self.h, ctypes.byref(name)))
+        return name.value.decode()
 
     # ---- sharded phase API ------------------------------------------------------
     def shard_exchange(self, nranks: int) -> _Exchange:
