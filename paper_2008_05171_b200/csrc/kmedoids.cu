@@ -2395,24 +2395,41 @@ km_status kmedoids_run_host(const void* D_host, km_dtype dtype, int64_t n, int64
     if (!use_build && !initial_medoids) return fail(KM_EINVAL, "initial_medoids required without BUILD");
     if (n < 3 || ld < n) return fail(KM_EINVAL, "bad n/ld");
     const size_t bytes = (size_t)n * (size_t)ld * 4;
+    const char* ep = getenv("KM_E2E_PROF");              // measurement aid: phase times to stderr
+    const bool prof = ep && ep[0] == '1';
+    auto now = [] { return std::chrono::steady_clock::now(); };
+    auto ms = [](std::chrono::steady_clock::time_point a, std::chrono::steady_clock::time_point b) {
+        return std::chrono::duration<double, std::milli>(b - a).count();
+    };
+    const auto t0 = now();
     void* Dd = nullptr;
     cudaError_t e = cudaMalloc(&Dd, bytes);
     if (e != cudaSuccess) return fail(KM_ENOMEM, "cudaMalloc(%zu) for D failed: %s", bytes, cudaGetErrorString(e));
+    const auto t1 = now();
     cudaStream_t st = (cudaStream_t)cuda_stream;
     km_status s = KM_OK;
     km_handle* h = nullptr;
     e = cudaMemcpyAsync(Dd, D_host, bytes, cudaMemcpyHostToDevice, st);
     if (e != cudaSuccess) s = fail(KM_ECUDA, "H2D copy of D failed: %s", cudaGetErrorString(e));
+    if (prof) cudaStreamSynchronize(st);
+    const auto t2 = now();
     if (s == KM_OK) s = kmedoids_create(&h, Dd, dtype, n, ld, 0, n, k, cuda_stream);
     if (s == KM_OK && !use_build) s = kmedoids_set_medoids(h, initial_medoids);
+    const auto t3 = now();
     if (s == KM_OK) {
         km_status r = kmedoids_run(h, use_build, variant, max_iter, medoids_out, assignment_out, td_out, n_iter_out,
                                    n_swaps_out);
         s = r;
     }
+    const auto t4 = now();
     kmedoids_destroy(h);
     cudaStreamSynchronize(st);
+    const auto t5 = now();
     cudaFree(Dd);
+    const auto t6 = now();
+    if (prof)
+        fprintf(stderr, "[kmedoids_run_host] ms: malloc %.1f h2d %.1f create %.1f run %.1f destroy %.1f free %.1f\n",
+                ms(t0, t1), ms(t1, t2), ms(t2, t3), ms(t3, t4), ms(t4, t5), ms(t5, t6));
     return s;
 }
 
