@@ -2533,23 +2533,41 @@ __global__ void k_fp2_slot_reduce(int k, int split, const Rec<A>* __restrict__ p
 template <typename A>
 __global__ void k_fp2_plan(const Rec<A>* __restrict__ best, int k, const A* __restrict__ td,
                            Decision<A>* __restrict__ dec, int* __restrict__ order, int* __restrict__ m_out,
-                           int* __restrict__ swaps_prev) {
+                           int* __restrict__ swaps_prev, bool staged_ok) {
     __shared__ int s_m;
+    extern __shared__ __align__(16) unsigned char plan_smem[];   // k values and flags (when they fit)
     if (threadIdx.x == 0) s_m = 0;
-    __syncthreads();
     const A tdv = *td;
     auto improving = [&](const Rec<A>& b) {
         if (b.slot == INT_MAX) return false;
         if (std::is_same<A, double>::value) return (double)b.v < -1e-12 * fabs((double)tdv);
         return b.v < 0;
     };
+    // stage (v_i, improving_i) in shared memory: the O(k^2) ranking reads them k times
+    A* sv = reinterpret_cast<A*>(plan_smem);
+    unsigned char* simp = plan_smem + (size_t)k * sizeof(A);
+    const bool staged = staged_ok;
+    if (staged)
+        for (int i = threadIdx.x; i < k; i += blockDim.x) {
+            const Rec<A> b = best[i];
+            sv[i] = b.v;
+            simp[i] = improving(b) ? 1 : 0;
+        }
+    __syncthreads();
     for (int i = threadIdx.x; i < k; i += blockDim.x) {
         const Rec<A> bi = best[i];
         if (!improving(bi)) continue;
         int rank = 0;
-        for (int j = 0; j < k; ++j) {
-            const Rec<A> bj = best[j];
-            if (j != i && improving(bj) && (bj.v < bi.v || (bj.v == bi.v && j < i))) ++rank;
+        if (staged) {
+            for (int j = 0; j < k; ++j) {
+                const A vj = sv[j];
+                if (j != i && simp[j] && (vj < bi.v || (vj == bi.v && j < i))) ++rank;
+            }
+        } else {
+            for (int j = 0; j < k; ++j) {
+                const Rec<A> bj = best[j];
+                if (j != i && improving(bj) && (bj.v < bi.v || (bj.v == bi.v && j < i))) ++rank;
+            }
         }
         order[rank] = i;
         atomicAdd(&s_m, 1);

@@ -1063,7 +1063,10 @@ struct Impl : ImplBase {
             const std::vector<int> order = fp2_order_slots(tdh);
             return fp2_sequential(order, nullptr, nullptr, swaps_out, td_out);
         }
-        km::k_fp2_plan<A><<<1, 1024, 0, st>>>(fp2_best, k, td, dec, fp2_order, fp2_m, fp2_swaps_prev);
+        const size_t psm = (size_t)k * (sizeof(A) + 1);
+        const bool pstaged = psm <= 40 * 1024;
+        km::k_fp2_plan<A><<<1, 1024, pstaged ? psm : 0, st>>>(fp2_best, k, td, dec, fp2_order, fp2_m, fp2_swaps_prev,
+                                                              pstaged);
         KM_CKL();
         KM_TRY(launch_fp2_sequential(nullptr, nullptr));
         km::k_fp2_finish<A><<<1, 1, 0, st>>>(dec, fp2_swaps_prev);
