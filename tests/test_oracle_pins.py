@@ -334,6 +334,173 @@ def test_fastpam2_reading_properties():
         assert r2.converged and r2.n_iter >= 1
 
 
+def bf_fastpam2(D, M0, max_iter=2000, eps_rel=None):
+    """FastPAM2 as DESIGN.md reading R6 states it,
+    written from the definitions only -- every dTD is a full recomputation of
+    TD (Eq. eqn:td), no cache, no removal loss, no FastPAM1 vector:
+
+    1-3. per slot i, (v_i, c_i) = lexicographic min over non-medoid c of
+         (TD(M with m_i <- c) - TD(M), c);
+    4.   stop if no v_i improves;
+    5.   slots in ascending (v_i, i);
+    6.   the first is applied with v_i;
+    7.   every later slot whose v_i improved at the start of the iteration is
+         skipped if c_i is a medoid by now, else re-evaluated on the current
+         medoids and applied iff that value improves.
+    Returns (medoids, td, n_iter, trace[(i, c, dTD)], converged)."""
+    Dw = D.astype(np.int64) if D.dtype == np.uint32 else D.astype(np.float64)
+    n = D.shape[0]
+    M = list(M0)
+    k = len(M)
+
+    def td_of(MM):
+        return Dw[:, MM].min(axis=1).sum()
+
+    def improving(v, t):
+        return v < 0 if eps_rel is None else v < -eps_rel * abs(t)
+
+    def delta(MM, i, c):
+        M2 = list(MM)
+        M2[i] = c
+        return td_of(M2) - td_of(MM)
+
+    td = td_of(M)
+    trace, iters, converged = [], 0, False
+    while iters < max_iter:
+        iters += 1
+        best = []
+        for i in range(k):
+            vals = [(delta(M, i, c), c) for c in range(n) if c not in M]
+            best.append(min(vals))
+        if not any(improving(v, td) for v, _ in best):
+            converged = True
+            break
+        td0 = td
+        order = sorted(range(k), key=lambda i: (best[i][0], i))
+        for r, i in enumerate(order):
+            v, c = best[i]
+            if not improving(v, td0):
+                continue
+            if r > 0:
+                if c in M:
+                    continue
+                v = delta(M, i, c)
+                if not improving(v, td):
+                    continue
+            trace.append((i, c, v))
+            M[i] = c
+            td = td_of(M)
+    return M, td, iters, trace, converged
+
+
+@pytest.mark.parametrize("symmetric", [True, False])
+def test_fastpam2_equals_bruteforce_reading_r6(symmetric):
+    """The oracle's FastPAM2 procedure (swap ORDER, skips and re-evaluations,
+    not only its end state) equals bf_fastpam2, a from-definition restatement
+    of reading R6, on integer instances with many exact ties (values 0..3)
+    and without them."""
+    rng = np.random.default_rng(620 + symmetric)
+    multi = 0
+    for trial in range(80):
+        n = int(rng.integers(8, 30))
+        k = int(rng.integers(2, min(8, n - 2) + 1))
+        D = rand_int_matrix(rng, n, hi=int(rng.choice([4, 4, 30, 1000])), symmetric=symmetric)
+        M0 = rng.choice(n, size=k, replace=False).tolist()
+        r = oracle.swap_run(D, M0, oracle.FASTPAM2)
+        M, td, iters, trace, conv = bf_fastpam2(D, M0)
+        assert [tuple(t) for t in r.trace] == trace
+        assert r.medoids.tolist() == M and r.td == td
+        assert r.n_iter == iters and r.converged == conv
+        assert r.assignment.tolist() == oracle.assign(D, M).nearest.tolist()
+        if r.n_swaps > r.n_iter - 1 + (not r.converged):
+            multi += 1             # some iteration applied more than one swap
+    assert multi > 20
+
+
+def test_fastpam2_float_equals_bruteforce_reading_r6():
+    rng = np.random.default_rng(626)
+    for _ in range(30):
+        n = int(rng.integers(10, 28))
+        k = int(rng.integers(2, 6))
+        X = rng.normal(size=(n, 3))
+        D = np.sqrt(((X[:, None, :] - X[None, :, :]) ** 2).sum(-1)).astype(np.float32)
+        M0 = rng.choice(n, size=k, replace=False).tolist()
+        r = oracle.swap_run(D, M0, oracle.FASTPAM2)
+        M, td, iters, trace, conv = bf_fastpam2(D, M0, eps_rel=oracle.EPS_REL)
+        assert [t[:2] for t in r.trace] == [t[:2] for t in trace]
+        assert np.allclose([t[2] for t in r.trace], [t[2] for t in trace], rtol=0, atol=1e-9)
+        assert r.medoids.tolist() == M and r.td == pytest.approx(td, rel=1e-12)
+        assert r.n_iter == iters and r.converged == conv
+
+
+def test_bf_fastpam2_detects_injected_deviations():
+    """bf_fastpam2 is sensitive to the two alternatives R6 rules out (slot
+    order instead of dTD order; no re-evaluation): on the same instances both
+    alternatives produce a different trace somewhere."""
+    rng = np.random.default_rng(627)
+
+    def variant(D, M0, by_slot=False, reeval=True):
+        Dw = D.astype(np.int64)
+        M = list(M0)
+        n, k = D.shape[0], len(M)
+        td_of = lambda MM: Dw[:, MM].min(axis=1).sum()
+        trace = []
+        for _ in range(100):
+            best = []
+            for i in range(k):
+                best.append(min((td_of(M[:i] + [c] + M[i + 1:]) - td_of(M), c) for c in range(n) if c not in M))
+            if not any(v < 0 for v, _ in best):
+                break
+            order = sorted(range(k), key=(lambda i: i) if by_slot else (lambda i: (best[i][0], i)))
+            for r, i in enumerate(order):
+                v, c = best[i]
+                if v >= 0 or c in M:
+                    continue
+                if reeval and r > 0:
+                    v = td_of(M[:i] + [c] + M[i + 1:]) - td_of(M)
+                    if v >= 0:
+                        continue
+                trace.append((i, c))
+                M[i] = c
+        return trace
+
+    diff_order = diff_reeval = 0
+    for _ in range(40):
+        n = int(rng.integers(12, 30))
+        k = int(rng.integers(3, 7))
+        D = rand_int_matrix(rng, n, hi=1000)
+        M0 = rng.choice(n, size=k, replace=False).tolist()
+        ref = [t[:2] for t in bf_fastpam2(D, M0)[3]]
+        diff_order += variant(D, M0, by_slot=True) != ref
+        diff_reeval += variant(D, M0, reeval=False) != ref
+    assert diff_order > 5 and diff_reeval > 5
+
+
+def test_candidate_col_and_assign_cols_equal_definitions():
+    """oracle.fastpam1_candidate_col (explicit column) and oracle.assign_cols
+    (explicit medoid columns) against brute force: vec[i] + plus is the exact
+    TD change of swapping slot i for the column's point, and the cache is the
+    sorted (d, slot) order."""
+    rng = np.random.default_rng(628)
+    for trial in range(60):
+        n = int(rng.integers(5, 20))
+        k = int(rng.integers(2, min(6, n - 1) + 1))
+        D = rand_int_matrix(rng, n, hi=int(rng.choice([4, 50])), symmetric=bool(trial % 2))
+        M = rng.choice(n, size=k, replace=False)
+        cols = np.ascontiguousarray(D[:, M].T)
+        c = oracle.assign_cols(cols)
+        for o in range(n):
+            order = sorted(range(k), key=lambda j: (int(D[o, M[j]]), j))
+            assert (c.nearest[o], c.second[o]) == (order[0], order[1])
+            assert (c.dn[o], c.ds[o]) == (D[o, M[order[0]]], D[o, M[order[1]]])
+        R = oracle.removal_loss(c, k)
+        for x in range(n):
+            if x in M:
+                continue
+            vec, plus = oracle.fastpam1_candidate_col(np.ascontiguousarray(D[:, x]), c, R)
+            assert [int(v + plus) for v in vec] == [bf_delta(D, M, i, x) for i in range(k)]
+
+
 # ---------- FasterPAM (Alg.4, P:988-1027; readings F1-F5) ----------
 
 def bf_eager(D, M0, max_iter=2000, eps_rel=None):
