@@ -23,7 +23,8 @@ seed + 1000 (k distinct indices, uniform without replacement).
 Distances: L1 on integer coordinates round(100 x) is exact integer
 arithmetic; Euclidean is f32(sqrt(sum_t (x_ot - x_ct)^2)) with each fp64
 operation rounded in t order, so the numpy and CUDA materialisations agree
-bit for bit (tests/test_synth.py).  Both are exactly symmetric with a zero
+bit for bit (tests/test_synth.py for the CPU pair, test_gpu_parity.py::
+test_synth_cuda_matches_numpy for CUDA).  Both are exactly symmetric with a zero
 diagonal.
 """
 from __future__ import annotations
@@ -163,6 +164,46 @@ def dist_numpy(X: np.ndarray, metric: int, c0: int = 0, c1: int | None = None, l
                 diff = Xa[:, t][:, None] - Y[:, t][None, :]
                 acc = acc + diff * diff
             out[a:a + step, :w] = np.sqrt(acc).astype(np.float32)
+    return out
+
+
+_CPU_SO = os.path.join(_HERE, "libkmsynth_cpu.so")
+_CPU_SRC = os.path.join(_HERE, "csrc", "synth_cpu.c")
+_cpu_lib = None
+
+
+def build_cpu_lib(force: bool = False) -> str:
+    """gcc -O2 -fopenmp, no fast-math, no FMA contraction (bit-identical to dist_numpy)."""
+    if force or not os.path.exists(_CPU_SO) or os.path.getmtime(_CPU_SO) < os.path.getmtime(_CPU_SRC):
+        tmp = _CPU_SO + f".tmp{os.getpid()}"
+        subprocess.check_call(["gcc", "-O2", "-std=c99", "-fopenmp", "-ffp-contract=off", "-shared", "-fPIC",
+                               "-o", tmp, _CPU_SRC, "-lm"])
+        os.replace(tmp, _CPU_SO)
+    return _CPU_SO
+
+
+def dist_cpu(X: np.ndarray, metric: int, c0: int = 0, c1: int | None = None, ld: int | None = None,
+             out: np.ndarray | None = None) -> np.ndarray:
+    """Multi-threaded CPU materialisation of columns [c0, c1) of D, bit-identical
+    to dist_numpy (an (n, ld) array; the slab is [:, :c1-c0])."""
+    global _cpu_lib
+    if _cpu_lib is None:
+        _cpu_lib = ctypes.CDLL(build_cpu_lib())
+    n, d = X.shape
+    c1 = n if c1 is None else c1
+    ld = round_ld(c1 - c0) if ld is None else ld
+    dt = np.uint32 if metric == L1_INT else np.float32
+    if out is None:
+        out = np.zeros((n, ld), dtype=dt)
+    assert out.shape == (n, ld) and out.dtype == dt and out.flags.c_contiguous
+    if metric == L1_INT:
+        Xc = np.ascontiguousarray(X, dtype=np.int32)
+        f = _cpu_lib.kmsynth_cpu_dist_l1
+    else:
+        Xc = np.ascontiguousarray(X, dtype=np.float64)
+        f = _cpu_lib.kmsynth_cpu_dist_l2
+    f(ctypes.c_void_p(Xc.ctypes.data), ctypes.c_int64(n), ctypes.c_int32(d), ctypes.c_int64(c0),
+      ctypes.c_int64(c1), ctypes.c_int64(ld), ctypes.c_void_p(out.ctypes.data))
     return out
 
 

@@ -216,6 +216,18 @@ def fastpam1_table(D, M, cache, R) -> np.ndarray:
     return table
 
 
+def fastpam2_slot_best(D, M, cache, R):
+    """Reading R6 steps 2-3: per slot i, (v_i, c_i) = lexicographic min over
+    non-medoid c of (dTD(m_i, x_c), c).  Returns (v[k], c[k])."""
+    f, acc = _fn(D, "oracle_fastpam2_slot_best")
+    M = _i32(M)
+    k = len(M)
+    sv = np.zeros(k, acc); sc = np.zeros(k, np.int32)
+    f(_ptr(D), ctypes.c_int64(_ld(D)), ctypes.c_int32(D.shape[0]), _ptr(M), ctypes.c_int32(k),
+      _ptr(cache.nearest), _ptr(cache.dn), _ptr(cache.ds), _ptr(np.ascontiguousarray(R, acc)), _ptr(sv), _ptr(sc))
+    return sv, sc
+
+
 @dataclass
 class RunResult:
     medoids: np.ndarray

@@ -213,6 +213,28 @@ int FN(oracle_fastpam1_best)(const D_T* D, int64_t ld, int32_t n, const int32_t*
     return bi >= 0;
 }
 
+/* FastPAM2, steps 2-3 of reading R6 (from P:861-862 and
+ * P:945-947): for every slot i the best candidate (sv[i], sc[i]) =
+ * lexicographic min over non-medoid c of (dTD(m_i, x_c), c), with dTD the
+ * FastPAM1 value of Alg.3 P:879-893 (candidates in ascending c, strict "<").
+ * sc[i] = -1 if there is no non-medoid. */
+void FN(oracle_fastpam2_slot_best)(const D_T* D, int64_t ld, int32_t n, const int32_t* M, int32_t k,
+                                   const int32_t* nearest, const ACC_T* dn, const ACC_T* ds,
+                                   const ACC_T* R, ACC_T* sv, int32_t* sc) {
+    ACC_T* vec = (ACC_T*)malloc(sizeof(ACC_T) * (size_t)k);
+    for (int32_t i = 0; i < k; ++i) { sv[i] = 0; sc[i] = -1; }
+    for (int32_t c = 0; c < n; ++c) {
+        if (FN(is_medoid)(M, k, c)) continue;
+        ACC_T plus;
+        FN(oracle_fastpam1_candidate)(D, ld, n, k, c, nearest, dn, ds, R, vec, &plus);
+        for (int32_t i = 0; i < k; ++i) {
+            ACC_T v = vec[i] + plus;
+            if (sc[i] < 0 || v < sv[i]) { sv[i] = v; sc[i] = c; }
+        }
+    }
+    free(vec);
+}
+
 /* One SWAP run (Alg.2 P:347-372 for variant 0 = PAM, Alg.3 P:871-905 for
  * variant 1 = FastPAM1, reading R6 for variant 2 = FastPAM2).
  * M (in/out, k slots) is updated in place (slot semantics P:366).  The
@@ -256,16 +278,7 @@ int FN(oracle_swap_run)(const D_T* D, int64_t ld, int32_t n, int32_t* M, int32_t
             /* Reading R6:
              * 2-3. per slot i the best candidate (v_i, c_i) = lexicographic
              *      min over non-medoid c of (dTD(m_i, x_c), c). */
-            for (int32_t i = 0; i < k; ++i) { sv[i] = 0; sc[i] = -1; }
-            for (int32_t c = 0; c < n; ++c) {
-                if (FN(is_medoid)(M, k, c)) continue;
-                ACC_T plus;
-                FN(oracle_fastpam1_candidate)(D, ld, n, k, c, nearest, dn, ds, R, vec, &plus);
-                for (int32_t i = 0; i < k; ++i) {
-                    ACC_T v = vec[i] + plus;
-                    if (sc[i] < 0 || v < sv[i]) { sv[i] = v; sc[i] = c; }
-                }
-            }
+            FN(oracle_fastpam2_slot_best)(D, ld, n, M, k, nearest, dn, ds, R, sv, sc);
             /* 4. stop when no slot improves (same rule as PAM). */
             int32_t any = 0;
             for (int32_t i = 0; i < k; ++i)

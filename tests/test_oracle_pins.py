@@ -701,3 +701,19 @@ def test_clara_full_sample_is_pam_and_best_sample_wins():
         Mj, _, _ = oracle.build_init(Dj, k)
         rj = oracle.swap_run(Dj, Mj, oracle.FASTPAM1)
         assert bf_td(D, S[rj.medoids]) >= t
+
+
+def test_fastpam2_slot_best_equals_bruteforce():
+    """Reading R6 steps 2-3 (oracle.fastpam2_slot_best, the per-slot plan the
+    full-size goldens record): (v_i, c_i) = lexicographic min over non-medoid
+    c of (TD(M with m_i <- c) - TD(M), c), recomputed from the definition."""
+    rng = np.random.default_rng(629)
+    for trial in range(60):
+        n = int(rng.integers(6, 22))
+        k = int(rng.integers(2, min(6, n - 1) + 1))
+        D = rand_int_matrix(rng, n, hi=int(rng.choice([4, 100])), symmetric=bool(trial % 2))
+        M = rng.choice(n, size=k, replace=False)
+        c = oracle.assign(D, M)
+        sv, sc = oracle.fastpam2_slot_best(D, M, c, oracle.removal_loss(c, k))
+        for i in range(k):
+            assert (sv[i], sc[i]) == min((bf_delta(D, M, i, x), x) for x in range(n) if x not in M)
