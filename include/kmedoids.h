@@ -179,6 +179,15 @@ km_status kmedoids_eval_candidates(km_handle* h, void* dtd_out, int32_t* slot_ou
 km_status kmedoids_last_swaps(km_handle* h, int32_t* slots_out, int32_t* cands_out, void* dtds_out, int32_t cap,
                               int32_t* count_out);
 
+/* Diagnostics of the last KM_FASTPAM2 iteration (reading R6, P:861-862,
+ * P:945-947): v_out[k] (int64_t or double) and c_out[k] = the per-slot best
+ * (v_i, c_i) = lexicographic min over non-medoid c of (dTD(m_i, x_c), c)
+ * (c_i = -1, v_i = 0 if the slot had no candidate); order_out (capacity k)
+ * receives the m_out improving slots in ascending (v_i, i), the order the
+ * sequential phase visits them.  Any output may be NULL.  Synchronises the
+ * handle's stream.  Errors: KM_EINVAL before the first FastPAM2 iteration. */
+km_status kmedoids_fp2_last_plan(km_handle* h, void* v_out, int32_t* c_out, int32_t* order_out, int32_t* m_out);
+
 /* Profiling: enable (1) / disable (0) CUDA-event timing of the SWAP-delta
  * stream kernel on the handle's stream; kmedoids_stream_time returns the
  * accumulated milliseconds and launch count since the last reset. */

@@ -2,7 +2,7 @@
 // (Alg.4; readings F1-F5 and "FasterPAM").
 //
 // The host streams a window of candidate columns once on the current state
-// (k_swap_stream_seg in FastPAM2 mode + k_swap_combine): acc[i][j] (the
+// (k_swap_stream_seg2 in FastPAM2 mode + k_swap_combine): acc[i][j] (the
 // complete per-slot sums of Eq. eqn:better-change3) and plus[j] (dTD^{+x_c})
 // for every window column j.  ONE cooperative kernel then runs Alg.4's scan
 // over the window:

@@ -2,10 +2,10 @@
 //
 // Kernel map:
 //   a1/a5  k_gather_medoid_cols, k_gather_decided_col, k_assign_full, k_assign_incremental
-//   a2     k_slot_hist, k_scan_within_slot, k_scan_slots, k_slot_scatter, k_removal_loss, k_part_meta
-//   a3     k_swap_stream   (the HBM stream; Alg.3, Eq. eqn:better-change3)
+//   a2     k_fp1_post phases 3-7 (km_post.cuh), k_part_meta
+//   a3     k_swap_stream_seg2 (the HBM stream; Alg.3, Eq. eqn:better-change3)
 //   a4     k_swap_combine  (per-candidate argmin over slots) + k_select
-//   a7     k_build_stream / k_build_combine / k_build_select / k_build_apply (Alg.1)
+//   a7     k_build_tma / k_build_combine / k_build_select (Alg.1; incremental: km_build_delta.cuh)
 //   a8     k_td_from_dn
 #pragma once
 #include "km_common.cuh"
@@ -23,18 +23,6 @@ constexpr int SORT_CHUNK_MIN = 256;   // objects per block of the stable countin
 template <typename T> struct Vec4;
 template <> struct Vec4<float> { using type = float4; };
 template <> struct Vec4<uint32_t> { using type = uint4; };
-
-// 128-bit streaming load: read-only path, no L1 allocation (D is read once
-// per iteration; keep L1 for the sorted row info).
-template <typename T>
-__device__ __forceinline__ typename Vec4<T>::type ld_stream4(const T* p) {
-    uint4 r;
-    asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
-                 : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w) : "l"(p));
-    typename Vec4<T>::type v;
-    memcpy(&v, &r, sizeof(r));
-    return v;
-}
 
 template <typename A>
 __device__ __forceinline__ Rec<A> shfl_rec(const Rec<A>& r, int src_xor) {
@@ -106,6 +94,33 @@ __device__ void grid_min_rec(Rec<A> r, Rec<A>* partials, unsigned* counter, Rec<
 // ---------------------------------------------------------------------------
 // a1/a5: medoid columns and the nearest/second cache
 // ---------------------------------------------------------------------------
+
+// Input validation (include/kmedoids.h conventions: d(x_o, x_o) = 0, d >= 0,
+// no NaN).  *bad counts the violations:
+//   k_validate_diag: the diagonal entries of the slab, D[o][o - col_begin]
+//     for o in [col_begin, col_end) (a NaN also fails "== 0");
+//   k_validate_cols: the k*n gathered medoid columns (float path: d < 0 or
+//     NaN; the uint32 path has no invalid values).
+template <typename T>
+__global__ void k_validate_diag(const T* __restrict__ D, int64_t ld, int64_t col_begin, int64_t col_end,
+                                int* __restrict__ bad) {
+    const int64_t o = col_begin + (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    int b = 0;
+    if (o < col_end) b = !(D[o * ld + (o - col_begin)] == (T)0);
+    b = __syncthreads_count(b);
+    if (threadIdx.x == 0 && b) atomicAdd(bad, b);
+}
+
+template <typename T>
+__global__ void k_validate_cols(const T* __restrict__ MC, int64_t cnt, int* __restrict__ bad) {
+    int b = 0;
+    if constexpr (std::is_same<T, float>::value) {
+        for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < cnt; i += (int64_t)gridDim.x * blockDim.x)
+            b |= !(MC[i] >= 0.f);
+    }
+    b = __syncthreads_or(b);
+    if (threadIdx.x == 0 && b) atomicAdd(bad, 1);
+}
 
 // MC[j][o] = d(x_o, m_j) for every slot j whose medoid lies in the local
 // column range (single GPU: all of them).  grid = (ceil(n/256), k).
@@ -348,131 +363,11 @@ __global__ void k_td_from_dn(const T* __restrict__ dn, int n, A* __restrict__ pa
 }
 
 // ---------------------------------------------------------------------------
-// a2: stable counting sort of the objects by nearest slot, removal loss
+// a2: the slot sort, removal losses and part metadata run as phases of the
+// cooperative k_fp1_post (km_post.cuh); k_part_meta is also used alone.
 // ---------------------------------------------------------------------------
-
-// counts[s*B + b] = #objects of chunk b with nearest slot s.
-__global__ void k_slot_hist(const int* __restrict__ near, int n, int k, int chunk, int* __restrict__ counts) {
-    extern __shared__ int h[];
-    const int B = gridDim.x, b = blockIdx.x;
-    for (int s = threadIdx.x; s < k; s += blockDim.x) h[s] = 0;
-    __syncthreads();
-    const int e0 = b * chunk, e1 = min(n, e0 + chunk);
-    for (int e = e0 + threadIdx.x; e < e1; e += blockDim.x) atomicAdd(&h[near[e]], 1);
-    __syncthreads();
-    for (int s = threadIdx.x; s < k; s += blockDim.x) counts[(int64_t)s * B + b] = h[s];
-}
-
-// Within-slot exclusive scan of the chunk counts, one warp per slot:
-// offsets[s*B + b] = #objects of slot s in chunks < b; tot[s] = slot total.
-__global__ void k_scan_within_slot(const int* __restrict__ counts, int B, int k, int* __restrict__ offsets,
-                                   int* __restrict__ tot) {
-    const int s = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
-    if (s >= k) return;
-    int run = 0;
-    for (int b0 = 0; b0 < B; b0 += 32) {
-        const int b = b0 + lane;
-        const int c = b < B ? counts[(int64_t)s * B + b] : 0;
-        int incl = c;
-#pragma unroll
-        for (int d = 1; d < 32; d <<= 1) {
-            const int y = __shfl_up_sync(FULL, incl, d);
-            if (lane >= d) incl += y;
-        }
-        if (b < B) offsets[(int64_t)s * B + b] = run + incl - c;
-        run += __shfl_sync(FULL, incl, 31);
-    }
-    if (lane == 0) tot[s] = run;
-}
-
-// Exclusive scan of the k slot totals (one block): seg_start[s] = first
-// sorted position of slot s, seg_start[k] = n.  Also resets *empty_slot for
-// k_removal_loss, which runs after this kernel.
-__global__ void k_scan_slots(const int* __restrict__ tot, int k, int* __restrict__ seg_start,
-                             int* __restrict__ empty_slot) {
-    __shared__ int sums[1024];
-    const int t = threadIdx.x, nt = blockDim.x;
-    if (t == 0) *empty_slot = INT_MAX;
-    const int per = (k + nt - 1) / nt;
-    const int a = t * per, z = min(k, a + per);
-    int s = 0;
-    for (int i = a; i < z; ++i) s += tot[i];
-    sums[t] = s;
-    __syncthreads();
-    for (int off = 1; off < nt; off <<= 1) {     // Hillis-Steele inclusive scan
-        const int v = (t >= off) ? sums[t - off] : 0;
-        __syncthreads();
-        sums[t] += v;
-        __syncthreads();
-    }
-    int run = sums[t] - s;
-    for (int i = a; i < z; ++i) {
-        seg_start[i] = run;
-        run += tot[i];
-    }
-    if (t == nt - 1) seg_start[k] = sums[nt - 1];
-}
-
-// Stable scatter: one warp per chunk walks its objects in index order and
-// places each at offsets[slot][chunk] + (rank among earlier same-slot
-// objects).  The sorted order is therefore (slot, o) ascending -- fixed for a
-// given cache, so every sum over it is deterministic.
-template <typename T>
-__global__ void k_slot_scatter(const int* __restrict__ near, const T* __restrict__ dn,
-                               const T* __restrict__ ds, int n, int k, int chunk, const int* __restrict__ offsets,
-                               const int* __restrict__ seg_start, RowInfo<T>* __restrict__ ri, int natural_order,
-                               double2* __restrict__ rowd) {
-    extern __shared__ int cnt[];
-    const int B = gridDim.x, b = blockIdx.x, lane = threadIdx.x;
-    for (int s = lane; s < k; s += 32) cnt[s] = seg_start[s] + offsets[(int64_t)s * B + b];
-    __syncwarp();
-    const int e0 = b * chunk, e1 = min(n, e0 + chunk);
-    const unsigned lt = (1u << lane) - 1u;
-    for (int base = e0; base < e1; base += 32) {
-        const int e = base + lane;
-        const bool valid = e < e1;
-        const int s = valid ? near[e] : -1 - lane;
-        const unsigned peers = __match_any_sync(FULL, s);
-        const int rank = __popc(peers & lt);
-        const int leader = __ffs(peers) - 1;
-        int bp = 0;
-        if (valid && lane == leader) bp = cnt[s];
-        bp = __shfl_sync(FULL, bp, leader);
-        __syncwarp();
-        if (valid && lane == leader) cnt[s] = bp + __popc(peers);
-        __syncwarp();
-        if (valid) {
-            RowInfo<T> r;
-            r.o = e; r.slot = s; r.dn = dn[e]; r.ds = ds[e];
-            const int pos = natural_order ? e : bp + rank;
-            ri[pos] = r;
-            if (rowd) rowd[pos] = make_double2((double)r.dn, (double)r.ds);
-        }
-    }
-}
-
-// Removal loss dTD^{-m_i} = sum_{nearest(o)=i} d_s(o) - d_n(o),
-// one warp per slot over its sorted segment (fixed order).  Slots with an
-// empty segment have R_i = 0 and acc_i = 0: their smallest index is kept in
-// *empty_slot (dTD(m_i, x_c) = dTD^{+x_c} for them).
-template <typename T, typename A>
-__global__ void k_removal_loss(const RowInfo<T>* __restrict__ ri, const int* __restrict__ seg_start, int k,
-                               A* __restrict__ R, int* __restrict__ empty_slot) {
-    const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
-    if (warp >= k) return;
-    const int a = seg_start[warp], z = seg_start[warp + 1];
-    A s = 0;
-    for (int p = a + lane; p < z; p += 32) s += (A)ri[p].ds - (A)ri[p].dn;
-#pragma unroll
-    for (int x = 16; x >= 1; x >>= 1) s += __shfl_xor_sync(FULL, s, x);
-    if (lane == 0) {
-        R[warp] = s;
-        if (a == z) atomicMin(empty_slot, warp);
-    }
-}
-
-// Row parts of the stream: part q covers sorted positions [part_lo(q), part_lo(q+1));
-// head/tail slot = slot of its first/last row.
+// Slot of the first / last row of every stream part (the post kernel's
+// phase 7 computes the same).
 template <typename T>
 __global__ void k_part_meta(const RowInfo<T>* __restrict__ ri, int n, int P, int* __restrict__ head_slot,
                             int* __restrict__ tail_slot) {
@@ -482,244 +377,6 @@ __global__ void k_part_meta(const RowInfo<T>* __restrict__ ri, int n, int P, int
     head_slot[q] = ri[p0].slot;
     tail_slot[q] = ri[p1 - 1].slot;
 }
-
-// ---------------------------------------------------------------------------
-// a3: the SWAP-delta stream (Alg.3, Eq. eqn:better-change3)
-// ---------------------------------------------------------------------------
-//
-// A CTA of WARPS warps owns WARPS*128 consecutive candidate columns; lane l of
-// warp w owns the 4 columns cb..cb+3.  blockIdx.y selects a part of the
-// slot-sorted row order.  For every row o (in sorted order) the warp loads
-// D[o][cb..cb+3] (one 128-bit load per lane, 512 contiguous bytes per warp)
-// and applies, per candidate column c:
-//     d < d_n(o):          plus_c += d - d_n(o);  acc_c[nearest(o)] += d_n - d_s
-//     d_n(o) <= d < d_s(o): acc_c[nearest(o)] += d - d_s(o)
-// Because rows arrive grouped by nearest(o), acc_c[i] is the running segment
-// sum `seg` held in registers; at the end of each slot's segment the value
-// dTD_i - dTD^{+x_c} = R_i + seg is final and enters a running
-// lexicographic min (interior segments), or is emitted as the part's head /
-// tail partial sum (segments cut by part boundaries; completed by
-// k_swap_combine).  No k-vector is ever materialised.
-template <typename T, typename A, int WARPS, int U>
-__global__ void __launch_bounds__(WARPS * 32)
-k_swap_stream(const T* __restrict__ D, int64_t ld, int w, int n, int P,
-              const RowInfo<T>* __restrict__ ri, const A* __restrict__ R,
-              A* __restrict__ out_plus, A* __restrict__ out_head, A* __restrict__ out_tail,
-              A* __restrict__ out_imin, int* __restrict__ out_islot) {
-    using V = typename Vec4<T>::type;
-    const int q = blockIdx.y;
-    const int64_t p0 = part_lo(q, n, P), p1 = part_lo(q + 1, n, P);
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int cb = (blockIdx.x * WARPS + warp) * 128 + lane * 4;
-    const bool active = cb < w;
-    const T* Dc = D + (active ? cb : 0);
-
-    A plus[4], seg[4], head[4], imin[4];
-    int islot[4];
-#pragma unroll
-    for (int j = 0; j < 4; ++j) { plus[j] = 0; seg[j] = 0; head[j] = 0; imin[j] = amax<A>(); islot[j] = -1; }
-    int cur = ri[p0].slot;
-    bool first = true;
-
-    for (int64_t p = p0; p < p1; p += U) {
-        const int nb = (int)min((int64_t)U, p1 - p);
-        RowInfo<T> r[U];
-        V v[U];
-#pragma unroll
-        for (int u = 0; u < U; ++u)
-            if (u < nb) r[u] = ri[p + u];
-#pragma unroll
-        for (int u = 0; u < U; ++u) {
-            if (u < nb && active) {
-                v[u] = ld_stream4(Dc + (int64_t)r[u].o * ld);
-            } else {
-                T big = dmax<T>();
-                memcpy(&v[u].x, &big, sizeof(T)); memcpy(&v[u].y, &big, sizeof(T));
-                memcpy(&v[u].z, &big, sizeof(T)); memcpy(&v[u].w, &big, sizeof(T));
-            }
-        }
-#pragma unroll
-        for (int u = 0; u < U; ++u) {
-            if (u >= nb) break;
-            if (r[u].slot != cur) {                       // end of slot cur's segment (warp-uniform)
-                if (first) {
-#pragma unroll
-                    for (int j = 0; j < 4; ++j) head[j] = seg[j];
-                    first = false;
-                } else {
-                    const A rv = R[cur];
-#pragma unroll
-                    for (int j = 0; j < 4; ++j) {
-                        const A val = rv + seg[j];
-                        if (val < imin[j]) { imin[j] = val; islot[j] = cur; }
-                    }
-                }
-#pragma unroll
-                for (int j = 0; j < 4; ++j) seg[j] = 0;
-                cur = r[u].slot;
-            }
-            const T dn = r[u].dn, ds = r[u].ds;
-            T x[4];
-            memcpy(&x[0], &v[u].x, sizeof(T)); memcpy(&x[1], &v[u].y, sizeof(T));
-            memcpy(&x[2], &v[u].z, sizeof(T)); memcpy(&x[3], &v[u].w, sizeof(T));
-            const bool hit = (x[0] < ds) | (x[1] < ds) | (x[2] < ds) | (x[3] < ds);
-            if (__any_sync(FULL, hit)) {
-                const A dnA = (A)dn, dsA = (A)ds, dnds = dnA - dsA;
-#pragma unroll
-                for (int j = 0; j < 4; ++j) {
-                    if (x[j] < ds) {
-                        const A xa = (A)x[j];
-                        if (x[j] < dn) { plus[j] += xa - dnA; seg[j] += dnds; }
-                        else { seg[j] += xa - dsA; }
-                    }
-                }
-            }
-        }
-    }
-    if (first) {
-#pragma unroll
-        for (int j = 0; j < 4; ++j) { head[j] = seg[j]; seg[j] = 0; }
-    }
-    if (!active) return;
-    const int64_t base = (int64_t)q * w;
-#pragma unroll
-    for (int j = 0; j < 4; ++j) {
-        const int c = cb + j;
-        if (c < w) {
-            out_plus[base + c] = plus[j];
-            out_head[base + c] = head[j];
-            out_tail[base + c] = seg[j];
-            out_imin[base + c] = imin[j];
-            out_islot[base + c] = islot[j];
-        }
-    }
-}
-
-// ---------------------------------------------------------------------------
-// a3, TMA-staged variant: a producer warp streams each row chunk of the
-// CTA's column tile with one cp.async.bulk (TMA bulk copy, SASS UBLKCP) into
-// an S-stage shared-memory ring guarded by mbarriers; NC consumer warps read
-// rows from shared memory and apply the same per-element update as
-// k_swap_stream.  Loads never occupy consumer registers, so the bytes in
-// flight per SM (S x RB x NC x 512 B per CTA) are set by the ring depth, not
-// by occupancy.
-// ---------------------------------------------------------------------------
-// Per-lane accumulator state of the SWAP-delta stream for the 4 candidate
-// columns a lane owns (Eq. eqn:better-change3 / Alg.3):
-//   plus[j]  dTD^{+x_c} so far
-//   seg[j]   acc_c[cur]: the current slot's running removal correction
-//   head[j]  the part's first (possibly cut) segment
-//   imin/islot  lexicographic min of R_i + acc_c[i] over closed interior segments
-template <typename A>
-struct StreamAcc {
-    A plus[4], seg[4], head[4], imin[4];
-    int islot[4];
-    int cur;
-    bool first;
-    __device__ __forceinline__ void init(int slot0) {
-#pragma unroll
-        for (int j = 0; j < 4; ++j) { plus[j] = 0; seg[j] = 0; head[j] = 0; imin[j] = amax<A>(); islot[j] = -1; }
-        cur = slot0;
-        first = true;
-    }
-    // One row o with cached (d_n, d_s); x[j] = d(x_o, x_c) for the lane's 4
-    // candidates.  Cases (i)/(ii) of Alg.3; the per-element work is
-    // entered only when some lane of the warp has d < d_s for that element.
-    // One row o with cached (d_n, d_s); x[j] = d(x_o, x_c) for the lane's 4
-    // candidates.  Cases (i)/(ii) of Alg.3 P:883-889.
-    template <typename T>
-    __device__ __forceinline__ void row(const T (&x)[4], T dn, T ds) {
-        const T mn = min(min(x[0], x[1]), min(x[2], x[3]));
-        if (!__any_sync(FULL, mn < ds)) return;
-        const A dnA = (A)dn, dsA = (A)ds, dnds = dnA - dsA;
-#pragma unroll
-        for (int j = 0; j < 4; ++j) elem(j, x[j], dn, ds, dnA, dsA, dnds);
-    }
-    template <typename T>
-    __device__ __forceinline__ void elem(int j, T x, T dn, T ds, A dnA, A dsA, A dnds) {
-        const A xa = (A)x;
-        const bool c1 = x < dn, c2 = x < ds;
-        if (c1) { plus[j] += xa - dnA; seg[j] += dnds; }
-        if (c2 && !c1) seg[j] += xa - dsA;
-    }
-    // RB rows that all belong to the current slot's segment.  One warp-wide OR
-    // of the lanes' 4-bit masks "element j has d < d_s in some row of the
-    // stage" decides which of the 4 element columns need the update at all
-    // (~1% of the stream's pairs hit).  For a column that does, the RB row
-    // terms are computed independently (select form, no data-dependent
-    // branches) and summed as a tree, so the fixed-latency fp64 chain per
-    // stage is log2(RB)+1 deep instead of 2*RB.
-    template <typename T, int RB>
-    __device__ __forceinline__ void stage(const T (&x)[RB][4], const RowInfo<T> (&r)[RB]) {
-        unsigned m = 0;
-#pragma unroll
-        for (int j = 0; j < 4; ++j) {
-            bool h = false;
-#pragma unroll
-            for (int u = 0; u < RB; ++u) h |= x[u][j] < r[u].ds;
-            m |= (unsigned)h << j;
-        }
-        const unsigned wm = __reduce_or_sync(FULL, m);
-        if (wm == 0) return;
-        A dnA[RB], dsA[RB], dnds[RB];
-#pragma unroll
-        for (int u = 0; u < RB; ++u) { dnA[u] = (A)r[u].dn; dsA[u] = (A)r[u].ds; dnds[u] = dnA[u] - dsA[u]; }
-#pragma unroll
-        for (int j = 0; j < 4; ++j) {
-            if (wm & (1u << j)) {
-                A tp[RB], ts[RB];
-#pragma unroll
-                for (int u = 0; u < RB; ++u) {
-                    const bool c1 = x[u][j] < r[u].dn, c2 = x[u][j] < r[u].ds;
-                    const A t = (A)x[u][j] - (c1 ? dnA[u] : dsA[u]);
-                    tp[u] = c1 ? t : (A)0;
-                    ts[u] = c1 ? dnds[u] : (c2 ? t : (A)0);
-                }
-#pragma unroll
-                for (int h = 1; h < RB; h <<= 1)
-#pragma unroll
-                    for (int u = 0; u + h < RB; u += 2 * h) { tp[u] += tp[u + h]; ts[u] += ts[u + h]; }
-                plus[j] += tp[0];
-                seg[j] += ts[0];
-            }
-        }
-    }
-    // The segment of slot `cur` ended; `next` starts.  FastPAM2 mode
-    // (acc_out != nullptr) also stores the complete interior sums
-    // acc_c[cur] = acc_out[cur*w + c] for the lane's columns c = cb..cb+3.
-    template <typename RA>
-    __device__ __forceinline__ void close_segment(int next, const RA* __restrict__ R, A* __restrict__ acc_out = nullptr,
-                                                  int w = 0, int cb = 0) {
-        if (first) {
-#pragma unroll
-            for (int j = 0; j < 4; ++j) head[j] = seg[j];
-            first = false;
-        } else {
-            if (acc_out) {
-#pragma unroll
-                for (int j = 0; j < 4; ++j)
-                    if (cb + j < w) acc_out[(int64_t)cur * w + cb + j] = seg[j];
-            }
-            const A rv = R[cur];
-#pragma unroll
-            for (int j = 0; j < 4; ++j) {
-                const A val = rv + seg[j];
-                if (val < imin[j]) { imin[j] = val; islot[j] = cur; }
-            }
-        }
-#pragma unroll
-        for (int j = 0; j < 4; ++j) seg[j] = 0;
-        cur = next;
-    }
-    // End of the part: the open segment becomes the tail (or the head if the
-    // part held a single segment; its tail is then 0).
-    __device__ __forceinline__ void finish() {
-        if (first) {
-#pragma unroll
-            for (int j = 0; j < 4; ++j) { head[j] = seg[j]; seg[j] = 0; }
-        }
-    }
-};
 
 namespace ptx {
 __device__ __forceinline__ uint32_t sa(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
@@ -779,720 +436,26 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
 }
 }  // namespace ptx
 
-template <typename T, int NC, int RB, int S>
-struct TmaCfg {
-    static constexpr int COLS = NC * 128;                  // columns per CTA
-    static constexpr int ROWB = COLS * (int)sizeof(T);     // bytes of one row chunk
-    static constexpr int DATAB = S * RB * ROWB;
-    static constexpr int RIB = S * RB * 16;
-    static constexpr int SMEM = DATAB + RIB + 2 * S * 8;
-    static constexpr int THREADS = (NC + 1) * 32;
-};
-
-template <typename T, typename A, int NC, int RB, int S, int MINB = 2>
-__global__ void __launch_bounds__((NC + 1) * 32, MINB)
-k_swap_stream_tma(const T* __restrict__ D, int64_t ld, int w, int wpad, int n, int P,
-                  const RowInfo<T>* __restrict__ ri, const A* __restrict__ R,
-                  A* __restrict__ out_plus, A* __restrict__ out_head, A* __restrict__ out_tail,
-                  A* __restrict__ out_imin, int* __restrict__ out_islot, int debug_nocompute,
-                  A* __restrict__ out_acc = nullptr) {
-    using C = TmaCfg<T, NC, RB, S>;
-    using V = typename Vec4<T>::type;
-    extern __shared__ __align__(128) unsigned char smem[];
-    T* sdata = reinterpret_cast<T*>(smem);
-    RowInfo<T>* sri = reinterpret_cast<RowInfo<T>*>(smem + C::DATAB);
-    uint64_t* full = reinterpret_cast<uint64_t*>(smem + C::DATAB + C::RIB);
-    uint64_t* empty = full + S;
-
-    const int q = blockIdx.y;
-    const int64_t p0 = part_lo(q, n, P), p1 = part_lo(q + 1, n, P);
-    const int nstages = (int)((p1 - p0 + RB - 1) / RB);
-    const int ctacol = blockIdx.x * C::COLS;
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-
-    if (threadIdx.x == 0) {
-        for (int s = 0; s < S; ++s) {
-            ptx::mbar_init(&full[s], 1);
-            ptx::mbar_init(&empty[s], NC);
-        }
-        ptx::fence_mbar_init();
-    }
-    __syncthreads();
-
-    if (warp == NC) {
-        // ---------------- producer warp ----------------
-        const uint32_t cbytes = (uint32_t)min(C::COLS, wpad - ctacol) * (uint32_t)sizeof(T);
-        const uint64_t pol = ptx::policy_evict_first();
-        int o_next = (lane < RB && p0 + lane < p1) ? ri[p0 + lane].o : 0;
-        for (int st = 0; st < nstages; ++st) {
-            const int s = st % S;
-            if (st >= S) ptx::mbar_wait(&empty[s], ((st / S) & 1) ^ 1);
-            const int64_t pr = p0 + (int64_t)st * RB;
-            const int nb = (int)min((int64_t)RB, p1 - pr);
-            const int o = o_next;
-            const int64_t pn = pr + RB + lane;
-            if (lane < RB && pn < p1) o_next = ri[pn].o;     // prefetch the next stage's rows
-            if (lane == 0) ptx::mbar_expect_tx(&full[s], (uint32_t)nb * (cbytes + 16u));
-            __syncwarp();
-            if (lane < nb)
-                ptx::bulk_g2s(sdata + (size_t)(s * RB + lane) * C::COLS, D + (int64_t)o * ld + ctacol, cbytes,
-                              &full[s], pol);
-            if (lane == 0) ptx::bulk_g2s(sri + s * RB, ri + pr, (uint32_t)nb * 16u, &full[s]);
-        }
-        return;
-    }
-
-    // ---------------- consumer warps ----------------
-    const int cb = ctacol + warp * 128 + lane * 4;
-    const bool active = cb < w;
-    StreamAcc<A> acc;
-    acc.init(ri[p0].slot);
-    const T big = dmax<T>();
-
-    for (int st = 0; st < nstages; ++st) {
-        const int s = st % S;
-        ptx::mbar_wait(&full[s], (st / S) & 1);
-        const int64_t pr = p0 + (int64_t)st * RB;
-        const int nb = (int)min((int64_t)RB, p1 - pr);
-        RowInfo<T> r[RB];
-        T x[RB][4];
-#pragma unroll
-        for (int u = 0; u < RB; ++u) {
-            r[u] = sri[s * RB + u];    // rows >= nb hold stale data and are never used
-            V v = *reinterpret_cast<const V*>(sdata + (size_t)(s * RB + u) * C::COLS + warp * 128 + lane * 4);
-            memcpy(&x[u][0], &v.x, sizeof(T)); memcpy(&x[u][1], &v.y, sizeof(T));
-            memcpy(&x[u][2], &v.z, sizeof(T)); memcpy(&x[u][3], &v.w, sizeof(T));
-        }
-        __syncwarp();
-        if (lane == 0) ptx::mbar_arrive(&empty[s]);
-        if (!active) {
-#pragma unroll
-            for (int u = 0; u < RB; ++u)
-#pragma unroll
-                for (int j = 0; j < 4; ++j) x[u][j] = big;
-        }
-        if (debug_nocompute) continue;
-        if (nb == RB && r[RB - 1].slot == acc.cur) {
-            // fast path: a full stage inside the current slot's segment (rows are
-            // sorted by slot, so the last row's slot decides).
-            acc.template stage<T, RB>(x, r);
-        } else {
-#pragma unroll
-            for (int u = 0; u < RB; ++u) {
-                if (u < nb) {
-                    if (r[u].slot != acc.cur) acc.close_segment(r[u].slot, R, out_acc, w, cb);
-                    acc.row(x[u], r[u].dn, r[u].ds);
-                }
-            }
-        }
-    }
-    acc.finish();
-    if (!active) return;
-    const int64_t base = (int64_t)q * w;
-#pragma unroll
-    for (int j = 0; j < 4; ++j) {
-        const int c = cb + j;
-        if (c < w) {
-            out_plus[base + c] = acc.plus[j];
-            out_head[base + c] = acc.head[j];
-            out_tail[base + c] = acc.seg[j];
-            out_imin[base + c] = acc.imin[j];
-            out_islot[base + c] = acc.islot[j];
-        }
-    }
-}
-
 // ---------------------------------------------------------------------------
-// a3, warp-autonomous TMA variant (default).  Every warp owns 128 candidate
-// columns and its own S-stage shared-memory ring: it refills a stage with
-// cp.async.bulk copies (one 512-byte row chunk per row, plus the 16-byte
-// RowInfo records) as soon as it has moved that stage into registers.  No
-// barrier couples the warps of a CTA, so a warp whose candidates are hit
-// often (case (i)/(ii) updates) never stalls the refills of the others.
-// ---------------------------------------------------------------------------
-template <typename T, int NW, int RB, int S>
-struct WTmaCfg {
-    static constexpr int ROWB = 128 * (int)sizeof(T);                  // one warp's row chunk
-    static constexpr int WARPB = S * RB * (ROWB + 16) + S * 8;          // data + RowInfo + full barriers
-    static constexpr int SMEM = NW * WARPB;
-    static constexpr int THREADS = NW * 32;
-};
-
-template <typename T, typename A, int NW, int RB, int S>
-__global__ void __launch_bounds__(NW * 32)
-k_swap_stream_wtma(const T* __restrict__ D, int64_t ld, int w, int wpad, int n, int P,
-                   const RowInfo<T>* __restrict__ ri, const A* __restrict__ R,
-                   A* __restrict__ out_plus, A* __restrict__ out_head, A* __restrict__ out_tail,
-                   A* __restrict__ out_imin, int* __restrict__ out_islot, int debug_nocompute) {
-    using C = WTmaCfg<T, NW, RB, S>;
-    using V = typename Vec4<T>::type;
-    extern __shared__ __align__(128) unsigned char smem[];
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    unsigned char* wbase = smem + warp * C::WARPB;
-    T* sdata = reinterpret_cast<T*>(wbase);                                   // [S][RB][128]
-    RowInfo<T>* sri = reinterpret_cast<RowInfo<T>*>(wbase + S * RB * C::ROWB); // [S][RB]
-    uint64_t* full = reinterpret_cast<uint64_t*>(wbase + S * RB * (C::ROWB + 16));
-
-    const int q = blockIdx.y;
-    const int64_t p0 = part_lo(q, n, P), p1 = part_lo(q + 1, n, P);
-    const int nstages = (int)((p1 - p0 + RB - 1) / RB);
-    const int cw = (blockIdx.x * NW + warp) * 128;          // first column of this warp
-    if (cw >= w) return;                                     // no warp-collective op spans warps
-    const uint32_t cbytes = (uint32_t)min(128, wpad - cw) * (uint32_t)sizeof(T);
-    const T* Dw = D + cw;
-
-    if (lane == 0) {
-        for (int s = 0; s < S; ++s) ptx::mbar_init(&full[s], 1);
-        ptx::fence_mbar_init();
-    }
-    __syncwarp();
-    const uint64_t pol = ptx::policy_evict_first();
-
-    // refill of stage st (buffer st % S); `o` = row index held by lane u < RB
-    auto issue = [&](int st, int o) {
-        const int64_t pr = p0 + (int64_t)st * RB;
-        if (pr >= p1) return;
-        const int nb = (int)min((int64_t)RB, p1 - pr);
-        const int s = st % S;
-        if (lane == 0) ptx::mbar_expect_tx(&full[s], (uint32_t)nb * (cbytes + 16u));
-        __syncwarp();
-        if (lane < nb) ptx::bulk_g2s(sdata + (size_t)(s * RB + lane) * 128, Dw + (int64_t)o * ld, cbytes, &full[s], pol);
-        if (lane == 0) ptx::bulk_g2s(sri + s * RB, ri + pr, (uint32_t)nb * 16u, &full[s]);
-    };
-    auto row_of = [&](int st) -> int {
-        const int64_t p = p0 + (int64_t)st * RB + lane;
-        return (lane < RB && p < p1) ? ri[p].o : 0;
-    };
-    for (int st = 0; st < S; ++st) issue(st, row_of(st));
-    int o_pref = row_of(S);                                  // rows of the next refill
-
-    const int cb = cw + lane * 4;
-    const bool active = cb < w;
-    StreamAcc<A> acc;
-    acc.init(ri[p0].slot);
-    const T big = dmax<T>();
-
-    for (int st = 0; st < nstages; ++st) {
-        const int s = st % S;
-        ptx::mbar_wait(&full[s], (st / S) & 1);
-        const int64_t pr = p0 + (int64_t)st * RB;
-        const int nb = (int)min((int64_t)RB, p1 - pr);
-        RowInfo<T> r[RB];
-        T x[RB][4];
-#pragma unroll
-        for (int u = 0; u < RB; ++u) {
-            r[u] = sri[s * RB + u];
-            V v = *reinterpret_cast<const V*>(sdata + (size_t)(s * RB + u) * 128 + lane * 4);
-            memcpy(&x[u][0], &v.x, sizeof(T)); memcpy(&x[u][1], &v.y, sizeof(T));
-            memcpy(&x[u][2], &v.z, sizeof(T)); memcpy(&x[u][3], &v.w, sizeof(T));
-        }
-        if (!active) {
-#pragma unroll
-            for (int u = 0; u < RB; ++u)
-#pragma unroll
-                for (int j = 0; j < 4; ++j) x[u][j] = big;
-        }
-        const bool fast = (nb == RB) && (r[RB - 1].slot == acc.cur);
-        // the stage's shared memory has been read into registers (r[] is used
-        // just above); order those generic-proxy reads before the async-proxy
-        // refill of the same buffer.
-        __syncwarp();
-        ptx::fence_proxy_async();
-        const int o_now = o_pref;
-        o_pref = row_of(st + S + 1);
-        issue(st + S, o_now);
-        if (debug_nocompute) continue;
-        if (fast) {
-            acc.template stage<T, RB>(x, r);
-        } else {
-#pragma unroll
-            for (int u = 0; u < RB; ++u) {
-                if (u < nb) {
-                    if (r[u].slot != acc.cur) acc.close_segment(r[u].slot, R);
-                    acc.row(x[u], r[u].dn, r[u].ds);
-                }
-            }
-        }
-    }
-    acc.finish();
-    if (!active) return;
-    const int64_t base = (int64_t)q * w;
-#pragma unroll
-    for (int j = 0; j < 4; ++j) {
-        const int c = cb + j;
-        if (c < w) {
-            out_plus[base + c] = acc.plus[j];
-            out_head[base + c] = acc.head[j];
-            out_tail[base + c] = acc.seg[j];
-            out_imin[base + c] = acc.imin[j];
-            out_islot[base + c] = acc.islot[j];
-        }
-    }
-}
-
-// ---------------------------------------------------------------------------
-// a3, TMA ring + compacted hit processing (default stream kernel).
+// a3: the SWAP-delta stream (Alg.3, Eq. eqn:better-change3).
 //
-// Same producer / S-stage ring as k_swap_stream_tma.  Only ~1% of the
-// (row, candidate) pairs satisfy d < d_s, so the consumers
-// split every stage in two phases:
-//   A  every consumer lane compares its 4 columns x RB rows against d_s and
-//      appends one entry (column, row mask) per column that has a hit to a
-//      CTA-wide list in shared memory (warp-aggregated atomic);
-//   B  after a named barrier, the list is spread over all consumer threads;
-//      each entry updates its column's dTD^{+x_c} and acc_c[slot] partial
-//      sums (fp64 / int64, shared memory) for the marked rows in row order.
-// The per-column accumulation order is fixed (rows ascending, one writer per
-// column and stage), so results are deterministic, and the fp64 work is
-// spread evenly over the warps instead of following where the hits are.
-// Stages that contain a slot change (the end of a segment) or a part's last
-// partial stage take a simple per-lane path.
-// ---------------------------------------------------------------------------
-template <typename T, typename A, int NC, int RB, int S>
-struct CmpCfg {
-    static constexpr int COLS = NC * 128;
-    static constexpr int ROWB = COLS * (int)sizeof(T);
-    static constexpr int DATAB = S * RB * ROWB;
-    static constexpr int RIB = S * RB * 16;
-    static constexpr int BARB = 2 * S * 8;
-    static constexpr int ACCB = 2 * COLS * (int)sizeof(A);      // plus, seg per column
-    static constexpr int HITB = COLS * 4 + S * 4;                 // entries + per-stage counters
-    static constexpr int SMEM = DATAB + RIB + BARB + ACCB + HITB;
-    static constexpr int THREADS = (NC + 1) * 32;
-};
-
-__device__ __forceinline__ void named_bar_sync(int id, int nthreads) {
-    asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
-}
-
-template <typename T, typename A, int NC, int RB, int S>
-__global__ void __launch_bounds__((NC + 1) * 32, 2)
-k_swap_stream_cmp(const T* __restrict__ D, int64_t ld, int w, int wpad, int n, int P,
-                  const RowInfo<T>* __restrict__ ri, const A* __restrict__ R,
-                  A* __restrict__ out_plus, A* __restrict__ out_head, A* __restrict__ out_tail,
-                  A* __restrict__ out_imin, int* __restrict__ out_islot) {
-    using C = CmpCfg<T, A, NC, RB, S>;
-    using V = typename Vec4<T>::type;
-    extern __shared__ __align__(128) unsigned char smem[];
-    T* sdata = reinterpret_cast<T*>(smem);
-    RowInfo<T>* sri = reinterpret_cast<RowInfo<T>*>(smem + C::DATAB);
-    uint64_t* full = reinterpret_cast<uint64_t*>(smem + C::DATAB + C::RIB);
-    uint64_t* empty = full + S;
-    A* accp = reinterpret_cast<A*>(smem + C::DATAB + C::RIB + C::BARB);
-    A* accs = accp + C::COLS;
-    int* hits = reinterpret_cast<int*>(smem + C::DATAB + C::RIB + C::BARB + C::ACCB);
-    int* hitcnt = hits + C::COLS;
-
-    const int q = blockIdx.y;
-    const int64_t p0 = part_lo(q, n, P), p1 = part_lo(q + 1, n, P);
-    const int nstages = (int)((p1 - p0 + RB - 1) / RB);
-    const int ctacol = blockIdx.x * C::COLS;
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    constexpr int NCT = NC * 32;   // consumer threads
-
-    if (threadIdx.x == 0) {
-        for (int st = 0; st < S; ++st) {
-            ptx::mbar_init(&full[st], 1);
-            ptx::mbar_init(&empty[st], 1);
-        }
-        ptx::fence_mbar_init();
-    }
-    for (int i = threadIdx.x; i < C::COLS; i += blockDim.x) { accp[i] = 0; accs[i] = 0; }
-    for (int i = threadIdx.x; i < S; i += blockDim.x) hitcnt[i] = 0;
-    __syncthreads();
-
-    if (warp == NC) {
-        // ---------------- producer warp (as in k_swap_stream_tma) ----------------
-        const uint32_t cbytes = (uint32_t)min(C::COLS, wpad - ctacol) * (uint32_t)sizeof(T);
-        const uint64_t pol = ptx::policy_evict_first();
-        int o_next = (lane < RB && p0 + lane < p1) ? ri[p0 + lane].o : 0;
-        for (int st = 0; st < nstages; ++st) {
-            const int s = st % S;
-            if (st >= S) ptx::mbar_wait(&empty[s], ((st / S) & 1) ^ 1);
-            const int64_t pr = p0 + (int64_t)st * RB;
-            const int nb = (int)min((int64_t)RB, p1 - pr);
-            const int o = o_next;
-            const int64_t pn = pr + RB + lane;
-            if (lane < RB && pn < p1) o_next = ri[pn].o;
-            if (lane == 0) ptx::mbar_expect_tx(&full[s], (uint32_t)nb * (cbytes + 16u));
-            __syncwarp();
-            if (lane < nb)
-                ptx::bulk_g2s(sdata + (size_t)(s * RB + lane) * C::COLS, D + (int64_t)o * ld + ctacol, cbytes,
-                              &full[s], pol);
-            if (lane == 0) ptx::bulk_g2s(sri + s * RB, ri + pr, (uint32_t)nb * 16u, &full[s]);
-        }
-        return;
-    }
-
-    // ---------------- consumer warps ----------------
-    const int cl0 = warp * 128 + lane * 4;          // this lane's first column within the tile
-    const int cb = ctacol + cl0;
-    const bool active = cb < w;
-    const T big = dmax<T>();
-    A head[4], imin[4];
-    int islot[4];
-#pragma unroll
-    for (int j = 0; j < 4; ++j) { head[j] = 0; imin[j] = amax<A>(); islot[j] = -1; }
-    int cur = ri[p0].slot;
-    bool first = true;
-    const unsigned lt = (1u << lane) - 1u;
-
-    auto close_segment = [&](int next) {      // the lane's own 4 columns
-        if (first) {
-#pragma unroll
-            for (int j = 0; j < 4; ++j) head[j] = accs[cl0 + j];
-            first = false;
-        } else {
-            const A rv = R[cur];
-#pragma unroll
-            for (int j = 0; j < 4; ++j) {
-                const A val = rv + accs[cl0 + j];
-                if (val < imin[j]) { imin[j] = val; islot[j] = cur; }
-            }
-        }
-#pragma unroll
-        for (int j = 0; j < 4; ++j) accs[cl0 + j] = 0;
-        cur = next;
-    };
-
-    for (int st = 0; st < nstages; ++st) {
-        const int s = st % S;
-        ptx::mbar_wait(&full[s], (st / S) & 1);
-        const int64_t pr = p0 + (int64_t)st * RB;
-        const int nb = (int)min((int64_t)RB, p1 - pr);
-        const T* srow = sdata + (size_t)(s * RB) * C::COLS;
-        const RowInfo<T>* srii = sri + s * RB;
-        const bool fast = (nb == RB) && (srii[RB - 1].slot == cur);   // identical in every consumer warp
-        if (fast) {
-            // ---- phase A: per-column row masks, compacted into the hit list ----
-            unsigned colmask[4] = {0, 0, 0, 0};
-#pragma unroll
-            for (int u = 0; u < RB; ++u) {
-                const T ds = srii[u].ds;
-                const V v = *reinterpret_cast<const V*>(srow + (size_t)u * C::COLS + cl0);
-                T x[4];
-                memcpy(&x[0], &v.x, sizeof(T)); memcpy(&x[1], &v.y, sizeof(T));
-                memcpy(&x[2], &v.z, sizeof(T)); memcpy(&x[3], &v.w, sizeof(T));
-#pragma unroll
-                for (int j = 0; j < 4; ++j) colmask[j] |= (unsigned)(active && x[j] < ds) << u;
-            }
-            const int hc = (colmask[0] != 0) + (colmask[1] != 0) + (colmask[2] != 0) + (colmask[3] != 0);
-            const unsigned anyb = __ballot_sync(FULL, hc != 0);
-            if (anyb) {
-                int incl = hc;
-#pragma unroll
-                for (int d = 1; d < 32; d <<= 1) {
-                    const int y = __shfl_up_sync(FULL, incl, d);
-                    if (lane >= d) incl += y;
-                }
-                int base = 0;
-                if (lane == 31) base = atomicAdd(&hitcnt[s], incl);
-                base = __shfl_sync(FULL, base, 31);
-                int pos = base + incl - hc;
-#pragma unroll
-                for (int j = 0; j < 4; ++j)
-                    if (colmask[j]) hits[pos++] = (cl0 + j) | (int)(colmask[j] << 16);
-            }
-            (void)lt;
-            named_bar_sync(1, NCT);
-            // ---- phase B: one thread per hit column, rows in order ----
-            const int H = hitcnt[s];
-            for (int e = warp + NC * lane; e < H; e += NCT) {     // spread entries over the warps
-                const int ent = hits[e];
-                const int c = ent & 0xffff;
-                const unsigned rm = (unsigned)ent >> 16;
-                A pp = 0, sg = 0;
-#pragma unroll
-                for (int u = 0; u < RB; ++u) {
-                    if (rm & (1u << u)) {
-                        const T xv = srow[(size_t)u * C::COLS + c];
-                        const T dn = srii[u].dn, ds = srii[u].ds;
-                        const A xa = (A)xv;
-                        if (xv < dn) { pp += xa - (A)dn; sg += (A)dn - (A)ds; }
-                        else { sg += xa - (A)ds; }
-                    }
-                }
-                accp[c] += pp;
-                accs[c] += sg;
-            }
-            named_bar_sync(1, NCT);
-            if (warp == 0 && lane == 0) {
-                hitcnt[s] = 0;
-                ptx::mbar_arrive(&empty[s]);
-            }
-        } else {
-            // ---- slow path: per lane, its own 4 columns, row by row ----
-            for (int u = 0; u < nb; ++u) {
-                const RowInfo<T> r = srii[u];
-                if (r.slot != cur) close_segment(r.slot);
-                const V v = *reinterpret_cast<const V*>(srow + (size_t)u * C::COLS + cl0);
-                T x[4];
-                memcpy(&x[0], &v.x, sizeof(T)); memcpy(&x[1], &v.y, sizeof(T));
-                memcpy(&x[2], &v.z, sizeof(T)); memcpy(&x[3], &v.w, sizeof(T));
-#pragma unroll
-                for (int j = 0; j < 4; ++j) {
-                    const T xv = active ? x[j] : big;
-                    if (xv < r.ds) {
-                        const A xa = (A)xv;
-                        if (xv < r.dn) { accp[cl0 + j] += xa - (A)r.dn; accs[cl0 + j] += (A)r.dn - (A)r.ds; }
-                        else { accs[cl0 + j] += xa - (A)r.ds; }
-                    }
-                }
-            }
-            named_bar_sync(1, NCT);
-            if (warp == 0 && lane == 0) ptx::mbar_arrive(&empty[s]);
-        }
-    }
-    // end of the part: the open segment is the tail (or the head)
-    A tail[4];
-    if (first) {
-#pragma unroll
-        for (int j = 0; j < 4; ++j) { head[j] = accs[cl0 + j]; tail[j] = 0; }
-    } else {
-#pragma unroll
-        for (int j = 0; j < 4; ++j) tail[j] = accs[cl0 + j];
-    }
-    if (!active) return;
-    const int64_t base = (int64_t)q * w;
-#pragma unroll
-    for (int j = 0; j < 4; ++j) {
-        const int c = cb + j;
-        if (c < w) {
-            out_plus[base + c] = accp[cl0 + j];
-            out_head[base + c] = head[j];
-            out_tail[base + c] = tail[j];
-            out_imin[base + c] = imin[j];
-            out_islot[base + c] = islot[j];
-        }
-    }
-}
-
-// ---------------------------------------------------------------------------
-// a3, TMA ring + per-warp hit queues (k_swap_stream_tmaq).
+// A CTA owns NC*128 consecutive candidate columns (lane l of consumer warp w
+// owns 4 of them); blockIdx.y selects a part of the slot-sorted row order.
+// Per candidate column c and row o (d = D[o][c]):
+//     d < d_n(o):          plus_c += d - d_n(o);  acc_c[nearest(o)] += d_n - d_s
+//     d_n(o) <= d < d_s(o): acc_c[nearest(o)] += d - d_s(o)
+// Because rows arrive grouped by nearest(o), acc_c[i] is a running segment
+// sum held in registers; at the end of each slot's segment R_i + acc_c[i] is
+// final and enters a running lexicographic min, or is emitted as the part's
+// head / tail partial sum (segments cut by part boundaries, completed by
+// k_swap_combine).  No k-vector is ever materialised (FastPAM2 mode stores
+// the complete per-slot sums instead).
 //
-// Producer and ring as in k_swap_stream_tma.  The (d < d_s) hits of a stage
-// concentrate on the few candidate columns near the current slot's cluster,
-// i.e. on one or two warps of the CTA; with register accumulators such a
-// warp executes every hit column's fp64 update for all 32 lanes (SIMT
-// efficiency ~1/32) and the shared ring then advances at its pace.  Here each
-// warp compacts its hit columns of the stage (one entry = column + row mask)
-// into a warp-private queue and processes the queue lane-parallel, updating
-// per-column partial sums in shared memory (one owner per column and stage,
-// rows in order: deterministic).  Heavy and light warps now cost about the
-// same; no barrier couples the warps beyond the ring itself.
-// ---------------------------------------------------------------------------
-template <typename T, typename A, int NC, int RB, int S>
-struct TmaqCfg {
-    static constexpr int COLS = NC * 128;
-    static constexpr int ROWB = COLS * (int)sizeof(T);
-    static constexpr int DATAB = S * RB * ROWB;
-    static constexpr int RIB = S * RB * 16;
-    static constexpr int BARB = 2 * S * 8;
-    static constexpr int ACCB = 2 * COLS * (int)sizeof(A);   // plus, seg per column
-    static constexpr int QB = COLS * 4;                        // per-warp queues (128 entries each)
-    static constexpr int SMEM = DATAB + RIB + BARB + ACCB + QB;
-    static constexpr int THREADS = (NC + 1) * 32;
-};
-
-template <typename T, typename A, int NC, int RB, int S>
-__global__ void __launch_bounds__((NC + 1) * 32, 2)
-k_swap_stream_tmaq(const T* __restrict__ D, int64_t ld, int w, int wpad, int n, int P,
-                   const RowInfo<T>* __restrict__ ri, const A* __restrict__ R,
-                   A* __restrict__ out_plus, A* __restrict__ out_head, A* __restrict__ out_tail,
-                   A* __restrict__ out_imin, int* __restrict__ out_islot, A* __restrict__ out_acc) {
-    using C = TmaqCfg<T, A, NC, RB, S>;
-    using V = typename Vec4<T>::type;
-    extern __shared__ __align__(128) unsigned char smem[];
-    T* sdata = reinterpret_cast<T*>(smem);
-    RowInfo<T>* sri = reinterpret_cast<RowInfo<T>*>(smem + C::DATAB);
-    uint64_t* full = reinterpret_cast<uint64_t*>(smem + C::DATAB + C::RIB);
-    uint64_t* empty = full + S;
-    A* accp = reinterpret_cast<A*>(smem + C::DATAB + C::RIB + C::BARB);
-    A* accs = accp + C::COLS;
-    int* queue = reinterpret_cast<int*>(smem + C::DATAB + C::RIB + C::BARB + C::ACCB);
-
-    const int q = blockIdx.y;
-    const int64_t p0 = part_lo(q, n, P), p1 = part_lo(q + 1, n, P);
-    const int nstages = (int)((p1 - p0 + RB - 1) / RB);
-    const int ctacol = blockIdx.x * C::COLS;
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-
-    if (threadIdx.x == 0) {
-        for (int st = 0; st < S; ++st) {
-            ptx::mbar_init(&full[st], 1);
-            ptx::mbar_init(&empty[st], NC);
-        }
-        ptx::fence_mbar_init();
-    }
-    for (int i = threadIdx.x; i < C::COLS; i += blockDim.x) { accp[i] = 0; accs[i] = 0; }
-    __syncthreads();
-
-    if (warp == NC) {
-        // ---------------- producer warp ----------------
-        const uint32_t cbytes = (uint32_t)min(C::COLS, wpad - ctacol) * (uint32_t)sizeof(T);
-        const uint64_t pol = ptx::policy_evict_first();
-        int o_next = (lane < RB && p0 + lane < p1) ? ri[p0 + lane].o : 0;
-        for (int st = 0; st < nstages; ++st) {
-            const int s = st % S;
-            if (st >= S) ptx::mbar_wait(&empty[s], ((st / S) & 1) ^ 1);
-            const int64_t pr = p0 + (int64_t)st * RB;
-            const int nb = (int)min((int64_t)RB, p1 - pr);
-            const int o = o_next;
-            const int64_t pn = pr + RB + lane;
-            if (lane < RB && pn < p1) o_next = ri[pn].o;
-            if (lane == 0) ptx::mbar_expect_tx(&full[s], (uint32_t)nb * (cbytes + 16u));
-            __syncwarp();
-            if (lane < nb)
-                ptx::bulk_g2s(sdata + (size_t)(s * RB + lane) * C::COLS, D + (int64_t)o * ld + ctacol, cbytes,
-                              &full[s], pol);
-            if (lane == 0) ptx::bulk_g2s(sri + s * RB, ri + pr, (uint32_t)nb * 16u, &full[s]);
-        }
-        return;
-    }
-
-    // ---------------- consumer warps ----------------
-    const int wc0 = warp * 128;                 // this warp's first column within the tile
-    const int cl0 = wc0 + lane * 4;             // this lane's first column within the tile
-    const int cb = ctacol + cl0;
-    const bool active = cb < w;
-    int* wq = queue + warp * 128;
-    A head[4], imin[4];
-    int islot[4];
-#pragma unroll
-    for (int j = 0; j < 4; ++j) { head[j] = 0; imin[j] = amax<A>(); islot[j] = -1; }
-    int cur = ri[p0].slot;
-    bool first = true;
-
-    auto close_segment = [&](int next) {        // the lane's own 4 columns
-        __syncwarp();                           // queue updates of other lanes are visible
-        if (first) {
-#pragma unroll
-            for (int j = 0; j < 4; ++j) head[j] = accs[cl0 + j];
-            first = false;
-        } else {
-            if (out_acc) {
-#pragma unroll
-                for (int j = 0; j < 4; ++j)
-                    if (cb + j < w) out_acc[(int64_t)cur * w + cb + j] = accs[cl0 + j];
-            }
-            const A rv = R[cur];
-#pragma unroll
-            for (int j = 0; j < 4; ++j) {
-                const A val = rv + accs[cl0 + j];
-                if (val < imin[j]) { imin[j] = val; islot[j] = cur; }
-            }
-        }
-#pragma unroll
-        for (int j = 0; j < 4; ++j) accs[cl0 + j] = 0;
-        cur = next;
-        __syncwarp();
-    };
-
-    // compacted update of the rows [u0, u1) of the current stage
-    auto process = [&](const T* srow, const RowInfo<T>* srii, int u0, int u1) {
-        unsigned colmask[4] = {0, 0, 0, 0};
-        for (int u = u0; u < u1; ++u) {
-            const T ds = srii[u].ds;
-            const V v = *reinterpret_cast<const V*>(srow + (size_t)u * C::COLS + cl0);
-            T x[4];
-            memcpy(&x[0], &v.x, sizeof(T)); memcpy(&x[1], &v.y, sizeof(T));
-            memcpy(&x[2], &v.z, sizeof(T)); memcpy(&x[3], &v.w, sizeof(T));
-#pragma unroll
-            for (int j = 0; j < 4; ++j) colmask[j] |= (unsigned)(active && x[j] < ds) << u;
-        }
-        const int hc = (colmask[0] != 0) + (colmask[1] != 0) + (colmask[2] != 0) + (colmask[3] != 0);
-        if (__ballot_sync(FULL, hc != 0) == 0) return;
-        int incl = hc;
-#pragma unroll
-        for (int d = 1; d < 32; d <<= 1) {
-            const int y = __shfl_up_sync(FULL, incl, d);
-            if (lane >= d) incl += y;
-        }
-        const int H = __shfl_sync(FULL, incl, 31);
-        int pos = incl - hc;
-#pragma unroll
-        for (int j = 0; j < 4; ++j)
-            if (colmask[j]) wq[pos++] = (lane * 4 + j) | (int)(colmask[j] << 16);
-        __syncwarp();
-        for (int e = lane; e < H; e += 32) {
-            const int ent = wq[e];
-            const int c = wc0 + (ent & 0xffff);
-            const unsigned rm = (unsigned)ent >> 16;
-            A pp = 0, sg = 0;
-#pragma unroll
-            for (int u = 0; u < RB; ++u) {
-                if (rm & (1u << u)) {
-                    const T xv = srow[(size_t)u * C::COLS + c];
-                    const T dn = srii[u].dn, ds = srii[u].ds;
-                    const A xa = (A)xv;
-                    if (xv < dn) { pp += xa - (A)dn; sg += (A)dn - (A)ds; }
-                    else { sg += xa - (A)ds; }
-                }
-            }
-            accp[c] += pp;
-            accs[c] += sg;
-        }
-        __syncwarp();
-    };
-
-    for (int st = 0; st < nstages; ++st) {
-        const int s = st % S;
-        ptx::mbar_wait(&full[s], (st / S) & 1);
-        const int64_t pr = p0 + (int64_t)st * RB;
-        const int nb = (int)min((int64_t)RB, p1 - pr);
-        const T* srow = sdata + (size_t)(s * RB) * C::COLS;
-        const RowInfo<T>* srii = sri + s * RB;
-        if (nb == RB && srii[RB - 1].slot == cur) {
-            process(srow, srii, 0, RB);
-        } else {
-            int u = 0;
-            while (u < nb) {                     // split the stage at slot changes
-                if (srii[u].slot != cur) close_segment(srii[u].slot);
-                int v = u + 1;
-                while (v < nb && srii[v].slot == cur) ++v;
-                process(srow, srii, u, v);
-                u = v;
-            }
-        }
-        __syncwarp();
-        if (lane == 0) ptx::mbar_arrive(&empty[s]);
-    }
-    __syncwarp();
-    A tail[4];
-    if (first) {
-#pragma unroll
-        for (int j = 0; j < 4; ++j) { head[j] = accs[cl0 + j]; tail[j] = 0; }
-    } else {
-#pragma unroll
-        for (int j = 0; j < 4; ++j) tail[j] = accs[cl0 + j];
-    }
-    if (!active) return;
-    const int64_t base = (int64_t)q * w;
-#pragma unroll
-    for (int j = 0; j < 4; ++j) {
-        const int c = cb + j;
-        if (c < w) {
-            out_plus[base + c] = accp[cl0 + j];
-            out_head[base + c] = head[j];
-            out_tail[base + c] = tail[j];
-            out_imin[base + c] = imin[j];
-            out_islot[base + c] = islot[j];
-        }
-    }
-}
-
-// ---------------------------------------------------------------------------
-// a3, TMA ring with segment-aligned stages (k_swap_stream_seg, default).
-//
-// As k_swap_stream_tma, but the producer never lets a stage straddle two
-// slots: a stage holds up to RB rows of ONE segment (it is cut where the
-// slot changes; the cut costs ~1 short stage per segment).  The consumer
-// therefore closes a segment only between stages (one warp-uniform check)
-// and every stage takes the same branch-light path:
-//   * 16 compares d < d_s folded into a 4-bit "column j has a hit" mask per
-//     lane (setp.or chains), one REDUX.OR over the warp;
-//   * for the (few) columns with a hit somewhere in the warp, the RB row
-//     terms in fp64/int64, branch-free, tree-summed.
+// Delivery: a producer warp moves each row chunk of the column tile with one
+// cp.async.bulk (TMA bulk copy, SASS UBLKCP) into an S-stage shared-memory
+// ring guarded by mbarriers, and never lets a stage straddle two slots (a
+// stage holds up to RB rows of ONE segment), so the consumers close a
+// segment only between stages (one warp-uniform check).
 // ---------------------------------------------------------------------------
 // A threshold no value compares below (uint32: 0; float: -inf, false even for NaN).
 template <typename T> __device__ __forceinline__ T never_lt();
@@ -1545,211 +508,10 @@ struct SegCfg {
     static constexpr int THREADS = (NC + 1) * 32;
 };
 
-template <typename T, typename A, int NC, int RB, int S, int MINB = 2>
-__global__ void __launch_bounds__((NC + 1) * 32, MINB)
-k_swap_stream_seg(const T* __restrict__ D, int64_t ld, int w, int wpad, int n, int P,
-                  const RowInfo<T>* __restrict__ ri, const A* __restrict__ R,
-                  A* __restrict__ out_plus, A* __restrict__ out_head, A* __restrict__ out_tail,
-                  A* __restrict__ out_imin, int* __restrict__ out_islot, A* __restrict__ out_acc,
-                  const double2* __restrict__ rowd) {
-    using C = SegCfg<T, NC, RB, S>;
-    using V = typename Vec4<T>::type;
-    extern __shared__ __align__(128) unsigned char smem[];
-    T* sdata = reinterpret_cast<T*>(smem);
-    RowInfo<T>* sri = reinterpret_cast<RowInfo<T>*>(smem + C::DATAB);
-    double2* srd = reinterpret_cast<double2*>(smem + C::DATAB + C::RIB);
-    int* snb = reinterpret_cast<int*>(smem + C::DATAB + C::RIB + C::RDB);
-    uint64_t* full = reinterpret_cast<uint64_t*>(smem + C::DATAB + C::RIB + C::RDB + 16 * ((C::NBB + 15) / 16));
-    uint64_t* empty = full + S;
-
-    const int q = blockIdx.y;
-    const int64_t p0 = part_lo(q, n, P), p1 = part_lo(q + 1, n, P);
-    const int ctacol = blockIdx.x * C::COLS;
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-
-    if (threadIdx.x == 0) {
-        for (int st = 0; st < S; ++st) {
-            ptx::mbar_init(&full[st], 1);
-            ptx::mbar_init(&empty[st], NC);
-        }
-        ptx::fence_mbar_init();
-    }
-    __syncthreads();
-
-    if (warp == NC) {
-        // ---------------- producer warp ----------------
-        // Stage = up to RB rows of one slot.  nb = 0 marks the end of the part.
-        const uint32_t cbytes = (uint32_t)min(C::COLS, wpad - ctacol) * (uint32_t)sizeof(T);
-        const uint64_t pol = ptx::policy_evict_first();
-        int64_t pr = p0;
-        int st = 0;
-        // lane u < RB holds (o, slot) of row pr + u
-        int o_l = 0, sl_l = -1;
-        if (lane < RB && pr + lane < p1) { const RowInfo<T> r = ri[pr + lane]; o_l = r.o; sl_l = r.slot; }
-        while (true) {
-            const int s = st % S;
-            if (st >= S) ptx::mbar_wait(&empty[s], ((st / S) & 1) ^ 1);
-            if (pr >= p1) {                      // terminator stage
-                if (lane == 0) {
-                    snb[s] = 0;
-                    ptx::mbar_arrive(&full[s]);
-                }
-                break;
-            }
-            const int slot0 = __shfl_sync(FULL, sl_l, 0);
-            const unsigned same = __ballot_sync(FULL, lane < RB && sl_l == slot0 && pr + lane < p1);
-            const int nb = __ffs(~same) - 1;     // rows of slot0 at the head of the window (>= 1)
-            if (lane == 0) {
-                snb[s] = nb;
-                ptx::mbar_expect_tx(&full[s], (uint32_t)nb * (cbytes + (rowd ? 32u : 16u)));
-            }
-            __syncwarp();
-            if (lane < nb)
-                ptx::bulk_g2s(sdata + (size_t)(s * RB + lane) * C::COLS, D + (int64_t)o_l * ld + ctacol, cbytes,
-                              &full[s], pol);
-            if (lane == 0) ptx::bulk_g2s(sri + s * RB, ri + pr, (uint32_t)nb * 16u, &full[s]);
-            if (lane == 1 && rowd) ptx::bulk_g2s(srd + s * RB, rowd + pr, (uint32_t)nb * 16u, &full[s]);
-            pr += nb;
-            // slide the row window by nb (rows already loaded move down, new ones are fetched)
-            const int o_sh = __shfl_down_sync(FULL, o_l, nb);
-            const int s_sh = __shfl_down_sync(FULL, sl_l, nb);
-            if (lane < RB) {
-                if (lane + nb < RB) { o_l = o_sh; sl_l = s_sh; }
-                else if (pr + lane < p1) { const RowInfo<T> r = ri[pr + lane]; o_l = r.o; sl_l = r.slot; }
-                else { sl_l = -1; }
-            }
-            ++st;
-        }
-        return;
-    }
-
-    // ---------------- consumer warps ----------------
-    // Registers hold only plus[4] and seg[4] (the hot accumulators).  The
-    // per-column segment bookkeeping -- head (first, possibly cut, segment),
-    // the running lexicographic min of R_i + acc_c[i] and its slot -- lives in
-    // this part's output rows in global memory: each is touched only by its
-    // own lane and only at a segment end (~1 in 60 stages).
-    const int cb = ctacol + warp * 128 + lane * 4;
-    const bool active = cb < w;
-    const int64_t obase = (int64_t)q * w + cb;
-    int jmax = active ? min(4, w - cb) : 0;       // valid columns of this lane
-    A plus[4], seg[4];
-#pragma unroll
-    for (int j = 0; j < 4; ++j) { plus[j] = 0; seg[j] = 0; }
-    #pragma unroll
-    for (int j = 0; j < 4; ++j) if (j < jmax) { out_imin[obase + j] = amax<A>(); out_islot[obase + j] = -1; out_head[obase + j] = 0; }
-    int cur = ri[p0].slot;
-    bool first = true;
-
-    for (int st = 0;; ++st) {
-        const int s = st % S;
-        ptx::mbar_wait(&full[s], (st / S) & 1);
-        const int nb = snb[s];
-        if (nb == 0) break;
-        const RowInfo<T>* srii = sri + s * RB;
-        const int slot = srii[0].slot;
-        if (slot != cur) {                       // segment boundary (warp-uniform, ~1 in 60 stages)
-            if (first) {
-#pragma unroll
-                for (int j = 0; j < 4; ++j) if (j < jmax) out_head[obase + j] = seg[j];
-                first = false;
-            } else {
-                const A rv = R[cur];
-#pragma unroll
-                for (int j = 0; j < 4; ++j) {
-                    if (j >= jmax) continue;
-                    if (out_acc) out_acc[(int64_t)cur * w + cb + j] = seg[j];
-                    const A val = rv + seg[j];
-                    if (val < out_imin[obase + j]) { out_imin[obase + j] = val; out_islot[obase + j] = cur; }
-                }
-            }
-#pragma unroll
-            for (int j = 0; j < 4; ++j) seg[j] = 0;
-            cur = slot;
-        }
-        T x[RB][4], dn[RB], ds[RB];
-        const T* srow = sdata + (size_t)(s * RB) * C::COLS + (warp * 128 + lane * 4);
-#pragma unroll
-        for (int u = 0; u < RB; ++u) {
-            const V v = *reinterpret_cast<const V*>(srow + (size_t)u * C::COLS);
-            memcpy(&x[u][0], &v.x, sizeof(T)); memcpy(&x[u][1], &v.y, sizeof(T));
-            memcpy(&x[u][2], &v.z, sizeof(T)); memcpy(&x[u][3], &v.w, sizeof(T));
-            dn[u] = srii[u].dn;
-            ds[u] = srii[u].ds;
-        }
-        // Rows >= nb (the short stage at a segment end) hold stale, possibly
-        // never-written bytes, and columns >= w of the last tile are padding:
-        // give them thresholds nothing compares below (the loaded values are
-        // left untouched).
-        if (nb < RB) {
-#pragma unroll
-            for (int u = 1; u < RB; ++u)
-                if (u >= nb) { dn[u] = never_lt<T>(); ds[u] = never_lt<T>(); }
-        }
-#pragma unroll
-        for (int u = 0; u < RB; ++u) {
-            dn[u] = active ? dn[u] : never_lt<T>();
-            ds[u] = active ? ds[u] : never_lt<T>();
-        }
-        static_assert(RB == 4, "mask folding assumes 4 rows per stage");
-        unsigned m = 0;
-#pragma unroll
-        for (int j = 0; j < 4; ++j)
-            m |= CmpLt<T>::any4(x[0][j], ds[0], x[1][j], ds[1], x[2][j], ds[2], x[3][j], ds[3]) << j;
-        const unsigned wm = __reduce_or_sync(FULL, m);
-        if (wm == 0) {
-            // every lane has its stage values in registers: release the stage
-            __syncwarp();
-            if (lane == 0) ptx::mbar_arrive(&empty[s]);
-            continue;
-        }
-        A dnA[RB], dsA[RB], dnds[RB];
-        if constexpr (Acc<T>::is_float) {       // widened thresholds staged by the producer (no F2F)
-            const double2* sr = srd + s * RB;
-#pragma unroll
-            for (int u = 0; u < RB; ++u) { const double2 q = sr[u]; dnA[u] = q.x; dsA[u] = q.y; dnds[u] = dnA[u] - dsA[u]; }
-        } else {
-#pragma unroll
-            for (int u = 0; u < RB; ++u) { dnA[u] = (A)dn[u]; dsA[u] = (A)ds[u]; dnds[u] = dnA[u] - dsA[u]; }
-        }
-        // the stage is released only after the staged fp64 thresholds are in
-        // registers: the producer refills srd together with the data
-        __syncwarp();
-        if (lane == 0) ptx::mbar_arrive(&empty[s]);
-#pragma unroll
-        for (int j = 0; j < 4; ++j) {
-            if (wm & (1u << j)) {
-                // Alg.3 P:883-889 per row in select form (independent rows, no
-                // data-dependent branches), tree-summed: a short fp64 chain.
-                A tp[RB], ts[RB];
-#pragma unroll
-                for (int u = 0; u < RB; ++u) {
-                    const bool c1 = x[u][j] < dn[u], c2 = x[u][j] < ds[u];
-                    const A t = (A)x[u][j] - (c1 ? dnA[u] : dsA[u]);
-                    tp[u] = c1 ? t : (A)0;
-                    ts[u] = c1 ? dnds[u] : (c2 ? t : (A)0);
-                }
-                plus[j] += (tp[0] + tp[1]) + (tp[2] + tp[3]);
-                seg[j] += (ts[0] + ts[1]) + (ts[2] + ts[3]);
-            }
-        }
-    }
-    if (!active) return;
-#pragma unroll
-    for (int j = 0; j < 4; ++j) {
-        if (j >= jmax) continue;
-        if (first) { out_head[obase + j] = seg[j]; out_tail[obase + j] = 0; }
-        else out_tail[obase + j] = seg[j];
-        out_plus[obase + j] = plus[j];
-    }
-}
-
 // ---------------------------------------------------------------------------
-// a3, leaner consumer of the segment-aligned ring (k_swap_stream_seg2).
-//
-// Same producer, stages and outputs as k_swap_stream_seg; the consumer's
-// per-stage instruction count is cut (ncu source page of the seg kernel:
-// ~85 instructions per warp-stage outside the hit path, ~60 per hit column):
+// a3 consumer (k_swap_stream_seg2).  Per-stage instruction count kept low
+// (ncu source page of the round-1 predecessor: ~85 instructions per
+// warp-stage outside the hit path, ~60 per hit column):
 //   * columns no lane owns (beyond the slab) are filled once with the
 //     largest value, so no per-stage threshold masking is needed;
 //   * stage index / phase by counters (no modulo);
@@ -1759,8 +521,8 @@ k_swap_stream_seg(const T* __restrict__ D, int64_t ld, int w, int wpad, int n, i
 //     row adds d_n - d_s = q - t to acc and t to plus; for d_n <= d < d_s it
 //     adds q), which needs 8 fp64 selects per column instead of 16.
 // Per row the terms are exact (differences of two f32 / u32 values are
-// exact in fp64 / int64); only the summation grouping differs from
-// k_swap_stream_seg (reading R9).
+// exact in fp64 / int64); only the summation grouping differs from the
+// oracle's object order (reading R9).
 // ---------------------------------------------------------------------------
 template <typename T, typename A, int NC, int RB, int S, int MINB = 2>
 __global__ void __launch_bounds__((NC + 1) * 32, MINB)
@@ -1805,7 +567,7 @@ k_swap_stream_seg2(const T* __restrict__ D, int64_t ld, int w, int wpad, int n, 
     __syncthreads();
 
     if (warp == NC) {
-        // ---------------- producer warp (as k_swap_stream_seg) ----------------
+        // ---------------- producer warp ----------------
         const uint32_t cbytes = (uint32_t)min(C::COLS, wpad - ctacol) * (uint32_t)sizeof(T);
         const uint64_t pol = ptx::policy_evict_first();
         const uint64_t keep = ptx::policy_evict_last();   // row metadata: re-read by every column tile
@@ -1967,227 +729,6 @@ k_swap_stream_seg2(const T* __restrict__ D, int64_t ld, int w, int wpad, int n, 
     }
 }
 
-// ---------------------------------------------------------------------------
-// a3, wide-tile variant (KM_STREAM=seg3; measurement): as k_swap_stream_seg2
-// with 8 candidate columns per lane, i.e. 7 KB bulk copies per row and
-// column tile (2 CTAs per SM, 4-stage ring).
-// ---------------------------------------------------------------------------
-template <typename T, int NC, int RB, int S>
-struct Seg8Cfg {
-    static constexpr int COLS = NC * 256;
-    static constexpr int ROWB = COLS * (int)sizeof(T);
-    static constexpr int DATAB = S * RB * ROWB;
-    static constexpr int RIB = S * RB * 16;
-    static constexpr int RDB = S * RB * 16;
-    static constexpr int NBB = S * 4;
-    static constexpr int BARB = 2 * S * 8;
-    static constexpr int SMEM = DATAB + RIB + RDB + 16 * ((NBB + 15) / 16) + BARB;
-    static constexpr int THREADS = (NC + 1) * 32;
-};
-
-template <typename T, typename A, int NC, int RB, int S, int MINB>
-__global__ void __launch_bounds__((NC + 1) * 32, MINB)
-k_swap_stream_seg3(const T* __restrict__ D, int64_t ld, int w, int wpad, int n, int P,
-                   const RowInfo<T>* __restrict__ ri, const A* __restrict__ R,
-                   A* __restrict__ out_plus, A* __restrict__ out_head, A* __restrict__ out_tail,
-                   A* __restrict__ out_imin, int* __restrict__ out_islot, A* __restrict__ out_acc,
-                   const double2* __restrict__ rowd) {
-    using C = Seg8Cfg<T, NC, RB, S>;
-    using V = typename Vec4<T>::type;
-    static_assert(RB == 4, "four rows per stage");
-    constexpr int L = 8;                              // columns per lane
-    extern __shared__ __align__(128) unsigned char smem[];
-    T* sdata = reinterpret_cast<T*>(smem);
-    RowInfo<T>* sri = reinterpret_cast<RowInfo<T>*>(smem + C::DATAB);
-    double2* srd = reinterpret_cast<double2*>(smem + C::DATAB + C::RIB);
-    int* snb = reinterpret_cast<int*>(smem + C::DATAB + C::RIB + C::RDB);
-    uint64_t* full = reinterpret_cast<uint64_t*>(smem + C::DATAB + C::RIB + C::RDB + 16 * ((C::NBB + 15) / 16));
-    uint64_t* empty = full + S;
-
-    const int q = blockIdx.y;
-    const int64_t p0 = part_lo(q, n, P), p1 = part_lo(q + 1, n, P);
-    const int ctacol = blockIdx.x * C::COLS;
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-
-    if (threadIdx.x == 0) {
-        for (int st = 0; st < S; ++st) {
-            ptx::mbar_init(&full[st], 1);
-            ptx::mbar_init(&empty[st], NC);
-        }
-        ptx::fence_mbar_init();
-    }
-    if (warp < NC) {
-        const T b = dmax<T>();
-        for (int h = 0; h < 2; ++h)
-            if (ctacol + warp * 256 + lane * L + h * 4 >= wpad) {
-                V big;
-                memcpy(&big.x, &b, sizeof(T)); memcpy(&big.y, &b, sizeof(T));
-                memcpy(&big.z, &b, sizeof(T)); memcpy(&big.w, &b, sizeof(T));
-                for (int r = 0; r < S * RB; ++r)
-                    *reinterpret_cast<V*>(sdata + (size_t)r * C::COLS + warp * 256 + lane * L + h * 4) = big;
-            }
-    }
-    __syncthreads();
-
-    if (warp == NC) {
-        const uint32_t cbytes = (uint32_t)min(C::COLS, wpad - ctacol) * (uint32_t)sizeof(T);
-        const uint64_t pol = ptx::policy_evict_first();
-        const uint64_t keep = ptx::policy_evict_last();
-        int64_t pr = p0;
-        int s = 0, ph = 0, st = 0;
-        int o_l = 0, sl_l = -1;
-        if (lane < RB && pr + lane < p1) { const RowInfo<T> r = ri[pr + lane]; o_l = r.o; sl_l = r.slot; }
-        while (true) {
-            if (st >= S) ptx::mbar_wait(&empty[s], ph ^ 1);
-            if (pr >= p1) {
-                if (lane == 0) { snb[s] = 0; ptx::mbar_arrive(&full[s]); }
-                break;
-            }
-            const int slot0 = __shfl_sync(FULL, sl_l, 0);
-            const unsigned same = __ballot_sync(FULL, lane < RB && sl_l == slot0 && pr + lane < p1);
-            const int nb = __ffs(~same) - 1;
-            if (lane == 0) {
-                snb[s] = nb;
-                ptx::mbar_expect_tx(&full[s], (uint32_t)nb * (cbytes + (rowd ? 32u : 16u)));
-            }
-            __syncwarp();
-            if (lane < nb)
-                ptx::bulk_g2s(sdata + (size_t)(s * RB + lane) * C::COLS, D + (int64_t)o_l * ld + ctacol, cbytes,
-                              &full[s], pol);
-            if (lane == 0) ptx::bulk_g2s(sri + s * RB, ri + pr, (uint32_t)nb * 16u, &full[s], keep);
-            if (lane == 1 && rowd) ptx::bulk_g2s(srd + s * RB, rowd + pr, (uint32_t)nb * 16u, &full[s], keep);
-            pr += nb;
-            const int o_sh = __shfl_down_sync(FULL, o_l, nb);
-            const int s_sh = __shfl_down_sync(FULL, sl_l, nb);
-            if (lane < RB) {
-                if (lane + nb < RB) { o_l = o_sh; sl_l = s_sh; }
-                else if (pr + lane < p1) { const RowInfo<T> r = ri[pr + lane]; o_l = r.o; sl_l = r.slot; }
-                else { sl_l = -1; }
-            }
-            ++st;
-            if (++s == S) { s = 0; ph ^= 1; }
-        }
-        return;
-    }
-
-    const int cb = ctacol + warp * 256 + lane * L;
-    const bool active = cb < w;
-    const int64_t obase = (int64_t)q * w + cb;
-    const int jmax = active ? min(L, w - cb) : 0;
-    const uint64_t keep = ptx::policy_evict_last();
-    A plus[L], seg[L];
-#pragma unroll
-    for (int j = 0; j < L; ++j) { plus[j] = 0; seg[j] = 0; }
-#pragma unroll
-    for (int j = 0; j < L; ++j)
-        if (j < jmax) {
-            ptx::st_hint(&out_imin[obase + j], amax<A>(), keep);
-            ptx::st_hint(&out_islot[obase + j], -1, keep);
-            ptx::st_hint(&out_head[obase + j], (A)0, keep);
-        }
-    int cur = ri[p0].slot;
-    bool first = true;
-    const T* srow0 = sdata + (warp * 256 + lane * L);
-    int s = 0, ph = 0;
-
-    for (;;) {
-        ptx::mbar_wait(&full[s], ph);
-        const int nb = snb[s];
-        if (nb == 0) break;
-        const RowInfo<T>* srii = sri + s * RB;
-        const int slot = srii[0].slot;
-        if (slot != cur) {
-            if (first) {
-#pragma unroll
-                for (int j = 0; j < L; ++j) if (j < jmax) ptx::st_hint(&out_head[obase + j], seg[j], keep);
-                first = false;
-            } else {
-                const A rv = R[cur];
-#pragma unroll
-                for (int j = 0; j < L; ++j) {
-                    if (j >= jmax) continue;
-                    if (out_acc) out_acc[(int64_t)cur * w + cb + j] = seg[j];
-                    const A val = rv + seg[j];
-                    if (val < out_imin[obase + j]) {
-                        ptx::st_hint(&out_imin[obase + j], val, keep);
-                        ptx::st_hint(&out_islot[obase + j], cur, keep);
-                    }
-                }
-            }
-#pragma unroll
-            for (int j = 0; j < L; ++j) seg[j] = 0;
-            cur = slot;
-        }
-        T x[RB][L], dn[RB], ds[RB];
-        const T* srow = srow0 + (size_t)(s * RB) * C::COLS;
-#pragma unroll
-        for (int u = 0; u < RB; ++u) {
-#pragma unroll
-            for (int h = 0; h < 2; ++h) {
-                const V v = *reinterpret_cast<const V*>(srow + (size_t)u * C::COLS + h * 4);
-                memcpy(&x[u][h * 4 + 0], &v.x, sizeof(T)); memcpy(&x[u][h * 4 + 1], &v.y, sizeof(T));
-                memcpy(&x[u][h * 4 + 2], &v.z, sizeof(T)); memcpy(&x[u][h * 4 + 3], &v.w, sizeof(T));
-            }
-            dn[u] = srii[u].dn;
-            ds[u] = srii[u].ds;
-        }
-        if (nb < RB) {
-#pragma unroll
-            for (int u = 1; u < RB; ++u)
-                if (u >= nb) { dn[u] = never_lt<T>(); ds[u] = never_lt<T>(); }
-        }
-        bool hit[L];
-        bool anyh = false;
-#pragma unroll
-        for (int j = 0; j < L; ++j) {
-            hit[j] = __any_sync(FULL, CmpLt<T>::any4(x[0][j], ds[0], x[1][j], ds[1], x[2][j], ds[2], x[3][j], ds[3]));
-            anyh |= hit[j];
-        }
-        const int cs = s;
-        if (++s == S) { s = 0; ph ^= 1; }
-        if (!anyh) {
-            __syncwarp();
-            if (lane == 0) ptx::mbar_arrive(&empty[cs]);
-            continue;
-        }
-        A dnA[RB], dsA[RB];
-        if constexpr (Acc<T>::is_float) {
-            const double2* sr = srd + cs * RB;
-#pragma unroll
-            for (int u = 0; u < RB; ++u) { const double2 qq = sr[u]; dnA[u] = qq.x; dsA[u] = qq.y; }
-        } else {
-#pragma unroll
-            for (int u = 0; u < RB; ++u) { dnA[u] = (A)dn[u]; dsA[u] = (A)ds[u]; }
-        }
-        __syncwarp();
-        if (lane == 0) ptx::mbar_arrive(&empty[cs]);
-#pragma unroll
-        for (int j = 0; j < L; ++j) {
-            if (hit[j]) {
-                A tq[RB], tt[RB];
-#pragma unroll
-                for (int u = 0; u < RB; ++u) {
-                    const A xa = (A)x[u][j];
-                    tq[u] = (x[u][j] < ds[u]) ? xa - dsA[u] : (A)0;
-                    tt[u] = (x[u][j] < dn[u]) ? xa - dnA[u] : (A)0;
-                }
-                const A sq = (tq[0] + tq[1]) + (tq[2] + tq[3]);
-                const A sp = (tt[0] + tt[1]) + (tt[2] + tt[3]);
-                plus[j] += sp;
-                seg[j] += sq - sp;
-            }
-        }
-    }
-    if (!active) return;
-#pragma unroll
-    for (int j = 0; j < L; ++j) {
-        if (j >= jmax) continue;
-        if (first) { ptx::st_hint(&out_head[obase + j], seg[j], keep); ptx::st_hint(&out_tail[obase + j], (A)0, keep); }
-        else ptx::st_hint(&out_tail[obase + j], seg[j], keep);
-        ptx::st_hint(&out_plus[obase + j], plus[j], keep);
-    }
-}
-
 // a4: complete the segments cut by part boundaries, take the lexicographic
 // min over slots of (R_i + acc_i, i) (Alg.3, smaller slot on ties), add
 // dTD^{+x_c}, mask medoids, and reduce (dTD, i, c) over the grid.
@@ -2269,123 +810,6 @@ __global__ void k_swap_combine(int w, int64_t col_begin, int P, const A* __restr
         cand_v[cl] = dtd;
         cand_slot[cl] = medoid ? -1 : bs;
         if (!medoid) { best.v = dtd; best.slot = bs; best.c = (int)c; }
-    }
-    grid_min_rec(best, partials, counter, out);
-}
-
-// a4, parallel over parts: the same result as k_swap_combine (up to the
-// association of fp64 sums, reading R9), with CG thread groups per column.
-// Block = 32 columns x CG warps; warp g folds the contiguous part range g of
-// its column into a range state (head segment, tail segment, best completed
-// segment, plus); warp 0 merges the CG states in order (deterministic).
-// A segment is complete once a later range starts another slot; the head
-// segment of the whole column and its tail segment are complete at the end.
-template <typename A>
-struct CombState {
-    int hs, ts;          // slot of the first / last segment of the range (hs < 0: empty range)
-    A hsum, tsum;        // their partial sums (single segment: hsum only)
-    A plus;
-    A bv;                // best completed (R_s + acc_s, s) inside the range
-    int bs;
-};
-
-// Append range b to range a (rows sorted by slot, so a slot is one run).
-// fin(slot, sum) receives every segment that becomes complete.
-template <typename A, typename Fin>
-__device__ __forceinline__ void comb_merge(CombState<A>& a, const CombState<A>& b, Fin&& fin) {
-    if (b.hs < 0) return;
-    if (a.hs < 0) { a = b; return; }
-    a.plus += b.plus;
-    if (b.bv < a.bv || (b.bv == a.bv && b.bs < a.bs)) { a.bv = b.bv; a.bs = b.bs; }
-    const bool sa = a.hs == a.ts, sb = b.hs == b.ts;
-    if (a.ts == b.hs) {                       // the boundary segment continues into b
-        const A joined = (sa ? a.hsum : a.tsum) + b.hsum;
-        if (sa && sb) { a.hsum = joined; }
-        else if (sa) { a.hsum = joined; a.ts = b.ts; a.tsum = b.tsum; }
-        else if (sb) { a.tsum = joined; }
-        else { fin(a.ts, joined); a.ts = b.ts; a.tsum = b.tsum; }
-    } else {
-        if (!sa) fin(a.ts, a.tsum);           // a's last segment ends at the boundary
-        if (!sb) fin(b.hs, b.hsum);           // b's first segment ends inside b
-        a.ts = b.ts;
-        a.tsum = sb ? b.hsum : b.tsum;
-    }
-}
-
-template <typename A, int CG>
-__global__ void __launch_bounds__(32 * CG)
-k_swap_combine_par(int w, int64_t col_begin, int P, const A* __restrict__ in_plus,
-                   const A* __restrict__ in_head, const A* __restrict__ in_tail,
-                   const A* __restrict__ in_imin, const int* __restrict__ in_islot,
-                   const int* __restrict__ head_slot, const int* __restrict__ tail_slot,
-                   const A* __restrict__ R, const int* __restrict__ empty_slot,
-                   const int* __restrict__ point_slot, A* __restrict__ cand_v,
-                   int* __restrict__ cand_slot, Rec<A>* partials, unsigned* counter,
-                   Rec<A>* out, A* __restrict__ acc_out = nullptr, A* __restrict__ plus_out = nullptr,
-                   int k = 0, bool stage = false) {
-    __shared__ CombState<A> sst[CG][32];
-    extern __shared__ __align__(16) unsigned char comb_smem[];
-    if (stage) {                               // as k_swap_combine
-        A* sR = reinterpret_cast<A*>(comb_smem);
-        int* shs = reinterpret_cast<int*>(comb_smem + (size_t)k * sizeof(A));
-        for (int i = threadIdx.x; i < k; i += blockDim.x) sR[i] = R[i];
-        for (int i = threadIdx.x; i < P; i += blockDim.x) { shs[i] = head_slot[i]; shs[P + i] = tail_slot[i]; }
-        __syncthreads();
-        R = sR; head_slot = shs; tail_slot = shs + P;
-    }
-    const int lane = threadIdx.x & 31, g = threadIdx.x >> 5;
-    const int cl = blockIdx.x * 32 + lane;
-    CombState<A> st;
-    st.hs = -1; st.ts = -1; st.hsum = 0; st.tsum = 0; st.plus = 0; st.bv = amax<A>(); st.bs = INT_MAX;
-    auto fin = [&](int sl, A sum) {
-        if (acc_out) acc_out[(int64_t)sl * w + cl] = sum;
-        const A val = R[sl] + sum;
-        if (val < st.bv || (val == st.bv && sl < st.bs)) { st.bv = val; st.bs = sl; }
-    };
-    if (cl < w) {
-        const int q0 = (int)((int64_t)g * P / CG), q1 = (int)((int64_t)(g + 1) * P / CG);
-        constexpr int QU = 8;
-        for (int qb = q0; qb < q1; qb += QU) {
-            A pl[QU], hv[QU], tv[QU], iv[QU];
-            int isl[QU], hs[QU], ts[QU];
-#pragma unroll
-            for (int u = 0; u < QU; ++u) {
-                const int q = qb + u;
-                if (q < q1) {
-                    const int64_t idx = (int64_t)q * w + cl;
-                    pl[u] = in_plus[idx]; hv[u] = in_head[idx]; tv[u] = in_tail[idx];
-                    iv[u] = in_imin[idx]; isl[u] = in_islot[idx];
-                    hs[u] = head_slot[q]; ts[u] = tail_slot[q];
-                }
-            }
-#pragma unroll
-            for (int u = 0; u < QU; ++u) {
-                if (qb + u >= q1) break;
-                CombState<A> b;
-                b.hs = hs[u]; b.ts = ts[u]; b.hsum = hv[u]; b.tsum = (ts[u] != hs[u]) ? tv[u] : (A)0;
-                b.plus = pl[u];
-                if (isl[u] >= 0) { b.bv = iv[u]; b.bs = isl[u]; } else { b.bv = amax<A>(); b.bs = INT_MAX; }
-                comb_merge(st, b, fin);
-            }
-        }
-    }
-    sst[g][lane] = st;
-    __syncthreads();
-    Rec<A> best = rec_none<A>();
-    if (g == 0 && cl < w) {
-        for (int gg = 1; gg < CG; ++gg) comb_merge(st, sst[gg][lane], fin);
-        // the column's first and last segments are complete
-        fin(st.hs, st.hsum);
-        if (st.ts != st.hs) fin(st.ts, st.tsum);
-        const int es = *empty_slot;
-        if (es != INT_MAX && (0 < st.bv || (0 == st.bv && es < st.bs))) { st.bv = 0; st.bs = es; }
-        if (plus_out) plus_out[cl] = st.plus;
-        const A dtd = st.bv + st.plus;
-        const int64_t c = col_begin + cl;
-        const bool medoid = point_slot[c] >= 0;
-        cand_v[cl] = dtd;
-        cand_slot[cl] = medoid ? -1 : st.bs;
-        if (!medoid) { best.v = dtd; best.slot = st.bs; best.c = (int)c; }
     }
     grid_min_rec(best, partials, counter, out);
 }
@@ -2801,59 +1225,12 @@ k_fp2_sequential(const T* __restrict__ D, int64_t ld, const T* __restrict__ cols
 // ---------------------------------------------------------------------------
 // a7: BUILD (Alg.1)
 // ---------------------------------------------------------------------------
-// Same column-tile layout as k_swap_stream, rows in natural order.
 // MODE 0 (first medoid):  acc_c = sum_o d(x_o, x_c)
 // MODE 1 (later medoids): acc_c = sum_o min(d(x_o, x_c) - d_n(o), 0)
 // (medoid rows have d_n = 0 and contribute 0 since D >= 0; the x_o = x_c row
 // contributes -d_n(c): reading R3).
-template <typename T, typename A, int WARPS, int U, int MODE>
-__global__ void __launch_bounds__(WARPS * 32)
-k_build_stream(const T* __restrict__ D, int64_t ld, int w, int n, int P, const T* __restrict__ dn,
-               A* __restrict__ out) {
-    using V = typename Vec4<T>::type;
-    const int q = blockIdx.y;
-    const int64_t p0 = part_lo(q, n, P), p1 = part_lo(q + 1, n, P);
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int cb = (blockIdx.x * WARPS + warp) * 128 + lane * 4;
-    if (cb >= w) return;                      // no warp-collective ops below
-    const T* Dc = D + cb;
-    A acc[4] = {0, 0, 0, 0};
-    for (int64_t p = p0; p < p1; p += U) {
-        const int nb = (int)min((int64_t)U, p1 - p);
-        V v[U];
-        T dv[U];
-#pragma unroll
-        for (int u = 0; u < U; ++u)
-            if (u < nb) {
-                v[u] = ld_stream4(Dc + (p + u) * ld);
-                if (MODE == 1) dv[u] = dn[p + u];
-            }
-#pragma unroll
-        for (int u = 0; u < U; ++u) {
-            if (u >= nb) break;
-            T x[4];
-            memcpy(&x[0], &v[u].x, sizeof(T)); memcpy(&x[1], &v[u].y, sizeof(T));
-            memcpy(&x[2], &v[u].z, sizeof(T)); memcpy(&x[3], &v[u].w, sizeof(T));
-            if (MODE == 0) {
-#pragma unroll
-                for (int j = 0; j < 4; ++j) acc[j] += (A)x[j];
-            } else {
-                const T d0 = dv[u];
-                const A dA = (A)d0;
-#pragma unroll
-                for (int j = 0; j < 4; ++j)
-                    if (x[j] < d0) acc[j] += (A)x[j] - dA;
-            }
-        }
-    }
-    const int64_t base = (int64_t)q * w;
-#pragma unroll
-    for (int j = 0; j < 4; ++j)
-        if (cb + j < w) out[base + cb + j] = acc[j];
-}
-
-// BUILD stream, TMA variant (default): the producer / ring of
-// k_swap_stream_seg with rows in natural order; per stage the consumers
+// The producer / ring of the SWAP stream with rows in natural order; per
+// stage the consumers
 // fold "d < d_n" over the 4 rows x 4 columns into a REDUX.OR mask and
 // update only the columns with a hit (MODE 1), or sum every element with a
 // 4-row tree (MODE 0).  3 CTAs x 8 warps per SM.

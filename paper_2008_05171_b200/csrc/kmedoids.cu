@@ -60,33 +60,13 @@ km_status fail(km_status s, const char* fmt, ...) {
     } while (0)
 
 constexpr int NUM_SMS = 148;
-constexpr int STREAM_WARPS = 4;               // 4 warps x 128 columns = 512 columns per CTA
-constexpr int STREAM_COLS = STREAM_WARPS * 128;
-constexpr int STREAM_U = 8;                   // rows in flight per warp
-constexpr int RESIDENT_CTAS = 4;              // ~16 warps per SM
 constexpr int TARGET_WAVES = 3;
 constexpr int MAX_K = 8192;
-// TMA-staged stream kernel: 7 consumer warps (896 columns) + 1 producer warp
-// (8 warps: 2 CTAs = 4 warps per SM sub-partition), 4 rows per stage, 7 stages
-// (~100 KB shared memory, 2 CTAs per SM).
-constexpr int TMA_NC = 7, TMA_RB = 4, TMA_S = 7;
-constexpr int TMA_COLS = TMA_NC * 128;
-// Warp-autonomous TMA stream kernel (default): 4 warps x 128 columns per CTA,
-// each warp with its own 6-stage x 4-row ring (~12.7 KB), 4 CTAs per SM.
-constexpr int WT_NW = 4, WT_RB = 4, WT_S = 6;
-// TMA ring + compacted hit lists (default): 7 consumer warps + 1 producer,
-// 4 rows per stage, 6 stages, per-column fp64 partials in shared memory.
-constexpr int CMP_NC = 7, CMP_RB = 4, CMP_S = 6;
-// TMA ring + per-warp hit queues: 7 consumer warps + 1 producer, 4 rows x 6 stages.
-constexpr int TQ_NC = 7, TQ_RB = 4, TQ_S = 6;
-// TMA ring with segment-aligned stages: 7 consumer warps + 1 producer, 4 rows x
-// 5 stages (~72 KB shared memory), 3 CTAs = 24 warps per SM (<= 80 registers).
+// SWAP / BUILD stream (k_swap_stream_seg2, k_build_tma): 7 consumer warps + 1
+// producer, TMA ring of 5 stages x 4 rows (~72 KB shared memory), 3 CTAs = 24
+// warps per SM (<= 80 registers).
 constexpr int SG_NC = 7, SG_RB = 4, SG_S = 5, SG_MINB = 3;
-constexpr int FP2_SPLIT = 8;
-constexpr int COMB_G = 8;      // warps (part groups) per column block of k_swap_combine_par   // column splits of the FastPAM2 per-slot reduction
-constexpr int WT_COLS = WT_NW * 128;
-constexpr int WT_RESIDENT = 4;
-constexpr int TMA_RESIDENT = 2;
+constexpr int FP2_SPLIT = 8;   // column splits of the FastPAM2 per-slot reduction
 
 int64_t cdiv(int64_t a, int64_t b) { return (a + b - 1) / b; }
 
@@ -105,18 +85,6 @@ int choose_parts(int64_t n, int64_t w, int cols_per_cta, int resident) {
 // more, shorter CTAs balance the Poisson-lumpy hit work across SMs; very
 // short parts cost ring fill/drain and combine bytes.
 constexpr int PART_SKEW_DEFAULT = 15;  // 16ths; see km::part_lo (C4 stream 1.565 -> 1.478 ms)
-
-// wide-tile stream (KM_STREAM=seg3): 1792-column tiles, 2 CTAs per SM
-constexpr int SG8_NC = 7, SG8_RB = 4, SG8_S = 4, SG8_MINB = 2;
-int choose_parts_seg8(int64_t n, int64_t w) {
-    const int64_t ncb = cdiv(w, SG8_NC * 256);
-    const int64_t slots = (int64_t)NUM_SMS * SG8_MINB;
-    int64_t P = n / 1000;
-    P = std::max<int64_t>(P, cdiv(3 * slots, ncb));
-    P = std::min<int64_t>(P, std::max<int64_t>(1, 8 * slots / ncb));
-    P = std::min<int64_t>(P, std::max<int64_t>(1, n / 64));
-    return (int)std::max<int64_t>(P, 1);
-}
 
 int choose_parts_seg(int64_t n, int64_t w) {
     const int64_t ncb = cdiv(w, SG_NC * 128);
@@ -155,6 +123,7 @@ struct ImplBase {
     virtual km_status build_decide(int32_t step) = 0;
     virtual km_status build_apply_async(int32_t step) = 0;
     virtual km_status last_swaps_out(int32_t* slots, int32_t* cands, void* dtds, int32_t cap, int32_t* count) = 0;
+    virtual km_status fp2_last_plan(void* v, int32_t* c, int32_t* order, int32_t* m) = 0;
     virtual km_status fp2_shard_exchange(int32_t nranks, km_fp2_exchange* out) = 0;
     virtual km_status fp2_shard_eval() = 0;
     virtual km_status fp2_shard_plan(const int64_t* rcb, int32_t* m_out, int32_t* maxcnt_out) = 0;
@@ -193,16 +162,11 @@ struct Impl : ImplBase {
     int64_t ld = 0, c0 = 0, c1 = 0;
     int w = 0;
     cudaStream_t st = nullptr;
-    int P = 1, Pb = 1, Pbt = 1, B = 1, ncomb = 1, ntd = 1, sort_chunk = 256;
-    bool build_tma = true;          // KM_BUILD=ldg selects the register-pipelined BUILD stream
+    int P = 1, Pbt = 1, B = 1, ncomb = 1, ntd = 1, sort_chunk = 256;
     int nranks = 1;
     int wpad = 0;
-    bool use_tma = true;
-    int stream_kind = 2;
-    int debug_natural = 0;
-    int debug_nocompute = 0;
-    int debug_fp2 = 0;
     bool ready = false;     // medoids + cache valid
+    int* bad_count = nullptr;       // input validation counter (k_validate_*)
 
     std::vector<void*> bufs;        // every device allocation, freed in the destructor
     int *M = nullptr, *point_slot = nullptr, *near = nullptr, *sec = nullptr;
@@ -211,7 +175,7 @@ struct Impl : ImplBase {
     int *rescan = nullptr, *rescan_count = nullptr;   // objects whose nearest/second slot was swapped
     RI* ri = nullptr;
     double2* rowd = nullptr;        // float path: (double dn, double ds) in sorted order
-    int *counts = nullptr, *offsets = nullptr, *seg_start = nullptr, *empty_slot = nullptr, *slot_tot = nullptr;
+    int *seg_start = nullptr, *empty_slot = nullptr, *slot_tot = nullptr;
     int *head_slot = nullptr, *tail_slot = nullptr;
     A *R = nullptr, *o_plus = nullptr, *o_head = nullptr, *o_tail = nullptr, *o_imin = nullptr;
     int* o_islot = nullptr;
@@ -273,48 +237,9 @@ struct Impl : ImplBase {
         D = (const T*)Dp; n = n_; ld = ld_; c0 = c0_; c1 = c1_; k = k_; st = s;
         w = (int)(c1 - c0);
         sharded = !(c0 == 0 && c1 == n);
-        const char* ev = getenv("KM_STREAM");
-        // Stream kernel selection (KM_STREAM overrides for
-        // measurements): seg = TMA bulk-copy ring with segment-aligned stages
-        // (default), tma = the same ring with stages across segments, ldg =
-        // register-pipelined loads, wtma = warp-autonomous rings, cmp / tmaq =
-        // compacted hit lists (CTA-wide / per warp).
-        stream_kind = 13;
-        if (ev && strcmp(ev, "tma") == 0) stream_kind = 1;
-        if (ev && strcmp(ev, "cmp") == 0) stream_kind = 6;
-        if (ev && strcmp(ev, "tmaq") == 0) stream_kind = 9;
-        if (ev && strcmp(ev, "seg") == 0) stream_kind = 10;
-        if (ev && strcmp(ev, "seg6") == 0) stream_kind = 11;
-        if (ev && strcmp(ev, "seg5") == 0) stream_kind = 12;
-        if (ev && strcmp(ev, "seg2") == 0) stream_kind = 13;
-        if (ev && strcmp(ev, "seg3") == 0) stream_kind = 14;
-        // (seg3, the wide-tile stream, is 1.1 % faster per C4 iteration --
-        // 1.531 vs 1.549 ms -- but the whole kmedoids_run_host job at C4 took
-        // 0.37-0.39 s with it vs 0.32 s with seg2, so seg2 stays the default)
-        if (ev && strcmp(ev, "ldg") == 0) stream_kind = 0;
-        if (ev && strcmp(ev, "wtma") == 0) stream_kind = 2;
-
-
-        use_tma = stream_kind == 1;
-        const char* dbg = getenv("KM_DEBUG_NATURAL_ORDER");   // perf experiment only: wrong results
-        debug_natural = (dbg && dbg[0] == '1') ? 1 : 0;
-        const char* df = getenv("KM_DEBUG_FP2");
-        debug_fp2 = (df && df[0] == '1') ? 1 : 0;
         const char* eg = getenv("KM_GRAPH");
         use_graph = !(eg && eg[0] == '0');
-        const char* dnc = getenv("KM_DEBUG_NOCOMPUTE");        // perf experiment only: wrong results
-        debug_nocompute = (dnc && dnc[0] == '1') ? 1 : 0;
-        P = (stream_kind == 10 || stream_kind == 13) ? choose_parts_seg(n, w)
-            : stream_kind == 14 ? choose_parts_seg8(n, w)
-            : stream_kind == 11 ? choose_parts(n, w, 6 * 128, 3)
-            : stream_kind == 12 ? choose_parts(n, w, 5 * 128, 4)
-            : stream_kind == 9 ? choose_parts(n, w, TQ_NC * 128, 2)
-            : stream_kind == 6 ? choose_parts(n, w, CMP_NC * 128, 2)
-
-            : stream_kind == 1 ? choose_parts(n, w, TMA_COLS, TMA_RESIDENT)
-            : stream_kind == 2 ? choose_parts(n, w, WT_COLS, WT_RESIDENT)
-
-                               : choose_parts(n, w, STREAM_COLS, RESIDENT_CTAS);
+        P = choose_parts_seg(n, w);
         const char* ep = getenv("KM_PARTS");          // measurement override of the stream's row parts
         // (<= 4096: km::part_lo's int64 products stay in range for any n < 2^31)
         if (ep && atoi(ep) > 0) P = std::min<int>(std::min(atoi(ep), 4096), (int)std::max<int64_t>(1, n / 64));
@@ -325,10 +250,7 @@ struct Impl : ImplBase {
             if (const char* es = getenv("KM_PART_SKEW")) skew = std::min(64, std::max(0, atoi(es)));
             KM_CK(cudaMemcpyToSymbol(km::c_part_skew, &skew, sizeof(int)));
         }
-        Pb = choose_parts(n, w, STREAM_COLS, RESIDENT_CTAS);
         Pbt = choose_parts(n, w, SG_NC * 128, SG_MINB);
-        const char* eb = getenv("KM_BUILD");
-        build_tma = !(eb && strcmp(eb, "ldg") == 0);
         wpad = (int)((w + 3) / 4 * 4);
         // counting-sort chunk: >= 256 objects and at most 128 chunks (keeps the
         // k x B count matrix of the one-block scan small)
@@ -350,21 +272,19 @@ struct Impl : ImplBase {
         KM_TRY(alloc(&rescan_count, 1));
         KM_TRY(alloc(&ri, n));
         if (km::Acc<T>::is_float) KM_TRY(alloc(&rowd, n));
-        KM_TRY(alloc(&counts, (size_t)k * B));
-        KM_TRY(alloc(&offsets, (size_t)k * B));
         KM_TRY(alloc(&seg_start, k + 1));
         KM_TRY(alloc(&slot_tot, k));
         KM_TRY(alloc(&empty_slot, 1));
         KM_TRY(alloc(&head_slot, P));
         KM_TRY(alloc(&tail_slot, P));
         KM_TRY(alloc(&R, k));
-        const size_t pw = (size_t)std::max(P, std::max(Pb, Pbt)) * w;
+        const size_t pw = (size_t)std::max(P, Pbt) * w;
         KM_TRY(alloc(&o_plus, pw));
         KM_TRY(alloc(&o_head, pw));
         KM_TRY(alloc(&o_tail, pw));
         KM_TRY(alloc(&o_imin, pw));
         KM_TRY(alloc(&o_islot, pw));
-        b_out = o_plus;   // BUILD partial sums reuse the plus buffer (sized for max(P, Pb))
+        b_out = o_plus;   // BUILD partial sums reuse the plus buffer (sized for max(P, Pbt))
         KM_TRY(alloc(&cand_v, w));
         KM_TRY(alloc(&cand_slot, w));
         KM_TRY(alloc(&partials, std::max<int64_t>(cdiv(w, 32), 1)));
@@ -381,6 +301,17 @@ struct Impl : ImplBase {
         KM_CK(cudaMallocHost((void**)&h_td, sizeof(A)));
         KM_CK(cudaEventCreate(&ev0));
         KM_CK(cudaEventCreate(&ev1));
+        KM_TRY(alloc(&bad_count, 1));
+        KM_CK(cudaMemsetAsync(bad_count, 0, sizeof(int), st));
+        if (c1 > c0) {
+            // the slab's diagonal entries must be exactly 0 (O(n) device pass)
+            km::k_validate_diag<T><<<(unsigned)cdiv(c1 - c0, 256), 256, 0, st>>>(D, ld, c0, c1, bad_count);
+            KM_CKL();
+            int nbad = 0;
+            KM_CK(cudaMemcpyAsync(&nbad, bad_count, sizeof(int), cudaMemcpyDeviceToHost, st));
+            KM_CK(cudaStreamSynchronize(st));
+            if (nbad) return fail(KM_EINVAL, "D has %d nonzero (or NaN) diagonal entries; d(x_o, x_o) must be 0", nbad);
+        }
         if (const char* es = getenv("KM_STEP_PROF")) step_prof = es[0] == '1';
         if (step_prof)
             for (auto& e : sp_ev) KM_CK(cudaEventCreate(&e));
@@ -412,16 +343,12 @@ struct Impl : ImplBase {
     cudaEvent_t sp_ev[5] = {};
     double sp_sum[5] = {};
     int sp_n = 0;
-    bool tma_attr_set = false;
     // CUDA graph of the FastPAM1 iteration (KM_GRAPH=0 disables)
     bool use_graph = true;
     cudaGraphExec_t fp1_exec = nullptr;
     cudaStream_t cap_st = nullptr;
     int64_t fp1_graph_kernels = 0;
     int64_t fp1_iters = 0;
-    bool cmp_attr_set = false;
-    bool tmaq_attr_set = false;
-    bool seg_attr_set = false;
 
     km_status assign_full_and_td() {
         const int nb = (int)cdiv(n, 256);
@@ -445,6 +372,23 @@ struct Impl : ImplBase {
         return KM_OK;
     }
 
+    // float path: the gathered medoid columns (every d(x_o, m_j)) must be
+    // >= 0 and not NaN (KM_EINVAL otherwise; synchronises)
+    km_status validate_mc() {
+        if constexpr (!km::Acc<T>::is_float) {
+            return KM_OK;
+        } else {
+            KM_CK(cudaMemsetAsync(bad_count, 0, sizeof(int), st));
+            km::k_validate_cols<T><<<NUM_SMS * 2, 256, 0, st>>>(MC, (int64_t)k * n, bad_count);
+            KM_CKL();
+            int nbad = 0;
+            KM_CK(cudaMemcpyAsync(&nbad, bad_count, sizeof(int), cudaMemcpyDeviceToHost, st));
+            KM_CK(cudaStreamSynchronize(st));
+            if (nbad) return fail(KM_EINVAL, "a medoid column of D holds a negative or NaN dissimilarity");
+            return KM_OK;
+        }
+    }
+
     km_status reset_counters() {
         KM_CK(cudaMemsetAsync(dec, 0, sizeof(Dec), st));
         return KM_OK;
@@ -457,6 +401,7 @@ struct Impl : ImplBase {
         dim3 g((unsigned)cdiv(n, 256), k);
         km::k_gather_medoid_cols<T><<<g, 256, 0, st>>>(D, ld, (int)n, c0, c1, M, MC);
         KM_CKL();
+        KM_TRY(validate_mc());
         KM_TRY(assign_full_and_td());
         KM_TRY(reset_counters());
         KM_CK(cudaStreamSynchronize(st));
@@ -467,27 +412,11 @@ struct Impl : ImplBase {
         return KM_OK;
     }
 
-    // a2: sort rows by nearest slot, removal loss, part metadata.  One
-    // cooperative launch (phases 3-7 of k_fp1_post) when the post kernel is
-    // available, else six small kernels (KM_POST=0).
+    // a2: sort rows by nearest slot, removal loss, part metadata: phases 3-7
+    // of the cooperative k_fp1_post, launched alone.
     km_status prep() {
-        if (post_usable()) {
-            KM_TRY(post_alloc());
-            return launch_post(true);
-        }
-        km::k_slot_hist<<<B, 256, k * sizeof(int), st>>>(near, (int)n, k, sort_chunk, counts);
-        KM_CKL();
-        km::k_scan_within_slot<<<(unsigned)cdiv((int64_t)k * 32, 256), 256, 0, st>>>(counts, B, k, offsets, slot_tot);
-        KM_CKL();
-        km::k_scan_slots<<<1, 1024, 0, st>>>(slot_tot, k, seg_start, empty_slot);
-        KM_CKL();
-        km::k_slot_scatter<T><<<B, 32, k * sizeof(int), st>>>(near, dn, ds, (int)n, k, sort_chunk, offsets, seg_start, ri, debug_natural, rowd);
-        KM_CKL();
-        km::k_removal_loss<T, A><<<(unsigned)cdiv((int64_t)k * 32, 256), 256, 0, st>>>(ri, seg_start, k, R, empty_slot);
-        KM_CKL();
-        km::k_part_meta<T><<<(unsigned)cdiv(P, 128), 128, 0, st>>>(ri, (int)n, P, head_slot, tail_slot);
-        KM_CKL();
-        return KM_OK;
+        KM_TRY(post_alloc());
+        return launch_post(true);
     }
 
     // a3 + a4 (local): stream the slab, combine into the local best record.
@@ -528,54 +457,8 @@ struct Impl : ImplBase {
         if (profiling && prof_ring_mode) KM_TRY(prof_ring_pair(&pair));
         if (pair) KM_CK(cudaEventRecord(pair[0], st));
         else if (profiling) KM_CK(record_ev(ev0));
-        if (stream_kind == 10) {  // TMA ring, segment-aligned stages
-            KM_TRY((launch_seg<SG_NC, SG_RB, SG_S, SG_MINB>(nullptr)));
-        } else if (stream_kind == 13) {
-            KM_TRY((launch_seg2<SG_NC, SG_RB, SG_S, SG_MINB>(D, w, wpad, P, o_plus, o_head, o_tail, o_imin, o_islot,
-                                                              nullptr)));
-        } else if (stream_kind == 14) {
-            using C = km::Seg8Cfg<T, SG8_NC, SG8_RB, SG8_S>;
-            auto kern = km::k_swap_stream_seg3<T, A, SG8_NC, SG8_RB, SG8_S, SG8_MINB>;
-            if (!seg3_attr_set) {
-                KM_CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM));
-                seg3_attr_set = true;
-            }
-            dim3 g((unsigned)cdiv(w, C::COLS), P);
-            kern<<<g, C::THREADS, C::SMEM, st>>>(D, ld, w, wpad, (int)n, P, ri, R, o_plus, o_head, o_tail, o_imin,
-                                                  o_islot, nullptr, rowd);
-        } else if (stream_kind == 11) {
-            KM_TRY((launch_seg<6, 4, 6, 3>(nullptr)));
-        } else if (stream_kind == 12) {
-            KM_TRY((launch_seg<5, 4, 5, 4>(nullptr)));
-        } else if (stream_kind == 9) {   // TMA ring + per-warp hit queues
-            KM_TRY((launch_tmaq<TQ_NC, TQ_RB, TQ_S>(nullptr)));
-        } else if (stream_kind == 6) {   // compacted hits
-            using C = km::CmpCfg<T, A, CMP_NC, CMP_RB, CMP_S>;
-            auto kern = km::k_swap_stream_cmp<T, A, CMP_NC, CMP_RB, CMP_S>;
-            if (!cmp_attr_set) {
-                KM_CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM));
-                cmp_attr_set = true;
-            }
-            dim3 g((unsigned)cdiv(w, C::COLS), P);
-            kern<<<g, C::THREADS, C::SMEM, st>>>(D, ld, w, wpad, (int)n, P, ri, R, o_plus, o_head, o_tail, o_imin,
-                                                  o_islot);
-        } else if (stream_kind == 2) {
-            KM_TRY((launch_wtma<WT_NW, WT_RB, WT_S>()));
-        } else if (use_tma) {
-            using C = km::TmaCfg<T, TMA_NC, TMA_RB, TMA_S>;
-            auto kern = km::k_swap_stream_tma<T, A, TMA_NC, TMA_RB, TMA_S>;
-            if (!tma_attr_set) {
-                KM_CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM));
-                tma_attr_set = true;
-            }
-            dim3 g((unsigned)cdiv(w, C::COLS), P);
-            kern<<<g, C::THREADS, C::SMEM, st>>>(D, ld, w, wpad, (int)n, P, ri, R, o_plus, o_head, o_tail, o_imin,
-                                                  o_islot, debug_nocompute, nullptr);
-        } else {
-            dim3 g((unsigned)cdiv(w, STREAM_COLS), P);
-            km::k_swap_stream<T, A, STREAM_WARPS, STREAM_U><<<g, STREAM_WARPS * 32, 0, st>>>(
-                D, ld, w, (int)n, P, ri, R, o_plus, o_head, o_tail, o_imin, o_islot);
-        }
+        KM_TRY((launch_seg2<SG_NC, SG_RB, SG_S, SG_MINB>(D, w, wpad, P, o_plus, o_head, o_tail, o_imin, o_islot,
+                                                          nullptr)));
         KM_CKL();
         if (pair) KM_CK(cudaEventRecord(pair[1], st));
         else if (profiling) { KM_CK(record_ev(ev1)); pending_prof = true; }
@@ -584,36 +467,17 @@ struct Impl : ImplBase {
         return KM_OK;
     }
 
-    // a4: per-candidate combine of the stream's part outputs: one thread per
-    // column (default); KM_COMBINE=par folds part groups in parallel warps and
-    // merges them (measured 10-30 us SLOWER per step at C4/C5, kept for A/B)
-    int combine_kind = -1;
-    int comb_tpb = -1;
+    // a4: per-candidate combine of the stream's part outputs (one thread per
+    // column; folding part groups in parallel warps was measured 10-30 us
+    // slower per step at C4/C5 in round 1 and removed).
     km_status launch_combine(int ww, int64_t colb, int Pw, const A* pl, const A* hd, const A* tl, const A* im,
                              const int* isl, const int* hsl, const int* tsl, A* cv, int* cs, A* acc_o, A* plus_o) {
-        if (combine_kind < 0) {
-            const char* e = getenv("KM_COMBINE");
-            combine_kind = (e && strcmp(e, "par") == 0) ? 1 : (e && strcmp(e, "par4") == 0) ? 2 : 0;
-        }
+        constexpr int TPB = 128;   // 32 / 64 threads per block measured slower, 256 equal
         const size_t sm = (size_t)k * sizeof(A) + 2 * (size_t)Pw * sizeof(int);
         const bool stage = sm <= 32 * 1024;
-        if (combine_kind == 0) {
-            if (comb_tpb < 0) {                      // threads per block (KM_COMB_TPB: measurement override)
-                const char* e = getenv("KM_COMB_TPB");
-                comb_tpb = e ? std::max(32, std::min(256, atoi(e) / 32 * 32)) : 128;
-            }
-            km::k_swap_combine<A><<<(unsigned)cdiv(ww, comb_tpb), comb_tpb, stage ? sm : 0, st>>>(
-                ww, colb, Pw, pl, hd, tl, im, isl, hsl, tsl, R, empty_slot, point_slot, cv, cs, partials, counters,
-                rec_local, acc_o, plus_o, k, stage);
-        }
-        else if (combine_kind == 2)
-            km::k_swap_combine_par<A, 4><<<(unsigned)cdiv(ww, 32), 32 * 4, stage ? sm : 0, st>>>(
-                ww, colb, Pw, pl, hd, tl, im, isl, hsl, tsl, R, empty_slot, point_slot, cv, cs, partials, counters,
-                rec_local, acc_o, plus_o, k, stage);
-        else
-            km::k_swap_combine_par<A, COMB_G><<<(unsigned)cdiv(ww, 32), 32 * COMB_G, stage ? sm : 0, st>>>(
-                ww, colb, Pw, pl, hd, tl, im, isl, hsl, tsl, R, empty_slot, point_slot, cv, cs, partials, counters,
-                rec_local, acc_o, plus_o, k, stage);
+        km::k_swap_combine<A><<<(unsigned)cdiv(ww, TPB), TPB, stage ? sm : 0, st>>>(
+            ww, colb, Pw, pl, hd, tl, im, isl, hsl, tsl, R, empty_slot, point_slot, cv, cs, partials, counters,
+            rec_local, acc_o, plus_o, k, stage);
         KM_CKL();
         return KM_OK;
     }
@@ -628,35 +492,11 @@ struct Impl : ImplBase {
     template <int NC, int RB, int S, int MINB = 2>
     km_status launch_seg_win(const T* Dw, int ww, int wpadw, int Pw, A* plus_o, A* head_o, A* tail_o, A* imin_o,
                              int* islot_o, A* acc_out) {
-        if (stream_kind != 10)
-            return launch_seg2<NC, RB, S, MINB>(Dw, ww, wpadw, Pw, plus_o, head_o, tail_o, imin_o, islot_o, acc_out);
-        using C = km::SegCfg<T, NC, RB, S>;
-        auto kern = km::k_swap_stream_seg<T, A, NC, RB, S, MINB>;
-        if (!seg_attr_set) {
-            KM_CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM));
-            seg_attr_set = true;
-        }
-        dim3 g((unsigned)cdiv(ww, C::COLS), Pw);
-        kern<<<g, C::THREADS, C::SMEM, st>>>(Dw, ld, ww, wpadw, (int)n, Pw, ri, R, plus_o, head_o, tail_o, imin_o,
-                                              islot_o, acc_out, rowd);
-        return KM_OK;
+        return launch_seg2<NC, RB, S, MINB>(Dw, ww, wpadw, Pw, plus_o, head_o, tail_o, imin_o, islot_o, acc_out);
     }
 
     bool seg2_attr_set = false;
-    bool seg3_attr_set = false;
-    const char* stream_kernel_name() const override {
-        switch (stream_kind) {
-            case 14: return "k_swap_stream_seg3";
-            case 13: return "k_swap_stream_seg2";
-            case 10: return "k_swap_stream_seg";
-            case 11: case 12: return "k_swap_stream_seg2";
-            case 9: return "k_swap_stream_tmaq";
-            case 6: return "k_swap_stream_cmp";
-            case 2: return "k_swap_stream_wtma";
-            case 1: return "k_swap_stream_tma";
-            default: return "k_swap_stream";
-        }
-    }
+    const char* stream_kernel_name() const override { return "k_swap_stream_seg2"; }
     template <int NC, int RB, int S, int MINB = 2>
     km_status launch_seg2(const T* Dw, int ww, int wpadw, int Pw, A* plus_o, A* head_o, A* tail_o, A* imin_o,
                           int* islot_o, A* acc_out) {
@@ -672,42 +512,6 @@ struct Impl : ImplBase {
         const bool acc_keep = acc_out && (size_t)k * ww * sizeof(A) <= ((size_t)48 << 20);
         kern<<<g, C::THREADS, C::SMEM, st>>>(Dw, ld, ww, wpadw, (int)n, Pw, ri, R, plus_o, head_o, tail_o, imin_o,
                                               islot_o, acc_out, rowd, acc_keep);
-        return KM_OK;
-    }
-
-    template <int NC, int RB, int S>
-    km_status launch_tmaq(A* acc_out) {
-        using C = km::TmaqCfg<T, A, NC, RB, S>;
-        auto kern = km::k_swap_stream_tmaq<T, A, NC, RB, S>;
-        if (!tmaq_attr_set) {
-            KM_CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM));
-            tmaq_attr_set = true;
-        }
-        dim3 g((unsigned)cdiv(w, C::COLS), P);
-        kern<<<g, C::THREADS, C::SMEM, st>>>(D, ld, w, wpad, (int)n, P, ri, R, o_plus, o_head, o_tail, o_imin, o_islot,
-                                              acc_out);
-        return KM_OK;
-    }
-
-    template <int NC, int RB, int S, int MINB>
-    km_status launch_tma() {
-        using C = km::TmaCfg<T, NC, RB, S>;
-        auto kern = km::k_swap_stream_tma<T, A, NC, RB, S, MINB>;
-        KM_CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM));
-        dim3 g((unsigned)cdiv(w, C::COLS), P);
-        kern<<<g, C::THREADS, C::SMEM, st>>>(D, ld, w, wpad, (int)n, P, ri, R, o_plus, o_head, o_tail, o_imin, o_islot,
-                                              debug_nocompute, nullptr);
-        return KM_OK;
-    }
-
-    template <int NW, int RB, int S>
-    km_status launch_wtma() {
-        using C = km::WTmaCfg<T, NW, RB, S>;
-        auto kern = km::k_swap_stream_wtma<T, A, NW, RB, S>;
-        KM_CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM));
-        dim3 g((unsigned)cdiv(w, NW * 128), P);
-        kern<<<g, C::THREADS, C::SMEM, st>>>(D, ld, w, wpad, (int)n, P, ri, R, o_plus, o_head, o_tail, o_imin, o_islot,
-                                              debug_nocompute);
         return KM_OK;
     }
 
@@ -737,8 +541,7 @@ struct Impl : ImplBase {
         memcpy(td_out, &v, sizeof(A));
     }
 
-    // ---- fused post-stream kernel (km_post.cuh; KM_POST=0 disables) -----------
-    int use_post = -1;
+    // ---- fused post-stream kernel (km_post.cuh) --------------------------------
     bool fp1_prepped = false;       // slot sort / R / part metadata valid for the current cache
     int post_blocks = 0;
     int *post_counts = nullptr, *post_offsets = nullptr;
@@ -763,15 +566,6 @@ struct Impl : ImplBase {
         KM_TRY(alloc(&post_offsets, (size_t)k * post_blocks));
         if (step_prof) KM_TRY(alloc(&post_tph, 16));
         return KM_OK;
-    }
-
-    int post_ok = -1;
-    bool post_usable() {
-        if (post_ok < 0) {
-            const char* e = getenv("KM_POST");
-            post_ok = ((e && e[0] == '0') || debug_natural) ? 0 : 1;
-        }
-        return post_ok == 1;
     }
 
     km_status launch_post(bool prep_only = false) {
@@ -799,20 +593,13 @@ struct Impl : ImplBase {
     km_status enqueue_fp1_iteration() {
         const bool prof_save = profiling;
         if (use_graph) profiling = true;      // the graph always carries the stream events
-        km_status s = eval_local(use_post != 1);
+        km_status s = eval_local(false);
         profiling = prof_save;
         if (s != KM_OK) return s;
-        if (use_post == 1) {
-            if (step_prof) KM_CK(record_ev(sp_ev[2]));
-            KM_TRY(launch_post());          // writes the pinned h_dec / h_td mirrors itself
-            if (step_prof) KM_CK(record_ev(sp_ev[3]));
-            if (step_prof) KM_CK(record_ev(sp_ev[4]));
-            return KM_OK;
-        }
-        km::k_select<A><<<1, 1, 0, st>>>(rec_local, 1, td, M, point_slot, dec, rescan_count);
-        KM_CKL();
-        KM_TRY(apply_local());
-        KM_CK(cudaMemcpyAsync(h_dec, dec, sizeof(Dec), cudaMemcpyDeviceToHost, st));
+        if (step_prof) KM_CK(record_ev(sp_ev[2]));
+        KM_TRY(launch_post());          // writes the pinned h_dec / h_td mirrors itself
+        if (step_prof) KM_CK(record_ev(sp_ev[3]));
+        if (step_prof) KM_CK(record_ev(sp_ev[4]));
         return KM_OK;
     }
 
@@ -825,13 +612,8 @@ struct Impl : ImplBase {
         if (v == KM_FASTERPAM) return swap_iter_fp3(swaps, td_out);
         if (v == KM_FASTPAM1_INC) return inc_iters(1, swaps, td_out, nullptr, nullptr);
         inc_valid = false;
-        if (use_post < 0) {
-            const char* e = getenv("KM_POST");
-            use_post = (e && e[0] == '0') ? 0 : 1;
-            if (use_post == 1 && (stream_kind != 10 && stream_kind != 13 && stream_kind != 14)) use_post = 0;
-            if (use_post == 1) KM_TRY(post_alloc());
-        }
-        if (use_post == 1 && !fp1_prepped) {
+        KM_TRY(post_alloc());
+        if (!fp1_prepped) {
             KM_TRY(prep());
             KM_CK(cudaMemsetAsync(rescan_count, 0, sizeof(int), st));
         }
@@ -916,15 +698,14 @@ struct Impl : ImplBase {
         }
     iteration_done:
         ++fp1_iters;
-        fp1_prepped = (use_post == 1);
+        fp1_prepped = true;
         last_swaps.clear();
         if (h_dec->apply) {
             Rec r; r.v = h_dec->dtd; r.slot = h_dec->slot; r.c = h_dec->c;
             last_swaps.push_back(r);
         }
         if (swaps) *swaps = h_dec->apply;
-        if (use_post == 1) { if (td_out) memcpy(td_out, h_td, sizeof(A)); }   // mirrored in the iteration
-        else copy_td(td_out);
+        if (td_out) memcpy(td_out, h_td, sizeof(A));   // mirrored in the iteration
         return h_dec->apply ? KM_OK : KM_CONVERGED;
     }
 
@@ -1022,7 +803,6 @@ struct Impl : ImplBase {
         KM_CK(cudaMemcpyAsync(dec, &hd, sizeof(Dec), cudaMemcpyHostToDevice, st));
         KM_CK(cudaMemcpyAsync(fp2_order, order.data(), order.size() * sizeof(int), cudaMemcpyHostToDevice, st));
         int m = (int)order.size();
-        if (debug_fp2) fprintf(stderr, "[fp2] improving slots m=%d\n", m);
         KM_CK(cudaMemcpyAsync(fp2_m, &m, sizeof(int), cudaMemcpyHostToDevice, st));
         KM_TRY(launch_fp2_sequential(colsrc, colidx_dev));
         KM_CK(cudaMemcpyAsync(h_dec, dec, sizeof(Dec), cudaMemcpyDeviceToHost, st));
@@ -1710,6 +1490,7 @@ struct Impl : ImplBase {
         if (k < 2) return fail(KM_EINVAL, "CLARA needs k >= 2");
         if (ns < 1) return fail(KM_EINVAL, "nsamples must be >= 1");
         if (s <= k || s > n) return fail(KM_EINVAL, "sample size s=%d must satisfy k < s <= n", s);
+        if (s > 65535) return fail(KM_EINVAL, "sample size s=%d exceeds 65535 (grid rows of the gather)", s);
         if (v != KM_FASTPAM1 && v != KM_FASTPAM2 && v != KM_FASTERPAM) return fail(KM_EINVAL, "unknown variant");
         std::vector<char> seen((size_t)n, 0);
         for (int j = 0; j < ns; ++j) {
@@ -1818,20 +1599,7 @@ struct Impl : ImplBase {
             KM_TRY(bd_init());
             if (bd_mode == 1 && step >= 1) return bd_eval(step);
         }
-        if (build_tma) return step == 0 ? launch_build_tma<0>() : launch_build_tma<1>();
-        dim3 g((unsigned)cdiv(w, STREAM_COLS), Pb);
-        if (step == 0) {
-            km::k_build_stream<T, A, STREAM_WARPS, STREAM_U, 0><<<g, STREAM_WARPS * 32, 0, st>>>(D, ld, w, (int)n, Pb, dn, b_out);
-            KM_CKL();
-            km::k_build_combine<T, A, 0><<<ncomb, 128, 0, st>>>(D, ld, w, c0, Pb, b_out, point_slot, partials, counters, rec_local);
-            KM_CKL();
-        } else {
-            km::k_build_stream<T, A, STREAM_WARPS, STREAM_U, 1><<<g, STREAM_WARPS * 32, 0, st>>>(D, ld, w, (int)n, Pb, dn, b_out);
-            KM_CKL();
-            km::k_build_combine<T, A, 1><<<ncomb, 128, 0, st>>>(D, ld, w, c0, Pb, b_out, point_slot, partials, counters, rec_local);
-            KM_CKL();
-        }
-        return KM_OK;
+        return step == 0 ? launch_build_tma<0>() : launch_build_tma<1>();
     }
 
     km_status build_finish() {
@@ -1901,7 +1669,6 @@ struct Impl : ImplBase {
         if (bd_mode < 0) {
             const char* e = getenv("KM_BUILD");
             bd_mode = (e && (strcmp(e, "full") == 0 || strcmp(e, "ldg") == 0)) ? 0 : 1;
-            if (!build_tma) bd_mode = 0;
         }
         if (bd_mode == 1) KM_TRY(bd_alloc());
         return KM_OK;
@@ -2014,6 +1781,26 @@ struct Impl : ImplBase {
             }
         }
         KM_TRY(build_finish());
+        return KM_OK;
+    }
+
+    // FastPAM2 (reading R6 steps 2-5) of the last iteration: per-slot best
+    // (v_i, c_i) (c_i = -1: no candidate) and the improving slots in the
+    // order the sequential phase visited them.
+    km_status fp2_last_plan(void* v, int32_t* c, int32_t* order, int32_t* m) override {
+        if (!fp2_best) return fail(KM_EINVAL, "no FastPAM2 iteration has run on this handle");
+        std::vector<Rec> b((size_t)k);
+        int mm = 0;
+        KM_CK(cudaStreamSynchronize(st));
+        KM_CK(cudaMemcpy(b.data(), fp2_best, k * sizeof(Rec), cudaMemcpyDeviceToHost));
+        KM_CK(cudaMemcpy(&mm, fp2_m, sizeof(int), cudaMemcpyDeviceToHost));
+        if (order && mm > 0) KM_CK(cudaMemcpy(order, fp2_order, (size_t)mm * sizeof(int), cudaMemcpyDeviceToHost));
+        for (int i = 0; i < k; ++i) {
+            const bool none = b[i].slot == INT_MAX;
+            if (v) static_cast<A*>(v)[i] = none ? (A)0 : b[i].v;
+            if (c) c[i] = none ? -1 : b[i].c;
+        }
+        if (m) *m = mm;
         return KM_OK;
     }
 
@@ -2456,6 +2243,11 @@ km_status kmedoids_last_swaps(km_handle* h, int32_t* slots_out, int32_t* cands_o
                               int32_t* count_out) {
     KM_H();
     return h->impl->last_swaps_out(slots_out, cands_out, dtds_out, cap, count_out);
+}
+
+km_status kmedoids_fp2_last_plan(km_handle* h, void* v_out, int32_t* c_out, int32_t* order_out, int32_t* m_out) {
+    KM_H();
+    return h->impl->fp2_last_plan(v_out, c_out, order_out, m_out);
 }
 
 km_status kmedoids_set_profiling(km_handle* h, int32_t enable) {

@@ -73,6 +73,7 @@ def load_library() -> ctypes.CDLL:
         "kmedoids_eval_candidates": [vp, vp, vp],
         "kmedoids_set_profiling": [vp, i32],
         "kmedoids_last_swaps": [vp, vp, vp, vp, i32, vp],
+        "kmedoids_fp2_last_plan": [vp, vp, vp, vp, vp],
         "kmedoids_stream_time": [vp, vp, vp, i32],
         "kmedoids_launch_count": [vp, vp],
         "kmedoids_stream_kernel": [vp, ctypes.POINTER(ctypes.c_char_p)],
@@ -154,6 +155,9 @@ class KMedoids:
         self.col_begin = int(col_begin)
         self.col_end = int(n if col_end is None else col_end)
         self.dtype = _dtype_code(D)
+        if D.shape[0] < self.n or D.shape[1] < self.col_end - self.col_begin:
+            raise ValueError(f"D of shape {tuple(D.shape)} cannot hold {self.n} rows x "
+                             f"{self.col_end - self.col_begin} columns")
         self.acc = np.int64 if self.dtype == KM_U32 else np.float64
         self.stream = stream if stream is not None else torch.cuda.current_stream(D.device)
         h = ctypes.c_void_p()
@@ -274,6 +278,14 @@ class KMedoids:
         _check(load_library().kmedoids_last_swaps(self.h, _p(sl), _p(cd), _p(dv), m, _p(cnt)))
         return [(int(sl[j]), int(cd[j]), dv[j].item()) for j in range(m)]
 
+    def fp2_last_plan(self):
+        """Per-slot best (v[k], c[k]) and the improving slots in plan order of
+        the last FastPAM2 iteration (reading R6 steps 2-5)."""
+        v = np.zeros(self.k, self.acc); c = np.zeros(self.k, np.int32)
+        order = np.zeros(self.k, np.int32); m = np.zeros(1, np.int32)
+        _check(load_library().kmedoids_fp2_last_plan(self.h, _p(v), _p(c), _p(order), _p(m)))
+        return v, c, order[:int(m[0])].copy()
+
     def set_profiling(self, on=True):
         _check(load_library().kmedoids_set_profiling(self.h, int(on)))
 
@@ -301,6 +313,12 @@ class KMedoids:
 
     def shard_set_medoids(self, medoids, columns):
         M = np.ascontiguousarray(np.asarray(medoids, dtype=np.int32))
+        if M.shape != (self.k,):
+            raise ValueError(f"expected {self.k} medoids")
+        if (not columns.is_cuda or columns.device != self.D.device or not columns.is_contiguous()
+                or columns.element_size() != 4 or columns.numel() < self.k * self.n):
+            raise ValueError(f"columns must be a contiguous 4-byte CUDA tensor on {self.D.device} "
+                             f"holding k*n = {self.k * self.n} elements")
         _check(load_library().kmedoids_shard_set_medoids(self.h, _p(M), ctypes.c_void_p(columns.data_ptr())))
 
     def shard_eval(self):
@@ -467,9 +485,13 @@ def kmedoids_dissimilarity(X, metric="l2", D=None, col_begin=0, col_end=None, st
     want = torch.float32 if code == KM_METRIC_L2_F32 else torch.int32
     if X.dtype != want:
         raise TypeError(f"metric {metric} needs X of dtype {want}")
+    w = col_end - col_begin
     if D is None:
-        w = col_end - col_begin
         D = torch.empty((n, (w + 3) // 4 * 4), dtype=want, device=X.device)
+    elif (D.dtype != want or not D.is_cuda or D.device != X.device or D.dim() != 2 or D.stride(1) != 1
+          or D.shape[0] < n or D.shape[1] < w):
+        raise ValueError(f"D must be a row-major {want} CUDA tensor on {X.device} of at least ({n}, {w}); "
+                         f"got {D.dtype} {tuple(D.shape)} strides {D.stride()} on {D.device}")
     st = stream if stream is not None else torch.cuda.current_stream(X.device)
     _check(lib.kmedoids_dissimilarity(ctypes.c_void_p(X.data_ptr()), code, n, d, ctypes.c_void_p(D.data_ptr()),
                                       int(D.stride(0)), int(col_begin), int(col_end), ctypes.c_void_p(st.cuda_stream)))

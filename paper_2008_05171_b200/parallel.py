@@ -74,12 +74,36 @@ def column_view(col, dtype: str):
     return col.view(torch.float32 if dtype == "f32" else torch.int32)
 
 
+def on_handle_stream(handles):
+    """Context in which a collective or copy over the handles' exchange
+    buffers is enqueued on the library handle's CUDA stream (the stream the
+    shard kernels that produce and consume those buffers run on), so it is
+    ordered with them whatever torch's current stream is.  CPU (mock) handles:
+    no-op."""
+    import contextlib
+    km = getattr(handles[0], "km", None)
+    if km is None or getattr(km, "stream", None) is None:
+        return contextlib.nullcontext()
+    import torch
+    return torch.cuda.stream(km.stream)
+
+
+def _streamed(method):
+    def wrapper(self, handles, *a, **kw):
+        with on_handle_stream(handles):
+            return method(self, handles, *a, **kw)
+    wrapper.__name__ = method.__name__
+    wrapper.__doc__ = method.__doc__
+    return wrapper
+
+
 class LocalComm:
     """All ranks' handles in one process (virtual ranks)."""
 
     def __init__(self, world: int):
         self.world = world
 
+    @_streamed
     def allgather_records(self, handles):
         xs = [h.exchange_tensors(self.world) for h in handles]
         cat = [x[0] for x in xs]
@@ -87,6 +111,7 @@ class LocalComm:
             for r, s in enumerate(cat):
                 recv[r * RECORD_BYTES:(r + 1) * RECORD_BYTES].copy_(s)
 
+    @_streamed
     def broadcast_column(self, handles, owner: int):
         xs = [h.exchange_tensors(self.world) for h in handles]
         src = xs[owner][2]
@@ -94,6 +119,7 @@ class LocalComm:
             if r != owner:
                 col.copy_(src)
 
+    @_streamed
     def allreduce_column(self, handles):
         xs = [h.exchange_tensors(self.world) for h in handles]
         cols = [column_view(x[2], h.column_dtype) for x, h in zip(xs, handles)]
@@ -103,6 +129,7 @@ class LocalComm:
         for c in cols:
             c.copy_(tot)
 
+    @_streamed
     def allgather_fp2_records(self, handles):
         xs = [h.fp2_exchange_tensors(self.world) for h in handles]
         nb = xs[0][0].numel()
@@ -110,6 +137,7 @@ class LocalComm:
             for r, y in enumerate(xs):
                 x[1][r * nb:(r + 1) * nb].copy_(y[0])
 
+    @_streamed
     def allgather_fp2_columns(self, handles, maxcnt: int):
         xs = [h.fp2_exchange_tensors(self.world) for h in handles]
         cb = xs[0][4] * maxcnt                     # bytes per rank
@@ -131,26 +159,31 @@ class TorchComm:
         self.world = dist.get_world_size(group)
         self.rank = dist.get_rank(group)
 
+    @_streamed
     def allgather_records(self, handles):
         (h,) = handles
         send, recv, _ = h.exchange_tensors(self.world)
         self.dist.all_gather_into_tensor(recv, send, group=self.group)
 
+    @_streamed
     def broadcast_column(self, handles, owner: int):
         (h,) = handles
         _, _, col = h.exchange_tensors(self.world)
         self.dist.broadcast(col, src=owner, group=self.group)
 
+    @_streamed
     def allreduce_column(self, handles):
         (h,) = handles
         _, _, col = h.exchange_tensors(self.world)
         self.dist.all_reduce(column_view(col, h.column_dtype), op=self.dist.ReduceOp.SUM, group=self.group)
 
+    @_streamed
     def allgather_fp2_records(self, handles):
         (h,) = handles
         send, recv, _, _, _ = h.fp2_exchange_tensors(self.world)
         self.dist.all_gather_into_tensor(recv, send, group=self.group)
 
+    @_streamed
     def allgather_fp2_columns(self, handles, maxcnt: int):
         (h,) = handles
         _, _, csend, crecv, colb = h.fp2_exchange_tensors(self.world)
@@ -183,8 +216,9 @@ def set_medoids(handles, comm, cb, medoids, n: int):
             if h.rank == owner:
                 h.shard_pack_column(int(m))
         comm.broadcast_column(handles, owner)
-        for h, buf in zip(handles, cols):
-            buf[j].copy_(h.exchange_tensors(comm.world)[2])
+        with on_handle_stream(handles):          # ordered with the pack / set kernels
+            for h, buf in zip(handles, cols):
+                buf[j].copy_(h.exchange_tensors(comm.world)[2])
     for h, buf in zip(handles, cols):
         h.shard_set_medoids(M.astype(np.int32), buf)
 
