@@ -99,7 +99,7 @@ def compare_trace(Dt, n, M0, gpu, ref, td0, exact):
     td = td0
     for j, (gs, rs) in enumerate(zip(gpu, ref)):
         (gi, gc, gv), (ri, rc, rv) = gs, rs
-        if (gi, gc) == (ri, rc):
+        if (int(gi), int(gc)) == (int(ri), int(rc)):
             assert close(gv, rv, td, exact), (j, gs, rs)
         else:
             assert not exact, f"swap {j}: GPU {gs} vs oracle {rs}"
@@ -197,7 +197,7 @@ def check_plans(Dt, n, g_iters, gpu_iters, plans, exact):
             assert np.allclose(v, p["v"], rtol=0, atol=REL * abs(td)), it
             assert c.tolist() == p["c"], it
             assert order.tolist() == p["order"], it
-            assert [s[:2] for s in sws] == [s[:2] for s in gi["swaps"]], it
+            assert [list(s[:2]) for s in sws] == [list(s[:2]) for s in gi["swaps"]], it
             assert np.allclose([s[2] for s in sws], [s[2] for s in gi["swaps"]], rtol=0, atol=REL * abs(td)), it
 
 
