@@ -266,9 +266,16 @@ def run_ours(args):
     torch.cuda.synchronize()
     with ClockSampler(0) as clk:
         ev[2].record(stream)
-        for _ in range(args.steps):
-            conv, sw, td = km.swap_iter(args.variant)
-            swaps += sw
+        if args.variant == "fastpam1":
+            # K iterations queued back to back (kmedoids_swap_iters: the product's
+            # run path; each is a full pass, the host reads each outcome)
+            conv, done, swaps, td = km.swap_iters(args.steps)
+            if done != args.steps:
+                raise SystemExit(f"converged after {done} of {args.steps} timed steps; use fewer --steps")
+        else:
+            for _ in range(args.steps):
+                conv, sw, td = km.swap_iter(args.variant)
+                swaps += sw
         ev[3].record(stream)
         torch.cuda.synchronize()
     total_ms = ev[2].elapsed_time(ev[3])
@@ -544,9 +551,42 @@ def run_sharded(args):
                "job": f"every rank: H2D of its {Dh.nbytes / 1e9:.2f} GB slab (pinned) + {cfg.init} init + {it} SWAP "
                       f"iterations to convergence + D2H of medoids/assignment/TD; max over ranks",
                "seconds": e2e_s, "n_iter": it, "td": st.td}
+    cpu = None
+    if rank == 0 and not args.no_cpu_baseline:
+        # the oracle on this host, one core, on a bounded sample of the same
+        # workload's candidates (columns of rank 0's slab, state after the run)
+        st0 = h.km.get_state() if e2e is None else st
+        own = np.arange(int(cb[0]), int(cb[1]))
+
+        def rows(idx):
+            loc = torch.as_tensor(np.asarray(idx, np.int64) - int(cb[0]), device=Dt.device)
+            t = Dt[:, loc].T.contiguous().cpu().numpy()
+            return t.view(np.uint32) if t.dtype == np.int32 else t
+        medoid_rows = kmsynth.dist_numpy(X, cfg.metric, 0, n)[st0.medoids] if n <= 20000 else None
+        if medoid_rows is None:
+            medoid_rows = np.stack([kmsynth.dist_numpy(X, cfg.metric, int(m), int(m) + 1)[:, 0] for m in st0.medoids])
+        import oracle
+        cache = oracle.assign_cols(np.ascontiguousarray(medoid_rows))
+        R = oracle.removal_loss(cache, k)
+        pool = np.setdiff1d(own, st0.medoids)
+        cand = np.random.default_rng(7).choice(pool, size=min(200, len(pool)), replace=False)
+        C = rows(cand)
+        t0 = time.perf_counter()
+        for j in range(len(cand)):
+            oracle.fastpam1_candidate_col(C[j], cache, R)
+        used = time.perf_counter() - t0
+        cores, model = host_info()
+        cpu = {"value": len(cand) * k / used, "unit": "pair-evals/s", "cores": 1, "kind": "oracle",
+               "sample": f"{len(cand)} oracle candidate evaluations (Alg.3 P:879-891 over all n={n} objects and "
+                         f"k={k} slots) on rank 0 after the run, 1 thread, {used:.1f} s",
+               "host_cores": cores, "cpu_model": model}
     if rank == 0:
         peak, peak_kind = measured_peaks()
         slab_bytes = 4.0 * n * (int(cb[1]) - int(cb[0]))
+        ct = committed_traffic(cfg.name) or {}
+        traffic = None
+        if ct.get("traffic_bytes"):
+            traffic = ct["traffic_bytes"] / (4.0 * n * (n - k)) * slab_bytes
         k1_avg = k1_ms / max(1, k1_n)
         ach = slab_bytes / (k1_avg / 1e3) / 1e9
         line = {"metric": "swap_pair_evals_per_s", "value": value, "unit": "pair-evals/s", "n_gpus": world,
@@ -558,11 +598,50 @@ def run_sharded(args):
                            "l2": "inputs larger than L2, no flush needed"},
                 "s_per_iteration": ms_step / 1e3,
                 "roofline": {"bound": "hbm", "achieved": ach, "peak": peak, "unit": "GB/s", "frac": ach / peak,
-                             "traffic": None, "kernel": "k_swap_stream_seg2 (rank 0 slab)", "kernel_ms": k1_avg,
+                             "traffic": traffic,
+                             "traffic_source": (f"{ct.get('source')} (1-GPU launch) scaled to the rank-0 slab"
+                                                if traffic else None),
+                             "kernel": "k_swap_stream_seg2 (rank 0 slab)", "kernel_ms": k1_avg,
                              "alg_bytes_per_launch": slab_bytes, "peak_kind": peak_kind},
                 "gpu_launches": launches, "clocks": clk.summary(), "init": {"kind": cfg.init, "s": init_s},
-                "e2e": e2e, "cpu_baseline": None}
+                "e2e": e2e, "cpu_baseline": cpu}
         print(json.dumps(line), flush=True)
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def _free_port() -> int:
+    import socket
+    with socket.socket() as so:
+        so.bind(("127.0.0.1", 0))
+        return so.getsockname()[1]
+
+
+def relaunch(n: int):
+    """`bench.py --gpus N` started without torchrun: run the same command as N
+    ranks (one per GPU) through torch.distributed.run on 127.0.0.1, with NCCL's
+    INFO log (communicator / rank lines) on, and exit with its status."""
+    env = dict(os.environ)
+    env.setdefault("NCCL_DEBUG", "INFO")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr", "127.0.0.1", "--master-port", str(_free_port()), os.path.abspath(__file__),
+           *sys.argv[1:]]
+    sys.stdout.flush()
+    r = subprocess.run(cmd, env=env)
+    sys.exit(r.returncode)
+
+
+def launcher_selftest(args):
+    """The N-rank launch path without GPUs: every rank joins a gloo group and
+    contributes 1 to an all-reduce; rank 0 prints what it saw."""
+    import torch
+    import torch.distributed as dist
+    dist.init_process_group("gloo")
+    t = torch.ones(1)
+    dist.all_reduce(t)
+    if dist.get_rank() == 0:
+        print(json.dumps({"launcher_selftest": True, "n_gpus": args.gpus, "world_size": dist.get_world_size(),
+                          "ranks_seen": int(t.item()), "nccl_debug": os.environ.get("NCCL_DEBUG")}), flush=True)
     dist.barrier()
     dist.destroy_process_group()
 
@@ -583,8 +662,14 @@ def main():
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
     ap.add_argument("--cpu-candidates", type=int, default=2000)
     ap.add_argument("--ref-candidates", type=int, default=400)
+    ap.add_argument("--launcher-selftest", action="store_true",
+                    help="only check the N-rank launch (gloo, CPU): rank 0 prints the world it saw")
     args = ap.parse_args()
-    if args.impl == "reference":
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        relaunch(args.gpus)                      # does not return
+    if args.launcher_selftest:
+        launcher_selftest(args)
+    elif args.impl == "reference":
         run_reference(args)
     else:
         run_ours(args)

@@ -135,6 +135,17 @@ km_status kmedoids_clara(km_handle* h, int32_t nsamples, int32_t s, const int32_
  * Single GPU only. */
 km_status kmedoids_swap_iter(km_handle* h, km_variant variant, int32_t* swaps_done_out, void* td_out);
 
+/* Up to `count` FastPAM1 iterations (Alg.3), each exactly one
+ * kmedoids_swap_iter(KM_FASTPAM1), enqueued back to back: the next iteration
+ * is queued on the device while the host reads the outcome of the current one
+ * (a pass without an improving swap makes every pass queued behind it a
+ * no-op), so no host round trip separates iterations.  Stops after the first
+ * non-improving pass (counted).  iters_out / swaps_out: passes
+ * and swaps done by this call; td_out (int64_t* or double*) the TD after
+ * them; any may be NULL.  Returns KM_CONVERGED if the last pass made no swap,
+ * else KM_OK.  kmedoids_run uses the same path for KM_FASTPAM1.  Single GPU. */
+km_status kmedoids_swap_iters(km_handle* h, int32_t count, int32_t* iters_out, int32_t* swaps_out, void* td_out);
+
 /* BUILD (if use_build) or the medoids already set, then SWAP iterations until
  * convergence or max_iter passes (max_iter <= 0 means 2000).  Outputs are
  * host arrays (any may be NULL): medoids_out[k], assignment_out[n] (slot of
@@ -156,6 +167,12 @@ km_status kmedoids_run_host(const void* D_host, km_dtype dtype, int64_t n, int64
                             int32_t max_iter, void* cuda_stream, int32_t* medoids_out,
                             int32_t* assignment_out, void* td_out, int32_t* n_iter_out,
                             int32_t* n_swaps_out);
+
+/* kmedoids_run_host keeps its device copy of D between calls (one buffer per
+ * process, reused while large enough, so repeated jobs pay no allocation);
+ * this frees it.  Safe to call at any time from any thread; KM_OK if there
+ * was nothing to free. */
+km_status kmedoids_release_host_cache(void);
 
 /* Copy the current state to host arrays (any may be NULL): medoids[k],
  * assignment[n], td, counters.  Synchronises the stream. */

@@ -369,3 +369,57 @@ def clara(D: np.ndarray, k: int, samples, variant: str = "fastpam1"):
         if best is None or t < best[0]:
             best = (t, j, M)
     return best
+
+
+def td_points(X: np.ndarray, metric: str, M):
+    """TD over all objects from the points (Eq. eqn:td; reading C2): metric
+    "l2" (float32 X, d = f32 Euclidean, fp64 sum) or "l1" (int32 X, int64).
+    Returns (TD, per-object minimum, assignment slot)."""
+    M = _i32(M)
+    n, d = X.shape
+    asg = np.zeros(n, np.int32)
+    if metric == "l2":
+        Xc = np.ascontiguousarray(X, dtype=np.float32)
+        mins = np.zeros(n, np.float64)
+        f = _load().oracle_td_points_l2
+        f.restype = ctypes.c_double
+    else:
+        Xc = np.ascontiguousarray(X, dtype=np.int32)
+        mins = np.zeros(n, np.int64)
+        f = _load().oracle_td_points_l1
+        f.restype = ctypes.c_int64
+    t = f(_ptr(Xc), ctypes.c_int32(n), ctypes.c_int32(d), _ptr(M), ctypes.c_int32(len(M)), _ptr(mins), _ptr(asg))
+    return t, mins, asg
+
+
+def sub_dissimilarity(X: np.ndarray, metric: str, S) -> np.ndarray:
+    """The sample's dissimilarity matrix from its points by the definitions:
+    l2 -> float32 of the fp64 Euclidean distance (oracle.dist_l2), l1 ->
+    uint32 of the int64 Manhattan distance (oracle.dist_l1)."""
+    S = np.asarray(S, np.int64)
+    if metric == "l2":
+        return dist_l2(np.ascontiguousarray(X[S], dtype=np.float32)).astype(np.float32)
+    D = dist_l1(np.ascontiguousarray(X[S], dtype=np.int32))
+    if D.size and D.max() > np.iinfo(np.uint32).max:
+        raise ValueError("L1 distances exceed uint32")
+    return D.astype(np.uint32)
+
+
+def clara_points(X: np.ndarray, metric: str, k: int, samples, variant: str = "fastpam1"):
+    """FastCLARA without the n x n matrix (P:414-419, P:1109-1129, P:618-620;
+    reading C2): for every caller-drawn sample S, PAM (BUILD, Alg.1, then
+    FastPAM1 Alg.3 or FasterPAM Alg.4) on the sample's dissimilarity matrix
+    computed from its points, medoids mapped back to point indices, TD over
+    ALL n objects from the points (td_points); the smallest (TD, sample index)
+    wins.  Returns (TD, best sample index, medoids, assignment of all n)."""
+    best = None
+    for j, S in enumerate(samples):
+        S = np.asarray(S, np.int64)
+        Dj = sub_dissimilarity(X, metric, S)
+        Mb, _, _ = build_init(Dj, k)
+        r = swap_run(Dj, Mb, FASTPAM1) if variant == "fastpam1" else fasterpam_run(Dj, Mb)
+        M = S[r.medoids].astype(np.int32)
+        t, _, asg = td_points(X, metric, M)
+        if best is None or t < best[0]:
+            best = (t, j, M, asg)
+    return best

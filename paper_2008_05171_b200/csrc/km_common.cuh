@@ -71,6 +71,17 @@ template <typename A> struct alignas(16) Decision {
     int32_t old_m;   // medoid that left slot i*
     int32_t iters;   // passes so far
     int32_t swaps;   // swaps so far
+    int32_t done;    // FastPAM1: a pass found no improving swap; later passes are no-ops
+};
+
+// One FastPAM1 iteration's outcome, written by the post kernel into a pinned
+// host ring (slot = launch sequence number % ring size), so the host can keep
+// iterations queued ahead of the one whose outcome it reads.
+template <typename A> struct alignas(16) IterMirror {
+    Decision<A> d;
+    A td;
+    int32_t seq;
+    int32_t noop;    // queued behind a converged pass: nothing ran
 };
 
 // Row parts of the SWAP / BUILD streams: part q of P covers slot-sorted

@@ -508,6 +508,7 @@ struct SegCfg {
     static constexpr int THREADS = (NC + 1) * 32;
 };
 
+
 // ---------------------------------------------------------------------------
 // a3 consumer (k_swap_stream_seg2).  Per-stage instruction count kept low
 // (ncu source page of the round-1 predecessor: ~85 instructions per
@@ -530,10 +531,12 @@ k_swap_stream_seg2(const T* __restrict__ D, int64_t ld, int w, int wpad, int n, 
                    const RowInfo<T>* __restrict__ ri, const A* __restrict__ R,
                    A* __restrict__ out_plus, A* __restrict__ out_head, A* __restrict__ out_tail,
                    A* __restrict__ out_imin, int* __restrict__ out_islot, A* __restrict__ out_acc,
-                   const double2* __restrict__ rowd, bool acc_keep = false) {
+                   const double2* __restrict__ rowd, bool acc_keep, const int* __restrict__ skip_if) {
     using C = SegCfg<T, NC, RB, S>;
     using V = typename Vec4<T>::type;
     static_assert(RB == 4, "four rows per stage");
+    // a queued FastPAM1 iteration after convergence (Decision::done): no-op
+    if (skip_if && __ldcg(skip_if)) return;
     extern __shared__ __align__(128) unsigned char smem[];
     T* sdata = reinterpret_cast<T*>(smem);
     RowInfo<T>* sri = reinterpret_cast<RowInfo<T>*>(smem + C::DATAB);

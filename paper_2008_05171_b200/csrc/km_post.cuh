@@ -2,26 +2,33 @@
 // cooperative kernel (SURVEY 8(a) rows a4 (accept), a5 (apply + cache
 // update) and a2 (slot sort, removal loss) for the NEXT iteration).
 //
-// The launch list of the default bench (profiles/r1d_launches_summary.md)
-// shows the non-stream part of a C4 step as ten small kernels (select,
-// column gather, incremental update, rescan, histogram, two scans, scatter,
-// removal loss, part metadata), each latency-bound, plus a launch gap each.
-// Here they are phases of one kernel separated by grid syncs (~1.2 us each,
-// measured; 4 of them when a swap is applied), with the same arithmetic and
-// the same deterministic orders:
-//   0 select    lexicographic min of the gathered records, acceptance R5
-//               (every block; block 0 records M / point_slot / TD / dec after
-//               the next sync that follows phase 0)     -- as k_select
-//   1 apply     MC[i*] <- column c*; incremental nearest/second for the
-//               block's chunk of objects and its histogram of the new
-//               nearest slots; objects whose nearest/second was slot i* listed
-//   2 rescan    warp per listed object, (d, slot) top-2, added to its chunk's
-//               histogram                                -- as k_assign_rescan
-//   3 histogram per block chunk (only without a swap / prep only)
-//   4 scan      warp per slot over its chunk counts; slot totals
-//   5 scan      every block: exclusive scan of the totals -> segment starts
-//   6 scatter   stable (slot, o) order, warp-ranked        -- as k_slot_scatter
-//   7 R, parts  removal loss per slot (fixed tree), empty slot, part heads/tails
+// Block b owns the objects of one contiguous chunk [ob0, ob1).  Three phases
+// separated by TWO grid syncs:
+//   A  select   lexicographic min of the gathered records, acceptance R5
+//               (every block decides identically)           -- Alg.3
+//      apply    MC[i*] <- column c* for the chunk; incremental nearest /
+//               second (O(1) per object); the chunk's objects
+//               whose nearest or second was slot i* are rescanned by the
+//               block's own warps (top-2 over the k medoid columns; the new
+//               column of those objects was written by this block, so no
+//               grid sync is needed); the result equals a from-scratch
+//               assignment (reading R2)
+//      count    per slot: the chunk's object count and its partial removal
+//               loss sum (ds - dn) (int64: exact, float: fp64 in
+//               object order within the chunk)
+//   -- grid sync --
+//   B  scan     warp per slot: exclusive scan of the chunk counts -> chunk
+//               offsets, slot total; R_i = fixed-order tree over the chunk
+//               partials; empty slot (block 0 records the decision: M,
+//               point_slot, TD, dec)
+//   -- grid sync --
+//   C  scatter  every block scans the slot totals into its shared memory
+//               (segment starts), places its chunk in stable (slot, o) order
+//               (warp-ranked), and the part head / tail slots come from a
+//               binary search of the segment starts (no pass over the rows).
+// All orders are fixed: deterministic; exact on int64 (reading R9 for float).
+// Round 1's version had four grid syncs (separate rescan, slot-scan and
+// removal-loss phases) and a global rescan list.
 #pragma once
 #include "km_kernels.cuh"
 
@@ -46,10 +53,11 @@ struct PostArgs {
     T* MC;
     int *near, *sec;
     T *dn, *ds;
-    int* rescan;
-    int* rescan_count;       // 0 on entry; reset to 0 on exit
+    int* rescan;             // [n]: block b lists its rescans in [ob0, ob1)
+    int* rescan_count;       // reset to 0 on exit (shared with the unfused kernels)
     int* counts;             // [k][gridDim]
     int* offsets;            // [k][gridDim]
+    A* rpart;                // [k][gridDim] partial removal losses
     int* slot_tot;           // [k]
     int* seg_start;          // [k+1]
     int* empty_slot;
@@ -58,9 +66,10 @@ struct PostArgs {
     A* R;
     int P;
     int *head_slot, *tail_slot;
-    int prep_only;             // 1: phases 3-7 only (slot sort, R, parts of the current cache)
-    Decision<A>* h_dec;        // pinned host mirrors written at the end (or null)
-    A* h_td;
+    int prep_only;             // 1: phases count, B, C only (slot sort, R, parts of the current cache)
+    IterMirror<A>* h_ring;     // pinned host ring of iteration outcomes (or null)
+    int ring;                  // its size
+    int* seq;                  // device counter of FastPAM1 post launches (ring slot = seq % ring)
     unsigned long long* tph;   // measurement aid (KM_STEP_PROF): globaltimer after each phase, or null
 };
 
@@ -72,34 +81,59 @@ __device__ __forceinline__ void post_stamp(unsigned long long* tph, int i) {
     }
 }
 
-template <typename T>
-__device__ __forceinline__ RowInfo<T> post_ld_ri(const RowInfo<T>* p) {
-    const int4 v = __ldcg(reinterpret_cast<const int4*>(p));
-    RowInfo<T> r;
-    memcpy(&r, &v, sizeof(r));
-    return r;
-}
-
 template <typename T, typename A>
-__global__ void __launch_bounds__(POST_THREADS)
+__global__ void __launch_bounds__(POST_THREADS, 3)
 k_fp1_post(PostArgs<T, A> g) {
     namespace cg = cooperative_groups;
     cg::grid_group grid = cg::this_grid();
-    extern __shared__ int post_smem[];           // k ints: histogram / scatter cursors
+    // dynamic shared memory: k ints (histogram, later segment starts /
+    // scatter cursors) then k A's (partial removal losses), 16-byte aligned
+    extern __shared__ __align__(16) unsigned char post_smem_raw[];
+    int* hh = reinterpret_cast<int*>(post_smem_raw);
+    A* pr = reinterpret_cast<A*>(post_smem_raw + (((size_t)g.k * sizeof(int) + 15) / 16) * 16);
     __shared__ Decision<A> sdec;
-    const int lane = threadIdx.x & 31;
+    __shared__ int s_nres;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int tid = blockIdx.x * blockDim.x + threadIdx.x, nth = gridDim.x * blockDim.x;
     const int gwarp = tid >> 5, nwarps = nth >> 5;
     const int n = g.n, k = g.k, B = gridDim.x, b = blockIdx.x;
     post_stamp(g.tph, 0);
 
     Decision<A> d{};
-    // block b owns the objects [ob0, ob1) in the apply and histogram phases
+    if (!g.prep_only) {
+        // a previous pass converged (sticky): this queued iteration is a no-op
+        // (the stream kernel returned at once); record the unchanged outcome.
+        // Every block reads dec here, before block 0 may write it (after a
+        // grid sync), so the exit is grid-uniform.
+        if (__ldcg(&g.dec->done)) {
+            if (b == 0 && threadIdx.x == 0) {
+                Decision<A> dd = *g.dec;
+                dd.apply = 0;
+                const int q = *g.seq;
+                if (g.h_ring) { IterMirror<A>& m = g.h_ring[q % g.ring]; m.d = dd; m.td = *g.td; m.seq = q; m.noop = 1; }
+                *g.seq = q + 1;
+            }
+            return;
+        }
+    }
     const int ochunk = (n + B - 1) / B;
     const int ob0 = min(n, b * ochunk), ob1 = min(n, ob0 + ochunk);
-    bool counted = false;
+    for (int s = threadIdx.x; s < k; s += blockDim.x) { hh[s] = 0; pr[s] = 0; }
+    if (threadIdx.x == 0) s_nres = 0;
+    if (b == 0 && threadIdx.x == 0) *g.empty_slot = INT_MAX;   // (read by the stream/combine before this kernel)
+
+    // chunks of at most POST_THREADS objects (n <= POST_THREADS * blocks:
+    // every BASELINE config) keep one object per thread in registers; the
+    // cache loads are issued before the decision is known
+    const bool reg = ob1 - ob0 <= POST_THREADS;
+    const int myo = ob0 + threadIdx.x;
+    const bool have = reg && myo < ob1;
+    int j1 = 0, j2 = 0;
+    T d1 = 0, d2 = 0;
+    if (have) { j1 = __ldcg(&g.near[myo]); j2 = __ldcg(&g.sec[myo]); d1 = __ldcg(&g.dn[myo]); d2 = __ldcg(&g.ds[myo]); }
+
+    // ---- A: select
     if (!g.prep_only) {
-        // ---- 0 select (every block decides identically; block 0 records)
         if (threadIdx.x == 0) {
             Rec<A> best = rec_none<A>();
             for (int r = 0; r < g.nrec; ++r) {
@@ -111,103 +145,142 @@ k_fp1_post(PostArgs<T, A> g) {
             if (best.slot == INT_MAX) improving = false;
             else if (std::is_same<A, double>::value) improving = (double)best.v < -1e-12 * fabs((double)tdv);
             else improving = best.v < 0;
-            Decision<A> d = *g.dec;
-            d.iters += 1;
-            d.apply = improving ? 1 : 0;
-            d.dtd = best.v;
-            d.slot = best.slot;
-            d.c = best.c;
+            Decision<A> dd = *g.dec;
+            dd.iters += 1;
+            dd.apply = improving ? 1 : 0;
+            dd.dtd = best.v;
+            dd.slot = best.slot;
+            dd.c = best.c;
             if (improving) {
-                d.old_m = g.M[best.slot];
-                d.swaps += 1;
+                dd.old_m = g.M[best.slot];
+                dd.swaps += 1;
+            } else {
+                dd.done = 1;
             }
-            sdec = d;
+            sdec = dd;
         }
-        __syncthreads();
-        d = sdec;
-        post_stamp(g.tph, 1);
-        // (block 0 records the decision in M / point_slot / TD / dec after
-        // the histogram's grid sync, when every block has read them; phases
-        // 1-3 do not read them)
+    }
+    __syncthreads();
+    if (!g.prep_only) d = sdec;
+    post_stamp(g.tph, 1);
 
-        // ---- 1 apply: column c*, incremental nearest/second, over the block's
-        // chunk of objects; the chunk's histogram of the new nearest slots is
-        // counted on the way (the rescanned objects are added in phase 2)
-        if (d.apply) {
-            const int i = d.slot;
-            const bool local = d.c >= g.c0 && d.c < g.c1;
-            int* hh = post_smem;
-            for (int s = threadIdx.x; s < k; s += blockDim.x) hh[s] = 0;
-            __syncthreads();
-            for (int o = ob0 + threadIdx.x; o < ob1; o += blockDim.x) {
-                if (local) g.MC[(int64_t)i * n + o] = g.D[(int64_t)o * g.ld + (d.c - g.c0)];
+    // ---- A: apply (column c*, incremental nearest/second, in-block rescans)
+    if (!g.prep_only && d.apply) {
+        __shared__ int r_j1[POST_THREADS], r_j2[POST_THREADS];
+        __shared__ T r_d1[POST_THREADS], r_d2[POST_THREADS];
+        const int i = d.slot;
+        const bool local = d.c >= g.c0 && d.c < g.c1;
+        int myent = -1;
+        if (reg) {
+            if (have) {
+                const T x = local ? g.D[(int64_t)myo * g.ld + (d.c - g.c0)] : g.MC[(int64_t)i * n + myo];
+                if (local) g.MC[(int64_t)i * n + myo] = x;
+                if (j1 == i || j2 == i) {
+                    myent = atomicAdd(&s_nres, 1);
+                    g.rescan[ob0 + myent] = myo;
+                } else if (x < d1 || (x == d1 && i < j1)) {
+                    j2 = j1; d2 = d1; j1 = i; d1 = x;
+                    g.near[myo] = j1; g.dn[myo] = d1; g.sec[myo] = j2; g.ds[myo] = d2;
+                } else if (x < d2 || (x == d2 && i < j2)) {
+                    j2 = i; d2 = x;
+                    g.sec[myo] = j2; g.ds[myo] = d2;
+                }
             }
+        } else {
+            for (int o = ob0 + threadIdx.x; o < ob1; o += blockDim.x)
+                if (local) g.MC[(int64_t)i * n + o] = g.D[(int64_t)o * g.ld + (d.c - g.c0)];
             // (the column is read back below by the same thread: same o mapping)
             for (int o = ob0 + threadIdx.x; o < ob1; o += blockDim.x) {
-                const int j1 = __ldcg(&g.near[o]), j2 = __ldcg(&g.sec[o]);
-                if (j1 == i || j2 == i) {
-                    g.rescan[atomicAdd(g.rescan_count, 1)] = o;
+                const int a1 = __ldcg(&g.near[o]), a2 = __ldcg(&g.sec[o]);
+                if (a1 == i || a2 == i) {
+                    g.rescan[ob0 + atomicAdd(&s_nres, 1)] = o;
                     continue;
                 }
                 const T x = g.MC[(int64_t)i * n + o];
-                const T d1 = __ldcg(&g.dn[o]), d2 = __ldcg(&g.ds[o]);
-                if (x < d1 || (x == d1 && i < j1)) {
-                    g.near[o] = i; g.dn[o] = x; g.sec[o] = j1; g.ds[o] = d1;
-                    atomicAdd(&hh[i], 1);
-                } else {
-                    if (x < d2 || (x == d2 && i < j2)) { g.sec[o] = i; g.ds[o] = x; }
-                    atomicAdd(&hh[j1], 1);
+                const T e1 = __ldcg(&g.dn[o]), e2 = __ldcg(&g.ds[o]);
+                if (x < e1 || (x == e1 && i < a1)) {
+                    g.near[o] = i; g.dn[o] = x; g.sec[o] = a1; g.ds[o] = e1;
+                } else if (x < e2 || (x == e2 && i < a2)) {
+                    g.sec[o] = i; g.ds[o] = x;
                 }
             }
-            __syncthreads();
-            for (int s = threadIdx.x; s < k; s += blockDim.x) g.counts[(int64_t)s * B + b] = hh[s];
-            grid.sync(); post_stamp(g.tph, 2);
-            // ---- 2 rescan
-            const int cnt = __ldcg(g.rescan_count);
-            for (int e = gwarp; e < cnt; e += nwarps) {
-                const int o = __ldcg(&g.rescan[e]);
-                T d1 = dmax<T>(), d2 = dmax<T>();
-                int j1 = INT_MAX, j2 = INT_MAX;
-    #pragma unroll 8
-                for (int j = lane; j < k; j += 32) {
-                    const T dd = __ldcg(&g.MC[(int64_t)j * n + o]);
-                    if (lex_lt(dd, j, d1, j1)) { d2 = d1; j2 = j1; d1 = dd; j1 = j; }
-                    else if (lex_lt(dd, j, d2, j2)) { d2 = dd; j2 = j; }
-                }
-    #pragma unroll
-                for (int x = 16; x >= 1; x >>= 1) {
-                    const T e1 = __shfl_xor_sync(FULL, d1, x), e2 = __shfl_xor_sync(FULL, d2, x);
-                    const int f1 = __shfl_xor_sync(FULL, j1, x), f2 = __shfl_xor_sync(FULL, j2, x);
-                    if (lex_lt(e1, f1, d1, j1)) {
-                        if (lex_lt(d1, j1, e2, f2)) { d2 = d1; j2 = j1; } else { d2 = e2; j2 = f2; }
-                        d1 = e1; j1 = f1;
-                    } else if (lex_lt(e1, f1, d2, j2)) {
-                        d2 = e1; j2 = f1;
-                    }
-                }
-                if (lane == 0) {
-                    g.near[o] = j1; g.sec[o] = j2; g.dn[o] = d1; g.ds[o] = d2;
-                    atomicAdd(&g.counts[(int64_t)j1 * B + o / ochunk], 1);   // the owner chunk's histogram
-                }
-            }
-            grid.sync(); post_stamp(g.tph, 3);
-            counted = true;
         }
+        __syncthreads();
+        const int nres = s_nres;
+        for (int e = warp; e < nres; e += POST_THREADS / 32) {
+            const int o = g.rescan[ob0 + e];
+            T q1 = dmax<T>(), q2 = dmax<T>();
+            int k1 = INT_MAX, k2 = INT_MAX;
+#pragma unroll 8
+            for (int j = lane; j < k; j += 32) {
+                const T dd = __ldcg(&g.MC[(int64_t)j * n + o]);
+                if (lex_lt(dd, j, q1, k1)) { q2 = q1; k2 = k1; q1 = dd; k1 = j; }
+                else if (lex_lt(dd, j, q2, k2)) { q2 = dd; k2 = j; }
+            }
+#pragma unroll
+            for (int x = 16; x >= 1; x >>= 1) {
+                const T e1 = __shfl_xor_sync(FULL, q1, x), e2 = __shfl_xor_sync(FULL, q2, x);
+                const int f1 = __shfl_xor_sync(FULL, k1, x), f2 = __shfl_xor_sync(FULL, k2, x);
+                if (lex_lt(e1, f1, q1, k1)) {
+                    if (lex_lt(q1, k1, e2, f2)) { q2 = q1; k2 = k1; } else { q2 = e2; k2 = f2; }
+                    q1 = e1; k1 = f1;
+                } else if (lex_lt(e1, f1, q2, k2)) {
+                    q2 = e1; k2 = f1;
+                }
+            }
+            if (lane == 0) {
+                g.near[o] = k1; g.sec[o] = k2; g.dn[o] = q1; g.ds[o] = q2;
+                if (reg) { r_j1[e] = k1; r_j2[e] = k2; r_d1[e] = q1; r_d2[e] = q2; }
+            }
+        }
+        __syncthreads();                        // the chunk's cache is final (block-visible)
+        if (myent >= 0) { j1 = r_j1[myent]; j2 = r_j2[myent]; d1 = r_d1[myent]; d2 = r_d2[myent]; }
+    }
+    post_stamp(g.tph, 2);
 
-    }
-    // ---- 3 histogram of the block's chunk (when no swap was applied, or
-    // prep only; otherwise counted in phases 1-2)
-    const int e0 = ob0, e1 = ob1;
-    if (!counted) {
-        int* h = post_smem;
-        for (int s = threadIdx.x; s < k; s += blockDim.x) h[s] = 0;
+    // ---- A: count -- per slot, the chunk's objects and partial removal loss
+    {
+        for (int base = ob0; base < ob1; base += POST_THREADS) {
+            const int o = base + threadIdx.x;
+            const bool v = o < ob1;
+            int s = 0;
+            A val = 0;
+            if (v) {
+                if (reg) { s = j1; val = (A)d2 - (A)d1; }
+                else { s = __ldcg(&g.near[o]); val = (A)__ldcg(&g.ds[o]) - (A)__ldcg(&g.dn[o]); }
+                atomicAdd(&hh[s], 1);
+            }
+            if constexpr (std::is_same<A, double>::value) {
+                // float path, deterministic: per warp, the leader of each
+                // slot's peers sums their values in lane order; the warps'
+                // sums then enter pr[] in warp order (one warp at a time)
+                const unsigned peers = __match_any_sync(FULL, v ? s : -1 - lane);
+                const int leader = __ffs(peers) - 1;
+                A acc = 0;
+#pragma unroll
+                for (int t = 0; t < 32; ++t) {
+                    const A vt = __shfl_sync(FULL, val, t);
+                    if ((peers >> t) & 1u) acc += vt;
+                }
+                const int nw = (min(POST_THREADS, ob1 - base) + 31) >> 5;
+                for (int w = 0; w < nw; ++w) {
+                    if (warp == w && v && lane == leader) pr[s] += acc;
+                    __syncthreads();
+                }
+            } else {
+                if (v) atomicAdd(reinterpret_cast<unsigned long long*>(&pr[s]), (unsigned long long)val);   // exact
+            }
+        }
         __syncthreads();
-        for (int e = e0 + threadIdx.x; e < e1; e += blockDim.x) atomicAdd(&h[__ldcg(&g.near[e])], 1);
-        __syncthreads();
-        for (int s = threadIdx.x; s < k; s += blockDim.x) g.counts[(int64_t)s * B + b] = h[s];
-        grid.sync(); post_stamp(g.tph, 4);
+        for (int s = threadIdx.x; s < k; s += blockDim.x) {
+            g.counts[(int64_t)s * B + b] = hh[s];
+            g.rpart[(int64_t)s * B + b] = pr[s];
+        }
     }
+    grid.sync(); post_stamp(g.tph, 3);
+
     if (!g.prep_only && b == 0 && threadIdx.x == 0) {
+        // every block has read dec / M / td (phase A): record the decision
         *g.dec = d;
         if (d.apply) {
             g.M[d.slot] = d.c;
@@ -217,17 +290,21 @@ k_fp1_post(PostArgs<T, A> g) {
         }
     }
 
-    // ---- 4 within-slot exclusive scan over the chunks, warp per slot: all
-    // B counts of the slot loaded first (coalesced, one memory round trip),
-    // then B/32 register-only warp scans
+    // ---- B: warp per slot -- chunk offsets (all B counts loaded first, then
+    // register-only warp scans), slot total, removal loss (fixed tree)
     for (int s = gwarp; s < k; s += nwarps) {
         const int* cs = g.counts + (int64_t)s * B;
+        const A* ps = g.rpart + (int64_t)s * B;
         int cv[POST_MAX_PER];
+        A rsum = 0;
 #pragma unroll
         for (int i = 0; i < POST_MAX_PER; ++i) {
             const int bb = i * 32 + lane;
             cv[i] = bb < B ? __ldcg(&cs[bb]) : 0;
+            if (bb < B) rsum += __ldcg(&ps[bb]);
         }
+#pragma unroll
+        for (int x = 16; x >= 1; x >>= 1) rsum += __shfl_xor_sync(FULL, rsum, x);
         int run = 0;
         int* os = g.offsets + (int64_t)s * B;
 #pragma unroll
@@ -243,16 +320,20 @@ k_fp1_post(PostArgs<T, A> g) {
             if (bb < B) os[bb] = run + incl - cv[i];
             run += __shfl_sync(FULL, incl, 31);
         }
-        if (lane == 0) g.slot_tot[s] = run;
+        if (lane == 0) {
+            g.slot_tot[s] = run;
+            g.R[s] = rsum;
+            if (run == 0) atomicMin(g.empty_slot, s);
+        }
     }
-    grid.sync(); post_stamp(g.tph, 5);
+    grid.sync(); post_stamp(g.tph, 4);
 
-    // ---- 5 exclusive scan of the slot totals, by EVERY block into its shared
-    // memory (no grid sync: the scatter below reads the block's own copy);
-    // block 0 also writes seg_start[] for the removal loss and the stream
+    // ---- C: segment starts (every block, its shared memory; block 0 also
+    // writes seg_start[] for the FastPAM2 / window paths), stable scatter of
+    // the chunk, part head / tail slots
     {
         __shared__ int wsum[POST_THREADS / 32];
-        int* segs = post_smem;                   // k ints: seg_start, then the scatter cursors
+        int* segs = hh;                          // k ints: segment starts, then the scatter cursors
         const int per = (k + blockDim.x - 1) / blockDim.x;
         const int a = threadIdx.x * per, z = min(k, a + per);
         int sum = 0;
@@ -263,10 +344,10 @@ k_fp1_post(PostArgs<T, A> g) {
             const int y = __shfl_up_sync(FULL, incl, dd);
             if (lane >= dd) incl += y;
         }
-        if (lane == 31) wsum[threadIdx.x >> 5] = incl;
+        if (lane == 31) wsum[warp] = incl;
         __syncthreads();
         int base = 0;
-        for (int w = 0; w < (int)(threadIdx.x >> 5); ++w) base += wsum[w];
+        for (int w = 0; w < warp; ++w) base += wsum[w];
         int run = base + incl - sum;
         for (int i = a; i < z; ++i) {
             segs[i] = run;
@@ -274,71 +355,68 @@ k_fp1_post(PostArgs<T, A> g) {
             run += __ldcg(&g.slot_tot[i]);
         }
         if (b == 0 && threadIdx.x == blockDim.x - 1) g.seg_start[k] = run;
-        if (b == 0 && threadIdx.x == 0) *g.empty_slot = INT_MAX;
         __syncthreads();
-    }
-    post_stamp(g.tph, 6);
-
-    // ---- 6 stable scatter into (slot, o) order: warp 0 of each block
-    if (threadIdx.x < 32) {
-        int* cur = post_smem;                    // seg_start of this block's copy + its chunk offsets
-        for (int s = lane; s < k; s += 32) cur[s] += __ldcg(&g.offsets[(int64_t)s * B + b]);
-        __syncwarp();
+        // part metadata: the slot of sorted position p is the last s with
+        // segs[s] <= p (empty slots share their successor's start)
+        for (int q = tid; q < g.P; q += nth) {
+            const int64_t p0 = part_lo(q, n, g.P), p1 = part_lo(q + 1, n, g.P);
+            for (int side = 0; side < 2; ++side) {
+                const int64_t p = side == 0 ? p0 : p1 - 1;
+                int lo = 0, hi = k - 1;              // segs[0] = 0 <= p
+                while (lo < hi) {
+                    const int mid = (lo + hi + 1) >> 1;
+                    if (segs[mid] <= p) lo = mid; else hi = mid - 1;
+                }
+                if (side == 0) g.head_slot[q] = lo; else g.tail_slot[q] = lo;
+            }
+        }
+        __syncthreads();                        // the part search reads segs; the cursors overwrite them
+        // stable scatter into (slot, o) order: every warp ranks its 32 objects
+        // among same-slot peers (match_any); the warps then take their slot
+        // ranges from the cursors one after another (warp order = object order)
+        int* cur = segs;
+        for (int s = threadIdx.x; s < k; s += blockDim.x) cur[s] += __ldcg(&g.offsets[(int64_t)s * B + b]);
+        __syncthreads();
         const unsigned lt = (1u << lane) - 1u;
-        for (int base = e0; base < e1; base += 32) {
-            const int e = base + lane;
-            const bool valid = e < e1;
-            const int s = valid ? __ldcg(&g.near[e]) : -1 - lane;
+        for (int base = ob0; base < ob1; base += POST_THREADS) {
+            const int e = base + threadIdx.x;
+            const bool valid = e < ob1;
+            int s = -1 - lane;
+            T en = 0, es = 0;
+            if (valid) {
+                if (reg) { s = j1; en = d1; es = d2; }
+                else { s = __ldcg(&g.near[e]); en = __ldcg(&g.dn[e]); es = __ldcg(&g.ds[e]); }
+            }
             const unsigned peers = __match_any_sync(FULL, s);
             const int rank = __popc(peers & lt);
             const int leader = __ffs(peers) - 1;
             int bp = 0;
-            if (valid && lane == leader) bp = cur[s];
+            const int nw = (min(POST_THREADS, ob1 - base) + 31) >> 5;
+            for (int w = 0; w < nw; ++w) {
+                if (warp == w && valid && lane == leader) { bp = cur[s]; cur[s] = bp + __popc(peers); }
+                __syncthreads();
+            }
             bp = __shfl_sync(FULL, bp, leader);
-            __syncwarp();
-            if (valid && lane == leader) cur[s] = bp + __popc(peers);
-            __syncwarp();
             if (valid) {
                 RowInfo<T> r;
-                r.o = e; r.slot = s; r.dn = __ldcg(&g.dn[e]); r.ds = __ldcg(&g.ds[e]);
+                r.o = e; r.slot = s; r.dn = en; r.ds = es;
                 const int pos = bp + rank;
                 g.ri[pos] = r;
-                if (g.rowd) g.rowd[pos] = make_double2((double)r.dn, (double)r.ds);
+                if (g.rowd) g.rowd[pos] = make_double2((double)en, (double)es);
             }
         }
     }
-    grid.sync(); post_stamp(g.tph, 7);
-
-    // ---- 7 removal loss (warp per slot, fixed tree) and part metadata
-    for (int s = gwarp; s < k; s += nwarps) {
-        const int a = __ldcg(&g.seg_start[s]), z = __ldcg(&g.seg_start[s + 1]);
-        A sum = 0;
-        for (int p = a + lane; p < z; p += 32) {
-            const RowInfo<T> r = post_ld_ri(&g.ri[p]);
-            sum += (A)r.ds - (A)r.dn;
-        }
-#pragma unroll
-        for (int x = 16; x >= 1; x >>= 1) sum += __shfl_xor_sync(FULL, sum, x);
-        if (lane == 0) {
-            g.R[s] = sum;
-            if (a == z) atomicMin(g.empty_slot, s);
-        }
-    }
-    for (int q = tid; q < g.P; q += nth) {
-        const int64_t p0 = part_lo(q, n, g.P), p1 = part_lo(q + 1, n, g.P);
-        g.head_slot[q] = post_ld_ri(&g.ri[p0]).slot;
-        g.tail_slot[q] = post_ld_ri(&g.ri[p1 - 1]).slot;
-    }
     if (b == 0 && threadIdx.x == 0) {
         *g.rescan_count = 0;
-        // the decision and TD straight into pinned host memory (visible to the
-        // host once the stream is synchronised): no copy nodes after the kernel
-        if (g.h_dec) {
-            *g.h_dec = d;
-            *g.h_td = *g.td;
+        if (!g.prep_only) {
+            // the outcome straight into pinned host memory (visible to the host
+            // once the launch's completion event is observed)
+            const int q = *g.seq;
+            if (g.h_ring) { IterMirror<A>& m = g.h_ring[q % g.ring]; m.d = d; m.td = *g.td; m.seq = q; m.noop = 0; }
+            *g.seq = q + 1;
         }
     }
-    post_stamp(g.tph, 8);
+    post_stamp(g.tph, 5);
 }
 
 }  // namespace km

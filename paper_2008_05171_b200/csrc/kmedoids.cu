@@ -134,6 +134,7 @@ struct ImplBase {
                             void* td_out, int32_t* best_out) = 0;
     virtual km_status inc_iters(int32_t max_iters, int32_t* swaps, void* td_out, int32_t* iters_done,
                                 bool* converged) = 0;
+    virtual km_status fp1_run_pipelined(int32_t max_iter, int32_t* iters_out, int32_t* swaps_out, bool* converged) = 0;
     bool profiling = false;
     double prof_ms = 0.0;
     int64_t prof_launches = 0;
@@ -205,7 +206,10 @@ struct Impl : ImplBase {
 
     ~Impl() override {
         for (auto& sl : clara_slots) { sl.sub.reset(); if (sl.stream) cudaStreamDestroy(sl.stream); }
-        if (fp1_exec) cudaGraphExecDestroy(fp1_exec);
+        for (auto& g : fp1_g) if (g) cudaGraphExecDestroy(g);
+        for (auto& p : g_ev) for (auto e : p) if (e) cudaEventDestroy(e);
+        for (auto e : g_done) if (e) cudaEventDestroy(e);
+        if (h_ring) cudaFreeHost(h_ring);
         if (build_exec) cudaGraphExecDestroy(build_exec);
         if (cap_st) cudaStreamDestroy(cap_st);
         for (void* p : bufs) cudaFree(p);
@@ -345,7 +349,6 @@ struct Impl : ImplBase {
     int sp_n = 0;
     // CUDA graph of the FastPAM1 iteration (KM_GRAPH=0 disables)
     bool use_graph = true;
-    cudaGraphExec_t fp1_exec = nullptr;
     cudaStream_t cap_st = nullptr;
     int64_t fp1_graph_kernels = 0;
     int64_t fp1_iters = 0;
@@ -451,25 +454,32 @@ struct Impl : ImplBase {
         return KM_OK;
     }
 
+    bool fp1_mode = false;          // eval_local is enqueueing a FastPAM1 iteration (sticky convergence applies)
+    cudaEvent_t ev_a = nullptr, ev_b = nullptr;   // stream-kernel events of the graph being captured
     km_status eval_local(bool do_prep = true) {
         if (do_prep) KM_TRY(prep());
         cudaEvent_t* pair = nullptr;
         if (profiling && prof_ring_mode) KM_TRY(prof_ring_pair(&pair));
         if (pair) KM_CK(cudaEventRecord(pair[0], st));
-        else if (profiling) KM_CK(record_ev(ev0));
+        else if (profiling) KM_CK(record_ev(ev_a ? ev_a : ev0));
         KM_TRY((launch_seg2<SG_NC, SG_RB, SG_S, SG_MINB>(D, w, wpad, P, o_plus, o_head, o_tail, o_imin, o_islot,
-                                                          nullptr)));
+                                                          nullptr, fp1_mode ? &dec->done : nullptr)));
         KM_CKL();
         if (pair) KM_CK(cudaEventRecord(pair[1], st));
-        else if (profiling) { KM_CK(record_ev(ev1)); pending_prof = true; }
-        KM_TRY(launch_combine(w, c0, P, o_plus, o_head, o_tail, o_imin, o_islot, head_slot, tail_slot, cand_v, cand_slot,
-                              nullptr, nullptr));
+        else if (profiling) { KM_CK(record_ev(ev_b ? ev_b : ev1)); pending_prof = true; }
+        KM_TRY(launch_combine(w, c0, P, o_plus, o_head, o_tail, o_imin, o_islot, head_slot, tail_slot, cand_v,
+                              cand_slot, nullptr, nullptr));
         return KM_OK;
     }
 
-    // a4: per-candidate combine of the stream's part outputs (one thread per
-    // column; folding part groups in parallel warps was measured 10-30 us
-    // slower per step at C4/C5 in round 1 and removed).
+    // a4: per-candidate combine of the stream's part outputs, one thread per
+    // column.  Measured slower and removed: folding part groups in parallel
+    // warps (round 1: +10-30 us per step at C4/C5), 2/4/8 threads per column
+    // merging range states by shuffles (round 2: +3-10 us at C4), and the
+    // fold in the stream's tail by the last CTA of each tile (round 2: the
+    // stream +90 us at C4: the fold of the last wave is latency-bound).  The
+    // combine reads the part outputs (36 B per part and column: ~0.4 us per
+    // part at C4), so its cost follows the part count P.
     km_status launch_combine(int ww, int64_t colb, int Pw, const A* pl, const A* hd, const A* tl, const A* im,
                              const int* isl, const int* hsl, const int* tsl, A* cv, int* cs, A* acc_o, A* plus_o) {
         constexpr int TPB = 128;   // 32 / 64 threads per block measured slower, 256 equal
@@ -499,7 +509,7 @@ struct Impl : ImplBase {
     const char* stream_kernel_name() const override { return "k_swap_stream_seg2"; }
     template <int NC, int RB, int S, int MINB = 2>
     km_status launch_seg2(const T* Dw, int ww, int wpadw, int Pw, A* plus_o, A* head_o, A* tail_o, A* imin_o,
-                          int* islot_o, A* acc_out) {
+                          int* islot_o, A* acc_out, const int* skip_if = nullptr) {
         using C = km::SegCfg<T, NC, RB, S>;
         auto kern = km::k_swap_stream_seg2<T, A, NC, RB, S, MINB>;
         if (!seg2_attr_set) {
@@ -511,7 +521,7 @@ struct Impl : ImplBase {
         // that follows when they fit comfortably (C3: 16 MB), else streamed
         const bool acc_keep = acc_out && (size_t)k * ww * sizeof(A) <= ((size_t)48 << 20);
         kern<<<g, C::THREADS, C::SMEM, st>>>(Dw, ld, ww, wpadw, (int)n, Pw, ri, R, plus_o, head_o, tail_o, imin_o,
-                                              islot_o, acc_out, rowd, acc_keep);
+                                              islot_o, acc_out, rowd, acc_keep, skip_if);
         return KM_OK;
     }
 
@@ -545,25 +555,28 @@ struct Impl : ImplBase {
     bool fp1_prepped = false;       // slot sort / R / part metadata valid for the current cache
     int post_blocks = 0;
     int *post_counts = nullptr, *post_offsets = nullptr;
+    A* post_rpart = nullptr;
     unsigned long long* post_tph = nullptr;   // KM_STEP_PROF: phase stamps of k_fp1_post
     double post_ph_sum[8] = {};
+    size_t post_smem() const { return ((size_t)k * sizeof(int) + 15) / 16 * 16 + (size_t)k * sizeof(A); }
 
     km_status post_alloc() {
         if (post_counts) return KM_OK;
         auto kern = km::k_fp1_post<T, A>;
-        const size_t sm = (size_t)k * sizeof(int);
+        const size_t sm = post_smem();
         if (sm > 48 * 1024) KM_CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
         int dev = 0, per_sm = 0, nsm = 0;
         KM_CK(cudaGetDevice(&dev));
         KM_CK(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
         KM_CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, km::POST_THREADS, sm));
         if (per_sm < 1) return fail(KM_ECUDA, "k_fp1_post cannot be resident");
-        int bps = 4;                                    // blocks per SM (KM_POST_BPS: measurement override)
+        int bps = 3;                                    // blocks per SM (KM_POST_BPS: measurement override)
         if (const char* e = getenv("KM_POST_BPS")) bps = std::max(1, std::min(8, atoi(e)));
         post_blocks = std::min(nsm * std::min(per_sm, bps), km::POST_MAX_BLOCKS);
         post_blocks = (int)std::min<int64_t>(post_blocks, std::max<int64_t>(1, cdiv(n, 64)));
         KM_TRY(alloc(&post_counts, (size_t)k * post_blocks));
         KM_TRY(alloc(&post_offsets, (size_t)k * post_blocks));
+        KM_TRY(alloc(&post_rpart, (size_t)k * post_blocks));
         if (step_prof) KM_TRY(alloc(&post_tph, 16));
         return KM_OK;
     }
@@ -573,15 +586,14 @@ struct Impl : ImplBase {
         g.D = D; g.ld = ld; g.n = (int)n; g.k = k; g.c0 = c0; g.c1 = c1; g.recs = rec_local; g.nrec = 1;
         g.td = td; g.M = M; g.point_slot = point_slot; g.dec = dec; g.MC = MC; g.near = near; g.sec = sec;
         g.dn = dn; g.ds = ds; g.rescan = rescan; g.rescan_count = rescan_count; g.counts = post_counts;
-        g.offsets = post_offsets; g.slot_tot = slot_tot; g.seg_start = seg_start; g.empty_slot = empty_slot;
+        g.offsets = post_offsets; g.rpart = post_rpart; g.slot_tot = slot_tot; g.seg_start = seg_start; g.empty_slot = empty_slot;
         g.ri = ri; g.rowd = rowd; g.R = R; g.P = P; g.head_slot = head_slot; g.tail_slot = tail_slot;
         g.tph = post_tph;
         g.prep_only = prep_only ? 1 : 0;
-        g.h_dec = prep_only ? nullptr : h_dec;
-        g.h_td = prep_only ? nullptr : h_td;
+        g.h_ring = h_ring; g.ring = RING; g.seq = post_seq;
         void* args[] = {&g};
         KM_CK(cudaLaunchCooperativeKernel((void*)km::k_fp1_post<T, A>, dim3(post_blocks), dim3(km::POST_THREADS), args,
-                                          (size_t)k * sizeof(int), st));
+                                          post_smem(), st));
         ++launches;
         return KM_OK;
     }
@@ -593,7 +605,9 @@ struct Impl : ImplBase {
     km_status enqueue_fp1_iteration() {
         const bool prof_save = profiling;
         if (use_graph) profiling = true;      // the graph always carries the stream events
+        fp1_mode = true;
         km_status s = eval_local(false);
+        fp1_mode = false;
         profiling = prof_save;
         if (s != KM_OK) return s;
         if (step_prof) KM_CK(record_ev(sp_ev[2]));
@@ -608,105 +622,200 @@ struct Impl : ImplBase {
         if (!ready) return fail(KM_EINVAL, "no medoids: call kmedoids_set_medoids or kmedoids_init_build first");
         if (v != KM_FASTPAM1 && v != KM_FASTPAM2 && v != KM_FASTERPAM && v != KM_FASTPAM1_INC)
             return fail(KM_EINVAL, "unknown variant %d", (int)v);
+        if (v != KM_FASTPAM1) KM_TRY(clear_fp1_done());
         if (v == KM_FASTPAM2) return swap_iter_fp2(swaps, td_out);
         if (v == KM_FASTERPAM) return swap_iter_fp3(swaps, td_out);
         if (v == KM_FASTPAM1_INC) return inc_iters(1, swaps, td_out, nullptr, nullptr);
+        KM_TRY(fp1_launch());
+        KM_TRY(fp1_collect(fp1_seq - 1, true));
+        return fp1_result(swaps, td_out);
+    }
+
+    // ---- FastPAM1 iterations: launch / collect ---------------------------------
+    // Each iteration (stream + post kernel) is one CUDA graph launch; its
+    // outcome reaches the host through the pinned ring h_ring (slot = launch
+    // sequence number % RING, written by the post kernel), so the host can
+    // keep the next iteration queued while it reads the current one
+    // (fp1_run_pipelined).  A pass that finds no improving swap sets the
+    // sticky Decision::done: iterations queued behind it are no-ops.  Two
+    // graphs alternate so that each queued iteration has its own stream-kernel
+    // events (profiling) while the previous one is collected.
+    static constexpr int RING = 8;
+    static constexpr int NGRAPH = 2;
+    km::IterMirror<A>* h_ring = nullptr;
+    int* post_seq = nullptr;            // device launch counter of the FastPAM1 post kernel
+    int64_t fp1_seq = 0;                // host copy: FastPAM1 iterations launched
+    cudaGraphExec_t fp1_g[NGRAPH] = {};
+    cudaEvent_t g_ev[NGRAPH][2] = {};   // stream kernel start / end inside graph g
+    cudaEvent_t g_done[NGRAPH] = {};    // recorded after each launch of graph g
+    bool fp1_any_done = false;          // a FastPAM1 pass may have set Decision::done
+
+    km_status fp1_ring_alloc() {
+        if (h_ring) return KM_OK;
+        KM_CK(cudaMallocHost((void**)&h_ring, RING * sizeof(km::IterMirror<A>)));
+        memset((void*)h_ring, 0, RING * sizeof(km::IterMirror<A>));
+        KM_TRY(alloc(&post_seq, 1));
+        KM_CK(cudaMemsetAsync(post_seq, 0, sizeof(int), st));
+        for (int g = 0; g < NGRAPH; ++g) {
+            KM_CK(cudaEventCreate(&g_ev[g][0]));
+            KM_CK(cudaEventCreate(&g_ev[g][1]));
+            KM_CK(cudaEventCreateWithFlags(&g_done[g], cudaEventDisableTiming));
+        }
+        return KM_OK;
+    }
+
+    // (other entry points that change the state clear the sticky flag)
+    km_status clear_fp1_done() {
+        if (!fp1_any_done) return KM_OK;
+        KM_CK(cudaMemsetAsync(&dec->done, 0, sizeof(int32_t), st));
+        fp1_any_done = false;
+        return KM_OK;
+    }
+
+    km_status fp1_capture(int gi) {
+        const int64_t l0 = launches;
+        // capture on a private stream (the caller's may be the legacy default
+        // stream, which cannot capture); launch on the caller's
+        if (!cap_st) KM_CK(cudaStreamCreateWithFlags(&cap_st, cudaStreamNonBlocking));
+        cudaStream_t user_st = st;
+        st = cap_st;
+        cudaError_t be = cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal);
+        if (be != cudaSuccess) { st = user_st; return fail(KM_ECUDA, "begin capture: %s", cudaGetErrorString(be)); }
+        capturing = true;
+        ev_a = g_ev[gi][0]; ev_b = g_ev[gi][1];
+        km_status cs = enqueue_fp1_iteration();
+        ev_a = ev_b = nullptr;
+        capturing = false;
+        cudaGraph_t g = nullptr;
+        cudaError_t ce = cudaStreamEndCapture(st, &g);
+        st = user_st;
+        if (cs == KM_OK && ce == cudaSuccess) {
+            ce = cudaGraphInstantiate(&fp1_g[gi], g, 0);
+            if (ce != cudaSuccess) fp1_g[gi] = nullptr;
+        }
+        if (g) cudaGraphDestroy(g);
+        fp1_graph_kernels = launches - l0;
+        launches = l0;
+        if (cs != KM_OK) return cs;
+        if (!fp1_g[gi]) return fail(KM_ECUDA, "FastPAM1 iteration graph: %s", cudaGetErrorString(ce));
+        return KM_OK;
+    }
+
+    // Enqueue FastPAM1 iteration number fp1_seq (no host wait).
+    km_status fp1_launch() {
+        KM_TRY(fp1_ring_alloc());
         inc_valid = false;
         KM_TRY(post_alloc());
         if (!fp1_prepped) {
             KM_TRY(prep());
             KM_CK(cudaMemsetAsync(rescan_count, 0, sizeof(int), st));
+            fp1_prepped = true;
         }
-        if (use_graph && fp1_iters >= 1) {
-            // the whole iteration (11 kernels + the 32-byte decision copy) as one CUDA graph
-            if (!fp1_exec) {
-                const int64_t l0 = launches;
-                // capture on a private stream (the caller's may be the legacy
-                // default stream, which cannot capture); launch on the caller's.
-                if (!cap_st) KM_CK(cudaStreamCreateWithFlags(&cap_st, cudaStreamNonBlocking));
-                cudaStream_t user_st = st;
-                st = cap_st;
-                cudaError_t be = cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal);
-                if (be != cudaSuccess) { st = user_st; return fail(KM_ECUDA, "begin capture: %s", cudaGetErrorString(be)); }
-                capturing = true;
-                km_status cs = enqueue_fp1_iteration();
-                capturing = false;
-                cudaGraph_t g = nullptr;
-                cudaError_t ce = cudaStreamEndCapture(st, &g);
-                st = user_st;
-                bool graph_ok = (cs == KM_OK && ce == cudaSuccess);
-                if (graph_ok) {
-                    ce = cudaGraphInstantiate(&fp1_exec, g, 0);
-                    if (ce != cudaSuccess) { fp1_exec = nullptr; graph_ok = false; }
-                }
-                if (g) cudaGraphDestroy(g);
-                const int64_t captured = launches - l0;
-                launches = l0;
-                if (!graph_ok) {
-                    // e.g. a cooperative launch the capture does not accept: run the
-                    // iteration directly from now on
-                    const cudaError_t le = cudaGetLastError();
-                    fprintf(stderr, "[kmedoids] FastPAM1 iteration graph unavailable (%s / %s); launching directly\n",
-                            cudaGetErrorString(ce), cudaGetErrorString(le));
-                    use_graph = false;
-                    KM_TRY(enqueue_fp1_iteration());
-                    KM_TRY(sync_dec());
-                    goto iteration_done;
-                }
-                fp1_graph_kernels = captured;
-            }
-            if (step_prof) KM_CK(cudaEventRecord(sp_ev[0], st));
-            KM_CK(cudaGraphLaunch(fp1_exec, st));
+        const int gi = (int)(fp1_seq % NGRAPH);
+        const bool graph = use_graph && fp1_iters >= 1;   // the first iteration runs directly (allocations)
+        if (graph && !fp1_g[gi]) KM_TRY(fp1_capture(gi));
+        if (step_prof) KM_CK(cudaEventRecord(sp_ev[0], st));
+        if (graph) {
+            KM_CK(cudaGraphLaunch(fp1_g[gi], st));
             launches += fp1_graph_kernels;
-            KM_CK(cudaStreamSynchronize(st));
-            if (step_prof) {
-                // phases of the iteration graph (KM_STEP_PROF=1, measurement aid):
-                // launch -> stream start, stream, combine, post, decision copies
-                float t[5];
-                KM_CK(cudaEventElapsedTime(&t[0], sp_ev[0], ev0));
-                KM_CK(cudaEventElapsedTime(&t[1], ev0, ev1));
-                KM_CK(cudaEventElapsedTime(&t[2], ev1, sp_ev[2]));
-                KM_CK(cudaEventElapsedTime(&t[3], sp_ev[2], sp_ev[3]));
-                KM_CK(cudaEventElapsedTime(&t[4], sp_ev[3], sp_ev[4]));
-                for (int i = 0; i < 5; ++i) sp_sum[i] += t[i];
-                if (post_tph) {
-                    unsigned long long h[9];
-                    KM_CK(cudaMemcpy(h, post_tph, sizeof(h), cudaMemcpyDeviceToHost));
-                    for (int i = 0; i < 8; ++i) post_ph_sum[i] += 1e-3 * (double)(h[i + 1] - h[i]);
-                }
-                if (++sp_n % 50 == 0) {
-                    fprintf(stderr, "[kmedoids] step phases over %d iterations (us): launch %.1f stream %.1f combine %.1f "
-                            "post %.1f copies %.1f\n", sp_n, 1e3 * sp_sum[0] / sp_n, 1e3 * sp_sum[1] / sp_n,
-                            1e3 * sp_sum[2] / sp_n, 1e3 * sp_sum[3] / sp_n, 1e3 * sp_sum[4] / sp_n);
-                    if (post_tph)
-                        fprintf(stderr, "[kmedoids] post phases (us): select %.1f apply %.1f rescan %.1f hist %.1f "
-                                "slotscan %.1f scan %.1f scatter %.1f R/parts %.1f\n", post_ph_sum[0] / sp_n,
-                                post_ph_sum[1] / sp_n, post_ph_sum[2] / sp_n, post_ph_sum[3] / sp_n,
-                                post_ph_sum[4] / sp_n, post_ph_sum[5] / sp_n, post_ph_sum[6] / sp_n,
-                                post_ph_sum[7] / sp_n);
-                }
-            }
-            if (profiling) {
-                float ms = 0.f;
-                KM_CK(cudaEventElapsedTime(&ms, ev0, ev1));
-                prof_ms += ms; prof_launches += 1;
-            }
-            pending_prof = false;
         } else {
-            KM_TRY(enqueue_fp1_iteration());
-            KM_TRY(sync_dec());
+            ev_a = g_ev[gi][0]; ev_b = g_ev[gi][1];
+            const bool prof_save = profiling;
+            profiling = true;
+            km_status s2 = enqueue_fp1_iteration();
+            profiling = prof_save;
+            ev_a = ev_b = nullptr;
+            KM_TRY(s2);
         }
-    iteration_done:
+        KM_CK(cudaEventRecord(g_done[gi], st));
+        ++fp1_seq;
         ++fp1_iters;
-        fp1_prepped = true;
+        fp1_any_done = true;
+        return KM_OK;
+    }
+
+    // Wait for iteration `seq` and take its outcome into h_dec / h_td.
+    km_status fp1_collect(int64_t seq, bool single) {
+        const int gi = (int)(seq % NGRAPH);
+        KM_CK(cudaEventSynchronize(g_done[gi]));
+        const km::IterMirror<A>& m = h_ring[seq % RING];
+        if (m.seq != (int32_t)seq) return fail(KM_ECUDA, "iteration ring out of step (%d vs %lld)", m.seq, (long long)seq);
+        *h_dec = m.d;
+        *h_td = m.td;
+        if (profiling && !m.noop) {
+            float ms = 0.f;
+            KM_CK(cudaEventElapsedTime(&ms, g_ev[gi][0], g_ev[gi][1]));
+            prof_ms += ms; prof_launches += 1;
+        }
+        pending_prof = false;
+        if (single && step_prof) KM_TRY(step_prof_take(gi));
+        return KM_OK;
+    }
+
+    km_status fp1_result(int32_t* swaps, void* td_out) {
         last_swaps.clear();
         if (h_dec->apply) {
             Rec r; r.v = h_dec->dtd; r.slot = h_dec->slot; r.c = h_dec->c;
             last_swaps.push_back(r);
         }
         if (swaps) *swaps = h_dec->apply;
-        if (td_out) memcpy(td_out, h_td, sizeof(A));   // mirrored in the iteration
+        if (td_out) memcpy(td_out, h_td, sizeof(A));
         return h_dec->apply ? KM_OK : KM_CONVERGED;
+    }
+
+    // Up to max_iter FastPAM1 iterations with one queued ahead of the one
+    // being read (no host round trip between iterations).  Stops at the first
+    // pass without an improving swap (counted).
+    km_status fp1_run_pipelined(int32_t max_iter, int32_t* iters_out, int32_t* swaps_out, bool* converged) override {
+        if (sharded) return fail(KM_EINVAL, "swap iterations on a sharded handle; use the kmedoids_shard_* phases");
+        if (!ready) return fail(KM_EINVAL, "no medoids: call kmedoids_set_medoids or kmedoids_init_build first");
+        int32_t done_it = 0, sw = 0;
+        bool conv = false;
+        int64_t next = fp1_seq;             // next iteration to collect
+        int64_t launched = 0;
+        while (done_it < max_iter && !conv) {
+            while (launched < max_iter && fp1_seq - next < 2) {
+                KM_TRY(fp1_launch());
+                ++launched;
+            }
+            KM_TRY(fp1_collect(next, false));
+            ++next;
+            ++done_it;
+            if (h_dec->apply) ++sw; else conv = true;
+        }
+        fp1_result(nullptr, nullptr);      // last_swaps of the last collected pass (KM_CONVERGED is not an error)
+        if (fp1_seq > next) KM_CK(cudaEventSynchronize(g_done[(fp1_seq - 1) % NGRAPH]));   // queued no-ops
+        if (iters_out) *iters_out = done_it;
+        if (swaps_out) *swaps_out = sw;
+        if (converged) *converged = conv;
+        return KM_OK;
+    }
+
+    km_status step_prof_take(int gi) {
+        // phases of the iteration (KM_STEP_PROF=1, measurement aid): launch ->
+        // stream start, stream, combine, post
+        float t[5];
+        KM_CK(cudaEventElapsedTime(&t[0], sp_ev[0], g_ev[gi][0]));
+        KM_CK(cudaEventElapsedTime(&t[1], g_ev[gi][0], g_ev[gi][1]));
+        KM_CK(cudaEventElapsedTime(&t[2], g_ev[gi][1], sp_ev[2]));
+        KM_CK(cudaEventElapsedTime(&t[3], sp_ev[2], sp_ev[3]));
+        KM_CK(cudaEventElapsedTime(&t[4], sp_ev[3], sp_ev[4]));
+        for (int i = 0; i < 5; ++i) sp_sum[i] += t[i];
+        if (post_tph) {
+            unsigned long long h[6];
+            KM_CK(cudaMemcpy(h, post_tph, sizeof(h), cudaMemcpyDeviceToHost));
+            for (int i = 0; i < 5; ++i) post_ph_sum[i] += 1e-3 * (double)(h[i + 1] - h[i]);
+        }
+        if (++sp_n % 50 == 0) {
+            fprintf(stderr, "[kmedoids] step phases over %d iterations (us): launch %.1f stream %.1f combine %.1f "
+                    "post %.1f copies %.1f\n", sp_n, 1e3 * sp_sum[0] / sp_n, 1e3 * sp_sum[1] / sp_n,
+                    1e3 * sp_sum[2] / sp_n, 1e3 * sp_sum[3] / sp_n, 1e3 * sp_sum[4] / sp_n);
+            if (post_tph)
+                fprintf(stderr, "[kmedoids] post phases (us): select %.1f apply+rescan %.1f count+sync %.1f "
+                        "scan+sync %.1f scatter/parts %.1f\n", post_ph_sum[0] / sp_n, post_ph_sum[1] / sp_n,
+                        post_ph_sum[2] / sp_n, post_ph_sum[3] / sp_n, post_ph_sum[4] / sp_n);
+        }
+        return KM_OK;
     }
 
     km_status fp2_alloc() {
@@ -1188,6 +1297,7 @@ struct Impl : ImplBase {
                         bool* conv_out) override {
         if (sharded) return fail(KM_EINVAL, "incremental FastPAM1 on a sharded handle");
         if (!ready) return fail(KM_EINVAL, "no medoids: call kmedoids_set_medoids or kmedoids_init_build first");
+        KM_TRY(clear_fp1_done());
         KM_TRY(inc_alloc());
         fp1_prepped = false;
         last_swaps.clear();
@@ -1386,6 +1496,7 @@ struct Impl : ImplBase {
     }
 
     km_status init_weighted(const double* u, int32_t* M_out, void* td_out) override {
+        KM_TRY(clear_fp1_done());
         if (sharded) return fail(KM_EINVAL, "init_weighted on a sharded handle");
         if (k < 2) return fail(KM_EINVAL, "SWAP needs k >= 2");
         for (int i = 0; i < k; ++i)
@@ -1420,6 +1531,7 @@ struct Impl : ImplBase {
     }
 
     km_status init_lab(int32_t s, const int32_t* seq, int32_t* M_out, void* td_out) override {
+        KM_TRY(clear_fp1_done());
         if (sharded) return fail(KM_EINVAL, "init_lab on a sharded handle");
         if (k < 2) return fail(KM_EINVAL, "SWAP needs k >= 2");
         if (s < 1 || s > n) return fail(KM_EINVAL, "sample size s=%d must be in [1, n]", s);
@@ -1695,6 +1807,7 @@ struct Impl : ImplBase {
     cudaGraphExec_t build_exec = nullptr;
     int build_graph = -1;
     km_status init_build(int32_t* M_out, void* td_out) override {
+        KM_TRY(clear_fp1_done());
         if (sharded) return fail(KM_EINVAL, "init_build on a sharded handle; use kmedoids_build_* phases");
         KM_TRY(bd_init());
         if (build_graph < 0) {
@@ -2167,13 +2280,62 @@ km_status kmedoids_run(km_handle* h, int32_t use_build, km_variant variant, int3
         KM_TRY(h->impl->get_state(medoids_out, assignment_out, td_out, n_iter_out, n_swaps_out));
         return conv ? KM_OK : KM_NOT_CONVERGED;
     }
-    for (int it = 0; it < max_iter; ++it) {
-        km_status s = h->impl->swap_iter(variant, nullptr, nullptr);
-        if (s == KM_CONVERGED) { st = KM_OK; break; }
-        if (s != KM_OK) return s;
+    if (variant == KM_FASTPAM1) {                   // iterations queued one ahead (no host round trip)
+        bool conv = false;
+        KM_TRY(h->impl->fp1_run_pipelined(max_iter, nullptr, nullptr, &conv));
+        if (conv) st = KM_OK;
+    } else {
+        for (int it = 0; it < max_iter; ++it) {
+            km_status s = h->impl->swap_iter(variant, nullptr, nullptr);
+            if (s == KM_CONVERGED) { st = KM_OK; break; }
+            if (s != KM_OK) return s;
+        }
     }
     KM_TRY(h->impl->get_state(medoids_out, assignment_out, td_out, n_iter_out, n_swaps_out));
     return st;
+}
+
+km_status kmedoids_swap_iters(km_handle* h, int32_t count, int32_t* iters_out, int32_t* swaps_out, void* td_out) {
+    KM_H();
+    if (count < 1) return fail(KM_EINVAL, "count=%d must be >= 1", count);
+    bool conv = false;
+    int32_t it = 0, sw = 0;
+    KM_TRY(h->impl->fp1_run_pipelined(count, &it, &sw, &conv));
+    if (iters_out) *iters_out = it;
+    if (swaps_out) *swaps_out = sw;
+    if (td_out) KM_TRY(h->impl->get_state(nullptr, nullptr, td_out, nullptr, nullptr));
+    return conv ? KM_CONVERGED : KM_OK;
+}
+
+// The device copy of D of kmedoids_run_host is kept between calls (one
+// buffer per process, reused when large enough) so a repeated job pays no
+// 10 GB cudaMalloc / cudaFree (round 1: occasional 0.3-0.6 s stalls around
+// them); kmedoids_release_host_cache frees it.  A call that finds the buffer
+// busy (concurrent jobs) allocates its own.
+namespace {
+struct HostJobCache {
+    std::mutex mu;
+    void* p = nullptr;
+    size_t bytes = 0;
+    int dev = -1;
+};
+HostJobCache g_job;
+}  // namespace
+
+km_status kmedoids_release_host_cache(void) {
+    g_err.clear();
+    std::lock_guard<std::mutex> lk(g_job.mu);
+    if (g_job.p) {
+        int cur = 0;
+        cudaGetDevice(&cur);
+        if (g_job.dev != cur) cudaSetDevice(g_job.dev);
+        cudaError_t e = cudaFree(g_job.p);
+        if (g_job.dev != cur) cudaSetDevice(cur);
+        g_job.p = nullptr;
+        g_job.bytes = 0;
+        if (e != cudaSuccess) return fail(KM_ECUDA, "cudaFree: %s", cudaGetErrorString(e));
+    }
+    return KM_OK;
 }
 
 km_status kmedoids_run_host(const void* D_host, km_dtype dtype, int64_t n, int64_t ld, int32_t k, int32_t use_build,
@@ -2193,8 +2355,23 @@ km_status kmedoids_run_host(const void* D_host, km_dtype dtype, int64_t n, int64
     };
     const auto t0 = now();
     void* Dd = nullptr;
-    cudaError_t e = cudaMalloc(&Dd, bytes);
-    if (e != cudaSuccess) return fail(KM_ENOMEM, "cudaMalloc(%zu) for D failed: %s", bytes, cudaGetErrorString(e));
+    int dev = 0;
+    cudaGetDevice(&dev);
+    std::unique_lock<std::mutex> lk(g_job.mu, std::try_to_lock);
+    const bool cached = lk.owns_lock();
+    cudaError_t e = cudaSuccess;
+    if (cached && g_job.p && (g_job.bytes < bytes || g_job.dev != dev)) {
+        if (g_job.dev == dev) cudaFree(g_job.p);
+        else { cudaSetDevice(g_job.dev); cudaFree(g_job.p); cudaSetDevice(dev); }
+        g_job.p = nullptr; g_job.bytes = 0;
+    }
+    if (cached && g_job.p) {
+        Dd = g_job.p;
+    } else {
+        e = cudaMalloc(&Dd, bytes);
+        if (e != cudaSuccess) return fail(KM_ENOMEM, "cudaMalloc(%zu) for D failed: %s", bytes, cudaGetErrorString(e));
+        if (cached) { g_job.p = Dd; g_job.bytes = bytes; g_job.dev = dev; }
+    }
     const auto t1 = now();
     cudaStream_t st = (cudaStream_t)cuda_stream;
     km_status s = KM_OK;
@@ -2215,7 +2392,7 @@ km_status kmedoids_run_host(const void* D_host, km_dtype dtype, int64_t n, int64
     kmedoids_destroy(h);
     cudaStreamSynchronize(st);
     const auto t5 = now();
-    cudaFree(Dd);
+    if (!cached) cudaFree(Dd);
     const auto t6 = now();
     if (prof)
         fprintf(stderr, "[kmedoids_run_host] ms: malloc %.1f h2d %.1f create %.1f run %.1f destroy %.1f free %.1f\n",

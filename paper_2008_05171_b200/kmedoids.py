@@ -66,9 +66,11 @@ def load_library() -> ctypes.CDLL:
         "kmedoids_set_medoids": [vp, vp],
         "kmedoids_init_build": [vp, vp, vp],
         "kmedoids_swap_iter": [vp, ctypes.c_int, vp, vp],
+        "kmedoids_swap_iters": [vp, i32, vp, vp, vp],
         "kmedoids_run": [vp, i32, ctypes.c_int, i32, vp, vp, vp, vp, vp],
         "kmedoids_run_host": [vp, ctypes.c_int, i64, i64, i32, i32, vp, ctypes.c_int, i32, vp, vp, vp, vp, vp, vp],
         "kmedoids_get_state": [vp, vp, vp, vp, vp, vp],
+        "kmedoids_release_host_cache": [],
         "kmedoids_get_cache": [vp, vp, vp, vp, vp],
         "kmedoids_eval_candidates": [vp, vp, vp],
         "kmedoids_set_profiling": [vp, i32],
@@ -237,6 +239,14 @@ class KMedoids:
         s = _check(load_library().kmedoids_swap_iter(self.h, VARIANTS[variant], psw, ptd), ok=(KM_OK, KM_CONVERGED))
         return s == KM_CONVERGED, int(sw[0]), td[0].item()
 
+    def swap_iters(self, count: int):
+        """Up to `count` FastPAM1 iterations queued back to back (no host round
+        trip between them); returns (converged, iterations, swaps, td)."""
+        it = np.zeros(1, np.int32); sw = np.zeros(1, np.int32); td = np.zeros(1, self.acc)
+        s = _check(load_library().kmedoids_swap_iters(self.h, int(count), _p(it), _p(sw), _p(td)),
+                   ok=(KM_OK, KM_CONVERGED))
+        return s == KM_CONVERGED, int(it[0]), int(sw[0]), td[0].item()
+
     def run(self, use_build=True, variant="fastpam1", max_iter=2000) -> Result:
         M = np.zeros(self.k, np.int32)
         asg = np.zeros(self.n, np.int32)
@@ -316,9 +326,9 @@ class KMedoids:
         if M.shape != (self.k,):
             raise ValueError(f"expected {self.k} medoids")
         if (not columns.is_cuda or columns.device != self.D.device or not columns.is_contiguous()
-                or columns.element_size() != 4 or columns.numel() < self.k * self.n):
-            raise ValueError(f"columns must be a contiguous 4-byte CUDA tensor on {self.D.device} "
-                             f"holding k*n = {self.k * self.n} elements")
+                or columns.numel() * columns.element_size() < 4 * self.k * self.n):
+            raise ValueError(f"columns must be a contiguous CUDA tensor on {self.D.device} holding "
+                             f"k*n = {self.k * self.n} 4-byte dissimilarities")
         _check(load_library().kmedoids_shard_set_medoids(self.h, _p(M), ctypes.c_void_p(columns.data_ptr())))
 
     def shard_eval(self):
@@ -453,6 +463,11 @@ def kmedoids_run_host(D_host: np.ndarray, k: int, use_build=True, medoids=None, 
                                      ctypes.c_void_p(st.cuda_stream), _p(M), _p(asg), _p(td), _p(it), _p(sw)),
                ok=(KM_OK, KM_NOT_CONVERGED))
     return Result(M, asg, td[0].item(), int(it[0]), int(sw[0]), s == KM_OK)
+
+
+def kmedoids_release_host_cache():
+    """Free the device copy of D that kmedoids_run_host keeps between calls."""
+    _check(load_library().kmedoids_release_host_cache())
 
 
 def pinned_empty(shape, dtype):

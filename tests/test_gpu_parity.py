@@ -103,6 +103,62 @@ def test_c1_build_fastpam1_bit_exact():
     assert st.td == ref.td and st.n_iter == ref.n_iter and st.n_swaps == ref.n_swaps
 
 
+@pytest.mark.parametrize("parts", [None, "1", "3", "37"])
+def test_part_counts_trace_exact(parts, monkeypatch):
+    """Any number of stream row parts (one part; ragged parts; the default)
+    gives the oracle's exact trace on integer data with many ties, on several
+    column tiles (n > 896): the combine (a4) completes every segment cut by a
+    part boundary."""
+    if parts:
+        monkeypatch.setenv("KM_PARTS", parts)
+    rng = np.random.default_rng(77)
+    for n, k, hi in [(2100, 9, 4), (1031, 17, 100000), (3001, 5, 50)]:
+        D = rand_int(rng, n, hi, symmetric=bool(n % 2))
+        M0 = rng.choice(n, size=k, replace=False).astype(np.int32)
+        ref = oracle.swap_run(D, M0, oracle.FASTPAM1)
+        km = KM(to_dev(D), n, k)
+        km.set_medoids(M0)
+        tr = gpu_trace(km, k)
+        got = [(ch[0], cs[0]) for ch, cs, _ in tr if ch]
+        assert got == [(i, c) for i, c, _ in ref.trace], (n, k)
+        st = km.get_state()
+        assert st.td == ref.td and st.n_iter == ref.n_iter and st.medoids.tolist() == ref.medoids.tolist()
+        km.close()
+
+
+@pytest.mark.parametrize("seed", range(4))
+def test_swap_iters_pipelined_equals_oracle(seed):
+    """kmedoids_swap_iters (FastPAM1 iterations queued one ahead, sticky
+    convergence) reaches the oracle's exact end state and counts; a bounded
+    call stops after `count` passes and the next call continues; after
+    convergence further calls are no-ops (no pass counted); other variants and
+    set_medoids clear the sticky flag."""
+    rng = np.random.default_rng(4000 + seed)
+    n, k = int(rng.choice([300, 1500, 2500])), int(rng.integers(3, 12))
+    D = rand_int(rng, n, int(rng.choice([4, 1000])), symmetric=bool(seed % 2))
+    M0 = rng.choice(n, size=k, replace=False).astype(np.int32)
+    ref = oracle.swap_run(D, M0, oracle.FASTPAM1)
+    km = KM(to_dev(D), n, k)
+    km.set_medoids(M0)
+    first = min(3, ref.n_iter)
+    conv, it, sw, td = km.swap_iters(first)
+    assert it == first and sw == min(first, ref.n_swaps) and conv == (first == ref.n_iter)
+    conv, it2, sw2, td = km.swap_iters(2000)
+    assert conv or first == ref.n_iter
+    st = km.get_state()
+    assert st.medoids.tolist() == ref.medoids.tolist() and st.td == ref.td == td
+    assert st.n_iter == ref.n_iter and st.n_swaps == ref.n_swaps
+    assert st.assignment.tolist() == ref.assignment.tolist()
+    conv, it3, sw3, _ = km.swap_iters(5)                     # sticky: nothing runs, nothing counted
+    assert conv and sw3 == 0 and km.get_state().n_iter == ref.n_iter
+    c2 = km.swap_iter("fastpam2")                            # other variant: a real (non-improving) pass
+    assert c2[0] and km.get_state().n_iter == ref.n_iter + 1
+    km.set_medoids(M0)                                       # fresh state: FastPAM1 runs again
+    tr = gpu_trace(km, k)
+    got = [(ch[0], cs[0]) for ch, cs, _ in tr if ch]
+    assert got == [(i, c) for i, c, _ in ref.trace]
+
+
 @pytest.mark.parametrize("seed", range(12))
 def test_random_int_instances_trace_exact(seed):
     rng = np.random.default_rng(1000 + seed)

@@ -717,3 +717,69 @@ def test_fastpam2_slot_best_equals_bruteforce():
         sv, sc = oracle.fastpam2_slot_best(D, M, c, oracle.removal_loss(c, k))
         for i in range(k):
             assert (sv[i], sc[i]) == min((bf_delta(D, M, i, x), x) for x in range(n) if x not in M)
+
+
+# ---------- NEXT-3 FastCLARA from points (reading C2) ----------
+
+def _cdist_f32(X):
+    from scipy.spatial.distance import cdist
+    return cdist(X.astype(np.float64), X.astype(np.float64)).astype(np.float32)
+
+
+def _cdist_u32(Xq):
+    from scipy.spatial.distance import cdist
+    return cdist(Xq, Xq, "cityblock").astype(np.uint32)
+
+
+@pytest.mark.parametrize("metric", ["l1", "l2"])
+def test_td_points_equals_td_of_the_matrix(metric):
+    """oracle.td_points (distances recomputed from the points) equals the
+    definition's TD on the dissimilarity matrix built by scipy (a library
+    routine of the same distances), with the assignment = sorted (d, slot)."""
+    rng = np.random.default_rng(71)
+    for n, d, k in [(40, 3, 4), (97, 8, 7), (150, 1, 2)]:
+        if metric == "l2":
+            X = rng.normal(size=(n, d)).astype(np.float32)
+            D = _cdist_f32(X)
+        else:
+            X = rng.integers(-300, 300, size=(n, d)).astype(np.int32)
+            D = _cdist_u32(X)
+        M = rng.choice(n, size=k, replace=False)
+        t, mins, asg = oracle.td_points(X, metric, M)
+        ref = bf_td(D, M)
+        if metric == "l2":
+            assert t == pytest.approx(ref, rel=1e-12)
+        else:
+            assert t == ref
+        for o in range(n):
+            order = sorted(range(k), key=lambda j: (D[o, M[j]], j))
+            assert asg[o] == order[0] and mins[o] == D[o, M[order[0]]]
+
+
+@pytest.mark.parametrize("metric", ["l1", "l2"])
+def test_clara_points_full_sample_is_pam_and_best_wins(metric):
+    """One sample holding every point makes CLARA-from-points the PAM
+    (BUILD + FastPAM1) of the whole set on the scipy-built matrix; with
+    several samples no sample's PAM solution has a smaller TD over all
+    points than the one returned."""
+    rng = np.random.default_rng(72)
+    n, d, k = 70, 4, 3
+    if metric == "l2":
+        X = rng.normal(size=(n, d)).astype(np.float32)
+        D = _cdist_f32(X)
+    else:
+        X = rng.integers(0, 500, size=(n, d)).astype(np.int32)
+        D = _cdist_u32(X)
+    t, j, M, asg = oracle.clara_points(X, metric, k, [np.arange(n)])
+    Mb, _, _ = oracle.build_init(D, k)
+    ref = oracle.swap_run(D, Mb, oracle.FASTPAM1)
+    assert j == 0 and M.tolist() == ref.medoids.tolist()
+    assert (t == ref.td) if metric == "l1" else t == pytest.approx(ref.td, rel=1e-12)
+    samples = [rng.choice(n, size=25, replace=False) for _ in range(4)]
+    t, j, M, asg = oracle.clara_points(X, metric, k, samples)
+    assert (t == bf_td(D, M)) if metric == "l1" else t == pytest.approx(bf_td(D, M), rel=1e-12)
+    for S in samples:
+        Dj = np.ascontiguousarray(D[np.ix_(S, S)])
+        Mj, _, _ = oracle.build_init(Dj, k)
+        rj = oracle.swap_run(Dj, Mj, oracle.FASTPAM1)
+        assert bf_td(D, S[rj.medoids]) >= t - 1e-9
