@@ -169,8 +169,8 @@ km_status kmedoids_run_host(const void* D_host, km_dtype dtype, int64_t n, int64
                             int32_t* n_swaps_out);
 
 /* kmedoids_run_host keeps its device copy of D between calls (one buffer per
- * process, reused while large enough, so repeated jobs pay no allocation);
- * this frees it.  Safe to call at any time from any thread; KM_OK if there
+ * process, reused while large enough, so repeated jobs pay no allocation),
+ * and kmedoids_clara_points its per-sample scratch; this frees both.  Safe to call at any time from any thread; KM_OK if there
  * was nothing to free. */
 km_status kmedoids_release_host_cache(void);
 
@@ -239,6 +239,34 @@ km_status kmedoids_launch_count(km_handle* h, int64_t* count_out);
 typedef enum { KM_METRIC_L2_F32 = 0, KM_METRIC_L1_U32 = 1 } km_metric;
 km_status kmedoids_dissimilarity(const void* X, km_metric metric, int64_t n, int32_t d, void* D, int64_t ld,
                                  int64_t col_begin, int64_t col_end, void* cuda_stream);
+
+/* NEXT-3 FastCLARA from points, without the n x n matrix ("the
+ * remaining objects are assigned to their closest medoid", P:1109-1129,
+ * P:618-620; reading C2), single GPU.  X (device, n x d row-major,
+ * 1 <= d <= 128): float32 coordinates for KM_METRIC_L2_F32, int32 for
+ * KM_METRIC_L1_U32.  For each of the nsamples caller-drawn samples (host
+ * samples[nsamples][s], distinct indices in [0, n), k < s <= n
+ * suggests s = 80 + 4k): the s x s dissimilarity matrix of the sample's
+ * points by the definitions (L2: fp64 sums, sqrt, rounded to float32; L1:
+ * exact, stored as uint32), PAM on it (BUILD, then SWAP with `variant` to
+ * convergence), medoids mapped back to point indices, and TD over ALL n
+ * objects with every distance recomputed from the points the same way (L2:
+ * double of the float32 distance; L1 int64).  The smallest (TD, sample
+ * index) wins.  Outputs (host, each may be NULL): medoids_out[k],
+ * td_out (double* for L2, int64_t* for L1), best_sample_out, assignment_out[n]
+ * (slot of each object's closest winning medoid, smallest slot on ties).
+ * Device memory: O(8 s^2 + n) scratch (up to 8 s x s buffers and nested
+ * handles), kept between calls with the same (device, s, k, n) so later
+ * samples replay each nested BUILD from its CUDA graph; freed by
+ * kmedoids_release_host_cache.
+ * Samples run concurrently (up to 8, each on its own stream); X must stay
+ * unchanged during the call, which synchronises cuda_stream first.
+ * Errors: KM_EINVAL (sizes, bad or duplicate indices, metric), KM_ENOMEM,
+ * KM_ECUDA. */
+km_status kmedoids_clara_points(const void* X, km_metric metric, int64_t n, int32_t d, int32_t k, int32_t nsamples,
+                                int32_t s, const int32_t* samples, km_variant variant, void* cuda_stream,
+                                int32_t* medoids_out, void* td_out, int32_t* best_sample_out,
+                                int32_t* assignment_out);
 
 /* ---------------- sharded (column-slab) phase API ----------------------
  * A sharded SWAP iteration on R ranks is, on every rank:

@@ -6,5 +6,6 @@ kernels in ``csrc/``).  ``kmedoids`` is its thin ctypes binding and
 ``torch.distributed``.
 """
 from .kmedoids import (KMedoids, KMError, Result, kmedoids_create, kmedoids_destroy, kmedoids_init_build,  # noqa: F401
-                       kmedoids_dissimilarity, kmedoids_run, kmedoids_run_host, kmedoids_set_medoids, kmedoids_swap_iter,
+                       kmedoids_clara_points, kmedoids_dissimilarity, kmedoids_run, kmedoids_run_host, kmedoids_set_medoids, kmedoids_swap_iter,
+                       kmedoids_release_host_cache,
                        load_library)

@@ -25,6 +25,7 @@
 #include "km_dist.cuh"
 #include "km_init.cuh"
 #include "km_build_delta.cuh"
+#include "km_clara.cuh"
 
 namespace {
 
@@ -2261,6 +2262,217 @@ km_status kmedoids_clara(km_handle* h, int32_t nsamples, int32_t s, const int32_
     return h->impl->clara(nsamples, s, samples, variant, medoids_out, td_out, best_sample_out);
 }
 
+// ---- FastCLARA from points (NEXT-3 without the n x n matrix) ----------------
+}  // extern "C"
+namespace {
+
+template <typename T>
+struct ClaraPointsCache {
+    using A = typename km::Acc<T>::type;
+    struct Slot {
+        T* buf = nullptr; int* idx = nullptr; int* med = nullptr; A* part = nullptr; A* tdv = nullptr;
+        cudaStream_t st = nullptr; std::unique_ptr<Impl<T>> sub;
+    };
+    std::mutex mu;
+    int dev = -1, s = 0, k = 0;
+    int64_t n = 0;
+    std::vector<Slot> slots;
+    void clear() {
+        int cur = 0;
+        cudaGetDevice(&cur);
+        if (dev >= 0 && dev != cur) cudaSetDevice(dev);
+        for (auto& sl : slots) {
+            sl.sub.reset();
+            if (sl.st) cudaStreamDestroy(sl.st);
+            cudaFree(sl.buf); cudaFree(sl.idx); cudaFree(sl.med); cudaFree(sl.part); cudaFree(sl.tdv);
+        }
+        if (dev >= 0 && dev != cur) cudaSetDevice(cur);
+        slots.clear();
+        dev = -1; s = 0; k = 0; n = 0;
+    }
+    static ClaraPointsCache& get() {
+        static ClaraPointsCache* c = new ClaraPointsCache;   // never destroyed: no CUDA calls at exit
+        return *c;
+    }
+};
+
+template <typename T>
+km_status clara_points_run(const void* Xv, int64_t n, int32_t d, int32_t k, int32_t ns, int32_t s,
+                           const int32_t* samples, km_variant variant, cudaStream_t ust, int32_t* M_out,
+                           void* td_out, int32_t* best_out, int32_t* asg_out) {
+    using A = typename km::Acc<T>::type;
+    using P = typename km::PointOf<T>::type;
+    const P* X = static_cast<const P*>(Xv);
+    // sample validation: distinct indices in range
+    {
+        std::vector<char> seen((size_t)n, 0);
+        for (int j = 0; j < ns; ++j) {
+            const int32_t* S = samples + (size_t)j * s;
+            for (int a = 0; a < s; ++a) {
+                if (S[a] < 0 || S[a] >= n) return fail(KM_EINVAL, "sample %d: index %d out of range", j, S[a]);
+                if (seen[S[a]]) return fail(KM_EINVAL, "sample %d: duplicate index %d", j, S[a]);
+                seen[S[a]] = 1;
+            }
+            for (int a = 0; a < s; ++a) seen[S[a]] = 0;
+        }
+    }
+    const int64_t lds = cdiv(s, 4) * 4;
+    const int conc = std::min(ns, 8);
+    const int tdb = (int)cdiv(n, 256);                      // k_td_points blocks
+    const int kc = std::max(1, std::min<int>(k, (46 * 1024) / (int)(d * sizeof(P))));   // < 48 KB with the statics
+    const size_t td_smem = (size_t)kc * d * sizeof(P);
+    // the per-sample slots (stream, s x s buffer, nested handle) are kept
+    // between calls with the same (device, s, k, n) so a handle's BUILD is
+    // replayed from its CUDA graph on later samples and calls
+    auto& cache = ClaraPointsCache<T>::get();
+    std::unique_lock<std::mutex> lk(cache.mu);
+    int dev = 0;
+    KM_CK(cudaGetDevice(&dev));
+    using Slot = typename ClaraPointsCache<T>::Slot;
+    std::vector<Slot>& slots = cache.slots;
+    if (cache.dev != dev || cache.s != s || cache.k != k || cache.n != n) {
+        cache.clear();
+        cache.dev = dev; cache.s = s; cache.k = k; cache.n = n;
+    }
+    auto cleanup = [&]() { cache.clear(); };
+    KM_CK(cudaStreamSynchronize(ust));                      // X is ready before other streams read it
+    while ((int)slots.size() < conc) {
+        slots.emplace_back();
+        Slot& sl = slots.back();
+        cudaError_t e = cudaMalloc(&sl.buf, (size_t)s * lds * sizeof(T));
+        if (e == cudaSuccess) e = cudaMalloc(&sl.idx, (size_t)s * sizeof(int));
+        if (e == cudaSuccess) e = cudaMalloc(&sl.med, (size_t)k * sizeof(int));
+        if (e == cudaSuccess) e = cudaMalloc(&sl.part, (size_t)tdb * sizeof(A));
+        if (e == cudaSuccess) e = cudaMalloc(&sl.tdv, sizeof(A));
+        if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&sl.st, cudaStreamNonBlocking);
+        if (e == cudaSuccess) e = cudaMemsetAsync(sl.buf, 0, (size_t)s * lds * sizeof(T), sl.st);
+        if (e != cudaSuccess) { cleanup(); cudaGetLastError(); return fail(KM_ENOMEM, "CLARA scratch: %s", cudaGetErrorString(e)); }
+        sl.sub.reset(new Impl<T>());
+        const km_status r = sl.sub->init(sl.buf, s, lds, 0, s, k, sl.st);
+        if (r != KM_OK) { cleanup(); return r; }
+    }
+    std::vector<std::vector<int32_t>> Mg((size_t)ns, std::vector<int32_t>((size_t)k));
+    std::vector<A> tds((size_t)ns);
+    std::vector<km_status> res((size_t)ns, KM_OK);
+    std::vector<std::string> errs((size_t)ns);
+    auto worker = [&](int si) {
+        Slot& sl = slots[si];
+        Impl<T>& sub = *sl.sub;
+        for (int j = si; j < ns; j += conc) {
+            const int32_t* S = samples + (size_t)j * s;
+            km_status r = KM_OK;
+            auto ck = [&](cudaError_t e, const char* what) {
+                if (r == KM_OK && e != cudaSuccess) r = fail(KM_ECUDA, "%s: %s", what, cudaGetErrorString(e));
+            };
+            ck(cudaMemcpyAsync(sl.idx, S, s * sizeof(int32_t), cudaMemcpyHostToDevice, sl.st), "sample indices");
+            if (r == KM_OK) {
+                const dim3 g((unsigned)cdiv(s, 32), (unsigned)cdiv(s, 32));
+                km::k_subdist_exact<T><<<g, 256, 64 * (size_t)d * sizeof(P), sl.st>>>(X, d, sl.idx, s, sl.buf, lds);
+                ck(cudaGetLastError(), "sample dissimilarities");
+            }
+            if (r == KM_OK) r = sub.init_build(nullptr, nullptr);
+            if (r == KM_OK) {
+                if (variant == KM_FASTPAM1) {
+                    bool conv = false;
+                    r = sub.fp1_run_pipelined(2000, nullptr, nullptr, &conv);
+                } else {
+                    for (int it = 0; r == KM_OK && it < 2000; ++it) {
+                        const km_status q = sub.swap_iter(variant, nullptr, nullptr);
+                        if (q == KM_CONVERGED) break;
+                        if (q != KM_OK) r = q;
+                    }
+                }
+            }
+            std::vector<int32_t> Mloc((size_t)k);
+            if (r == KM_OK) r = sub.get_state(Mloc.data(), nullptr, nullptr, nullptr, nullptr);
+            if (r == KM_OK) {
+                for (int i = 0; i < k; ++i) Mg[j][i] = S[Mloc[i]];
+                // TD over all n objects from the points (Eq. eqn:td, reading C2)
+                ck(cudaMemcpyAsync(sl.med, Mg[j].data(), k * sizeof(int32_t), cudaMemcpyHostToDevice, sl.st), "medoids");
+                if (r == KM_OK) {
+                    km::k_td_points<T, A><<<tdb, 256, td_smem, sl.st>>>(X, (int)n, d, sl.med, k, kc, sl.part, nullptr);
+                    km::k_sum_partials<A><<<1, 32, 0, sl.st>>>(sl.part, tdb, sl.tdv);
+                    ck(cudaGetLastError(), "TD from points");
+                }
+                A v = 0;
+                ck(cudaMemcpyAsync(&v, sl.tdv, sizeof(A), cudaMemcpyDeviceToHost, sl.st), "TD");
+                ck(cudaStreamSynchronize(sl.st), "sample");
+                tds[j] = v;
+            }
+            res[j] = r;
+            if (r != KM_OK) errs[j] = g_err;
+        }
+    };
+    {
+        std::vector<std::thread> th;
+        for (int t = 1; t < conc; ++t) th.emplace_back(worker, t);
+        worker(0);
+        for (auto& x : th) x.join();
+    }
+    for (int j = 0; j < ns; ++j)
+        if (res[j] != KM_OK) { cleanup(); return fail(res[j], "CLARA sample %d: %s", j, errs[j].c_str()); }
+    int bj = 0;
+    for (int j = 1; j < ns; ++j)
+        if (tds[j] < tds[bj]) bj = j;                       // smallest (TD, sample index)
+    if (asg_out) {
+        // the assignment of every object to the winning medoids
+        Slot& sl = slots[0];
+        int* asg = nullptr;
+        cudaError_t e = cudaMalloc(&asg, (size_t)n * sizeof(int));
+        if (e == cudaSuccess) e = cudaMemcpyAsync(sl.med, Mg[bj].data(), k * sizeof(int32_t), cudaMemcpyHostToDevice, sl.st);
+        if (e == cudaSuccess) {
+            km::k_td_points<T, A><<<tdb, 256, td_smem, sl.st>>>(X, (int)n, d, sl.med, k, kc, sl.part, asg);
+            e = cudaGetLastError();
+        }
+        if (e == cudaSuccess) e = cudaMemcpyAsync(asg_out, asg, (size_t)n * sizeof(int), cudaMemcpyDeviceToHost, sl.st);
+        if (e == cudaSuccess) e = cudaStreamSynchronize(sl.st);
+        cudaFree(asg);
+        if (e != cudaSuccess) { cleanup(); return fail(KM_ECUDA, "CLARA assignment: %s", cudaGetErrorString(e)); }
+    }
+    if (M_out) memcpy(M_out, Mg[bj].data(), k * sizeof(int32_t));
+    if (td_out) memcpy(td_out, &tds[bj], sizeof(A));
+    if (best_out) *best_out = bj;
+    return KM_OK;
+}
+
+}  // namespace
+
+void clara_points_release() {
+    {
+        auto& c = ClaraPointsCache<float>::get();
+        std::lock_guard<std::mutex> lk(c.mu);
+        c.clear();
+    }
+    auto& c = ClaraPointsCache<uint32_t>::get();
+    std::lock_guard<std::mutex> lk(c.mu);
+    c.clear();
+}
+
+extern "C" {
+
+km_status kmedoids_clara_points(const void* X, km_metric metric, int64_t n, int32_t d, int32_t k, int32_t nsamples,
+                                int32_t s, const int32_t* samples, km_variant variant, void* cuda_stream,
+                                int32_t* medoids_out, void* td_out, int32_t* best_sample_out,
+                                int32_t* assignment_out) {
+    g_err.clear();
+    if (!X || !samples) return fail(KM_EINVAL, "X and samples must not be NULL");
+    if (n < 3 || n >= (int64_t)INT32_MAX) return fail(KM_EINVAL, "n=%lld out of range [3, 2^31)", (long long)n);
+    if (d < 1 || d > km::CLARA_MAXD) return fail(KM_EINVAL, "d=%d must be in [1, %d]", d, km::CLARA_MAXD);
+    if (k < 2 || k > MAX_K) return fail(KM_EINVAL, "k=%d out of range [2, %d]", k, MAX_K);
+    if (nsamples < 1) return fail(KM_EINVAL, "nsamples must be >= 1");
+    if (s <= k || s > n) return fail(KM_EINVAL, "sample size s=%d must satisfy k < s <= n", s);
+    if (variant != KM_FASTPAM1 && variant != KM_FASTPAM2 && variant != KM_FASTERPAM)
+        return fail(KM_EINVAL, "unknown variant %d", (int)variant);
+    cudaStream_t st = (cudaStream_t)cuda_stream;
+    if (metric == KM_METRIC_L2_F32)
+        return clara_points_run<float>(X, n, d, k, nsamples, s, samples, variant, st, medoids_out, td_out,
+                                       best_sample_out, assignment_out);
+    if (metric == KM_METRIC_L1_U32)
+        return clara_points_run<uint32_t>(X, n, d, k, nsamples, s, samples, variant, st, medoids_out, td_out,
+                                          best_sample_out, assignment_out);
+    return fail(KM_EINVAL, "unknown metric %d", (int)metric);
+}
+
 km_status kmedoids_swap_iter(km_handle* h, km_variant variant, int32_t* swaps_done_out, void* td_out) {
     KM_H();
     return h->impl->swap_iter(variant, swaps_done_out, td_out);
@@ -2324,6 +2536,7 @@ HostJobCache g_job;
 
 km_status kmedoids_release_host_cache(void) {
     g_err.clear();
+    clara_points_release();
     std::lock_guard<std::mutex> lk(g_job.mu);
     if (g_job.p) {
         int cur = 0;

@@ -102,6 +102,7 @@ def load_library() -> ctypes.CDLL:
         "kmedoids_init_weighted": [vp, vp, vp, vp],
         "kmedoids_init_lab": [vp, i32, vp, vp, vp],
         "kmedoids_clara": [vp, i32, i32, vp, ctypes.c_int, vp, vp, vp],
+        "kmedoids_clara_points": [vp, ctypes.c_int, i64, i32, i32, i32, i32, vp, ctypes.c_int, vp, vp, vp, vp, vp],
     }
     for name, args in sig.items():
         f = getattr(lib, name)
@@ -511,3 +512,32 @@ def kmedoids_dissimilarity(X, metric="l2", D=None, col_begin=0, col_end=None, st
     _check(lib.kmedoids_dissimilarity(ctypes.c_void_p(X.data_ptr()), code, n, d, ctypes.c_void_p(D.data_ptr()),
                                       int(D.stride(0)), int(col_begin), int(col_end), ctypes.c_void_p(st.cuda_stream)))
     return D
+
+
+def kmedoids_clara_points(X, metric, k: int, samples, variant="fastpam1", stream=None, assignment=False):
+    """FastCLARA from points without the n x n matrix (kmedoids.h): X is a
+    (n, d) CUDA tensor (float32 for "l2", int32 for "l1"), samples an
+    (nsamples, s) array of distinct point indices.  Returns (medoids, TD,
+    best sample index, assignment or None)."""
+    import torch
+    lib = load_library()
+    if not X.is_cuda or X.dim() != 2:
+        raise ValueError("X must be a 2-D CUDA tensor")
+    code = {"l2": KM_METRIC_L2_F32, "l1": KM_METRIC_L1_U32}[metric]
+    want = torch.float32 if code == KM_METRIC_L2_F32 else torch.int32
+    if X.dtype != want:
+        raise TypeError(f"metric {metric} needs X of dtype {want}")
+    X = X.contiguous()
+    n, d = X.shape
+    q = np.ascontiguousarray(np.asarray(samples, np.int32))
+    if q.ndim != 2:
+        raise ValueError("samples must be (nsamples, s)")
+    M = np.zeros(k, np.int32)
+    td = np.zeros(1, np.float64 if code == KM_METRIC_L2_F32 else np.int64)
+    b = np.zeros(1, np.int32)
+    asg = np.zeros(n, np.int32) if assignment else None
+    st = stream if stream is not None else torch.cuda.current_stream(X.device)
+    _check(lib.kmedoids_clara_points(ctypes.c_void_p(X.data_ptr()), code, n, d, int(k), q.shape[0], q.shape[1],
+                                     _p(q), VARIANTS[variant], ctypes.c_void_p(st.cuda_stream), _p(M), _p(td),
+                                     _p(b), _p(asg) if asg is not None else None))
+    return M, td[0].item(), int(b[0]), asg

@@ -190,6 +190,11 @@ class TorchComm:
         cb = colb * maxcnt
         self.dist.all_gather_into_tensor(crecv[:cb * self.world], csend[:cb], group=self.group)
 
+    def allgather_object(self, obj):
+        out = [None] * self.world
+        self.dist.all_gather_object(out, obj, group=self.group)
+        return out
+
     def max_over_ranks(self, x: float) -> float:
         import torch
         dev = "cuda" if self.dist.get_backend(self.group) == "nccl" else "cpu"
@@ -408,3 +413,33 @@ class CudaShard:
 
     def __getattr__(self, name):       # shard_eval, shard_select, ... -> the handle
         return getattr(self.km, name)
+
+
+# ---------------------------------------------------------------------------
+# FastCLARA from points over several GPUs (NEXT-3; "CLARA can be
+# trivially parallelized")
+# ---------------------------------------------------------------------------
+def clara_points(X, metric: str, k: int, samples, comm, variant: str = "fastpam1", runner=None):
+    """Samples are independent units: rank r runs samples r, r + R, ... on its
+    GPU (kmedoids_clara_points over its share; X replicated, no D anywhere),
+    then one all-gather of (TD, sample index, medoids) per rank and every rank
+    takes the same smallest (TD, sample index).  No data-path collective other
+    than that one small exchange.  Returns (medoids, TD, best sample index).
+
+    ``runner(X, metric, k, samples, variant) -> (medoids, TD, local best)``
+    defaults to the CUDA library call (the CPU tests pass their own)."""
+    if runner is None:
+        from .kmedoids import kmedoids_clara_points
+
+        def runner(X_, m_, k_, s_, v_):
+            M, td, b, _ = kmedoids_clara_points(X_, m_, k_, s_, v_)
+            return M, td, b
+    samples = np.asarray(samples)
+    mine = list(range(comm.rank, len(samples), comm.world))
+    rec = None
+    if mine:
+        M, td, b = runner(X, metric, k, samples[mine], variant)
+        rec = (td, mine[b], [int(x) for x in M])
+    recs = [r for r in comm.allgather_object(rec) if r is not None]
+    td, j, M = min(recs, key=lambda r: (r[0], r[1]))
+    return np.asarray(M, np.int32), td, j

@@ -315,3 +315,50 @@ def test_gloo_world2_fp2_exchange_layout():
             for j in range(maxcnt):
                 blk = cols[(r * maxcnt + j) * colb:(r * maxcnt + j + 1) * colb]
                 assert (blk == (10 * r + j) % 251).all()
+
+
+# ---------- FastCLARA from points over ranks (NEXT-3) ----------
+
+def _oracle_runner(X, metric, k, samples, variant):
+    t, j, M, _ = oracle.clara_points(X, metric, k, samples, variant)
+    return M, t, j
+
+
+def _clara_worker(rank, world, port, q):
+    import torch.distributed as dist
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        rng = np.random.default_rng(91)
+        X = rng.integers(0, 400, size=(160, 3)).astype(np.int32)
+        samples = np.stack([rng.choice(160, size=30, replace=False) for _ in range(5)])
+        M, td, j = parallel.clara_points(X, "l1", 4, samples, parallel.TorchComm(), runner=_oracle_runner)
+        q.put((rank, M.tolist(), int(td), j))
+    except Exception as e:
+        q.put((rank, "error", repr(e), 0))
+        raise
+    finally:
+        dist.destroy_process_group()
+
+
+def test_gloo_world2_clara_points_equals_oracle():
+    """Samples split over 2 ranks (r, r+2, ...), one all-gather of (TD,
+    sample, medoids): every rank returns oracle.clara_points over ALL samples."""
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    ps = [ctx.Process(target=_clara_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in ps:
+        p.start()
+    out = sorted([q.get(timeout=240) for _ in ps], key=lambda t: t[0])
+    for p in ps:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    assert all(t[1] != "error" for t in out), out
+    rng = np.random.default_rng(91)
+    X = rng.integers(0, 400, size=(160, 3)).astype(np.int32)
+    samples = np.stack([rng.choice(160, size=30, replace=False) for _ in range(5)])
+    t, j, M, _ = oracle.clara_points(X, "l1", 4, samples)
+    for (rank, Mr, tr, jr) in out:
+        assert (Mr, tr, jr) == (M.tolist(), int(t), j)
