@@ -385,6 +385,29 @@ def run_ours(args):
         del D2, Xt
         torch.cuda.empty_cache()
 
+    # NEXT-3: FastCLARA from the config's points (no n x n matrix): 5 samples of
+    # s = 80 + 4k, BUILD + SWAP per sample, TD over all n from points
+    clara = None
+    if not args.no_clara:
+        from paper_2008_05171_b200 import kmedoids_clara_points
+        metric = "l2" if cfg.metric == kmsynth.L2_F32 else "l1"
+        Xt = torch.from_numpy(np.ascontiguousarray(X, dtype=np.float32 if metric == "l2" else np.int32)).cuda()
+        s_cl = min(n, 80 + 4 * k)
+        crng = np.random.default_rng(cfg.seed + 2000)
+        samples = np.stack([crng.choice(n, size=s_cl, replace=False) for _ in range(5)])
+        clara = {"samples": 5, "s": s_cl, "input": "the config's points; no n x n matrix is formed",
+                 "timing": "wall clock of the third identical call (host threads, one stream per sample)"}
+        for v in ("fastpam1", "fasterpam"):
+            for _ in range(2):
+                kmedoids_clara_points(Xt, metric, k, samples, v)
+            torch.cuda.synchronize()
+            t1 = time.perf_counter()
+            Mc, tdc, bc, _ = kmedoids_clara_points(Xt, metric, k, samples, v)
+            clara[v] = {"ms": (time.perf_counter() - t1) * 1e3, "td": tdc, "best_sample": bc}
+        if fpm:
+            clara["td_of_pam_on_all_of_D"] = fpm["fastpam1_td"]
+        del Xt
+
     # e2e: the public host-buffer call kmedoids_run_host (H2D of D, init, SWAP to
     # convergence, D2H of medoids/assignment/TD) -- one whole job per e2e step.
     e2e = None
@@ -440,7 +463,7 @@ def run_ours(args):
         "e2e": e2e,
         "cpu_baseline": cpu,
         "fasterpam": fpm,
-        "dissimilarity": dis,
+        "dissimilarity": dis, "clara_points": clara,
     }
     print(json.dumps(line), flush=True)
 
@@ -659,6 +682,7 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-fasterpam", action="store_true")
     ap.add_argument("--no-dissimilarity", action="store_true")
+    ap.add_argument("--no-clara", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
     ap.add_argument("--cpu-candidates", type=int, default=2000)
     ap.add_argument("--ref-candidates", type=int, default=400)
