@@ -358,7 +358,11 @@ km_status kmedoids_shard_trace(km_handle* h, int32_t* slots_out, int32_t* cands_
  *   4. if m > 0: all-gather maxcnt*n elements per rank from col_send into
  *      col_recv (rank order), then kmedoids_fp2_shard_apply(h, ...) runs the
  *      sequential phase redundantly on every rank (identical results).
- * Buffers are device memory owned by the handle. */
+ * Buffers are device memory owned by the handle.  The column buffers hold
+ * col_capacity columns per rank and grow on demand: when step 3 returns a
+ * maxcnt above the capacity last returned by kmedoids_fp2_shard_exchange,
+ * the buffers were reallocated and the caller calls it again for the new
+ * pointers before step 4. */
 typedef struct {
     void* record_send;          /* k records of 16 bytes */
     void* record_recv;          /* R*k records, rank order */
@@ -366,7 +370,7 @@ typedef struct {
     void* col_send;             /* col_capacity columns of n elements */
     void* col_recv;             /* R*col_capacity columns (use R*maxcnt) */
     size_t col_bytes_per_column;
-    int32_t col_capacity;       /* = k */
+    int32_t col_capacity;       /* columns per rank the buffers hold now (<= k) */
 } km_fp2_exchange;
 
 km_status kmedoids_fp2_shard_exchange(km_handle* h, int32_t nranks, km_fp2_exchange* out);

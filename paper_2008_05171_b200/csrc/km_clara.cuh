@@ -61,6 +61,7 @@ k_subdist_exact(const typename PointOf<T>::type* __restrict__ X, int d, const in
     const int a0 = blockIdx.y * 32, b0 = blockIdx.x * 32;
     for (int e = threadIdx.x; e < 32 * d; e += blockDim.x) {
         const int r = e / d, t = e - r * d;
+        KM_ASSERT(a0 + r >= s || idx[a0 + r] >= 0);
         ra[e] = (a0 + r < s) ? X[(int64_t)idx[a0 + r] * d + t] : (P)0;
         rb[e] = (b0 + r < s) ? X[(int64_t)idx[b0 + r] * d + t] : (P)0;
     }

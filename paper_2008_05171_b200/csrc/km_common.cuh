@@ -10,6 +10,17 @@
 #include <stdint.h>
 #include <limits.h>
 #include <float.h>
+#include <assert.h>
+
+// Device-side index checks of the checked build (libkmedoids_checked.so,
+// -DKM_DEVICE_ASSERTS; compute-sanitizer is not available on this pool):
+// a violated check traps the kernel (cudaErrorAssert).  No code in the
+// product build.
+#ifdef KM_DEVICE_ASSERTS
+#define KM_ASSERT(c) assert(c)
+#else
+#define KM_ASSERT(c) ((void)0)
+#endif
 
 namespace km {
 

@@ -159,6 +159,16 @@ __global__ void k_gather_col(const T* __restrict__ D, int64_t ld, int n, int64_t
     if (o < n) colbuf[o] = D[(int64_t)o * ld + (c - col_begin)];
 }
 
+// Columns cols[0..cnt) of the slab into out[j][o] (grid.y = cnt): the
+// FastPAM2 sharded pack in one launch.
+template <typename T>
+__global__ void k_gather_cols(const T* __restrict__ D, int64_t ld, int n, int64_t col_begin,
+                              const int* __restrict__ cols, T* __restrict__ out) {
+    const int o = blockIdx.x * blockDim.x + threadIdx.x;
+    const int c = cols[blockIdx.y];
+    if (o < n) out[(int64_t)blockIdx.y * n + o] = D[(int64_t)o * ld + (c - col_begin)];
+}
+
 // Sharded, device-decided iteration (no host round trip): the status of the
 // run, mirrored into pinned host memory by the decide kernel.
 template <typename A>
@@ -595,6 +605,7 @@ k_swap_stream_seg2(const T* __restrict__ D, int64_t ld, int w, int wpad, int n, 
                 ptx::mbar_expect_tx(&full[s], (uint32_t)nb * (cbytes + (rowd ? 32u : 16u)));
             }
             __syncwarp();
+            KM_ASSERT(lane >= nb || (o_l >= 0 && o_l < n));
             if (lane < nb)
                 ptx::bulk_g2s(sdata + (size_t)(s * RB + lane) * C::COLS, D + (int64_t)o_l * ld + ctacol, cbytes,
                               &full[s], pol);
@@ -765,6 +776,7 @@ __global__ void k_swap_combine(int w, int64_t col_begin, int P, const A* __restr
         const int es = *empty_slot;
         if (es != INT_MAX) { bv = 0; bs = es; }
         auto fin = [&](int s, A sum) {
+            KM_ASSERT(s >= 0 && s < k);
             if (acc_out) acc_out[(int64_t)s * w + cl] = sum;     // FastPAM2: complete acc_c[s]
             const A val = R[s] + sum;
             if (val < bv || (val == bv && s < bs)) { bv = val; bs = s; }

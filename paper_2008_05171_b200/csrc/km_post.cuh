@@ -177,6 +177,7 @@ k_fp1_post(PostArgs<T, A> g) {
                 if (local) g.MC[(int64_t)i * n + myo] = x;
                 if (j1 == i || j2 == i) {
                     myent = atomicAdd(&s_nres, 1);
+                    KM_ASSERT(ob0 + myent < ob1);
                     g.rescan[ob0 + myent] = myo;
                 } else if (x < d1 || (x == d1 && i < j1)) {
                     j2 = j1; d2 = d1; j1 = i; d1 = x;
@@ -209,6 +210,7 @@ k_fp1_post(PostArgs<T, A> g) {
         const int nres = s_nres;
         for (int e = warp; e < nres; e += POST_THREADS / 32) {
             const int o = g.rescan[ob0 + e];
+            KM_ASSERT(o >= ob0 && o < ob1);
             T q1 = dmax<T>(), q2 = dmax<T>();
             int k1 = INT_MAX, k2 = INT_MAX;
 #pragma unroll 8
@@ -229,6 +231,7 @@ k_fp1_post(PostArgs<T, A> g) {
                 }
             }
             if (lane == 0) {
+                KM_ASSERT(k1 >= 0 && k1 < k && k2 >= 0 && k2 < k && k1 != k2);
                 g.near[o] = k1; g.sec[o] = k2; g.dn[o] = q1; g.ds[o] = q2;
                 if (reg) { r_j1[e] = k1; r_j2[e] = k2; r_d1[e] = q1; r_d2[e] = q2; }
             }
@@ -248,6 +251,7 @@ k_fp1_post(PostArgs<T, A> g) {
             if (v) {
                 if (reg) { s = j1; val = (A)d2 - (A)d1; }
                 else { s = __ldcg(&g.near[o]); val = (A)__ldcg(&g.ds[o]) - (A)__ldcg(&g.dn[o]); }
+                KM_ASSERT(s >= 0 && s < k && val >= 0);
                 atomicAdd(&hh[s], 1);
             }
             if constexpr (std::is_same<A, double>::value) {
@@ -367,6 +371,7 @@ k_fp1_post(PostArgs<T, A> g) {
                     const int mid = (lo + hi + 1) >> 1;
                     if (segs[mid] <= p) lo = mid; else hi = mid - 1;
                 }
+                KM_ASSERT(lo >= 0 && lo < k && segs[lo] <= p && (lo == k - 1 || segs[lo + 1] > p));
                 if (side == 0) g.head_slot[q] = lo; else g.tail_slot[q] = lo;
             }
         }
@@ -401,6 +406,7 @@ k_fp1_post(PostArgs<T, A> g) {
                 RowInfo<T> r;
                 r.o = e; r.slot = s; r.dn = en; r.ds = es;
                 const int pos = bp + rank;
+                KM_ASSERT(pos >= 0 && pos < n && s >= 0 && s < k);
                 g.ri[pos] = r;
                 if (g.rowd) g.rowd[pos] = make_double2((double)en, (double)es);
             }

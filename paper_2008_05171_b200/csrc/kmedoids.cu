@@ -224,6 +224,12 @@ struct Impl : ImplBase {
         if (ev1) cudaEventDestroy(ev1);
     }
 
+    void dealloc(void* p) {
+        if (!p) return;
+        for (auto& b : bufs)
+            if (b == p) { cudaFree(p); b = nullptr; }
+    }
+
     template <typename X>
     km_status alloc(X** out, size_t count) {
         void* p = nullptr;
@@ -1371,7 +1377,8 @@ struct Impl : ImplBase {
     T* f2_col_send = nullptr;
     T* f2_col_recv = nullptr;
     int* f2_colidx = nullptr;
-    int f2_ranks = 0, f2_maxcnt = 0;
+    int f2_ranks = 0, f2_maxcnt = 0, f2_cap = 0;
+    int* f2_packcols = nullptr;        // [k] the owned candidates packed this iteration
     std::vector<int> f2_order;
 
     km_status fp2_shard_exchange(int32_t nr, km_fp2_exchange* out) override {
@@ -1381,9 +1388,9 @@ struct Impl : ImplBase {
             if (f2_ranks != 0) return fail(KM_ECOMM, "fp2 exchange already sized for %d ranks", f2_ranks);
             f2_ranks = nr;
             KM_TRY(alloc(&f2_rec_recv, (size_t)nr * k));
-            KM_TRY(alloc(&f2_col_send, (size_t)k * n));
-            KM_TRY(alloc(&f2_col_recv, (size_t)nr * k * n));
             KM_TRY(alloc(&f2_colidx, k));
+            KM_TRY(alloc(&f2_packcols, k));
+            KM_TRY(f2_grow(std::min(k, 32)));
         }
         out->record_send = fp2_best;
         out->record_recv = f2_rec_recv;
@@ -1391,7 +1398,23 @@ struct Impl : ImplBase {
         out->col_send = f2_col_send;
         out->col_recv = f2_col_recv;
         out->col_bytes_per_column = (size_t)n * sizeof(T);
-        out->col_capacity = k;
+        out->col_capacity = f2_cap;
+        return KM_OK;
+    }
+
+    // column exchange buffers for `cap` columns per rank (grown on demand:
+    // the plan needs max over ranks of the owned planned candidates, usually
+    // far below k; round 1 sized them for k, i.e. R * k * n elements)
+    km_status f2_grow(int cap) {
+        if (cap <= f2_cap) return KM_OK;
+        cap = std::min(k, std::max(cap, 2 * f2_cap));
+        KM_CK(cudaStreamSynchronize(st));
+        dealloc(f2_col_send);
+        dealloc(f2_col_recv);
+        f2_col_send = f2_col_recv = nullptr;
+        KM_TRY(alloc(&f2_col_send, (size_t)cap * n));
+        KM_TRY(alloc(&f2_col_recv, (size_t)f2_ranks * cap * n));
+        f2_cap = cap;
         return KM_OK;
     }
 
@@ -1450,9 +1473,12 @@ struct Impl : ImplBase {
         for (size_t r = 0; r < f2_order.size(); ++r) colidx[r] = own_of[r] * maxcnt + pos_of[r];
         if (!colidx.empty())
             KM_CK(cudaMemcpyAsync(f2_colidx, colidx.data(), colidx.size() * sizeof(int), cudaMemcpyHostToDevice, st));
-        const int nb = (int)cdiv(n, 256);
-        for (size_t j = 0; j < owned[me].size(); ++j) {
-            km::k_gather_col<T><<<nb, 256, 0, st>>>(D, ld, (int)n, c0, owned[me][j], f2_col_send + j * (size_t)n);
+        KM_TRY(f2_grow(maxcnt));                     // (the caller re-queries the exchange when it grew)
+        if (!owned[me].empty()) {
+            KM_CK(cudaMemcpyAsync(f2_packcols, owned[me].data(), owned[me].size() * sizeof(int),
+                                  cudaMemcpyHostToDevice, st));
+            km::k_gather_cols<T><<<dim3((unsigned)cdiv(n, 256), (unsigned)owned[me].size()), 256, 0, st>>>(
+                D, ld, (int)n, c0, f2_packcols, f2_col_send);
             KM_CKL();
         }
         KM_CK(cudaStreamSynchronize(st));

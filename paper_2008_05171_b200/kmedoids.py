@@ -19,7 +19,10 @@ from dataclasses import dataclass
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libkmedoids.so")
+# KM_LIBRARY=checked selects the build with device-side index asserts
+# (libkmedoids_checked.so, test runs); the default is the product build
+LIB_PATH = os.path.join(_HERE, "libkmedoids_checked.so" if os.environ.get("KM_LIBRARY") == "checked"
+                        else "libkmedoids.so")
 
 KM_OK, KM_CONVERGED, KM_NOT_CONVERGED = 0, 1, 2
 KM_EINVAL, KM_ENOMEM, KM_ECUDA, KM_ECOMM = 10, 11, 12, 13

@@ -303,6 +303,8 @@ def fp2_iter(handles, comm, cb):
     if any(p != plans[0] for p in plans):
         raise RuntimeError(f"ranks disagree on the FastPAM2 plan: {plans}")
     if m > 0:
+        for h in handles:                       # the column buffers grow on demand (kmedoids.h)
+            h.fp2_exchange_tensors(comm.world, need=maxcnt)
         comm.allgather_fp2_columns(handles, maxcnt)
     res = [h.fp2_shard_apply() for h in handles]
     if any(r[:2] != res[0][:2] for r in res):
@@ -392,11 +394,14 @@ class CudaShard:
             self._x = (send, recv, col)
         return self._x
 
-    def fp2_exchange_tensors(self, world: int):
-        """(record_send, record_recv, col_send, col_recv, bytes per column) as uint8 tensors."""
+    def fp2_exchange_tensors(self, world: int, need: int = 0):
+        """(record_send, record_recv, col_send, col_recv, bytes per column) as
+        uint8 tensors; re-queried when a plan needs more columns per rank than
+        the buffers held (the library grew them)."""
         import torch
-        if getattr(self, "_f2", None) is None:
+        if getattr(self, "_f2", None) is None or need > getattr(self, "_f2_cap", 0):
             x = self.km.fp2_shard_exchange(world)
+            self._f2_cap = int(x.col_capacity)
             dev = self.km.D.device
             cap = x.col_capacity * x.col_bytes_per_column
             self._f2 = (torch.as_tensor(_DevBytes(x.record_send, x.record_bytes), device=dev),

@@ -1,3 +1,17 @@
 mkdir -p gpurun_out
-python scripts/sanitize_small.py > gpurun_out/r2j_plain.log 2>&1 && \
-timeout 1500 compute-sanitizer --tool memcheck --leak-check no --print-limit 50 python scripts/sanitize_small.py > gpurun_out/r2j_memcheck.log 2>&1; echo "rc=$?" >> gpurun_out/r2j_memcheck.log
+KM_E2E_PROF=1 python - > gpurun_out/r2l_e2e.log 2>&1 <<'PY'
+import time, numpy as np, torch, kmsynth
+from paper_2008_05171_b200 import kmedoids_run_host
+from paper_2008_05171_b200.kmedoids import pinned_empty
+cfg = kmsynth.CONFIGS[4]
+X = kmsynth.make_points(cfg)
+Dt = kmsynth.dist_cuda(X, cfg.metric)
+Dh, Dh_t = pinned_empty(tuple(Dt.shape), cfg.dtype)
+Dh_t.copy_(Dt)
+del Dt
+torch.cuda.synchronize(); torch.cuda.empty_cache()
+for i in range(8):
+    t = time.perf_counter()
+    r = kmedoids_run_host(Dh, cfg.k, use_build=True)
+    print("job", i, time.perf_counter() - t, r.n_iter, flush=True)
+PY

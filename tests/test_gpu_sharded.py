@@ -89,7 +89,7 @@ def test_sharded_random_init_set_medoids():
     assert st.assignment.tolist() == ref.assignment.tolist()
 
 
-@pytest.mark.parametrize("world,cid,n,k", [(2, 5, 900, 11), (3, 5, 1300, 17), (4, 3, 800, 9)])
+@pytest.mark.parametrize("world,cid,n,k", [(2, 5, 900, 11), (3, 5, 1300, 17), (4, 3, 800, 9), (2, 5, 1600, 90)])
 def test_sharded_fastpam2_equals_single_gpu(world, cid, n, k):
     from paper_2008_05171_b200 import KMedoids, parallel
     cfg = kmsynth.CONFIGS[cid]
