@@ -136,6 +136,7 @@ struct ImplBase {
     virtual km_status inc_iters(int32_t max_iters, int32_t* swaps, void* td_out, int32_t* iters_done,
                                 bool* converged) = 0;
     virtual km_status fp1_run_pipelined(int32_t max_iter, int32_t* iters_out, int32_t* swaps_out, bool* converged) = 0;
+    virtual km_status check_diagonal() = 0;
     bool profiling = false;
     double prof_ms = 0.0;
     int64_t prof_launches = 0;
@@ -313,16 +314,7 @@ struct Impl : ImplBase {
         KM_CK(cudaEventCreate(&ev0));
         KM_CK(cudaEventCreate(&ev1));
         KM_TRY(alloc(&bad_count, 1));
-        KM_CK(cudaMemsetAsync(bad_count, 0, sizeof(int), st));
-        if (c1 > c0) {
-            // the slab's diagonal entries must be exactly 0 (O(n) device pass)
-            km::k_validate_diag<T><<<(unsigned)cdiv(c1 - c0, 256), 256, 0, st>>>(D, ld, c0, c1, bad_count);
-            KM_CKL();
-            int nbad = 0;
-            KM_CK(cudaMemcpyAsync(&nbad, bad_count, sizeof(int), cudaMemcpyDeviceToHost, st));
-            KM_CK(cudaStreamSynchronize(st));
-            if (nbad) return fail(KM_EINVAL, "D has %d nonzero (or NaN) diagonal entries; d(x_o, x_o) must be 0", nbad);
-        }
+        KM_TRY(check_diagonal());
         if (const char* es = getenv("KM_STEP_PROF")) step_prof = es[0] == '1';
         if (step_prof)
             for (auto& e : sp_ev) KM_CK(cudaEventCreate(&e));
@@ -379,6 +371,19 @@ struct Impl : ImplBase {
         KM_CK(cudaMemcpyAsync(M, Mh, k * sizeof(int32_t), cudaMemcpyHostToDevice, st));
         KM_CK(cudaMemcpyAsync(point_slot, ps.data(), n * sizeof(int32_t), cudaMemcpyHostToDevice, st));
         KM_CK(cudaStreamSynchronize(st));   // ps goes out of scope
+        return KM_OK;
+    }
+
+    // the slab's diagonal entries must be exactly 0 (O(n) device pass; synchronises)
+    km_status check_diagonal() override {
+        if (c1 <= c0) return KM_OK;
+        KM_CK(cudaMemsetAsync(bad_count, 0, sizeof(int), st));
+        km::k_validate_diag<T><<<(unsigned)cdiv(c1 - c0, 256), 256, 0, st>>>(D, ld, c0, c1, bad_count);
+        KM_CKL();
+        int nbad = 0;
+        KM_CK(cudaMemcpyAsync(&nbad, bad_count, sizeof(int), cudaMemcpyDeviceToHost, st));
+        KM_CK(cudaStreamSynchronize(st));
+        if (nbad) return fail(KM_EINVAL, "D has %d nonzero (or NaN) diagonal entries; d(x_o, x_o) must be 0", nbad);
         return KM_OK;
     }
 
@@ -2556,6 +2561,14 @@ struct HostJobCache {
     void* p = nullptr;
     size_t bytes = 0;
     int dev = -1;
+    // the handle of the last job, reused by a job of the same shape on the
+    // same buffer and stream (its scratch, graphs and events stay allocated:
+    // destroying a handle measured 4-380 ms per job in round 2)
+    km_handle* h = nullptr;
+    int64_t hn = 0, hld = 0;
+    int32_t hk = 0;
+    km_dtype hdt = KM_U32;
+    void* hst = nullptr;
 };
 HostJobCache g_job;
 }  // namespace
@@ -2564,6 +2577,7 @@ km_status kmedoids_release_host_cache(void) {
     g_err.clear();
     clara_points_release();
     std::lock_guard<std::mutex> lk(g_job.mu);
+    if (g_job.h) { kmedoids_destroy(g_job.h); g_job.h = nullptr; }
     if (g_job.p) {
         int cur = 0;
         cudaGetDevice(&cur);
@@ -2600,6 +2614,7 @@ km_status kmedoids_run_host(const void* D_host, km_dtype dtype, int64_t n, int64
     const bool cached = lk.owns_lock();
     cudaError_t e = cudaSuccess;
     if (cached && g_job.p && (g_job.bytes < bytes || g_job.dev != dev)) {
+        if (g_job.h) { kmedoids_destroy(g_job.h); g_job.h = nullptr; }
         if (g_job.dev == dev) cudaFree(g_job.p);
         else { cudaSetDevice(g_job.dev); cudaFree(g_job.p); cudaSetDevice(dev); }
         g_job.p = nullptr; g_job.bytes = 0;
@@ -2619,7 +2634,17 @@ km_status kmedoids_run_host(const void* D_host, km_dtype dtype, int64_t n, int64
     if (e != cudaSuccess) s = fail(KM_ECUDA, "H2D copy of D failed: %s", cudaGetErrorString(e));
     if (prof) cudaStreamSynchronize(st);
     const auto t2 = now();
-    if (s == KM_OK) s = kmedoids_create(&h, Dd, dtype, n, ld, 0, n, k, cuda_stream);
+    if (s == KM_OK && cached && g_job.h && g_job.hn == n && g_job.hld == ld && g_job.hk == k && g_job.hdt == dtype &&
+        g_job.hst == cuda_stream && g_job.dev == dev) {
+        h = g_job.h;                                     // same shape, buffer and stream: reuse
+        s = h->impl->check_diagonal();                   // the new D is validated like a new handle's
+    } else if (s == KM_OK) {
+        if (cached && g_job.h) { kmedoids_destroy(g_job.h); g_job.h = nullptr; }
+        s = kmedoids_create(&h, Dd, dtype, n, ld, 0, n, k, cuda_stream);
+        if (s == KM_OK && cached) {
+            g_job.h = h; g_job.hn = n; g_job.hld = ld; g_job.hk = k; g_job.hdt = dtype; g_job.hst = cuda_stream;
+        }
+    }
     if (s == KM_OK && !use_build) s = kmedoids_set_medoids(h, initial_medoids);
     const auto t3 = now();
     if (s == KM_OK) {
@@ -2628,7 +2653,7 @@ km_status kmedoids_run_host(const void* D_host, km_dtype dtype, int64_t n, int64
         s = r;
     }
     const auto t4 = now();
-    kmedoids_destroy(h);
+    if (!(cached && g_job.h == h)) kmedoids_destroy(h);
     cudaStreamSynchronize(st);
     const auto t5 = now();
     if (!cached) cudaFree(Dd);

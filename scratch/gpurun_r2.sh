@@ -1,5 +1,6 @@
 mkdir -p gpurun_out
-KM_E2E_PROF=1 python - > gpurun_out/r2l_e2e.log 2>&1 <<'PY'
+python -m pytest tests/test_gpu_parity.py -x -q -p no:cacheprovider -k "run_host or swap_iters" > gpurun_out/r2m_pytest.log 2>&1; echo pytest_rc=$? >> gpurun_out/r2m_pytest.log
+KM_E2E_PROF=1 python - > gpurun_out/r2m_e2e.log 2>&1 <<'PY'
 import time, numpy as np, torch, kmsynth
 from paper_2008_05171_b200 import kmedoids_run_host
 from paper_2008_05171_b200.kmedoids import pinned_empty

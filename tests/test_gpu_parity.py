@@ -459,3 +459,37 @@ def test_part_tilt_does_not_change_results(monkeypatch, skew):
         r = km.run(use_build=False)
         assert r.medoids.tolist() == ref.medoids.tolist() and r.td == ref.td and r.n_iter == ref.n_iter
         km.close()
+
+
+def test_run_host_jobs_reuse_buffer_and_handle():
+    """kmedoids_run_host (H2D of D, init, SWAP to convergence, D2H): repeated
+    jobs of one shape reuse the device buffer and the handle; every job equals
+    the oracle on ITS matrix (BUILD and given-medoid inits, FastPAM1 and
+    FastPAM2), a job whose D has a nonzero diagonal is refused (KM_EINVAL)
+    even on a reused handle, and the cache can be released."""
+    from paper_2008_05171_b200 import KMError, kmedoids_release_host_cache, kmedoids_run_host
+    rng = np.random.default_rng(808)
+    n, k = 700, 6
+    for job in range(4):
+        D = rand_int(rng, n, [5, 1000][job % 2], symmetric=bool(job % 3))
+        Dh = np.zeros((n, kmsynth.round_ld(n)), np.uint32)
+        Dh[:, :n] = D
+        if job % 2 == 0:
+            r = kmedoids_run_host(Dh, k, use_build=True)
+            Mb, _, _ = oracle.build_init(D, k)
+            ref = oracle.swap_run(D, Mb, oracle.FASTPAM1)
+        else:
+            M0 = rng.choice(n, size=k, replace=False)
+            r = kmedoids_run_host(Dh, k, use_build=False, medoids=M0, variant="fastpam2")
+            ref = oracle.swap_run(D, M0, oracle.FASTPAM2)
+        assert r.medoids.tolist() == ref.medoids.tolist() and r.td == ref.td
+        assert r.assignment.tolist() == ref.assignment.tolist()
+        assert (r.n_iter, r.n_swaps) == (ref.n_iter, ref.n_swaps)
+    Dh[3, 3] = 1
+    with pytest.raises(KMError):
+        kmedoids_run_host(Dh, k, use_build=True)
+    kmedoids_release_host_cache()
+    Dh[3, 3] = 0
+    r = kmedoids_run_host(Dh, k, use_build=True)
+    assert r.td == oracle.td(Dh[:, :n], r.medoids)
+    kmedoids_release_host_cache()
