@@ -1,18 +1,6 @@
 mkdir -p gpurun_out
-python -m pytest tests/test_gpu_parity.py -x -q -p no:cacheprovider -k "run_host or swap_iters" > gpurun_out/r2m_pytest.log 2>&1; echo pytest_rc=$? >> gpurun_out/r2m_pytest.log
-KM_E2E_PROF=1 python - > gpurun_out/r2m_e2e.log 2>&1 <<'PY'
-import time, numpy as np, torch, kmsynth
-from paper_2008_05171_b200 import kmedoids_run_host
-from paper_2008_05171_b200.kmedoids import pinned_empty
-cfg = kmsynth.CONFIGS[4]
-X = kmsynth.make_points(cfg)
-Dt = kmsynth.dist_cuda(X, cfg.metric)
-Dh, Dh_t = pinned_empty(tuple(Dt.shape), cfg.dtype)
-Dh_t.copy_(Dt)
-del Dt
-torch.cuda.synchronize(); torch.cuda.empty_cache()
-for i in range(8):
-    t = time.perf_counter()
-    r = kmedoids_run_host(Dh, cfg.k, use_build=True)
-    print("job", i, time.perf_counter() - t, r.n_iter, flush=True)
-PY
+CMD="python bench.py --steps 5 --warmup 3 --no-e2e --no-fasterpam --no-dissimilarity --no-cpu-baseline --no-clara"
+$CMD > gpurun_out/r2n_plain.log 2>&1 && \
+ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/r2n_launches.csv $CMD > gpurun_out/r2n_ncu1.log 2>&1 && \
+ncu --set full --clock-control none --import-source on -k regex:"k_swap_stream_seg2|k_fp1_post|k_swap_combine" -s 12 -c 3 -o gpurun_out/r2n_prof $CMD > gpurun_out/r2n_ncu2.log 2>&1
+echo "rc=$?"

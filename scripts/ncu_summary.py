@@ -54,12 +54,16 @@ def full(rep, out, tjson, tag):
         res = {}
         for r in rows[2:]:
             f.write("| metric | unit | value |\n|---|---|---|\n")
+            cur = {}
             for w in want:
                 if w in h:
                     i = h.index(w)
                     f.write(f"| {w} | {u[i]} | {r[i]} |\n")
-                    res[w] = (u[i], r[i])
+                    cur[w] = (u[i], r[i])
             f.write("\n")
+            # the traffic record is the SWAP stream's (the dominant kernel), else the last kernel's
+            if not res or "stream" in cur.get("Kernel Name", ("", ""))[1] or "stream" not in res["Kernel Name"][1]:
+                res = cur
         def val(k, to):
             unit, v = res[k]
             v = float(v.replace(",", ""))
