@@ -13,6 +13,8 @@
 //     3-term split x = hi + lo (hi = tf32(x), lo = tf32(x - hi)):
 //     <x,y> ~ hi.hi + hi.lo + lo.hi, fp32 accumulation (the dropped lo.lo
 //     term is < 2^-22 |x||y|).  Norms are exact fp64 sums rounded to f32.
+//     The points are centred first (x - mean; k_dist_mean), so the error
+//     follows |x - mu|^2 + |y - mu|^2 instead of |x|^2 + |y|^2.
 //     The diagonal is set to 0 exactly (d(x, x) = 0).
 //   L1 (uint32): d(x_i, x_j) = sum_t |x_it - x_jt| on integer coordinates
 //     (the C1/C5 "L1 of round(100 x)" dissimilarities), exact, CUDA cores
@@ -71,12 +73,40 @@ __device__ __forceinline__ int dt_off(int r, int k, int kc) {
     return (((r >> 3) * kc + (k >> 2)) << 5) + ((r & 7) << 2) + (k & 3);
 }
 
-// fp64 squared norms rounded to f32: nrm[i] = |x_i|^2
-__global__ void k_dist_norms(const float* __restrict__ X, int n, int d, float* __restrict__ nrm) {
+// Centering (round 2): distances are translation invariant, while the
+// error of the norm expansion |x|^2 + |y|^2 - 2<x,y> scales with |x|^2 +
+// |y|^2.  The operands are therefore x - mu, mu = the per-dimension mean of
+// all n points (fp64 sums in a fixed order, rounded to f32; any mu is exact
+// in the mathematics, the rounding of x - mu costs 2^-24 |x - mu|).
+// grid = d blocks: block t sums dimension t.
+__global__ void k_dist_mean(const float* __restrict__ X, int n, int d, float* __restrict__ mu) {
+    __shared__ double ws[8];
+    const int t = blockIdx.x;
+    double s = 0;
+    for (int i = threadIdx.x; i < n; i += blockDim.x) s += (double)X[(int64_t)i * d + t];
+#pragma unroll
+    for (int x = 16; x >= 1; x >>= 1) s += __shfl_xor_sync(FULL, s, x);
+    if ((threadIdx.x & 31) == 0) ws[threadIdx.x >> 5] = s;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double a = 0;
+        for (int w = 0; w < (int)(blockDim.x >> 5); ++w) a += ws[w];
+        mu[t] = (float)(a / (double)n);
+    }
+}
+
+__device__ __forceinline__ float dt_centered(const float* X, const float* mu, int64_t j, int d, int k) {
+    const float v = X[j * d + k];
+    return mu ? v - mu[k] : v;
+}
+
+// fp64 squared norms of the (centred) points rounded to f32: nrm[i] = |x_i - mu|^2
+__global__ void k_dist_norms(const float* __restrict__ X, const float* __restrict__ mu, int n, int d,
+                             float* __restrict__ nrm) {
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= n) return;
     double s = 0;
-    for (int t = 0; t < d; ++t) { const double v = X[(int64_t)i * d + t]; s += v * v; }
+    for (int t = 0; t < d; ++t) { const double v = dt_centered(X, mu, i, d, t); s += v * v; }
     nrm[i] = (float)s;
 }
 
@@ -86,15 +116,15 @@ __global__ void k_dist_norms(const float* __restrict__ X, int n, int d, float* _
 // whole tile.  Rows beyond r1 and columns beyond d are zero.
 __host__ __device__ inline int64_t dt_tile_floats(int dpad) { return 2LL * DT_M * dpad + DT_M; }
 
-__global__ void k_dist_pack(const float* __restrict__ X, const float* __restrict__ nrm, int d, int dpad, int64_t r0,
-                            int64_t r1, float* __restrict__ out) {
+__global__ void k_dist_pack(const float* __restrict__ X, const float* __restrict__ mu, const float* __restrict__ nrm,
+                            int d, int dpad, int64_t r0, int64_t r1, float* __restrict__ out) {
     const int kc = dpad / 4;
     const int64_t tile = blockIdx.x;
     float* o = out + tile * dt_tile_floats(dpad);
     for (int idx = threadIdx.x; idx < DT_M * dpad; idx += blockDim.x) {
         const int r = idx / dpad, k = idx - r * dpad;
         const int64_t j = r0 + tile * DT_M + r;
-        const float v = (j < r1 && k < d) ? X[j * d + k] : 0.f;
+        const float v = (j < r1 && k < d) ? dt_centered(X, mu, j, d, k) : 0.f;
         const float hi = dt_tf32(v);
         o[dt_off(r, k, kc)] = hi;
         o[DT_M * dpad + dt_off(r, k, kc)] = dt_tf32(v - hi);
@@ -309,15 +339,15 @@ __host__ __device__ inline size_t dw_smem_bytes(int dpad, int nstage) {
 }
 
 // hi / lo core matrices of rows [r0, r1), 128-row tiles (no norms appended)
-__global__ void k_dist_pack2(const float* __restrict__ X, int d, int dpad, int64_t r0, int64_t r1,
-                             float* __restrict__ out) {
+__global__ void k_dist_pack2(const float* __restrict__ X, const float* __restrict__ mu, int d, int dpad, int64_t r0,
+                             int64_t r1, float* __restrict__ out) {
     const int kc = dpad / 4;
     const int64_t tile = blockIdx.x;
     float* o = out + tile * dw_tile_floats(dpad);
     for (int idx = threadIdx.x; idx < DT_M * dpad; idx += blockDim.x) {
         const int r = idx / dpad, k = idx - r * dpad;
         const int64_t j = r0 + tile * DT_M + r;
-        const float v = (j < r1 && k < d) ? X[j * d + k] : 0.f;
+        const float v = (j < r1 && k < d) ? dt_centered(X, mu, j, d, k) : 0.f;
         const float hi = dt_tf32(v);
         o[dt_off(r, k, kc)] = hi;
         o[DT_M * dpad + dt_off(r, k, kc)] = dt_tf32(v - hi);

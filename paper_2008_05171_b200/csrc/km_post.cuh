@@ -35,7 +35,7 @@
 namespace km {
 
 constexpr int POST_THREADS = 256;
-constexpr int POST_MAX_BLOCKS = 768;                  // chunk counts per slot scanned in registers
+constexpr int POST_MAX_BLOCKS = 512;                  // chunk counts per slot scanned in registers (16 per lane)
 constexpr int POST_MAX_PER = POST_MAX_BLOCKS / 32;
 
 template <typename T, typename A>
@@ -285,12 +285,12 @@ k_fp1_post(PostArgs<T, A> g) {
 
     if (!g.prep_only && b == 0 && threadIdx.x == 0) {
         // every block has read dec / M / td (phase A): record the decision
-        *g.dec = d;
-        if (d.apply) {
-            g.M[d.slot] = d.c;
-            g.point_slot[d.old_m] = -1;
-            g.point_slot[d.c] = d.slot;
-            *g.td = *g.td + d.dtd;
+        *g.dec = sdec;
+        if (sdec.apply) {
+            g.M[sdec.slot] = sdec.c;
+            g.point_slot[sdec.old_m] = -1;
+            g.point_slot[sdec.c] = sdec.slot;
+            *g.td = *g.td + sdec.dtd;
         }
     }
 
@@ -418,7 +418,7 @@ k_fp1_post(PostArgs<T, A> g) {
             // the outcome straight into pinned host memory (visible to the host
             // once the launch's completion event is observed)
             const int q = *g.seq;
-            if (g.h_ring) { IterMirror<A>& m = g.h_ring[q % g.ring]; m.d = d; m.td = *g.td; m.seq = q; m.noop = 0; }
+            if (g.h_ring) { IterMirror<A>& m = g.h_ring[q % g.ring]; m.d = sdec; m.td = *g.td; m.seq = q; m.noop = 0; }
             *g.seq = q + 1;
         }
     }

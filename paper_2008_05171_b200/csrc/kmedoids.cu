@@ -2766,7 +2766,8 @@ km_status kmedoids_dissimilarity(const void* X, km_metric metric, int64_t n, int
         const bool same = (col_begin == 0);
         const int64_t TF = ws ? km::dw_tile_floats(dpad) : km::dt_tile_floats(dpad);
         const size_t nrm_floats = (size_t)cdiv(n, 64) * 64;          // keeps the packed tiles 256-byte aligned
-        const size_t scratch = nrm_floats + (size_t)nm * TF + (same ? 0 : (size_t)ntc * TF);
+        const size_t mu_floats = 64;                                 // d <= 64
+        const size_t scratch = nrm_floats + (size_t)nm * TF + (same ? 0 : (size_t)ntc * TF) + mu_floats;
         // persistent per-device scratch (norms + packed operands), grown on
         // demand: a stream-ordered allocation per call pays the pool's page
         // mapping again whenever the pool was trimmed at a synchronisation
@@ -2775,13 +2776,19 @@ km_status kmedoids_dissimilarity(const void* X, km_metric metric, int64_t n, int
         if (e != cudaSuccess) return fail(KM_ENOMEM, "dissimilarity scratch: %s", cudaGetErrorString(e));
         float* PA = nrm + nrm_floats;
         float* PB = same ? PA : PA + nm * TF;
-        km::k_dist_norms<<<(unsigned)cdiv(n, 256), 256, 0, st>>>((const float*)X, (int)n, d, nrm);
+        float* mu = PA + nm * TF + (same ? 0 : ntc * TF);
+        const char* ec = getenv("KM_DIST_CENTER");       // measurement override: 0 = no centring
+        const bool center = !(ec && ec[0] == '0');
+        if (center) km::k_dist_mean<<<(unsigned)d, 256, 0, st>>>((const float*)X, (int)n, d, mu);
+        const float* mup = center ? mu : nullptr;
+        km::k_dist_norms<<<(unsigned)cdiv(n, 256), 256, 0, st>>>((const float*)X, mup, (int)n, d, nrm);
         // work items (row tile x column range): at least 8 per SM for balance
         const int nsplit = (int)std::max<int64_t>(1, std::min<int64_t>(ntc, cdiv((int64_t)nsm * 8, nm)));
         const int grid = (int)std::min<int64_t>(nsm, nm * nsplit);
         if (ws) {
-            km::k_dist_pack2<<<(unsigned)nm, 256, 0, st>>>((const float*)X, d, dpad, 0, n, PA);
-            if (!same) km::k_dist_pack2<<<(unsigned)ntc, 256, 0, st>>>((const float*)X, d, dpad, col_begin, col_end, PB);
+            km::k_dist_pack2<<<(unsigned)nm, 256, 0, st>>>((const float*)X, mup, d, dpad, 0, n, PA);
+            if (!same)
+                km::k_dist_pack2<<<(unsigned)ntc, 256, 0, st>>>((const float*)X, mup, d, dpad, col_begin, col_end, PB);
             static PFN_cuTensorMapEncodeTiled_v12000 encode = nullptr;
             if (!encode) {
                 void* fn = nullptr;
@@ -2805,8 +2812,10 @@ km_status kmedoids_dissimilarity(const void* X, km_metric metric, int64_t n, int
             km::k_dist_l2_ws<<<grid, km::DW_THREADS, smem, st>>>(tm, PA, PB, nrm, (int)n, dpad, nsplit, wstage,
                                                                   col_begin, col_end);
         } else {
-            km::k_dist_pack<<<(unsigned)nm, 256, 0, st>>>((const float*)X, nrm, d, dpad, 0, n, PA);
-            if (!same) km::k_dist_pack<<<(unsigned)ntc, 256, 0, st>>>((const float*)X, nrm, d, dpad, col_begin, col_end, PB);
+            km::k_dist_pack<<<(unsigned)nm, 256, 0, st>>>((const float*)X, mup, nrm, d, dpad, 0, n, PA);
+            if (!same)
+                km::k_dist_pack<<<(unsigned)ntc, 256, 0, st>>>((const float*)X, mup, nrm, d, dpad, col_begin, col_end,
+                                                               PB);
             const int nstage = km::dt_smem_bytes(dpad, 2) + 1024 <= (size_t)smax ? 2 : 1;
             const size_t smem = km::dt_smem_bytes(dpad, nstage);
             e = cudaFuncSetAttribute(km::k_dist_l2_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);

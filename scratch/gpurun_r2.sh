@@ -1,6 +1,4 @@
 mkdir -p gpurun_out
-CMD="python bench.py --steps 5 --warmup 3 --no-e2e --no-fasterpam --no-dissimilarity --no-cpu-baseline --no-clara"
-$CMD > gpurun_out/r2n_plain.log 2>&1 && \
-ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/r2n_launches.csv $CMD > gpurun_out/r2n_ncu1.log 2>&1 && \
-ncu --set full --clock-control none --import-source on -k regex:"k_swap_stream_seg2|k_fp1_post|k_swap_combine" -s 12 -c 3 -o gpurun_out/r2n_prof $CMD > gpurun_out/r2n_ncu2.log 2>&1
-echo "rc=$?"
+python -m pytest tests/test_gpu_dist.py -x -q -p no:cacheprovider > gpurun_out/r2o_pytest.log 2>&1; echo pytest_rc=$? >> gpurun_out/r2o_pytest.log
+python scratch/dist_accuracy.py > gpurun_out/r2o_acc.log 2>&1
+python bench.py --no-e2e --no-fasterpam --no-cpu-baseline --no-clara --steps 10 --warmup 3 > gpurun_out/r2o_bench.log 2>&1

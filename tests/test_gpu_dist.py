@@ -22,7 +22,12 @@ def _cuda():
 
 
 def l2_bound(X, d):
-    nrm = (X.astype(np.float64) ** 2).sum(axis=1)
+    """The arithmetic's bound on squared distances with the points centred
+    (km_dist.cuh: x - mu, mu = the f32-rounded fp64 mean) -- the norms are
+    those of the centred points."""
+    Xd = X.astype(np.float64)
+    mu = Xd.mean(axis=0).astype(np.float32).astype(np.float64)
+    nrm = ((X - mu.astype(np.float32)).astype(np.float64) ** 2).sum(axis=1)
     return (6 * d + 16) * 2.0 ** -24 * (nrm[:, None] + nrm[None, :])
 
 
@@ -147,3 +152,24 @@ def test_l1_fp32_kernel_forced(monkeypatch, n, d, c0, c1):
     Xq = rng.integers(-5000, 5000, size=(n, d)).astype(np.int32)
     Dg = kmedoids_dissimilarity(torch.from_numpy(Xq).cuda(), "l1", col_begin=c0, col_end=c1)
     assert (Dg[:, :c1 - c0].cpu().numpy().view(np.uint32).astype(np.int64) == oracle.dist_l1(Xq)[:, c0:c1]).all()
+
+
+def test_l2_centering_removes_the_offset_error(monkeypatch):
+    """Distances are translation invariant; the norm expansion's error scales
+    with |x|^2 + |y|^2 unless the points are centred first.  Points near
+    (1000, ..., 1000): relative error below 1e-5 with centring, far above it
+    without (KM_DIST_CENTER=0, measurement override)."""
+    from paper_2008_05171_b200 import kmedoids_dissimilarity
+    rng = np.random.default_rng(5)
+    X = (rng.normal(size=(1500, 16)) + 1000.0).astype(np.float32)
+    Dx = oracle.dist_l2(X)
+    off = ~np.eye(1500, dtype=bool)
+
+    def rel(env):
+        monkeypatch.setenv("KM_DIST_CENTER", env)
+        Dg = kmedoids_dissimilarity(torch.from_numpy(X).cuda(), "l2")[:, :1500].double().cpu().numpy()
+        assert (np.diag(Dg) == 0).all()
+        return (np.abs(Dg - Dx)[off] / Dx[off]).max()
+
+    assert rel("1") < 1e-5
+    assert rel("0") > 1e-3
