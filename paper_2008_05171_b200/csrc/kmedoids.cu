@@ -2630,7 +2630,33 @@ km_status kmedoids_run_host(const void* D_host, km_dtype dtype, int64_t n, int64
     cudaStream_t st = (cudaStream_t)cuda_stream;
     km_status s = KM_OK;
     km_handle* h = nullptr;
-    e = cudaMemcpyAsync(Dd, D_host, bytes, cudaMemcpyHostToDevice, st);
+    {
+        // H2D of D, optionally as KM_H2D_STREAMS (measurement override) chunked
+        // copies on as many streams joined back into st
+        int ns = 1;
+        if (const char* eh = getenv("KM_H2D_STREAMS")) ns = std::max(1, std::min(8, atoi(eh)));
+        if (ns == 1) {
+            e = cudaMemcpyAsync(Dd, D_host, bytes, cudaMemcpyHostToDevice, st);
+        } else {
+            std::vector<cudaStream_t> ss(ns, nullptr);
+            std::vector<cudaEvent_t> ev(ns + 1, nullptr);
+            for (int i = 0; i < ns && e == cudaSuccess; ++i) e = cudaStreamCreateWithFlags(&ss[i], cudaStreamNonBlocking);
+            for (int i = 0; i <= ns && e == cudaSuccess; ++i) e = cudaEventCreateWithFlags(&ev[i], cudaEventDisableTiming);
+            if (e == cudaSuccess) e = cudaEventRecord(ev[ns], st);
+            const size_t rows = (size_t)n, rb = (size_t)ld * 4;
+            for (int i = 0; i < ns && e == cudaSuccess; ++i) {
+                const size_t r0 = rows * i / ns, r1 = rows * (i + 1) / ns;
+                e = cudaStreamWaitEvent(ss[i], ev[ns], 0);
+                if (e == cudaSuccess)
+                    e = cudaMemcpyAsync((char*)Dd + r0 * rb, (const char*)D_host + r0 * rb, (r1 - r0) * rb,
+                                        cudaMemcpyHostToDevice, ss[i]);
+                if (e == cudaSuccess) e = cudaEventRecord(ev[i], ss[i]);
+                if (e == cudaSuccess) e = cudaStreamWaitEvent(st, ev[i], 0);
+            }
+            for (auto x : ss) if (x) cudaStreamDestroy(x);       // (destroyed once their work completes)
+            for (auto x : ev) if (x) cudaEventDestroy(x);
+        }
+    }
     if (e != cudaSuccess) s = fail(KM_ECUDA, "H2D copy of D failed: %s", cudaGetErrorString(e));
     if (prof) cudaStreamSynchronize(st);
     const auto t2 = now();

@@ -493,3 +493,39 @@ def test_run_host_jobs_reuse_buffer_and_handle():
     r = kmedoids_run_host(Dh, k, use_build=True)
     assert r.td == oracle.td(Dh[:, :n], r.medoids)
     kmedoids_release_host_cache()
+
+
+def test_input_validation_diagonal_nan_negative():
+    """The documented preconditions are checked (include/kmedoids.h): a
+    nonzero or NaN diagonal is refused at create (also for a column slab),
+    a negative or NaN dissimilarity in a medoid column at set_medoids (float
+    path); valid inputs pass."""
+    from paper_2008_05171_b200 import KMError
+    rng = np.random.default_rng(31)
+    D = rand_int(rng, 40, 100)
+    Dbad = D.copy()
+    Dbad[7, 7] = 3
+    with pytest.raises(KMError):
+        KM(to_dev(Dbad), 40, 3)
+    # a column slab [8, 40): its diagonal entries D[o][o - 8]
+    slab = np.ascontiguousarray(D[:, 8:])
+    slab[20, 12] = 1
+    with pytest.raises(KMError):
+        KM(torch.from_numpy(np.ascontiguousarray(np.pad(slab, ((0, 0), (0, 0)))).view(np.int32)).cuda(), 40, 3,
+           col_begin=8, col_end=40)
+    F = rand_int(rng, 40, 100).astype(np.float32)
+    Fn = F.copy()
+    Fn[5, 5] = np.nan
+    with pytest.raises(KMError):
+        KM(to_dev(Fn), 40, 3)
+    Fm = F.copy()
+    Fm[11, 2] = -1.0                              # d(x_11, m) < 0 for the medoid m = 2
+    km = KM(to_dev(Fm), 40, 3)
+    with pytest.raises(KMError):
+        km.set_medoids([2, 4, 6])
+    Fm[11, 2] = np.nan
+    km = KM(to_dev(Fm), 40, 3)
+    with pytest.raises(KMError):
+        km.set_medoids([2, 4, 6])
+    km.set_medoids([3, 4, 6])                     # columns without the bad value: accepted
+    KM(to_dev(F), 40, 3).set_medoids([2, 4, 6])
