@@ -746,7 +746,7 @@ k_swap_stream_seg2(const T* __restrict__ D, int64_t ld, int w, int wpad, int n, 
 // a4: complete the segments cut by part boundaries, take the lexicographic
 // min over slots of (R_i + acc_i, i) (Alg.3, smaller slot on ties), add
 // dTD^{+x_c}, mask medoids, and reduce (dTD, i, c) over the grid.
-template <typename A>
+template <typename A, int QU = 8>
 __global__ void k_swap_combine(int w, int64_t col_begin, int P, const A* __restrict__ in_plus,
                                const A* __restrict__ in_head, const A* __restrict__ in_tail,
                                const A* __restrict__ in_imin, const int* __restrict__ in_islot,
@@ -783,10 +783,12 @@ __global__ void k_swap_combine(int w, int64_t col_begin, int P, const A* __restr
         };
         A plus = 0, carry = 0;
         int cs = -1;
-        constexpr int QU = 8;                  // parts loaded ahead (memory-level parallelism)
+        // QU parts loaded ahead (memory-level parallelism: one thread per
+        // column gives only ~10 warps per SM at C4, so each keeps 5 QU loads
+        // in flight); the part slots are read in the fold (shared memory)
         for (int q0 = 0; q0 < P; q0 += QU) {
             A pl[QU], hv[QU], tv[QU], iv[QU];
-            int isl[QU], hs[QU], ts[QU];
+            int isl[QU];
 #pragma unroll
             for (int u = 0; u < QU; ++u) {
                 const int q = q0 + u;
@@ -794,14 +796,13 @@ __global__ void k_swap_combine(int w, int64_t col_begin, int P, const A* __restr
                     const int64_t idx = (int64_t)q * w + cl;
                     pl[u] = in_plus[idx]; hv[u] = in_head[idx]; tv[u] = in_tail[idx];
                     iv[u] = in_imin[idx]; isl[u] = in_islot[idx];
-                    hs[u] = head_slot[q]; ts[u] = tail_slot[q];
                 }
             }
 #pragma unroll
             for (int u = 0; u < QU; ++u) {
                 if (q0 + u >= P) break;
                 plus += pl[u];
-                const int h = hs[u], t = ts[u];
+                const int h = head_slot[q0 + u], t = tail_slot[q0 + u];
                 if (h == cs) {
                     carry += hv[u];
                 } else {
