@@ -90,6 +90,15 @@ const char* kmedoids_last_error(void);
  * Errors: KM_EINVAL for duplicates / out of range. */
 km_status kmedoids_set_medoids(km_handle* h, const int32_t* medoids);
 
+/* Declare D exactly symmetric (symmetric = 1): d(x_o, x_c) == d(x_c, x_o)
+ * bitwise for all o, c < n -- true of every metric dissimilarity matrix.
+ * Verified by one tiled pass over D (KM_EINVAL and the flag stays off if any
+ * pair differs).  With it, the FastPAM2 sequential phase reads candidate c's
+ * distances as row c (4n contiguous bytes) instead of the strided column
+ * (n separate sectors); results are unchanged.  symmetric = 0 turns it off.
+ * Single GPU only (a column slab holds no whole rows: KM_EINVAL). */
+km_status kmedoids_set_symmetric(km_handle* h, int32_t symmetric);
+
 /* PAM BUILD (Alg.1; readings R3/R4) on the device; leaves the
  * handle ready for SWAP.  medoids_out (host, k entries) and td_out
  * (int64_t* or double*) may be NULL.  Single GPU only (sharded BUILD is

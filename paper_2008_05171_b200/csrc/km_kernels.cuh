@@ -122,6 +122,34 @@ __global__ void k_validate_cols(const T* __restrict__ MC, int64_t cnt, int* __re
     if (threadIdx.x == 0 && b) atomicAdd(bad, 1);
 }
 
+// Exact symmetry of the n x n matrix (kmedoids_set_symmetric): tile (bi, bj)
+// with bi <= bj is compared with the transpose of tile (bj, bi) through
+// shared memory (both read coalesced: one pass over D); *bad counts the
+// mismatching pairs (bitwise comparison).
+template <typename T>
+__global__ void k_check_symmetric(const T* __restrict__ D, int64_t ld, int n, int* __restrict__ bad) {
+    __shared__ T ta[32][33], tb[32][33];
+    const int bi = blockIdx.y, bj = blockIdx.x;
+    if (bj < bi) return;
+    const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;     // 32 x 8 threads
+    for (int r = ty; r < 32; r += 8) {
+        const int i = bi * 32 + r, j = bj * 32 + tx;
+        ta[r][tx] = (i < n && j < n) ? D[(int64_t)i * ld + j] : (T)0;
+        const int i2 = bj * 32 + r, j2 = bi * 32 + tx;
+        tb[r][tx] = (i2 < n && j2 < n) ? D[(int64_t)i2 * ld + j2] : (T)0;
+    }
+    __syncthreads();
+    int cnt = 0;
+    for (int r = ty; r < 32; r += 8) {
+        uint32_t a, b;                                  // bitwise (4-byte elements)
+        const T va = ta[r][tx], vb = tb[tx][r];
+        memcpy(&a, &va, 4); memcpy(&b, &vb, 4);
+        cnt += a != b;
+    }
+    cnt = __syncthreads_count(cnt);
+    if (threadIdx.x == 0 && cnt) atomicAdd(bad, cnt);
+}
+
 // MC[j][o] = d(x_o, m_j) for every slot j whose medoid lies in the local
 // column range (single GPU: all of them).  grid = (ceil(n/256), k).
 template <typename T>
@@ -1062,7 +1090,7 @@ k_fp2_sequential(const T* __restrict__ D, int64_t ld, const T* __restrict__ cols
                  T* __restrict__ MC, int* __restrict__ near, int* __restrict__ sec, T* __restrict__ dn,
                  T* __restrict__ ds, T* __restrict__ cols, A* __restrict__ td, A* __restrict__ partials,
                  Decision<A>* __restrict__ dec, Rec<A>* __restrict__ trace, int trace_cap,
-                 int* __restrict__ rescan, int* __restrict__ rescan_count) {
+                 int* __restrict__ rescan, int* __restrict__ rescan_count, int sym) {
     namespace cg = cooperative_groups;
     cg::grid_group grid = cg::this_grid();
     __shared__ A sred[8][FP2_B];
@@ -1108,7 +1136,11 @@ k_fp2_sequential(const T* __restrict__ D, int64_t ld, const T* __restrict__ cols
 #pragma unroll
             for (int b = 0; b < FP2_B; ++b) {
                 if (b >= nb) continue;               // (fully unrolled: part[] stays in registers)
-                const T x = colsrc ? colsrc[(int64_t)colidx[s_r[b]] * n + o] : D[(int64_t)o * ld + s_c[b]];
+                // column c of the batch: the gathered copy (sharded), row c when D is
+                // declared symmetric (coalesced: 4n bytes instead of n sectors), else
+                // the strided column
+                const T x = colsrc ? colsrc[(int64_t)colidx[s_r[b]] * n + o]
+                                   : sym ? D[(int64_t)s_c[b] * ld + o] : D[(int64_t)o * ld + s_c[b]];
                 cols[(int64_t)b * n + o] = x;
                 if (r > 0) {
                     A f = 0;

@@ -137,6 +137,7 @@ struct ImplBase {
                                 bool* converged) = 0;
     virtual km_status fp1_run_pipelined(int32_t max_iter, int32_t* iters_out, int32_t* swaps_out, bool* converged) = 0;
     virtual km_status check_diagonal() = 0;
+    virtual km_status set_symmetric(int32_t on) = 0;
     bool profiling = false;
     double prof_ms = 0.0;
     int64_t prof_launches = 0;
@@ -371,6 +372,25 @@ struct Impl : ImplBase {
         KM_CK(cudaMemcpyAsync(M, Mh, k * sizeof(int32_t), cudaMemcpyHostToDevice, st));
         KM_CK(cudaMemcpyAsync(point_slot, ps.data(), n * sizeof(int32_t), cudaMemcpyHostToDevice, st));
         KM_CK(cudaStreamSynchronize(st));   // ps goes out of scope
+        return KM_OK;
+    }
+
+    // D declared exactly symmetric (kmedoids_set_symmetric): verified by one
+    // tiled pass; the FastPAM2 re-evaluations then read candidate rows
+    bool symmetric = false;
+    km_status set_symmetric(int32_t on) override {
+        if (!on) { symmetric = false; return KM_OK; }
+        if (sharded) return fail(KM_EINVAL, "set_symmetric on a sharded handle (a slab holds no whole rows)");
+        KM_CK(cudaMemsetAsync(bad_count, 0, sizeof(int), st));
+        const unsigned nb = (unsigned)cdiv(n, 32);
+        if (nb > 65535) return fail(KM_EINVAL, "set_symmetric: n too large for the check grid");
+        km::k_check_symmetric<T><<<dim3(nb, nb), 256, 0, st>>>(D, ld, (int)n, bad_count);
+        KM_CKL();
+        int nbad = 0;
+        KM_CK(cudaMemcpyAsync(&nbad, bad_count, sizeof(int), cudaMemcpyDeviceToHost, st));
+        KM_CK(cudaStreamSynchronize(st));
+        if (nbad) return fail(KM_EINVAL, "D is not symmetric (%d mismatching entries)", nbad);
+        symmetric = true;
         return KM_OK;
     }
 
@@ -1000,8 +1020,9 @@ struct Impl : ImplBase {
         int* op = fp2_order; Rec* bp = fp2_best; const int* mp = fp2_m;
         const T* csp = colsrc; const int* cip = colidx_dev;
         int* rsp = rescan; int* rcp = rescan_count;
+        int symv = symmetric ? 1 : 0;
         void* args[] = {&Dp, &ldv, &csp, &cip, &nn, &kk, &op, &mp, &bp, &Mp, &psp, &MCp, &nr, &sc, &dnp, &dsp, &cb,
-                        &tdp, &pp, &dp, &tr, &tc, &rsp, &rcp};
+                        &tdp, &pp, &dp, &tr, &tc, &rsp, &rcp, &symv};
         KM_CK(cudaLaunchCooperativeKernel((void*)km::k_fp2_sequential<T, A>, dim3(fp2_blocks), dim3(256), args, 0,
                                           st));
         ++launches;
@@ -2694,6 +2715,11 @@ km_status kmedoids_last_swaps(km_handle* h, int32_t* slots_out, int32_t* cands_o
 km_status kmedoids_fp2_last_plan(km_handle* h, void* v_out, int32_t* c_out, int32_t* order_out, int32_t* m_out) {
     KM_H();
     return h->impl->fp2_last_plan(v_out, c_out, order_out, m_out);
+}
+
+km_status kmedoids_set_symmetric(km_handle* h, int32_t symmetric) {
+    KM_H();
+    return h->impl->set_symmetric(symmetric);
 }
 
 km_status kmedoids_set_profiling(km_handle* h, int32_t enable) {

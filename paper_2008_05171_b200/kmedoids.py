@@ -77,6 +77,7 @@ def load_library() -> ctypes.CDLL:
         "kmedoids_get_cache": [vp, vp, vp, vp, vp],
         "kmedoids_eval_candidates": [vp, vp, vp],
         "kmedoids_set_profiling": [vp, i32],
+        "kmedoids_set_symmetric": [vp, i32],
         "kmedoids_last_swaps": [vp, vp, vp, vp, i32, vp],
         "kmedoids_fp2_last_plan": [vp, vp, vp, vp, vp],
         "kmedoids_stream_time": [vp, vp, vp, i32],
@@ -195,6 +196,10 @@ class KMedoids:
         if M.shape != (self.k,):
             raise ValueError(f"expected {self.k} medoids")
         _check(load_library().kmedoids_set_medoids(self.h, _p(M)))
+
+    def set_symmetric(self, on=True):
+        """Declare D exactly symmetric (verified on the device; kmedoids.h)."""
+        _check(load_library().kmedoids_set_symmetric(self.h, int(on)))
 
     def init_build(self):
         M = np.zeros(self.k, np.int32)

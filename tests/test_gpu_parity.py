@@ -529,3 +529,28 @@ def test_input_validation_diagonal_nan_negative():
         km.set_medoids([2, 4, 6])
     km.set_medoids([3, 4, 6])                     # columns without the bad value: accepted
     KM(to_dev(F), 40, 3).set_medoids([2, 4, 6])
+
+
+@pytest.mark.parametrize("seed", range(3))
+def test_fastpam2_symmetric_rows_equal_oracle(seed):
+    """kmedoids_set_symmetric: verified on the device (an asymmetric D is
+    refused), after which the FastPAM2 re-evaluations read candidate rows --
+    the trace is still the oracle's, bit for bit."""
+    from paper_2008_05171_b200 import KMError
+    rng = np.random.default_rng(6100 + seed)
+    n, k = int(rng.choice([513, 1500, 2222])), int(rng.integers(5, 60))
+    D = rand_int(rng, n, int(rng.choice([6, 1000])))
+    M0 = rng.choice(n, size=k, replace=False).astype(np.int32)
+    ref = oracle.swap_run(D, M0, oracle.FASTPAM2)
+    km = KM(to_dev(D), n, k)
+    km.set_symmetric(True)
+    km.set_medoids(M0)
+    r = km.run(use_build=False, variant="fastpam2")
+    assert r.medoids.tolist() == ref.medoids.tolist() and r.td == ref.td
+    assert (r.n_iter, r.n_swaps) == (ref.n_iter, ref.n_swaps)
+    A = rand_int(rng, 300, 50, symmetric=False)
+    km2 = KM(to_dev(A), 300, 4)
+    with pytest.raises(KMError):
+        km2.set_symmetric(True)
+    A[np.tril_indices(300, -1)] = A.T[np.tril_indices(300, -1)]      # now symmetric
+    KM(to_dev(A), 300, 4).set_symmetric(True)
