@@ -67,6 +67,7 @@ struct PostArgs {
     int P;
     int *head_slot, *tail_slot;
     int prep_only;             // 1: phases count, B, C only (slot sort, R, parts of the current cache)
+    int allow_reg;             // 0: always the chunk loops (KM_POST_REG=0, tests of chunks > POST_THREADS)
     IterMirror<A>* h_ring;     // pinned host ring of iteration outcomes (or null)
     int ring;                  // its size
     int* seq;                  // device counter of FastPAM1 post launches (ring slot = seq % ring)
@@ -125,7 +126,7 @@ k_fp1_post(PostArgs<T, A> g) {
     // chunks of at most POST_THREADS objects (n <= POST_THREADS * blocks:
     // every BASELINE config) keep one object per thread in registers; the
     // cache loads are issued before the decision is known
-    const bool reg = ob1 - ob0 <= POST_THREADS;
+    const bool reg = g.allow_reg && ob1 - ob0 <= POST_THREADS;
     const int myo = ob0 + threadIdx.x;
     const bool have = reg && myo < ob1;
     int j1 = 0, j2 = 0;

@@ -614,6 +614,7 @@ struct Impl : ImplBase {
         return KM_OK;
     }
 
+    int post_reg = -1;
     km_status launch_post(bool prep_only = false) {
         km::PostArgs<T, A> g;
         g.D = D; g.ld = ld; g.n = (int)n; g.k = k; g.c0 = c0; g.c1 = c1; g.recs = rec_local; g.nrec = 1;
@@ -623,6 +624,11 @@ struct Impl : ImplBase {
         g.ri = ri; g.rowd = rowd; g.R = R; g.P = P; g.head_slot = head_slot; g.tail_slot = tail_slot;
         g.tph = post_tph;
         g.prep_only = prep_only ? 1 : 0;
+        if (post_reg < 0) {                 // KM_POST_REG=0: the chunk-loop path (large-n path, for tests)
+            const char* e = getenv("KM_POST_REG");
+            post_reg = (e && e[0] == '0') ? 0 : 1;
+        }
+        g.allow_reg = post_reg;
         g.h_ring = h_ring; g.ring = RING; g.seq = post_seq;
         void* args[] = {&g};
         KM_CK(cudaLaunchCooperativeKernel((void*)km::k_fp1_post<T, A>, dim3(post_blocks), dim3(km::POST_THREADS), args,

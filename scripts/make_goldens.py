@@ -16,6 +16,8 @@ whole trajectory with:
   c4_fastpam1   C4: FastPAM1 from the BUILD medoids of c4_build, to convergence
   c5_fastpam2   C5 n=100000 k=500 u32: random init + 3 FastPAM2 iterations,
                 with the per-slot plan of each iteration
+  c3_fasterpam  C3: random init + FasterPAM (Alg.4, readings F1-F5) to convergence
+  c4_fasterpam  C4: FasterPAM from the c4_build medoids to convergence
 
 D is materialised on the CPU by kmsynth.dist_cpu, which is bit-identical to
 kmsynth.dist_numpy and to the CUDA materialiser the GPU tests use (tests:
@@ -159,6 +161,23 @@ def job_random(cid, name, variant, plan_iters=0, max_iter=2000):
     write(name, g)
 
 
+def job_fasterpam(cid, name, from_build=None):
+    cfg, D = make_D(cid)
+    if from_build:
+        with open(os.path.join(OUT, from_build + ".json")) as f:
+            M0 = np.asarray(json.load(f)["build"]["medoids"], np.int32)
+        what = f"FasterPAM (Alg.4, F1-F5) to convergence from the {from_build} medoids"
+    else:
+        M0 = kmsynth.random_medoids(cfg)
+        what = "random init (seed+1000) + FasterPAM (Alg.4, F1-F5) to convergence"
+    t = time.time()
+    r = oracle.fasterpam_run(D, M0)
+    g = header(cfg, D, name, what)
+    g["run"] = {"init": M0.tolist(), "trace": [[a, b, num(v), int(p)] for a, b, v, p in r.trace],
+                "final": final_block(D, r), "oracle_s": round(time.time() - t, 1)}
+    write(name, g)
+
+
 JOBS = {
     "c2_fastpam1": lambda: job_build_fp1(2, "c2_fastpam1"),
     "c3_fastpam1": lambda: job_random(3, "c3_fastpam1", oracle.FASTPAM1),
@@ -166,6 +185,8 @@ JOBS = {
     "c4_build": lambda: job_build_fp1(4, "c4_build", with_swap=False),
     "c4_fastpam1": job_c4_fastpam1,
     "c5_fastpam2": lambda: job_random(5, "c5_fastpam2", oracle.FASTPAM2, plan_iters=3, max_iter=3),
+    "c3_fasterpam": lambda: job_fasterpam(3, "c3_fasterpam"),
+    "c4_fasterpam": lambda: job_fasterpam(4, "c4_fasterpam", from_build="c4_build"),
 }
 
 if __name__ == "__main__":

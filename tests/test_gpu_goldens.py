@@ -259,3 +259,44 @@ def test_c5_fastpam2_three_iterations_bit_exact():
         f = ref["final"]
         assert r.medoids.tolist() == f["medoids"] and r.td == f["td"]
         assert sha(r.assignment.astype(np.int32)) == f["assignment_sha256"]
+
+
+def fasterpam_passes(km, max_iter=2000):
+    trace, passes = [], 0
+    for _ in range(max_iter):
+        conv, sw, td = km.swap_iter("fasterpam")
+        got = km.last_swaps()
+        assert len(got) == sw
+        trace += got
+        passes += 1
+        if conv:
+            return trace, passes, True
+    return trace, passes, False
+
+
+def check_fasterpam(name):
+    """FasterPAM (Alg.4, readings F1-F5) at full size: the eager swap sequence
+    (slot, candidate, dTD) equals the oracle's scan, up to an R8-admissible
+    near tie; passes, swaps, medoids, TD and the assignment of the end state."""
+    from paper_2008_05171_b200 import KMedoids
+    g = gold(name)
+    cfg, Dt = make_D(g)
+    ref = g["run"]
+    with KMedoids(Dt, cfg.n, cfg.k) as km:
+        km.set_medoids(ref["init"])
+        td0 = km.get_state().td
+        trace, passes, conv = fasterpam_passes(km)
+        assert conv
+        j = compare_trace(Dt, cfg.n, ref["init"], trace, [t[:3] for t in ref["trace"]], td0, exact=False)
+        f = dict(ref["final"])
+        check_final(km, Dt, f, False, j < len(ref["trace"]))
+
+
+def test_c3_fasterpam_full_run():
+    """C3 (n=20000, k=100, f32), random init: FasterPAM to convergence."""
+    check_fasterpam("c3_fasterpam")
+
+
+def test_c4_fasterpam_full_run():
+    """C4 (n=50000, k=200, f32): FasterPAM from the oracle's BUILD medoids."""
+    check_fasterpam("c4_fasterpam")

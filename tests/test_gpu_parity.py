@@ -554,3 +554,23 @@ def test_fastpam2_symmetric_rows_equal_oracle(seed):
         km2.set_symmetric(True)
     A[np.tril_indices(300, -1)] = A.T[np.tril_indices(300, -1)]      # now symmetric
     KM(to_dev(A), 300, 4).set_symmetric(True)
+
+
+@pytest.mark.parametrize("variant", ["fastpam1", "fastpam2"])
+def test_post_chunk_loop_path_equals_oracle(variant, monkeypatch):
+    """The post kernel's chunk-loop path (taken when a block owns more than 256
+    objects, n > ~113,000 on a B200; forced here with KM_POST_REG=0) gives the
+    oracle's exact trace, on several sizes and many ties."""
+    monkeypatch.setenv("KM_POST_REG", "0")
+    rng = np.random.default_rng(9100)
+    for n, k, hi in [(2500, 11, 5), (777, 40, 1000), (3000, 3, 100000)]:
+        D = rand_int(rng, n, hi, symmetric=bool(k % 2))
+        M0 = rng.choice(n, size=k, replace=False).astype(np.int32)
+        ref = oracle.swap_run(D, M0, oracle.FASTPAM1 if variant == "fastpam1" else oracle.FASTPAM2)
+        km = KM(to_dev(D), n, k)
+        km.set_medoids(M0)
+        r = km.run(use_build=False, variant=variant)
+        assert r.medoids.tolist() == ref.medoids.tolist() and r.td == ref.td
+        assert (r.n_iter, r.n_swaps) == (ref.n_iter, ref.n_swaps)
+        assert r.assignment.tolist() == ref.assignment.tolist()
+        km.close()
