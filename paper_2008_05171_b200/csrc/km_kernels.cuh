@@ -614,8 +614,15 @@ k_swap_stream_seg2(const T* __restrict__ D, int64_t ld, int w, int wpad, int n, 
         const uint64_t keep = ptx::policy_evict_last();   // row metadata: re-read by every column tile
         int64_t pr = p0;
         int s = 0, ph = 0, st = 0;
-        int o_l = 0, sl_l = -1;
-        if (lane < RB && pr + lane < p1) { const RowInfo<T> r = ri[pr + lane]; o_l = r.o; sl_l = r.slot; }
+        // row metadata in a 64-row register window: lane l holds (o, slot)
+        // of rows wb + l (current half) and wb + 32 + l (next half, loaded
+        // 32 rows ahead), so forming a stage never waits on a global load
+        // (round 1 reloaded the vacated rows every stage: one dependent L2
+        // round trip in the producer's loop)
+        int64_t wb = p0;
+        int o_c = 0, s_c = -1, o_n = 0, s_n = -1;
+        if (wb + lane < p1) { const RowInfo<T> r = ri[wb + lane]; o_c = r.o; s_c = r.slot; }
+        if (wb + 32 + lane < p1) { const RowInfo<T> r = ri[wb + 32 + lane]; o_n = r.o; s_n = r.slot; }
         while (true) {
             if (st >= S) ptx::mbar_wait(&empty[s], ph ^ 1);
             if (pr >= p1) {
@@ -625,6 +632,12 @@ k_swap_stream_seg2(const T* __restrict__ D, int64_t ld, int w, int wpad, int n, 
                 }
                 break;
             }
+            // rows pr .. pr + RB - 1 (window positions li .. li + RB - 1 < 64)
+            const int li = (int)(pr - wb);
+            const int src = (li + lane) & 31;
+            const int oc = __shfl_sync(FULL, o_c, src), sc = __shfl_sync(FULL, s_c, src);
+            const int on = __shfl_sync(FULL, o_n, src), sn = __shfl_sync(FULL, s_n, src);
+            const int o_l = li + lane < 32 ? oc : on, sl_l = li + lane < 32 ? sc : sn;
             const int slot0 = __shfl_sync(FULL, sl_l, 0);
             const unsigned same = __ballot_sync(FULL, lane < RB && sl_l == slot0 && pr + lane < p1);
             const int nb = __ffs(~same) - 1;
@@ -640,12 +653,11 @@ k_swap_stream_seg2(const T* __restrict__ D, int64_t ld, int w, int wpad, int n, 
             if (lane == 0) ptx::bulk_g2s(sri + s * RB, ri + pr, (uint32_t)nb * 16u, &full[s], keep);
             if (lane == 1 && rowd) ptx::bulk_g2s(srd + s * RB, rowd + pr, (uint32_t)nb * 16u, &full[s], keep);
             pr += nb;
-            const int o_sh = __shfl_down_sync(FULL, o_l, nb);
-            const int s_sh = __shfl_down_sync(FULL, sl_l, nb);
-            if (lane < RB) {
-                if (lane + nb < RB) { o_l = o_sh; sl_l = s_sh; }
-                else if (pr + lane < p1) { const RowInfo<T> r = ri[pr + lane]; o_l = r.o; sl_l = r.slot; }
-                else { sl_l = -1; }
+            if (pr - wb >= 32) {                 // advance the window by 32 rows, prefetch the next half
+                wb += 32;
+                o_c = o_n; s_c = s_n;
+                s_n = -1;
+                if (wb + 32 + lane < p1) { const RowInfo<T> r = ri[wb + 32 + lane]; o_n = r.o; s_n = r.slot; }
             }
             ++st;
             if (++s == S) { s = 0; ph ^= 1; }
