@@ -131,16 +131,30 @@ k_build_delta_tma(const T* __restrict__ D, int64_t ld, int w, int wpad, int P, c
     if (warp == NC) {
         const uint32_t cbytes = (uint32_t)min(C::COLS, wpad - ctacol) * (uint32_t)sizeof(T);
         const uint64_t pol = ptx::policy_evict_first();
+        // the list entries in a 64-row register window, the next 32 loaded
+        // 32 rows ahead (no dependent global load in front of a stage's copies)
+        int64_t wb = p0;
+        int o_c = wb + lane < p1 ? lst_o[wb + lane] : 0;
+        int o_n = wb + 32 + lane < p1 ? lst_o[wb + 32 + lane] : 0;
         for (int st = 0; st < nstages; ++st) {
             const int s = st % S;
             if (st >= S) ptx::mbar_wait(&empty[s], ((st / S) & 1) ^ 1);
             const int64_t pr = p0 + (int64_t)st * RB;
             const int nb = (int)min((int64_t)RB, p1 - pr);
+            const int li = (int)(pr - wb);
+            const int src = (li + lane) & 31;
+            const int oc = __shfl_sync(FULL, o_c, src), on = __shfl_sync(FULL, o_n, src);
+            const int o = li + lane < 32 ? oc : on;
             if (lane == 0) ptx::mbar_expect_tx(&full[s], (uint32_t)nb * cbytes);
             __syncwarp();
             if (lane < nb)
-                ptx::bulk_g2s(sdata + (size_t)(s * RB + lane) * C::COLS, D + (int64_t)lst_o[pr + lane] * ld + ctacol,
-                              cbytes, &full[s], pol);
+                ptx::bulk_g2s(sdata + (size_t)(s * RB + lane) * C::COLS, D + (int64_t)o * ld + ctacol, cbytes,
+                              &full[s], pol);
+            if (pr + RB - wb >= 32) {            // the next stage starts in the next half
+                wb += 32;
+                o_c = o_n;
+                o_n = wb + 32 + lane < p1 ? lst_o[wb + 32 + lane] : 0;
+            }
         }
         return;
     }
