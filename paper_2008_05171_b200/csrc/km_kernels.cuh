@@ -563,7 +563,7 @@ struct SegCfg {
 // exact in fp64 / int64); only the summation grouping differs from the
 // oracle's object order (reading R9).
 // ---------------------------------------------------------------------------
-template <typename T, typename A, int NC, int RB, int S, int MINB = 2, bool STAGED = true, bool CMP64 = false>
+template <typename T, typename A, int NC, int RB, int S, int MINB = 2>
 __global__ void __launch_bounds__((NC + 1) * 32, MINB)
 k_swap_stream_seg2(const T* __restrict__ D, int64_t ld, int w, int wpad, int n, int P,
                    const RowInfo<T>* __restrict__ ri, const A* __restrict__ R,
@@ -746,11 +746,11 @@ k_swap_stream_seg2(const T* __restrict__ D, int64_t ld, int w, int wpad, int n, 
             continue;
         }
         A dnA[RB], dsA[RB];
-        if constexpr (Acc<T>::is_float && STAGED) {   // widened thresholds staged by the producer
+        if constexpr (Acc<T>::is_float) {       // widened thresholds staged by the producer
             const double2* sr = srd + cs * RB;
 #pragma unroll
             for (int u = 0; u < RB; ++u) { const double2 qq = sr[u]; dnA[u] = qq.x; dsA[u] = qq.y; }
-            if (CMP64 && nb < RB) {                     // rows beyond a short stage never compare below
+            if (nb < RB) {                              // rows beyond a short stage never compare below
 #pragma unroll
                 for (int u = 1; u < RB; ++u)
                     if (u >= nb) { dnA[u] = -INFINITY; dsA[u] = -INFINITY; }
@@ -768,13 +768,11 @@ k_swap_stream_seg2(const T* __restrict__ D, int64_t ld, int w, int wpad, int n, 
 #pragma unroll
                 for (int u = 0; u < RB; ++u) {
                     const A xa = (A)x[u][j];
-                    if constexpr (CMP64) {           // compare the widened values: dn / ds dead after the vote
-                        tq[u] = (xa < dsA[u]) ? xa - dsA[u] : (A)0;
-                        tt[u] = (xa < dnA[u]) ? xa - dnA[u] : (A)0;
-                    } else {
-                        tq[u] = (x[u][j] < ds[u]) ? xa - dsA[u] : (A)0;
-                        tt[u] = (x[u][j] < dn[u]) ? xa - dnA[u] : (A)0;
-                    }
+                    // compared on the widened values (exact): the f32 dn / ds
+                    // are dead after the vote (round 2: no spills, C4 stream
+                    // -19 us, C3 -9 us against f32 compares here)
+                    tq[u] = (xa < dsA[u]) ? xa - dsA[u] : (A)0;
+                    tt[u] = (xa < dnA[u]) ? xa - dnA[u] : (A)0;
                 }
                 const A sq = (tq[0] + tq[1]) + (tq[2] + tq[3]);
                 const A sp = (tt[0] + tt[1]) + (tt[2] + tt[3]);

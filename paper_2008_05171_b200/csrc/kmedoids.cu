@@ -539,28 +539,14 @@ struct Impl : ImplBase {
     }
 
     bool seg2_attr_set = false;
-    int stream_staged = -1;
     const char* stream_kernel_name() const override { return "k_swap_stream_seg2"; }
     template <int NC, int RB, int S, int MINB = 2>
     km_status launch_seg2(const T* Dw, int ww, int wpadw, int Pw, A* plus_o, A* head_o, A* tail_o, A* imin_o,
                           int* islot_o, A* acc_out, const int* skip_if = nullptr) {
         using C = km::SegCfg<T, NC, RB, S>;
-        if (stream_staged < 0) {            // KM_STREAM_STAGED=0: float thresholds widened in the consumer (A/B)
-            const char* e = getenv("KM_STREAM_STAGED");
-            stream_staged = (e && e[0] == '0') ? 0 : (e && e[0] == '2') ? 2 : 1;
-        }
-        // 1: thresholds widened by the producer (rowd), f32 compares; 0: widened in
-        // the consumer; 2: staged, compares on the widened values (measurement)
-        auto kern = stream_staged == 1 ? km::k_swap_stream_seg2<T, A, NC, RB, S, MINB, true, false>
-                    : stream_staged == 2 ? km::k_swap_stream_seg2<T, A, NC, RB, S, MINB, true, true>
-                                         : km::k_swap_stream_seg2<T, A, NC, RB, S, MINB, false, false>;
+        auto kern = km::k_swap_stream_seg2<T, A, NC, RB, S, MINB>;
         if (!seg2_attr_set) {
-            KM_CK(cudaFuncSetAttribute(km::k_swap_stream_seg2<T, A, NC, RB, S, MINB, true, false>,
-                                       cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM));
-            KM_CK(cudaFuncSetAttribute(km::k_swap_stream_seg2<T, A, NC, RB, S, MINB, true, true>,
-                                       cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM));
-            KM_CK(cudaFuncSetAttribute(km::k_swap_stream_seg2<T, A, NC, RB, S, MINB, false, false>,
-                                       cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM));
+            KM_CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM));
             seg2_attr_set = true;
         }
         dim3 g((unsigned)cdiv(ww, C::COLS), Pw);
@@ -568,7 +554,7 @@ struct Impl : ImplBase {
         // that follows when they fit comfortably (C3: 16 MB), else streamed
         const bool acc_keep = acc_out && (size_t)k * ww * sizeof(A) <= ((size_t)48 << 20);
         kern<<<g, C::THREADS, C::SMEM, st>>>(Dw, ld, ww, wpadw, (int)n, Pw, ri, R, plus_o, head_o, tail_o, imin_o,
-                                              islot_o, acc_out, stream_staged ? rowd : nullptr, acc_keep, skip_if);
+                                              islot_o, acc_out, rowd, acc_keep, skip_if);
         return KM_OK;
     }
 
