@@ -24,7 +24,8 @@ def launches(path, out):
         agg[name][0] += 1
         agg[name][1] += float(r[iv].replace(",", "")) * scale.get(r[iu], 1.0)
     tot = sum(v for _, v in agg.values())
-    init_only = ("km::k_assign_full", "km::k_td_from_dn", "km::k_chunk_scan", "km::k_gather_medoid_cols")
+    init_only = ("km::k_assign_full", "km::k_td_from_dn", "km::k_chunk_scan", "km::k_gather_medoid_cols",
+                 "km::k_check_symmetric", "km::k_validate_diag", "km::k_validate_cols")
     swap = [k for k in agg if k.startswith("km::") and "build" not in k and "changed_scatter" not in k
             and not k.startswith(init_only)]
     swap_tot = sum(agg[k][1] for k in swap)
