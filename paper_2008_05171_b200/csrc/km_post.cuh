@@ -72,7 +72,40 @@ struct PostArgs {
     int ring;                  // its size
     int* seq;                  // device counter of FastPAM1 post launches (ring slot = seq % ring)
     unsigned long long* tph;   // measurement aid (KM_STEP_PROF): globaltimer after each phase, or null
+    // phase 0 (fused combine, FastPAM1 single-handle path): the stream's part
+    // outputs [P][w] are folded here instead of by k_swap_combine
+    int fuse;                  // 1: run phase 0; recs/nrec are then ignored
+    int w;                     // local columns
+    int stage0;                // 1: R and the part slots staged in dynamic shared memory
+    const A *pp_plus, *pp_head, *pp_tail, *pp_imin;
+    const int* pp_islot;
+    A* cand_v;                 // [w] dTD of the best swap per candidate (medoids: slot -1)
+    int* cand_slot;
+    Rec<A>* blk_recs;          // [gridDim] per-block best record
 };
+
+constexpr int POST_QU = 4;     // part outputs loaded ahead per lane in phase 0
+constexpr int POST_RG = 4;     // phase-0 column groups per round (merged by warps 0..3 in parallel)
+
+// Phase-0 range state of one lane (column) over a contiguous range of parts:
+// the first segment piece (may continue the previous range), the open piece
+// at the end (may continue into the next), the best completed segment / part
+// interior minimum in between, and the partial dTD^{+x_c} sum.
+template <typename A>
+struct RangeState {
+    A plus, hc, tc, bv;
+    int hs, ts, bs, single;    // single: the whole range lies in one segment (hs == ts)
+};
+
+// dynamic shared memory of k_fp1_post: k ints (16-aligned) | k A | [k A | 2P ints]
+// (phase-0 staging) | range states (16-aligned)
+template <typename A>
+__host__ __device__ inline size_t post_rs_offset(int k, int P, bool stage) {
+    const size_t base = ((size_t)k * sizeof(int) + 15) / 16 * 16 + (size_t)k * sizeof(A);
+    return (base + (stage ? (size_t)k * sizeof(A) + 2 * (size_t)P * sizeof(int) : 0) + 15) / 16 * 16;
+}
+template <typename A>
+__host__ __device__ inline size_t post_rs_bytes() { return (size_t)POST_RG * (POST_THREADS / 32) * 32 * sizeof(RangeState<A>); }
 
 __device__ __forceinline__ void post_stamp(unsigned long long* tph, int i) {
     if (tph && blockIdx.x == 0 && threadIdx.x == 0) {
@@ -121,7 +154,6 @@ k_fp1_post(PostArgs<T, A> g) {
     const int ob0 = min(n, b * ochunk), ob1 = min(n, ob0 + ochunk);
     for (int s = threadIdx.x; s < k; s += blockDim.x) { hh[s] = 0; pr[s] = 0; }
     if (threadIdx.x == 0) s_nres = 0;
-    if (b == 0 && threadIdx.x == 0) *g.empty_slot = INT_MAX;   // (read by the stream/combine before this kernel)
 
     // chunks of at most POST_THREADS objects (n <= POST_THREADS * blocks:
     // every BASELINE config) keep one object per thread in registers; the
@@ -133,14 +165,187 @@ k_fp1_post(PostArgs<T, A> g) {
     T d1 = 0, d2 = 0;
     if (have) { j1 = __ldcg(&g.near[myo]); j2 = __ldcg(&g.sec[myo]); d1 = __ldcg(&g.dn[myo]); d2 = __ldcg(&g.ds[myo]); }
 
+    const bool fused = g.fuse && !g.prep_only;
+    if (fused) {
+        // ---- 0: combine (a4, Alg.3).  Column groups of 32 (lane =
+        // column); the 8 warps of the block split the P parts into 8
+        // contiguous ranges and fold them at once (more loads in flight than
+        // one thread folding all P parts); warp 0 then merges the 8 range
+        // states in part order.  Lexicographic minima are order-free; the
+        // fp64 sums of a segment cut by parts and of dTD^{+x_c} are grouped
+        // by range (reading R9; exact on int64).
+        const int P = g.P, w = g.w;
+        // range states [POST_RG][8 warps][32 lanes] after the staging area (dynamic)
+        typedef RangeState<A> RSRow[POST_THREADS / 32][32];
+        RSRow* rs = reinterpret_cast<RSRow*>(post_smem_raw + post_rs_offset<A>(k, P, g.stage0 != 0));
+        const A* sR = g.R;
+        const int *hsl = g.head_slot, *tsl = g.tail_slot;
+        if (g.stage0) {
+            A* r_s = pr + k;
+            int* h_s = reinterpret_cast<int*>(r_s + k);
+            for (int i = threadIdx.x; i < k; i += blockDim.x) r_s[i] = __ldcg(&g.R[i]);
+            for (int i = threadIdx.x; i < P; i += blockDim.x) { h_s[i] = __ldcg(&g.head_slot[i]); h_s[P + i] = __ldcg(&g.tail_slot[i]); }
+            __syncthreads();
+            sR = r_s; hsl = h_s; tsl = h_s + P;
+        }
+        const int es = __ldcg(g.empty_slot);
+        const int nw8 = POST_THREADS / 32;
+        const int qa = warp * P / nw8, qb = (warp + 1) * P / nw8;
+        const int ngrp = (w + 31) >> 5;
+        Rec<A> best = rec_none<A>();
+        // rounds of up to POST_RG column groups: every warp folds its part
+        // range for each group of the round (no barrier in between, so the
+        // warps' loads overlap), then warp r merges group r of the round
+        for (int g0 = b; g0 < ngrp; g0 += POST_RG * B) {
+            for (int r = 0; r < POST_RG; ++r) {
+                const int grp = g0 + r * B;
+                if (grp >= ngrp) break;
+                const int cl = grp * 32 + lane;
+                const bool valid = cl < w;
+                RangeState<A> st;
+                st.plus = 0; st.hc = 0; st.tc = 0; st.bv = amax<A>();
+                st.hs = -1; st.ts = -1; st.bs = INT_MAX; st.single = 1;
+                A carry = 0;
+                int cs = -1;
+                for (int q0 = qa; q0 < qb; q0 += POST_QU) {
+                    A pl[POST_QU], hv[POST_QU], tv[POST_QU], iv[POST_QU];
+                    int isl[POST_QU];
+#pragma unroll
+                    for (int u = 0; u < POST_QU; ++u) {
+                        const int q = q0 + u;
+                        if (valid && q < qb) {
+                            const int64_t idx = (int64_t)q * w + cl;
+                            pl[u] = __ldcg(&g.pp_plus[idx]); hv[u] = __ldcg(&g.pp_head[idx]);
+                            tv[u] = __ldcg(&g.pp_tail[idx]); iv[u] = __ldcg(&g.pp_imin[idx]);
+                            isl[u] = __ldcg(&g.pp_islot[idx]);
+                        } else {
+                            pl[u] = 0; hv[u] = 0; tv[u] = 0; iv[u] = 0; isl[u] = -1;
+                        }
+                    }
+#pragma unroll
+                    for (int u = 0; u < POST_QU; ++u) {
+                        const int q = q0 + u;
+                        if (q >= qb) break;
+                        // a completed segment (s, sum): the range's first one may
+                        // continue the previous range -> kept as the head piece
+                        auto fin = [&](int s, A sum) {
+                            if (st.single) { st.hs = s; st.hc = sum; st.single = 0; }
+                            else {
+                                const A val = sR[s] + sum;
+                                if (val < st.bv || (val == st.bv && s < st.bs)) { st.bv = val; st.bs = s; }
+                            }
+                        };
+                        st.plus += pl[u];
+                        const int h = hsl[q], t = tsl[q];
+                        if (h == cs) carry += hv[u];
+                        else {
+                            if (cs >= 0) fin(cs, carry);
+                            cs = h;
+                            carry = hv[u];
+                        }
+                        if (isl[u] >= 0 && (iv[u] < st.bv || (iv[u] == st.bv && isl[u] < st.bs))) { st.bv = iv[u]; st.bs = isl[u]; }
+                        if (t != h) {
+                            fin(cs, carry);
+                            cs = t;
+                            carry = tv[u];
+                        }
+                    }
+                }
+                st.ts = cs; st.tc = carry;
+                if (st.single) { st.hs = cs; st.hc = carry; }
+                rs[r][warp][lane] = st;
+            }
+            __syncthreads();
+            {
+                const int grp = g0 + warp * B;
+                const int cl = grp * 32 + lane;
+                if (warp < POST_RG && grp < ngrp && cl < w) {
+                    A bv = amax<A>();
+                    int bs = INT_MAX;
+                    if (es != INT_MAX) { bv = 0; bs = es; }
+                    auto fin = [&](int s, A sum) {
+                        KM_ASSERT(s >= 0 && s < k);
+                        const A val = sR[s] + sum;
+                        if (val < bv || (val == bv && s < bs)) { bv = val; bs = s; }
+                    };
+                    A plus = 0, cr = 0;
+                    int c_s = -1;
+                    for (int r = 0; r < nw8; ++r) {
+                        if (r * P / nw8 == (r + 1) * P / nw8) continue;      // empty range
+                        const RangeState<A> x = rs[warp][r][lane];
+                        plus += x.plus;
+                        if (x.bs != INT_MAX && (x.bv < bv || (x.bv == bv && x.bs < bs))) { bv = x.bv; bs = x.bs; }
+                        if (x.single) {
+                            if (x.hs == c_s) cr += x.hc;
+                            else { if (c_s >= 0) fin(c_s, cr); c_s = x.hs; cr = x.hc; }
+                        } else {
+                            if (x.hs == c_s) fin(c_s, cr + x.hc);
+                            else { if (c_s >= 0) fin(c_s, cr); fin(x.hs, x.hc); }
+                            c_s = x.ts; cr = x.tc;
+                        }
+                    }
+                    fin(c_s, cr);
+                    const A dtd = bv + plus;
+                    const int64_t c = g.c0 + cl;
+                    const bool medoid = __ldcg(&g.point_slot[c]) >= 0;
+                    g.cand_v[cl] = dtd;
+                    g.cand_slot[cl] = medoid ? -1 : bs;
+                    if (!medoid) {
+                        Rec<A> x; x.v = dtd; x.slot = bs; x.c = (int)c;
+                        if (rec_less(x, best)) best = x;
+                    }
+                }
+            }
+            __syncthreads();                     // rs is rewritten by the next round
+        }
+        {
+            __shared__ Rec<A> wbest[POST_THREADS / 32];
+            best = warp_min_rec(best);
+            if (lane == 0) wbest[warp] = best;
+            __syncthreads();
+            if (warp == 0) {
+                best = lane < POST_THREADS / 32 ? wbest[lane] : rec_none<A>();
+                best = warp_min_rec(best);
+                if (lane == 0) g.blk_recs[b] = best;
+            }
+        }
+        grid.sync();
+        post_stamp(g.tph, 6);
+    }
+    if (b == 0 && threadIdx.x == 0) *g.empty_slot = INT_MAX;   // (read by the stream and the combine / phase 0)
+
     // ---- A: select
     if (!g.prep_only) {
-        if (threadIdx.x == 0) {
-            Rec<A> best = rec_none<A>();
-            for (int r = 0; r < g.nrec; ++r) {
-                const Rec<A> x = g.recs[r];
-                if (rec_less(x, best)) best = x;
+        Rec<A> best = rec_none<A>();
+        if (fused) {                            // every block: min over the block records (order-free)
+            if (warp == 0) {
+                // one 16-byte load per record, all of a lane's records in flight
+                static_assert(sizeof(Rec<A>) == 16, "Rec is 16 bytes");
+                const int4* br = reinterpret_cast<const int4*>(g.blk_recs);
+                for (int i0 = 0; i0 * 32 < B; i0 += 8) {
+                    int4 raw[8];
+#pragma unroll
+                    for (int i = 0; i < 8; ++i) {
+                        const int r = (i0 + i) * 32 + lane;
+                        raw[i] = r < B ? __ldcg(&br[r]) : make_int4(0, 0, INT_MAX, INT_MAX);
+                    }
+#pragma unroll
+                    for (int i = 0; i < 8; ++i) {
+                        if ((i0 + i) * 32 + lane >= B) continue;
+                        Rec<A> x;
+                        memcpy(&x, &raw[i], sizeof(x));
+                        if (rec_less(x, best)) best = x;
+                    }
+                }
+                best = warp_min_rec(best);
             }
+        }
+        if (threadIdx.x == 0) {
+            if (!fused)
+                for (int r = 0; r < g.nrec; ++r) {
+                    const Rec<A> x = g.recs[r];
+                    if (rec_less(x, best)) best = x;
+                }
             const A tdv = *g.td;
             bool improving;
             if (best.slot == INT_MAX) improving = false;

@@ -499,8 +499,10 @@ struct Impl : ImplBase {
         KM_CKL();
         if (pair) KM_CK(cudaEventRecord(pair[1], st));
         else if (profiling) { KM_CK(record_ev(ev_b ? ev_b : ev1)); pending_prof = true; }
-        KM_TRY(launch_combine(w, c0, P, o_plus, o_head, o_tail, o_imin, o_islot, head_slot, tail_slot, cand_v,
-                              cand_slot, nullptr, nullptr));
+        // FastPAM1 iterations fold the part outputs in the post kernel's phase 0
+        if (!(fp1_mode && post_fuse))
+            KM_TRY(launch_combine(w, c0, P, o_plus, o_head, o_tail, o_imin, o_islot, head_slot, tail_slot, cand_v,
+                                  cand_slot, nullptr, nullptr));
         return KM_OK;
     }
 
@@ -591,11 +593,22 @@ struct Impl : ImplBase {
     A* post_rpart = nullptr;
     unsigned long long* post_tph = nullptr;   // KM_STEP_PROF: phase stamps of k_fp1_post
     double post_ph_sum[8] = {};
-    size_t post_smem() const { return ((size_t)k * sizeof(int) + 15) / 16 * 16 + (size_t)k * sizeof(A); }
+    Rec* post_recs = nullptr;                  // [post_blocks] phase-0 block records
+    // k_fp1_post phase 0 (the combine folded into the post kernel; KM_POST_FUSE=0:
+    // the separate k_swap_combine, measurement override)
+    bool post_fuse = true;
+    size_t post_smem_base() const { return ((size_t)k * sizeof(int) + 15) / 16 * 16 + (size_t)k * sizeof(A); }
+    size_t post_stage_bytes() const { return (size_t)k * sizeof(A) + 2 * (size_t)P * sizeof(int); }
+    bool post_stage0() const { return post_smem_base() + post_stage_bytes() <= 24 * 1024; }
+    // fused: the staging area (when R and the part slots fit), then the range states
+    size_t post_smem() const {
+        return post_fuse ? km::post_rs_offset<A>(k, P, post_stage0()) + km::post_rs_bytes<A>() : post_smem_base();
+    }
 
     km_status post_alloc() {
         if (post_counts) return KM_OK;
         auto kern = km::k_fp1_post<T, A>;
+        if (const char* e = getenv("KM_POST_FUSE")) post_fuse = e[0] != '0';
         const size_t sm = post_smem();
         if (sm > 48 * 1024) KM_CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
         int dev = 0, per_sm = 0, nsm = 0;
@@ -610,6 +623,7 @@ struct Impl : ImplBase {
         KM_TRY(alloc(&post_counts, (size_t)k * post_blocks));
         KM_TRY(alloc(&post_offsets, (size_t)k * post_blocks));
         KM_TRY(alloc(&post_rpart, (size_t)k * post_blocks));
+        KM_TRY(alloc(&post_recs, post_blocks));
         if (step_prof) KM_TRY(alloc(&post_tph, 16));
         return KM_OK;
     }
@@ -630,6 +644,10 @@ struct Impl : ImplBase {
         }
         g.allow_reg = post_reg;
         g.h_ring = h_ring; g.ring = RING; g.seq = post_seq;
+        g.fuse = (post_fuse && !prep_only) ? 1 : 0;
+        g.w = w; g.stage0 = post_stage0() ? 1 : 0;
+        g.pp_plus = o_plus; g.pp_head = o_head; g.pp_tail = o_tail; g.pp_imin = o_imin; g.pp_islot = o_islot;
+        g.cand_v = cand_v; g.cand_slot = cand_slot; g.blk_recs = post_recs;
         void* args[] = {&g};
         KM_CK(cudaLaunchCooperativeKernel((void*)km::k_fp1_post<T, A>, dim3(post_blocks), dim3(km::POST_THREADS), args,
                                           post_smem(), st));
@@ -843,17 +861,21 @@ struct Impl : ImplBase {
         KM_CK(cudaEventElapsedTime(&t[4], sp_ev[3], sp_ev[4]));
         for (int i = 0; i < 5; ++i) sp_sum[i] += t[i];
         if (post_tph) {
-            unsigned long long h[6];
+            unsigned long long h[7];
             KM_CK(cudaMemcpy(h, post_tph, sizeof(h), cudaMemcpyDeviceToHost));
-            for (int i = 0; i < 5; ++i) post_ph_sum[i] += 1e-3 * (double)(h[i + 1] - h[i]);
+            const bool f = post_fuse;        // phase 0 (fused combine) stamped in h[6]
+            post_ph_sum[5] += f ? 1e-3 * (double)(h[6] - h[0]) : 0.0;
+            post_ph_sum[0] += 1e-3 * (double)(h[1] - (f ? h[6] : h[0]));
+            for (int i = 1; i < 5; ++i) post_ph_sum[i] += 1e-3 * (double)(h[i + 1] - h[i]);
         }
         if (++sp_n % 50 == 0) {
             fprintf(stderr, "[kmedoids] step phases over %d iterations (us): launch %.1f stream %.1f combine %.1f "
                     "post %.1f copies %.1f\n", sp_n, 1e3 * sp_sum[0] / sp_n, 1e3 * sp_sum[1] / sp_n,
                     1e3 * sp_sum[2] / sp_n, 1e3 * sp_sum[3] / sp_n, 1e3 * sp_sum[4] / sp_n);
             if (post_tph)
-                fprintf(stderr, "[kmedoids] post phases (us): select %.1f apply+rescan %.1f count+sync %.1f "
-                        "scan+sync %.1f scatter/parts %.1f\n", post_ph_sum[0] / sp_n, post_ph_sum[1] / sp_n,
+                fprintf(stderr, "[kmedoids] post phases (us): combine0+sync %.1f select %.1f apply+rescan %.1f "
+                        "count+sync %.1f scan+sync %.1f scatter/parts %.1f\n", post_ph_sum[5] / sp_n,
+                        post_ph_sum[0] / sp_n, post_ph_sum[1] / sp_n,
                         post_ph_sum[2] / sp_n, post_ph_sum[3] / sp_n, post_ph_sum[4] / sp_n);
         }
         return KM_OK;
