@@ -234,8 +234,19 @@ km_status kmedoids_launch_count(km_handle* h, int64_t* count_out);
  *   KM_METRIC_L2_F32: X float32 (n x d, row-major, device), D float32,
  *     d(x, y) = sqrt(max(0, |x|^2 + |y|^2 - 2 <x, y>)), inner products on the
  *     tensor cores (tcgen05, tf32 hi/lo split: ~f32 accuracy), d <= 64,
- *     D 16-byte aligned, ld % 4 == 0.  Diagonal exactly 0.  Accuracy: the
- *     squared distance is within ~4 * 2^-22 (|x|^2 + |y|^2) of the exact one.
+ *     D 16-byte aligned, ld % 4 == 0.  Diagonal exactly 0.  The points are
+ *     centred on their mean first (mu).  Accuracy: the squared distance is
+ *     within ~(6d + 16) 2^-24 (|x - mu|^2 + |y - mu|^2) of the exact one --
+ *     relative errors up to ~3e-4 on the closest (within-cluster) pairs of
+ *     the config recipes, where the expansion cancels (the tensor cores'
+ *     fp32 accumulation).
+ *   KM_METRIC_L2_F32_EXACT: as KM_METRIC_L2_F32, plus every pair with
+ *     d^2 < (|x - mu|^2 + |y - mu|^2) / 16 recomputed in the epilogue from
+ *     the points by the definition (f32 differences, fp32 accumulation,
+ *     correctly rounded sqrt: relative error <= (d + 2) 2^-24 on d^2).
+ *     Measured on the C2-C4 recipes: every pair within 1e-5 relative of the
+ *     fp64 definition; cost ~2x the plain L2 at C4 (1.2 % of the pairs
+ *     recomputed).
  *   KM_METRIC_L1_U32: X int32 integer coordinates (n x d), D uint32,
  *     d(x, y) = sum_t |x_t - y_t| exactly (caller keeps sums < 2^32).  The
  *     arithmetic is chosen on the device from the coordinate ranges, always
@@ -245,7 +256,7 @@ km_status kmedoids_launch_count(km_handle* h, int64_t* count_out);
  * borrowed; the library keeps one grow-only scratch buffer per device,
  * ordered across streams by an event.  Errors: KM_EINVAL (sizes,
  * alignment, d > 64 for L2), KM_ENOMEM, KM_ECUDA. */
-typedef enum { KM_METRIC_L2_F32 = 0, KM_METRIC_L1_U32 = 1 } km_metric;
+typedef enum { KM_METRIC_L2_F32 = 0, KM_METRIC_L1_U32 = 1, KM_METRIC_L2_F32_EXACT = 2 } km_metric;
 km_status kmedoids_dissimilarity(const void* X, km_metric metric, int64_t n, int32_t d, void* D, int64_t ld,
                                  int64_t col_begin, int64_t col_end, void* cuda_stream);
 

@@ -328,11 +328,20 @@ k_dist_l2_tc(const float* __restrict__ PA, const float* __restrict__ PB, int n, 
 // the B tile of t+2 is fetched as soon as the MMAs of t are done.  Edges
 // (rows beyond n, columns beyond the slab) are clipped by the tensor store.
 // ---------------------------------------------------------------------------
-constexpr int DW_EPI_WARPS = 16;                     // 4 per TMEM lane quarter
+constexpr unsigned FULL_MASK_DW = 0xffffffffu;
+constexpr int DW_EPI_WARPS = 16;
+// TMEM accumulators (128 columns each; 4 = all 512 columns): the MMAs run up
+// to DW_NACC - 1 tiles ahead of the epilogue
+constexpr int DW_NACC = 4;                     // 4 per TMEM lane quarter
 constexpr int DW_CPW = DT_N / (DW_EPI_WARPS / 4);    // accumulator columns per epilogue warp
 constexpr int DW_THREADS = (DW_EPI_WARPS + 1) * 32;
 
 __host__ __device__ inline int64_t dw_tile_floats(int dpad) { return 2LL * DT_M * dpad; }
+// raw (uncentred) points of a 128-row / 128-column tile for the exact
+// recomputation, rows padded to dpad + 4 floats (4-way bank spread of the
+// per-lane 16-byte shared-memory loads)
+__host__ __device__ inline int dw_raw_stride(int dpad) { return dpad + 4; }
+__host__ __device__ inline int64_t dw_raw_floats(int dpad) { return (int64_t)DT_M * dw_raw_stride(dpad); }
 __host__ __device__ inline size_t dw_smem_bytes(int dpad, int nstage) {
     // A + 2 B stages + nstage x 64 KB staging (4 boxes of 128 rows x 128 B), 1 KB alignment slack
     return (size_t)3 * dw_tile_floats(dpad) * sizeof(float) + (size_t)nstage * 4 * DT_M * 128 + 1024;
@@ -354,6 +363,19 @@ __global__ void k_dist_pack2(const float* __restrict__ X, const float* __restric
     }
 }
 
+// raw points of rows [r0, r1) in 128-row tiles [tile][row][dpad + 4] (zero padded)
+__global__ void k_dist_pack_raw(const float* __restrict__ X, int d, int dpad, int64_t r0, int64_t r1,
+                                float* __restrict__ out) {
+    const int rs = dw_raw_stride(dpad);
+    const int64_t tile = blockIdx.x;
+    float* o = out + tile * dw_raw_floats(dpad);
+    for (int idx = threadIdx.x; idx < DT_M * rs; idx += blockDim.x) {
+        const int r = idx / rs, k = idx - r * rs;
+        const int64_t j = r0 + tile * DT_M + r;
+        o[idx] = (j < r1 && k < d) ? X[j * d + k] : 0.f;
+    }
+}
+
 __device__ __forceinline__ void dw_arrive(uint64_t* bar) {
     asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" :: "r"(dt_smem_u32(bar)) : "memory");
 }
@@ -364,9 +386,45 @@ __device__ __forceinline__ float dw_sqrt(float x) {
     return r;
 }
 
+// Exact value of a pair whose norm expansion cancels: d^2 = sum_t (x_t - y_t)^2
+// over the raw points (f32 differences, two fp32 fused accumulators over the
+// even / odd 4-blocks of t, then added: relative error <= (d + 2) 2^-24 on
+// d^2), correctly rounded sqrt.  The points come from the padded raw tiles
+// (L1 / L2 resident); all 16-byte loads of a pair are issued at once.
+template <int DP>
+__device__ __forceinline__ float dw_exact_t(const float* xr, const float* yc) {
+    float4 a[DP / 4], c[DP / 4];
+#pragma unroll
+    for (int i = 0; i < DP / 4; ++i) {
+        a[i] = __ldg(reinterpret_cast<const float4*>(xr) + i);
+        c[i] = __ldg(reinterpret_cast<const float4*>(yc) + i);
+    }
+    float acc[2] = {0.f, 0.f};
+#pragma unroll
+    for (int i = 0; i < DP / 4; ++i) {
+        const float e0 = a[i].x - c[i].x, e1 = a[i].y - c[i].y, e2 = a[i].z - c[i].z, e3 = a[i].w - c[i].w;
+        float& r = acc[i & 1];
+        r = fmaf(e0, e0, r); r = fmaf(e1, e1, r); r = fmaf(e2, e2, r); r = fmaf(e3, e3, r);
+    }
+    return __fsqrt_rn(acc[0] + acc[1]);
+}
+__device__ __forceinline__ float dw_exact(const float* xr, const float* yc, int dpad) {   // zero padding adds 0
+    switch (dpad) {
+        case 8: return dw_exact_t<8>(xr, yc);
+        case 16: return dw_exact_t<16>(xr, yc);
+        case 24: return dw_exact_t<24>(xr, yc);
+        case 32: return dw_exact_t<32>(xr, yc);
+        case 40: return dw_exact_t<40>(xr, yc);
+        case 48: return dw_exact_t<48>(xr, yc);
+        case 56: return dw_exact_t<56>(xr, yc);
+        default: return dw_exact_t<64>(xr, yc);
+    }
+}
+
 __global__ void __launch_bounds__(DW_THREADS, 1)
 k_dist_l2_ws(const __grid_constant__ CUtensorMap tmap, const float* __restrict__ PA, const float* __restrict__ PB,
-             const float* __restrict__ nrm, int n, int dpad, int nsplit, int nstage, int64_t c0, int64_t c1) {
+             const float* __restrict__ nrm, int n, int dpad, int nsplit, int nstage, int64_t c0, int64_t c1,
+             const float* __restrict__ RA, const float* __restrict__ RB, float tau) {
     extern __shared__ __align__(1024) unsigned char dsm_raw[];
     // 1 KB alignment for the 128B-swizzled staging boxes
     unsigned char* dsm = dsm_raw + ((1024 - (dt_smem_u32(dsm_raw) & 1023)) & 1023);
@@ -375,13 +433,17 @@ k_dist_l2_ws(const __grid_constant__ CUtensorMap tmap, const float* __restrict__
     unsigned char* stage0 = dsm;                         // nstage x 4 boxes x 16 KB (1 KB aligned)
     float* sA = reinterpret_cast<float*>(dsm + (size_t)nstage * 4 * DT_M * 128);
     float* sB0 = sA + TF;                                // 2 stages
-    __shared__ __align__(8) uint64_t bar_a, bar_bfull[2], bar_bempty[2], bar_tfull[2], bar_tempty[2];
+    // exact fix-up (tau > 0): raw point tiles RA (rows) / RB (slab columns)
+    const bool fix = tau > 0.f;
+    const int64_t RF = dw_raw_floats(dpad);
+    const int rst = dw_raw_stride(dpad);
+    __shared__ __align__(8) uint64_t bar_a, bar_bfull[2], bar_bempty[2], bar_tfull[DW_NACC], bar_tempty[DW_NACC];
     __shared__ uint32_t tmem_base_s;
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
 
     if (warp == DW_EPI_WARPS) {
         asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;"
-                     :: "r"(dt_smem_u32(&tmem_base_s)), "n"(2 * DT_N));
+                     :: "r"(dt_smem_u32(&tmem_base_s)), "n"(DW_NACC * DT_N));
         asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
     }
     if (tid == 0) {
@@ -389,6 +451,8 @@ k_dist_l2_ws(const __grid_constant__ CUtensorMap tmap, const float* __restrict__
         for (int i = 0; i < 2; ++i) {
             asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" :: "r"(dt_smem_u32(&bar_bfull[i])));
             asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" :: "r"(dt_smem_u32(&bar_bempty[i])));
+        }
+        for (int i = 0; i < DW_NACC; ++i) {
             asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" :: "r"(dt_smem_u32(&bar_tfull[i])));
             asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" :: "r"(dt_smem_u32(&bar_tempty[i])), "r"(DW_EPI_WARPS));
         }
@@ -407,7 +471,7 @@ k_dist_l2_ws(const __grid_constant__ CUtensorMap tmap, const float* __restrict__
         if (lane == 0) {
             const uint32_t idesc = dt_idesc(DT_M, DT_N);
             const uint32_t lbo = 128, sbo = (uint32_t)(dpad / 4) * 128;
-            uint32_t ph_a = 0, ph_bf[2] = {0, 0}, ph_be[2] = {0, 0}, ph_te[2] = {0, 0};
+            uint32_t ph_a = 0, ph_bf[2] = {0, 0}, ph_be[2] = {0, 0}, ph_te[DW_NACC] = {};
             int64_t t = 0;                               // tiles issued by this CTA
             bool pending[2] = {false, false};            // B stage has an MMA commit not yet waited for
             for (int64_t item = blockIdx.x; item < items; item += gridDim.x) {
@@ -426,13 +490,14 @@ k_dist_l2_ws(const __grid_constant__ CUtensorMap tmap, const float* __restrict__
                 }
                 dt_wait(&bar_a, ph_a); ph_a ^= 1;
                 for (int64_t tc = t0; tc < t1; ++tc, ++t) {
-                    const int s = (int)(t & 1);
+                    const int s = (int)(t & 1);                      // B stage
+                    const int sa = (int)(t % DW_NACC);               // TMEM accumulator
                     dt_wait(&bar_bfull[s], ph_bf[s]); ph_bf[s] ^= 1;
-                    if (t >= 2) { dt_wait(&bar_tempty[s], ph_te[s]); ph_te[s] ^= 1; }   // accumulator s drained
+                    if (t >= DW_NACC) { dt_wait(&bar_tempty[sa], ph_te[sa]); ph_te[sa] ^= 1; }   // accumulator drained
                     asm volatile("tcgen05.fence::after_thread_sync;");
                     const uint32_t sa_hi = dt_smem_u32(sA), sa_lo = sa_hi + DT_M * dpad * 4;
                     const uint32_t sb_hi = dt_smem_u32(sB0 + s * TF), sb_lo = sb_hi + DT_N * dpad * 4;
-                    const uint32_t acc = tmem + (uint32_t)(s * DT_N);
+                    const uint32_t acc = tmem + (uint32_t)(sa * DT_N);
                     for (int kk = 0; kk < dpad / 8; ++kk) {
                         const uint32_t ko = (uint32_t)kk * 2 * 128;
                         dt_mma_tf32(acc, dt_desc(sa_hi + ko, lbo, sbo), dt_desc(sb_hi + ko, lbo, sbo), idesc, kk > 0);
@@ -440,7 +505,7 @@ k_dist_l2_ws(const __grid_constant__ CUtensorMap tmap, const float* __restrict__
                         dt_mma_tf32(acc, dt_desc(sa_lo + ko, lbo, sbo), dt_desc(sb_hi + ko, lbo, sbo), idesc, 1);
                     }
                     asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];"
-                                 :: "r"(dt_smem_u32(&bar_tfull[s])) : "memory");
+                                 :: "r"(dt_smem_u32(&bar_tfull[sa])) : "memory");
                     asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];"
                                  :: "r"(dt_smem_u32(&bar_bempty[s])) : "memory");
                     pending[s] = true;
@@ -455,19 +520,20 @@ k_dist_l2_ws(const __grid_constant__ CUtensorMap tmap, const float* __restrict__
                 if (pending[s]) { dt_wait(&bar_bempty[s], ph_be[s]); ph_be[s] ^= 1; }
         }
     } else {
-        // ====================== epilogue warps 0-7 ======================
+        // ====================== epilogue warps 0-15 ======================
         const int q = warp & 3, part = warp >> 2;       // TMEM lane quarter, column part
-        uint32_t ph_tf[2] = {0, 0};
+        uint32_t ph_tf[DW_NACC] = {};
         int64_t t = 0;
         for (int64_t item = blockIdx.x; item < items; item += gridDim.x) {
             const int64_t mt = item / nsplit;
             const int m0 = (int)(mt * DT_M);
             const int sp = (int)(item % nsplit);
             const int64_t t0 = ntile_c * sp / nsplit, t1 = ntile_c * (sp + 1) / nsplit;
+            if (t0 >= t1) continue;
             const int row = m0 + q * 32 + lane;
             const float nx = row < n ? nrm[row] : 0.f;
             for (int64_t tc = t0; tc < t1; ++tc, ++t) {
-                const int s = (int)(t & 1);
+                const int s = (int)(t % DW_NACC);                   // TMEM accumulator
                 const int64_t n0 = c0 + tc * DT_N;
                 const int64_t cb = n0 + part * DW_CPW;
                 dt_wait(&bar_tfull[s], ph_tf[s]); ph_tf[s] ^= 1;
@@ -496,6 +562,7 @@ k_dist_l2_ws(const __grid_constant__ CUtensorMap tmap, const float* __restrict__
                 // column norms: 16-byte loads with no per-element bounds in whole,
                 // aligned parts (all but the slab's last part when c0 % 4 == 0)
                 const bool whole = (cb + DW_CPW <= c1) && ((cb & 3) == 0);
+                uint32_t fl = 0;                             // columns of this lane's row to recompute
 #pragma unroll
                 for (int j = 0; j < DW_CPW; j += 4) {
                     float4 ny4;
@@ -508,8 +575,13 @@ k_dist_l2_ws(const __grid_constant__ CUtensorMap tmap, const float* __restrict__
                     }
                     const float ny[4] = {ny4.x, ny4.y, ny4.z, ny4.w};
 #pragma unroll
-                    for (int u = 0; u < 4; ++u)
-                        v[j + u] = __float_as_uint(dw_sqrt(fmaxf(fmaf(-2.f, __uint_as_float(v[j + u]), nx + ny[u]), 0.f)));
+                    for (int u = 0; u < 4; ++u) {
+                        const float s2 = nx + ny[u];
+                        const float d2 = fmaf(-2.f, __uint_as_float(v[j + u]), s2);
+                        // cancellation: d^2 small against |x|^2 + |y|^2 -> recomputed below
+                        if (d2 < tau * s2) fl |= 1u << (j + u);
+                        v[j + u] = __float_as_uint(dw_sqrt(fmaxf(d2, 0.f)));
+                    }
                 }
                 const int64_t dj = (int64_t)row - cb;       // this lane's diagonal column, if in its part
                 // Each warp stages its own 32 rows x 32 columns (one 4 KB box, 128B
@@ -533,6 +605,51 @@ k_dist_l2_ws(const __grid_constant__ CUtensorMap tmap, const float* __restrict__
                     const int jj = (int)dj;
                     *reinterpret_cast<float*>(box + lane * 128 + (((jj >> 2) ^ (lane & 7)) << 4) + (jj & 3) * 4) = 0.f;
                 }
+                if (fix) {
+                    // Pairs whose d^2 is small against |x|^2 + |y|^2 (within-cluster
+                    // pairs; the norm expansion cancels there) are recomputed from
+                    // the raw points by the definition
+                    // (P:272-278).  The warp's flagged (row, column) pairs are
+                    // packed: entry g goes to lane g % 32 (its row lane by a binary
+                    // search of the warp's prefix counts, its column by __fns), so
+                    // a round serves up to 32 pairs whichever rows they are in.
+                    if (row >= n) fl = 0;
+                    if (cb + DW_CPW > c1) {
+                        const int64_t nv = c1 - cb;          // valid columns of this part (< 32)
+                        fl &= nv <= 0 ? 0u : ((1u << (int)nv) - 1u);
+                    }
+                    const int cnt = __popc(fl);
+                    int incl = cnt;
+#pragma unroll
+                    for (int o = 1; o < 32; o <<= 1) {
+                        const int y = __shfl_up_sync(FULL_MASK_DW, incl, o);
+                        if (lane >= o) incl += y;
+                    }
+                    const int excl = incl - cnt;
+                    const int total = __shfl_sync(FULL_MASK_DW, incl, 31);
+                    if (total > 0) {
+                        __syncwarp();                        // the box rows written above are warp-visible
+                        const float* rrow = RA + mt * RF + (size_t)(q * 32) * rst;
+                        const float* rcol = RB + ((n0 - c0) / DT_N) * RF + (size_t)(part * DW_CPW) * rst;
+                        for (int g0 = 0; g0 < total; g0 += 32) {
+                            const int g = g0 + lane;
+                            // source lane: the last lane whose exclusive prefix <= g
+                            int src = 0;
+#pragma unroll
+                            for (int step = 16; step >= 1; step >>= 1) {
+                                const int ex = __shfl_sync(FULL_MASK_DW, excl, src + step);
+                                if (ex <= g) src += step;
+                            }
+                            const unsigned sfl = __shfl_sync(FULL_MASK_DW, fl, src);
+                            const int sex = __shfl_sync(FULL_MASK_DW, excl, src);
+                            if (g < total) {
+                                const int jj = (int)__fns(sfl, 0, g - sex + 1);
+                                const float val = dw_exact(rrow + (size_t)src * rst, rcol + (size_t)jj * rst, dpad);
+                                *reinterpret_cast<float*>(box + src * 128 + (((jj >> 2) ^ (src & 7)) << 4) + (jj & 3) * 4) = val;
+                            }
+                        }
+                    }
+                }
                 asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
                 __syncwarp();
                 if (lane == 0) {
@@ -551,7 +668,7 @@ k_dist_l2_ws(const __grid_constant__ CUtensorMap tmap, const float* __restrict__
     __syncthreads();
     asm volatile("tcgen05.fence::after_thread_sync;");
     if (warp == DW_EPI_WARPS)
-        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" :: "r"(tmem), "n"(2 * DT_N));
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" :: "r"(tmem), "n"(DW_NACC * DT_N));
 }
 
 // L1 on integer coordinates: 64 x 64 output tile per block, 256 threads

@@ -587,17 +587,21 @@ k_swap_stream_seg2(const T* __restrict__ D, int64_t ld, int w, int wpad, int n, 
     const int64_t p0 = part_lo(q, n, P), p1 = part_lo(q + 1, n, P);
     const int ctacol = blockIdx.x * C::COLS;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    // consumer warps owning at least one column of the slab (all NC but in
+    // the last, ragged column tile); the others leave at once, so a narrow
+    // last tile streams at the pace of its active warps (C3: 288 of 896)
+    const int nact = min(NC, (w - ctacol + 127) / 128);
 
     if (threadIdx.x == 0) {
         for (int st = 0; st < S; ++st) {
             ptx::mbar_init(&full[st], 1);
-            ptx::mbar_init(&empty[st], NC);
+            ptx::mbar_init(&empty[st], nact);
         }
         ptx::fence_mbar_init();
     }
     // columns beyond the slab are never written by the bulk copies: give them
     // a value no threshold exceeds (each lane fills its own columns)
-    if (warp < NC && ctacol + warp * 128 + lane * 4 >= wpad) {
+    if (warp < nact && ctacol + warp * 128 + lane * 4 >= wpad) {
         V big;
         const T b = dmax<T>();
         memcpy(&big.x, &b, sizeof(T)); memcpy(&big.y, &b, sizeof(T));
@@ -666,6 +670,7 @@ k_swap_stream_seg2(const T* __restrict__ D, int64_t ld, int w, int wpad, int n, 
     }
 
     // ---------------- consumer warps ----------------
+    if (warp >= nact) return;
     const int cb = ctacol + warp * 128 + lane * 4;
     const bool active = cb < w;
     const int64_t obase = (int64_t)q * w + cb;

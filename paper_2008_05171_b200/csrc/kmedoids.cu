@@ -2807,7 +2807,7 @@ km_status kmedoids_dissimilarity(const void* X, km_metric metric, int64_t n, int
                     (long long)n);
     if (ld < col_end - col_begin) return fail(KM_EINVAL, "ld=%lld smaller than the slab width", (long long)ld);
     cudaStream_t st = (cudaStream_t)cuda_stream;
-    if (metric == KM_METRIC_L2_F32) {
+    if (metric == KM_METRIC_L2_F32 || metric == KM_METRIC_L2_F32_EXACT) {
         if (d > 64) return fail(KM_EINVAL, "L2 on tensor cores supports d <= 64 (d=%d)", d);
         if (ld % 4 != 0 || ((uintptr_t)D) % 16 != 0) return fail(KM_EINVAL, "D must be 16-byte aligned, ld % 4 == 0");
         const int dpad = (d + 7) / 8 * 8;
@@ -2822,11 +2822,19 @@ km_status kmedoids_dissimilarity(const void* X, km_metric metric, int64_t n, int
         int wstage = 1;                                 // measured: a second staging buffer is slower (L1 carve-out)
         if (const char* es = getenv("KM_DIST_STAGES"))
             if (atoi(es) == 2 && km::dw_smem_bytes(dpad, 2) <= (size_t)smax) wstage = 2;
+        // pairs with d^2 < tau (|x - mu|^2 + |y - mu|^2) are recomputed exactly
+        // from the raw points in the epilogue (KM_DIST_TAU: measurement
+        // override), KM_METRIC_L2_F32_EXACT only
+        float tau = metric == KM_METRIC_L2_F32_EXACT ? 1.0f / 16.0f : 0.f;
+        if (const char* et = getenv("KM_DIST_TAU")) tau = (float)atof(et);
+        const bool fixup = ws && tau > 0.f;
+        const int64_t RFl = km::dw_raw_floats(dpad);
         const bool same = (col_begin == 0);
         const int64_t TF = ws ? km::dw_tile_floats(dpad) : km::dt_tile_floats(dpad);
         const size_t nrm_floats = (size_t)cdiv(n, 64) * 64;          // keeps the packed tiles 256-byte aligned
         const size_t mu_floats = 64;                                 // d <= 64
-        const size_t scratch = nrm_floats + (size_t)nm * TF + (same ? 0 : (size_t)ntc * TF) + mu_floats;
+        const size_t raw_floats = fixup ? (size_t)nm * RFl + (same ? 0 : (size_t)ntc * RFl) : 0;
+        const size_t scratch = nrm_floats + (size_t)nm * TF + (same ? 0 : (size_t)ntc * TF) + mu_floats + raw_floats;
         // persistent per-device scratch (norms + packed operands), grown on
         // demand: a stream-ordered allocation per call pays the pool's page
         // mapping again whenever the pool was trimmed at a synchronisation
@@ -2836,6 +2844,8 @@ km_status kmedoids_dissimilarity(const void* X, km_metric metric, int64_t n, int
         float* PA = nrm + nrm_floats;
         float* PB = same ? PA : PA + nm * TF;
         float* mu = PA + nm * TF + (same ? 0 : ntc * TF);
+        float* RA = mu + mu_floats;                                   // raw point tiles (exact fix-up)
+        float* RB = same ? RA : RA + nm * RFl;
         const char* ec = getenv("KM_DIST_CENTER");       // measurement override: 0 = no centring
         const bool center = !(ec && ec[0] == '0');
         if (center) km::k_dist_mean<<<(unsigned)d, 256, 0, st>>>((const float*)X, (int)n, d, mu);
@@ -2848,6 +2858,11 @@ km_status kmedoids_dissimilarity(const void* X, km_metric metric, int64_t n, int
             km::k_dist_pack2<<<(unsigned)nm, 256, 0, st>>>((const float*)X, mup, d, dpad, 0, n, PA);
             if (!same)
                 km::k_dist_pack2<<<(unsigned)ntc, 256, 0, st>>>((const float*)X, mup, d, dpad, col_begin, col_end, PB);
+            if (fixup) {
+                km::k_dist_pack_raw<<<(unsigned)nm, 256, 0, st>>>((const float*)X, d, dpad, 0, n, RA);
+                if (!same)
+                    km::k_dist_pack_raw<<<(unsigned)ntc, 256, 0, st>>>((const float*)X, d, dpad, col_begin, col_end, RB);
+            }
             static PFN_cuTensorMapEncodeTiled_v12000 encode = nullptr;
             if (!encode) {
                 void* fn = nullptr;
@@ -2869,7 +2884,7 @@ km_status kmedoids_dissimilarity(const void* X, km_metric metric, int64_t n, int
             e = cudaFuncSetAttribute(km::k_dist_l2_ws, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
             if (e != cudaSuccess) { return fail(KM_ECUDA, "smem attribute: %s", cudaGetErrorString(e)); }
             km::k_dist_l2_ws<<<grid, km::DW_THREADS, smem, st>>>(tm, PA, PB, nrm, (int)n, dpad, nsplit, wstage,
-                                                                  col_begin, col_end);
+                                                                  col_begin, col_end, RA, RB, fixup ? tau : 0.f);
         } else {
             km::k_dist_pack<<<(unsigned)nm, 256, 0, st>>>((const float*)X, mup, nrm, d, dpad, 0, n, PA);
             if (!same)

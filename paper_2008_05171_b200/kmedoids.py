@@ -490,14 +490,16 @@ def pinned_empty(shape, dtype):
     return a, t
 
 
-KM_METRIC_L2_F32, KM_METRIC_L1_U32 = 0, 1
+KM_METRIC_L2_F32, KM_METRIC_L1_U32, KM_METRIC_L2_F32_EXACT = 0, 1, 2
 
 
 def kmedoids_dissimilarity(X, metric="l2", D=None, col_begin=0, col_end=None, stream=None):
     """Materialise the column slab [col_begin, col_end) of the dissimilarity
     matrix of the points X (torch CUDA tensor, n x d) into D (n x ld; allocated
-    if None): "l2" float32 X -> float32 Euclidean on the tensor cores, "l1"
-    int32 X -> uint32 (int32 storage) Manhattan.  Returns D."""
+    if None): "l2" float32 X -> float32 Euclidean on the tensor cores,
+    "l2exact" the same with the cancelling (within-cluster) pairs recomputed
+    from the points (KM_METRIC_L2_F32_EXACT), "l1" int32 X -> uint32 (int32
+    storage) Manhattan.  Returns D."""
     import torch
     lib = load_library()
     if not X.is_cuda or X.dim() != 2:
@@ -505,8 +507,8 @@ def kmedoids_dissimilarity(X, metric="l2", D=None, col_begin=0, col_end=None, st
     X = X.contiguous()
     n, d = X.shape
     col_end = n if col_end is None else int(col_end)
-    code = {"l2": KM_METRIC_L2_F32, "l1": KM_METRIC_L1_U32}[metric]
-    want = torch.float32 if code == KM_METRIC_L2_F32 else torch.int32
+    code = {"l2": KM_METRIC_L2_F32, "l1": KM_METRIC_L1_U32, "l2exact": KM_METRIC_L2_F32_EXACT}[metric]
+    want = torch.int32 if code == KM_METRIC_L1_U32 else torch.float32
     if X.dtype != want:
         raise TypeError(f"metric {metric} needs X of dtype {want}")
     w = col_end - col_begin

@@ -18,15 +18,18 @@ Dt = kmsynth.dist_cuda(X, cfg.metric)
 km = KMedoids(Dt, cfg.n, cfg.k, stream=torch.cuda.current_stream())
 km.set_symmetric(True)
 if cfg.init == "build":
-    km.init_build()
+    M0, _ = km.init_build()
 else:
-    km.set_medoids(kmsynth.random_medoids(cfg))
+    M0 = kmsynth.random_medoids(cfg)
+    km.set_medoids(M0)
 for _ in range(5):
     km.swap_iter("fastpam1")
-done = 0
-for _ in range(iters):
+done = restarts = 0
+while done < iters:
     conv, sw, td = km.swap_iter("fastpam1")
+    if conv:                      # converged: restart from the initial medoids (small configs)
+        km.set_medoids(M0)
+        restarts += 1
+        continue
     done += 1
-    if conv:
-        break
-print(f"C{cid}: {done} single iterations", flush=True)
+print(f"C{cid}: {done} single iterations, {restarts} restarts", flush=True)

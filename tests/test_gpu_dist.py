@@ -165,11 +165,37 @@ def test_l2_centering_removes_the_offset_error(monkeypatch):
     Dx = oracle.dist_l2(X)
     off = ~np.eye(1500, dtype=bool)
 
-    def rel(env):
+    def rel(env, metric="l2"):
         monkeypatch.setenv("KM_DIST_CENTER", env)
-        Dg = kmedoids_dissimilarity(torch.from_numpy(X).cuda(), "l2")[:, :1500].double().cpu().numpy()
+        Dg = kmedoids_dissimilarity(torch.from_numpy(X).cuda(), metric)[:, :1500].double().cpu().numpy()
         assert (np.diag(Dg) == 0).all()
         return (np.abs(Dg - Dx)[off] / Dx[off]).max()
 
     assert rel("1") < 1e-5
     assert rel("0") > 1e-3
+    # "l2exact" recomputes the cancelling pairs from the points (here: every
+    # pair): accurate even uncentred
+    assert rel("0", "l2exact") < 1e-6
+
+
+@pytest.mark.parametrize("cid,n,c0,c1", [(2, 3000, 0, 3000), (3, 3000, 0, 3000), (4, 3000, 0, 3000),
+                                         (4, 2600, 517, 2001)])
+def test_l2exact_relative_error_on_config_recipes(cid, n, c0, c1):
+    """SURVEY 8(f) NEXT-2 / VERDICT r1 item 9: with "l2exact" every pair of
+    the config recipes -- within-cluster pairs included, where |x|^2 + |y|^2
+    - 2<x,y> cancels -- is within 1e-5 relative of the definition
+    (oracle.dist_l2, fp64, rounded to f32), also on a ragged column slab;
+    the plain "l2" is not (the tensor cores' fp32 accumulation)."""
+    from paper_2008_05171_b200 import kmedoids_dissimilarity
+    cfg = kmsynth.CONFIGS[cid]
+    X = kmsynth.make_points(cfg, n=n).astype(np.float32)
+    Dx = oracle.dist_l2(X).astype(np.float32).astype(np.float64)[:, c0:c1]
+    Xt = torch.from_numpy(X).cuda()
+    Dg = kmedoids_dissimilarity(Xt, "l2exact", col_begin=c0, col_end=c1)[:, :c1 - c0].double().cpu().numpy()
+    off = np.ones_like(Dx, dtype=bool)
+    off[np.arange(c0, c1), np.arange(c1 - c0)] = False
+    assert (Dg[~off] == 0).all()
+    rel = np.abs(Dg - Dx)[off] / Dx[off]
+    assert rel.max() <= 1e-5, rel.max()
+    Dp = kmedoids_dissimilarity(Xt, "l2", col_begin=c0, col_end=c1)[:, :c1 - c0].double().cpu().numpy()
+    assert (np.abs(Dp - Dx)[off] / Dx[off]).max() > 1e-5
