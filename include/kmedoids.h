@@ -398,6 +398,34 @@ km_status kmedoids_fp2_shard_eval(km_handle* h);
 km_status kmedoids_fp2_shard_plan(km_handle* h, const int64_t* rank_col_begin, int32_t* m_out, int32_t* maxcnt_out);
 km_status kmedoids_fp2_shard_apply(km_handle* h, int32_t* swaps_done_out, void* td_out);
 
+/* Sharded FastPAM2, owner-side form of step 4 (reading R6 unchanged;
+ * parallel.fp2_iter(mode="owner")).  After step 3 returned m > 0 (no column
+ * all-gather), repeat on every rank until *more_out == 0:
+ *   a. kmedoids_fp2_round_eval(h)   this rank re-evaluates, on the current
+ *      state, its own unskipped plan entries from the round's first position
+ *      in plan order (later swaps are re-checked) and publishes
+ *      its first improving one -- plan position, dTD, slot, candidate and the
+ *      candidate's n-element column -- into its round buffer (32-byte header
+ *      {int32 pos (INT32_MAX = none), int32 pad, dTD (int64/double), int32
+ *      slot, int32 c, 8 pad bytes}, then the column); round 0 publishes plan
+ *      entry 0 as is (it is FastPAM1's swap);
+ *   b. all-gather the round buffers: stride bytes per rank, rank order
+ *      (caller; send -> recv of kmedoids_fp2_round_buffers);
+ *   c. kmedoids_fp2_round_apply(h, &more, &swaps, td)  applies the published
+ *      entry with the smallest plan position (identical on every rank); when
+ *      none is published the iteration is over: *more_out = 0, *swaps_done_out
+ *      = swaps of the iteration, *td_out (int64_t* / double*) = TD.
+ * Same trace, medoids and TD as kmedoids_fp2_shard_apply and as one GPU
+ * (same per-entry arithmetic and summation tree); one column per applied
+ * swap crosses the interconnect instead of every planned candidate's.
+ * Buffers are device memory owned by the handle (valid until destroy).
+ * Errors: KM_ECOMM before kmedoids_fp2_shard_exchange, KM_EINVAL without a
+ * plan / with an empty plan (converged: use kmedoids_fp2_shard_apply),
+ * KM_ECUDA. */
+km_status kmedoids_fp2_round_buffers(km_handle* h, void** send_out, void** recv_out, size_t* stride_out);
+km_status kmedoids_fp2_round_eval(km_handle* h);
+km_status kmedoids_fp2_round_apply(km_handle* h, int32_t* more_out, int32_t* swaps_done_out, void* td_out);
+
 /* Sharded BUILD: step 0 evaluates the distance sums (first medoid), steps
  * 1..k-1 the BUILD gains of the local candidates into record_send; after the
  * gather, kmedoids_build_select picks the global (value, c) minimum, the

@@ -26,6 +26,7 @@
 #include "km_init.cuh"
 #include "km_build_delta.cuh"
 #include "km_clara.cuh"
+#include "km_fp2_owner.cuh"
 
 namespace {
 
@@ -129,6 +130,9 @@ struct ImplBase {
     virtual km_status fp2_shard_eval() = 0;
     virtual km_status fp2_shard_plan(const int64_t* rcb, int32_t* m_out, int32_t* maxcnt_out) = 0;
     virtual km_status fp2_shard_apply(int32_t* swaps_out, void* td_out) = 0;
+    virtual km_status fp2_round_buffers(void** send, void** recv, size_t* stride) = 0;
+    virtual km_status fp2_round_eval() = 0;
+    virtual km_status fp2_round_apply(int32_t* more_out, int32_t* swaps_out, void* td_out) = 0;
     virtual km_status init_weighted(const double* u, int32_t* M_out, void* td_out) = 0;
     virtual km_status init_lab(int32_t s, const int32_t* seq, int32_t* M_out, void* td_out) = 0;
     virtual km_status clara(int32_t ns, int32_t s, const int32_t* samples, km_variant v, int32_t* M_out,
@@ -1539,13 +1543,107 @@ struct Impl : ImplBase {
             KM_CKL();
         }
         KM_CK(cudaStreamSynchronize(st));
+        f2_me = me;
+        f2_round = 0;                                // owner-side rounds may follow (km_fp2_owner.cuh)
         if (m_out) *m_out = (int)f2_order.size();
         if (maxcnt_out) *maxcnt_out = maxcnt;
         return KM_OK;
     }
 
     km_status fp2_shard_apply(int32_t* swaps_out, void* td_out) override {
+        f2_round = -1;
         return fp2_sequential(f2_order, f2_col_recv, f2_colidx, swaps_out, td_out);
+    }
+
+    // ---- sharded FastPAM2, owner-side rounds (km_fp2_owner.cuh) ---------------
+    unsigned char* f2_rsend = nullptr;    // this rank's round buffer (header + column)
+    unsigned char* f2_rrecv = nullptr;    // R round buffers, rank order
+    size_t f2_rstride = 0;
+    int* f2_state = nullptr;              // [2]: next plan position, another round needed
+    int f2_round = -1;                    // rounds done in this iteration (-1: no plan)
+    int f2_me = -1;
+    Dec f2_hd{};                          // the iteration's decision bookkeeping (host)
+    int f2_swaps0 = 0;
+
+    km_status fp2_round_buffers(void** send, void** recv, size_t* stride) override {
+        if (!f2_ranks) return fail(KM_ECOMM, "call kmedoids_fp2_shard_exchange first");
+        if (!f2_rsend) {
+            f2_rstride = km::fp2_round_stride<T>(n);
+            KM_TRY(alloc(&f2_rsend, f2_rstride));
+            KM_TRY(alloc(&f2_rrecv, f2_rstride * (size_t)f2_ranks));
+            KM_TRY(alloc(&f2_state, 2));
+        }
+        if (send) *send = f2_rsend;
+        if (recv) *recv = f2_rrecv;
+        if (stride) *stride = f2_rstride;
+        return KM_OK;
+    }
+
+    km_status fp2_round_eval() override {
+        if (f2_round < 0) return fail(KM_EINVAL, "no FastPAM2 plan: call kmedoids_fp2_shard_plan first");
+        if (f2_order.empty()) return fail(KM_EINVAL, "empty plan (converged): use kmedoids_fp2_shard_apply");
+        KM_TRY(fp2_round_buffers(nullptr, nullptr, nullptr));
+        if (f2_round == 0) {
+            // the iteration's bookkeeping, as fp2_sequential: counted now, its
+            // swaps counted from 0 by the apply kernels
+            KM_CK(cudaMemcpyAsync(h_dec, dec, sizeof(Dec), cudaMemcpyDeviceToHost, st));
+            KM_CK(cudaStreamSynchronize(st));
+            f2_hd = *h_dec;
+            f2_hd.iters += 1;
+            f2_hd.apply = 0;
+            f2_swaps0 = f2_hd.swaps;
+            f2_hd.swaps = 0;
+            KM_CK(cudaMemcpyAsync(dec, &f2_hd, sizeof(Dec), cudaMemcpyHostToDevice, st));
+            KM_CK(cudaMemcpyAsync(fp2_order, f2_order.data(), f2_order.size() * sizeof(int), cudaMemcpyHostToDevice, st));
+            const int m = (int)f2_order.size();
+            const int init[2] = {0, 1};
+            KM_CK(cudaMemcpyAsync(fp2_m, &m, sizeof(int), cudaMemcpyHostToDevice, st));
+            KM_CK(cudaMemcpyAsync(f2_state, init, sizeof(init), cudaMemcpyHostToDevice, st));
+            last_swaps.clear();
+        }
+        const T* csp = f2_col_send; const int* cip = f2_colidx; int me = f2_me; int mc = std::max(1, f2_maxcnt);
+        int nn = (int)n; const int* op = fp2_order; const int* mp = fp2_m; const Rec* bp = fp2_best;
+        const int* psp = point_slot; const int* nr = near; const T* dnp = dn; const T* dsp = ds; const A* tdp = td;
+        A* pp = fp2_partials; const int* rp = f2_state; int* rcp = rescan_count; unsigned char* outp = f2_rsend;
+        void* args[] = {&csp, &cip, &me, &mc, &nn, &op, &mp, &bp, &psp, &nr, &dnp, &dsp, &tdp, &pp, &rp, &rcp, &outp};
+        KM_CK(cudaLaunchCooperativeKernel((void*)km::k_fp2_owned_eval<T, A>, dim3(fp2_blocks), dim3(256), args, 0, st));
+        ++launches;
+        return KM_OK;
+    }
+
+    km_status fp2_round_apply(int32_t* more_out, int32_t* swaps_out, void* td_out) override {
+        if (f2_round < 0 || !f2_rsend) return fail(KM_EINVAL, "no FastPAM2 round: call kmedoids_fp2_round_eval first");
+        const unsigned char* rv = f2_rrecv; int nrk = f2_ranks; size_t strd = f2_rstride; int nn = (int)n; int kk = k;
+        const int* mp = fp2_m; int* Mp = M; int* psp = point_slot; T* MCp = MC; int* nr = near; int* sc = sec;
+        T* dnp = dn; T* dsp = ds; A* tdp = td; Dec* dp = dec; Rec* tr = trace; int tc = trace_cap; int* rsp = rescan;
+        int* rcp = rescan_count; int* stp = f2_state;
+        void* args[] = {&rv, &nrk, &strd, &nn, &kk, &mp, &Mp, &psp, &MCp, &nr, &sc, &dnp, &dsp, &tdp, &dp, &tr, &tc,
+                        &rsp, &rcp, &stp};
+        KM_CK(cudaLaunchCooperativeKernel((void*)km::k_fp2_round_apply<T, A>, dim3(fp2_blocks), dim3(256), args, 0,
+                                          st));
+        ++launches;
+        int hs[2];
+        KM_CK(cudaMemcpyAsync(hs, f2_state, sizeof(hs), cudaMemcpyDeviceToHost, st));
+        KM_CK(cudaStreamSynchronize(st));
+        ++f2_round;
+        if (more_out) *more_out = hs[1];
+        if (hs[1]) return KM_OK;
+        // the iteration is over: its swaps (the kernels counted them from 0)
+        KM_CK(cudaMemcpyAsync(h_dec, dec, sizeof(Dec), cudaMemcpyDeviceToHost, st));
+        KM_CK(cudaStreamSynchronize(st));
+        const int done = h_dec->swaps;
+        last_swaps.resize(std::min(done, trace_cap));
+        if (!last_swaps.empty())
+            KM_CK(cudaMemcpy(last_swaps.data(), trace, last_swaps.size() * sizeof(Rec), cudaMemcpyDeviceToHost));
+        Dec hd = *h_dec;
+        hd.swaps = f2_swaps0 + done;
+        KM_CK(cudaMemcpyAsync(dec, &hd, sizeof(Dec), cudaMemcpyHostToDevice, st));
+        KM_CK(cudaStreamSynchronize(st));
+        *h_dec = hd;
+        f2_round = -1;
+        if (swaps_out) *swaps_out = done;
+        copy_td(td_out);
+        return KM_OK;
     }
 
     // ---- NEXT-4 initialisations (km_init.cuh) ----------------------------------
@@ -3056,6 +3154,21 @@ km_status kmedoids_fp2_shard_plan(km_handle* h, const int64_t* rank_col_begin, i
 km_status kmedoids_fp2_shard_apply(km_handle* h, int32_t* swaps_done_out, void* td_out) {
     KM_H();
     return h->impl->fp2_shard_apply(swaps_done_out, td_out);
+}
+
+km_status kmedoids_fp2_round_buffers(km_handle* h, void** send_out, void** recv_out, size_t* stride_out) {
+    KM_H();
+    return h->impl->fp2_round_buffers(send_out, recv_out, stride_out);
+}
+
+km_status kmedoids_fp2_round_eval(km_handle* h) {
+    KM_H();
+    return h->impl->fp2_round_eval();
+}
+
+km_status kmedoids_fp2_round_apply(km_handle* h, int32_t* more_out, int32_t* swaps_done_out, void* td_out) {
+    KM_H();
+    return h->impl->fp2_round_apply(more_out, swaps_done_out, td_out);
 }
 
 km_status kmedoids_build_eval(km_handle* h, int32_t step) {

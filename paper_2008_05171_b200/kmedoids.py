@@ -99,6 +99,9 @@ def load_library() -> ctypes.CDLL:
         "kmedoids_fp2_shard_eval": [vp],
         "kmedoids_fp2_shard_plan": [vp, vp, vp, vp],
         "kmedoids_fp2_shard_apply": [vp, vp, vp],
+        "kmedoids_fp2_round_buffers": [vp, vp, vp, vp],
+        "kmedoids_fp2_round_eval": [vp],
+        "kmedoids_fp2_round_apply": [vp, vp, vp, vp],
         "kmedoids_build_eval": [vp, i32],
         "kmedoids_build_select": [vp, vp, vp, vp, vp],
         "kmedoids_build_apply": [vp, i32],
@@ -404,6 +407,21 @@ class KMedoids:
         sw = np.zeros(1, np.int32); td = np.zeros(1, self.acc)
         s = _check(load_library().kmedoids_fp2_shard_apply(self.h, _p(sw), _p(td)), ok=(KM_OK, KM_CONVERGED))
         return s == KM_CONVERGED, int(sw[0]), td[0].item()
+
+    def fp2_round_buffers(self):
+        """(send pointer, recv pointer, stride bytes) of the owner-side round buffers."""
+        sp, rp, st = ctypes.c_void_p(), ctypes.c_void_p(), ctypes.c_size_t()
+        _check(load_library().kmedoids_fp2_round_buffers(self.h, ctypes.byref(sp), ctypes.byref(rp), ctypes.byref(st)))
+        return int(sp.value), int(rp.value), int(st.value)
+
+    def fp2_round_eval(self):
+        _check(load_library().kmedoids_fp2_round_eval(self.h))
+
+    def fp2_round_apply(self):
+        """-> (more rounds, swaps of the iteration, TD) (the last two once more is False)."""
+        mo = np.zeros(1, np.int32); sw = np.zeros(1, np.int32); td = np.zeros(1, self.acc)
+        _check(load_library().kmedoids_fp2_round_apply(self.h, _p(mo), _p(sw), _p(td)))
+        return bool(mo[0]), int(sw[0]), td[0].item()
 
     def build_eval(self, step: int):
         _check(load_library().kmedoids_build_eval(self.h, int(step)))

@@ -145,6 +145,13 @@ class LocalComm:
             for r, y in enumerate(xs):
                 x[3][r * cb:(r + 1) * cb].copy_(y[2][:cb])
 
+    @_streamed
+    def allgather_fp2_round(self, handles):
+        xs = [h.fp2_round_tensors(self.world) for h in handles]
+        for x in xs:
+            for r, y in enumerate(xs):
+                x[1][r * y[2]:(r + 1) * y[2]].copy_(y[0])
+
     def max_over_ranks(self, x: float) -> float:
         return x
 
@@ -189,6 +196,12 @@ class TorchComm:
         _, _, csend, crecv, colb = h.fp2_exchange_tensors(self.world)
         cb = colb * maxcnt
         self.dist.all_gather_into_tensor(crecv[:cb * self.world], csend[:cb], group=self.group)
+
+    @_streamed
+    def allgather_fp2_round(self, handles):
+        (h,) = handles
+        send, recv, _ = h.fp2_round_tensors(self.world)
+        self.dist.all_gather_into_tensor(recv, send, group=self.group)
 
     def allgather_object(self, obj):
         out = [None] * self.world
@@ -287,13 +300,36 @@ def build_async(handles, comm, cb, k: int):
     return Ms[0]
 
 
-def fp2_iter(handles, comm, cb):
+FP2_MODES = ("gather", "owner")
+
+
+def fp2_iter(handles, comm, cb, mode: str = "gather"):
     """One sharded FastPAM2 iteration (reading R6); returns (converged, swaps).
 
     per-slot bests of the local candidates -> all-gather (k*16 B per rank) ->
-    identical plan on every rank -> all-gather of the planned candidates'
-    columns (each rank sends the ones it owns) -> every rank runs the
-    sequential phase redundantly on the gathered columns."""
+    identical plan on every rank, then the sequential phase:
+
+    * ``owner``: rounds of owner-side re-evaluation
+      (kmedoids_fp2_round_eval: each rank re-checks its own plan entries on
+      the current state and publishes its first improving one with its
+      column) -> all-gather of the round buffers -> every rank applies the
+      published entry with the smallest plan position
+      (kmedoids_fp2_round_apply).  Rounds = applied swaps + 1; one column
+      per applied swap crosses the interconnect.
+    * ``gather`` (default): all-gather of the columns of the planned
+      candidates (distinct candidates only; each rank sends the ones it
+      owns), then every rank runs the whole sequential phase redundantly on
+      the gathered columns.
+
+    Both give the single-GPU trace.  Measured on virtual ranks (C5 / C3,
+    G = 8): the planned slots share few distinct
+    candidates (2-3 columns per rank), so ``gather`` moves 6-10 MB per rank
+    in one collective while ``owner`` needs swaps + 1 collectives and host
+    round trips per iteration -- ``gather`` is the default; ``owner`` moves
+    one column per applied swap, the better choice when the plan names many
+    distinct candidates."""
+    if mode not in FP2_MODES:
+        raise ValueError(f"mode must be one of {FP2_MODES}")
     for h in handles:
         h.fp2_exchange_tensors(comm.world)      # sizes the exchange buffers once
         h.fp2_shard_eval()
@@ -302,6 +338,17 @@ def fp2_iter(handles, comm, cb):
     m, maxcnt = plans[0]
     if any(p != plans[0] for p in plans):
         raise RuntimeError(f"ranks disagree on the FastPAM2 plan: {plans}")
+    if m > 0 and mode == "owner":
+        while True:
+            for h in handles:
+                h.fp2_round_eval()
+            comm.allgather_fp2_round(handles)
+            res = [h.fp2_round_apply() for h in handles]
+            if any(r != res[0] for r in res):
+                raise RuntimeError(f"ranks disagree on a FastPAM2 round: {res}")
+            more, swaps, _ = res[0]
+            if not more:
+                return False, swaps
     if m > 0:
         for h in handles:                       # the column buffers grow on demand (kmedoids.h)
             h.fp2_exchange_tensors(comm.world, need=maxcnt)
@@ -410,6 +457,17 @@ class CudaShard:
                         torch.as_tensor(_DevBytes(x.col_recv, cap * world), device=dev),
                         int(x.col_bytes_per_column))
         return self._f2
+
+    def fp2_round_tensors(self, world: int):
+        """(round send, round recv, stride) of the owner-side FastPAM2 rounds
+        as uint8 tensors (kmedoids_fp2_round_buffers)."""
+        import torch
+        if getattr(self, "_f2r", None) is None:
+            sp, rp, stride = self.km.fp2_round_buffers()
+            dev = self.km.D.device
+            self._f2r = (torch.as_tensor(_DevBytes(sp, stride), device=dev),
+                         torch.as_tensor(_DevBytes(rp, stride * world), device=dev), stride)
+        return self._f2r
 
     @property
     def column_dtype(self) -> str:

@@ -89,8 +89,10 @@ def test_sharded_random_init_set_medoids():
     assert st.assignment.tolist() == ref.assignment.tolist()
 
 
-@pytest.mark.parametrize("world,cid,n,k", [(2, 5, 900, 11), (3, 5, 1300, 17), (4, 3, 800, 9), (2, 5, 1600, 90)])
-def test_sharded_fastpam2_equals_single_gpu(world, cid, n, k):
+@pytest.mark.parametrize("mode", ["owner", "gather"])
+@pytest.mark.parametrize("world,cid,n,k", [(2, 5, 900, 11), (3, 5, 1300, 17), (4, 3, 800, 9), (2, 5, 1600, 90),
+                                          (8, 3, 2000, 40)])
+def test_sharded_fastpam2_equals_single_gpu(world, cid, n, k, mode):
     from paper_2008_05171_b200 import KMedoids, parallel
     cfg = kmsynth.CONFIGS[cid]
     X = kmsynth.make_points(cfg, n=n)
@@ -110,7 +112,7 @@ def test_sharded_fastpam2_equals_single_gpu(world, cid, n, k):
     parallel.set_medoids(hs, comm, cb, M0, n)
     tr2 = []
     while True:
-        conv, sw = parallel.fp2_iter(hs, comm, cb)
+        conv, sw = parallel.fp2_iter(hs, comm, cb, mode=mode)
         tr2.append(hs[0].km.last_swaps())
         if conv:
             break

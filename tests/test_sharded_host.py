@@ -317,6 +317,53 @@ def test_gloo_world2_fp2_exchange_layout():
                 assert (blk == (10 * r + j) % 251).all()
 
 
+class RoundShard:
+    """Only the owner-side FastPAM2 round buffers (CPU tensors), rank-tagged."""
+
+    def __init__(self, rank, world, stride):
+        self.x = (torch.full((stride,), 7 + rank, dtype=torch.uint8), torch.zeros(stride * world, dtype=torch.uint8),
+                  stride)
+        self.x[0][:4] = torch.tensor([rank, 0, 0, 0], dtype=torch.uint8)
+
+    def fp2_round_tensors(self, world):
+        return self.x
+
+
+def _round_worker(rank, world, port, q):
+    import torch.distributed as dist
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        h = RoundShard(rank, world, 48)
+        parallel.TorchComm().allgather_fp2_round([h])
+        q.put((rank, h.x[1].numpy().copy()))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_gloo_world2_fp2_round_layout():
+    """Owner-side rounds: rank r's round buffer (header + column) lands at
+    [r*stride, (r+1)*stride) of every rank's receive buffer -- the layout
+    k_fp2_round_apply reads -- and LocalComm (virtual ranks) does the same."""
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    ps = [ctx.Process(target=_round_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in ps:
+        p.start()
+    out = sorted([q.get(timeout=120) for _ in ps], key=lambda t: t[0])
+    for p in ps:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    local = [RoundShard(r, 3, 48) for r in range(3)]
+    parallel.LocalComm(3).allgather_fp2_round(local)
+    for got, world in [(out[0][1], 2), (out[1][1], 2), (local[0].x[1].numpy(), 3), (local[2].x[1].numpy(), 3)]:
+        for r in range(world):
+            blk = got[r * 48:(r + 1) * 48]
+            assert blk[0] == r and (blk[4:] == 7 + r).all()
+
+
 # ---------- FastCLARA from points over ranks (NEXT-3; P:618-620) ----------
 
 def _oracle_runner(X, metric, k, samples, variant):
