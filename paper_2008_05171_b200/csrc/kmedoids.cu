@@ -82,17 +82,21 @@ int choose_parts(int64_t n, int64_t w, int cols_per_cta, int resident) {
 }
 
 
-// Row parts of the segment stream (measured): about 1000
-// rows per part, but between 3 and 8 waves of resident CTAs (3 per SM) --
-// more, shorter CTAs balance the Poisson-lumpy hit work across SMs; very
-// short parts cost ring fill/drain and combine bytes.
+// Row parts of the segment stream (measured): at most
+// ~1500 rows per part, at least 1.7 and at most 8 waves of resident CTAs (3
+// per SM) -- more, shorter CTAs balance the Poisson-lumpy hit work across
+// SMs; every part costs ring fill/drain and 36 bytes per column of part
+// outputs that the post kernel folds.  Round 2 sweep of the step (stream +
+// post): C3 P = 58 -> 33 (0.300 -> 0.290 ms), C4 P = 50 -> 34 (1.509 ->
+// 1.500 ms); round 1's rule (n/1000 rows, >= 3 waves) predates the fused
+// post kernel.
 constexpr int PART_SKEW_DEFAULT = 15;  // 16ths; see km::part_lo (C4 stream 1.565 -> 1.478 ms)
 
 int choose_parts_seg(int64_t n, int64_t w) {
     const int64_t ncb = cdiv(w, SG_NC * 128);
     const int64_t slots = (int64_t)NUM_SMS * SG_MINB;
-    int64_t P = n / 1000;
-    P = std::max<int64_t>(P, cdiv(3 * slots, ncb));
+    int64_t P = cdiv(n, 1500);
+    P = std::max<int64_t>(P, cdiv(17 * slots, 10 * ncb));
     P = std::min<int64_t>(P, std::max<int64_t>(1, 8 * slots / ncb));
     P = std::min<int64_t>(P, std::max<int64_t>(1, n / 64));
     return (int)std::max<int64_t>(P, 1);
