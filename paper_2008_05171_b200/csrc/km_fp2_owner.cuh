@@ -103,16 +103,10 @@ k_fp2_owned_eval(const T* __restrict__ colsrc, const int* __restrict__ colidx, i
     int q = r0, round = 0;
     while (true) {
         __syncthreads();
-        if (threadIdx.x == 0) {
+        if (wib == 0) {                          // warp 0 forms the batch (own entries only)
             int nb = 0;
-            for (; q < m && nb < FP2_B; ++q) {
-                const int ci = colidx[q];
-                if (ci / maxcnt != me) continue;                 // another rank's candidate
-                const int i = order[q], c = best[i].c;
-                if (point_slot[c] >= 0) continue;                // c became a medoid: skipped
-                s_r[nb] = q; s_i[nb] = i; s_c[nb] = c; s_l[nb] = ci % maxcnt; ++nb;
-            }
-            s_nb = nb; s_next = q;
+            fp2_batch_window(order, best, point_slot, colidx, me, maxcnt, m, lane, q, nb, s_r, s_i, s_c, s_l);
+            if (lane == 0) { s_nb = nb; s_next = q; }
         }
         __syncthreads();
         const int nb = s_nb;

@@ -1022,7 +1022,7 @@ __global__ void k_fp2_slot_reduce(int k, int split, const Rec<A>* __restrict__ p
 // per-slot bests, ordered by (v_i, i) -- the rank of slot i is the number of
 // improving slots before it in that order (k <= a few thousand: one block).
 // Also the iteration's decision bookkeeping (the sequential kernel counts
-// this iteration's swaps from 0; k_fp2_finish adds the previous total).
+// this iteration's swaps from 0, then adds the previous total back).
 template <typename A>
 __global__ void k_fp2_plan(const Rec<A>* __restrict__ best, int k, const A* __restrict__ td,
                            Decision<A>* __restrict__ dec, int* __restrict__ order, int* __restrict__ m_out,
@@ -1075,15 +1075,6 @@ __global__ void k_fp2_plan(const Rec<A>* __restrict__ best, int k, const A* __re
     }
 }
 
-template <typename A>
-__global__ void k_fp2_finish(Decision<A>* __restrict__ dec, const int* __restrict__ swaps_prev) {
-    dec->swaps += *swaps_prev;
-}
-
-template <typename A>
-__global__ void k_fp2_count(const Decision<A>* __restrict__ dec, int* __restrict__ swaps_iter) {
-    *swaps_iter = dec->swaps;
-}
 
 // The sequential phase of one FastPAM2 iteration as ONE cooperative kernel.
 // order[0..m) are the improving slots sorted by (v_i, i) (host), best[i] =
@@ -1107,6 +1098,49 @@ __global__ void k_fp2_count(const Decision<A>* __restrict__ dec, int* __restrict
 // grid syncs per batch (plus two per applied swap) instead of two per entry.
 // Applied swaps are appended to trace[] (slot, c, dTD).
 constexpr int FP2_B = 32;
+
+// The next batch of the sequential phase, formed by one warp: plan entries q,
+// q+1, ... in order, skipping those whose candidate became a medoid (and,
+// owner-side rounds, colidx != null, those owned by another rank), until
+// FP2_B are taken or q reaches m.  The 32 entries of a window are examined at
+// once; q ends behind the last entry examined (entries skipped after the
+// last one taken are consumed too: nothing changes the state within a batch).
+template <typename A>
+__device__ __forceinline__ void fp2_batch_window(const int* __restrict__ order, const Rec<A>* __restrict__ best,
+                                                 const int* __restrict__ point_slot, const int* __restrict__ colidx,
+                                                 int me, int maxcnt, int m, int lane, int& q, int& nb, int* s_r,
+                                                 int* s_i, int* s_c, int* s_l) {
+    while (q < m && nb < FP2_B) {
+        const int qq = q + lane;
+        bool ok = false;
+        int i = 0, c = 0, l = 0;
+        if (qq < m) {
+            ok = true;
+            if (colidx) {
+                const int ci = colidx[qq];
+                ok = ci / maxcnt == me;                  // another rank's candidate
+                l = ci % maxcnt;
+            }
+            if (ok) {
+                i = order[qq];
+                c = best[i].c;
+                ok = point_slot[c] < 0;                  // c became a medoid: skipped
+            }
+        }
+        const unsigned bal = __ballot_sync(0xffffffffu, ok);
+        const int nv = __popc(bal);
+        const int take = min(nv, FP2_B - nb);
+        const int rank = __popc(bal & ((1u << lane) - 1u));
+        if (ok && rank < take) {
+            s_r[nb + rank] = qq; s_i[nb + rank] = i; s_c[nb + rank] = c;
+            if (s_l) s_l[nb + rank] = l;
+        }
+        q = take < nv ? q + (int)__fns(bal, 0, take) + 1 : q + 32;
+        nb += take;
+    }
+    q = min(q, m);
+}
+
 template <typename T, typename A>
 __global__ void __launch_bounds__(256)
 k_fp2_sequential(const T* __restrict__ D, int64_t ld, const T* __restrict__ colsrc, const int* __restrict__ colidx,
@@ -1115,7 +1149,8 @@ k_fp2_sequential(const T* __restrict__ D, int64_t ld, const T* __restrict__ cols
                  T* __restrict__ MC, int* __restrict__ near, int* __restrict__ sec, T* __restrict__ dn,
                  T* __restrict__ ds, T* __restrict__ cols, A* __restrict__ td, A* __restrict__ partials,
                  Decision<A>* __restrict__ dec, Rec<A>* __restrict__ trace, int trace_cap,
-                 int* __restrict__ rescan, int* __restrict__ rescan_count, int sym) {
+                 int* __restrict__ rescan, int* __restrict__ rescan_count, int sym, int* __restrict__ swaps_iter,
+                 const int* __restrict__ swaps_prev) {
     namespace cg = cooperative_groups;
     cg::grid_group grid = cg::this_grid();
     __shared__ A sred[8][FP2_B];
@@ -1133,18 +1168,18 @@ k_fp2_sequential(const T* __restrict__ D, int64_t ld, const T* __restrict__ cols
         // the barrier keeps thread 0 from overwriting the shared batch / pick
         // values before every thread of the block has read the last ones
         __syncthreads();
-        if (threadIdx.x == 0) {
+        if (wib == 0) {
+            // warp 0 forms the batch, 32 plan entries per window (their loads
+            // in parallel; round 1: thread 0 walked the entries one dependent
+            // load chain at a time, ~1 us per entry)
             int nb = 0, q = r;
             if (r == 0) {                            // FastPAM1's swap, applied as is
-                s_r[0] = 0; s_i[0] = order[0]; s_c[0] = best[order[0]].c; nb = 1; q = 1;
+                if (lane == 0) { s_r[0] = 0; s_i[0] = order[0]; s_c[0] = best[order[0]].c; }
+                nb = 1; q = 1;
             } else {
-                for (; q < m && nb < FP2_B; ++q) {
-                    const int i = order[q], c = best[i].c;
-                    if (point_slot[c] >= 0) continue;   // c became a medoid: skipped
-                    s_r[nb] = q; s_i[nb] = i; s_c[nb] = c; ++nb;
-                }
+                fp2_batch_window(order, best, point_slot, nullptr, 0, 1, m, lane, q, nb, s_r, s_i, s_c, nullptr);
             }
-            s_nb = nb; s_next = q;
+            if (lane == 0) { s_nb = nb; s_next = q; }
         }
         __syncthreads();
         const int nb = s_nb;
@@ -1292,6 +1327,13 @@ k_fp2_sequential(const T* __restrict__ D, int64_t ld, const T* __restrict__ cols
         grid.sync();
         r = s_r[pick] + 1;
         ++round;
+    }
+    // this iteration's swaps (counted from 0) and, device-plan path, the
+    // running total restored (block 0 / thread 0 is dec's only writer)
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+        const int sw = dec->swaps;
+        *swaps_iter = sw;
+        if (swaps_prev) dec->swaps = sw + *swaps_prev;
     }
 }
 

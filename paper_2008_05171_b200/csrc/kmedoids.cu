@@ -226,6 +226,7 @@ struct Impl : ImplBase {
         for (void* p : bufs) cudaFree(p);
         if (h_dec) cudaFreeHost(h_dec);
         if (h_td) cudaFreeHost(h_td);
+        if (h_f2out) cudaFreeHost(h_f2out);
         for (auto e : sp_ev) if (e) cudaEventDestroy(e);
         for (auto e : sh_ev) if (e) cudaEventDestroy(e);
         for (auto& p : pr_ev) for (auto e : p) if (e) cudaEventDestroy(e);
@@ -1028,28 +1029,32 @@ struct Impl : ImplBase {
         km::k_fp2_plan<A><<<1, 1024, pstaged ? psm : 0, st>>>(fp2_best, k, td, dec, fp2_order, fp2_m, fp2_swaps_prev,
                                                               pstaged);
         KM_CKL();
-        KM_TRY(launch_fp2_sequential(nullptr, nullptr));
-        km::k_fp2_finish<A><<<1, 1, 0, st>>>(dec, fp2_swaps_prev);
-        KM_CKL();
-        launches += 2;
+        KM_TRY(launch_fp2_sequential(nullptr, nullptr, fp2_swaps_prev));
+        ++launches;
+        // the outcome in ONE host wait: decision, TD, this iteration's swap
+        // count and the whole trace buffer (k records at most) into pinned memory
+        if (!h_f2out) {
+            KM_CK(cudaMallocHost((void**)&h_f2out, sizeof(Rec) * (size_t)(trace_cap + 1)));
+        }
         KM_CK(cudaMemcpyAsync(h_dec, dec, sizeof(Dec), cudaMemcpyDeviceToHost, st));
         KM_CK(cudaMemcpyAsync(h_td, td, sizeof(A), cudaMemcpyDeviceToHost, st));
+        KM_CK(cudaMemcpyAsync(h_f2out, fp2_m + 1, sizeof(int), cudaMemcpyDeviceToHost, st));
+        KM_CK(cudaMemcpyAsync(h_f2out + 1, trace, (size_t)trace_cap * sizeof(Rec), cudaMemcpyDeviceToHost, st));
         KM_CK(cudaStreamSynchronize(st));
         KM_TRY(fp2_finish_profiling());
-        // this iteration's swaps: the tail of the trace (dec->swaps counts all)
+        // this iteration's swaps: the head of the trace (the kernel counts from 0)
         int done = 0;
-        KM_CK(cudaMemcpy(&done, fp2_m + 1, sizeof(int), cudaMemcpyDeviceToHost));
-        last_swaps.resize(std::min(done, trace_cap));
-        if (!last_swaps.empty())
-            KM_CK(cudaMemcpy(last_swaps.data(), trace, last_swaps.size() * sizeof(Rec), cudaMemcpyDeviceToHost));
+        memcpy(&done, h_f2out, sizeof(int));
+        last_swaps.assign(h_f2out + 1, h_f2out + 1 + std::min(done, trace_cap));
         if (swaps_out) *swaps_out = done;
         if (td_out) memcpy(td_out, h_td, sizeof(A));
         return done > 0 ? KM_OK : KM_CONVERGED;
     }
 
+    Rec* h_f2out = nullptr;          // pinned: [0] swaps of the iteration (int), [1..] the trace
     int* fp2_m = nullptr;            // [2]: improving slots m; swaps of the iteration
     int* fp2_swaps_prev = nullptr;
-    km_status launch_fp2_sequential(const T* colsrc, const int* colidx_dev) {
+    km_status launch_fp2_sequential(const T* colsrc, const int* colidx_dev, const int* swaps_prev_dev = nullptr) {
         const T* Dp = D; int64_t ldv = ld; int nn = (int)n; int kk = k;
         int* Mp = M; int* psp = point_slot; T* MCp = MC; int* nr = near; int* sc = sec; T* dnp = dn; T* dsp = ds;
         T* cb = fp2_cols; A* tdp = td; A* pp = fp2_partials; Dec* dp = dec; Rec* tr = trace; int tc = trace_cap;
@@ -1057,14 +1062,13 @@ struct Impl : ImplBase {
         const T* csp = colsrc; const int* cip = colidx_dev;
         int* rsp = rescan; int* rcp = rescan_count;
         int symv = symmetric ? 1 : 0;
+        int* swi = fp2_m + 1;               // swaps of this iteration (written by the kernel)
+        const int* swp = swaps_prev_dev;
         void* args[] = {&Dp, &ldv, &csp, &cip, &nn, &kk, &op, &mp, &bp, &Mp, &psp, &MCp, &nr, &sc, &dnp, &dsp, &cb,
-                        &tdp, &pp, &dp, &tr, &tc, &rsp, &rcp, &symv};
+                        &tdp, &pp, &dp, &tr, &tc, &rsp, &rcp, &symv, &swi, &swp};
         KM_CK(cudaLaunchCooperativeKernel((void*)km::k_fp2_sequential<T, A>, dim3(fp2_blocks), dim3(256), args, 0,
                                           st));
         ++launches;
-        // swaps of this iteration (the kernel counted them in dec->swaps from 0)
-        km::k_fp2_count<A><<<1, 1, 0, st>>>(dec, fp2_m + 1);
-        KM_CKL();
         return KM_OK;
     }
 
