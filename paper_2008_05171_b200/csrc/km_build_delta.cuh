@@ -101,8 +101,103 @@ k_changed_scatter(int n, const int* __restrict__ flag, const T* __restrict__ dn_
     }
 }
 
+// Parts of the delta stream for m listed rows: at least BD_ROWS_MIN rows per
+// part (late steps list a few hundred rows: the 1-2 us fixed cost of a CTA,
+// ring set-up and drain, then dominates), at most P.  A deterministic function
+// of m, so the stream and the combine agree without a host round trip.
+constexpr int BD_ROWS_MIN = 64;
+__host__ __device__ inline int bd_parts(int m, int P) {
+    const int p = (m + BD_ROWS_MIN - 1) / BD_ROWS_MIN;
+    return p < 1 ? 1 : (p > P ? P : p);
+}
+
+// k_build_dn_delta + k_chunk_scan + k_changed_scatter as ONE cooperative
+// kernel (one grid sync instead of two kernel boundaries): block b owns the
+// objects [b*chunk, (b+1)*chunk); phase A as k_build_dn_delta, then every
+// block sums the counts of the blocks before it (its list offset; block 0
+// also writes the total *m) and places its changed objects in object order
+// (the same list, bit for bit, as the three kernels).
+template <typename T, typename A>
+__global__ void __launch_bounds__(BD_CHUNK_THREADS)
+k_build_changed(const T* __restrict__ D, int64_t ld, int n, int64_t col_begin, const Decision<A>* __restrict__ dec,
+                T* __restrict__ MC, const int* __restrict__ point_slot, T* __restrict__ dn, T* __restrict__ dn_old,
+                int* __restrict__ flag, int chunk, int* __restrict__ cnt, int* __restrict__ lst_o,
+                T* __restrict__ lst_old, T* __restrict__ lst_new, int* __restrict__ m_out) {
+    namespace cg = cooperative_groups;
+    cg::grid_group grid = cg::this_grid();
+    __shared__ int wsum[BD_CHUNK_THREADS / 32];
+    __shared__ int s_off;
+    const int step = dec->slot;
+    const int64_t c = dec->c;
+    const int o0 = min(n, (int)blockIdx.x * chunk), o1 = min(n, o0 + chunk);
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    int count = 0;
+    for (int ob = o0; ob < o1; ob += blockDim.x) {
+        const int o = ob + threadIdx.x;
+        int f = 0;
+        if (o < o1) {
+            const T x = D[(int64_t)o * ld + (c - col_begin)];
+            MC[(int64_t)step * n + o] = x;
+            const T old = dn[o];
+            const T nw = point_slot[o] >= 0 ? (T)0 : (x < old ? x : old);
+            if (nw != old) { f = 1; dn_old[o] = old; dn[o] = nw; }
+            flag[o] = f;
+        }
+        count += __syncthreads_count(f);
+    }
+    if (threadIdx.x == 0) cnt[blockIdx.x] = count;
+    grid.sync();
+    {
+        // offset = sum of the counts of blocks 0..b-1 (fixed order: exact int)
+        int s = 0, t = 0;
+        for (int b = threadIdx.x; b < (int)gridDim.x; b += blockDim.x) {
+            const int v = __ldcg(&cnt[b]);
+            if (b < (int)blockIdx.x) s += v;
+            t += v;
+        }
+#pragma unroll
+        for (int x = 16; x >= 1; x >>= 1) {
+            s += __shfl_xor_sync(0xffffffffu, s, x);
+            t += __shfl_xor_sync(0xffffffffu, t, x);
+        }
+        if (lane == 0) wsum[warp] = s;
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            int a = 0;
+            for (int w2 = 0; w2 < BD_CHUNK_THREADS / 32; ++w2) a += wsum[w2];
+            s_off = a;
+        }
+        __syncthreads();
+        if (lane == 0) wsum[warp] = t;
+        __syncthreads();
+        if (blockIdx.x == 0 && threadIdx.x == 0) {
+            int a = 0;
+            for (int w2 = 0; w2 < BD_CHUNK_THREADS / 32; ++w2) a += wsum[w2];
+            *m_out = a;
+        }
+        __syncthreads();
+    }
+    int run = s_off;
+    for (int ob = o0; ob < o1; ob += blockDim.x) {
+        const int o = ob + threadIdx.x;
+        const int f = (o < o1) ? flag[o] : 0;
+        const unsigned bal = __ballot_sync(0xffffffffu, f);
+        if (lane == 0) wsum[warp] = __popc(bal);
+        __syncthreads();
+        int base = 0, tot = 0;
+        for (int w2 = 0; w2 < BD_CHUNK_THREADS / 32; ++w2) { if (w2 < warp) base += wsum[w2]; tot += wsum[w2]; }
+        if (f) {
+            const int pos = run + base + __popc(bal & ((1u << lane) - 1u));
+            lst_o[pos] = o; lst_old[pos] = dn_old[o]; lst_new[pos] = dn[o];
+        }
+        run += tot;
+        __syncthreads();
+    }
+}
+
 // The delta stream: as k_build_tma (MODE 1) over the rows lst_o[0..*m), with
-// two thresholds per row.  Part q covers list entries [q*m/P, (q+1)*m/P).
+// two thresholds per row.  Part q of Pe = bd_parts(m, P) covers list entries
+// [q*m/Pe, (q+1)*m/Pe); CTAs with q >= Pe leave at once.
 template <typename T, typename A, int NC, int RB, int S, int MINB>
 __global__ void __launch_bounds__((NC + 1) * 32, MINB)
 k_build_delta_tma(const T* __restrict__ D, int64_t ld, int w, int wpad, int P, const int* __restrict__ m_dev,
@@ -116,7 +211,9 @@ k_build_delta_tma(const T* __restrict__ D, int64_t ld, int w, int wpad, int P, c
     uint64_t* empty = full + S;
     const int m = *m_dev;
     const int q = blockIdx.y;
-    const int64_t p0 = part_lo_uniform(q, m, P), p1 = part_lo_uniform(q + 1, m, P);   // a few changed rows: no tilt
+    const int Pe = bd_parts(m, P);
+    if (q >= Pe) return;
+    const int64_t p0 = part_lo_uniform(q, m, Pe), p1 = part_lo_uniform(q + 1, m, Pe);   // a few changed rows: no tilt
     const int nstages = (int)((p1 - p0 + RB - 1) / RB);
     const int ctacol = blockIdx.x * C::COLS;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -209,22 +306,31 @@ k_build_delta_tma(const T* __restrict__ D, int64_t ld, int w, int wpad, int P, c
         if (cb + j < w) ptx::st_hint(&out[base + cb + j], acc[j], keep);
 }
 
-// gain[c] (+)= sum of the parts; lexicographic min of (gain, c) over non-medoids
+// gain[c] (+)= sum of the parts (m_dev: the delta stream's bd_parts(*m_dev, P)
+// parts, else P); lexicographic min of (gain, c) over non-medoids.  With
+// sel_step >= 0 (single GPU) the last block also takes the BUILD step itself
+// (k_build_select's bookkeeping: medoid sel_step <- c*, TD += gain), after
+// every block has read point_slot.
 template <typename A>
 __global__ void k_build_gain_combine(int w, int64_t col_begin, int P, const A* __restrict__ in, int accumulate,
-                                     A* __restrict__ gain, const int* __restrict__ point_slot, Rec<A>* partials,
-                                     unsigned* counter, Rec<A>* out) {
+                                     A* __restrict__ gain, int* __restrict__ point_slot, Rec<A>* partials,
+                                     unsigned* counter, Rec<A>* out, const int* __restrict__ m_dev = nullptr,
+                                     int sel_step = -1, A* __restrict__ td = nullptr, int* __restrict__ M = nullptr,
+                                     Decision<A>* __restrict__ dec = nullptr) {
     const int cl = blockIdx.x * blockDim.x + threadIdx.x;
+    const int Pe = m_dev ? bd_parts(*m_dev, P) : P;
     Rec<A> best = rec_none<A>();
     if (cl < w) {
         A s = 0;
-        for (int q = 0; q < P; ++q) s += in[(int64_t)q * w + cl];
+        for (int q = 0; q < Pe; ++q) s += in[(int64_t)q * w + cl];
         const A g = accumulate ? gain[cl] + s : s;
         gain[cl] = g;
         const int64_t c = col_begin + cl;
         if (point_slot[c] < 0) { best.v = g; best.slot = 0; best.c = (int)c; }
     }
-    grid_min_rec(best, partials, counter, out);
+    Rec<A> m;
+    if (grid_min_rec_last(best, partials, counter, out, &m) && sel_step >= 0 && threadIdx.x == 0)
+        build_take(m, sel_step, td, M, point_slot, dec);
 }
 
 }  // namespace km

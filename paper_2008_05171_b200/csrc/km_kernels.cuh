@@ -63,8 +63,9 @@ __device__ Rec<A> block_min_rec(Rec<A> r) {
 // Grid-wide lexicographic min with the last-block-done pattern: every block
 // writes its partial; the last block to finish reduces them in block order
 // (deterministic) and writes *out.  *counter must be 0 on entry; it is reset.
+// Returns true in the last block (the minimum is then in thread 0's *res).
 template <typename A>
-__device__ void grid_min_rec(Rec<A> r, Rec<A>* partials, unsigned* counter, Rec<A>* out) {
+__device__ bool grid_min_rec_last(Rec<A> r, Rec<A>* partials, unsigned* counter, Rec<A>* out, Rec<A>* res) {
     __shared__ bool am_last;
     r = block_min_rec(r);
     if (threadIdx.x == 0) {
@@ -74,7 +75,7 @@ __device__ void grid_min_rec(Rec<A> r, Rec<A>* partials, unsigned* counter, Rec<
         am_last = (prev == gridDim.x - 1);
     }
     __syncthreads();
-    if (!am_last) return;
+    if (!am_last) return false;
     __threadfence();
     Rec<A> m = rec_none<A>();
     for (int b = threadIdx.x; b < (int)gridDim.x; b += blockDim.x) {
@@ -88,7 +89,14 @@ __device__ void grid_min_rec(Rec<A> r, Rec<A>* partials, unsigned* counter, Rec<
     if (threadIdx.x == 0) {
         *out = m;
         *counter = 0;
+        *res = m;
     }
+    return true;
+}
+template <typename A>
+__device__ void grid_min_rec(Rec<A> r, Rec<A>* partials, unsigned* counter, Rec<A>* out) {
+    Rec<A> m;
+    grid_min_rec_last(r, partials, counter, out, &m);
 }
 
 // ---------------------------------------------------------------------------
@@ -1472,11 +1480,8 @@ __global__ void k_build_combine(const T* __restrict__ D, int64_t ld, int w, int6
 // BUILD step bookkeeping: slot `step` <- c*, TD <- value (step
 // 0) or TD + dTD* (later steps).
 template <typename A>
-__global__ void k_build_select(const Rec<A>* __restrict__ recs, int nrec, int step, A* __restrict__ td,
-                               int* __restrict__ M, int* __restrict__ point_slot, Decision<A>* __restrict__ dec) {
-    Rec<A> b = rec_none<A>();
-    for (int r = 0; r < nrec; ++r)
-        if (rec_less(recs[r], b)) b = recs[r];
+__device__ __forceinline__ void build_take(const Rec<A>& b, int step, A* __restrict__ td, int* __restrict__ M,
+                                           int* __restrict__ point_slot, Decision<A>* __restrict__ dec) {
     dec->apply = 1;
     dec->dtd = b.v;
     dec->slot = step;
@@ -1485,6 +1490,14 @@ __global__ void k_build_select(const Rec<A>* __restrict__ recs, int nrec, int st
     M[step] = b.c;
     point_slot[b.c] = step;
     if (step == 0) *td = b.v; else *td += b.v;
+}
+template <typename A>
+__global__ void k_build_select(const Rec<A>* __restrict__ recs, int nrec, int step, A* __restrict__ td,
+                               int* __restrict__ M, int* __restrict__ point_slot, Decision<A>* __restrict__ dec) {
+    Rec<A> b = rec_none<A>();
+    for (int r = 0; r < nrec; ++r)
+        if (rec_less(recs[r], b)) b = recs[r];
+    build_take(b, step, td, M, point_slot, dec);
 }
 
 // d_nearest update (P:295-298 for step 0, P:313-316 later): medoids get 0.

@@ -1945,7 +1945,7 @@ struct Impl : ImplBase {
     // step >= 1 gains into bd_gain and the best record into rec_local:
     // a full pass (step 1) or the delta pass over the objects changed by the
     // previous step
-    km_status bd_eval(int step) {
+    km_status bd_eval(int step, bool fuse_select = false) {
         using C = km::SegCfg<T, SG_NC, SG_RB, SG_S>;
         if (step == 1) {
             auto kern = km::k_build_tma<T, A, SG_NC, SG_RB, SG_S, SG_MINB, 1>;
@@ -1960,8 +1960,11 @@ struct Impl : ImplBase {
         }
         KM_CKL();
         ++launches;
+        // (the delta stream ran bd_parts(m, Pbt) parts; fused: the last block
+        // also takes the step, as k_build_select)
         km::k_build_gain_combine<A><<<ncomb, 128, 0, st>>>(w, c0, Pbt, b_out, step == 1 ? 0 : 1, bd_gain, point_slot,
-                                                            partials, counters, rec_local);
+                                                            partials, counters, rec_local, step == 1 ? nullptr : bd_m,
+                                                            fuse_select ? step : -1, td, M, dec);
         KM_CKL();
         ++launches;
         return KM_OK;
@@ -1977,7 +1980,26 @@ struct Impl : ImplBase {
     }
 
     // changed-object list of the step just applied (its column is in MC)
+    int bd_coop = -1;               // 1: k_build_changed (cooperative) fits, 0: the three kernels
     km_status bd_changed_list(int from_mc) {
+        if (bd_coop < 0) {
+            int dev = 0, per_sm = 0, nsm = 0;
+            KM_CK(cudaGetDevice(&dev));
+            KM_CK(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
+            KM_CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, km::k_build_changed<T, A>, km::BD_CHUNK_THREADS, 0));
+            bd_coop = (int64_t)per_sm * nsm >= bd_B ? 1 : 0;
+            if (const char* e = getenv("KM_BUILD_COOP")) bd_coop = bd_coop && e[0] != '0';   // measurement override
+        }
+        if (!from_mc && bd_coop) {
+            const T* Dp = D; int64_t ldv = ld; int nn = (int)n; int64_t cbg = c0; const Dec* dp = dec; T* MCp = MC;
+            const int* psp = point_slot; T* dnp = dn; T* dop = bd_dnold; int* fp = bd_flag; int ch = bd_chunk;
+            int* cp = bd_cnt; int* lo = bd_lo; T* lold = bd_lold; T* lnew = bd_lnew; int* mp = bd_m;
+            void* args[] = {&Dp, &ldv, &nn, &cbg, &dp, &MCp, &psp, &dnp, &dop, &fp, &ch, &cp, &lo, &lold, &lnew, &mp};
+            KM_CK(cudaLaunchCooperativeKernel((void*)km::k_build_changed<T, A>, dim3(bd_B), dim3(km::BD_CHUNK_THREADS),
+                                              args, 0, st));
+            ++launches;
+            return KM_OK;
+        }
         km::k_build_dn_delta<T, A><<<bd_B, km::BD_CHUNK_THREADS, 0, st>>>(
             D, ld, (int)n, c0, dec, MC, point_slot, dn, bd_dnold, bd_flag, bd_chunk, bd_cnt, from_mc);
         KM_CKL();
@@ -2065,10 +2087,13 @@ struct Impl : ImplBase {
         ready = false;
         const int nb = (int)cdiv(n, 256);
         for (int step = 0; step < k; ++step) {
-            if (bd_mode == 1 && step >= 1) KM_TRY(bd_eval(step));
-            else KM_TRY(build_eval(step));
-            km::k_build_select<A><<<1, 1, 0, st>>>(rec_local, 1, step, td, M, point_slot, dec);
-            KM_CKL();
+            if (bd_mode == 1 && step >= 1) {
+                KM_TRY(bd_eval(step, true));             // the combine's last block takes the step
+            } else {
+                KM_TRY(build_eval(step));
+                km::k_build_select<A><<<1, 1, 0, st>>>(rec_local, 1, step, td, M, point_slot, dec);
+                KM_CKL();
+            }
             if (bd_mode == 1 && step >= 1) {
                 if (step + 1 < k) {
                     KM_TRY(bd_changed_list(0));
