@@ -68,6 +68,7 @@ struct PostArgs {
     int *head_slot, *tail_slot;
     int prep_only;             // 1: phases count, B, C only (slot sort, R, parts of the current cache)
     int allow_reg;             // 0: always the chunk loops (KM_POST_REG=0, tests of chunks > POST_THREADS)
+    int sym;                   // D declared exactly symmetric (single GPU): d(o, c*) read from row c*
     IterMirror<A>* h_ring;     // pinned host ring of iteration outcomes (or null)
     int ring;                  // its size
     int* seq;                  // device counter of FastPAM1 post launches (ring slot = seq % ring)
@@ -84,7 +85,7 @@ struct PostArgs {
     Rec<A>* blk_recs;          // [gridDim] per-block best record
 };
 
-constexpr int POST_QU = 4;     // part outputs loaded ahead per lane in phase 0
+constexpr int POST_QU = 5;     // part outputs loaded ahead per lane in phase 0 (P <= 40: one batch per range)
 constexpr int POST_RG = 4;     // phase-0 column groups per round (merged by warps 0..3 in parallel)
 
 // Phase-0 range state of one lane (column) over a contiguous range of parts:
@@ -379,7 +380,10 @@ k_fp1_post(PostArgs<T, A> g) {
         int myent = -1;
         if (reg) {
             if (have) {
-                const T x = local ? g.D[(int64_t)myo * g.ld + (d.c - g.c0)] : g.MC[(int64_t)i * n + myo];
+                // column c* of D (n scattered sectors), or row c* when D is
+                // symmetric (one coalesced 4n-byte read, the same values)
+                const T x = !local ? g.MC[(int64_t)i * n + myo]
+                                   : g.sym ? g.D[(int64_t)d.c * g.ld + myo] : g.D[(int64_t)myo * g.ld + (d.c - g.c0)];
                 if (local) g.MC[(int64_t)i * n + myo] = x;
                 if (j1 == i || j2 == i) {
                     myent = atomicAdd(&s_nres, 1);

@@ -652,6 +652,7 @@ struct Impl : ImplBase {
             post_reg = (e && e[0] == '0') ? 0 : 1;
         }
         g.allow_reg = post_reg;
+        g.sym = symmetric ? 1 : 0;
         g.h_ring = h_ring; g.ring = RING; g.seq = post_seq;
         g.fuse = (post_fuse && !prep_only) ? 1 : 0;
         g.w = w; g.stage0 = post_stage0() ? 1 : 0;
