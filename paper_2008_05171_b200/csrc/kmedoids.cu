@@ -223,6 +223,8 @@ struct Impl : ImplBase {
         if (h_ring) cudaFreeHost(h_ring);
         if (build_exec) cudaGraphExecDestroy(build_exec);
         if (cap_st) cudaStreamDestroy(cap_st);
+        if (side_st) cudaStreamDestroy(side_st);
+        for (auto& e : fork_ev) if (e) cudaEventDestroy(e);
         for (void* p : bufs) cudaFree(p);
         if (h_dec) cudaFreeHost(h_dec);
         if (h_td) cudaFreeHost(h_td);
@@ -671,7 +673,7 @@ struct Impl : ImplBase {
     // one (or by swap_iter before the first).
     km_status enqueue_fp1_iteration() {
         const bool prof_save = profiling;
-        if (use_graph) profiling = true;      // the graph always carries the stream events
+        if (use_graph) profiling = graph_events() == 1;   // inline stream events (mode 2: fp1_capture adds them)
         fp1_mode = true;
         km_status s = eval_local(false);
         fp1_mode = false;
@@ -681,6 +683,33 @@ struct Impl : ImplBase {
         KM_TRY(launch_post());          // writes the pinned h_dec / h_td mirrors itself
         if (step_prof) KM_CK(record_ev(sp_ev[3]));
         if (step_prof) KM_CK(record_ev(sp_ev[4]));
+        return KM_OK;
+    }
+
+    // the iteration with its stream-kernel events on a side branch of the
+    // graph: start event as a root beside the stream kernel, end event after
+    // it, the post kernel depending on the stream kernel only
+    km_status enqueue_fp1_iteration_side(int gi) {
+        if (!side_st) {
+            KM_CK(cudaStreamCreateWithFlags(&side_st, cudaStreamNonBlocking));
+            for (auto& e : fork_ev) KM_CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+        }
+        KM_CK(cudaEventRecord(fork_ev[0], st));
+        KM_CK(cudaStreamWaitEvent(side_st, fork_ev[0], 0));
+        KM_CK(cudaEventRecordWithFlags(g_ev[gi][0], side_st, cudaEventRecordExternal));
+        const bool prof_save = profiling;
+        profiling = false;
+        fp1_mode = true;
+        km_status s = eval_local(false);
+        fp1_mode = false;
+        profiling = prof_save;
+        if (s != KM_OK) return s;
+        KM_CK(cudaEventRecord(fork_ev[1], st));
+        KM_CK(cudaStreamWaitEvent(side_st, fork_ev[1], 0));
+        KM_CK(cudaEventRecordWithFlags(g_ev[gi][1], side_st, cudaEventRecordExternal));
+        KM_TRY(launch_post());
+        KM_CK(cudaEventRecord(fork_ev[2], side_st));
+        KM_CK(cudaStreamWaitEvent(st, fork_ev[2], 0));
         return KM_OK;
     }
 
@@ -715,12 +744,13 @@ struct Impl : ImplBase {
     cudaGraphExec_t fp1_g[NGRAPH] = {};
     cudaEvent_t g_ev[NGRAPH][2] = {};   // stream kernel start / end inside graph g
     cudaEvent_t g_done[NGRAPH] = {};    // recorded after each launch of graph g
+    bool gev_ok[NGRAPH] = {};           // the last launch of slot g recorded its stream events
     bool fp1_any_done = false;          // a FastPAM1 pass may have set Decision::done
 
     km_status fp1_ring_alloc() {
         if (h_ring) return KM_OK;
         KM_CK(cudaMallocHost((void**)&h_ring, RING * sizeof(km::IterMirror<A>)));
-        memset((void*)h_ring, 0, RING * sizeof(km::IterMirror<A>));
+        memset((void*)h_ring, 0xff, RING * sizeof(km::IterMirror<A>));   // seq = -1: nothing written yet
         KM_TRY(alloc(&post_seq, 1));
         KM_CK(cudaMemsetAsync(post_seq, 0, sizeof(int), st));
         for (int g = 0; g < NGRAPH; ++g) {
@@ -739,6 +769,25 @@ struct Impl : ImplBase {
         return KM_OK;
     }
 
+    // stream-kernel events of the iteration graph (measurement override
+    // KM_GRAPH_EVENTS): 1 = on the path (event -> stream -> event -> post),
+    // 2 = on a side branch (the post depends on the stream kernel only),
+    // 0 = none.  Measured (scratch/evcost.py, K queued iterations): every
+    // event record node on the path cost ~3 us of step time; on the side
+    // branch the step equals the event-free graph (C2 82 -> 75 us, C3 291 ->
+    // 285 us, C4 -5 us) and the stream kernel is still timed.
+    int graph_events_mode = -1;
+    int graph_events() {
+        if (graph_events_mode < 0) {
+            const char* e = getenv("KM_GRAPH_EVENTS");
+            graph_events_mode = e ? std::max(0, std::min(2, atoi(e))) : 2;
+            if (step_prof) graph_events_mode = 1;         // KM_STEP_PROF stamps the path itself
+        }
+        return graph_events_mode;
+    }
+    cudaStream_t side_st = nullptr;
+    cudaEvent_t fork_ev[3] = {};
+
     km_status fp1_capture(int gi) {
         const int64_t l0 = launches;
         // capture on a private stream (the caller's may be the legacy default
@@ -750,7 +799,9 @@ struct Impl : ImplBase {
         if (be != cudaSuccess) { st = user_st; return fail(KM_ECUDA, "begin capture: %s", cudaGetErrorString(be)); }
         capturing = true;
         ev_a = g_ev[gi][0]; ev_b = g_ev[gi][1];
-        km_status cs = enqueue_fp1_iteration();
+        km_status cs;
+        if (graph_events() == 2) cs = enqueue_fp1_iteration_side(gi);
+        else cs = enqueue_fp1_iteration();
         ev_a = ev_b = nullptr;
         capturing = false;
         cudaGraph_t g = nullptr;
@@ -784,6 +835,7 @@ struct Impl : ImplBase {
             for (int g = 0; g < NGRAPH; ++g)               // both graphs at once: no capture inside later steps
                 if (!fp1_g[g]) KM_TRY(fp1_capture(g));
         if (step_prof) KM_CK(cudaEventRecord(sp_ev[0], st));
+        gev_ok[gi] = !graph || graph_events() != 0;
         if (graph) {
             KM_CK(cudaGraphLaunch(fp1_g[gi], st));
             launches += fp1_graph_kernels;
@@ -811,8 +863,9 @@ struct Impl : ImplBase {
         if (m.seq != (int32_t)seq) return fail(KM_ECUDA, "iteration ring out of step (%d vs %lld)", m.seq, (long long)seq);
         *h_dec = m.d;
         *h_td = m.td;
-        if (profiling && !m.noop) {
+        if (profiling && !m.noop && gev_ok[gi]) {
             float ms = 0.f;
+            KM_CK(cudaEventSynchronize(g_ev[gi][1]));
             KM_CK(cudaEventElapsedTime(&ms, g_ev[gi][0], g_ev[gi][1]));
             prof_ms += ms; prof_launches += 1;
         }
