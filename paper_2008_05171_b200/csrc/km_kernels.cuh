@@ -1084,6 +1084,73 @@ __global__ void k_fp2_plan(const Rec<A>* __restrict__ best, int k, const A* __re
 }
 
 
+// FastPAM2 steps 4-5 for k <= FP2_SORT_MAX in one block, with the per-slot
+// reduction folded in: per slot, the lexicographic min over the column
+// splits (fixed order, as k_fp2_slot_reduce) -> best[i]; the improving slots
+// keyed by (v_i, i) and the non-improving ones by a sentinel, sorted by a
+// bitonic network in shared memory (the keys are distinct: the same order as
+// k_fp2_plan's ranks); order[0..m) = the first m keys.
+constexpr int FP2_SORT_MAX = 2048;     // keys in 24 KB of shared memory
+template <typename A>
+__global__ void __launch_bounds__(1024)
+k_fp2_plan_sort(const Rec<A>* __restrict__ part, int split, Rec<A>* __restrict__ best, int k, int npow2,
+                const A* __restrict__ td, Decision<A>* __restrict__ dec, int* __restrict__ order,
+                int* __restrict__ m_out, int* __restrict__ swaps_prev) {
+    __shared__ int s_m;
+    extern __shared__ __align__(16) unsigned char sort_smem[];
+    A* kv = reinterpret_cast<A*>(sort_smem);
+    int* ki = reinterpret_cast<int*>(sort_smem + (size_t)npow2 * sizeof(A));
+    if (threadIdx.x == 0) s_m = 0;
+    __syncthreads();
+    const A tdv = *td;
+    for (int i = threadIdx.x; i < npow2; i += blockDim.x) {
+        A v = amax<A>();
+        int key = INT_MAX;
+        if (i < k) {
+            Rec<A> b = rec_none<A>();
+            constexpr int U = 8;                 // partials loaded ahead (one round trip for FP2_SPLIT = 8)
+            for (int y0 = 0; y0 < split; y0 += U) {
+                Rec<A> r[U];
+#pragma unroll
+                for (int u = 0; u < U; ++u) r[u] = y0 + u < split ? part[(int64_t)i * split + y0 + u] : rec_none<A>();
+#pragma unroll
+                for (int u = 0; u < U; ++u) if (rec_less(r[u], b)) b = r[u];
+            }
+            best[i] = b;
+            bool imp;
+            if (b.slot == INT_MAX) imp = false;
+            else if (std::is_same<A, double>::value) imp = (double)b.v < -1e-12 * fabs((double)tdv);
+            else imp = b.v < 0;
+            if (imp) { v = b.v; key = i; atomicAdd(&s_m, 1); }
+        }
+        kv[i] = v;
+        ki[i] = key;
+    }
+    __syncthreads();
+    for (int size = 2; size <= npow2; size <<= 1) {
+        for (int stride = size >> 1; stride > 0; stride >>= 1) {
+            for (int t = threadIdx.x; t < (npow2 >> 1); t += blockDim.x) {
+                const int a = 2 * t - (t & (stride - 1)), b = a + stride;
+                const bool up = (a & size) == 0;
+                const A va = kv[a], vb = kv[b];
+                const int ia = ki[a], ib = ki[b];
+                const bool gt = va > vb || (va == vb && ia > ib);
+                if (gt == up) { kv[a] = vb; kv[b] = va; ki[a] = ib; ki[b] = ia; }
+            }
+            __syncthreads();
+        }
+    }
+    const int m = s_m;
+    for (int r = threadIdx.x; r < m; r += blockDim.x) order[r] = ki[r];
+    if (threadIdx.x == 0) {
+        *m_out = m;
+        dec->iters += 1;
+        dec->apply = 0;
+        *swaps_prev = dec->swaps;
+        dec->swaps = 0;
+    }
+}
+
 // The sequential phase of one FastPAM2 iteration as ONE cooperative kernel.
 // order[0..m) are the improving slots sorted by (v_i, i) (host), best[i] =
 // (v_i, i, c_i).  r = 0 applies best[order[0]] as is (it is FastPAM1's swap).
@@ -1149,6 +1216,17 @@ __device__ __forceinline__ void fp2_batch_window(const int* __restrict__ order, 
     q = min(q, m);
 }
 
+// pinned host destinations of one FastPAM2 iteration's outcome (single-GPU
+// device-plan path; null pointers elsewhere): written by block 0 at the end
+// of k_fp2_sequential instead of four device-to-host copies after it
+template <typename A>
+struct F2HostOut {
+    Decision<A>* dec;
+    A* td;
+    int* swaps;          // this iteration's swaps
+    Rec<A>* trace;       // its first min(swaps, trace_cap) records
+};
+
 template <typename T, typename A>
 __global__ void __launch_bounds__(256)
 k_fp2_sequential(const T* __restrict__ D, int64_t ld, const T* __restrict__ colsrc, const int* __restrict__ colidx,
@@ -1158,7 +1236,7 @@ k_fp2_sequential(const T* __restrict__ D, int64_t ld, const T* __restrict__ cols
                  T* __restrict__ ds, T* __restrict__ cols, A* __restrict__ td, A* __restrict__ partials,
                  Decision<A>* __restrict__ dec, Rec<A>* __restrict__ trace, int trace_cap,
                  int* __restrict__ rescan, int* __restrict__ rescan_count, int sym, int* __restrict__ swaps_iter,
-                 const int* __restrict__ swaps_prev) {
+                 const int* __restrict__ swaps_prev, F2HostOut<A> hout) {
     namespace cg = cooperative_groups;
     cg::grid_group grid = cg::this_grid();
     __shared__ A sred[8][FP2_B];
@@ -1342,6 +1420,16 @@ k_fp2_sequential(const T* __restrict__ D, int64_t ld, const T* __restrict__ cols
         const int sw = dec->swaps;
         *swaps_iter = sw;
         if (swaps_prev) dec->swaps = sw + *swaps_prev;
+        if (hout.dec) {
+            *hout.dec = *dec;
+            *hout.td = *td;
+            *hout.swaps = sw;
+        }
+    }
+    if (hout.trace && blockIdx.x == 0) {
+        __syncthreads();                         // the trace records were written by thread 0
+        const int cnt = min(*swaps_iter, trace_cap);
+        for (int t = threadIdx.x; t < cnt; t += blockDim.x) hout.trace[t] = trace[t];
     }
 }
 

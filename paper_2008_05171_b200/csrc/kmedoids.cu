@@ -230,6 +230,7 @@ struct Impl : ImplBase {
         if (h_td) cudaFreeHost(h_td);
         if (h_f2out) cudaFreeHost(h_f2out);
         for (auto e : sp_ev) if (e) cudaEventDestroy(e);
+        for (auto e : f2_ev) if (e) cudaEventDestroy(e);
         for (auto e : sh_ev) if (e) cudaEventDestroy(e);
         for (auto& p : pr_ev) for (auto e : p) if (e) cudaEventDestroy(e);
         if (sh_mirror) cudaFreeHost(sh_mirror);
@@ -356,6 +357,29 @@ struct Impl : ImplBase {
     bool pending_prof = false;
     bool step_prof = false;
     cudaEvent_t sp_ev[5] = {};
+    // KM_STEP_PROF, FastPAM2: prep | stream | combine | slot best | plan | sequential | host copies
+    cudaEvent_t f2_ev[8] = {};
+    double f2_sum[7] = {};
+    int f2_n = 0;
+    void f2_mark(int i) {
+        if (!step_prof) return;
+        if (!f2_ev[0]) for (auto& e : f2_ev) cudaEventCreate(&e);
+        cudaEventRecord(f2_ev[i], st);
+    }
+    void f2_take() {
+        if (!step_prof || !f2_ev[0]) return;
+        cudaEventSynchronize(f2_ev[7]);
+        for (int i = 0; i < 7; ++i) {
+            float t = 0.f;
+            cudaEventElapsedTime(&t, f2_ev[i], f2_ev[i + 1]);
+            f2_sum[i] += t;
+        }
+        if (++f2_n % 10 == 0)
+            fprintf(stderr, "[kmedoids] FastPAM2 phases over %d iterations (us): prep %.1f stream %.1f combine %.1f "
+                    "slot_best %.1f plan %.1f sequential %.1f copies %.1f\n", f2_n, 1e3 * f2_sum[0] / f2_n,
+                    1e3 * f2_sum[1] / f2_n, 1e3 * f2_sum[2] / f2_n, 1e3 * f2_sum[3] / f2_n, 1e3 * f2_sum[4] / f2_n,
+                    1e3 * f2_sum[5] / f2_n, 1e3 * f2_sum[6] / f2_n);
+    }
     double sp_sum[5] = {};
     int sp_n = 0;
     // CUDA graph of the FastPAM1 iteration (KM_GRAPH=0 disables)
@@ -971,21 +995,27 @@ struct Impl : ImplBase {
 
     // FastPAM2 step 1-3 (reading R6), local part: per-slot best over this
     // handle's candidates into fp2_best (device).
-    km_status fp2_eval_local() {
+    km_status fp2_eval_local(bool fused_plan = false) {
         KM_TRY(fp2_alloc());
+        f2_mark(0);
         KM_TRY(prep());
+        f2_mark(1);
         // FastPAM2 always uses the segment-aligned TMA stream (it stores acc_c[i]).
         if (profiling) KM_CK(record_ev(ev0));
         KM_TRY((launch_seg<SG_NC, SG_RB, SG_S, SG_MINB>(fp2_acc)));
         KM_CKL();
         if (profiling) { KM_CK(record_ev(ev1)); pending_prof = true; }
+        f2_mark(2);
         KM_TRY(launch_combine(w, c0, P, o_plus, o_head, o_tail, o_imin, o_islot, head_slot, tail_slot, cand_v, cand_slot,
                               fp2_acc, fp2_plus));
+        f2_mark(3);
         km::k_fp2_slot_best<A><<<dim3(k, FP2_SPLIT), 256, 0, st>>>(w, c0, fp2_acc, fp2_plus, R, seg_start, point_slot,
                                                                      fp2_part);
         KM_CKL();
-        km::k_fp2_slot_reduce<A><<<(unsigned)cdiv(k, 128), 128, 0, st>>>(k, FP2_SPLIT, fp2_part, fp2_best);
-        KM_CKL();
+        if (!fused_plan) {                 // (single-GPU device plan: folded into k_fp2_plan_sort)
+            km::k_fp2_slot_reduce<A><<<(unsigned)cdiv(k, 128), 128, 0, st>>>(k, FP2_SPLIT, fp2_part, fp2_best);
+            KM_CKL();
+        }
         return KM_OK;
     }
 
@@ -1068,7 +1098,8 @@ struct Impl : ImplBase {
             const char* e = getenv("KM_FP2_HOSTPLAN");
             fp2_hostplan = (e && e[0] == '1') ? 1 : 0;
         }
-        KM_TRY(fp2_eval_local());
+        const bool sort_plan = !fp2_hostplan && k <= km::FP2_SORT_MAX;
+        KM_TRY(fp2_eval_local(sort_plan));
         if (fp2_hostplan) {
             A tdh;
             KM_CK(cudaMemcpyAsync(h_best.data(), fp2_best, k * sizeof(Rec), cudaMemcpyDeviceToHost, st));
@@ -1078,23 +1109,33 @@ struct Impl : ImplBase {
             const std::vector<int> order = fp2_order_slots(tdh);
             return fp2_sequential(order, nullptr, nullptr, swaps_out, td_out);
         }
-        const size_t psm = (size_t)k * (sizeof(A) + 1);
-        const bool pstaged = psm <= 40 * 1024;
-        km::k_fp2_plan<A><<<1, 1024, pstaged ? psm : 0, st>>>(fp2_best, k, td, dec, fp2_order, fp2_m, fp2_swaps_prev,
-                                                              pstaged);
+        f2_mark(4);
+        if (sort_plan) {
+            int np2 = 2;
+            while (np2 < k) np2 <<= 1;
+            km::k_fp2_plan_sort<A><<<1, 1024, (size_t)np2 * (sizeof(A) + sizeof(int)), st>>>(
+                fp2_part, FP2_SPLIT, fp2_best, k, np2, td, dec, fp2_order, fp2_m, fp2_swaps_prev);
+        } else {
+            const size_t psm = (size_t)k * (sizeof(A) + 1);
+            const bool pstaged = psm <= 40 * 1024;
+            km::k_fp2_plan<A><<<1, 1024, pstaged ? psm : 0, st>>>(fp2_best, k, td, dec, fp2_order, fp2_m,
+                                                                  fp2_swaps_prev, pstaged);
+        }
         KM_CKL();
-        KM_TRY(launch_fp2_sequential(nullptr, nullptr, fp2_swaps_prev));
-        ++launches;
+        f2_mark(5);
         // the outcome in ONE host wait: decision, TD, this iteration's swap
-        // count and the whole trace buffer (k records at most) into pinned memory
+        // count and trace records written by the kernel into pinned memory
         if (!h_f2out) {
             KM_CK(cudaMallocHost((void**)&h_f2out, sizeof(Rec) * (size_t)(trace_cap + 1)));
         }
-        KM_CK(cudaMemcpyAsync(h_dec, dec, sizeof(Dec), cudaMemcpyDeviceToHost, st));
-        KM_CK(cudaMemcpyAsync(h_td, td, sizeof(A), cudaMemcpyDeviceToHost, st));
-        KM_CK(cudaMemcpyAsync(h_f2out, fp2_m + 1, sizeof(int), cudaMemcpyDeviceToHost, st));
-        KM_CK(cudaMemcpyAsync(h_f2out + 1, trace, (size_t)trace_cap * sizeof(Rec), cudaMemcpyDeviceToHost, st));
+        km::F2HostOut<A> ho;
+        ho.dec = h_dec; ho.td = h_td; ho.swaps = reinterpret_cast<int*>(h_f2out); ho.trace = h_f2out + 1;
+        KM_TRY(launch_fp2_sequential(nullptr, nullptr, fp2_swaps_prev, ho));
+        ++launches;
+        f2_mark(6);
+        f2_mark(7);
         KM_CK(cudaStreamSynchronize(st));
+        f2_take();
         KM_TRY(fp2_finish_profiling());
         // this iteration's swaps: the head of the trace (the kernel counts from 0)
         int done = 0;
@@ -1108,7 +1149,8 @@ struct Impl : ImplBase {
     Rec* h_f2out = nullptr;          // pinned: [0] swaps of the iteration (int), [1..] the trace
     int* fp2_m = nullptr;            // [2]: improving slots m; swaps of the iteration
     int* fp2_swaps_prev = nullptr;
-    km_status launch_fp2_sequential(const T* colsrc, const int* colidx_dev, const int* swaps_prev_dev = nullptr) {
+    km_status launch_fp2_sequential(const T* colsrc, const int* colidx_dev, const int* swaps_prev_dev = nullptr,
+                                    km::F2HostOut<A> ho = km::F2HostOut<A>{nullptr, nullptr, nullptr, nullptr}) {
         const T* Dp = D; int64_t ldv = ld; int nn = (int)n; int kk = k;
         int* Mp = M; int* psp = point_slot; T* MCp = MC; int* nr = near; int* sc = sec; T* dnp = dn; T* dsp = ds;
         T* cb = fp2_cols; A* tdp = td; A* pp = fp2_partials; Dec* dp = dec; Rec* tr = trace; int tc = trace_cap;
@@ -1119,7 +1161,7 @@ struct Impl : ImplBase {
         int* swi = fp2_m + 1;               // swaps of this iteration (written by the kernel)
         const int* swp = swaps_prev_dev;
         void* args[] = {&Dp, &ldv, &csp, &cip, &nn, &kk, &op, &mp, &bp, &Mp, &psp, &MCp, &nr, &sc, &dnp, &dsp, &cb,
-                        &tdp, &pp, &dp, &tr, &tc, &rsp, &rcp, &symv, &swi, &swp};
+                        &tdp, &pp, &dp, &tr, &tc, &rsp, &rcp, &symv, &swi, &swp, &ho};
         KM_CK(cudaLaunchCooperativeKernel((void*)km::k_fp2_sequential<T, A>, dim3(fp2_blocks), dim3(256), args, 0,
                                           st));
         ++launches;
