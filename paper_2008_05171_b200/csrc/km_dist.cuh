@@ -78,21 +78,38 @@ __device__ __forceinline__ int dt_off(int r, int k, int kc) {
 // |y|^2.  The operands are therefore x - mu, mu = the per-dimension mean of
 // all n points (fp64 sums in a fixed order, rounded to f32; any mu is exact
 // in the mathematics, the rounding of x - mu costs 2^-24 |x - mu|).
-// grid = d blocks: block t sums dimension t.
-__global__ void k_dist_mean(const float* __restrict__ X, int n, int d, float* __restrict__ mu) {
-    __shared__ double ws[8];
-    const int t = blockIdx.x;
+// Two launches, fixed order: block b of DM_BLOCKS sums rows [b n / B,
+// (b + 1) n / B) (thread (ty, tx): dimension tx, rows ty, ty + lanes, ...;
+// coalesced), its lanes combined in ty order -> part[b][t]; then one thread
+// per dimension adds the B partials in block order.  (Round 2's first form,
+// one block per dimension with strided loads, took 40-90 us at C3 / C4.)
+constexpr int DM_BLOCKS = 256;
+__global__ void __launch_bounds__(256) k_dist_mean_part(const float* __restrict__ X, int n, int d,
+                                                        double* __restrict__ part) {
+    __shared__ double ws[256];
+    const int lanes = (int)blockDim.x / d;
+    const int tx = threadIdx.x % d, ty = threadIdx.x / d;
+    const int64_t r0 = (int64_t)blockIdx.x * n / gridDim.x, r1 = (int64_t)(blockIdx.x + 1) * n / gridDim.x;
     double s = 0;
-    for (int i = threadIdx.x; i < n; i += blockDim.x) s += (double)X[(int64_t)i * d + t];
-#pragma unroll
-    for (int x = 16; x >= 1; x >>= 1) s += __shfl_xor_sync(FULL, s, x);
-    if ((threadIdx.x & 31) == 0) ws[threadIdx.x >> 5] = s;
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        double a = 0;
-        for (int w = 0; w < (int)(blockDim.x >> 5); ++w) a += ws[w];
-        mu[t] = (float)(a / (double)n);
+    if (ty < lanes) {
+#pragma unroll 4
+        for (int64_t i = r0 + ty; i < r1; i += lanes) s += (double)X[i * d + tx];
     }
+    ws[threadIdx.x] = s;
+    __syncthreads();
+    if ((int)threadIdx.x < d) {
+        double a = 0;
+        for (int y = 0; y < lanes; ++y) a += ws[y * d + threadIdx.x];
+        part[(int64_t)blockIdx.x * d + threadIdx.x] = a;
+    }
+}
+__global__ void k_dist_mean_fin(const double* __restrict__ part, int nb, int n, int d, float* __restrict__ mu) {
+    const int t = threadIdx.x;
+    if (t >= d) return;
+    double a = 0;
+#pragma unroll 8
+    for (int b = 0; b < nb; ++b) a += part[(int64_t)b * d + t];
+    mu[t] = (float)(a / (double)n);
 }
 
 __device__ __forceinline__ float dt_centered(const float* X, const float* mu, int64_t j, int d, int k) {

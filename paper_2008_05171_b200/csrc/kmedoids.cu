@@ -3059,7 +3059,7 @@ km_status kmedoids_dissimilarity(const void* X, km_metric metric, int64_t n, int
         const bool same = (col_begin == 0);
         const int64_t TF = ws ? km::dw_tile_floats(dpad) : km::dt_tile_floats(dpad);
         const size_t nrm_floats = (size_t)cdiv(n, 64) * 64;          // keeps the packed tiles 256-byte aligned
-        const size_t mu_floats = 64;                                 // d <= 64
+        const size_t mu_floats = 64 + 2 * (size_t)km::DM_BLOCKS * 64;  // mu (d <= 64) + the fp64 block partials
         const size_t raw_floats = fixup ? (size_t)nm * RFl + (same ? 0 : (size_t)ntc * RFl) : 0;
         const size_t scratch = nrm_floats + (size_t)nm * TF + (same ? 0 : (size_t)ntc * TF) + mu_floats + raw_floats;
         // persistent per-device scratch (norms + packed operands), grown on
@@ -3075,7 +3075,11 @@ km_status kmedoids_dissimilarity(const void* X, km_metric metric, int64_t n, int
         float* RB = same ? RA : RA + nm * RFl;
         const char* ec = getenv("KM_DIST_CENTER");       // measurement override: 0 = no centring
         const bool center = !(ec && ec[0] == '0');
-        if (center) km::k_dist_mean<<<(unsigned)d, 256, 0, st>>>((const float*)X, (int)n, d, mu);
+        if (center) {
+            double* mpart = reinterpret_cast<double*>(mu + 64);
+            km::k_dist_mean_part<<<km::DM_BLOCKS, 256, 0, st>>>((const float*)X, (int)n, d, mpart);
+            km::k_dist_mean_fin<<<1, 64, 0, st>>>(mpart, km::DM_BLOCKS, (int)n, d, mu);
+        }
         const float* mup = center ? mu : nullptr;
         km::k_dist_norms<<<(unsigned)cdiv(n, 256), 256, 0, st>>>((const float*)X, mup, (int)n, d, nrm);
         // work items (row tile x column range): at least 8 per SM for balance
