@@ -116,6 +116,18 @@ __device__ __forceinline__ void post_stamp(unsigned long long* tph, int i) {
     }
 }
 
+// One iteration outcome into the pinned ring: the payload, a system-scope
+// fence, then the sequence number (a host poller that sees seq == q reads a
+// complete entry).
+template <typename A>
+__device__ __forceinline__ void ring_put(IterMirror<A>& m, const Decision<A>& d, A td, int q, int noop) {
+    m.d = d;
+    m.td = td;
+    m.noop = noop;
+    __threadfence_system();
+    *reinterpret_cast<volatile int*>(&m.seq) = q;
+}
+
 template <typename T, typename A>
 __global__ void __launch_bounds__(POST_THREADS, 3)
 k_fp1_post(PostArgs<T, A> g) {
@@ -145,7 +157,7 @@ k_fp1_post(PostArgs<T, A> g) {
                 Decision<A> dd = *g.dec;
                 dd.apply = 0;
                 const int q = *g.seq;
-                if (g.h_ring) { IterMirror<A>& m = g.h_ring[q % g.ring]; m.d = dd; m.td = *g.td; m.seq = q; m.noop = 1; }
+                if (g.h_ring) ring_put(g.h_ring[q % g.ring], dd, *g.td, q, 1);
                 *g.seq = q + 1;
             }
             return;
@@ -626,9 +638,10 @@ k_fp1_post(PostArgs<T, A> g) {
         *g.rescan_count = 0;
         if (!g.prep_only) {
             // the outcome straight into pinned host memory (visible to the host
-            // once the launch's completion event is observed)
+            // once the launch's completion event is observed, or once it
+            // reads seq == q: seq is written last, behind a system fence)
             const int q = *g.seq;
-            if (g.h_ring) { IterMirror<A>& m = g.h_ring[q % g.ring]; m.d = sdec; m.td = *g.td; m.seq = q; m.noop = 0; }
+            if (g.h_ring) ring_put(g.h_ring[q % g.ring], sdec, *g.td, q, 0);
             *g.seq = q + 1;
         }
     }

@@ -3,6 +3,7 @@
 // km_kernels.cuh; this file only validates arguments, owns scratch buffers,
 // enqueues kernels on the handle's stream and copies the per-iteration
 // decision (one 32-byte record) back to the host for the convergence test.
+#include <atomic>
 #include <cstdarg>
 #include <cstdlib>
 #include <cstdio>
@@ -216,7 +217,13 @@ struct Impl : ImplBase {
     cudaEvent_t ev0 = nullptr, ev1 = nullptr;
 
     ~Impl() override {
-        for (auto& sl : clara_slots) { sl.sub.reset(); if (sl.stream) cudaStreamDestroy(sl.stream); }
+        for (auto& sl : clara_slots) {
+            sl.sub.reset();
+            if (sl.stream) cudaStreamDestroy(sl.stream);
+            if (sl.fin) cudaEventDestroy(sl.fin);
+            if (sl.h_med) cudaFreeHost(sl.h_med);
+            if (sl.h_td) cudaFreeHost(sl.h_td);
+        }
         for (auto& g : fp1_g) if (g) cudaGraphExecDestroy(g);
         for (auto& p : g_ev) for (auto e : p) if (e) cudaEventDestroy(e);
         for (auto e : g_done) if (e) cudaEventDestroy(e);
@@ -872,7 +879,7 @@ struct Impl : ImplBase {
             ev_a = ev_b = nullptr;
             KM_TRY(s2);
         }
-        KM_CK(cudaEventRecord(g_done[gi], st));
+        if (!fp1_ring_polled) KM_CK(cudaEventRecord(g_done[gi], st));
         ++fp1_seq;
         ++fp1_iters;
         fp1_any_done = true;
@@ -934,6 +941,67 @@ struct Impl : ImplBase {
         if (iters_out) *iters_out = done_it;
         if (swaps_out) *swaps_out = sw;
         if (converged) *converged = conv;
+        return KM_OK;
+    }
+
+    // The same loop split for a host thread that drives several handles at
+    // once (FastCLARA samples, one stream each): fp1_async_begin queues the
+    // first two iterations, fp1_async_poll collects every finished one
+    // without blocking (cudaEventQuery on its completion event) and queues
+    // the next; *finished once a pass without an improving swap (or
+    // max_iter passes) has been collected.  Work enqueued on the handle's
+    // stream afterwards is ordered behind the queued no-op iteration.
+    // Completion is seen in the pinned ring itself (the post kernel writes
+    // the entry's seq last, behind a system fence): no event record per
+    // launch, no event query per poll.
+    struct Fp1Async { int64_t next = 0, launched = 0; int32_t max_iter = 0, done_it = 0, sw = 0; bool conv = false;
+                      int misses = 0; };
+    Fp1Async fa;
+    bool fp1_ring_polled = false;           // launches record no g_done event (fp1_async_*)
+    km_status fp1_async_begin(int32_t max_iter) {
+        if (sharded) return fail(KM_EINVAL, "swap iterations on a sharded handle; use the kmedoids_shard_* phases");
+        if (!ready) return fail(KM_EINVAL, "no medoids: call kmedoids_set_medoids or kmedoids_init_build first");
+        KM_TRY(fp1_ring_alloc());
+        fp1_ring_polled = true;
+        fa = Fp1Async();
+        fa.next = fp1_seq;
+        fa.max_iter = max_iter;
+        while (fa.launched < max_iter && fp1_seq - fa.next < 2) {
+            KM_TRY(fp1_launch());
+            ++fa.launched;
+        }
+        return KM_OK;
+    }
+    km_status fp1_async_poll(bool* finished) {
+        *finished = false;
+        while (fa.done_it < fa.max_iter && !fa.conv) {
+            const km::IterMirror<A>& m = h_ring[fa.next % RING];
+            if (*reinterpret_cast<const volatile int32_t*>(&m.seq) != (int32_t)fa.next) {
+                // not written yet: every 256th miss, check that the stream is
+                // still working on it (a fault or an idle stream is an error)
+                if (++fa.misses % 256 == 0) {
+                    const cudaError_t q = cudaStreamQuery(st);
+                    if (q == cudaSuccess && *reinterpret_cast<const volatile int32_t*>(&m.seq) != (int32_t)fa.next)
+                        return fail(KM_ECUDA, "iteration ring out of step (%d vs %lld)", m.seq, (long long)fa.next);
+                    if (q != cudaSuccess && q != cudaErrorNotReady)
+                        return fail(KM_ECUDA, "FastPAM1 iteration: %s", cudaGetErrorString(q));
+                }
+                return KM_OK;
+            }
+            std::atomic_thread_fence(std::memory_order_acquire);
+            *h_dec = m.d;
+            *h_td = m.td;
+            ++fa.next;
+            ++fa.done_it;
+            if (h_dec->apply) ++fa.sw; else fa.conv = true;
+            while (!fa.conv && fa.launched < fa.max_iter && fp1_seq - fa.next < 2) {
+                KM_TRY(fp1_launch());
+                ++fa.launched;
+            }
+        }
+        fp1_result(nullptr, nullptr);
+        fp1_ring_polled = false;
+        *finished = true;
         return KM_OK;
     }
 
@@ -1876,6 +1944,12 @@ struct Impl : ImplBase {
     struct ClaraSlot {
         T* buf = nullptr;
         int* idx = nullptr;
+        int* med = nullptr;                 // the sample's medoids as object indices
+        A* part = nullptr;                  // TD block sums
+        A* tdv = nullptr;
+        int* h_med = nullptr;               // pinned: the sample's result
+        A* h_td = nullptr;
+        cudaEvent_t fin = nullptr;          // recorded behind the sample's TD pass
         cudaStream_t stream = nullptr;
         std::unique_ptr<Impl<T>> sub;
     };
@@ -1909,6 +1983,12 @@ struct Impl : ImplBase {
             ClaraSlot sl;
             KM_TRY(alloc(&sl.buf, (size_t)s * lds));
             KM_TRY(alloc(&sl.idx, s));
+            KM_TRY(alloc(&sl.med, k));
+            KM_TRY(alloc(&sl.part, cdiv(n, 256)));
+            KM_TRY(alloc(&sl.tdv, 1));
+            KM_CK(cudaMallocHost(&sl.h_med, (size_t)k * sizeof(int)));
+            KM_CK(cudaMallocHost(&sl.h_td, sizeof(A)));
+            KM_CK(cudaEventCreateWithFlags(&sl.fin, cudaEventDisableTiming));
             KM_CK(cudaStreamCreateWithFlags(&sl.stream, cudaStreamNonBlocking));
             KM_CK(cudaMemsetAsync(sl.buf, 0, (size_t)s * lds * sizeof(T), sl.stream));
             sl.sub.reset(new Impl<T>());
@@ -1945,23 +2025,110 @@ struct Impl : ImplBase {
                 if (r != KM_OK) errs[j] = g_err;
             }
         };
-        {
+        std::vector<A> tds((size_t)ns);
+        const int tdb = (int)cdiv(n, 256);
+        if (v == KM_FASTPAM1) {
+            // ONE host thread drives the samples, `conc` at a time, each on
+            // its slot's stream (as kmedoids_clara_points): sub-matrix gather,
+            // BUILD and the first two iterations enqueued at once, finished
+            // iterations collected by event queries and the next queued,
+            // then the medoids as object indices and their TD over all n
+            // objects (Eq. eqn:td) into pinned memory behind the converging
+            // pass.
+            std::vector<int> cur((size_t)conc, -1), phase((size_t)conc, 0);
+            int nextj = 0, left = ns, rj = -1;
+            km_status r = KM_OK;
+            while (left > 0 && r == KM_OK) {
+                bool progress = false;
+                for (int si = 0; si < conc && r == KM_OK; ++si) {
+                    ClaraSlot& sl = clara_slots[si];
+                    Impl<T>& sub = *sl.sub;
+                    const int j = cur[si];
+                    auto ck = [&](cudaError_t e, const char* what) {
+                        if (r == KM_OK && e != cudaSuccess) r = fail(KM_ECUDA, "%s: %s", what, cudaGetErrorString(e));
+                    };
+                    if (j < 0) {
+                        if (nextj >= ns) continue;
+                        const int jj = nextj++;
+                        cur[si] = jj;
+                        rj = jj;
+                        ck(cudaMemcpyAsync(sl.idx, samples + (size_t)jj * s, s * sizeof(int32_t), cudaMemcpyHostToDevice,
+                                           sl.stream), "sample indices");
+                        if (r == KM_OK) {
+                            km::k_gather_submatrix<T><<<dim3((unsigned)cdiv(s, 256), (unsigned)s), 256, 0, sl.stream>>>(
+                                D, ld, sl.idx, s, sl.buf, lds);
+                            ck(cudaGetLastError(), "sample gather");
+                        }
+                        sub.build_async = true;
+                        if (r == KM_OK) r = sub.init_build(nullptr, nullptr);
+                        sub.build_async = false;
+                        if (r == KM_OK) r = sub.fp1_async_begin(2000);
+                        phase[si] = 1;
+                        progress = true;
+                    } else if (phase[si] == 1) {
+                        bool fin = false;
+                        rj = j;
+                        r = sub.fp1_async_poll(&fin);
+                        if (r != KM_OK || !fin) continue;
+                        km::k_map_sample_medoids<<<1, 256, 0, sl.stream>>>(sub.M, sl.idx, k, sl.med);
+                        km::k_td_cols<T, A><<<tdb, 256, (size_t)k * sizeof(int), sl.stream>>>(D, ld, (int)n, sl.med, k,
+                                                                                               sl.part);
+                        km::k_sum_partials<A><<<1, 32, 0, sl.stream>>>(sl.part, tdb, sl.tdv);
+                        ck(cudaGetLastError(), "sample TD");
+                        ck(cudaMemcpyAsync(sl.h_med, sl.med, k * sizeof(int32_t), cudaMemcpyDeviceToHost, sl.stream), "medoids");
+                        ck(cudaMemcpyAsync(sl.h_td, sl.tdv, sizeof(A), cudaMemcpyDeviceToHost, sl.stream), "TD");
+                        ck(cudaEventRecord(sl.fin, sl.stream), "sample event");
+                        phase[si] = 2;
+                        progress = true;
+                    } else {
+                        rj = j;
+                        const cudaError_t q = cudaEventQuery(sl.fin);
+                        if (q == cudaErrorNotReady) continue;
+                        ck(q, "sample");
+                        if (r != KM_OK) continue;
+                        memcpy(Mg[j].data(), sl.h_med, k * sizeof(int32_t));
+                        tds[j] = *sl.h_td;
+                        cur[si] = -1;
+                        --left;
+                        progress = true;
+                    }
+                }
+                if (!progress) std::this_thread::yield();
+            }
+            if (r != KM_OK) {
+                const std::string msg = g_err;
+                for (int si = 0; si < conc; ++si) {
+                    cudaStreamSynchronize(clara_slots[si].stream);
+                    clara_slots[si].sub->fp1_ring_polled = false;
+                }
+                cudaGetLastError();
+                return fail(r, "CLARA sample %d: %s", rj, msg.c_str());
+            }
+        } else {
+            // FastPAM2 / FasterPAM iterations wait on the host inside
+            // swap_iter: one worker thread per slot keeps the samples
+            // concurrent; the TD of each sample's medoids by the same pass
             std::vector<std::thread> th;
             for (int t = 1; t < conc; ++t) th.emplace_back(worker, t);
             worker(0);
             for (auto& x : th) x.join();
+            for (int j = 0; j < ns; ++j)
+                if (res[j] != KM_OK) return fail(res[j], "CLARA sample %d: %s", j, errs[j].c_str());
+            ClaraSlot& sl = clara_slots[0];
+            for (int j = 0; j < ns; ++j) {
+                KM_CK(cudaMemcpyAsync(sl.med, Mg[j].data(), k * sizeof(int32_t), cudaMemcpyHostToDevice, sl.stream));
+                km::k_td_cols<T, A><<<tdb, 256, (size_t)k * sizeof(int), sl.stream>>>(D, ld, (int)n, sl.med, k, sl.part);
+                km::k_sum_partials<A><<<1, 32, 0, sl.stream>>>(sl.part, tdb, sl.tdv);
+                KM_CKL();
+                KM_CK(cudaMemcpyAsync(sl.h_td, sl.tdv, sizeof(A), cudaMemcpyDeviceToHost, sl.stream));
+                KM_CK(cudaStreamSynchronize(sl.stream));
+                tds[j] = *sl.h_td;
+            }
         }
-        for (int j = 0; j < ns; ++j)
-            if (res[j] != KM_OK) return fail(res[j], "CLARA sample %d: %s", j, errs[j].c_str());
         for (auto& sl : clara_slots) { launches += sl.sub->launches + 1; sl.sub->launches = 0; }
-        A best_td = km::amax<A>();
-        int best_j = -1;
-        for (int j = 0; j < ns; ++j) {
-            KM_TRY(set_medoids(Mg[j].data()));          // TD over all n objects (Eq. eqn:td)
-            A tdj;
-            KM_CK(cudaMemcpy(&tdj, td, sizeof(A), cudaMemcpyDeviceToHost));
-            if (best_j < 0 || tdj < best_td) { best_td = tdj; best_j = j; }
-        }
+        int best_j = 0;
+        for (int j = 1; j < ns; ++j)
+            if (tds[j] < tds[best_j]) best_j = j;       // smallest (TD, sample index)
         KM_TRY(set_medoids(Mg[best_j].data()));
         if (M_out) memcpy(M_out, Mg[best_j].data(), k * sizeof(int32_t));
         if (best_out) *best_out = best_j;
@@ -2168,11 +2335,13 @@ struct Impl : ImplBase {
             KM_TRY(build_steps());
         }
         build_finish_host();                     // host-side state (not part of a graph replay)
+        if (build_async && !M_out && !td_out) return KM_OK;   // stream-ordered (CLARA's single-thread driver)
         KM_CK(cudaStreamSynchronize(st));
         if (M_out) KM_CK(cudaMemcpy(M_out, M, k * sizeof(int32_t), cudaMemcpyDeviceToHost));
         copy_td(td_out);
         return KM_OK;
     }
+    bool build_async = false;               // init_build without the closing host wait (no outputs requested)
     bool build_attr_set = false;
     int64_t build_graph_kernels = 0;
     int build_calls = 0;
@@ -2581,6 +2750,8 @@ struct ClaraPointsCache {
     using A = typename km::Acc<T>::type;
     struct Slot {
         T* buf = nullptr; int* idx = nullptr; int* med = nullptr; A* part = nullptr; A* tdv = nullptr;
+        int* h_med = nullptr; A* h_td = nullptr;       // pinned: the sample's result
+        cudaEvent_t fin = nullptr;                     // recorded behind the sample's TD pass
         cudaStream_t st = nullptr; std::unique_ptr<Impl<T>> sub;
     };
     std::mutex mu;
@@ -2594,7 +2765,9 @@ struct ClaraPointsCache {
         for (auto& sl : slots) {
             sl.sub.reset();
             if (sl.st) cudaStreamDestroy(sl.st);
+            if (sl.fin) cudaEventDestroy(sl.fin);
             cudaFree(sl.buf); cudaFree(sl.idx); cudaFree(sl.med); cudaFree(sl.part); cudaFree(sl.tdv);
+            cudaFreeHost(sl.h_med); cudaFreeHost(sl.h_td);
         }
         if (dev >= 0 && dev != cur) cudaSetDevice(cur);
         slots.clear();
@@ -2628,9 +2801,13 @@ km_status clara_points_run(const void* Xv, int64_t n, int32_t d, int32_t k, int3
     }
     const int64_t lds = cdiv(s, 4) * 4;
     const int conc = std::min(ns, 8);
-    const int tdb = (int)cdiv(n, 256);                      // k_td_points blocks
-    const int kc = std::max(1, std::min<int>(k, (46 * 1024) / (int)(d * sizeof(P))));   // < 48 KB with the statics
-    const size_t td_smem = (size_t)kc * d * sizeof(P);
+    const int tdb = (int)cdiv(n, km::TDP_THREADS);          // k_td_points blocks
+    // medoid rows per chunk (widened): the staged objects plus kc rows in 96 KB
+    const int kc = std::max(1, std::min<int>(k, (int)((96 * 1024 - km::td_points_xs_bytes<T>(d)) /
+                                                      ((size_t)d * sizeof(typename km::PointWide<T>::type)))));
+    const size_t td_smem = km::td_points_smem<T>(d, kc);
+    const size_t sd_smem = 64 * (size_t)km::clara_row_stride(d) * sizeof(P);   // k_subdist_exact
+    KM_CK(cudaFuncSetAttribute(km::k_td_points<T, A>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)td_smem));
     // the per-sample slots (stream, s x s buffer, nested handle) are kept
     // between calls with the same (device, s, k, n) so a handle's BUILD is
     // replayed from its CUDA graph on later samples and calls
@@ -2654,6 +2831,9 @@ km_status clara_points_run(const void* Xv, int64_t n, int32_t d, int32_t k, int3
         if (e == cudaSuccess) e = cudaMalloc(&sl.med, (size_t)k * sizeof(int));
         if (e == cudaSuccess) e = cudaMalloc(&sl.part, (size_t)tdb * sizeof(A));
         if (e == cudaSuccess) e = cudaMalloc(&sl.tdv, sizeof(A));
+        if (e == cudaSuccess) e = cudaMallocHost(&sl.h_med, (size_t)k * sizeof(int));
+        if (e == cudaSuccess) e = cudaMallocHost(&sl.h_td, sizeof(A));
+        if (e == cudaSuccess) e = cudaEventCreateWithFlags(&sl.fin, cudaEventDisableTiming);
         if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&sl.st, cudaStreamNonBlocking);
         if (e == cudaSuccess) e = cudaMemsetAsync(sl.buf, 0, (size_t)s * lds * sizeof(T), sl.st);
         if (e != cudaSuccess) { cleanup(); cudaGetLastError(); return fail(KM_ENOMEM, "CLARA scratch: %s", cudaGetErrorString(e)); }
@@ -2677,7 +2857,7 @@ km_status clara_points_run(const void* Xv, int64_t n, int32_t d, int32_t k, int3
             ck(cudaMemcpyAsync(sl.idx, S, s * sizeof(int32_t), cudaMemcpyHostToDevice, sl.st), "sample indices");
             if (r == KM_OK) {
                 const dim3 g((unsigned)cdiv(s, 32), (unsigned)cdiv(s, 32));
-                km::k_subdist_exact<T><<<g, 256, 64 * (size_t)d * sizeof(P), sl.st>>>(X, d, sl.idx, s, sl.buf, lds);
+                km::k_subdist_exact<T><<<g, 256, sd_smem, sl.st>>>(X, d, sl.idx, s, sl.buf, lds);
                 ck(cudaGetLastError(), "sample dissimilarities");
             }
             if (r == KM_OK) r = sub.init_build(nullptr, nullptr);
@@ -2700,7 +2880,7 @@ km_status clara_points_run(const void* Xv, int64_t n, int32_t d, int32_t k, int3
                 // TD over all n objects from the points (Eq. eqn:td, reading C2)
                 ck(cudaMemcpyAsync(sl.med, Mg[j].data(), k * sizeof(int32_t), cudaMemcpyHostToDevice, sl.st), "medoids");
                 if (r == KM_OK) {
-                    km::k_td_points<T, A><<<tdb, 256, td_smem, sl.st>>>(X, (int)n, d, sl.med, k, kc, sl.part, nullptr);
+                    km::k_td_points<T, A><<<tdb, km::TDP_THREADS, td_smem, sl.st>>>(X, (int)n, d, sl.med, k, kc, sl.part, nullptr);
                     km::k_sum_partials<A><<<1, 32, 0, sl.st>>>(sl.part, tdb, sl.tdv);
                     ck(cudaGetLastError(), "TD from points");
                 }
@@ -2713,7 +2893,85 @@ km_status clara_points_run(const void* Xv, int64_t n, int32_t d, int32_t k, int3
             if (r != KM_OK) errs[j] = g_err;
         }
     };
-    {
+    if (variant == KM_FASTPAM1) {
+        // ONE host thread drives the samples, `conc` at a time, each on its
+        // slot's stream: sample indices, s x s dissimilarities, BUILD and the
+        // first two FastPAM1 iterations are enqueued at once; finished
+        // iterations are collected by event queries (never a blocking wait)
+        // and the next queued; behind the converging pass the medoids are
+        // mapped to object indices and the TD over all n objects computed,
+        // then copied into pinned memory (the slot's `fin` event).
+        std::vector<int> cur((size_t)conc, -1), phase((size_t)conc, 0);
+        int nextj = 0, left = ns;
+        km_status r = KM_OK;
+        int rj = -1;
+        while (left > 0 && r == KM_OK) {
+            bool progress = false;
+            for (int si = 0; si < conc && r == KM_OK; ++si) {
+                Slot& sl = slots[si];
+                Impl<T>& sub = *sl.sub;
+                const int j = cur[si];
+                auto ck = [&](cudaError_t e, const char* what) {
+                    if (r == KM_OK && e != cudaSuccess) { r = fail(KM_ECUDA, "%s: %s", what, cudaGetErrorString(e)); rj = j; }
+                };
+                if (j < 0) {
+                    if (nextj >= ns) continue;
+                    const int jj = nextj++;
+                    cur[si] = jj;
+                    rj = jj;
+                    const int32_t* S = samples + (size_t)jj * s;
+                    ck(cudaMemcpyAsync(sl.idx, S, s * sizeof(int32_t), cudaMemcpyHostToDevice, sl.st), "sample indices");
+                    if (r == KM_OK) {
+                        const dim3 g((unsigned)cdiv(s, 32), (unsigned)cdiv(s, 32));
+                        km::k_subdist_exact<T><<<g, 256, sd_smem, sl.st>>>(X, d, sl.idx, s, sl.buf, lds);
+                        ck(cudaGetLastError(), "sample dissimilarities");
+                    }
+                    sub.build_async = true;
+                    if (r == KM_OK) r = sub.init_build(nullptr, nullptr);
+                    sub.build_async = false;
+                    if (r == KM_OK) r = sub.fp1_async_begin(2000);
+                    phase[si] = 1;
+                    progress = true;
+                } else if (phase[si] == 1) {
+                    bool fin = false;
+                    rj = j;
+                    r = sub.fp1_async_poll(&fin);
+                    if (r != KM_OK || !fin) continue;
+                    // the medoids as object indices, the TD over all n objects
+                    // (Eq. eqn:td, reading C2), both into pinned memory
+                    km::k_map_sample_medoids<<<1, 256, 0, sl.st>>>(sub.M, sl.idx, k, sl.med);
+                    km::k_td_points<T, A><<<tdb, km::TDP_THREADS, td_smem, sl.st>>>(X, (int)n, d, sl.med, k, kc, sl.part, nullptr);
+                    km::k_sum_partials<A><<<1, 32, 0, sl.st>>>(sl.part, tdb, sl.tdv);
+                    ck(cudaGetLastError(), "TD from points");
+                    ck(cudaMemcpyAsync(sl.h_med, sl.med, k * sizeof(int32_t), cudaMemcpyDeviceToHost, sl.st), "medoids");
+                    ck(cudaMemcpyAsync(sl.h_td, sl.tdv, sizeof(A), cudaMemcpyDeviceToHost, sl.st), "TD");
+                    ck(cudaEventRecord(sl.fin, sl.st), "sample event");
+                    phase[si] = 2;
+                    progress = true;
+                } else {
+                    const cudaError_t q = cudaEventQuery(sl.fin);
+                    if (q == cudaErrorNotReady) continue;
+                    ck(q, "sample");
+                    if (r != KM_OK) continue;
+                    memcpy(Mg[j].data(), sl.h_med, k * sizeof(int32_t));
+                    tds[j] = *sl.h_td;
+                    cur[si] = -1;
+                    --left;
+                    progress = true;
+                }
+            }
+            if (!progress) std::this_thread::yield();
+        }
+        if (r != KM_OK) {
+            const std::string msg = g_err;
+            for (int si = 0; si < conc; ++si) cudaStreamSynchronize(slots[si].st);
+            cleanup();
+            cudaGetLastError();
+            return fail(r, "CLARA sample %d: %s", rj, msg.c_str());
+        }
+    } else {
+        // FastPAM2 / FasterPAM iterations wait on the host inside swap_iter:
+        // one worker thread per slot keeps the samples concurrent
         std::vector<std::thread> th;
         for (int t = 1; t < conc; ++t) th.emplace_back(worker, t);
         worker(0);
@@ -2731,7 +2989,7 @@ km_status clara_points_run(const void* Xv, int64_t n, int32_t d, int32_t k, int3
         cudaError_t e = cudaMalloc(&asg, (size_t)n * sizeof(int));
         if (e == cudaSuccess) e = cudaMemcpyAsync(sl.med, Mg[bj].data(), k * sizeof(int32_t), cudaMemcpyHostToDevice, sl.st);
         if (e == cudaSuccess) {
-            km::k_td_points<T, A><<<tdb, 256, td_smem, sl.st>>>(X, (int)n, d, sl.med, k, kc, sl.part, asg);
+            km::k_td_points<T, A><<<tdb, km::TDP_THREADS, td_smem, sl.st>>>(X, (int)n, d, sl.med, k, kc, sl.part, asg);
             e = cudaGetLastError();
         }
         if (e == cudaSuccess) e = cudaMemcpyAsync(asg_out, asg, (size_t)n * sizeof(int), cudaMemcpyDeviceToHost, sl.st);

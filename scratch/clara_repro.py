@@ -3,6 +3,8 @@ FasterPAM, three calls each (as bench.py), repeated R times."""
 import os
 import sys
 
+import time
+
 import numpy as np
 import torch
 
@@ -22,6 +24,9 @@ samples = np.stack([crng.choice(n, size=s_cl, replace=False) for _ in range(NS)]
 for r in range(R):
     for v in ("fastpam1", "fasterpam"):
         for _ in range(3):
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
             M, td, b, _ = kmedoids_clara_points(Xt, "l2", k, samples, v)
-    print("rep", r, "td", td, "best", b, flush=True)
+            ms = (time.perf_counter() - t0) * 1e3
+        print("rep", r, v, "td", td, "best", b, f"third call {ms:.2f} ms", flush=True)
 print("clara repro ok", flush=True)
