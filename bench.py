@@ -520,8 +520,11 @@ def run_sharded(args):
     cb = parallel.column_bounds(n, world)
     X = kmsynth.make_points(cfg)
     Dt = kmsynth.dist_cuda(X, cfg.metric, int(cb[rank]), int(cb[rank + 1]))
-    stream = torch.cuda.current_stream()
     fp2 = args.variant == "fastpam2"
+    use_graph = not fp2 and not args.no_graph
+    # the iteration graph is captured on the handle's stream, which must not be
+    # the legacy default stream
+    stream = torch.cuda.Stream() if use_graph else torch.cuda.current_stream()
 
     def job(D_slab):
         h = parallel.CudaShard(D_slab, n, k, rank, cb, stream=stream)
@@ -548,21 +551,42 @@ def run_sharded(args):
 
     for _ in range(args.warmup):
         step(h)
-    h.km.set_profiling(True)
-    h.km.stream_time(reset=True)
+    graph = None
+    if use_graph:
+        # FastPAM1: the whole device-decided iteration (eval, all-gather,
+        # decide, all-reduce, apply) captured once with its NCCL calls and
+        # replayed per step (parallel.IterationGraph)
+        graph = parallel.IterationGraph([h], comm)
+    else:
+        h.km.set_profiling(True)
+        h.km.stream_time(reset=True)
     l0 = h.km.launch_count()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     torch.cuda.synchronize()
     dist.barrier()
     with ClockSampler(local) as clk:
         e0.record(stream)
-        for _ in range(args.steps):
-            step(h)
+        if graph is not None:
+            graph.replay(args.steps)
+        else:
+            for _ in range(args.steps):
+                step(h)
         e1.record(stream)
         torch.cuda.synchronize()
     dist.barrier()
     ms = comm.max_over_ranks(e0.elapsed_time(e1))
-    launches = h.km.launch_count() - l0
+    if graph is not None:
+        graph.resync()
+        launches = args.steps * graph.kernels_per_iter[0]
+        # the stream kernel's time: CUDA events around it over a few directly
+        # enqueued iterations right after the timed replays (same state)
+        h.km.set_profiling(True)
+        h.km.stream_time(reset=True)
+        for _ in range(3):
+            step(h)
+        torch.cuda.synchronize()
+    else:
+        launches = h.km.launch_count() - l0
     k1_ms, k1_n = h.km.stream_time(reset=True)
     k1_ms = comm.max_over_ranks(k1_ms)
     h.km.set_profiling(False)
@@ -581,7 +605,8 @@ def run_sharded(args):
         torch.cuda.synchronize()
         dist.barrier()
         t1 = time.perf_counter()
-        Dd = Dh_t.to(Dt.device, non_blocking=True)
+        with torch.cuda.stream(stream):          # the handle's stream: the copy is ordered before its kernels
+            Dd = Dh_t.to(Dt.device, non_blocking=True)
         h2 = job(Dd)
         if fp2:
             it = 0
@@ -651,7 +676,8 @@ def run_sharded(args):
                                                 if traffic else None),
                              "kernel": "k_swap_stream_seg2 (rank 0 slab)", "kernel_ms": k1_avg,
                              "alg_bytes_per_launch": slab_bytes, "peak_kind": peak_kind},
-                "gpu_launches": launches, "clocks": clk.summary(), "init": {"kind": cfg.init, "s": init_s},
+                "gpu_launches": launches, "iteration_graph": graph is not None,
+                "clocks": clk.summary(), "init": {"kind": cfg.init, "s": init_s},
                 "e2e": e2e, "cpu_baseline": cpu}
         print(json.dumps(line), flush=True)
     dist.barrier()
@@ -703,6 +729,8 @@ def main():
     ap.add_argument("--config", type=int, default=4)
     ap.add_argument("--variant", default="fastpam1", choices=["fastpam1", "fastpam2"])
     ap.add_argument("--sharded", action="store_true", help="use the column-sharded path even on 1 GPU")
+    ap.add_argument("--no-graph", action="store_true",
+                    help="sharded FastPAM1: enqueue every iteration instead of replaying its CUDA graph")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-fasterpam", action="store_true")

@@ -365,6 +365,15 @@ km_status kmedoids_shard_status(km_handle* h, int32_t wait, int32_t* converged, 
                                 void* td_out);
 km_status kmedoids_shard_trace(km_handle* h, int32_t* slots_out, int32_t* cands_out, void* dtds_out, int32_t cap,
                                int32_t* count_out);
+/* After the five calls above were captured once into a CUDA graph on the
+ * handle's stream (with the caller's collectives) and the graph replayed:
+ * waits for the handle's stream and takes the number of decide steps from
+ * the device status (the host did not see the replays), so
+ * kmedoids_shard_status / kmedoids_shard_trace read the right mirror.
+ * *calls_out (may be NULL): decide steps since the last reset.  The launch
+ * counter does not count replayed kernels.  Errors: KM_EINVAL (NULL handle),
+ * KM_ECUDA. */
+km_status kmedoids_shard_resync(km_handle* h, int32_t* calls_out);
 
 /* Sharded FastPAM2 (reading R6) iteration, on every rank:
  *   1. kmedoids_fp2_shard_eval(h)      per-slot best (v_i, i, c_i) over the local

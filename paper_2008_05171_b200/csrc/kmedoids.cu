@@ -123,6 +123,7 @@ struct ImplBase {
     virtual km_status shard_decide() = 0;
     virtual km_status shard_apply_async() = 0;
     virtual km_status shard_status(int32_t wait, int32_t* conv, int32_t* iters, int32_t* swaps, void* td) = 0;
+    virtual km_status shard_resync(int32_t* calls) = 0;
     virtual km_status shard_trace(int32_t* slots, int32_t* cands, void* dtds, int32_t cap, int32_t* count) = 0;
     virtual km_status build_eval(int32_t step) = 0;
     virtual km_status build_select(const int64_t* rcb, int32_t* cand, int32_t* owner, void* gain) = 0;
@@ -2566,6 +2567,20 @@ struct Impl : ImplBase {
         ++sh_ev_count;
         return KM_OK;
     }
+    // After iterations the host did not enqueue itself (replays of a CUDA
+    // graph that captured eval / decide / apply): wait for the stream, take
+    // the decide count from the device status, forget the event ring.
+    km_status shard_resync(int32_t* calls) override {
+        if (!sh_status) KM_TRY(sh_reset());
+        KM_CK(cudaStreamSynchronize(st));
+        SStat m{};
+        KM_CK(cudaMemcpy(&m, sh_status, sizeof(SStat), cudaMemcpyDeviceToHost));
+        sh_calls = m.calls;
+        sh_ev_last = -1;
+        sh_ev_count = 0;
+        if (calls) *calls = m.calls;
+        return KM_OK;
+    }
     // wait: 0 = read the mirror as it is, 1 = after all enqueued work, 2 =
     // after the iteration BEFORE the most recently enqueued one (so the host
     // can keep one iteration queued ahead of the one it inspects)
@@ -3500,6 +3515,11 @@ km_status kmedoids_shard_status(km_handle* h, int32_t wait, int32_t* converged, 
     KM_H();
     if (wait < 0 || wait > 2) return fail(KM_EINVAL, "wait must be 0, 1 or 2");
     return h->impl->shard_status(wait, converged, n_iter, n_swaps, td_out);
+}
+
+km_status kmedoids_shard_resync(km_handle* h, int32_t* calls_out) {
+    KM_H();
+    return h->impl->shard_resync(calls_out);
 }
 
 km_status kmedoids_shard_trace(km_handle* h, int32_t* slots_out, int32_t* cands_out, void* dtds_out, int32_t cap,

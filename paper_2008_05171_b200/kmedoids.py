@@ -94,6 +94,7 @@ def load_library() -> ctypes.CDLL:
         "kmedoids_build_apply_async": [vp, i32],
         "kmedoids_shard_apply_async": [vp],
         "kmedoids_shard_status": [vp, i32, vp, vp, vp, vp],
+        "kmedoids_shard_resync": [vp, vp],
         "kmedoids_shard_trace": [vp, vp, vp, vp, i32, vp],
         "kmedoids_fp2_shard_exchange": [vp, i32, ctypes.POINTER(_Fp2Exchange)],
         "kmedoids_fp2_shard_eval": [vp],
@@ -380,6 +381,13 @@ class KMedoids:
         td = np.zeros(1, self.acc)
         _check(load_library().kmedoids_shard_status(self.h, int(wait), _p(cv), _p(it), _p(sw), _p(td)))
         return bool(cv[0]), int(it[0]), int(sw[0]), td[0].item()
+
+    def shard_resync(self) -> int:
+        """Host bookkeeping after CUDA-graph replays of the sharded iteration
+        (kmedoids_shard_resync); returns the decide steps since the reset."""
+        c = np.zeros(1, np.int32)
+        _check(load_library().kmedoids_shard_resync(self.h, _p(c)))
+        return int(c[0])
 
     def shard_trace(self, cap: int = 4096):
         """Applied swaps of the sharded run: [(slot, cand, dTD)]."""

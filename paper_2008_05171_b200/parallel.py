@@ -412,6 +412,73 @@ def run(handles, comm, cb, max_iter: int = 2000):
     return traces[0], it, conv
 
 
+class IterationGraph:
+    """The device-decided sharded FastPAM1 iteration (eval -> all-gather ->
+    decide -> all-reduce -> apply, swap_iter_async) captured ONCE into a CUDA
+    graph together with its collectives, then replayed per iteration: one
+    graph launch instead of ~10 kernel launches and two collective calls per
+    iteration.  The state lives on the device (the decision is sticky after
+    convergence), so replaying the same graph K times is K iterations.
+
+    The handles must share one non-default stream (capture cannot run on the
+    legacy default stream); profiling is switched off (its event ring is
+    host-side bookkeeping).  The capture itself executes nothing; resync()
+    after the replays brings the library's host-side counters up to date
+    (kmedoids_shard_resync) before status() / shard_trace().  Collectives:
+    any comm whose calls are stream-ordered on the handle stream
+    (LocalComm copies, TorchComm over NCCL)."""
+
+    def __init__(self, handles, comm):
+        import torch
+        st = handles[0].km.stream
+        if any(h.km.stream != st for h in handles):
+            raise ValueError("all handles of the graph must run on one stream")
+        if st == torch.cuda.default_stream(st.device):
+            raise ValueError("capture needs the handles on a non-default stream (KMedoids(..., stream=...))")
+        for h in handles:
+            # decide steps since the last set_medoids / BUILD (syncs the stream)
+            if getattr(h, "_x", None) is None or h.km.shard_resync() == 0:
+                raise ValueError("run one sharded iteration (swap_iter_async) before the capture: the exchange "
+                                 "buffers and the library's scratch are allocated on first use")
+            h.km.set_profiling(False)
+        self.handles = handles
+        self.stream = st
+        l0 = [h.km.launch_count() for h in handles]
+        torch.cuda.synchronize()
+        self.graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(self.graph, stream=st, capture_error_mode="thread_local"):
+            swap_iter_async(handles, comm)
+        # kernels of one iteration per handle (the capture counted them once)
+        self.kernels_per_iter = [h.km.launch_count() - a for h, a in zip(handles, l0)]
+
+    def replay(self, count: int = 1):
+        import torch
+        with torch.cuda.stream(self.stream):      # CUDAGraph.replay launches on the current stream
+            for _ in range(count):
+                self.graph.replay()
+
+    def resync(self):
+        """Host bookkeeping after replays; returns the decide steps per handle."""
+        return [h.km.shard_resync() for h in self.handles]
+
+
+def run_graph(handles, comm, graph: IterationGraph, max_iter: int = 2000, chunk: int = 8):
+    """Sharded FastPAM1 to convergence by graph replays, `chunk` iterations
+    between status checks (iterations after convergence are no-ops).
+    Returns (trace, n_iter, converged) as run()."""
+    conv, it, done = False, 0, 0
+    while done < max_iter and not conv:
+        c = min(chunk, max_iter - done)
+        graph.replay(c)
+        done += c
+        graph.resync()
+        conv, it, _, _ = status(handles, comm, wait=1)
+    traces = [h.shard_trace() for h in handles]
+    if any(t != traces[0] for t in traces):
+        raise RuntimeError("ranks disagree on the swap trace")
+    return traces[0], it, conv
+
+
 # ---------------------------------------------------------------------------
 # CUDA shard handle: KMedoids on a column slab + exchange tensors
 # ---------------------------------------------------------------------------

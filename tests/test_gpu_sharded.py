@@ -162,3 +162,44 @@ def test_sharded_device_decided_equals_host_decided(world, cid, n, k):
         st = h.km.get_state()
         assert st.medoids.tolist() == s.medoids.tolist()
         assert st.assignment.tolist() == s.assignment.tolist()
+
+
+@pytest.mark.parametrize("world,cid,n,k", [(2, 5, 1200, 9), (3, 1, 500, 5), (1, 4, 900, 7)])
+def test_sharded_iteration_graph_replays_equal_direct(world, cid, n, k):
+    """The device-decided iteration captured once into a CUDA graph with its
+    collectives (parallel.IterationGraph) and replayed: the same swaps,
+    iteration count and state as the directly enqueued run; replays after
+    convergence are no-ops; status / trace read correctly after resync."""
+    from paper_2008_05171_b200 import parallel
+    cfg = kmsynth.CONFIGS[cid]
+    X = kmsynth.make_points(cfg, n=n)
+    Dt = kmsynth.dist_cuda(X, cfg.metric)
+    M0 = kmsynth.random_medoids(cfg, k=k, n=n)
+    hs, cb = shards(Dt, n, k, world)
+    comm = parallel.LocalComm(world)
+    parallel.set_medoids(hs, comm, cb, M0, n)
+    t1, it1, c1 = parallel.run(hs, comm, cb)
+    s1 = [h.km.get_state() for h in hs]
+    side = torch.cuda.Stream()
+    cbs = parallel.column_bounds(n, world)
+    hg = [parallel.CudaShard(Dt[:, int(cbs[r]):], n, k, r, cbs, stream=side) for r in range(world)]
+    parallel.set_medoids(hg, comm, cbs, M0, n)
+    with pytest.raises(ValueError):
+        parallel.IterationGraph(hg, comm)          # before the first iteration
+    parallel.swap_iter_async(hg, comm)             # one direct iteration: buffers allocated
+    g = parallel.IterationGraph(hg, comm)
+    assert all(x > 0 for x in g.kernels_per_iter)
+    t2, it2, c2 = parallel.run_graph(hg, comm, g, chunk=5)
+    assert c1 and c2 and it1 == it2
+    if cfg.metric == kmsynth.L1_INT:
+        assert [(a, b, int(v)) for a, b, v in t1] == [(a, b, int(v)) for a, b, v in t2]
+    else:
+        assert [(a, b) for a, b, v in t1] == [(a, b) for a, b, v in t2]
+    g.replay(3)                                    # after convergence: no-ops
+    g.resync()
+    conv, it, sw, td = parallel.status(hg, comm, wait=1)
+    assert conv and it == it1 and sw == len(t1)
+    for h, a in zip(hg, s1):
+        st = h.km.get_state()
+        assert st.medoids.tolist() == a.medoids.tolist() and st.assignment.tolist() == a.assignment.tolist()
+        assert st.td == a.td
