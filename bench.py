@@ -551,13 +551,19 @@ def run_sharded(args):
 
     for _ in range(args.warmup):
         step(h)
-    graph = None
+    graph, graph_err = None, None
     if use_graph:
         # FastPAM1: the whole device-decided iteration (eval, all-gather,
         # decide, all-reduce, apply) captured once with its NCCL calls and
-        # replayed per step (parallel.IterationGraph)
-        graph = parallel.IterationGraph([h], comm)
-    else:
+        # replayed per step (parallel.IterationGraph); a capture the runtime
+        # refuses falls back to the enqueued iteration (reported in the line)
+        try:
+            graph = parallel.IterationGraph([h], comm)
+        except Exception as e:              # noqa: BLE001
+            graph_err = f"{type(e).__name__}: {e}"[:300]
+            print(f"[bench] iteration graph unavailable, enqueuing iterations: {graph_err}", file=sys.stderr)
+            torch.cuda.synchronize()
+    if graph is None:
         h.km.set_profiling(True)
         h.km.stream_time(reset=True)
     l0 = h.km.launch_count()
@@ -676,7 +682,7 @@ def run_sharded(args):
                                                 if traffic else None),
                              "kernel": "k_swap_stream_seg2 (rank 0 slab)", "kernel_ms": k1_avg,
                              "alg_bytes_per_launch": slab_bytes, "peak_kind": peak_kind},
-                "gpu_launches": launches, "iteration_graph": graph is not None,
+                "gpu_launches": launches, "iteration_graph": graph is not None, "iteration_graph_error": graph_err,
                 "clocks": clk.summary(), "init": {"kind": cfg.init, "s": init_s},
                 "e2e": e2e, "cpu_baseline": cpu}
         print(json.dumps(line), flush=True)
