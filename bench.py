@@ -281,16 +281,11 @@ def run_ours(args):
     torch.cuda.synchronize()
     with ClockSampler(0) as clk:
         ev[2].record(stream)
-        if args.variant == "fastpam1":
-            # K iterations queued back to back (kmedoids_swap_iters: the product's
-            # run path; each is a full pass, the host reads each outcome)
-            conv, done, swaps, td = km.swap_iters(args.steps)
-            if done != args.steps:
-                raise SystemExit(f"converged after {done} of {args.steps} timed steps; use fewer --steps")
-        else:
-            for _ in range(args.steps):
-                conv, sw, td = km.swap_iter(args.variant)
-                swaps += sw
+        # K iterations queued back to back (kmedoids_swap_iters[_variant]: the
+        # product's run path; each is a full pass, the host reads each outcome)
+        conv, done, swaps, td = km.swap_iters(args.steps, args.variant)
+        if done != args.steps:
+            raise SystemExit(f"converged after {done} of {args.steps} timed steps; use fewer --steps")
         ev[3].record(stream)
         torch.cuda.synchronize()
     total_ms = ev[2].elapsed_time(ev[3])

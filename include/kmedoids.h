@@ -154,6 +154,16 @@ km_status kmedoids_swap_iter(km_handle* h, km_variant variant, int32_t* swaps_do
  * them; any may be NULL.  Returns KM_CONVERGED if the last pass made no swap,
  * else KM_OK.  kmedoids_run uses the same path for KM_FASTPAM1.  Single GPU. */
 km_status kmedoids_swap_iters(km_handle* h, int32_t count, int32_t* iters_out, int32_t* swaps_out, void* td_out);
+/* The same for KM_FASTPAM2 (reading R6) as well as
+ * KM_FASTPAM1: up to `count` iterations, each exactly one
+ * kmedoids_swap_iter(variant), the next queued on the device while the host
+ * reads the current one's outcome from pinned memory; a FastPAM2 pass with no
+ * improving slot sets a sticky flag, so passes queued behind it plan, swap and
+ * count nothing.  Outputs and return value as kmedoids_swap_iters;
+ * kmedoids_run uses this path for both variants.  Errors: KM_EINVAL (count
+ * < 1, another variant, no medoids, sharded handle), KM_ECUDA.  Single GPU. */
+km_status kmedoids_swap_iters_variant(km_handle* h, km_variant variant, int32_t count, int32_t* iters_out,
+                                      int32_t* swaps_out, void* td_out);
 
 /* BUILD (if use_build) or the medoids already set, then SWAP iterations until
  * convergence or max_iter passes (max_iter <= 0 means 2000).  Outputs are

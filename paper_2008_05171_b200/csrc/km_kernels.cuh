@@ -1031,13 +1031,31 @@ __global__ void k_fp2_slot_reduce(int k, int split, const Rec<A>* __restrict__ p
 // improving slots before it in that order (k <= a few thousand: one block).
 // Also the iteration's decision bookkeeping (the sequential kernel counts
 // this iteration's swaps from 0, then adds the previous total back).
+// Queued FastPAM2 iterations (kmedoids_swap_iters_variant): an iteration
+// that finds no improving slot sets the sticky Decision::done (it is counted,
+// P:1390-1392); a plan kernel behind it plans nothing and counts nothing, the
+// stream behind it returns at once, and the sequential kernel restores the
+// running swap total as after any pass.
+template <typename A>
+__device__ __forceinline__ void fp2_plan_done(Decision<A>* dec, int* m_out, int* swaps_prev) {
+    *m_out = 0;
+    dec->apply = 0;
+    *swaps_prev = dec->swaps;
+    dec->swaps = 0;
+}
+
 template <typename A>
 __global__ void k_fp2_plan(const Rec<A>* __restrict__ best, int k, const A* __restrict__ td,
                            Decision<A>* __restrict__ dec, int* __restrict__ order, int* __restrict__ m_out,
-                           int* __restrict__ swaps_prev, bool staged_ok) {
-    __shared__ int s_m;
+                           int* __restrict__ swaps_prev, bool staged_ok, int sticky) {
+    __shared__ int s_m, s_done;
     extern __shared__ __align__(16) unsigned char plan_smem[];   // k values and flags (when they fit)
-    if (threadIdx.x == 0) s_m = 0;
+    if (threadIdx.x == 0) { s_m = 0; s_done = sticky ? dec->done : 0; }
+    __syncthreads();
+    if (s_done) {                              // queued behind a converged pass: a no-op (fp2_plan_done)
+        if (threadIdx.x == 0) fp2_plan_done(dec, m_out, swaps_prev);
+        return;
+    }
     const A tdv = *td;
     auto improving = [&](const Rec<A>& b) {
         if (b.slot == INT_MAX) return false;
@@ -1080,6 +1098,7 @@ __global__ void k_fp2_plan(const Rec<A>* __restrict__ best, int k, const A* __re
         dec->apply = 0;
         *swaps_prev = dec->swaps;
         dec->swaps = 0;
+        if (sticky && s_m == 0) dec->done = 1;
     }
 }
 
@@ -1095,13 +1114,17 @@ template <typename A>
 __global__ void __launch_bounds__(1024)
 k_fp2_plan_sort(const Rec<A>* __restrict__ part, int split, Rec<A>* __restrict__ best, int k, int npow2,
                 const A* __restrict__ td, Decision<A>* __restrict__ dec, int* __restrict__ order,
-                int* __restrict__ m_out, int* __restrict__ swaps_prev) {
-    __shared__ int s_m;
+                int* __restrict__ m_out, int* __restrict__ swaps_prev, int sticky) {
+    __shared__ int s_m, s_done;
     extern __shared__ __align__(16) unsigned char sort_smem[];
     A* kv = reinterpret_cast<A*>(sort_smem);
     int* ki = reinterpret_cast<int*>(sort_smem + (size_t)npow2 * sizeof(A));
-    if (threadIdx.x == 0) s_m = 0;
+    if (threadIdx.x == 0) { s_m = 0; s_done = sticky ? dec->done : 0; }
     __syncthreads();
+    if (s_done) {
+        if (threadIdx.x == 0) fp2_plan_done(dec, m_out, swaps_prev);
+        return;
+    }
     const A tdv = *td;
     for (int i = threadIdx.x; i < npow2; i += blockDim.x) {
         A v = amax<A>();
@@ -1148,6 +1171,7 @@ k_fp2_plan_sort(const Rec<A>* __restrict__ part, int split, Rec<A>* __restrict__
         dec->apply = 0;
         *swaps_prev = dec->swaps;
         dec->swaps = 0;
+        if (sticky && m == 0) dec->done = 1;
     }
 }
 

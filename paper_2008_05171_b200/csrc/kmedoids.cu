@@ -146,6 +146,7 @@ struct ImplBase {
     virtual km_status inc_iters(int32_t max_iters, int32_t* swaps, void* td_out, int32_t* iters_done,
                                 bool* converged) = 0;
     virtual km_status fp1_run_pipelined(int32_t max_iter, int32_t* iters_out, int32_t* swaps_out, bool* converged) = 0;
+    virtual km_status fp2_run_pipelined(int32_t max_iter, int32_t* iters_out, int32_t* swaps_out, bool* converged) = 0;
     virtual km_status check_diagonal() = 0;
     virtual km_status set_symmetric(int32_t on) = 0;
     bool profiling = false;
@@ -237,6 +238,9 @@ struct Impl : ImplBase {
         if (h_dec) cudaFreeHost(h_dec);
         if (h_td) cudaFreeHost(h_td);
         if (h_f2out) cudaFreeHost(h_f2out);
+        if (h_f2dec) cudaFreeHost(h_f2dec);
+        if (h_f2td) cudaFreeHost(h_f2td);
+        for (auto e : f2_done) if (e) cudaEventDestroy(e);
         for (auto e : sp_ev) if (e) cudaEventDestroy(e);
         for (auto e : f2_ev) if (e) cudaEventDestroy(e);
         for (auto e : sh_ev) if (e) cudaEventDestroy(e);
@@ -572,8 +576,9 @@ struct Impl : ImplBase {
 
     template <int NC, int RB, int S, int MINB = 2>
     km_status launch_seg(A* acc_out) {
-        return launch_seg_win<NC, RB, S, MINB>(D, w, wpad, P, o_plus, o_head, o_tail, o_imin, o_islot, acc_out);
+        return launch_seg2<NC, RB, S, MINB>(D, w, wpad, P, o_plus, o_head, o_tail, o_imin, o_islot, acc_out, f2_skip);
     }
+    const int* f2_skip = nullptr;   // queued FastPAM2 iterations: the stream returns once Decision::done is set
 
     // The stream over the column window [Dw, Dw + ww) of the slab (Dw 16-byte
     // aligned) with Pw row parts; outputs indexed [part][column of window].
@@ -1178,44 +1183,120 @@ struct Impl : ImplBase {
             const std::vector<int> order = fp2_order_slots(tdh);
             return fp2_sequential(order, nullptr, nullptr, swaps_out, td_out);
         }
-        f2_mark(4);
-        if (sort_plan) {
-            int np2 = 2;
-            while (np2 < k) np2 <<= 1;
-            km::k_fp2_plan_sort<A><<<1, 1024, (size_t)np2 * (sizeof(A) + sizeof(int)), st>>>(
-                fp2_part, FP2_SPLIT, fp2_best, k, np2, td, dec, fp2_order, fp2_m, fp2_swaps_prev);
-        } else {
-            const size_t psm = (size_t)k * (sizeof(A) + 1);
-            const bool pstaged = psm <= 40 * 1024;
-            km::k_fp2_plan<A><<<1, 1024, pstaged ? psm : 0, st>>>(fp2_best, k, td, dec, fp2_order, fp2_m,
-                                                                  fp2_swaps_prev, pstaged);
-        }
-        KM_CKL();
-        f2_mark(5);
-        // the outcome in ONE host wait: decision, TD, this iteration's swap
-        // count and trace records written by the kernel into pinned memory
-        if (!h_f2out) {
-            KM_CK(cudaMallocHost((void**)&h_f2out, sizeof(Rec) * (size_t)(trace_cap + 1)));
-        }
-        km::F2HostOut<A> ho;
-        ho.dec = h_dec; ho.td = h_td; ho.swaps = reinterpret_cast<int*>(h_f2out); ho.trace = h_f2out + 1;
-        KM_TRY(launch_fp2_sequential(nullptr, nullptr, fp2_swaps_prev, ho));
-        ++launches;
+        KM_TRY(fp2_enqueue_tail(sort_plan, 0, false));
         f2_mark(6);
         f2_mark(7);
         KM_CK(cudaStreamSynchronize(st));
         f2_take();
         KM_TRY(fp2_finish_profiling());
-        // this iteration's swaps: the head of the trace (the kernel counts from 0)
+        return fp2_read(0, swaps_out, td_out);
+    }
+
+    // Steps 4-7 on the device behind fp2_eval_local: the plan, then the
+    // sequential kernel, which writes the outcome (decision, TD, this
+    // iteration's swap count and trace) into pinned ring slot `slot`.
+    // sticky: the plan kernels honour / set Decision::done (queued iterations).
+    static constexpr int F2RING = 2;
+    Rec* h_f2out = nullptr;          // pinned, F2RING slots of (trace_cap + 1) records: [0] swaps (int), [1..] trace
+    Dec* h_f2dec = nullptr;          // pinned, F2RING decisions
+    A* h_f2td = nullptr;             // pinned, F2RING TDs
+    cudaEvent_t f2_done[F2RING] = {};
+    km_status fp2_enqueue_tail(bool sort_plan, int slot, bool sticky) {
+        f2_mark(4);
+        if (sort_plan) {
+            int np2 = 2;
+            while (np2 < k) np2 <<= 1;
+            km::k_fp2_plan_sort<A><<<1, 1024, (size_t)np2 * (sizeof(A) + sizeof(int)), st>>>(
+                fp2_part, FP2_SPLIT, fp2_best, k, np2, td, dec, fp2_order, fp2_m, fp2_swaps_prev, sticky ? 1 : 0);
+        } else {
+            const size_t psm = (size_t)k * (sizeof(A) + 1);
+            const bool pstaged = psm <= 40 * 1024;
+            km::k_fp2_plan<A><<<1, 1024, pstaged ? psm : 0, st>>>(fp2_best, k, td, dec, fp2_order, fp2_m,
+                                                                  fp2_swaps_prev, pstaged, sticky ? 1 : 0);
+        }
+        KM_CKL();
+        ++launches;
+        f2_mark(5);
+        if (!h_f2out) {
+            KM_CK(cudaMallocHost((void**)&h_f2out, sizeof(Rec) * (size_t)(trace_cap + 1) * F2RING));
+            KM_CK(cudaMallocHost((void**)&h_f2dec, sizeof(Dec) * F2RING));
+            KM_CK(cudaMallocHost((void**)&h_f2td, sizeof(A) * F2RING));
+            for (auto& e : f2_done) KM_CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+        }
+        Rec* out = h_f2out + (size_t)slot * (trace_cap + 1);
+        km::F2HostOut<A> ho;
+        ho.dec = h_f2dec + slot; ho.td = h_f2td + slot; ho.swaps = reinterpret_cast<int*>(out); ho.trace = out + 1;
+        KM_TRY(launch_fp2_sequential(nullptr, nullptr, fp2_swaps_prev, ho));
+        KM_CK(cudaEventRecord(f2_done[slot], st));
+        return KM_OK;
+    }
+    // The outcome in ring slot `slot` (its iteration has completed).
+    km_status fp2_read(int slot, int32_t* swaps_out, void* td_out) {
+        const Rec* out = h_f2out + (size_t)slot * (trace_cap + 1);
         int done = 0;
-        memcpy(&done, h_f2out, sizeof(int));
-        last_swaps.assign(h_f2out + 1, h_f2out + 1 + std::min(done, trace_cap));
+        memcpy(&done, out, sizeof(int));
+        last_swaps.assign(out + 1, out + 1 + std::min(done, trace_cap));
+        *h_dec = h_f2dec[slot];
+        *h_td = h_f2td[slot];
         if (swaps_out) *swaps_out = done;
         if (td_out) memcpy(td_out, h_td, sizeof(A));
         return done > 0 ? KM_OK : KM_CONVERGED;
     }
 
-    Rec* h_f2out = nullptr;          // pinned: [0] swaps of the iteration (int), [1..] the trace
+    // Up to max_iter FastPAM2 iterations, the next one queued on the device
+    // while the host reads the current one (as fp1_run_pipelined): no host
+    // round trip between iterations.  Each is exactly one swap_iter_fp2
+    // (same plan, same swaps, same counts); stops after the first pass
+    // without an improving slot (counted); passes queued behind
+    // it are no-ops (sticky Decision::done).
+    km_status fp2_run_pipelined(int32_t max_iter, int32_t* iters_out, int32_t* swaps_out, bool* converged) override {
+        if (sharded) return fail(KM_EINVAL, "swap iterations on a sharded handle; use the kmedoids_fp2_shard_* phases");
+        if (!ready) return fail(KM_EINVAL, "no medoids: call kmedoids_set_medoids or kmedoids_init_build first");
+        if (fp2_hostplan < 0) {
+            const char* e = getenv("KM_FP2_HOSTPLAN");
+            fp2_hostplan = (e && e[0] == '1') ? 1 : 0;
+        }
+        int32_t it = 0, sw = 0;
+        bool conv = false;
+        if (fp2_hostplan) {                  // measurement override: the host plans, one iteration at a time
+            while (it < max_iter && !conv) {
+                int32_t s1 = 0;
+                const km_status q = swap_iter(KM_FASTPAM2, &s1, nullptr);
+                if (q != KM_OK && q != KM_CONVERGED) return q;
+                ++it; sw += s1; conv = q == KM_CONVERGED;
+            }
+        } else {
+            KM_TRY(clear_fp1_done());
+            fp1_any_done = true;             // the plan may set Decision::done
+            const bool sort_plan = k <= km::FP2_SORT_MAX;
+            f2_skip = &dec->done;
+            int64_t launched = 0, next = 0;
+            km_status r = KM_OK;
+            while (r == KM_OK && it < max_iter && !conv) {
+                while (r == KM_OK && launched < max_iter && launched - next < F2RING) {
+                    fp1_prepped = false;
+                    inc_valid = false;
+                    r = fp2_eval_local(sort_plan);
+                    if (r == KM_OK) r = fp2_enqueue_tail(sort_plan, (int)(launched % F2RING), true);
+                    ++launched;
+                }
+                if (r != KM_OK) break;
+                if (cudaEventSynchronize(f2_done[next % F2RING]) != cudaSuccess) { r = fail(KM_ECUDA, "FastPAM2 iteration"); break; }
+                int32_t s1 = 0;
+                conv = fp2_read((int)(next % F2RING), &s1, nullptr) == KM_CONVERGED;
+                ++next; ++it; sw += s1;
+            }
+            f2_skip = nullptr;
+            if (r != KM_OK) return r;
+            if (launched > next) KM_CK(cudaStreamSynchronize(st));   // the queued no-ops
+            KM_TRY(fp2_finish_profiling());
+        }
+        if (iters_out) *iters_out = it;
+        if (swaps_out) *swaps_out = sw;
+        if (converged) *converged = conv;
+        return KM_OK;
+    }
+
     int* fp2_m = nullptr;            // [2]: improving slots m; swaps of the iteration
     int* fp2_swaps_prev = nullptr;
     km_status launch_fp2_sequential(const T* colsrc, const int* colidx_dev, const int* swaps_prev_dev = nullptr,
@@ -3075,9 +3156,10 @@ km_status kmedoids_run(km_handle* h, int32_t use_build, km_variant variant, int3
         KM_TRY(h->impl->get_state(medoids_out, assignment_out, td_out, n_iter_out, n_swaps_out));
         return conv ? KM_OK : KM_NOT_CONVERGED;
     }
-    if (variant == KM_FASTPAM1) {                   // iterations queued one ahead (no host round trip)
+    if (variant == KM_FASTPAM1 || variant == KM_FASTPAM2) {   // iterations queued one ahead (no host round trip)
         bool conv = false;
-        KM_TRY(h->impl->fp1_run_pipelined(max_iter, nullptr, nullptr, &conv));
+        if (variant == KM_FASTPAM1) KM_TRY(h->impl->fp1_run_pipelined(max_iter, nullptr, nullptr, &conv));
+        else KM_TRY(h->impl->fp2_run_pipelined(max_iter, nullptr, nullptr, &conv));
         if (conv) st = KM_OK;
     } else {
         for (int it = 0; it < max_iter; ++it) {
@@ -3088,6 +3170,22 @@ km_status kmedoids_run(km_handle* h, int32_t use_build, km_variant variant, int3
     }
     KM_TRY(h->impl->get_state(medoids_out, assignment_out, td_out, n_iter_out, n_swaps_out));
     return st;
+}
+
+km_status kmedoids_swap_iters_variant(km_handle* h, km_variant variant, int32_t count, int32_t* iters_out,
+                                      int32_t* swaps_out, void* td_out) {
+    KM_H();
+    if (count < 1) return fail(KM_EINVAL, "count=%d must be >= 1", count);
+    if (variant != KM_FASTPAM1 && variant != KM_FASTPAM2)
+        return fail(KM_EINVAL, "queued iterations: variant must be KM_FASTPAM1 or KM_FASTPAM2");
+    bool conv = false;
+    int32_t it = 0, sw = 0;
+    if (variant == KM_FASTPAM1) KM_TRY(h->impl->fp1_run_pipelined(count, &it, &sw, &conv));
+    else KM_TRY(h->impl->fp2_run_pipelined(count, &it, &sw, &conv));
+    if (iters_out) *iters_out = it;
+    if (swaps_out) *swaps_out = sw;
+    if (td_out) KM_TRY(h->impl->get_state(nullptr, nullptr, td_out, nullptr, nullptr));
+    return conv ? KM_CONVERGED : KM_OK;
 }
 
 km_status kmedoids_swap_iters(km_handle* h, int32_t count, int32_t* iters_out, int32_t* swaps_out, void* td_out) {

@@ -70,6 +70,7 @@ def load_library() -> ctypes.CDLL:
         "kmedoids_init_build": [vp, vp, vp],
         "kmedoids_swap_iter": [vp, ctypes.c_int, vp, vp],
         "kmedoids_swap_iters": [vp, i32, vp, vp, vp],
+        "kmedoids_swap_iters_variant": [vp, ctypes.c_int, i32, vp, vp, vp],
         "kmedoids_run": [vp, i32, ctypes.c_int, i32, vp, vp, vp, vp, vp],
         "kmedoids_run_host": [vp, ctypes.c_int, i64, i64, i32, i32, vp, ctypes.c_int, i32, vp, vp, vp, vp, vp, vp],
         "kmedoids_get_state": [vp, vp, vp, vp, vp, vp],
@@ -252,12 +253,16 @@ class KMedoids:
         s = _check(load_library().kmedoids_swap_iter(self.h, VARIANTS[variant], psw, ptd), ok=(KM_OK, KM_CONVERGED))
         return s == KM_CONVERGED, int(sw[0]), td[0].item()
 
-    def swap_iters(self, count: int):
-        """Up to `count` FastPAM1 iterations queued back to back (no host round
-        trip between them); returns (converged, iterations, swaps, td)."""
+    def swap_iters(self, count: int, variant: str = "fastpam1"):
+        """Up to `count` FastPAM1 or FastPAM2 iterations queued back to back (no
+        host round trip between them); returns (converged, iterations, swaps, td)."""
         it = np.zeros(1, np.int32); sw = np.zeros(1, np.int32); td = np.zeros(1, self.acc)
-        s = _check(load_library().kmedoids_swap_iters(self.h, int(count), _p(it), _p(sw), _p(td)),
-                   ok=(KM_OK, KM_CONVERGED))
+        if variant == "fastpam1":
+            s = _check(load_library().kmedoids_swap_iters(self.h, int(count), _p(it), _p(sw), _p(td)),
+                       ok=(KM_OK, KM_CONVERGED))
+        else:
+            s = _check(load_library().kmedoids_swap_iters_variant(self.h, VARIANTS[variant], int(count), _p(it),
+                                                                  _p(sw), _p(td)), ok=(KM_OK, KM_CONVERGED))
         return s == KM_CONVERGED, int(it[0]), int(sw[0]), td[0].item()
 
     def run(self, use_build=True, variant="fastpam1", max_iter=2000) -> Result:
