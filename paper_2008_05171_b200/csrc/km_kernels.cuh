@@ -977,40 +977,62 @@ __global__ void k_fp3_pick(const A* __restrict__ cand_v, const int* __restrict__
 // of (dTD(m_i, x_c), c) with dTD = R_i + acc_c[i] + dTD^{+x_c}
 // (Eq. eqn:better-change3).  Slots with an empty segment have acc_c[i] = 0.
 // One block per slot; reads row i of the k x w acc matrix (coalesced).
-template <typename A>
-__global__ void k_fp2_slot_best(int w, int64_t col_begin, const A* __restrict__ acc, const A* __restrict__ plus,
-                                const A* __restrict__ R, const int* __restrict__ seg_start,
-                                const int* __restrict__ point_slot, Rec<A>* __restrict__ part) {
-    // grid (k, FP2_SPLIT): block (i, y) scans columns [y*w/SPLIT, (y+1)*w/SPLIT) of row i
-    const int i = blockIdx.x, y = blockIdx.y;
-    const bool empty = seg_start[i] == seg_start[i + 1];
-    const A ri = R[i];
+// SB slots per block (grid (ceil(k / SB), FP2_SPLIT)): the candidate's
+// point_slot and plus are loaded once for SB rows of acc (at C5, k = 500,
+// SB = 1 re-read them once per slot: 600 MB of L2 traffic beside the 400 MB
+// of acc).  Per slot the same (v, c) lexicographic minimum.
+template <typename A, int SB = 1>
+__global__ void k_fp2_slot_best(int w, int k, int64_t col_begin, const A* __restrict__ acc,
+                                const A* __restrict__ plus, const A* __restrict__ R,
+                                const int* __restrict__ seg_start, const int* __restrict__ point_slot,
+                                Rec<A>* __restrict__ part) {
+    // block (ib, y) scans columns [y*w/SPLIT, (y+1)*w/SPLIT) of rows ib*SB .. ib*SB + SB - 1
+    const int i0 = blockIdx.x * SB, y = blockIdx.y;
+    bool empty[SB];
+    A ri[SB];
+    const A* arow[SB];
+#pragma unroll
+    for (int q = 0; q < SB; ++q) {
+        const int i = min(i0 + q, k - 1);
+        empty[q] = seg_start[i] == seg_start[i + 1];
+        ri[q] = R[i];
+        arow[q] = acc + (int64_t)i * w;
+    }
     const int a = (int)((int64_t)y * w / gridDim.y), z = (int)((int64_t)(y + 1) * w / gridDim.y);
-    Rec<A> b = rec_none<A>();
-    const A* arow = acc + (int64_t)i * w;
-    constexpr int U = 4;                      // columns loaded ahead per thread (memory-level parallelism)
+    Rec<A> b[SB];
+#pragma unroll
+    for (int q = 0; q < SB; ++q) b[q] = rec_none<A>();
+    constexpr int U = SB >= 4 ? 2 : 4;        // columns loaded ahead per thread (memory-level parallelism)
     for (int c0l = a + threadIdx.x; c0l < z; c0l += U * blockDim.x) {
-        A av[U], pv[U];
+        A av[U][SB], pv[U];
         int ps[U];
 #pragma unroll
         for (int u = 0; u < U; ++u) {
             const int cl = c0l + u * blockDim.x;
             if (cl < z) {
                 ps[u] = point_slot[col_begin + cl];
-                av[u] = empty ? (A)0 : __ldcs(&arow[cl]);   // read once: streaming
                 pv[u] = plus[cl];
+#pragma unroll
+                for (int q = 0; q < SB; ++q) av[u][q] = empty[q] ? (A)0 : __ldcs(&arow[q][cl]);   // read once: streaming
             }
         }
 #pragma unroll
         for (int u = 0; u < U; ++u) {
             const int cl = c0l + u * blockDim.x;
             if (cl >= z || ps[u] >= 0) continue;
-            Rec<A> r; r.v = ri + av[u] + pv[u]; r.slot = i; r.c = (int)(col_begin + cl);
-            if (rec_less(r, b)) b = r;        // same slot: (v, c) order
+#pragma unroll
+            for (int q = 0; q < SB; ++q) {
+                Rec<A> r; r.v = ri[q] + av[u][q] + pv[u]; r.slot = i0 + q; r.c = (int)(col_begin + cl);
+                if (rec_less(r, b[q])) b[q] = r;        // same slot: (v, c) order
+            }
         }
     }
-    b = block_min_rec(b);
-    if (threadIdx.x == 0) part[(int64_t)i * gridDim.y + y] = b;
+#pragma unroll
+    for (int q = 0; q < SB; ++q) {
+        const Rec<A> m = block_min_rec(b[q]);
+        if (threadIdx.x == 0 && i0 + q < k) part[(int64_t)(i0 + q) * gridDim.y + y] = m;
+        __syncthreads();                          // block_min_rec's shared buffer is reused
+    }
 }
 
 // Per slot: lexicographic min over the FP2_SPLIT partials (fixed order).

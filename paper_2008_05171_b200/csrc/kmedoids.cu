@@ -69,7 +69,8 @@ constexpr int MAX_K = 8192;
 // producer, TMA ring of 5 stages x 4 rows (~72 KB shared memory), 3 CTAs = 24
 // warps per SM (<= 80 registers).
 constexpr int SG_NC = 7, SG_RB = 4, SG_S = 5, SG_MINB = 3;
-constexpr int FP2_SPLIT = 8;   // column splits of the FastPAM2 per-slot reduction
+constexpr int FP2_SPLIT = 8;
+constexpr int FP2_SB_MIN_K = 256;   // k from which k_fp2_slot_best takes 4 slots per block   // column splits of the FastPAM2 per-slot reduction
 
 int64_t cdiv(int64_t a, int64_t b) { return (a + b - 1) / b; }
 
@@ -1083,8 +1084,12 @@ struct Impl : ImplBase {
         KM_TRY(launch_combine(w, c0, P, o_plus, o_head, o_tail, o_imin, o_islot, head_slot, tail_slot, cand_v, cand_slot,
                               fp2_acc, fp2_plus));
         f2_mark(3);
-        km::k_fp2_slot_best<A><<<dim3(k, FP2_SPLIT), 256, 0, st>>>(w, c0, fp2_acc, fp2_plus, R, seg_start, point_slot,
-                                                                     fp2_part);
+        if (k >= FP2_SB_MIN_K)           // 4 slots per block: point_slot / plus loaded once per 4 rows of acc
+            km::k_fp2_slot_best<A, 4><<<dim3((unsigned)cdiv(k, 4), FP2_SPLIT), 256, 0, st>>>(
+                w, k, c0, fp2_acc, fp2_plus, R, seg_start, point_slot, fp2_part);
+        else
+            km::k_fp2_slot_best<A, 1><<<dim3(k, FP2_SPLIT), 256, 0, st>>>(w, k, c0, fp2_acc, fp2_plus, R, seg_start,
+                                                                         point_slot, fp2_part);
         KM_CKL();
         if (!fused_plan) {                 // (single-GPU device plan: folded into k_fp2_plan_sort)
             km::k_fp2_slot_reduce<A><<<(unsigned)cdiv(k, 128), 128, 0, st>>>(k, FP2_SPLIT, fp2_part, fp2_best);
